@@ -1,0 +1,386 @@
+"""Benchmark: Pro-Prophet EP MoE layer fwd+bwd tokens/s on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference] [--config cfg2|cfg3|...]
+    torchrun --nproc-per-node N bench.py --gpus N ...        (N > 1: EP over NCCL/NVLink)
+
+One "step" = one forward + backward of one MoE layer over this rank's T tokens
+(synthetic bf16 activations, random-init weights, Zipf-skewed gate bias,
+planner re-planning every iteration when N > 1).  Prints ONE JSON line on rank 0.
+
+Workloads (BASELINE.json configs): N == 1 -> configs[1] ("cfg2": 16 experts,
+top-2, d=1024, f=4096, 16K tokens/GPU); N > 1 -> configs[2] ("cfg3": 32
+experts, top-2, d=2048, f=4096, 32K tokens/GPU, EP across the N GPUs).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CONFIGS = {
+    "cfg1": dict(E=8, k=2, d=512, f=1024, T=1024, desc="8 experts top-2 d512 4096 tokens over 4 ranks"),
+    "cfg2": dict(E=16, k=2, d=1024, f=4096, T=16384, desc="16 experts top-2 d1024 f4096 16K tokens/GPU skewed"),
+    "cfg3": dict(E=32, k=2, d=2048, f=4096, T=32768, desc="32 experts top-2 d2048 f4096 32K tokens/GPU EP"),
+    "cfg4": dict(E=64, k=2, d=2048, f=4096, T=32768, desc="64 experts top-2 d2048 32K tokens/GPU Zipf drift"),
+}
+METRIC = "MoE-layer tokens/s fwd+bwd at 1/2/4/8 B200; planner ms/iter; load imbalance"
+
+
+def zipf_bias(E: int, skew: float, seed: int):
+    """Per-expert logit bias log(p_e), p = Zipf(skew) in a seeded random order
+    (the popularity shape of the reference generator, workload.py:89-95)."""
+    import numpy as np
+
+    w = np.arange(1, E + 1, dtype=np.float64) ** -skew
+    w /= w.sum()
+    perm = np.random.default_rng(seed).permutation(E)
+    p = np.empty(E)
+    p[perm] = w
+    return np.log(p)
+
+
+class ClockSampler:
+    FIELDS = ("clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int) -> None:
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + ",".join(self.FIELDS),
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], 0.0, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) != 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def load_peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {"hbm": d["hbm_gbs"], "tc_burst": d["bf16_tflops"], "tc_sustained": d["bf16_tflops_sustained"],
+                "source": "measured"}
+    return {"hbm": 6650.0, "tc_burst": 1590.0, "tc_sustained": 1400.0, "source": "fallback"}
+
+
+# --------------------------------------------------------------------------- CPU baseline
+def cpu_baseline(cfg: dict, budget_s: float = 15.0) -> dict:
+    """Oracle torch-CPU restatement of the same layer (fp32, all host threads),
+    on a bounded sample of the workload's tokens."""
+    import torch
+
+    from oracle import moe_ref
+
+    threads = os.cpu_count() or 1
+    torch.set_num_threads(threads)
+    E, k, d, f = cfg["E"], cfg["k"], cfg["d"], cfg["f"]
+    Ts = min(cfg["T"], 2048)
+    g = torch.Generator().manual_seed(0)
+    x = torch.randn((Ts, d), generator=g).to(torch.bfloat16)
+    dy = (torch.randn((Ts, d), generator=g) * 0.1).to(torch.bfloat16)
+    wg = torch.randn((E, d), generator=g) / math.sqrt(d)
+    w1 = torch.randn((E, f, d), generator=g) / math.sqrt(d)
+    w2 = torch.randn((E, d, f), generator=g) / math.sqrt(f)
+    moe_ref.cpu_layer_step(x[:128], wg, w1, w2, k, dy[:128])  # warm
+    steps, t0 = 0, time.perf_counter()
+    while True:
+        moe_ref.cpu_layer_step(x, wg, w1, w2, k, dy)
+        steps += 1
+        el = time.perf_counter() - t0
+        if el > budget_s or steps >= 50:
+            break
+    return {"value": steps * Ts / el, "unit": "tokens/s", "cores": threads, "kind": "port",
+            "sample": f"{steps} fwd+bwd steps of {Ts} tokens (of {cfg['T']}) at E={E} k={k} d={d} f={f}, "
+                      f"torch-CPU fp32 oracle (oracle/moe_ref.cpu_layer_step), {el:.1f}s"}
+
+
+def cpu_planner_ms(E: int, k: int, T: int, d: int, f: int) -> dict:
+    """Oracle planner (restatement of reference greedy_search, pinned to its
+    goldens) on a Zipf-skewed virtual-slot LoadMatrix, 1 core."""
+    import numpy as np
+
+    from oracle import planner_ref as P
+
+    rng = np.random.default_rng(0)
+    p = np.exp(zipf_bias(E, 1.2, 0))
+    mats = [np.stack([rng.multinomial(T * k // E if E else 0, p) for _ in range(E)]) for _ in range(8)]
+    cm = P.cost_model_dict(E, k, 2 * d, 4 * d * f, 8 * d * f, 450e9, 1.2e15 / (6.0 * d * f))
+    t0 = time.perf_counter()
+    for mm in mats:
+        P.greedy_search(mm, 1, 0.5, False, cm)
+    return {"ms_per_layer": (time.perf_counter() - t0) / len(mats) * 1e3, "mats": mats, "cm": cm}
+
+
+# --------------------------------------------------------------------------- reference arm
+def run_reference(args, cfg_name: str, cfg: dict) -> None:
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import torch
+
+    from oracle import moe_ref
+
+    torch.set_num_threads(os.cpu_count() or 1)
+    E, k, d, f = cfg["E"], cfg["k"], cfg["d"], cfg["f"]
+    Ts = min(cfg["T"], 1024)
+    g = torch.Generator().manual_seed(0)
+    x = torch.randn((Ts, d), generator=g).to(torch.bfloat16)
+    dy = (torch.randn((Ts, d), generator=g) * 0.1).to(torch.bfloat16)
+    wg = torch.randn((E, d), generator=g) / math.sqrt(d)
+    w1 = torch.randn((E, f, d), generator=g) / math.sqrt(d)
+    w2 = torch.randn((E, d, f), generator=g) / math.sqrt(f)
+    for _ in range(args.warmup):
+        moe_ref.cpu_layer_step(x, wg, w1, w2, k, dy)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        moe_ref.cpu_layer_step(x, wg, w1, w2, k, dy)
+    el = time.perf_counter() - t0
+    value = args.steps * Ts / el
+    threads = os.cpu_count() or 1
+    out = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic", "config": {"workload": f"{cfg_name}: {cfg['desc']}", "sample_tokens_per_step": Ts},
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": "port",
+                         "sample": f"{Ts} tokens/step of {cfg['T']} (reference has no layer code: "
+                                   "oracle torch-CPU restatement, fp32, all host threads)"},
+        "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+
+
+# --------------------------------------------------------------------------- our arm
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-only", action="store_true", help="short run for ncu (no CPU legs)")
+    args = ap.parse_args()
+    world_env = int(os.environ.get("WORLD_SIZE", "1"))
+    cfg_name = args.config or ("cfg2" if max(args.gpus, world_env) == 1 else "cfg3")
+    cfg = dict(CONFIGS[cfg_name])
+    if args.impl == "reference":
+        run_reference(args, cfg_name, cfg)
+        return
+    args.warmup = max(args.warmup, 3)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2411_10003_b200 as pp
+    from paper_2411_10003_b200 import _lib
+
+    world = world_env
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    group = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        group = dist.group.WORLD
+    E, k, d, f, T = cfg["E"], cfg["k"], cfg["d"], cfg["f"], cfg["T"]
+    planner = pp.PlannerConfig(n=1, alpha=0.5, reuse_interval=1, overlap_aware=True)
+    layer = pp.MoELayer(d, f, E, k, tokens=T, group=group, planner=planner, seed=0)
+    layer.set_gate_bias(zipf_bias(E, 1.2, 0))
+    g = torch.Generator(device="cpu").manual_seed(1000 + rank)
+    x = torch.randn((T, d), generator=g).to(dev, torch.bfloat16)
+    dy = (torch.randn((T, d), generator=g) * 0.1).to(dev, torch.bfloat16)
+
+    def step(xin, dyin):
+        xin.requires_grad_(True)
+        y = layer(xin)
+        y.backward(dyin)
+        return y
+
+    # ---- warmup
+    for _ in range(args.warmup):
+        step(x.detach().clone(), dy)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+
+    # ---- timed region (device events), GEMM launches timed on their stream
+    layer.gemm_timing = []
+    _lib.reset_launch_count()
+    xs = [x.detach().clone() for _ in range(2)]
+    torch.cuda.synchronize()
+    with ClockSampler(local_rank) as clk:
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record()
+        for i in range(args.steps):
+            step(xs[i % 2].detach(), dy)
+        t1.record()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    launches = _lib.launch_count()
+    ms_total = t0.elapsed_time(t1)
+    ms_tensor = torch.tensor([ms_total], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms_tensor, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_tensor.item())
+    value = world * T * args.steps / (ms_max / 1e3)
+
+    # ---- roofline of the grouped tcgen05 GEMM family (dominant kernel)
+    gemm = layer.collect_gemm_timing()
+    peaks = load_peaks()
+    rows_real = int(layer.total_real_rows())
+    flops_step = 2.0 * rows_real * d * f * 6  # FWD1, FWD2, DGRAD2, DGRAD1, WGRAD2, WGRAD1
+    gemm_ms_step = gemm["ms_per_step"]
+    achieved = flops_step / (gemm_ms_step / 1e3) / 1e12 if gemm_ms_step > 0 else 0.0
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": peaks["tc_sustained"], "unit": "TFLOP/s",
+                "frac": achieved / peaks["tc_sustained"], "traffic": None,
+                "kernel": "grouped_gemm_kernel (6 launches/step: FWD1 FWD2 DGRAD2 DGRAD1 WGRAD2 WGRAD1)",
+                "peak_source": f"{peaks['source']} bf16_tflops_sustained",
+                "flops_per_step": flops_step, "gemm_ms_per_step": gemm_ms_step,
+                "gemm_share_of_step": gemm_ms_step / (ms_total / args.steps),
+                "per_mode_ms": gemm["per_mode_ms"]}
+
+    # ---- e2e through the public API with host buffers
+    e2e = None
+    if not args.profile_only:
+        xh = x.detach().cpu().pin_memory()
+        dyh = dy.detach().cpu().pin_memory()
+        yh = torch.empty((T, d), dtype=torch.bfloat16).pin_memory()
+        xdev = torch.empty_like(x)
+        dydev = torch.empty_like(dy)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.steps):
+            xdev.copy_(xh, non_blocking=True)
+            dydev.copy_(dyh, non_blocking=True)
+            y = step(xdev.detach(), dydev)
+            yh.copy_(y.detach(), non_blocking=True)
+        e1.record()
+        torch.cuda.synchronize()
+        em = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(em, op=dist.ReduceOp.MAX)
+        e2e = {"value": world * T * args.steps / (float(em.item()) / 1e3), "unit": "tokens/s",
+               "h2d_bytes_per_step": 2 * T * d * 2, "d2h_bytes_per_step": T * d * 2,
+               "path": "MoELayer.__call__ + backward (public API), pinned host x/dy in, y out"}
+
+    # ---- planner + imbalance (device planner vs oracle CPU planner)
+    planner_info, imbalance = None, None
+    if rank == 0 and not args.profile_only:
+        Ev = E
+        cpu = cpu_planner_ms(Ev, k, T * world, d, f)
+        cl = pp.ClusterSpec(Ev, cpu["cm"]["avg_bandwidth"], cpu["cm"]["compute_throughput"])
+        mo = pp.ModelSpec(Ev, 1, k, cpu["cm"]["input_bytes"], cpu["cm"]["expert_param_bytes"],
+                          cpu["cm"]["expert_grad_bytes"])
+        from paper_2411_10003_b200 import _device
+        import numpy as np
+
+        counts_dev = torch.from_numpy(np.stack(cpu["mats"])).to(dev)
+        out = _device.PlanBuffers(len(cpu["mats"]), Ev, dev)
+        cmd, pcfg = _device.cost_model(cl, mo, Ev), _device.planner_cfg(pp.PlannerConfig(n=1, alpha=0.5))
+        for _ in range(3):
+            _device.launch_plan(counts_dev, out, cmd, pcfg)
+        p0 = torch.cuda.Event(enable_timing=True)
+        p1 = torch.cuda.Event(enable_timing=True)
+        p0.record()
+        for _ in range(20):
+            _device.launch_plan(counts_dev, out, cmd, pcfg)
+        p1.record()
+        torch.cuda.synchronize()
+        planner_info = {"device_us_per_launch": p0.elapsed_time(p1) / 20 * 1e3,
+                        "layers_per_launch": len(cpu["mats"]), "E_virtual": Ev,
+                        "cpu_oracle_ms_per_layer": cpu["ms_per_layer"]}
+        lm = layer.last_load_matrix()
+        H0, _ = np.asarray(lm.counts).sum(axis=0), None
+        imbalance = {"virtual_slot_H_sigma_vanilla": float(np.std(H0)),
+                     "max_over_mean_vanilla": float(H0.max() / max(H0.mean(), 1e-9))}
+        if world > 1:
+            mask = layer.current_mask()
+            from oracle import planner_ref as P
+            Hp, _ = P.derive_loads(lm.counts, mask)
+            imbalance.update({"virtual_slot_H_sigma_planned": float(np.std(Hp)),
+                              "rb": P.rb_ratio(H0, Hp)})
+
+    cpu_info = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile_only:
+        cpu_info = cpu_baseline(cfg)
+
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": f"{cfg_name}: {cfg['desc']}", "experts": E, "top_k": k, "d_model": d,
+                       "d_ff": f, "tokens_per_gpu": T, "parallelism": f"ep{world}",
+                       "l2": "working set > L2 (activations+weights >> 126 MB), no flush",
+                       "routing": "Zipf(1.2) gate bias, random bf16 tokens"},
+            "roofline": roofline, "cpu_baseline": cpu_info, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clk.summary(), "planner": planner_info, "imbalance": imbalance,
+        }
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

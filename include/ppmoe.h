@@ -1,0 +1,223 @@
+/*
+ * ppmoe.h -- C ABI of the B200-native Pro-Prophet expert-parallel MoE hot path.
+ *
+ * Every entry point takes plain pointers and sizes (device pointers unless
+ * stated), an opaque cudaStream_t passed as void*, and returns an int code:
+ *   PP_OK 0, PP_EINVAL 1 (-> ValidationError), PP_EDIM 2 (-> DimensionMismatchError),
+ *   PP_ECUDA 3, PP_EPEER 4 (-> RuntimeError).  pp_last_error() gives the
+ *   thread-local message of the last failing call.
+ * All calls are stream-ordered and re-entrant; the only library-owned state is
+ * the per-(device, tensor-map) cache inside the GEMM launcher and peer
+ * contexts created/destroyed explicitly with pp_peer_*.
+ *
+ * Reference interfaces each entry point replaces (reference = arxiv 2411.10003
+ * "moebal" package, /root/reference/pkg/src/moebal):
+ *   pp_plan_greedy    <- planner.greedy_search        planner.py:80-129
+ *                        (+ derive_loads core.py:255-275, cost _build perf_model.py:86-107)
+ *   pp_derive_loads   <- core.derive_loads             core.py:255-275
+ *   pp_route_topk     <- the gate that produces LoadMatrix rows (core.py:88-95;
+ *                        gate described in PAPER.md:106-108); no reference code
+ *   pp_slot_histogram <- LoadMatrix construction (virtual expert-slot rows)
+ *   pp_dispatch_layout/pp_dispatch/pp_combine (+ _bwd)
+ *                     <- routing rule of derive_loads core.py:267-274 realised on
+ *                        tokens; A2A modelled by t_a2a perf_model.py:36-39
+ *   pp_grouped_gemm   <- expert compute modelled by t_fec/t_bec perf_model.py:42-51
+ *   pp_replica_trans / pp_replica_agg
+ *                     <- Trans/Agg modelled by t_trans/t_agg perf_model.py:61-73,
+ *                        split by partition_trans/agg scheduler.py:91-108
+ */
+#ifndef PPMOE_H
+#define PPMOE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PP_OK 0
+#define PP_EINVAL 1
+#define PP_EDIM 2
+#define PP_ECUDA 3
+#define PP_EPEER 4
+
+const char* pp_last_error(void);
+int pp_version(void);
+
+/* ---- cost model + planner (K2) ------------------------------------------ */
+typedef struct pp_cost_model {
+  double input_bytes;
+  double expert_param_bytes;
+  double expert_grad_bytes;
+  double avg_bandwidth;
+  double compute_throughput;
+  double fnec_time;
+  double bnec_time;
+  int32_t num_devices; /* D == E for the planner (virtual expert slots) */
+  int32_t num_experts;
+  int32_t top_k;
+  int32_t _pad;
+} pp_cost_model;
+
+typedef struct pp_planner_cfg {
+  double alpha;
+  int32_t n;
+  int32_t overlap_aware;
+} pp_planner_cfg;
+
+/* Plan L layers, one CTA each.  counts: [L][E][E] int64 (device).
+ * Outputs (device): selected [L][E] int32 (search order, first num_selected
+ * valid), num_selected [L], num_explored [L], mask [L][E][E] uint8 replica
+ * mask of the returned plan, H/R [L][E] int64 of the returned plan,
+ * best_cost [L] fp64 (objective of the returned plan).  E <= 1024. */
+int pp_plan_greedy(const int64_t* counts, int32_t num_layers, int32_t E,
+                   const pp_cost_model* cm, const pp_planner_cfg* cfg,
+                   int32_t* selected, int32_t* num_selected, int32_t* num_explored,
+                   uint8_t* mask, int64_t* H, int64_t* R, double* best_cost,
+                   void* stream);
+
+/* counts [D][E] int64, mask [D][E] uint8 -> H [D], R [D] int64.  E <= D. */
+int pp_derive_loads(const int64_t* counts, const uint8_t* mask, int32_t D, int32_t E,
+                    int64_t* H, int64_t* R, void* stream);
+
+/* ---- routing (K1) -------------------------------------------------------- */
+/* x [T][d] bf16, wg [E][d] bf16, bias [E] fp32 (nullable).
+ * logits fp32 = x.wg^T + bias; top-k on logits, ties -> lowest expert;
+ * weights = softmax(all E logits) at the chosen experts (not renormalised).
+ * Outputs: idx [T][k] int32, w [T][k] fp32, probs [T][E] fp32 (for backward),
+ * rank [T][k] int32 = position of the pair among the pairs of its expert in
+ * its 128-token chunk (token order), chunk_counts [T/128][E] int32.
+ * The gate GEMM runs on tcgen05 (N = E padded to 16/32/64/128) with the
+ * softmax / top-k / rank epilogue read straight from TMEM.
+ * Requires T % 128 == 0, d % 64 == 0, 4 <= E <= 128, E % 4 == 0, 1 <= k <= min(E,8). */
+int pp_route_topk(const void* x, const void* wg, const float* bias,
+                  int32_t T, int32_t d, int32_t E, int32_t k,
+                  int32_t* idx, float* w, float* probs, int32_t* rank,
+                  int32_t* chunk_counts, void* stream);
+
+/* Local virtual-slot histogram: chunk_counts [T/128][E] -> hist [m][E] int64
+ * written at row offset `row0` of `out` (out has >= row0+m rows of E). */
+int pp_slot_histogram(const int32_t* chunk_counts, int32_t T, int32_t E, int32_t m,
+                      int64_t* out, int32_t row0, void* stream);
+
+/* ---- dispatch layout / permute / combine (K3) --------------------------- */
+#define PP_CHUNK 128
+#define PP_ROW_ALIGN 128
+
+typedef struct pp_group {
+  int32_t row_off;  /* first row of the group's (padded) segment */
+  int32_t rows;     /* real rows */
+  int32_t rows_pad; /* rows rounded up to PP_ROW_ALIGN */
+  int32_t wslot;    /* weight slot in this rank's arena (home: e % m, replicas after) */
+  int32_t expert;   /* global expert id */
+  int32_t src_rank; /* home rank of the expert (== this rank for home groups) */
+  int32_t _pad[2];
+} pp_group;
+
+/* Single-CTA layout solver.  counts [Ev][E] int64 all-gathered virtual-slot
+ * histogram (Ev = D*m), mask [Ev][E] uint8 replica mask (nullable = vanilla
+ * EP), chunk_counts [T/128][E] of this rank.  Outputs (device):
+ *   chunk_base [T/128][E] int32 destination row of the first pair of each (chunk, expert)
+ *   slot_dest  [m][E]   int32   destination rank of (local slot, expert)
+ *   groups     [max_groups] pp_group of THIS rank, num_groups [1] int32,
+ *   total_rows [1] int32 (padded rows of this rank's receive buffer)
+ *   seg_start  [D][E] int32 segment start of expert e on rank r (-1 if absent)
+ *   rep_slot   [D][E] int32 weight slot of replica expert e on rank r (-1 if
+ *              none; nullable) -- consumed by pp_replica_agg. */
+int pp_dispatch_layout(const int64_t* counts, const uint8_t* mask, const int32_t* chunk_counts,
+                       int32_t D, int32_t m, int32_t E, int32_t T, int32_t my_rank,
+                       int32_t max_groups, int32_t rows_capacity,
+                       int32_t* chunk_base, int32_t* slot_dest, pp_group* groups,
+                       int32_t* num_groups, int32_t* total_rows, int32_t* seg_start,
+                       int32_t* rep_slot, void* stream);
+
+/* Permute + all-to-all in one kernel: row of token t goes to rank
+ * slot_dest[t/(T/m)][e] at row chunk_base[t/128][e] + rank[t][j] of that
+ * rank's receive buffer.  recv_ptrs: device array [D] of receive-buffer
+ * base pointers (peer-mapped for D > 1).  Also zero-fills this rank's own
+ * padding rows (groups/num_groups) and records pair_dest/pair_row [T][k]. */
+int pp_dispatch(const void* x, const int32_t* idx, const int32_t* rank,
+                const int32_t* chunk_base, const int32_t* slot_dest,
+                int32_t T, int32_t d, int32_t k, int32_t m, int32_t E,
+                void* const* recv_ptrs, void* own_recv,
+                const pp_group* groups, const int32_t* num_groups, int32_t max_groups,
+                int32_t* pair_dest, int32_t* pair_row, void* stream);
+
+/* y[t] = sum_j w[t][j] * out_ptrs[pair_dest][pair_row] (fp32 accumulate, bf16 out). */
+int pp_combine(void* const* out_ptrs, const int32_t* pair_dest, const int32_t* pair_row,
+               const float* w, int32_t T, int32_t d, int32_t k, void* y, void* stream);
+
+/* Backward of combine: dw[t][j] = <dy[t], Yp[pair]> ; dYp[pair] = w[t][j]*dy[t]
+ * (pushed to dgrad_ptrs[pair_dest]); zero-fills own padding rows of own_dgrad. */
+int pp_combine_bwd(const void* dy, void* const* out_ptrs, void* const* dgrad_ptrs, void* own_dgrad,
+                   const int32_t* pair_dest, const int32_t* pair_row, const float* w,
+                   const pp_group* groups, const int32_t* num_groups, int32_t max_groups,
+                   int32_t T, int32_t d, int32_t k, float* dw, void* stream);
+
+/* Backward of dispatch + gate:  dlogits = softmax'(probs) . dw (top-k scatter),
+ * dx[t] = sum_j dXp[pair] + sum_e dlogits[t][e] * wg[e];  writes dx bf16 and
+ * dlogits [T][E] fp32. */
+int pp_dispatch_bwd(void* const* dxp_ptrs, const int32_t* pair_dest, const int32_t* pair_row,
+                    const int32_t* idx, const float* probs, const float* dw, const void* wg,
+                    int32_t T, int32_t d, int32_t k, int32_t E, void* dx, float* dlogits,
+                    void* stream);
+
+/* dwg [E][d] fp32 (+)= dlogits^T . x  (accumulates; caller zeroes). */
+int pp_gate_wgrad(const float* dlogits, const void* x, int32_t T, int32_t d, int32_t E,
+                  float* dwg, void* stream);
+
+/* ---- grouped expert GEMM on tcgen05 (K4) -------------------------------- */
+#define PP_GEMM_FWD1 0   /* pre,act[rows][f] = GeLU-split( Xp[rows][d] . W1[slot][f][d]^T ) */
+#define PP_GEMM_FWD2 1   /* Yp[rows][d] = act[rows][f] . W2[slot][d][f]^T */
+#define PP_GEMM_DGRAD2 2 /* dPre[rows][f] = (dYp[rows][d] . W2[slot][d][f]) * GeLU'(pre) */
+#define PP_GEMM_DGRAD1 3 /* dXp[rows][d] = dPre[rows][f] . W1[slot][f][d] */
+#define PP_GEMM_WGRAD2 4 /* dW2[slot][d][f] = dYp_g^T . act_g   (fp32) */
+#define PP_GEMM_WGRAD1 5 /* dW1[slot][f][d] = dPre_g^T . Xp_g  (fp32) */
+#define PP_GEMM_PLAIN 6  /* C[rows][n] = A[rows][k] . B[slot][n][k]^T (bf16), test/utility */
+
+/* a, b: operand base pointers as listed above; c: main output; c2: second
+ * output (FWD1: act) or the pre-activation input (DGRAD2, may alias c).
+ * rows_capacity: rows allocated in the row-indexed buffers; num_slots:
+ * weight slots in the arena; d_model/d_ff: the two feature sizes (for
+ * PP_GEMM_PLAIN: K = d_model, N = d_ff).  groups/num_groups on device. */
+int pp_grouped_gemm(int32_t mode, const void* a, const void* b, void* c, void* c2,
+                    const pp_group* groups, const int32_t* num_groups, int32_t max_groups,
+                    int32_t rows_capacity, int32_t num_slots, int32_t d_model, int32_t d_ff,
+                    int32_t num_sms, void* stream);
+
+/* ---- replica Trans / Agg over peer memory (K5) --------------------------- */
+/* Trans: for every replica group of this rank (groups[g].src_rank != me) pull
+ * the expert's W1/W2 from the home rank's weight arena (peer pointer tables
+ * w1_ptrs/w2_ptrs [D], arenas [slots][f][d] and [slots][d][f] bf16) into this
+ * rank's replica slot.  `max_ctas` bounds the SMs taken from concurrent GEMMs. */
+int pp_replica_trans(void* const* w1_ptrs, void* const* w2_ptrs, const pp_group* groups,
+                     const int32_t* num_groups, int32_t max_groups, int32_t my_rank, int32_t m,
+                     int32_t d_model, int32_t d_ff, int32_t max_ctas, void* stream);
+
+/* Agg: the home rank pulls the replicas' fp32 grads (g1_ptrs/g2_ptrs [D]) and
+ * adds them, in ascending rank order, into its own home slots.  rep_slot
+ * [D][E] from pp_dispatch_layout. */
+int pp_replica_agg(void* const* g1_ptrs, void* const* g2_ptrs, const int32_t* rep_slot,
+                   int32_t D, int32_t E, int32_t m, int32_t my_rank, int32_t d_model,
+                   int32_t d_ff, int32_t max_ctas, void* stream);
+
+/* ---- peer memory (CUDA IPC) + device barrier ----------------------------- */
+/* Library-owned cudaMalloc allocations (IPC-exportable as a whole). */
+int pp_device_alloc(uint64_t bytes, void** dev_ptr);
+int pp_device_free(void* dev_ptr);
+/* Export a device allocation: writes a 64-byte IPC handle. */
+int pp_ipc_export(void* dev_ptr, uint8_t* handle64);
+/* Import a peer allocation (on the current device). */
+int pp_ipc_import(const uint8_t* handle64, void** dev_ptr);
+int pp_ipc_close(void* dev_ptr);
+
+/* Cross-rank barrier over peer-mapped signal words.  signal_ptrs: device
+ * array [D] of each rank's signal area (uint64_t[D] each); epoch must grow
+ * by one per call.  Spins with a 20 s timeout (traps instead of hanging). */
+int pp_peer_barrier(void* const* signal_ptrs, int32_t D, int32_t my_rank, uint64_t epoch,
+                    void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PPMOE_H */

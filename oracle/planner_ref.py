@@ -1,0 +1,160 @@
+"""ORACLE (test infrastructure only) -- CPU restatement of the reference planner path.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s cpu_baseline /
+``--impl reference`` leg may import this module, and only as the checker or
+the timed CPU baseline.  The product (``paper_2411_10003_b200``) never calls it.
+
+Parity status: PINNED.  Every function below restates a reference function
+(``/root/reference/pkg/src/moebal``, cited per function) and is checked in
+``tests/test_oracle_golden.py`` against golden vectors produced by running the
+reference itself (``tests/golden/gen_golden.py``): FIG8 cases, the SURVEY
+appendix-B step traces, fuzzed instances and generator traces.
+
+Pure Python + numpy, integer arithmetic exact, fp64 in the reference's
+association order.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+
+def replica_mask(D: int, E: int, selected, excluded) -> np.ndarray:
+    """reference core.py:213-222 -- diagonal homes, selected columns minus excluded."""
+    mask = np.zeros((D, E), dtype=bool)
+    for e in range(E):
+        mask[e, e] = True
+    for e, ex in zip(selected, excluded):
+        mask[:, e] = True
+        for dv in ex:
+            mask[dv, e] = False
+    return mask
+
+
+def derive_loads(counts: np.ndarray, mask: np.ndarray):
+    """reference core.py:255-275: a (d, e) batch stays on d when d holds e,
+    otherwise it is computed (H) and received (R) at e's home, device e."""
+    counts = np.asarray(counts, dtype=np.int64)
+    D, E = counts.shape
+    kept = np.where(mask, counts, 0).sum(axis=1)
+    sent = np.where(mask, 0, counts).sum(axis=0)
+    H = kept.astype(np.int64)
+    H[:E] += sent
+    R = np.zeros(D, dtype=np.int64)
+    R[:E] = sent
+    return H, R
+
+
+def derive_loads_cellwise(counts: np.ndarray, mask: np.ndarray):
+    """Cell-by-cell restatement of the same rule (independent cross-check, in
+    the style of the reference's routed_by_hand, test_core.py:19-36)."""
+    counts = np.asarray(counts, dtype=np.int64)
+    D, E = counts.shape
+    H = np.zeros(D, dtype=np.int64)
+    R = np.zeros(D, dtype=np.int64)
+    for d in range(D):
+        for e in range(E):
+            c = int(counts[d, e])
+            if mask[d, e]:
+                H[d] += c
+            else:
+                H[e] += c
+                R[e] += c
+    return H, R
+
+
+def cost_terms(rmax: int, hmax: int, s: int, n: int, cm: dict) -> dict:
+    """reference perf_model.py:36-107 in its evaluation order."""
+    D = cm["num_devices"]
+    a2a = rmax * cm["input_bytes"] / cm["avg_bandwidth"]
+    fec = hmax / cm["compute_throughput"]
+    bec = 2.0 * fec
+    trans = s * (D - n) * cm["expert_param_bytes"] / (D * cm["avg_bandwidth"])
+    agg = s * (D - n) * cm["expert_grad_bytes"] / (D * cm["avg_bandwidth"])
+    ptrans = max(0.0, trans - fec - cm["fnec_time"])
+    pagg = max(0.0, agg - bec - cm["bnec_time"])
+    return {
+        "a2a": a2a, "fec": fec, "bec": bec, "trans": trans, "agg": agg,
+        "ptrans": ptrans, "pagg": pagg,
+        "unscheduled": 4.0 * a2a + fec + bec + trans + agg,
+        "scheduled": 4.0 * a2a + fec + bec + ptrans + pagg,
+    }
+
+
+def objective(H, R, s: int, n: int, cm: dict, overlap_aware: bool) -> float:
+    """reference planner.py:98-102."""
+    t = cost_terms(int(np.max(R)), int(np.max(H)), s, n, cm)
+    return t["scheduled"] if overlap_aware else t["unscheduled"]
+
+
+def bottom_devices(counts: np.ndarray, expert: int, n: int) -> frozenset:
+    """reference planner.py:71-77 (home excluded, key (count, index), original matrix)."""
+    col = counts[:, expert]
+    cands = sorted((int(col[d]), d) for d in range(counts.shape[0]) if d != expert)
+    return frozenset(d for _, d in cands[:n])
+
+
+def is_balanced(H, total_inputs: int, E: int, alpha: float) -> bool:
+    """reference planner.py:63-68."""
+    H = np.asarray(H)
+    return float(H.max() - H.min()) < alpha * total_inputs / E
+
+
+def greedy_search(counts, n: int, alpha: float, overlap_aware: bool, cm: dict) -> dict:
+    """reference planner.py:80-129 (Algorithm 1).  Returns the plan plus the
+    objective of the returned plan and the number of explored steps."""
+    counts = np.asarray(counts, dtype=np.int64)
+    D, E = counts.shape
+    assert D == E, "greedy search requires num_experts == num_devices"
+    total_inputs = int(counts.sum()) // cm["top_k"]
+    H, R = derive_loads(counts, replica_mask(D, E, (), ()))
+    best = objective(H, R, 0, 0, cm, overlap_aware)
+    selected, bottoms, used = [], [], set()
+    cnt = 0
+    while not is_balanced(H, total_inputs, E, alpha):
+        i = int(np.argmax(H))
+        if i in used:
+            break
+        used.add(i)
+        selected.append(i)
+        bottoms.append(bottom_devices(counts, i, n))
+        H, R = derive_loads(counts, replica_mask(D, E, selected, bottoms))
+        changed = objective(H, R, len(selected), n, cm, overlap_aware)
+        if changed < best:
+            best = changed
+            cnt = len(selected)
+    sel = tuple(selected[:cnt])
+    exc = tuple(bottoms[:cnt])
+    mask = replica_mask(D, E, sel, exc)
+    Hf, Rf = derive_loads(counts, mask)
+    return {"selected": sel, "excluded": exc, "best": best, "explored": len(selected),
+            "mask": mask, "H": Hf, "R": Rf}
+
+
+def plan_for_iteration(history, iter_index: int, reuse_interval: int, planner):
+    """reference planner.py:132-156; ``planner(counts)`` runs the search."""
+    anchor = (iter_index // reuse_interval) * reuse_interval
+    if anchor == 0:
+        return None
+    return planner(history[anchor - 1])
+
+
+def balance_degree(H) -> float:
+    """reference simulator.py:106-111 (population sigma)."""
+    return float(np.std(np.asarray(H, dtype=np.float64)))
+
+
+def rb_ratio(H_before, H_after) -> float:
+    """reference simulator.py:114-124."""
+    sb, sa = balance_degree(H_before), balance_degree(H_after)
+    if sa == 0.0:
+        return 1.0 if sb == 0.0 else float("inf")
+    return sb / sa
+
+
+def cost_model_dict(num_devices, top_k, input_bytes, param_bytes, grad_bytes, avg_bandwidth,
+                    compute_throughput, fnec=0.0, bnec=0.0) -> dict:
+    return {"num_devices": num_devices, "top_k": top_k, "input_bytes": input_bytes,
+            "expert_param_bytes": param_bytes, "expert_grad_bytes": grad_bytes,
+            "avg_bandwidth": avg_bandwidth, "compute_throughput": compute_throughput,
+            "fnec_time": fnec, "bnec_time": bnec}

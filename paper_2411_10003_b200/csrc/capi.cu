@@ -1,0 +1,26 @@
+// C-ABI error plumbing shared by every entry point of libppmoe.
+#include <stdarg.h>
+
+#include "common.cuh"
+
+namespace pp {
+
+static thread_local std::string t_last_error;
+
+void set_error(const std::string& msg) { t_last_error = msg; }
+
+int fail(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  t_last_error = buf;
+  return code;
+}
+
+}  // namespace pp
+
+extern "C" const char* pp_last_error(void) { return pp::t_last_error.c_str(); }
+
+extern "C" int pp_version(void) { return 1; }

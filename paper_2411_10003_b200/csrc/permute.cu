@@ -1,0 +1,539 @@
+// K1 host wrapper + K3: routing histogram, dispatch layout, fused permute/all-to-all,
+// combine, and their backward passes.
+//
+// Routing rule (reference derive_loads, pkg/src/moebal/core.py:267-274), applied
+// at virtual-expert-slot granularity: the pairs
+// of virtual slot v routed to expert e are computed on rank v / m when the plan's
+// replica mask holds mask[v][e], otherwise on e's home rank e / m.  The receive
+// layout of every rank is expert-major: one segment per expert the rank holds
+// (ascending expert id, padded to 128 rows), and inside a segment pairs are
+// ordered by (source slot v, token t) -- a stable order every rank derives from
+// the all-gathered LoadMatrix, so no host round trip is needed.
+//
+// Data moves over peer-mapped pointers: dispatch STORES a token row directly into
+// the computing rank's receive buffer (local or NVLink peer), combine LOADS the
+// expert outputs back from wherever they were computed.  At D = 1 the pointer
+// tables hold a single local buffer.
+#include "common.cuh"
+
+namespace pp {
+
+int route_gemm(const void* x, const void* wg, const float* bias, int T, int d, int E, int k,
+               int32_t* idx, float* w, float* probs, int32_t* rank, int32_t* chunk_counts,
+               cudaStream_t st);
+
+// ---------------------------------------------------------------------------
+__global__ void slot_histogram_kernel(const int32_t* chunk_counts, int chunks_per_slot, int E,
+                                      int m, int64_t* out) {
+  const int cell = blockIdx.x * blockDim.x + threadIdx.x;
+  if (cell >= m * E) return;
+  const int v = cell / E, e = cell % E;
+  int64_t s = 0;
+  for (int c = 0; c < chunks_per_slot; ++c)
+    s += chunk_counts[(size_t)(v * chunks_per_slot + c) * E + e];
+  out[(size_t)v * E + e] = s;
+}
+
+// ---------------------------------------------------------------------------
+// Layout solver: one CTA.  See ppmoe.h for the outputs.
+constexpr int kLayoutThreads = 1024;
+
+__global__ void __launch_bounds__(kLayoutThreads)
+    dispatch_layout_kernel(const int64_t* counts, const uint8_t* mask, const int32_t* chunk_counts,
+                           int D, int m, int E, int T, int me, int max_groups, int rows_capacity,
+                           int32_t* chunk_base, int32_t* slot_dest, pp_group* groups,
+                           int32_t* num_groups, int32_t* total_rows, int32_t* seg_start,
+                           int32_t* rep_slot) {
+  extern __shared__ int32_t sh[];
+  const int Ev = D * m;
+  int32_t* rows = sh;                   // [D][E]
+  int32_t* seg = rows + D * E;          // [D][E]
+  uint8_t* present = reinterpret_cast<uint8_t*>(seg + D * E);  // [D][E]
+  const int tid = threadIdx.x;
+
+  auto comp = [&](int v, int e) -> int {
+    const bool local = mask ? (mask[(size_t)v * E + e] != 0) : (v == e);
+    return local ? v / m : e / m;
+  };
+
+  // rows[r][e], present[r][e]
+  for (int cell = tid; cell < D * E; cell += blockDim.x) {
+    const int r = cell / E, e = cell % E;
+    int64_t acc = 0;
+    bool pres = (e / m == r);
+    for (int v = 0; v < Ev; ++v) {
+      const bool local = mask ? (mask[(size_t)v * E + e] != 0) : (v == e);
+      const int c = local ? v / m : e / m;
+      if (c == r) acc += counts[(size_t)v * E + e];
+      if (local && v / m == r) pres = true;
+    }
+    rows[cell] = (int32_t)acc;
+    present[cell] = pres;
+  }
+  __syncthreads();
+  // segment starts per rank (ascending expert order)
+  for (int r = tid; r < D; r += blockDim.x) {
+    int off = 0, nrep = 0;
+    for (int e = 0; e < E; ++e) {
+      const int cell = r * E + e;
+      const bool rep = present[cell] && (e / m != r);
+      if (rep_slot) rep_slot[cell] = rep ? m + nrep++ : -1;
+      if (present[cell]) {
+        seg[cell] = off;
+        off += (rows[cell] + PP_ROW_ALIGN - 1) / PP_ROW_ALIGN * PP_ROW_ALIGN;
+      } else {
+        seg[cell] = -1;
+      }
+      seg_start[cell] = seg[cell];
+    }
+    if (r == me) *total_rows = off;
+  }
+  __syncthreads();
+  // this rank's group table
+  if (tid == 0) {
+    int g = 0, nrep = 0;
+    for (int e = 0; e < E; ++e) {
+      const int cell = me * E + e;
+      if (!present[cell] || g >= max_groups) continue;
+      pp_group gr;
+      gr.row_off = seg[cell];
+      gr.rows = rows[cell];
+      gr.rows_pad = (rows[cell] + PP_ROW_ALIGN - 1) / PP_ROW_ALIGN * PP_ROW_ALIGN;
+      const bool home = (e / m == me);
+      gr.wslot = home ? (e % m) : (m + nrep++);
+      gr.expert = e;
+      gr.src_rank = e / m;
+      gr._pad[0] = gr._pad[1] = 0;
+      groups[g++] = gr;
+    }
+    *num_groups = g;
+  }
+  // per local slot j: destination and base row for each expert, then per chunk
+  const int chunks_per_slot = (T / m) / PP_CHUNK;
+  for (int cell = tid; cell < m * E; cell += blockDim.x) {
+    const int j = cell / E, e = cell % E;
+    const int v = me * m + j;
+    const int dest = comp(v, e);
+    int64_t base = seg[dest * E + e];
+    for (int v2 = 0; v2 < v; ++v2)
+      if (comp(v2, e) == dest) base += counts[(size_t)v2 * E + e];
+    slot_dest[cell] = dest;
+    for (int c = 0; c < chunks_per_slot; ++c) {
+      const int chunk = j * chunks_per_slot + c;
+      chunk_base[(size_t)chunk * E + e] = (int32_t)base;
+      base += chunk_counts[(size_t)chunk * E + e];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+template <int VPL>  // 16-byte vectors per lane per row (d = VPL * 256)
+__global__ void __launch_bounds__(256)
+    dispatch_kernel(const __nv_bfloat16* __restrict__ x, const int32_t* __restrict__ idx,
+                    const int32_t* __restrict__ rank, const int32_t* __restrict__ chunk_base,
+                    const int32_t* __restrict__ slot_dest, int T, int d, int k, int m, int E,
+                    void* const* recv_ptrs, int32_t* pair_dest, int32_t* pair_row) {
+  const int lane = threadIdx.x & 31;
+  const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  const int slot_tokens = T / m;
+  for (int t = warp_global; t < T; t += nwarps) {
+    uint4 v[VPL];
+    const uint4* src = reinterpret_cast<const uint4*>(x + (size_t)t * d);
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) v[i] = ld_nc_v4(src + lane + 32 * i);
+    int my_dest = 0, my_row = 0;
+    if (lane < k) {
+      const int e = idx[(size_t)t * k + lane];
+      const int slot = t / slot_tokens;
+      my_dest = slot_dest[slot * E + e];
+      my_row = chunk_base[(size_t)(t / PP_CHUNK) * E + e] + rank[(size_t)t * k + lane];
+      pair_dest[(size_t)t * k + lane] = my_dest;
+      pair_row[(size_t)t * k + lane] = my_row;
+    }
+    for (int j = 0; j < k; ++j) {
+      const int dest = __shfl_sync(0xffffffffu, my_dest, j);
+      const int row = __shfl_sync(0xffffffffu, my_row, j);
+      uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(recv_ptrs[dest]) +
+                                            (size_t)row * d);
+#pragma unroll
+      for (int i = 0; i < VPL; ++i) st_v4(dst + lane + 32 * i, v[i]);
+    }
+  }
+}
+
+// zero rows [row_off+rows, row_off+rows_pad) of every group of this rank
+__global__ void zero_padding_kernel(const pp_group* groups, const int32_t* num_groups, int d,
+                                    __nv_bfloat16* buf) {
+  const int g = blockIdx.x;
+  if (g >= *num_groups) return;
+  const pp_group gr = groups[g];
+  const size_t begin = (size_t)(gr.row_off + gr.rows) * d;
+  const size_t end = (size_t)(gr.row_off + gr.rows_pad) * d;
+  uint4* p = reinterpret_cast<uint4*>(buf);
+  for (size_t i = begin / 8 + threadIdx.x; i < end / 8; i += blockDim.x) p[i] = make_uint4(0, 0, 0, 0);
+}
+
+template <int VPL>
+__global__ void __launch_bounds__(256)
+    combine_kernel(void* const* out_ptrs, const int32_t* __restrict__ pair_dest,
+                   const int32_t* __restrict__ pair_row, const float* __restrict__ w, int T, int d,
+                   int k, __nv_bfloat16* y) {
+  const int lane = threadIdx.x & 31;
+  const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int t = warp_global; t < T; t += nwarps) {
+    float acc[VPL][8];
+#pragma unroll
+    for (int i = 0; i < VPL; ++i)
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc[i][u] = 0.f;
+    int my_dest = 0, my_row = 0;
+    float my_w = 0.f;
+    if (lane < k) {
+      my_dest = pair_dest[(size_t)t * k + lane];
+      my_row = pair_row[(size_t)t * k + lane];
+      my_w = w[(size_t)t * k + lane];
+    }
+    for (int j = 0; j < k; ++j) {
+      const int dest = __shfl_sync(0xffffffffu, my_dest, j);
+      const int row = __shfl_sync(0xffffffffu, my_row, j);
+      const float wj = __shfl_sync(0xffffffffu, my_w, j);
+      const uint4* src = reinterpret_cast<const uint4*>(
+          reinterpret_cast<const __nv_bfloat16*>(out_ptrs[dest]) + (size_t)row * d);
+      uint4 v[VPL];
+#pragma unroll
+      for (int i = 0; i < VPL; ++i) v[i] = ld_v4(src + lane + 32 * i);
+#pragma unroll
+      for (int i = 0; i < VPL; ++i) {
+        float f[8];
+        bf16x8_to_f32(v[i], f);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc[i][u] = fmaf(wj, f[u], acc[i][u]);
+      }
+    }
+    uint4* dst = reinterpret_cast<uint4*>(y + (size_t)t * d);
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) st_v4(dst + lane + 32 * i, f32x8_to_bf16(acc[i]));
+  }
+}
+
+template <int VPL>
+__global__ void __launch_bounds__(256)
+    combine_bwd_kernel(const __nv_bfloat16* __restrict__ dy, void* const* out_ptrs,
+                       void* const* dgrad_ptrs, const int32_t* __restrict__ pair_dest,
+                       const int32_t* __restrict__ pair_row, const float* __restrict__ w, int T,
+                       int d, int k, float* dw) {
+  const int lane = threadIdx.x & 31;
+  const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int t = warp_global; t < T; t += nwarps) {
+    float g[VPL][8];
+    const uint4* src = reinterpret_cast<const uint4*>(dy + (size_t)t * d);
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) bf16x8_to_f32(ld_nc_v4(src + lane + 32 * i), g[i]);
+    int my_dest = 0, my_row = 0;
+    float my_w = 0.f;
+    if (lane < k) {
+      my_dest = pair_dest[(size_t)t * k + lane];
+      my_row = pair_row[(size_t)t * k + lane];
+      my_w = w[(size_t)t * k + lane];
+    }
+    float my_dw = 0.f;
+    for (int j = 0; j < k; ++j) {
+      const int dest = __shfl_sync(0xffffffffu, my_dest, j);
+      const int row = __shfl_sync(0xffffffffu, my_row, j);
+      const float wj = __shfl_sync(0xffffffffu, my_w, j);
+      const size_t off = (size_t)row * d;
+      const uint4* ysrc =
+          reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(out_ptrs[dest]) + off);
+      uint4* gdst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(dgrad_ptrs[dest]) + off);
+      float dot = 0.f;
+#pragma unroll
+      for (int i = 0; i < VPL; ++i) {
+        float yv[8], o[8];
+        bf16x8_to_f32(ld_v4(ysrc + lane + 32 * i), yv);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          dot = fmaf(g[i][u], yv[u], dot);
+          o[u] = wj * g[i][u];
+        }
+        st_v4(gdst + lane + 32 * i, f32x8_to_bf16(o));
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+      if (lane == j) my_dw = dot;
+    }
+    if (lane < k) dw[(size_t)t * k + lane] = my_dw;
+  }
+}
+
+// dx[t] = sum_j dXp[pair] + sum_e dlogits[t][e] * wg[e]; dlogits from softmax backward.
+template <int VPL, int EMAX>
+__global__ void __launch_bounds__(256)
+    dispatch_bwd_kernel(void* const* dxp_ptrs, const int32_t* __restrict__ pair_dest,
+                        const int32_t* __restrict__ pair_row, const int32_t* __restrict__ idx,
+                        const float* __restrict__ probs, const float* __restrict__ dw,
+                        const __nv_bfloat16* __restrict__ wg, int T, int d, int k, int E,
+                        __nv_bfloat16* dx, float* dlogits) {
+  const int lane = threadIdx.x & 31;
+  const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int t = warp_global; t < T; t += nwarps) {
+    // ---- softmax backward restricted to the selected experts
+    int my_e = -1, my_dest = 0, my_row = 0;
+    float my_dw = 0.f, my_p = 0.f;
+    if (lane < k) {
+      my_e = idx[(size_t)t * k + lane];
+      my_dest = pair_dest[(size_t)t * k + lane];
+      my_row = pair_row[(size_t)t * k + lane];
+      my_dw = dw[(size_t)t * k + lane];
+      my_p = probs[(size_t)t * E + my_e];
+    }
+    float gsum = my_dw * my_p;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) gsum += __shfl_xor_sync(0xffffffffu, gsum, o);
+    // dlogits_i = p_i * (dw_{j(i)} [i selected] - gsum)
+    float dl[(EMAX + 31) / 32];
+#pragma unroll
+    for (int q = 0; q < (EMAX + 31) / 32; ++q) {
+      const int i = lane + 32 * q;
+      float sel_dw = 0.f;
+      for (int j = 0; j < k; ++j) {
+        const int ej = __shfl_sync(0xffffffffu, my_e, j);
+        const float dwj = __shfl_sync(0xffffffffu, my_dw, j);
+        if (ej == i) sel_dw = dwj;
+      }
+      dl[q] = 0.f;
+      if (i < E) {
+        dl[q] = probs[(size_t)t * E + i] * (sel_dw - gsum);
+        dlogits[(size_t)t * E + i] = dl[q];
+      }
+    }
+    // ---- gather expert-input grads
+    float acc[VPL][8];
+#pragma unroll
+    for (int i = 0; i < VPL; ++i)
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc[i][u] = 0.f;
+    for (int j = 0; j < k; ++j) {
+      const int dest = __shfl_sync(0xffffffffu, my_dest, j);
+      const int row = __shfl_sync(0xffffffffu, my_row, j);
+      const uint4* src = reinterpret_cast<const uint4*>(
+          reinterpret_cast<const __nv_bfloat16*>(dxp_ptrs[dest]) + (size_t)row * d);
+      uint4 v[VPL];
+#pragma unroll
+      for (int i = 0; i < VPL; ++i) v[i] = ld_v4(src + lane + 32 * i);
+#pragma unroll
+      for (int i = 0; i < VPL; ++i) {
+        float f[8];
+        bf16x8_to_f32(v[i], f);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc[i][u] += f[u];
+      }
+    }
+    // ---- gate input grad: sum_e dlogits[e] * wg[e]
+    for (int e = 0; e < E; ++e) {
+      const float de = __shfl_sync(0xffffffffu, dl[e >> 5], e & 31);
+      const uint4* wrow = reinterpret_cast<const uint4*>(wg + (size_t)e * d);
+#pragma unroll
+      for (int i = 0; i < VPL; ++i) {
+        float f[8];
+        bf16x8_to_f32(__ldg(wrow + lane + 32 * i), f);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc[i][u] = fmaf(de, f[u], acc[i][u]);
+      }
+    }
+    uint4* dst = reinterpret_cast<uint4*>(dx + (size_t)t * d);
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) st_v4(dst + lane + 32 * i, f32x8_to_bf16(acc[i]));
+  }
+}
+
+// dwg[e][col] += sum_t dlogits[t][e] * x[t][col]; block = 256 columns x a token split
+template <int EMAX>
+__global__ void __launch_bounds__(256)
+    gate_wgrad_kernel(const float* __restrict__ dlogits, const __nv_bfloat16* __restrict__ x,
+                      int T, int d, int E, int tokens_per_split, float* dwg) {
+  __shared__ float sdl[64][EMAX];
+  const int col = blockIdx.x * 256 + threadIdx.x;
+  const int t0 = blockIdx.y * tokens_per_split;
+  const int t1 = min(T, t0 + tokens_per_split);
+  float acc[EMAX];
+#pragma unroll
+  for (int e = 0; e < EMAX; ++e) acc[e] = 0.f;
+  for (int tb = t0; tb < t1; tb += 64) {
+    const int nt = min(64, t1 - tb);
+    __syncthreads();
+    for (int i = threadIdx.x; i < nt * E; i += 256) sdl[i / E][i % E] = dlogits[(size_t)tb * E + i];
+    __syncthreads();
+    for (int tt = 0; tt < nt; ++tt) {
+      const float xv = __bfloat162float(x[(size_t)(tb + tt) * d + col]);
+#pragma unroll
+      for (int e = 0; e < EMAX; ++e)
+        if (e < E) acc[e] = fmaf(sdl[tt][e], xv, acc[e]);
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < EMAX; ++e)
+    if (e < E) atomicAdd(dwg + (size_t)e * d + col, acc[e]);
+}
+
+static int grid_for_tokens(int T) {
+  int blocks = (T + 7) / 8;  // 8 warps per block, one token per warp per step
+  return blocks < 148 * 8 ? blocks : 148 * 8;
+}
+
+}  // namespace pp
+
+using namespace pp;
+
+#define PP_VPL_SWITCH(d, ...)                                               \
+  switch ((d) / 256) {                                                      \
+    case 1: { constexpr int VPL = 1; __VA_ARGS__; break; }                  \
+    case 2: { constexpr int VPL = 2; __VA_ARGS__; break; }                  \
+    case 4: { constexpr int VPL = 4; __VA_ARGS__; break; }                  \
+    case 8: { constexpr int VPL = 8; __VA_ARGS__; break; }                  \
+    case 16: { constexpr int VPL = 16; __VA_ARGS__; break; }                \
+    default: return fail(PP_EINVAL, "d=%d must be 256 * {1,2,4,8,16}", d);  \
+  }
+
+extern "C" int pp_route_topk(const void* x, const void* wg, const float* bias, int32_t T,
+                             int32_t d, int32_t E, int32_t k, int32_t* idx, float* w,
+                             float* probs, int32_t* rank, int32_t* chunk_counts, void* stream) {
+  PP_CHECK_ARG(x && wg && idx && w && probs && rank && chunk_counts, "pp_route_topk: null pointer");
+  PP_CHECK_ARG(T > 0 && T % PP_CHUNK == 0, "pp_route_topk: T=%d must be a positive multiple of %d",
+               T, PP_CHUNK);
+  PP_CHECK_ARG(d > 0 && d % 64 == 0, "pp_route_topk: d=%d must be a multiple of 64", d);
+  PP_CHECK_ARG(E >= 4 && E <= 128 && E % 4 == 0, "pp_route_topk: E=%d unsupported", E);
+  PP_CHECK_ARG(k >= 1 && k <= 8 && k <= E, "pp_route_topk: k=%d unsupported", k);
+  return route_gemm(x, wg, bias, T, d, E, k, idx, w, probs, rank, chunk_counts, as_stream(stream));
+}
+
+extern "C" int pp_slot_histogram(const int32_t* chunk_counts, int32_t T, int32_t E, int32_t m,
+                                 int64_t* out, int32_t row0, void* stream) {
+  PP_CHECK_ARG(chunk_counts && out, "pp_slot_histogram: null pointer");
+  PP_CHECK_ARG(m >= 1 && T % (m * PP_CHUNK) == 0,
+               "pp_slot_histogram: T=%d must split into m=%d slots of whole %d-token chunks", T, m,
+               PP_CHUNK);
+  const int cps = (T / m) / PP_CHUNK;
+  const int cells = m * E;
+  slot_histogram_kernel<<<(cells + 255) / 256, 256, 0, as_stream(stream)>>>(
+      chunk_counts, cps, E, m, out + (size_t)row0 * E);
+  PP_LAUNCH_CHECK();
+  return PP_OK;
+}
+
+extern "C" int pp_dispatch_layout(const int64_t* counts, const uint8_t* mask,
+                                  const int32_t* chunk_counts, int32_t D, int32_t m, int32_t E,
+                                  int32_t T, int32_t my_rank, int32_t max_groups,
+                                  int32_t rows_capacity, int32_t* chunk_base, int32_t* slot_dest,
+                                  pp_group* groups, int32_t* num_groups, int32_t* total_rows,
+                                  int32_t* seg_start, int32_t* rep_slot, void* stream) {
+  PP_CHECK_ARG(counts && chunk_counts && chunk_base && slot_dest && groups && num_groups &&
+                   total_rows && seg_start,
+               "pp_dispatch_layout: null pointer");
+  PP_CHECK_ARG(D >= 1 && m >= 1 && E == D * m, "pp_dispatch_layout: need E == D*m (E=%d D=%d m=%d)",
+               E, D, m);
+  PP_CHECK_ARG(my_rank >= 0 && my_rank < D, "pp_dispatch_layout: bad rank %d", my_rank);
+  PP_CHECK_ARG(T % (m * PP_CHUNK) == 0, "pp_dispatch_layout: T=%d not a multiple of m*%d", T,
+               PP_CHUNK);
+  const size_t smem = (size_t)D * E * (2 * sizeof(int32_t) + 1);
+  PP_CHECK_ARG(smem <= 48 * 1024, "pp_dispatch_layout: D*E too large");
+  dispatch_layout_kernel<<<1, kLayoutThreads, smem, as_stream(stream)>>>(
+      counts, mask, chunk_counts, D, m, E, T, my_rank, max_groups, rows_capacity, chunk_base,
+      slot_dest, groups, num_groups, total_rows, seg_start, rep_slot);
+  PP_LAUNCH_CHECK();
+  return PP_OK;
+}
+
+extern "C" int pp_dispatch(const void* x, const int32_t* idx, const int32_t* rank,
+                           const int32_t* chunk_base, const int32_t* slot_dest, int32_t T,
+                           int32_t d, int32_t k, int32_t m, int32_t E, void* const* recv_ptrs,
+                           void* own_recv, const pp_group* groups, const int32_t* num_groups,
+                           int32_t max_groups, int32_t* pair_dest, int32_t* pair_row,
+                           void* stream) {
+  PP_CHECK_ARG(x && idx && rank && chunk_base && slot_dest && recv_ptrs && own_recv && groups &&
+                   num_groups && pair_dest && pair_row,
+               "pp_dispatch: null pointer");
+  cudaStream_t st = as_stream(stream);
+  zero_padding_kernel<<<max_groups, 256, 0, st>>>(groups, num_groups, d,
+                                                  reinterpret_cast<__nv_bfloat16*>(own_recv));
+  PP_LAUNCH_CHECK();
+  PP_VPL_SWITCH(d, (dispatch_kernel<VPL><<<grid_for_tokens(T), 256, 0, st>>>(
+                       reinterpret_cast<const __nv_bfloat16*>(x), idx, rank, chunk_base,
+                       slot_dest, T, d, k, m, E, recv_ptrs, pair_dest, pair_row)));
+  PP_LAUNCH_CHECK();
+  return PP_OK;
+}
+
+extern "C" int pp_combine(void* const* out_ptrs, const int32_t* pair_dest, const int32_t* pair_row,
+                          const float* w, int32_t T, int32_t d, int32_t k, void* y, void* stream) {
+  PP_CHECK_ARG(out_ptrs && pair_dest && pair_row && w && y, "pp_combine: null pointer");
+  PP_VPL_SWITCH(d, (combine_kernel<VPL><<<grid_for_tokens(T), 256, 0, as_stream(stream)>>>(
+                       out_ptrs, pair_dest, pair_row, w, T, d, k,
+                       reinterpret_cast<__nv_bfloat16*>(y))));
+  PP_LAUNCH_CHECK();
+  return PP_OK;
+}
+
+extern "C" int pp_combine_bwd(const void* dy, void* const* out_ptrs, void* const* dgrad_ptrs,
+                              void* own_dgrad, const int32_t* pair_dest, const int32_t* pair_row,
+                              const float* w, const pp_group* groups, const int32_t* num_groups,
+                              int32_t max_groups, int32_t T, int32_t d, int32_t k, float* dw,
+                              void* stream) {
+  PP_CHECK_ARG(dy && out_ptrs && dgrad_ptrs && own_dgrad && pair_dest && pair_row && w && groups &&
+                   num_groups && dw,
+               "pp_combine_bwd: null pointer");
+  cudaStream_t st = as_stream(stream);
+  zero_padding_kernel<<<max_groups, 256, 0, st>>>(groups, num_groups, d,
+                                                  reinterpret_cast<__nv_bfloat16*>(own_dgrad));
+  PP_LAUNCH_CHECK();
+  PP_VPL_SWITCH(d, (combine_bwd_kernel<VPL><<<grid_for_tokens(T), 256, 0, st>>>(
+                       reinterpret_cast<const __nv_bfloat16*>(dy), out_ptrs, dgrad_ptrs,
+                       pair_dest, pair_row, w, T, d, k, dw)));
+  PP_LAUNCH_CHECK();
+  return PP_OK;
+}
+
+extern "C" int pp_dispatch_bwd(void* const* dxp_ptrs, const int32_t* pair_dest,
+                               const int32_t* pair_row, const int32_t* idx, const float* probs,
+                               const float* dw, const void* wg, int32_t T, int32_t d, int32_t k,
+                               int32_t E, void* dx, float* dlogits, void* stream) {
+  PP_CHECK_ARG(dxp_ptrs && pair_dest && pair_row && idx && probs && dw && wg && dx && dlogits,
+               "pp_dispatch_bwd: null pointer");
+  PP_CHECK_ARG(E <= 128, "pp_dispatch_bwd: E=%d > 128", E);
+  cudaStream_t st = as_stream(stream);
+  const auto* wgp = reinterpret_cast<const __nv_bfloat16*>(wg);
+  auto* dxp = reinterpret_cast<__nv_bfloat16*>(dx);
+  if (E <= 32) {
+    PP_VPL_SWITCH(d, (dispatch_bwd_kernel<VPL, 32><<<grid_for_tokens(T), 256, 0, st>>>(
+                         dxp_ptrs, pair_dest, pair_row, idx, probs, dw, wgp, T, d, k, E, dxp, dlogits)));
+  } else if (E <= 64) {
+    PP_VPL_SWITCH(d, (dispatch_bwd_kernel<VPL, 64><<<grid_for_tokens(T), 256, 0, st>>>(
+                         dxp_ptrs, pair_dest, pair_row, idx, probs, dw, wgp, T, d, k, E, dxp, dlogits)));
+  } else {
+    PP_VPL_SWITCH(d, (dispatch_bwd_kernel<VPL, 128><<<grid_for_tokens(T), 256, 0, st>>>(
+                         dxp_ptrs, pair_dest, pair_row, idx, probs, dw, wgp, T, d, k, E, dxp, dlogits)));
+  }
+  PP_LAUNCH_CHECK();
+  return PP_OK;
+}
+
+extern "C" int pp_gate_wgrad(const float* dlogits, const void* x, int32_t T, int32_t d, int32_t E,
+                             float* dwg, void* stream) {
+  PP_CHECK_ARG(dlogits && x && dwg, "pp_gate_wgrad: null pointer");
+  PP_CHECK_ARG(d % 256 == 0, "pp_gate_wgrad: d=%d must be a multiple of 256", d);
+  PP_CHECK_ARG(E <= 64, "pp_gate_wgrad: E=%d > 64", E);
+  const int splits = (T + 511) / 512;
+  dim3 grid(d / 256, splits);
+  const auto* xp = reinterpret_cast<const __nv_bfloat16*>(x);
+  if (E <= 16)
+    gate_wgrad_kernel<16><<<grid, 256, 0, as_stream(stream)>>>(dlogits, xp, T, d, E, 512, dwg);
+  else if (E <= 32)
+    gate_wgrad_kernel<32><<<grid, 256, 0, as_stream(stream)>>>(dlogits, xp, T, d, E, 512, dwg);
+  else
+    gate_wgrad_kernel<64><<<grid, 256, 0, as_stream(stream)>>>(dlogits, xp, T, d, E, 512, dwg);
+  PP_LAUNCH_CHECK();
+  return PP_OK;
+}

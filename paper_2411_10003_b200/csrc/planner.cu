@@ -1,0 +1,273 @@
+// K2: Pro-Prophet greedy replica-placement planner on device (Algorithm 1).
+//
+// Bit-exact restatement of reference greedy_search (pkg/src/moebal/planner.py:80-129):
+//   * total_inputs = sum(counts) // top_k                         planner.py:104
+//   * loop while not is_balanced(H)                               planner.py:114, :63-68
+//   * i = first argmax(H); stop if i was already used             planner.py:115-117
+//   * excluded = n non-home devices with fewest counts[:, i] on the ORIGINAL
+//     matrix, key (count, index)                                  planner.py:71-77, :120
+//   * re-derive H/R under the candidate (derive_loads core.py:255-275) -- here
+//     incrementally: selecting i only moves column i's non-excluded cells from
+//     "sent to home" to "computed locally"; exact int64 arithmetic
+//   * objective = total_(un)scheduled with the exact fp64 association order of
+//     perf_model._build (perf_model.py:86-107); strict improvement accepts,
+//     and the search continues from rejected candidates       planner.py:122-127
+//   * return the accepted prefix selected[:cnt]                   planner.py:129
+//
+// One CTA per layer; thread d owns device d (== expert d, since D == E).  All
+// fp64 math uses __d*_rn intrinsics so no FMA contraction can change a bit.
+#include <stdarg.h>
+
+#include "common.cuh"
+
+namespace pp {
+
+struct PlanArgs {
+  const int64_t* counts;
+  int E;
+  pp_cost_model cm;
+  pp_planner_cfg cfg;
+  int32_t* selected;
+  int32_t* num_selected;
+  int32_t* num_explored;
+  uint8_t* mask;
+  int64_t* H;
+  int64_t* R;
+  double* best_cost;
+};
+
+constexpr int kMaxPlanThreads = 1024;
+constexpr int kMaxWarps = kMaxPlanThreads / 32;
+
+struct Red {
+  int64_t v;
+  int32_t i;
+};
+
+// block-wide reductions over one value per thread (threads >= E contribute neutral values)
+template <typename Op>
+__device__ __forceinline__ Red block_reduce(Red x, Op op, Red* scratch) {
+  for (int o = 16; o > 0; o >>= 1) {
+    Red y;
+    y.v = __shfl_xor_sync(0xffffffffu, x.v, o);
+    y.i = __shfl_xor_sync(0xffffffffu, x.i, o);
+    x = op(x, y);
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  __syncthreads();
+  if (lane == 0) scratch[warp] = x;
+  __syncthreads();
+  Red r = scratch[0];
+  for (int w = 1; w < nwarps; ++w) r = op(r, scratch[w]);
+  return r;
+}
+
+struct MaxFirst {  // larger value wins, ties -> lower index (np.argmax first max)
+  __device__ Red operator()(Red a, Red b) const {
+    if (a.v > b.v) return a;
+    if (b.v > a.v) return b;
+    return a.i <= b.i ? a : b;
+  }
+};
+struct MinOp {
+  __device__ Red operator()(Red a, Red b) const { return a.v <= b.v ? a : b; }
+};
+struct SumOp {
+  __device__ Red operator()(Red a, Red b) const { return Red{a.v + b.v, 0}; }
+};
+
+// perf_model._build + the objective selector of planner.py:98-102
+__device__ double objective(const pp_cost_model& cm, bool overlap, int64_t rmax, int64_t hmax,
+                            int s, int n) {
+  const double a2a = __ddiv_rn(__dmul_rn((double)rmax, cm.input_bytes), cm.avg_bandwidth);
+  const double fec = __ddiv_rn((double)hmax, cm.compute_throughput);
+  const double bec = __dmul_rn(2.0, fec);
+  const double D = (double)cm.num_devices;
+  const double sdn = (double)((int64_t)s * (int64_t)(cm.num_devices - n));
+  const double denom = __dmul_rn(D, cm.avg_bandwidth);
+  const double trans = __ddiv_rn(__dmul_rn(sdn, cm.expert_param_bytes), denom);
+  const double agg = __ddiv_rn(__dmul_rn(sdn, cm.expert_grad_bytes), denom);
+  double t = __dadd_rn(__dadd_rn(__dmul_rn(4.0, a2a), fec), bec);
+  if (overlap) {
+    double pt = __dsub_rn(__dsub_rn(trans, fec), cm.fnec_time);
+    double pa = __dsub_rn(__dsub_rn(agg, bec), cm.bnec_time);
+    pt = pt > 0.0 ? pt : 0.0;
+    pa = pa > 0.0 ? pa : 0.0;
+    return __dadd_rn(__dadd_rn(t, pt), pa);
+  }
+  return __dadd_rn(__dadd_rn(t, trans), agg);
+}
+
+// rank of device d among the non-home candidates of column `col` (key: count, index)
+__device__ __forceinline__ int bottom_rank(const int64_t* col, int E, int home, int d) {
+  const int64_t c = col[d];
+  int r = 0;
+  for (int j = 0; j < E; ++j) {
+    if (j == home || j == d) continue;
+    const int64_t cj = col[j];
+    r += (cj < c) || (cj == c && j < d);
+  }
+  return r;
+}
+
+__global__ void __launch_bounds__(kMaxPlanThreads) plan_greedy_kernel(PlanArgs a) {
+  const int L = blockIdx.x;
+  const int E = a.E;
+  const int d = threadIdx.x;
+  const bool active = d < E;
+  const int64_t* counts = a.counts + (size_t)L * E * E;
+  const int n = a.cfg.n;
+  const bool overlap = a.cfg.overlap_aware != 0;
+
+  extern __shared__ int64_t smem_col[];  // [E] column of the expert being placed
+  __shared__ Red scratch[kMaxWarps];
+  __shared__ int32_t sel_list[kMaxPlanThreads];
+  __shared__ uint8_t used[kMaxPlanThreads];
+
+  if (active) used[d] = 0;
+
+  // initial (vanilla EP) loads: local[d] = counts[d][d]; remote[d] = sum_{d'!=d} counts[d'][d]
+  int64_t local = 0, remote = 0, rowsum = 0;
+  if (active) {
+    local = counts[(size_t)d * E + d];
+    for (int j = 0; j < E; ++j) {
+      if (j != d) remote += counts[(size_t)j * E + d];
+      rowsum += counts[(size_t)d * E + j];
+    }
+  }
+  const int64_t total = block_reduce(Red{rowsum, 0}, SumOp(), scratch).v;
+  const int64_t total_inputs = total / a.cm.top_k;  // non-negative: floor == Python //
+  const double threshold = __ddiv_rn(__dmul_rn(a.cfg.alpha, (double)total_inputs), (double)E);
+
+  const Red neutral_max{INT64_MIN, 0x7fffffff};
+  const Red neutral_min{INT64_MAX, 0x7fffffff};
+
+  auto loads_reduce = [&](int64_t h, int64_t r, Red& hmax, Red& hmin, Red& rmax) {
+    hmax = block_reduce(active ? Red{h, d} : neutral_max, MaxFirst(), scratch);
+    hmin = block_reduce(active ? Red{h, d} : neutral_min, MinOp(), scratch);
+    rmax = block_reduce(active ? Red{r, d} : neutral_max, MaxFirst(), scratch);
+  };
+
+  Red hmax, hmin, rmax;
+  loads_reduce(local + remote, remote, hmax, hmin, rmax);
+  double best = objective(a.cm, overlap, rmax.v, hmax.v, 0, 0);
+  int cnt = 0, s = 0;
+
+  while (true) {
+    const double spread = (double)(hmax.v - hmin.v);
+    if (spread < threshold) break;  // is_balanced
+    const int i = hmax.i;
+    if (used[i]) break;
+    __syncthreads();
+    if (d == 0) {
+      used[i] = 1;
+      sel_list[s] = i;
+    }
+    if (active) smem_col[d] = counts[(size_t)d * E + i];
+    __syncthreads();
+    ++s;
+    // move column i's non-excluded, non-home cells to local compute
+    int64_t moved = 0;
+    if (active && d != i) {
+      const bool excluded = bottom_rank(smem_col, E, i, d) < n;
+      if (!excluded) {
+        moved = smem_col[d];
+        local += moved;
+      }
+    }
+    const int64_t moved_total = block_reduce(Red{moved, 0}, SumOp(), scratch).v;
+    if (d == i) remote -= moved_total;
+    loads_reduce(local + remote, remote, hmax, hmin, rmax);
+    const double changed = objective(a.cm, overlap, rmax.v, hmax.v, s, n);
+    if (changed < best) {
+      best = changed;
+      cnt = s;
+    }
+  }
+  __syncthreads();
+
+  // Replay the accepted prefix to emit its mask and H/R (derive_loads of the result).
+  uint8_t* mask = a.mask + (size_t)L * E * E;
+  if (active) {
+    for (int e = 0; e < E; ++e) mask[(size_t)d * E + e] = (d == e);
+  }
+  __syncthreads();
+  for (int p = 0; p < cnt; ++p) {
+    const int i = sel_list[p];
+    if (active) smem_col[d] = counts[(size_t)d * E + i];
+    __syncthreads();
+    if (active && d != i) mask[(size_t)d * E + i] = bottom_rank(smem_col, E, i, d) >= n;
+    __syncthreads();
+  }
+  __threadfence_block();
+  __syncthreads();
+  if (active) {
+    int64_t loc = 0, rem = 0;
+    for (int j = 0; j < E; ++j) {
+      const int64_t c_dj = counts[(size_t)d * E + j];
+      if (mask[(size_t)d * E + j]) loc += c_dj;
+      const int64_t c_jd = counts[(size_t)j * E + d];
+      if (!mask[(size_t)j * E + d]) rem += c_jd;
+    }
+    a.H[(size_t)L * E + d] = loc + rem;
+    a.R[(size_t)L * E + d] = rem;
+    a.selected[(size_t)L * E + d] = d < cnt ? sel_list[d] : -1;
+  }
+  if (d == 0) {
+    a.num_selected[L] = cnt;
+    a.num_explored[L] = s;
+    a.best_cost[L] = best;
+  }
+}
+
+__global__ void derive_loads_kernel(const int64_t* counts, const uint8_t* mask, int D, int E,
+                                    int64_t* H, int64_t* R) {
+  for (int x = threadIdx.x; x < D; x += blockDim.x) {
+    int64_t loc = 0, rem = 0;
+    for (int e = 0; e < E; ++e)
+      if (mask[(size_t)x * E + e]) loc += counts[(size_t)x * E + e];
+    if (x < E) {
+      for (int j = 0; j < D; ++j)
+        if (!mask[(size_t)j * E + x]) rem += counts[(size_t)j * E + x];
+    }
+    H[x] = loc + rem;
+    R[x] = rem;
+  }
+}
+
+}  // namespace pp
+
+using namespace pp;
+
+extern "C" int pp_plan_greedy(const int64_t* counts, int32_t num_layers, int32_t E,
+                              const pp_cost_model* cm, const pp_planner_cfg* cfg,
+                              int32_t* selected, int32_t* num_selected, int32_t* num_explored,
+                              uint8_t* mask, int64_t* H, int64_t* R, double* best_cost,
+                              void* stream) {
+  PP_CHECK_ARG(counts && cm && cfg && selected && num_selected && num_explored && mask && H && R &&
+                   best_cost,
+               "pp_plan_greedy: null pointer");
+  PP_CHECK_ARG(num_layers >= 1, "pp_plan_greedy: num_layers must be >= 1, got %d", num_layers);
+  PP_CHECK_ARG(E >= 1 && E <= kMaxPlanThreads, "pp_plan_greedy: E must be in [1, %d], got %d",
+               kMaxPlanThreads, E);
+  if (cm->num_devices != E || cm->num_experts != E)
+    return fail(PP_EDIM, "pp_plan_greedy: cost model is %dx%d, load is %dx%d", cm->num_devices,
+                cm->num_experts, E, E);
+  PP_CHECK_ARG(cfg->n >= 0 && cfg->n < E, "n must be < num_devices=%d, got %d", E, cfg->n);
+  PP_CHECK_ARG(cm->top_k >= 1, "top_k must be >= 1");
+  PlanArgs a{counts, E, *cm, *cfg, selected, num_selected, num_explored, mask, H, R, best_cost};
+  const int threads = ((E + 31) / 32) * 32;
+  plan_greedy_kernel<<<num_layers, threads, sizeof(int64_t) * E, as_stream(stream)>>>(a);
+  PP_LAUNCH_CHECK();
+  return PP_OK;
+}
+
+extern "C" int pp_derive_loads(const int64_t* counts, const uint8_t* mask, int32_t D, int32_t E,
+                               int64_t* H, int64_t* R, void* stream) {
+  PP_CHECK_ARG(counts && mask && H && R, "pp_derive_loads: null pointer");
+  PP_CHECK_ARG(D >= 1 && E >= 1, "pp_derive_loads: empty dims");
+  if (E > D) return fail(PP_EDIM, "pp_derive_loads: identity homes need E <= D (E=%d, D=%d)", E, D);
+  derive_loads_kernel<<<1, 256, 0, as_stream(stream)>>>(counts, mask, D, E, H, R);
+  PP_LAUNCH_CHECK();
+  return PP_OK;
+}

@@ -1,0 +1,443 @@
+"""Expert-parallel MoE layer with Pro-Prophet planning, B200-native.
+
+The reference (``moebal``) never executes this layer: it prices it with
+Eq. 1-7 (``perf_model.py:36-107``) from a LoadMatrix (``core.py:88-142``)
+and a placement (``core.py:145-222``).  Here the layer runs for real, and
+the reference's objects are its interface:
+
+  forward  (per rank, stream-ordered, no host sync)
+    K1 pp_route_topk       gate GEMM on tcgen05 + softmax/top-k/chunk ranks
+       pp_slot_histogram   this rank's virtual-slot rows of the LoadMatrix
+       all-gather          -> LoadMatrix [E x E] on every rank (tiny)
+    K3 pp_dispatch_layout  receive layout from LoadMatrix + replica mask
+    K5 pp_replica_trans    (D>1) replicas pull the planned experts' params
+    K3 pp_dispatch         permute + all-to-all in one kernel (peer stores)
+       barrier
+    K4 FWD1, FWD2          grouped tcgen05 GEMMs (GeLU fused)
+       barrier
+    K3 pp_combine          weighted gather back (peer loads)
+    K2 pp_plan_greedy      (D>1, side stream) plan for iteration j+1 on this
+                           iteration's LoadMatrix (plan_for_iteration rule)
+  backward mirrors it: combine_bwd (push), DGRAD2/WGRAD2/DGRAD1/WGRAD1,
+  dispatch_bwd (pull) + gate grads, K5 pp_replica_agg (D>1).
+
+Virtual expert slots: with m = E/D experts per rank, each
+rank's T tokens are cut into m contiguous slots; slot v = rank*m + j is a
+planner "device", so the reference planner (which needs E == D,
+``planner.py:88-90``) applies unmodified to an E x E LoadMatrix.
+
+Weight layout per rank: arenas W1 [slots, f, d] and W2 [slots, d, f] (bf16),
+slots 0..m-1 = home experts (expert rank*m + j), then replica slots.  Gradients
+are fp32 ``main_grad`` arenas of the same shape (Megatron-style: the bf16
+parameters get no ``.grad``; read ``layer.w1_main_grad`` etc.).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _device, _lib
+from .core import ClusterSpec, LoadMatrix, ModelSpec, ValidationError
+from .planner import PlannerConfig
+
+
+class _CAI:
+    def __init__(self, ptr: int, nbytes: int) -> None:
+        self.__cuda_array_interface__ = {
+            "shape": (nbytes,), "typestr": "|u1", "data": (ptr, False), "version": 3, "strides": None,
+        }
+
+
+def _wrap(ptr: int, nbytes: int, dtype, shape) -> torch.Tensor:
+    raw = torch.as_tensor(_CAI(ptr, nbytes), device="cuda")
+    return raw.view(dtype).view(shape)
+
+
+class PeerBuffer:
+    """One symmetric buffer: this rank's allocation + a device table of every
+    rank's mapping of its peer (CUDA IPC over NVLink).  At D == 1 it is a
+    plain local tensor and a one-entry table."""
+
+    def __init__(self, shape, dtype, group, device) -> None:
+        self.shape = tuple(shape)
+        self.dtype = dtype
+        nbytes = int(np.prod(self.shape)) * torch.empty((), dtype=dtype).element_size()
+        self.world = dist.get_world_size(group) if group is not None else 1
+        self.rank = dist.get_rank(group) if group is not None else 0
+        self._owned = None
+        self._imported = []
+        if self.world == 1:
+            self.local = torch.zeros(self.shape, dtype=dtype, device=device)
+            ptrs = [self.local.data_ptr()]
+        else:
+            lib = _lib.load()
+            p = ctypes.c_void_p()
+            _lib.check(lib.pp_device_alloc(nbytes, ctypes.byref(p)), "pp_device_alloc")
+            self._owned = p.value
+            self.local = _wrap(self._owned, nbytes, dtype, self.shape)
+            self.local.zero_()
+            h = (ctypes.c_uint8 * 64)()
+            _lib.check(lib.pp_ipc_export(self._owned, h), "pp_ipc_export")
+            handles = [None] * self.world
+            dist.all_gather_object(handles, bytes(h), group=group)
+            ptrs = []
+            for r, hb in enumerate(handles):
+                if r == self.rank:
+                    ptrs.append(self._owned)
+                    continue
+                q = ctypes.c_void_p()
+                hh = (ctypes.c_uint8 * 64).from_buffer_copy(hb)
+                _lib.check(lib.pp_ipc_import(hh, ctypes.byref(q)), "pp_ipc_import")
+                self._imported.append(q.value)
+                ptrs.append(q.value)
+        self.ptrs = torch.tensor(ptrs, dtype=torch.int64, device=device)
+
+    def close(self) -> None:
+        lib = _lib.load()
+        for q in self._imported:
+            lib.pp_ipc_close(q)
+        self._imported = []
+        if self._owned is not None:
+            lib.pp_device_free(self._owned)
+            self._owned = None
+
+
+class _Barrier:
+    def __init__(self, group, device) -> None:
+        self.world = dist.get_world_size(group) if group is not None else 1
+        self.rank = dist.get_rank(group) if group is not None else 0
+        self.epoch = 0
+        if self.world > 1:
+            self.sig = PeerBuffer((self.world,), torch.int64, group, device)
+            torch.cuda.synchronize()
+            dist.barrier(group=group)
+
+    def __call__(self, stream=None) -> None:
+        if self.world == 1:
+            return
+        self.epoch += 1
+        _lib.call("pp_peer_barrier", self.sig.ptrs.data_ptr(), self.world, self.rank, self.epoch,
+                  _device.stream_ptr(stream))
+
+
+def default_specs(E: int, k: int, d: int, f: int, tokens_total: int, fnec: float = 0.0,
+                  bnec: float = 0.0, avg_bandwidth: float = 450e9, throughput: float | None = None):
+    """Cost-model constants for the virtual-slot planner of one layer.
+
+    input_bytes = one routed row (d bf16); param bytes = W1+W2 bf16; grad
+    bytes = fp32 grads.  compute_throughput defaults to the pairs/s of one
+    B200 slot at ~1.2 PFLOP/s (6*d*f flops per pair fwd) split over m slots
+    -- calibrate from a measured run."""
+    if throughput is None:
+        throughput = 1.2e15 / (6.0 * d * f)
+    cluster = ClusterSpec(num_devices=max(E, 2), avg_bandwidth=avg_bandwidth, compute_throughput=throughput)
+    model = ModelSpec(num_experts=max(E, 2), num_blocks=1, top_k=k, input_bytes=2 * d,
+                      expert_param_bytes=2 * 2 * d * f, expert_grad_bytes=2 * 4 * d * f,
+                      fnec_time=fnec, bnec_time=bnec)
+    return cluster, model
+
+
+class MoELayer(torch.nn.Module):
+    """Pro-Prophet EP MoE layer (GeLU FFN experts, top-k softmax gate).
+
+    Args:
+      d_model, d_ff, num_experts, top_k: layer shape (E % world == 0).
+      tokens: tokens per rank per call (multiple of (E/world)*128).
+      group: torch.distributed process group spanning the EP ranks (None = 1 GPU).
+      planner: PlannerConfig (n, alpha, reuse_interval, overlap_aware); planning
+        runs only when world > 1 (ClusterSpec needs D >= 2).
+      cluster/model: cost-model specs for the planner (default: default_specs).
+      capacity_rows: receive-buffer rows (default: worst case world*tokens*k + E*128,
+        i.e. no token is ever dropped).
+    """
+
+    def __init__(self, d_model: int, d_ff: int, num_experts: int, top_k: int, tokens: int,
+                 group=None, planner: PlannerConfig | None = None, cluster=None, model=None,
+                 capacity_rows: int | None = None, max_replicas: int | None = None,
+                 seed: int = 0, device=None, trans_ctas: int = 16) -> None:
+        super().__init__()
+        if not torch.cuda.is_available():
+            raise RuntimeError("MoELayer needs a CUDA device (B200); there is no CPU path")
+        _lib.load()
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.group = group
+        self.world = dist.get_world_size(group) if (group is not None and dist.is_initialized()) else 1
+        self.rank = dist.get_rank(group) if self.world > 1 else 0
+        if self.world == 1:
+            self.group = None
+        E, D = num_experts, self.world
+        if E % D:
+            raise ValidationError(f"num_experts={E} must be a multiple of the EP world size {D}")
+        self.d, self.f, self.E, self.k, self.T = d_model, d_ff, E, top_k, tokens
+        self.m = E // D
+        if tokens % (self.m * _lib.PP_CHUNK):
+            raise ValidationError(f"tokens={tokens} must be a multiple of (E/D)*{_lib.PP_CHUNK}={self.m * _lib.PP_CHUNK}")
+        if d_model % 256 or d_ff % 256:
+            raise ValidationError("d_model and d_ff must be multiples of 256")
+        self.planner_cfg = planner or PlannerConfig()
+        if cluster is None or model is None:
+            cluster, model = default_specs(E, top_k, d_model, d_ff, tokens * D)
+        self.cluster, self.model = cluster, model
+        self.max_replicas = (E - self.m) if max_replicas is None else max_replicas
+        self.slots = self.m + (self.max_replicas if D > 1 else 0)
+        self.max_groups = min(256, self.m + self.max_replicas)
+        rows = capacity_rows if capacity_rows is not None else D * tokens * top_k + E * _lib.PP_ROW_ALIGN
+        self.rows_cap = int(math.ceil(rows / _lib.PP_ROW_ALIGN) * _lib.PP_ROW_ALIGN)
+        dev = self.device
+        g = torch.Generator(device="cpu").manual_seed(seed)
+
+        # ---- parameters (bf16) in peer-visible arenas -------------------------
+        self.w1_arena = PeerBuffer((self.slots, d_ff, d_model), torch.bfloat16, self.group, dev)
+        self.w2_arena = PeerBuffer((self.slots, d_model, d_ff), torch.bfloat16, self.group, dev)
+        self.g1_arena = PeerBuffer((self.slots, d_ff, d_model), torch.float32, self.group, dev)
+        self.g2_arena = PeerBuffer((self.slots, d_model, d_ff), torch.float32, self.group, dev)
+        w1_all = torch.randn((E, d_ff, d_model), generator=g) / math.sqrt(d_model)
+        w2_all = torch.randn((E, d_model, d_ff), generator=g) / math.sqrt(d_ff)
+        wg = torch.randn((E, d_model), generator=g) / math.sqrt(d_model)
+        lo = self.rank * self.m
+        with torch.no_grad():
+            self.w1_arena.local[: self.m].copy_(w1_all[lo: lo + self.m].to(torch.bfloat16))
+            self.w2_arena.local[: self.m].copy_(w2_all[lo: lo + self.m].to(torch.bfloat16))
+        self.w1 = torch.nn.Parameter(self.w1_arena.local[: self.m], requires_grad=True)
+        self.w2 = torch.nn.Parameter(self.w2_arena.local[: self.m], requires_grad=True)
+        self.wg = torch.nn.Parameter(wg.to(dev, torch.bfloat16))
+        self.w1.main_grad = self.g1_arena.local[: self.m]
+        self.w2.main_grad = self.g2_arena.local[: self.m]
+        self.wg.main_grad = torch.zeros((E, d_model), dtype=torch.float32, device=dev)
+        self.register_buffer("gate_bias", torch.zeros(E, dtype=torch.float32, device=dev))
+
+        # ---- routing / layout workspaces --------------------------------------
+        T, k, C = tokens, top_k, tokens // _lib.PP_CHUNK
+        i32 = dict(dtype=torch.int32, device=dev)
+        self.idx = torch.empty((T, k), **i32)
+        self.rank_in_chunk = torch.empty((T, k), **i32)
+        self.w = torch.empty((T, k), dtype=torch.float32, device=dev)
+        self.probs = torch.empty((T, E), dtype=torch.float32, device=dev)
+        self.chunk_counts = torch.empty((C, E), **i32)
+        self.counts = torch.zeros((E, E), dtype=torch.int64, device=dev)  # virtual-slot LoadMatrix
+        self.chunk_base = torch.empty((C, E), **i32)
+        self.slot_dest = torch.empty((self.m, E), **i32)
+        self.groups = torch.zeros((self.max_groups, 8), **i32)
+        self.num_groups = torch.zeros((1,), **i32)
+        self.total_rows = torch.zeros((1,), **i32)
+        self.seg_start = torch.empty((D, E), **i32)
+        self.rep_slot = torch.full((D, E), -1, **i32)
+        self.pair_dest = torch.empty((T, k), **i32)
+        self.pair_row = torch.empty((T, k), **i32)
+        self.dw = torch.empty((T, k), dtype=torch.float32, device=dev)
+        self.dlogits = torch.empty((T, E), dtype=torch.float32, device=dev)
+        # ---- expert activations ---------------------------------------------
+        R = self.rows_cap
+        self.xp = PeerBuffer((R, d_model), torch.bfloat16, self.group, dev)
+        self.yp = PeerBuffer((R, d_model), torch.bfloat16, self.group, dev)
+        self.dyp = PeerBuffer((R, d_model), torch.bfloat16, self.group, dev)
+        self.dxp = PeerBuffer((R, d_model), torch.bfloat16, self.group, dev)
+        self.pre = torch.zeros((R, d_ff), dtype=torch.bfloat16, device=dev)
+        self.act = torch.zeros((R, d_ff), dtype=torch.bfloat16, device=dev)
+        # ---- planning state -------------------------------------------------
+        self.iteration = 0
+        self.plan_enabled = D > 1
+        self.mask_cur = None  # None = vanilla EP for iteration 0
+        self._plan_out = _device.PlanBuffers(1, E, dev) if self.plan_enabled else None
+        self._plan_next_ready = None
+        self._cm = _device.cost_model(self.cluster, self.model, E) if self.plan_enabled else None
+        self._pcfg = _device.planner_cfg(self.planner_cfg)
+        self.plan_stream = torch.cuda.Stream(device=dev) if self.plan_enabled else None
+        self.comm_stream = torch.cuda.Stream(device=dev) if D > 1 else None
+        self.trans_ctas = trans_ctas
+        self.barrier = _Barrier(self.group, dev)
+        self.history = []  # host copies of LoadMatrix per iteration (optional, record_history)
+        self.record_history = False
+        self.events = {}
+        self.gemm_timing = None
+        if D > 1:
+            torch.cuda.synchronize()
+            dist.barrier(group=self.group)
+
+    # ------------------------------------------------------------------------
+    def set_gate_bias(self, bias) -> None:
+        self.gate_bias.copy_(torch.as_tensor(bias, dtype=torch.float32))
+
+    def _sp(self):
+        return _device.stream_ptr()
+
+    def _route_and_layout(self, x: torch.Tensor) -> None:
+        sp = self._sp()
+        T, d, E, k, m = self.T, self.d, self.E, self.k, self.m
+        _lib.call("pp_route_topk", x.data_ptr(), self.wg.data_ptr(), self.gate_bias.data_ptr(), T, d,
+                  E, k, self.idx.data_ptr(), self.w.data_ptr(), self.probs.data_ptr(),
+                  self.rank_in_chunk.data_ptr(), self.chunk_counts.data_ptr(), sp)
+        _lib.call("pp_slot_histogram", self.chunk_counts.data_ptr(), T, E, m, self.counts.data_ptr(),
+                  self.rank * m, sp)
+        if self.world > 1:
+            mine = self.counts[self.rank * m: (self.rank + 1) * m].clone()
+            dist.all_gather_into_tensor(self.counts, mine, group=self.group)
+        # plan for this iteration (computed during the previous one on the side stream)
+        if self._plan_next_ready is not None:
+            torch.cuda.current_stream().wait_event(self._plan_next_ready)
+            self._plan_mask_cur.record_stream(torch.cuda.current_stream())
+            self.mask_cur = self._plan_mask_cur
+            self._plan_next_ready = None
+        mask_ptr = self.mask_cur.data_ptr() if self.mask_cur is not None else None
+        _lib.call("pp_dispatch_layout", self.counts.data_ptr(), mask_ptr, self.chunk_counts.data_ptr(),
+                  self.world, m, E, T, self.rank, self.max_groups, self.rows_cap,
+                  self.chunk_base.data_ptr(), self.slot_dest.data_ptr(), self.groups.data_ptr(),
+                  self.num_groups.data_ptr(), self.total_rows.data_ptr(), self.seg_start.data_ptr(),
+                  self.rep_slot.data_ptr(), sp)
+        if self.record_history:
+            self.history.append(self.counts.clone())
+
+    def _launch_planner(self) -> None:
+        """plan_for_iteration rule: iteration j+1 searches on iteration j's load
+        when (j+1) % reuse_interval == 0, otherwise it keeps the current plan."""
+        if not self.plan_enabled:
+            return
+        nxt = self.iteration + 1
+        if nxt % self.planner_cfg.reuse_interval != 0:
+            return
+        snapshot = self.counts.clone()  # the next iteration overwrites self.counts
+        ev = torch.cuda.Event()
+        ev.record()
+        with torch.cuda.stream(self.plan_stream):
+            self.plan_stream.wait_event(ev)
+            snapshot.record_stream(self.plan_stream)
+            _device.launch_plan(snapshot.view(1, self.E, self.E), self._plan_out, self._cm, self._pcfg,
+                                self.plan_stream)
+            self._plan_mask_cur = self._plan_out.mask[0].clone()
+            done = torch.cuda.Event()
+            done.record(self.plan_stream)
+        self._plan_next_ready = done
+
+    def _gemm(self, mode, a, b, c, c2=None, stream=None):
+        timing = self.gemm_timing
+        if timing is not None:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+        _device.grouped_gemm(mode, a, b, c, c2, self.groups, self.num_groups, self.max_groups,
+                             self.rows_cap, self.slots, self.d, self.f, stream=stream)
+        if timing is not None:
+            e1.record()
+            timing.append((mode, e0, e1))
+
+    def collect_gemm_timing(self) -> dict:
+        """Average device time per step of each GEMM mode recorded while
+        ``gemm_timing`` was a list (events on the launching stream)."""
+        per, steps = {}, 0
+        for mode, e0, e1 in self.gemm_timing or []:
+            per[mode] = per.get(mode, 0.0) + e0.elapsed_time(e1)
+            steps += mode == _lib.PP_GEMM_FWD1
+        steps = max(steps, 1)
+        names = {0: "FWD1", 1: "FWD2", 2: "DGRAD2", 3: "DGRAD1", 4: "WGRAD2", 5: "WGRAD1"}
+        per_mode = {names.get(m, str(m)): v / steps for m, v in per.items()}
+        return {"ms_per_step": sum(per_mode.values()), "per_mode_ms": per_mode}
+
+    def total_real_rows(self) -> int:
+        n = int(self.num_groups.item())
+        return int(self.groups[:n, 1].sum().item())
+
+    # ------------------------------------------------------------------------
+    def forward_raw(self, x: torch.Tensor) -> torch.Tensor:
+        """Forward without autograd bookkeeping (x: [T, d] bf16 on this device)."""
+        assert x.shape == (self.T, self.d) and x.dtype == torch.bfloat16 and x.is_contiguous()
+        sp = self._sp()
+        self._route_and_layout(x)
+        if self.world > 1 and self.mask_cur is not None:
+            # K5 Trans: replicas pull this iteration's planned experts (side stream, overlaps dispatch)
+            ev = torch.cuda.Event()
+            ev.record()
+            with torch.cuda.stream(self.comm_stream):
+                self.comm_stream.wait_event(ev)
+                _lib.call("pp_replica_trans", self.w1_arena.ptrs.data_ptr(), self.w2_arena.ptrs.data_ptr(),
+                          self.groups.data_ptr(), self.num_groups.data_ptr(), self.max_groups, self.rank,
+                          self.m, self.d, self.f, self.trans_ctas, _device.stream_ptr(self.comm_stream))
+                trans_done = torch.cuda.Event()
+                trans_done.record(self.comm_stream)
+        else:
+            trans_done = None
+        _lib.call("pp_dispatch", x.data_ptr(), self.idx.data_ptr(), self.rank_in_chunk.data_ptr(),
+                  self.chunk_base.data_ptr(), self.slot_dest.data_ptr(), self.T, self.d, self.k, self.m,
+                  self.E, self.xp.ptrs.data_ptr(), self.xp.local.data_ptr(), self.groups.data_ptr(),
+                  self.num_groups.data_ptr(), self.max_groups, self.pair_dest.data_ptr(),
+                  self.pair_row.data_ptr(), sp)
+        if trans_done is not None:
+            torch.cuda.current_stream().wait_event(trans_done)
+        self.barrier()  # every rank's rows have landed (and replicas' params, via the next barrier use)
+        self._gemm(_lib.PP_GEMM_FWD1, self.xp.local, self.w1_arena.local, self.pre, self.act)
+        self._gemm(_lib.PP_GEMM_FWD2, self.act, self.w2_arena.local, self.yp.local)
+        self.barrier()
+        y = torch.empty((self.T, self.d), dtype=torch.bfloat16, device=self.device)
+        _lib.call("pp_combine", self.yp.ptrs.data_ptr(), self.pair_dest.data_ptr(), self.pair_row.data_ptr(),
+                  self.w.data_ptr(), self.T, self.d, self.k, y.data_ptr(), sp)
+        self._launch_planner()
+        return y
+
+    def backward_raw(self, x: torch.Tensor, dy: torch.Tensor) -> torch.Tensor:
+        assert dy.shape == (self.T, self.d) and dy.dtype == torch.bfloat16 and dy.is_contiguous()
+        sp = self._sp()
+        _lib.call("pp_combine_bwd", dy.data_ptr(), self.yp.ptrs.data_ptr(), self.dyp.ptrs.data_ptr(),
+                  self.dyp.local.data_ptr(), self.pair_dest.data_ptr(), self.pair_row.data_ptr(),
+                  self.w.data_ptr(), self.groups.data_ptr(), self.num_groups.data_ptr(), self.max_groups,
+                  self.T, self.d, self.k, self.dw.data_ptr(), sp)
+        self.barrier()
+        self._gemm(_lib.PP_GEMM_DGRAD2, self.dyp.local, self.w2_arena.local, self.pre, self.pre)
+        self._gemm(_lib.PP_GEMM_WGRAD2, self.dyp.local, self.act, self.g2_arena.local)
+        self._gemm(_lib.PP_GEMM_DGRAD1, self.pre, self.w1_arena.local, self.dxp.local)
+        self._gemm(_lib.PP_GEMM_WGRAD1, self.pre, self.xp.local, self.g1_arena.local)
+        self.barrier()
+        if self.world > 1 and self.mask_cur is not None:
+            _lib.call("pp_replica_agg", self.g1_arena.ptrs.data_ptr(), self.g2_arena.ptrs.data_ptr(),
+                      self.rep_slot.data_ptr(), self.world, self.E, self.m, self.rank, self.d, self.f,
+                      self.trans_ctas * 4, sp)
+        dx = torch.empty((self.T, self.d), dtype=torch.bfloat16, device=self.device)
+        _lib.call("pp_dispatch_bwd", self.dxp.ptrs.data_ptr(), self.pair_dest.data_ptr(),
+                  self.pair_row.data_ptr(), self.idx.data_ptr(), self.probs.data_ptr(), self.dw.data_ptr(),
+                  self.wg.data_ptr(), self.T, self.d, self.k, self.E, dx.data_ptr(),
+                  self.dlogits.data_ptr(), sp)
+        self.wg.main_grad.zero_()
+        _lib.call("pp_gate_wgrad", self.dlogits.data_ptr(), x.data_ptr(), self.T, self.d, self.E,
+                  self.wg.main_grad.data_ptr(), sp)
+        self.iteration += 1
+        return dx
+
+    def forward(self, x: torch.Tensor) -> torch.Tensor:
+        return _MoEFunction.apply(x, self)
+
+    # ---- introspection (LoadMatrix / placement of the last call) -------------
+    def last_load_matrix(self) -> LoadMatrix:
+        return LoadMatrix(self.counts.cpu().numpy())
+
+    def current_mask(self) -> np.ndarray:
+        if self.mask_cur is None:
+            return np.eye(self.E, dtype=bool)
+        return self.mask_cur.cpu().numpy().astype(bool)
+
+    def group_table(self) -> list:
+        n = int(self.num_groups.item())
+        t = self.groups[:n].cpu().numpy()
+        return [dict(row_off=int(r[0]), rows=int(r[1]), rows_pad=int(r[2]), wslot=int(r[3]),
+                     expert=int(r[4]), src_rank=int(r[5])) for r in t]
+
+    def close(self) -> None:
+        for b in (self.w1_arena, self.w2_arena, self.g1_arena, self.g2_arena, self.xp, self.yp, self.dyp, self.dxp):
+            b.close()
+
+
+class _MoEFunction(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x, layer):
+        x = x.contiguous()
+        ctx.layer = layer
+        ctx.save_for_backward(x)
+        return layer.forward_raw(x)
+
+    @staticmethod
+    def backward(ctx, dy):
+        (x,) = ctx.saved_tensors
+        dx = ctx.layer.backward_raw(x, dy.contiguous().to(torch.bfloat16))
+        return dx, None

@@ -1,0 +1,114 @@
+"""Grouped tcgen05 GEMM (K4) vs a plain PyTorch fp32 reference, every mode.
+
+Tolerance: bf16 outputs compared with rtol 2e-2 / atol scaled to the output
+magnitude (fp32 accumulation order differs; one bf16 rounding on each side);
+fp32 wgrad outputs with rtol 1e-3 of the max magnitude."""
+
+import math
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+from paper_2411_10003_b200 import _device, _lib  # noqa: E402
+
+
+def gelu(x):
+    k0, k1 = 0.7978845608028654, 0.044715
+    return 0.5 * x * (1.0 + torch.tanh(k0 * (x + k1 * x * x * x)))
+
+
+def dgelu(x):
+    k0, k1 = 0.7978845608028654, 0.044715
+    t = torch.tanh(k0 * (x + k1 * x * x * x))
+    return 0.5 * (1.0 + t) + 0.5 * x * (1.0 - t * t) * k0 * (1.0 + 3.0 * k1 * x * x)
+
+
+def close(got, ref, rtol=2e-2, what=""):
+    if ref.numel() == 0:
+        return
+    got = got.float()
+    ref = ref.float()
+    scale = ref.abs().max().item() + 1e-6
+    err = (got - ref).abs().max().item()
+    assert err <= rtol * scale, f"{what}: max err {err:.4g} vs scale {scale:.4g}"
+
+
+def make_case(rows, d, f, slots=None, seed=0):
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    dev = torch.device("cuda")
+    G = len(rows)
+    slots = slots or G
+    groups, ng, total = _device.groups_tensor(rows, device=dev)
+    cap = max(128, int(math.ceil((total + 256) / 128) * 128))
+    X = torch.zeros((cap, d), dtype=torch.bfloat16, device=dev)
+    segs = []
+    off = 0
+    for r in rows:
+        pad = (r + 127) // 128 * 128
+        X[off: off + r] = (torch.randn((r, d), generator=g) * 0.5).to(dev, torch.bfloat16)
+        segs.append((off, r))
+        off += pad
+    W1 = (torch.randn((slots, f, d), generator=g) / math.sqrt(d)).to(dev, torch.bfloat16)
+    W2 = (torch.randn((slots, d, f), generator=g) / math.sqrt(f)).to(dev, torch.bfloat16)
+    return dict(groups=groups, ng=ng, cap=cap, X=X, segs=segs, W1=W1, W2=W2, G=G, slots=slots)
+
+
+@pytest.mark.parametrize("rows,d,f", [([300, 0, 128, 77, 1], 256, 512), ([2048, 1000], 512, 1024), ([130] * 6, 1024, 768)])
+def test_fwd_bwd_modes(rows, d, f):
+    c = make_case(rows, d, f)
+    dev = torch.device("cuda")
+    cap, G, S = c["cap"], c["G"], c["slots"]
+    pre = torch.zeros((cap, f), dtype=torch.bfloat16, device=dev)
+    act = torch.zeros((cap, f), dtype=torch.bfloat16, device=dev)
+    yp = torch.zeros((cap, d), dtype=torch.bfloat16, device=dev)
+    run = lambda mode, a, b, out, out2=None: _device.grouped_gemm(  # noqa: E731
+        mode, a, b, out, out2, c["groups"], c["ng"], G, cap, S, d, f)
+    run(_lib.PP_GEMM_FWD1, c["X"], c["W1"], pre, act)
+    run(_lib.PP_GEMM_FWD2, act, c["W2"], yp)
+    g = torch.Generator(device="cpu").manual_seed(5)
+    dyp = torch.zeros((cap, d), dtype=torch.bfloat16, device=dev)
+    for off, r in c["segs"]:
+        dyp[off: off + r] = torch.randn((r, d), generator=g).to(dev, torch.bfloat16)
+    pre_saved = pre.clone()
+    dpre = pre  # in place, like the layer
+    run(_lib.PP_GEMM_DGRAD2, dyp, c["W2"], dpre, dpre)
+    dw2 = torch.zeros((S, d, f), dtype=torch.float32, device=dev)
+    run(_lib.PP_GEMM_WGRAD2, dyp, act, dw2)
+    dxp = torch.zeros((cap, d), dtype=torch.bfloat16, device=dev)
+    run(_lib.PP_GEMM_DGRAD1, dpre, c["W1"], dxp)
+    dw1 = torch.zeros((S, f, d), dtype=torch.float32, device=dev)
+    run(_lib.PP_GEMM_WGRAD1, dpre, c["X"], dw1)
+    torch.cuda.synchronize()
+
+    for gi, (off, r) in enumerate(c["segs"]):
+        s = slice(off, off + r)
+        X = c["X"][s].float()
+        W1, W2 = c["W1"][gi].float(), c["W2"][gi].float()
+        ref_pre = X @ W1.t()
+        close(pre_saved[s], ref_pre, what=f"pre g{gi}")
+        ref_act = gelu(pre_saved[s].float())
+        close(act[s], ref_act, what=f"act g{gi}")
+        close(yp[s], act[s].float() @ W2.t(), what=f"yp g{gi}")
+        ref_dpre = (dyp[s].float() @ W2) * dgelu(pre_saved[s].float())
+        close(dpre[s], ref_dpre, what=f"dpre g{gi}")
+        close(dxp[s], dpre[s].float() @ W1, what=f"dxp g{gi}")
+        close(dw2[gi], dyp[s].float().t() @ act[s].float(), rtol=2e-3, what=f"dw2 g{gi}")
+        close(dw1[gi], dpre[s].float().t() @ X, rtol=2e-3, what=f"dw1 g{gi}")
+        # padding rows stay zero through the forward
+        pad = slice(off + r, off + (r + 127) // 128 * 128)
+        assert act[pad].float().abs().max().item() == 0 if pad.stop > pad.start else True
+
+
+def test_plain_mode_large():
+    d, f = 1024, 4096
+    rows = [4096, 3000, 1]
+    c = make_case(rows, d, f, seed=3)
+    cap, G = c["cap"], c["G"]
+    out = torch.zeros((cap, f), dtype=torch.bfloat16, device="cuda")
+    _device.grouped_gemm(_lib.PP_GEMM_PLAIN, c["X"], c["W1"], out, None, c["groups"], c["ng"], G, cap, G, d, f)
+    torch.cuda.synchronize()
+    for gi, (off, r) in enumerate(c["segs"]):
+        s = slice(off, off + r)
+        close(out[s], c["X"][s].float() @ c["W1"][gi].float().t(), what=f"plain g{gi}")

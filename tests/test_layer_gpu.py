@@ -1,0 +1,112 @@
+"""K1 routing and the whole 1-GPU MoE layer (K1+K3+K4) against the CPU oracle.
+
+Bit-exact: top-k indices, per-chunk ranks/counts, the virtual-slot LoadMatrix,
+every (token, k) destination row, and the permuted rows themselves (exact
+arithmetic inputs).  Within tolerance: gate weights (1e-5 rel,
+expf vs libm), layer output and all gradients (bf16 storage: 2e-2 of the
+tensor's max magnitude; fp32 weight grads 1e-2)."""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+import paper_2411_10003_b200 as pp  # noqa: E402
+from paper_2411_10003_b200 import _lib  # noqa: E402
+from oracle import moe_ref as M  # noqa: E402
+from oracle import planner_ref as P  # noqa: E402
+
+
+def close(got, ref, rtol=2e-2, what=""):
+    got, ref = got.float().cpu(), ref.float().cpu()
+    scale = ref.abs().max().item() + 1e-6
+    err = (got - ref).abs().max().item()
+    assert err <= rtol * scale, f"{what}: max err {err:.4g} vs scale {scale:.4g}"
+
+
+@pytest.mark.parametrize("T,d,E,k", [(1024, 256, 16, 2), (2048, 512, 8, 1), (512, 1024, 64, 2), (256, 128, 32, 4), (1024, 256, 100, 2)])
+def test_route_exact(T, d, E, k):
+    x, wg = M.exact_inputs(T, d, E, seed=T + E)
+    bias = (torch.randint(-3, 4, (E,)).float() * 0.5)
+    dev = torch.device("cuda")
+    xd, wd, bd = x.to(dev), wg.to(dev), bias.to(dev)
+    idx = torch.empty((T, k), dtype=torch.int32, device=dev)
+    rank = torch.empty_like(idx)
+    w = torch.empty((T, k), dtype=torch.float32, device=dev)
+    probs = torch.empty((T, E), dtype=torch.float32, device=dev)
+    cc = torch.empty((T // 128, E), dtype=torch.int32, device=dev)
+    _lib.call("pp_route_topk", xd.data_ptr(), wd.data_ptr(), bd.data_ptr(), T, d, E, k, idx.data_ptr(),
+              w.data_ptr(), probs.data_ptr(), rank.data_ptr(), cc.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    logits, ridx, rw, rprobs = M.route(x, wg, bias, k)
+    assert torch.equal(idx.cpu().long(), ridx), "top-k indices differ"
+    rrank, rcc = M.chunk_ranks(ridx.numpy(), E)
+    assert np.array_equal(rank.cpu().numpy(), rrank)
+    assert np.array_equal(cc.cpu().numpy(), rcc)
+    torch.testing.assert_close(w.cpu(), rw, rtol=1e-5, atol=1e-7)
+    torch.testing.assert_close(probs.cpu(), rprobs, rtol=1e-5, atol=1e-7)
+
+
+def run_layer(T, d, f, E, k, bias=None, seed=0):
+    layer = pp.MoELayer(d, f, E, k, tokens=T, seed=seed)
+    x, wg = M.exact_inputs(T, d, E, seed=seed + 11)
+    with torch.no_grad():
+        layer.wg.copy_(wg.to(layer.device))
+    if bias is not None:
+        layer.set_gate_bias(bias)
+    g = torch.Generator().manual_seed(seed + 3)
+    dy = (torch.randn((T, d), generator=g) * 0.1).to(torch.bfloat16)
+    xd = x.to(layer.device).requires_grad_(True)
+    y = layer(xd)
+    y.backward(dy.to(layer.device))
+    torch.cuda.synchronize()
+    return layer, x, wg, dy, y, xd.grad
+
+
+@pytest.mark.parametrize("T,d,f,E,k", [(2048, 256, 512, 16, 2), (1024, 256, 256, 8, 1), (4096, 512, 768, 32, 2)])
+def test_layer_vs_oracle(T, d, f, E, k):
+    bias = torch.log(torch.tensor([1.0 / (i + 1) ** 1.2 for i in range(E)]))  # Zipf skew
+    bias = torch.round(bias * 4) / 4  # keep logits exact
+    layer, x, wg, dy, y, dx = run_layer(T, d, f, E, k, bias=bias, seed=E)
+    w1 = layer.w1.detach().cpu()
+    w2 = layer.w2.detach().cpu()
+    ref = M.LayerRef(w1, w2, wg, bias, k, D=1)
+    ys, st = ref.forward([x])
+    # integer contract
+    assert np.array_equal(layer.idx.cpu().numpy(), st["routes"][0][1].numpy())
+    assert np.array_equal(layer.counts.cpu().numpy(), st["hist"])
+    dest, row = st["pos"][0]
+    assert np.array_equal(layer.pair_row.cpu().numpy(), row)
+    assert np.array_equal(layer.pair_dest.cpu().numpy(), dest)
+    groups = layer.group_table()
+    assert [(g["expert"], g["row_off"], g["rows"], g["rows_pad"]) for g in groups] == \
+        [(g["expert"], g["row_off"], g["rows"], g["rows_pad"]) for g in st["lay"]["groups"][0]]
+    # permuted rows are exact copies
+    xp = layer.xp.local.cpu()
+    for gr in groups:
+        s = slice(gr["row_off"], gr["row_off"] + gr["rows"])
+        assert torch.equal(xp[s], st["xp"][0][s].to(torch.bfloat16))
+    # H/R implied by the layout == reference derive_loads (vanilla EP, 1 rank)
+    H, R = P.derive_loads(st["hist"], np.eye(E, dtype=bool))
+    assert sum(g["rows"] for g in groups) == int(H.sum())
+    # floating point
+    close(y, ys[0], what="y")
+    dxs, dw1, dw2, dwg, dws = ref.backward([dy], st)
+    close(layer.dw, dws[0], what="dw")
+    close(dx, dxs[0], what="dx")
+    close(layer.w1.main_grad, dw1, rtol=1e-2, what="dW1")
+    close(layer.w2.main_grad, dw2, rtol=1e-2, what="dW2")
+    close(layer.wg.main_grad, dwg, rtol=1e-2, what="dWg")
+
+
+def test_layer_repeatable_and_iteration_counter():
+    layer, x, wg, dy, y1, dx1 = run_layer(2048, 256, 512, 16, 2, seed=1)
+    y2 = layer(x.to(layer.device))
+    torch.cuda.synchronize()
+    assert torch.equal(y1, y2)
+    assert layer.iteration == 1
+    lm = layer.last_load_matrix()
+    assert lm.total() == 2048 * 2

@@ -1,0 +1,121 @@
+"""Device planner K2 (pp_plan_greedy) bit-exact against the pinned oracle and the
+reference goldens: selected order, excluded sets, H/R, fp64 objective bits."""
+
+import json
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+import paper_2411_10003_b200 as pp  # noqa: E402
+from oracle import planner_ref as P  # noqa: E402
+
+G = Path(__file__).resolve().parent / "golden"
+
+
+def specs(cm, E):
+    cl = pp.ClusterSpec(E, cm["avg_bandwidth"], cm["compute_throughput"])
+    mo = pp.ModelSpec(E, 1, cm["top_k"], cm["input_bytes"], cm["param_bytes"], cm["grad_bytes"],
+                      fnec_time=cm["fnec"], bnec_time=cm["bnec"])
+    return cl, mo
+
+
+def assert_same(res, c):
+    pl = res.placement
+    assert list(pl.selected) == c["selected"]
+    assert [sorted(x) for x in pl.excluded] == c["excluded"]
+    assert res.H.tolist() == c["H"] and res.R.tolist() == c["R"]
+    assert float(res.best_cost).hex() == c["best_hex"]
+
+
+def test_golden_planner_cases():
+    cases = json.loads((G / "planner_cases.json").read_text())
+    counts = np.load(G / "planner_counts.npz")
+    for c in cases:
+        k = counts[f"arr_{c['counts_index']}"]
+        E = k.shape[0]
+        cl, mo = specs(c["cm"], E)
+        cfg = pp.PlannerConfig(n=c["n"], alpha=c["alpha"], overlap_aware=c["overlap"])
+        res = pp.greedy_search_many([k], cfg, cl, mo)[0]
+        assert_same(res, c)
+
+
+def test_golden_generator_traces():
+    meta = json.loads((G / "trace_cases.json").read_text())
+    traces = np.load(G / "trace_cases.npz")
+    for c in meta:
+        k = traces[c["key"]]
+        cl, mo = specs(c["cm"], k.shape[0])
+        cfg = pp.PlannerConfig(n=c["n"], alpha=c["alpha"], overlap_aware=c["overlap"])
+        assert_same(pp.greedy_search_many([k], cfg, cl, mo)[0], c)
+
+
+@pytest.mark.parametrize("E", [2, 3, 5, 8, 16, 32, 64, 128])
+def test_fuzz_vs_oracle(E):
+    """>= 10 000 instances over all E values (batched, one CTA per instance)."""
+    rng = np.random.default_rng(1000 + E)
+    batches = 8 if E <= 64 else 2
+    per = 200 if E <= 64 else 50
+    for b in range(batches):
+        k = int(rng.integers(1, 3))
+        cm = P.cost_model_dict(E, k, float(rng.integers(1, 1 << 14)), float(10 ** rng.uniform(3, 8)),
+                               float(10 ** rng.uniform(3, 8)), float(10 ** rng.uniform(8, 11)),
+                               float(10 ** rng.uniform(3, 6)), float(rng.uniform(0, 1e-3)),
+                               float(rng.uniform(0, 2e-3)))
+        n = int(rng.integers(0, E))
+        alpha = float(rng.choice([0.05, 0.3, 0.5, 1.5]))
+        ov = bool(b % 2)
+        row_total = int(rng.integers(1, 400)) * k
+        mats = []
+        for _ in range(per):
+            probs = rng.dirichlet(np.ones(E) * rng.choice([0.1, 0.5, 2.0]))
+            mats.append(np.stack([rng.multinomial(row_total, probs) for _ in range(E)]))
+        cl = pp.ClusterSpec(E, cm["avg_bandwidth"], cm["compute_throughput"])
+        mo = pp.ModelSpec(E, 1, k, cm["input_bytes"], cm["expert_param_bytes"], cm["expert_grad_bytes"],
+                          fnec_time=cm["fnec_time"], bnec_time=cm["bnec_time"])
+        res = pp.greedy_search_many(mats, pp.PlannerConfig(n=n, alpha=alpha, overlap_aware=ov), cl, mo)
+        for mat, r in zip(mats, res):
+            o = P.greedy_search(mat, n, alpha, ov, cm)
+            assert r.placement.selected == o["selected"]
+            assert r.placement.excluded == tuple(frozenset(x) for x in o["excluded"])
+            assert r.explored == o["explored"]
+            assert float(r.best_cost).hex() == float(o["best"]).hex()
+            assert r.H.tolist() == o["H"].tolist() and r.R.tolist() == o["R"].tolist()
+
+
+def test_derive_loads_golden():
+    for c in json.loads((G / "derive_cases.json").read_text()):
+        counts = np.array(c["counts"])
+        D, E = counts.shape
+        pl = pp.ExpertPlacement(D, E, tuple(c["selected"]), tuple(frozenset(x) for x in c["excluded"]))
+        dl = pp.derive_loads(pp.LoadMatrix(counts), pl)
+        assert dl.H.tolist() == c["H"] and dl.R.tolist() == c["R"]
+
+
+def test_reference_api_errors():
+    cl = pp.ClusterSpec(3, 1e9, 1e3)
+    mo = pp.ModelSpec(3, 1, 1, 1e6, 1e5, 1e5)
+    with pytest.raises(pp.ValidationError):
+        pp.greedy_search(pp.LoadMatrix([[1, 2], [2, 1], [0, 3]]), pp.PlannerConfig(), cl, mo)
+    with pytest.raises(pp.DimensionMismatchError):
+        pp.greedy_search(pp.LoadMatrix([[1, 2], [2, 1]]), pp.PlannerConfig(), cl, mo)
+    with pytest.raises(pp.ValidationError):
+        pp.greedy_search(pp.LoadMatrix([[3, 0, 0], [2, 1, 0], [0, 1, 2]]), pp.PlannerConfig(n=3), cl, mo)
+
+
+def test_plan_for_iteration_reuse():
+    cl = pp.ClusterSpec(3, 1e9, 1000.0)
+    mo = pp.ModelSpec(3, 1, 1, 1e6, 1e5, 1e5)
+    fig8 = pp.LoadMatrix([[3, 0, 0], [2, 1, 0], [0, 1, 2]])
+    flat = pp.LoadMatrix([[1, 1, 1]] * 3)
+    hist = [fig8, flat, fig8, flat]
+    cfg = pp.PlannerConfig(n=1, alpha=0.5, reuse_interval=2)
+    assert pp.plan_for_iteration(hist, 0, cfg, cl, mo).selected == ()
+    assert pp.plan_for_iteration(hist, 1, cfg, cl, mo).selected == ()
+    assert pp.plan_for_iteration(hist, 2, cfg, cl, mo) == pp.greedy_search(flat, cfg, cl, mo)
+    assert pp.plan_for_iteration(hist, 3, cfg, cl, mo) == pp.greedy_search(flat, cfg, cl, mo)
+    assert pp.plan_for_iteration(hist, 4, cfg, cl, mo) == pp.greedy_search(flat, cfg, cl, mo)
+    with pytest.raises(pp.ValidationError):
+        pp.plan_for_iteration(hist, 6, cfg, cl, mo)
