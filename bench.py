@@ -55,17 +55,18 @@ class ClockSampler:
               "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
               "clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, index: int) -> None:
-        self.index = index
+    def __init__(self, index) -> None:
+        self.index = index  # nvidia-smi id: UUID of the torch device (robust to CUDA_VISIBLE_DEVICES)
         self.proc = None
         self.lines = []
 
     def __enter__(self):
         try:
+            sel = ["-i", str(self.index)] if self.index is not None else []
             self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + ",".join(self.FIELDS),
+                ["nvidia-smi", *sel, "--query-gpu=" + ",".join(self.FIELDS),
                  "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
         except OSError:
@@ -99,8 +100,11 @@ class ClockSampler:
             for n, v in zip(names, parts[2:]):
                 if v.lower().startswith("active"):
                     reasons.add(n)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        out = {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+               "reasons": sorted(reasons), "samples": len(sm)}
+        if not sm and self.lines:
+            out["error"] = self.lines[0][:200]
+        return out
 
 
 def load_peaks() -> dict:
@@ -259,7 +263,11 @@ def main() -> None:
     _lib.reset_launch_count()
     xs = [x.detach().clone() for _ in range(2)]
     torch.cuda.synchronize()
-    with ClockSampler(local_rank) as clk:
+    try:
+        smi_id = "GPU-" + str(torch.cuda.get_device_properties(dev).uuid)
+    except Exception:
+        smi_id = None
+    with ClockSampler(smi_id) as clk:
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
@@ -298,30 +306,57 @@ def main() -> None:
     # ---- e2e through the public API with host buffers
     e2e = None
     if not args.profile_only:
-        xh = x.detach().cpu().pin_memory()
-        dyh = dy.detach().cpu().pin_memory()
-        yh = torch.empty((T, d), dtype=torch.bfloat16).pin_memory()
-        xdev = torch.empty_like(x)
-        dydev = torch.empty_like(dy)
+        # pinned host buffers; H2D of step i+1 and D2H of step i-1 overlap step i
+        xh = [x.detach().cpu().pin_memory() for _ in range(2)]
+        dyh = [dy.detach().cpu().pin_memory() for _ in range(2)]
+        yh = [torch.empty((T, d), dtype=torch.bfloat16).pin_memory() for _ in range(2)]
+        xdev = [torch.empty_like(x) for _ in range(2)]
+        dydev = [torch.empty_like(dy) for _ in range(2)]
+        copy = torch.cuda.Stream(device=dev)
+        main = torch.cuda.current_stream()
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(args.steps):
-            xdev.copy_(xh, non_blocking=True)
-            dydev.copy_(dyh, non_blocking=True)
-            y = step(xdev.detach(), dydev)
-            yh.copy_(y.detach(), non_blocking=True)
-        e1.record()
+        ev_in = [torch.cuda.Event() for _ in range(2)]
+        ev_free = [torch.cuda.Event() for _ in range(2)]
+        ev_out = [torch.cuda.Event() for _ in range(2)]
+        e0.record(main)
+
+        def h2d(i):
+            b = i % 2
+            with torch.cuda.stream(copy):
+                copy.wait_event(ev_free[b]) if i >= 2 else copy.wait_event(e0)
+                xdev[b].copy_(xh[b], non_blocking=True)
+                dydev[b].copy_(dyh[b], non_blocking=True)
+                ev_in[b].record(copy)
+
+        h2d(0)
+        keep = [None, None]
+        for i in range(args.steps):
+            b = i % 2
+            if i + 1 < args.steps:
+                h2d(i + 1)
+            main.wait_event(ev_in[b])
+            y = step(xdev[b].detach(), dydev[b])
+            ev_free[b].record(main)
+            keep[b] = y
+            with torch.cuda.stream(copy):
+                copy.wait_event(ev_free[b])
+                yh[b].copy_(y.detach(), non_blocking=True)
+                ev_out[b].record(copy)
+        for b in range(2):
+            main.wait_event(ev_out[b])
+        e1.record(main)
         torch.cuda.synchronize()
         em = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(em, op=dist.ReduceOp.MAX)
         e2e = {"value": world * T * args.steps / (float(em.item()) / 1e3), "unit": "tokens/s",
                "h2d_bytes_per_step": 2 * T * d * 2, "d2h_bytes_per_step": T * d * 2,
-               "path": "MoELayer.__call__ + backward (public API), pinned host x/dy in, y out"}
+               "path": "MoELayer.__call__ + backward (public API); pinned host x/dy in, y out; "
+                       "copies on a side stream, double-buffered (H2D of step i+1, D2H of step i overlap compute)"}
 
     # ---- planner + imbalance (device planner vs oracle CPU planner)
     planner_info, imbalance = None, None

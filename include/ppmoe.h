@@ -154,17 +154,20 @@ int pp_combine_bwd(const void* dy, void* const* out_ptrs, void* const* dgrad_ptr
                    const pp_group* groups, const int32_t* num_groups, int32_t max_groups,
                    int32_t T, int32_t d, int32_t k, float* dw, void* stream);
 
-/* Backward of dispatch + gate:  dlogits = softmax'(probs) . dw (top-k scatter),
- * dx[t] = sum_j dXp[pair] + sum_e dlogits[t][e] * wg[e];  writes dx bf16 and
- * dlogits [T][E] fp32. */
+/* Backward of dispatch + gate softmax:  dx[t] = sum_j dXp[pair] (pulled from
+ * dxp_ptrs[pair_dest]) and dl [T][EP] bf16 = dL/dlogits restricted to the top-k
+ * (dl_i = p_i * (dw_{j(i)} [i selected] - sum_j dw_j p_{e_j})), zero-padded to
+ * EP in {64, 128} columns for the tensor-core gate GEMMs. */
 int pp_dispatch_bwd(void* const* dxp_ptrs, const int32_t* pair_dest, const int32_t* pair_row,
-                    const int32_t* idx, const float* probs, const float* dw, const void* wg,
-                    int32_t T, int32_t d, int32_t k, int32_t E, void* dx, float* dlogits,
+                    const int32_t* idx, const float* probs, const float* dw,
+                    int32_t T, int32_t d, int32_t k, int32_t E, int32_t EP, void* dx, void* dl,
                     void* stream);
 
-/* dwg [E][d] fp32 (+)= dlogits^T . x  (accumulates; caller zeroes). */
-int pp_gate_wgrad(const float* dlogits, const void* x, int32_t T, int32_t d, int32_t E,
-                  float* dwg, void* stream);
+/* Gate GEMMs on tcgen05:  dx [T][d] bf16 += dl [T][EP] . wg [E][d]   and
+ * dwg [E][d] fp32 += dl^T . x (split-K over token chunks, fp32 atomics;
+ * caller zeroes dwg). */
+int pp_gate_bwd(const void* dl, const void* wg, const void* x, int32_t T, int32_t d, int32_t E,
+                int32_t EP, void* dx, float* dwg, void* stream);
 
 /* ---- grouped expert GEMM on tcgen05 (K4) -------------------------------- */
 #define PP_GEMM_FWD1 0   /* pre,act[rows][f] = GeLU-split( Xp[rows][d] . W1[slot][f][d]^T ) */

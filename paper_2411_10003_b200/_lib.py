@@ -69,8 +69,8 @@ SIGNATURES = {
     "pp_dispatch": [P, P, P, P, P, I, I, I, I, I, P, P, P, P, I, P, P, P],
     "pp_combine": [P, P, P, P, I, I, I, P, P],
     "pp_combine_bwd": [P, P, P, P, P, P, P, P, P, I, I, I, I, P, P],
-    "pp_dispatch_bwd": [P, P, P, P, P, P, P, I, I, I, I, P, P, P],
-    "pp_gate_wgrad": [P, P, I, I, I, P, P],
+    "pp_dispatch_bwd": [P, P, P, P, P, P, I, I, I, I, I, P, P, P],
+    "pp_gate_bwd": [P, P, P, I, I, I, I, P, P, P],
     "pp_grouped_gemm": [I, P, P, P, P, P, P, I, I, I, I, I, I, P],
     "pp_replica_trans": [P, P, P, P, I, I, I, I, I, I, P],
     "pp_replica_agg": [P, P, P, I, I, I, I, I, I, I, P],
@@ -128,7 +128,7 @@ def check(rc: int, what: str = "") -> None:
 KERNELS_PER_CALL = {
     "pp_plan_greedy": 1, "pp_derive_loads": 1, "pp_route_topk": 1, "pp_slot_histogram": 1,
     "pp_dispatch_layout": 1, "pp_dispatch": 2, "pp_combine": 1, "pp_combine_bwd": 2,
-    "pp_dispatch_bwd": 1, "pp_gate_wgrad": 1, "pp_grouped_gemm": 1, "pp_replica_trans": 1,
+    "pp_dispatch_bwd": 1, "pp_gate_bwd": 2, "pp_grouped_gemm": 1, "pp_replica_trans": 1,
     "pp_replica_agg": 1, "pp_peer_barrier": 1,
 }
 _launches = [0]

@@ -33,10 +33,19 @@ namespace pp {
 
 constexpr int BM = 128;
 constexpr int BK = 64;  // 64 bf16 = 128 B = one SWIZZLE_128B span
-constexpr int kThreads = 256;
+constexpr int kThreads = 384;  // 4 non-epilogue warps + up to 8 epilogue warps
 constexpr int kMaxGroups = 256;
 
-enum Epi { EPI_BF16 = 0, EPI_GELU = 1, EPI_DGELU = 2, EPI_F32 = 3, EPI_ROUTE = 4 };
+
+enum Epi { EPI_BF16 = 0, EPI_GELU = 1, EPI_DGELU = 2, EPI_F32 = 3, EPI_ROUTE = 4, EPI_BF16_ADD = 5, EPI_F32_ATOMIC = 6 };
+
+// per-epilogue-warp staging for the TMA-store epilogue: one 32x32 block
+// (bf16: 2 KB, SWIZZLE_64B; fp32: 4 KB, SWIZZLE_128B); DGELU adds a second
+// 2 KB block that receives the TMA-loaded pre-activation
+template <int EPI>
+constexpr int stage_bytes_per_warp() {
+  return EPI == EPI_F32 ? 4096 : EPI == EPI_DGELU ? 4096 : 2048;
+}
 
 struct GemmParams {
   const pp_group* groups;
@@ -57,7 +66,9 @@ struct GemmParams {
   int32_t* chunk_counts;
   int topk;
   int e_real;       // route: real expert count (<= BN; padded experts read as zero rows)
-  int single_rows;  // > 0: one implicit group {row_off 0, rows_pad single_rows, slot 0}
+  int single_rows;  // > 0: implicit groups over rows [0, single_rows), slot 0
+  int split_rows;   // with single_rows: split-K chunk size (one implicit group per chunk)
+  int m_real;       // EPI_F32_ATOMIC: rows of the output that exist (< M_fixed)
 };
 
 struct SchedSmem {
@@ -128,15 +139,164 @@ __device__ __forceinline__ bool decode_tile(int t, const SchedSmem& s, const Gem
   return true;
 }
 
+template <int EPI>
+constexpr bool tma_out() {
+  return EPI == EPI_BF16 || EPI == EPI_GELU || EPI == EPI_DGELU || EPI == EPI_F32;
+}
+
+// Stage a 32x32 bf16 block (row = lane, 16-byte chunk j) with the SWIZZLE_64B
+// pattern the output tensor map uses, then one lane TMA-stores it.  The
+// staging buffer is reused only after the previous store finished reading it.
+__device__ __forceinline__ void stage_and_store(uint8_t* stage, const uint4 (&v)[4], const void* tmap,
+                                                int col, int row, int lane) {
+  if (lane == 0) bulk_wait_read0();
+  __syncwarp();
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+    *reinterpret_cast<uint4*>(stage + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4)) = v[j];
+  fence_async_shared();
+  __syncwarp();
+  if (lane == 0) {
+    tma_store_2d(tmap, stage, col, row);
+    bulk_commit();
+  }
+}
+
+// fp32 variant: 32 rows x 128 B, SWIZZLE_128B (16-byte chunk j of row l at j ^ (l & 7))
+__device__ __forceinline__ void stage_and_store_f32(uint8_t* stage, const uint32_t (&raw)[32],
+                                                    const void* tmap, int col, int row, int lane) {
+  if (lane == 0) bulk_wait_read0();
+  __syncwarp();
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    *reinterpret_cast<uint4*>(stage + lane * 128 + ((j ^ (lane & 7)) << 4)) =
+        make_uint4(raw[4 * j], raw[4 * j + 1], raw[4 * j + 2], raw[4 * j + 3]);
+  fence_async_shared();
+  __syncwarp();
+  if (lane == 0) {
+    tma_store_2d(tmap, stage, col, row);
+    bulk_commit();
+  }
+}
+
+// Epilogue of one 32-column chunk of one accumulator row (thread = row r).
+template <int EPI>
+__device__ __forceinline__ void epilogue_chunk(const uint32_t (&raw)[32], const GemmParams& p,
+                                               const Tile& tl, int r, int c, const uint4 (&pre_v)[4],
+                                               uint8_t* stage, const CUtensorMap* tmC,
+                                               const CUtensorMap* tmC2, int lane) {
+  if constexpr (EPI == EPI_F32) {
+    stage_and_store_f32(stage, raw, tmC, tl.n0 + c, tl.wslot * p.M_fixed + tl.m0 + (r & ~31), lane);
+  } else if constexpr (tma_out<EPI>()) {
+    const int col = tl.n0 + c;
+    const int row = tl.row_off + tl.m0 + (r & ~31);
+    uint4 v[4];
+    if constexpr (EPI == EPI_BF16) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float f[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) f[u] = __uint_as_float(raw[8 * j + u]);
+        v[j] = f32x8_to_bf16(f);
+      }
+      stage_and_store(stage, v, tmC, col, row, lane);
+    } else if constexpr (EPI == EPI_GELU) {
+      uint4 g4[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float f[8], g[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) f[u] = __uint_as_float(raw[8 * j + u]);
+        v[j] = f32x8_to_bf16(f);
+        bf16x8_to_f32(v[j], f);  // GeLU of the bf16-rounded pre-activation, as the backward sees it
+#pragma unroll
+        for (int u = 0; u < 8; ++u) g[u] = gelu_f(f[u]);
+        g4[j] = f32x8_to_bf16(g);
+      }
+      stage_and_store(stage, v, tmC, col, row, lane);
+      stage_and_store(stage, g4, tmC2, col, row, lane);
+    } else {  // EPI_DGELU
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float x[8], f[8];
+        bf16x8_to_f32(pre_v[j], x);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) f[u] = __uint_as_float(raw[8 * j + u]) * dgelu_f(x[u]);
+        v[j] = f32x8_to_bf16(f);
+      }
+      stage_and_store(stage + 2048, v, tmC, col, row, lane);
+    }
+  } else if constexpr (EPI == EPI_F32_ATOMIC) {  // split-K partial: out[m][n] += acc
+    if (tl.m0 + r < p.m_real) {
+      float* out = reinterpret_cast<float*>(p.c) + (size_t)(tl.m0 + r) * p.N + tl.n0 + c;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) atomicAdd(out + j, __uint_as_float(raw[j]));
+    }
+  } else {
+    const size_t off = ((size_t)tl.row_off + tl.m0 + r) * p.N + tl.n0 + c;
+    if constexpr (EPI == EPI_BF16) {
+      __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.c) + off;
+#pragma unroll
+      for (int j = 0; j < 32; j += 8) {
+        float f[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) f[u] = __uint_as_float(raw[j + u]);
+        st_v4(out + j, f32x8_to_bf16(f));
+      }
+    } else if constexpr (EPI == EPI_GELU) {
+      __nv_bfloat16* pre = reinterpret_cast<__nv_bfloat16*>(p.c) + off;
+      __nv_bfloat16* act = reinterpret_cast<__nv_bfloat16*>(p.c2) + off;
+#pragma unroll
+      for (int j = 0; j < 32; j += 8) {
+        float f[8], g[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) f[u] = __uint_as_float(raw[j + u]);
+        const uint4 pv = f32x8_to_bf16(f);
+        bf16x8_to_f32(pv, f);  // GeLU of the bf16-rounded pre-activation, as the backward sees it
+#pragma unroll
+        for (int u = 0; u < 8; ++u) g[u] = gelu_f(f[u]);
+        st_v4(pre + j, pv);
+        st_v4(act + j, f32x8_to_bf16(g));
+      }
+    } else if constexpr (EPI == EPI_BF16_ADD) {  // out += acc (pre_v holds the old out)
+      __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.c) + off;
+#pragma unroll
+      for (int j = 0; j < 32; j += 8) {
+        float x[8], f[8];
+        bf16x8_to_f32(pre_v[j / 8], x);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) f[u] = __uint_as_float(raw[j + u]) + x[u];
+        st_v4(out + j, f32x8_to_bf16(f));
+      }
+    } else if constexpr (EPI == EPI_DGELU) {
+      __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.c) + off;
+#pragma unroll
+      for (int j = 0; j < 32; j += 8) {
+        float x[8], f[8];
+        bf16x8_to_f32(pre_v[j / 8], x);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) f[u] = __uint_as_float(raw[j + u]) * dgelu_f(x[u]);
+        st_v4(out + j, f32x8_to_bf16(f));
+      }
+    }
+  }
+}
+
 template <int BN, bool A_MN, bool B_MN, int EPI, int STAGES>
 __global__ void __launch_bounds__(kThreads, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
-                        const __grid_constant__ CUtensorMap tmB, const GemmParams p) {
+                        const __grid_constant__ CUtensorMap tmB,
+                        const __grid_constant__ CUtensorMap tmC,
+                        const __grid_constant__ CUtensorMap tmC2, const GemmParams p) {
   constexpr uint32_t A_BYTES = BM * BK * 2;
   constexpr uint32_t B_BYTES = BN * BK * 2;
   constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
   constexpr uint32_t TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
   constexpr uint32_t IDESC = make_idesc<BN, A_MN, B_MN>();
+  // epilogue warps: two per TMEM lane quarter (each takes half of the columns),
+  // except the route epilogue which needs a whole logits row per thread
+  constexpr int EPI_WARPS = (EPI == EPI_ROUTE) ? 4 : (BN >= 128 ? 8 : 4);
+  constexpr int EPI_COLS = BN * 4 / EPI_WARPS;
 
   extern __shared__ __align__(1024) uint8_t dsmem[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsmem) + 1023) & ~uintptr_t(1023));
@@ -145,6 +305,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ __align__(8) uint64_t empty_bar[STAGES];
   __shared__ __align__(8) uint64_t tfull_bar[2];
   __shared__ __align__(8) uint64_t tempty_bar[2];
+  __shared__ __align__(8) uint64_t pre_bar[8];  // DGELU: per-epilogue-warp pre-activation loads
   __shared__ uint32_t tmem_base_sh;
   __shared__ SchedSmem sched;
   __shared__ int32_t route_cnt[4][(EPI == EPI_ROUTE) ? BN : 1];
@@ -154,12 +315,18 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   // ---- schedule: copy the group table, build the tile prefix -------------
   if (threadIdx.x == 0 && p.single_rows > 0) {
-    sched.G = 1;
-    sched.row_off[0] = 0;
-    sched.rows_pad[0] = p.single_rows;
-    sched.wslot[0] = 0;
-    sched.prefix[0] = 0;
-    sched.prefix[1] = (p.single_rows / BM) * (p.N / BN);
+    const int chunk = p.split_rows > 0 ? p.split_rows : p.single_rows;
+    const int G = p.single_rows / chunk;
+    const int nt = p.N / BN;
+    sched.G = G;
+    for (int g = 0; g <= G; ++g) {
+      if (g < G) {
+        sched.row_off[g] = g * chunk;
+        sched.rows_pad[g] = chunk;
+        sched.wslot[g] = 0;
+      }
+      sched.prefix[g] = g * (p.ragged_k ? (p.M_fixed / BM) * nt : (chunk / BM) * nt);
+    }
   } else if (threadIdx.x == 0) {
     int G = *p.num_groups;
     if (G > p.max_groups) G = p.max_groups;
@@ -169,17 +336,34 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int nt = p.N / BN;
     for (int g = 0; g < G; ++g) {
       const pp_group gr = p.groups[g];
-      sched.row_off[g] = gr.row_off;
-      sched.rows_pad[g] = gr.rows_pad;
-      sched.wslot[g] = gr.wslot;
+      // ragged-K (wgrad): keep groups sorted by K descending so the static
+      // round-robin tile walk hands out the long tiles first (LPT balance)
+      int pos = g;
+      if (p.ragged_k) {
+        while (pos > 0 && sched.rows_pad[pos - 1] < gr.rows_pad) {
+          sched.row_off[pos] = sched.row_off[pos - 1];
+          sched.rows_pad[pos] = sched.rows_pad[pos - 1];
+          sched.wslot[pos] = sched.wslot[pos - 1];
+          --pos;
+        }
+      }
+      sched.row_off[pos] = gr.row_off;
+      sched.rows_pad[pos] = gr.rows_pad;
+      sched.wslot[pos] = gr.wslot;
+    }
+    for (int g = 0; g < G; ++g) {
       sched.prefix[g] = acc;
-      acc += p.ragged_k ? (p.M_fixed / BM) * nt : (gr.rows_pad / BM) * nt;
+      acc += p.ragged_k ? (p.M_fixed / BM) * nt : (sched.rows_pad[g] / BM) * nt;
     }
     sched.prefix[G] = acc;
   }
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
+    if constexpr (tma_out<EPI>()) {
+      tma_prefetch_desc(&tmC);
+      if constexpr (EPI == EPI_GELU) tma_prefetch_desc(&tmC2);
+    }
   }
   if (warp == 1 && lane == 0) {
     for (int i = 0; i < STAGES; ++i) {
@@ -188,8 +372,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull_bar[i], 1);
-      mbar_init(&tempty_bar[i], 4);
+      mbar_init(&tempty_bar[i], EPI_WARPS);
     }
+    for (int i = 0; i < 8; ++i) mbar_init(&pre_bar[i], 1);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc<TMEM_COLS>(&tmem_base_sh);
@@ -198,6 +383,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = tmem_base_sh;
   const int total_tiles = sched.prefix[sched.G];
+  // Static persistent walk.  Ragged-K (wgrad) tiles are sorted by K descending
+  // and dealt in snake order (0..G-1, G-1..0, ...) so long tiles spread evenly.
+  const bool snake = p.ragged_k != 0;
+  auto tile_of = [&](int it) -> int {
+    const int G = (int)gridDim.x, b = (int)blockIdx.x;
+    return it * G + ((snake && (it & 1)) ? (G - 1 - b) : b);
+  };
 
   if (warp == 0) {
     // ================= TMA producer =================
@@ -205,7 +397,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       Tile tl;
-      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+      for (int it = 0, t = tile_of(0); t < total_tiles; t = tile_of(++it)) {
         if (!decode_tile<BN>(t, sched, p, tl)) break;
         for (int kb = 0; kb < tl.num_kb; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
@@ -246,7 +438,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     Tile tl;
-    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+    for (int it = 0, t = tile_of(0); t < total_tiles; t = tile_of(++it)) {
       if (!decode_tile<BN>(t, sched, p, tl)) break;
       mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
       tc_fence_after();
@@ -282,15 +474,24 @@ __global__ void __launch_bounds__(kThreads, 1)
         acc_phase ^= 1;
       }
     }
-  } else if (warp >= 4) {
+  } else if (warp >= 4 && warp < 4 + EPI_WARPS) {
     // ================= epilogue =================
-    const int q = warp - 4;  // TMEM lane quarter
+    const int q = warp & 3;                  // TMEM lane quarter (hardware: warp % 4)
+    const int col0 = ((warp - 4) >> 2) * EPI_COLS;  // column slice of this warp
+    uint8_t* stage = smem + STAGES * STAGE_BYTES + (warp - 4) * stage_bytes_per_warp<EPI>();
+    uint32_t pre_phase = 0;  // DGELU: parity of this warp's pre-activation TMA barrier
     const int r = q * 32 + lane;
     int acc = 0;
     uint32_t acc_phase = 0;
     Tile tl;
-    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+    for (int it = 0, t = tile_of(0); t < total_tiles; t = tile_of(++it)) {
       if (!decode_tile<BN>(t, sched, p, tl)) break;
+      if constexpr (EPI == EPI_DGELU) {  // first pre-activation block, in flight during the MMAs
+        if (lane == 0) {
+          mbar_arrive_expect_tx(&pre_bar[warp - 4], 2048);
+          tma_load_2d(stage, &tmC, &pre_bar[warp - 4], tl.n0 + col0, tl.row_off + tl.m0 + q * 32);
+        }
+      }
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       const uint32_t t_row = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
@@ -387,67 +588,47 @@ __global__ void __launch_bounds__(kThreads, 1)
           p.chunk_counts[(size_t)chunk * E + e] =
               route_cnt[0][e] + route_cnt[1][e] + route_cnt[2][e] + route_cnt[3][e];
       } else {
-#pragma unroll 1
-        for (int c = 0; c < BN; c += 32) {
-          uint32_t raw[32];
+        // software-pipelined: the TMEM read of chunk i+1 is in flight while chunk i is processed
+        constexpr int NCH = EPI_COLS / 32;
+        uint32_t rawA[32], rawB[32];
+        if (!zero) tmem_ld_32x32b_x32(t_row + col0, rawA);
+#pragma unroll
+        for (int i = 0; i < NCH; ++i) {
+          uint32_t(&cur)[32] = (i & 1) ? rawB : rawA;
+          uint32_t(&nxt)[32] = (i & 1) ? rawA : rawB;
+          const int c = col0 + 32 * i;
+          uint4 pre_v[4];
+          if constexpr (EPI == EPI_BF16_ADD) {  // old output: loads overlap the TMEM read
+            const __nv_bfloat16* old = reinterpret_cast<const __nv_bfloat16*>(p.c) +
+                                       ((size_t)tl.row_off + tl.m0 + r) * p.N + tl.n0 + c;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) pre_v[u] = ld_v4(old + 8 * u);
+          }
+          if constexpr (EPI == EPI_DGELU) {  // pre-activation block (TMA, SWIZZLE_64B)
+            mbar_wait(&pre_bar[warp - 4], pre_phase);
+            pre_phase ^= 1;
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              pre_v[u] = *reinterpret_cast<const uint4*>(stage + lane * 64 + ((u ^ ((lane >> 1) & 3)) << 4));
+            __syncwarp();
+            if (lane == 0 && i + 1 < NCH) {
+              mbar_arrive_expect_tx(&pre_bar[warp - 4], 2048);
+              tma_load_2d(stage, &tmC, &pre_bar[warp - 4], tl.n0 + c + 32, tl.row_off + tl.m0 + q * 32);
+            }
+          }
           if (!zero) {
-            tmem_ld_32x32b_x32(t_row + c, raw);
             tmem_ld_wait();
+            if (i + 1 < NCH) tmem_ld_32x32b_x32(t_row + c + 32, nxt);
           } else {
 #pragma unroll
-            for (int j = 0; j < 32; ++j) raw[j] = 0u;
+            for (int j = 0; j < 32; ++j) cur[j] = 0u;
           }
-          if (c + 32 == BN) {
+          if (i + 1 == NCH) {  // every TMEM read of this tile has completed
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty_bar[acc]);
           }
-          if constexpr (EPI == EPI_F32) {
-            float* out = reinterpret_cast<float*>(p.c) +
-                         ((size_t)tl.wslot * p.M_fixed + tl.m0 + r) * p.N + tl.n0 + c;
-#pragma unroll
-            for (int j = 0; j < 32; j += 4)
-              st_v4(out + j, make_uint4(raw[j], raw[j + 1], raw[j + 2], raw[j + 3]));
-          } else {
-            const size_t row = (size_t)tl.row_off + tl.m0 + r;
-            const size_t off = row * p.N + tl.n0 + c;
-            if constexpr (EPI == EPI_BF16) {
-              __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.c) + off;
-#pragma unroll
-              for (int j = 0; j < 32; j += 8) {
-                float f[8];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) f[u] = __uint_as_float(raw[j + u]);
-                st_v4(out + j, f32x8_to_bf16(f));
-              }
-            } else if constexpr (EPI == EPI_GELU) {
-              __nv_bfloat16* pre = reinterpret_cast<__nv_bfloat16*>(p.c) + off;
-              __nv_bfloat16* act = reinterpret_cast<__nv_bfloat16*>(p.c2) + off;
-#pragma unroll
-              for (int j = 0; j < 32; j += 8) {
-                float f[8], g[8];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                  f[u] = __uint_as_float(raw[j + u]);
-                  // GeLU of the bf16-rounded pre-activation, as the backward sees it
-                  g[u] = gelu_f(__bfloat162float(__float2bfloat16_rn(f[u])));
-                }
-                st_v4(pre + j, f32x8_to_bf16(f));
-                st_v4(act + j, f32x8_to_bf16(g));
-              }
-            } else if constexpr (EPI == EPI_DGELU) {
-              const __nv_bfloat16* pre = reinterpret_cast<const __nv_bfloat16*>(p.c2) + off;
-              __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.c) + off;
-#pragma unroll
-              for (int j = 0; j < 32; j += 8) {
-                float x[8], f[8];
-                bf16x8_to_f32(ld_v4(pre + j), x);
-#pragma unroll
-                for (int u = 0; u < 8; ++u) f[u] = __uint_as_float(raw[j + u]) * dgelu_f(x[u]);
-                st_v4(out + j, f32x8_to_bf16(f));
-              }
-            }
-          }
+          epilogue_chunk<EPI>(cur, p, tl, r, c, pre_v, stage, &tmC, &tmC2, lane);
         }
       }
       if (++acc == 2) {
@@ -457,6 +638,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
 
+  if constexpr (tma_out<EPI>()) {
+    if (warp >= 4 && lane == 0) bulk_wait0();
+  }
   tc_fence_before();
   __syncthreads();
   if (warp == 2) tmem_free<TMEM_COLS>(tmem_base);
@@ -480,15 +664,18 @@ static int get_encode() {
 
 // 2-D bf16 tensor [outer][inner] (inner contiguous), box [box_outer][box_inner], 128B swizzle
 static int make_tmap(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer,
-                     uint32_t box_inner, uint32_t box_outer) {
+                     uint32_t box_inner, uint32_t box_outer,
+                     CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B,
+                     CUtensorMapDataType dt = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16) {
   if (int rc = get_encode()) return rc;
+  const uint64_t esize = dt == CU_TENSOR_MAP_DATA_TYPE_FLOAT32 ? 4 : 2;
   cuuint64_t dims[2] = {inner, outer};
-  cuuint64_t strides[1] = {inner * 2};
+  cuuint64_t strides[1] = {inner * esize};
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims,
+  CUresult r = g_encode(m, dt, 2, const_cast<void*>(ptr), dims,
                         strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     return fail(PP_ECUDA, "cuTensorMapEncodeTiled failed (%d) inner=%llu outer=%llu box=%ux%u",
@@ -497,13 +684,25 @@ static int make_tmap(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t o
   return PP_OK;
 }
 
+// output tensor map for the TMA-store epilogue: bf16 [outer][inner], box 32 x 32, SWIZZLE_64B
+static int make_out_tmap(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer) {
+  return make_tmap(m, ptr, inner, outer, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
+}
+// fp32 output (wgrad): box 32 x 32 fp32 = 128 B rows, SWIZZLE_128B
+static int make_out_tmap_f32(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer) {
+  return make_tmap(m, ptr, inner, outer, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_DATA_TYPE_FLOAT32);
+}
+
 template <int BN, bool A_MN, bool B_MN, int EPI, int STAGES>
 static int launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, int grid,
-                  cudaStream_t st) {
+                  cudaStream_t st, const CUtensorMap* tc = nullptr, const CUtensorMap* tc2 = nullptr) {
   auto kern = grouped_gemm_kernel<BN, A_MN, B_MN, EPI, STAGES>;
-  const int smem = STAGES * (BM * BK * 2 + BN * BK * 2) + 1024;
+  const int staging = tma_out<EPI>() ? 8 * stage_bytes_per_warp<EPI>() : 0;
+  const int smem = STAGES * (BM * BK * 2 + BN * BK * 2) + staging + 1024;
+  static CUtensorMap dummy{};
   PP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  kern<<<grid, kThreads, smem, st>>>(ta, tb, p);
+  kern<<<grid, kThreads, smem, st>>>(ta, tb, tc ? *tc : dummy, tc2 ? *tc2 : dummy, p);
   PP_LAUNCH_CHECK();
   return PP_OK;
 }
@@ -548,6 +747,35 @@ int route_gemm(const void* x, const void* wg, const float* bias, int T, int d, i
   }
 }
 
+int gate_bwd_gemms(const void* dl, const void* wg, const void* x, int T, int d, int E, int EP,
+                   void* dx, float* dwg, int split, cudaStream_t st) {
+  const int grid = sm_count();
+  CUtensorMap ta, tb;
+  // dx[T][d] += dl[T][EP] . wg[E][d]      (K = EP; wg rows >= E read as zeros)
+  GemmParams p{};
+  p.max_groups = 1;
+  p.single_rows = T;
+  p.N = d;
+  p.K_fixed = EP;
+  p.c = dx;
+  if (int rc = make_tmap(&ta, dl, EP, T, BK, BM)) return rc;
+  if (int rc = make_tmap(&tb, wg, d, E, 64, BK)) return rc;
+  if (int rc = launch<256, false, true, EPI_BF16_ADD, 4>(ta, tb, p, grid, st)) return rc;
+  // dwg[E][d] += dl^T . x  (split-K over token chunks, fp32 atomics; M padded to 128)
+  GemmParams q{};
+  q.max_groups = 1;
+  q.single_rows = T;
+  q.split_rows = split;
+  q.ragged_k = 1;
+  q.M_fixed = BM;
+  q.m_real = E;
+  q.N = d;
+  q.c = dwg;
+  if (int rc = make_tmap(&ta, dl, EP, T, 64, BK)) return rc;
+  if (int rc = make_tmap(&tb, x, d, T, 64, BK)) return rc;
+  return launch<256, true, true, EPI_F32_ATOMIC, 4>(ta, tb, q, grid, st);
+}
+
 }  // namespace pp
 
 using namespace pp;
@@ -566,7 +794,7 @@ extern "C" int pp_grouped_gemm(int32_t mode, const void* a, const void* b, void*
   cudaStream_t st = as_stream(stream);
   const int grid = num_sms > 0 ? num_sms : sm_count();
   const int R = rows_capacity, S = num_slots, dm = d_model, df = d_ff;
-  CUtensorMap ta, tb;
+  CUtensorMap ta, tb, tc, tc2;
   GemmParams p{};
   p.groups = groups;
   p.num_groups = num_groups;
@@ -579,32 +807,40 @@ extern "C" int pp_grouped_gemm(int32_t mode, const void* a, const void* b, void*
       PP_CHECK_ARG(c2, "FWD1 needs the act output");
       if ((rc = make_tmap(&ta, a, dm, R, BK, BM)) || (rc = make_tmap(&tb, b, dm, (uint64_t)S * df, BK, 256))) return rc;
       p.N = df; p.K_fixed = dm;
-      return launch<256, false, false, EPI_GELU, 4>(ta, tb, p, grid, st);
+      if ((rc = make_out_tmap(&tc, c, df, R)) || (rc = make_out_tmap(&tc2, c2, df, R))) return rc;
+      return launch<256, false, false, EPI_GELU, 4>(ta, tb, p, grid, st, &tc, &tc2);
     case PP_GEMM_FWD2:
       if ((rc = make_tmap(&ta, a, df, R, BK, BM)) || (rc = make_tmap(&tb, b, df, (uint64_t)S * dm, BK, 256))) return rc;
       p.N = dm; p.K_fixed = df;
-      return launch<256, false, false, EPI_BF16, 4>(ta, tb, p, grid, st);
+      if ((rc = make_out_tmap(&tc, c, dm, R))) return rc;
+      return launch<256, false, false, EPI_BF16, 4>(ta, tb, p, grid, st, &tc);
     case PP_GEMM_DGRAD2:
       PP_CHECK_ARG(c2, "DGRAD2 needs the pre-activation");
       if ((rc = make_tmap(&ta, a, dm, R, BK, BM)) || (rc = make_tmap(&tb, b, df, (uint64_t)S * dm, 64, BK))) return rc;
       p.N = df; p.K_fixed = dm;
-      return launch<256, false, true, EPI_DGELU, 4>(ta, tb, p, grid, st);
+      PP_CHECK_ARG(c2 == c, "DGRAD2 runs in place: dPre must alias pre");
+      if ((rc = make_out_tmap(&tc, c, df, R))) return rc;
+      return launch<256, false, true, EPI_DGELU, 3>(ta, tb, p, grid, st, &tc);
     case PP_GEMM_DGRAD1:
       if ((rc = make_tmap(&ta, a, df, R, BK, BM)) || (rc = make_tmap(&tb, b, dm, (uint64_t)S * df, 64, BK))) return rc;
       p.N = dm; p.K_fixed = df;
-      return launch<256, false, true, EPI_BF16, 4>(ta, tb, p, grid, st);
+      if ((rc = make_out_tmap(&tc, c, dm, R))) return rc;
+      return launch<256, false, true, EPI_BF16, 4>(ta, tb, p, grid, st, &tc);
     case PP_GEMM_WGRAD2:
       if ((rc = make_tmap(&ta, a, dm, R, 64, BK)) || (rc = make_tmap(&tb, b, df, R, 64, BK))) return rc;
       p.M_fixed = dm; p.N = df; p.ragged_k = 1;
-      return launch<256, true, true, EPI_F32, 4>(ta, tb, p, grid, st);
+      if ((rc = make_out_tmap_f32(&tc, c, df, (uint64_t)S * dm))) return rc;
+      return launch<256, true, true, EPI_F32, 3>(ta, tb, p, grid, st, &tc);
     case PP_GEMM_WGRAD1:
       if ((rc = make_tmap(&ta, a, df, R, 64, BK)) || (rc = make_tmap(&tb, b, dm, R, 64, BK))) return rc;
       p.M_fixed = df; p.N = dm; p.ragged_k = 1;
-      return launch<256, true, true, EPI_F32, 4>(ta, tb, p, grid, st);
+      if ((rc = make_out_tmap_f32(&tc, c, dm, (uint64_t)S * df))) return rc;
+      return launch<256, true, true, EPI_F32, 3>(ta, tb, p, grid, st, &tc);
     case PP_GEMM_PLAIN:
       if ((rc = make_tmap(&ta, a, dm, R, BK, BM)) || (rc = make_tmap(&tb, b, dm, (uint64_t)S * df, BK, 256))) return rc;
       p.N = df; p.K_fixed = dm;
-      return launch<256, false, false, EPI_BF16, 4>(ta, tb, p, grid, st);
+      if ((rc = make_out_tmap(&tc, c, df, R))) return rc;
+      return launch<256, false, false, EPI_BF16, 4>(ta, tb, p, grid, st, &tc);
     default:
       return fail(PP_EINVAL, "pp_grouped_gemm: unknown mode %d", mode);
   }

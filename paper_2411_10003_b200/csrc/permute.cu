@@ -268,19 +268,19 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-// dx[t] = sum_j dXp[pair] + sum_e dlogits[t][e] * wg[e]; dlogits from softmax backward.
-template <int VPL, int EMAX>
+// dx[t] = sum_j dXp[pair]  and  dl[t][:] = softmax backward of the gate (bf16,
+// padded to EP columns with zeros); the gate GEMMs (dx += dl.wg, dwg += dl^T.x)
+// then run on tensor cores (gate_bwd_gemms in gemm.cu).
+template <int VPL, int EP>
 __global__ void __launch_bounds__(256)
     dispatch_bwd_kernel(void* const* dxp_ptrs, const int32_t* __restrict__ pair_dest,
                         const int32_t* __restrict__ pair_row, const int32_t* __restrict__ idx,
-                        const float* __restrict__ probs, const float* __restrict__ dw,
-                        const __nv_bfloat16* __restrict__ wg, int T, int d, int k, int E,
-                        __nv_bfloat16* dx, float* dlogits) {
+                        const float* __restrict__ probs, const float* __restrict__ dw, int T, int d,
+                        int k, int E, __nv_bfloat16* dx, __nv_bfloat16* dl) {
   const int lane = threadIdx.x & 31;
   const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
   for (int t = warp_global; t < T; t += nwarps) {
-    // ---- softmax backward restricted to the selected experts
     int my_e = -1, my_dest = 0, my_row = 0;
     float my_dw = 0.f, my_p = 0.f;
     if (lane < k) {
@@ -290,27 +290,7 @@ __global__ void __launch_bounds__(256)
       my_dw = dw[(size_t)t * k + lane];
       my_p = probs[(size_t)t * E + my_e];
     }
-    float gsum = my_dw * my_p;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) gsum += __shfl_xor_sync(0xffffffffu, gsum, o);
-    // dlogits_i = p_i * (dw_{j(i)} [i selected] - gsum)
-    float dl[(EMAX + 31) / 32];
-#pragma unroll
-    for (int q = 0; q < (EMAX + 31) / 32; ++q) {
-      const int i = lane + 32 * q;
-      float sel_dw = 0.f;
-      for (int j = 0; j < k; ++j) {
-        const int ej = __shfl_sync(0xffffffffu, my_e, j);
-        const float dwj = __shfl_sync(0xffffffffu, my_dw, j);
-        if (ej == i) sel_dw = dwj;
-      }
-      dl[q] = 0.f;
-      if (i < E) {
-        dl[q] = probs[(size_t)t * E + i] * (sel_dw - gsum);
-        dlogits[(size_t)t * E + i] = dl[q];
-      }
-    }
-    // ---- gather expert-input grads
+    // gather the expert-input grads first (long-latency loads in flight)
     float acc[VPL][8];
 #pragma unroll
     for (int i = 0; i < VPL; ++i)
@@ -332,51 +312,27 @@ __global__ void __launch_bounds__(256)
         for (int u = 0; u < 8; ++u) acc[i][u] += f[u];
       }
     }
-    // ---- gate input grad: sum_e dlogits[e] * wg[e]
-    for (int e = 0; e < E; ++e) {
-      const float de = __shfl_sync(0xffffffffu, dl[e >> 5], e & 31);
-      const uint4* wrow = reinterpret_cast<const uint4*>(wg + (size_t)e * d);
-#pragma unroll
-      for (int i = 0; i < VPL; ++i) {
-        float f[8];
-        bf16x8_to_f32(__ldg(wrow + lane + 32 * i), f);
-#pragma unroll
-        for (int u = 0; u < 8; ++u) acc[i][u] = fmaf(de, f[u], acc[i][u]);
-      }
-    }
     uint4* dst = reinterpret_cast<uint4*>(dx + (size_t)t * d);
 #pragma unroll
     for (int i = 0; i < VPL; ++i) st_v4(dst + lane + 32 * i, f32x8_to_bf16(acc[i]));
-  }
-}
-
-// dwg[e][col] += sum_t dlogits[t][e] * x[t][col]; block = 256 columns x a token split
-template <int EMAX>
-__global__ void __launch_bounds__(256)
-    gate_wgrad_kernel(const float* __restrict__ dlogits, const __nv_bfloat16* __restrict__ x,
-                      int T, int d, int E, int tokens_per_split, float* dwg) {
-  __shared__ float sdl[64][EMAX];
-  const int col = blockIdx.x * 256 + threadIdx.x;
-  const int t0 = blockIdx.y * tokens_per_split;
-  const int t1 = min(T, t0 + tokens_per_split);
-  float acc[EMAX];
+    // softmax backward restricted to the selected experts:
+    //   dl_i = p_i * (dw_{j(i)} [i selected] - sum_j dw_j p_{e_j})
+    float gsum = my_dw * my_p;
 #pragma unroll
-  for (int e = 0; e < EMAX; ++e) acc[e] = 0.f;
-  for (int tb = t0; tb < t1; tb += 64) {
-    const int nt = min(64, t1 - tb);
-    __syncthreads();
-    for (int i = threadIdx.x; i < nt * E; i += 256) sdl[i / E][i % E] = dlogits[(size_t)tb * E + i];
-    __syncthreads();
-    for (int tt = 0; tt < nt; ++tt) {
-      const float xv = __bfloat162float(x[(size_t)(tb + tt) * d + col]);
+    for (int o = 16; o > 0; o >>= 1) gsum += __shfl_xor_sync(0xffffffffu, gsum, o);
 #pragma unroll
-      for (int e = 0; e < EMAX; ++e)
-        if (e < E) acc[e] = fmaf(sdl[tt][e], xv, acc[e]);
+    for (int q = 0; q < EP / 32; ++q) {
+      const int i = lane + 32 * q;
+      float sel_dw = 0.f;
+      for (int j = 0; j < k; ++j) {
+        const int ej = __shfl_sync(0xffffffffu, my_e, j);
+        const float dwj = __shfl_sync(0xffffffffu, my_dw, j);
+        if (ej == i) sel_dw = dwj;
+      }
+      const float v = i < E ? probs[(size_t)t * E + i] * (sel_dw - gsum) : 0.f;
+      dl[(size_t)t * EP + i] = __float2bfloat16_rn(v);
     }
   }
-#pragma unroll
-  for (int e = 0; e < EMAX; ++e)
-    if (e < E) atomicAdd(dwg + (size_t)e * d + col, acc[e]);
 }
 
 static int grid_for_tokens(int T) {
@@ -498,42 +454,40 @@ extern "C" int pp_combine_bwd(const void* dy, void* const* out_ptrs, void* const
 
 extern "C" int pp_dispatch_bwd(void* const* dxp_ptrs, const int32_t* pair_dest,
                                const int32_t* pair_row, const int32_t* idx, const float* probs,
-                               const float* dw, const void* wg, int32_t T, int32_t d, int32_t k,
-                               int32_t E, void* dx, float* dlogits, void* stream) {
-  PP_CHECK_ARG(dxp_ptrs && pair_dest && pair_row && idx && probs && dw && wg && dx && dlogits,
+                               const float* dw, int32_t T, int32_t d, int32_t k, int32_t E,
+                               int32_t EP, void* dx, void* dl, void* stream) {
+  PP_CHECK_ARG(dxp_ptrs && pair_dest && pair_row && idx && probs && dw && dx && dl,
                "pp_dispatch_bwd: null pointer");
-  PP_CHECK_ARG(E <= 128, "pp_dispatch_bwd: E=%d > 128", E);
+  PP_CHECK_ARG(EP == 64 || EP == 128, "pp_dispatch_bwd: EP=%d must be 64 or 128", EP);
+  PP_CHECK_ARG(E <= EP, "pp_dispatch_bwd: E=%d > EP=%d", E, EP);
   cudaStream_t st = as_stream(stream);
-  const auto* wgp = reinterpret_cast<const __nv_bfloat16*>(wg);
   auto* dxp = reinterpret_cast<__nv_bfloat16*>(dx);
-  if (E <= 32) {
-    PP_VPL_SWITCH(d, (dispatch_bwd_kernel<VPL, 32><<<grid_for_tokens(T), 256, 0, st>>>(
-                         dxp_ptrs, pair_dest, pair_row, idx, probs, dw, wgp, T, d, k, E, dxp, dlogits)));
-  } else if (E <= 64) {
+  auto* dlp = reinterpret_cast<__nv_bfloat16*>(dl);
+  if (EP == 64) {
     PP_VPL_SWITCH(d, (dispatch_bwd_kernel<VPL, 64><<<grid_for_tokens(T), 256, 0, st>>>(
-                         dxp_ptrs, pair_dest, pair_row, idx, probs, dw, wgp, T, d, k, E, dxp, dlogits)));
+                         dxp_ptrs, pair_dest, pair_row, idx, probs, dw, T, d, k, E, dxp, dlp)));
   } else {
     PP_VPL_SWITCH(d, (dispatch_bwd_kernel<VPL, 128><<<grid_for_tokens(T), 256, 0, st>>>(
-                         dxp_ptrs, pair_dest, pair_row, idx, probs, dw, wgp, T, d, k, E, dxp, dlogits)));
+                         dxp_ptrs, pair_dest, pair_row, idx, probs, dw, T, d, k, E, dxp, dlp)));
   }
   PP_LAUNCH_CHECK();
   return PP_OK;
 }
 
-extern "C" int pp_gate_wgrad(const float* dlogits, const void* x, int32_t T, int32_t d, int32_t E,
-                             float* dwg, void* stream) {
-  PP_CHECK_ARG(dlogits && x && dwg, "pp_gate_wgrad: null pointer");
-  PP_CHECK_ARG(d % 256 == 0, "pp_gate_wgrad: d=%d must be a multiple of 256", d);
-  PP_CHECK_ARG(E <= 64, "pp_gate_wgrad: E=%d > 64", E);
-  const int splits = (T + 511) / 512;
-  dim3 grid(d / 256, splits);
-  const auto* xp = reinterpret_cast<const __nv_bfloat16*>(x);
-  if (E <= 16)
-    gate_wgrad_kernel<16><<<grid, 256, 0, as_stream(stream)>>>(dlogits, xp, T, d, E, 512, dwg);
-  else if (E <= 32)
-    gate_wgrad_kernel<32><<<grid, 256, 0, as_stream(stream)>>>(dlogits, xp, T, d, E, 512, dwg);
-  else
-    gate_wgrad_kernel<64><<<grid, 256, 0, as_stream(stream)>>>(dlogits, xp, T, d, E, 512, dwg);
-  PP_LAUNCH_CHECK();
-  return PP_OK;
+namespace pp {
+int gate_bwd_gemms(const void* dl, const void* wg, const void* x, int T, int d, int E, int EP,
+                   void* dx, float* dwg, int split, cudaStream_t st);
+}
+
+extern "C" int pp_gate_bwd(const void* dl, const void* wg, const void* x, int32_t T, int32_t d,
+                           int32_t E, int32_t EP, void* dx, float* dwg, void* stream) {
+  PP_CHECK_ARG(dl && wg && x && dx && dwg, "pp_gate_bwd: null pointer");
+  PP_CHECK_ARG(d % 256 == 0, "pp_gate_bwd: d=%d must be a multiple of 256", d);
+  PP_CHECK_ARG(T % PP_CHUNK == 0, "pp_gate_bwd: T=%d must be a multiple of %d", T, PP_CHUNK);
+  PP_CHECK_ARG((EP == 64 || EP == 128) && E <= EP, "pp_gate_bwd: bad E=%d/EP=%d", E, EP);
+  // split-K chunk: ~4 chunks per SM-row of output tiles, multiple of 128 dividing T
+  int split = 1024;
+  while (split > 128 && T % split) split >>= 1;
+  if (T % split) split = T;
+  return gate_bwd_gemms(dl, wg, x, T, d, E, EP, dx, dwg, split, as_stream(stream));
 }

@@ -230,7 +230,8 @@ class MoELayer(torch.nn.Module):
         self.pair_dest = torch.empty((T, k), **i32)
         self.pair_row = torch.empty((T, k), **i32)
         self.dw = torch.empty((T, k), dtype=torch.float32, device=dev)
-        self.dlogits = torch.empty((T, E), dtype=torch.float32, device=dev)
+        self.EP = 64 if E <= 64 else 128
+        self.dlogits = torch.zeros((T, self.EP), dtype=torch.bfloat16, device=dev)  # gate dL/dlogits
         # ---- expert activations ---------------------------------------------
         R = self.rows_cap
         self.xp = PeerBuffer((R, d_model), torch.bfloat16, self.group, dev)
@@ -397,11 +398,10 @@ class MoELayer(torch.nn.Module):
         dx = torch.empty((self.T, self.d), dtype=torch.bfloat16, device=self.device)
         _lib.call("pp_dispatch_bwd", self.dxp.ptrs.data_ptr(), self.pair_dest.data_ptr(),
                   self.pair_row.data_ptr(), self.idx.data_ptr(), self.probs.data_ptr(), self.dw.data_ptr(),
-                  self.wg.data_ptr(), self.T, self.d, self.k, self.E, dx.data_ptr(),
-                  self.dlogits.data_ptr(), sp)
+                  self.T, self.d, self.k, self.E, self.EP, dx.data_ptr(), self.dlogits.data_ptr(), sp)
         self.wg.main_grad.zero_()
-        _lib.call("pp_gate_wgrad", self.dlogits.data_ptr(), x.data_ptr(), self.T, self.d, self.E,
-                  self.wg.main_grad.data_ptr(), sp)
+        _lib.call("pp_gate_bwd", self.dlogits.data_ptr(), self.wg.data_ptr(), x.data_ptr(), self.T, self.d,
+                  self.E, self.EP, dx.data_ptr(), self.wg.main_grad.data_ptr(), sp)
         self.iteration += 1
         return dx
 
