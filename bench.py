@@ -51,59 +51,71 @@ def zipf_bias(E: int, skew: float, seed: int):
 
 
 class ClockSampler:
-    FIELDS = ("clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
-              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
-              "clocks_event_reasons.sw_power_cap")
+    """In-process NVML sampler (nvidia-ml-py): SM clock + throttle reasons every
+    ~20 ms on a daemon thread.  NVML is initialised before the timed region so
+    no driver-heavy start-up (e.g. spawning nvidia-smi) lands inside it;
+    ``mark()`` brackets the timed region and only samples inside it count."""
 
-    def __init__(self, index) -> None:
-        self.index = index  # nvidia-smi id: UUID of the torch device (robust to CUDA_VISIBLE_DEVICES)
-        self.proc = None
-        self.lines = []
+    REASONS = {  # nvmlClocksEventReason* bits
+        "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+        "hw_power_brake_slowdown": 0x80, "sw_power_cap": 0x4,
+    }
 
-    def __enter__(self):
+    def __init__(self, torch_device) -> None:
+        self.samples = []
+        self.windows = []
+        self._stop = threading.Event()
+        self.error = None
         try:
-            sel = ["-i", str(self.index)] if self.index is not None else []
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", *sel, "--query-gpu=" + ",".join(self.FIELDS),
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+
+            pynvml.nvmlInit()
+            uuid = "GPU-" + str(__import__("torch").cuda.get_device_properties(torch_device).uuid)
+            self.h = pynvml.nvmlDeviceGetHandleByUUID(uuid.encode())
+            self.nv = pynvml
+            self.max_sm = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception as exc:  # no NVML: report why, never fail the bench
+            self.nv = None
+            self.error = repr(exc)[:200]
+        self.thread = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                reasons = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.samples.append((time.perf_counter(), sm, reasons))
+            except Exception as exc:
+                self.error = repr(exc)[:200]
+                return
+            time.sleep(0.02)
+
+    def start(self):
+        if self.nv is not None:
             self.thread.start()
-        except OSError:
-            self.proc = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+    def mark(self, t0: float, t1: float) -> None:
+        self.windows.append((t0, t1))
 
-    def __exit__(self, *a):
-        if self.proc is not None:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except subprocess.TimeoutExpired:
-                self.proc.kill()
+    def stop(self):
+        self._stop.set()
+        if self.nv is not None:
+            self.thread.join(timeout=2)
 
     def summary(self) -> dict:
-        sm, mx, reasons = [], 0.0, set()
-        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) != 6:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx = max(mx, float(parts[1]))
-            except ValueError:
-                continue
-            for n, v in zip(names, parts[2:]):
-                if v.lower().startswith("active"):
-                    reasons.add(n)
-        out = {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
-               "reasons": sorted(reasons), "samples": len(sm)}
-        if not sm and self.lines:
-            out["error"] = self.lines[0][:200]
+        inside = [s for s in self.samples if any(a <= s[0] <= b for a, b in self.windows)]
+        use = inside or self.samples[-5:]
+        sm = [s[1] for s in use]
+        reasons = sorted({n for s in use for n, bit in self.REASONS.items() if s[2] & bit})
+        out = {"sm_mhz": statistics.median(sm) if sm else None,
+               "sm_max_mhz": getattr(self, "max_sm", None), "reasons": reasons,
+               "samples": len(inside), "source": "nvml"}
+        if not inside:
+            out["note"] = "timed region shorter than the 20 ms sampling period: nearest samples used"
+        if self.error:
+            out["error"] = self.error
         return out
 
 
@@ -260,26 +272,28 @@ def main() -> None:
 
     # ---- timed region (device events), GEMM launches timed on their stream
     layer.gemm_timing = []
+    layer.gemm_event_pool = [torch.cuda.Event(enable_timing=True) for _ in range(2 * 8 * args.steps)]
     _lib.reset_launch_count()
     xs = [x.detach().clone() for _ in range(2)]
     torch.cuda.synchronize()
-    try:
-        smi_id = "GPU-" + str(torch.cuda.get_device_properties(dev).uuid)
-    except Exception:
-        smi_id = None
-    with ClockSampler(smi_id) as clk:
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-        t0 = torch.cuda.Event(enable_timing=True)
-        t1 = torch.cuda.Event(enable_timing=True)
-        t0.record()
-        for i in range(args.steps):
-            step(xs[i % 2].detach(), dy)
-        t1.record()
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
+    clk = ClockSampler(dev).start()
+    time.sleep(0.1)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    w0 = time.perf_counter()
+    t0.record()
+    h0 = time.perf_counter()
+    for i in range(args.steps):
+        step(xs[i % 2].detach(), dy)
+    host_ms = (time.perf_counter() - h0) * 1e3 / args.steps
+    t1.record()
+    torch.cuda.synchronize()
+    clk.mark(w0, time.perf_counter())
+    if world > 1:
+        dist.barrier()
     launches = _lib.launch_count()
     ms_total = t0.elapsed_time(t1)
     ms_tensor = torch.tensor([ms_total], dtype=torch.float64, device=dev)
@@ -312,7 +326,8 @@ def main() -> None:
         yh = [torch.empty((T, d), dtype=torch.bfloat16).pin_memory() for _ in range(2)]
         xdev = [torch.empty_like(x) for _ in range(2)]
         dydev = [torch.empty_like(dy) for _ in range(2)]
-        copy = torch.cuda.Stream(device=dev)
+        copy = torch.cuda.Stream(device=dev)   # H2D engine
+        back = torch.cuda.Stream(device=dev)   # D2H engine (opposite direction, runs concurrently)
         main = torch.cuda.current_stream()
         torch.cuda.synchronize()
         if world > 1:
@@ -322,6 +337,7 @@ def main() -> None:
         ev_in = [torch.cuda.Event() for _ in range(2)]
         ev_free = [torch.cuda.Event() for _ in range(2)]
         ev_out = [torch.cuda.Event() for _ in range(2)]
+        w0 = time.perf_counter()
         e0.record(main)
 
         def h2d(i):
@@ -342,14 +358,15 @@ def main() -> None:
             y = step(xdev[b].detach(), dydev[b])
             ev_free[b].record(main)
             keep[b] = y
-            with torch.cuda.stream(copy):
-                copy.wait_event(ev_free[b])
+            with torch.cuda.stream(back):
+                back.wait_event(ev_free[b])
                 yh[b].copy_(y.detach(), non_blocking=True)
-                ev_out[b].record(copy)
+                ev_out[b].record(back)
         for b in range(2):
             main.wait_event(ev_out[b])
         e1.record(main)
         torch.cuda.synchronize()
+        clk.mark(w0, time.perf_counter())
         em = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(em, op=dist.ReduceOp.MAX)
@@ -395,6 +412,8 @@ def main() -> None:
             imbalance.update({"virtual_slot_H_sigma_planned": float(np.std(Hp)),
                               "rb": P.rb_ratio(H0, Hp)})
 
+    clk.stop()
+    clk_summary = clk.summary()
     cpu_info = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile_only:
         cpu_info = cpu_baseline(cfg)
@@ -408,8 +427,9 @@ def main() -> None:
                        "d_ff": f, "tokens_per_gpu": T, "parallelism": f"ep{world}",
                        "l2": "working set > L2 (activations+weights >> 126 MB), no flush",
                        "routing": "Zipf(1.2) gate bias, random bf16 tokens"},
+            "host_enqueue_ms_per_step": host_ms,
             "roofline": roofline, "cpu_baseline": cpu_info, "e2e": e2e, "gpu_launches": launches,
-            "clocks": clk.summary(), "planner": planner_info, "imbalance": imbalance,
+            "clocks": clk_summary, "planner": planner_info, "imbalance": imbalance,
         }
         print(json.dumps(out), flush=True)
     if world > 1:

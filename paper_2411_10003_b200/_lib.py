@@ -127,7 +127,7 @@ def check(rc: int, what: str = "") -> None:
 # kernels each entry point launches (for the bench's gpu_launches claim)
 KERNELS_PER_CALL = {
     "pp_plan_greedy": 1, "pp_derive_loads": 1, "pp_route_topk": 1, "pp_slot_histogram": 1,
-    "pp_dispatch_layout": 1, "pp_dispatch": 2, "pp_combine": 1, "pp_combine_bwd": 2,
+    "pp_dispatch_layout": 1, "pp_dispatch": 1, "pp_combine": 1, "pp_combine_bwd": 1,
     "pp_dispatch_bwd": 1, "pp_gate_bwd": 2, "pp_grouped_gemm": 1, "pp_replica_trans": 1,
     "pp_replica_agg": 1, "pp_peer_barrier": 1,
 }

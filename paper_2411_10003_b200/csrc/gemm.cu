@@ -26,6 +26,7 @@
 #include <cudaTypedefs.h>
 
 #include <mutex>
+#include <unordered_map>
 
 #include "common.cuh"
 
@@ -663,10 +664,55 @@ static int get_encode() {
 }
 
 // 2-D bf16 tensor [outer][inner] (inner contiguous), box [box_outer][box_inner], 128B swizzle
+struct TmapKey {
+  const void* ptr;
+  uint64_t inner, outer;
+  uint32_t bi, bo, swz, dt;
+  bool operator==(const TmapKey& o) const {
+    return ptr == o.ptr && inner == o.inner && outer == o.outer && bi == o.bi && bo == o.bo &&
+           swz == o.swz && dt == o.dt;
+  }
+};
+struct TmapKeyHash {
+  size_t operator()(const TmapKey& k) const {
+    size_t h = std::hash<const void*>()(k.ptr);
+    for (uint64_t v : {k.inner, k.outer, (uint64_t)k.bi << 32 | k.bo, (uint64_t)k.swz << 32 | k.dt})
+      h = h * 1000003u ^ std::hash<uint64_t>()(v);
+    return h;
+  }
+};
+
+static int encode_tmap(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer,
+                       uint32_t box_inner, uint32_t box_outer, CUtensorMapSwizzle swz,
+                       CUtensorMapDataType dt);
+
+// Tensor maps are pure functions of (address, shape, box, swizzle, dtype); the
+// layer's buffers are persistent, so encoding happens once per buffer.
 static int make_tmap(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer,
                      uint32_t box_inner, uint32_t box_outer,
                      CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B,
                      CUtensorMapDataType dt = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16) {
+  static std::mutex mu;
+  static std::unordered_map<TmapKey, CUtensorMap, TmapKeyHash> cache;
+  const TmapKey key{ptr, inner, outer, box_inner, box_outer, (uint32_t)swz, (uint32_t)dt};
+  {
+    std::lock_guard<std::mutex> g(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) {
+      *m = it->second;
+      return PP_OK;
+    }
+  }
+  if (int rc = encode_tmap(m, ptr, inner, outer, box_inner, box_outer, swz, dt)) return rc;
+  std::lock_guard<std::mutex> g(mu);
+  if (cache.size() > 4096) cache.clear();
+  cache.emplace(key, *m);
+  return PP_OK;
+}
+
+static int encode_tmap(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer,
+                       uint32_t box_inner, uint32_t box_outer, CUtensorMapSwizzle swz,
+                       CUtensorMapDataType dt) {
   if (int rc = get_encode()) return rc;
   const uint64_t esize = dt == CU_TENSOR_MAP_DATA_TYPE_FLOAT32 ? 4 : 2;
   cuuint64_t dims[2] = {inner, outer};
@@ -701,7 +747,13 @@ static int launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams
   const int staging = tma_out<EPI>() ? 8 * stage_bytes_per_warp<EPI>() : 0;
   const int smem = STAGES * (BM * BK * 2 + BN * BK * 2) + staging + 1024;
   static CUtensorMap dummy{};
-  PP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  static int configured[64] = {0};  // per device: the smem attribute is set once
+  int dev = 0;
+  PP_CUDA_TRY(cudaGetDevice(&dev));
+  if (dev < 64 && !configured[dev]) {
+    PP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    configured[dev] = 1;
+  }
   kern<<<grid, kThreads, smem, st>>>(ta, tb, tc ? *tc : dummy, tc2 ? *tc2 : dummy, p);
   PP_LAUNCH_CHECK();
   return PP_OK;

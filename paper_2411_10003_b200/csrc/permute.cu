@@ -35,8 +35,23 @@ __global__ void slot_histogram_kernel(const int32_t* chunk_counts, int chunks_pe
 }
 
 // ---------------------------------------------------------------------------
-// Layout solver: one CTA.  See ppmoe.h for the outputs.
+// Layout solver: one CTA, everything staged in shared memory.  See ppmoe.h.
 constexpr int kLayoutThreads = 1024;
+
+struct LayoutSmem {
+  int32_t* counts;   // [Ev][E]
+  uint8_t* comp;     // [Ev][E] computing rank of (slot, expert)
+  uint8_t* local;    // [Ev][E] replica mask (diagonal when none)
+  int32_t* cc;       // [C][E] chunk counts of this rank
+  int32_t* rows;     // [D][E]
+  int32_t* seg;      // [D][E]
+  uint8_t* present;  // [D][E]
+};
+
+__host__ __device__ inline size_t layout_smem_bytes(int D, int m, int E, int T) {
+  const size_t Ev = (size_t)D * m, C = (size_t)T / PP_CHUNK;
+  return Ev * E * (4 + 1 + 1) + C * E * 4 + (size_t)D * E * (4 + 4 + 1) + 64;
+}
 
 __global__ void __launch_bounds__(kLayoutThreads)
     dispatch_layout_kernel(const int64_t* counts, const uint8_t* mask, const int32_t* chunk_counts,
@@ -44,61 +59,66 @@ __global__ void __launch_bounds__(kLayoutThreads)
                            int32_t* chunk_base, int32_t* slot_dest, pp_group* groups,
                            int32_t* num_groups, int32_t* total_rows, int32_t* seg_start,
                            int32_t* rep_slot) {
-  extern __shared__ int32_t sh[];
-  const int Ev = D * m;
-  int32_t* rows = sh;                   // [D][E]
-  int32_t* seg = rows + D * E;          // [D][E]
-  uint8_t* present = reinterpret_cast<uint8_t*>(seg + D * E);  // [D][E]
-  const int tid = threadIdx.x;
+  extern __shared__ __align__(16) uint8_t lsm[];
+  const int Ev = D * m, C = T / PP_CHUNK, tid = threadIdx.x, nt = blockDim.x;
+  LayoutSmem S;
+  uint8_t* p = lsm;
+  S.counts = reinterpret_cast<int32_t*>(p); p += (size_t)Ev * E * 4;
+  S.cc = reinterpret_cast<int32_t*>(p); p += (size_t)C * E * 4;
+  S.rows = reinterpret_cast<int32_t*>(p); p += (size_t)D * E * 4;
+  S.seg = reinterpret_cast<int32_t*>(p); p += (size_t)D * E * 4;
+  S.comp = p; p += (size_t)Ev * E;
+  S.local = p; p += (size_t)Ev * E;
+  S.present = p;
 
-  auto comp = [&](int v, int e) -> int {
-    const bool local = mask ? (mask[(size_t)v * E + e] != 0) : (v == e);
-    return local ? v / m : e / m;
-  };
-
-  // rows[r][e], present[r][e]
-  for (int cell = tid; cell < D * E; cell += blockDim.x) {
+  // phase 0: stage inputs
+  for (int i = tid; i < Ev * E; i += nt) {
+    const int v = i / E, e = i % E;
+    S.counts[i] = (int32_t)counts[i];
+    const bool loc = mask ? (mask[i] != 0) : (v == e);
+    S.local[i] = loc;
+    S.comp[i] = (uint8_t)(loc ? v / m : e / m);
+  }
+  for (int i = tid; i < C * E; i += nt) S.cc[i] = chunk_counts[i];
+  __syncthreads();
+  // phase 1: rows / presence of every (rank, expert)
+  for (int cell = tid; cell < D * E; cell += nt) {
     const int r = cell / E, e = cell % E;
-    int64_t acc = 0;
+    int acc = 0;
     bool pres = (e / m == r);
     for (int v = 0; v < Ev; ++v) {
-      const bool local = mask ? (mask[(size_t)v * E + e] != 0) : (v == e);
-      const int c = local ? v / m : e / m;
-      if (c == r) acc += counts[(size_t)v * E + e];
-      if (local && v / m == r) pres = true;
+      const int i = v * E + e;
+      if (S.comp[i] == r) acc += S.counts[i];
+      pres |= S.local[i] && (v / m == r);
     }
-    rows[cell] = (int32_t)acc;
-    present[cell] = pres;
+    S.rows[cell] = acc;
+    S.present[cell] = pres;
   }
   __syncthreads();
-  // segment starts per rank (ascending expert order)
-  for (int r = tid; r < D; r += blockDim.x) {
+  // phase 2: expert-major segments per rank (ascending expert id, 128-row padding)
+  for (int r = tid; r < D; r += nt) {
     int off = 0, nrep = 0;
     for (int e = 0; e < E; ++e) {
       const int cell = r * E + e;
-      const bool rep = present[cell] && (e / m != r);
-      if (rep_slot) rep_slot[cell] = rep ? m + nrep++ : -1;
-      if (present[cell]) {
-        seg[cell] = off;
-        off += (rows[cell] + PP_ROW_ALIGN - 1) / PP_ROW_ALIGN * PP_ROW_ALIGN;
-      } else {
-        seg[cell] = -1;
-      }
-      seg_start[cell] = seg[cell];
+      const bool pres = S.present[cell];
+      if (rep_slot) rep_slot[cell] = (pres && e / m != r) ? m + nrep++ : -1;
+      S.seg[cell] = pres ? off : -1;
+      seg_start[cell] = S.seg[cell];
+      if (pres) off += (S.rows[cell] + PP_ROW_ALIGN - 1) / PP_ROW_ALIGN * PP_ROW_ALIGN;
     }
     if (r == me) *total_rows = off;
   }
   __syncthreads();
-  // this rank's group table
+  // phase 3: this rank's group table
   if (tid == 0) {
     int g = 0, nrep = 0;
-    for (int e = 0; e < E; ++e) {
+    for (int e = 0; e < E && g < max_groups; ++e) {
       const int cell = me * E + e;
-      if (!present[cell] || g >= max_groups) continue;
+      if (!S.present[cell]) continue;
       pp_group gr;
-      gr.row_off = seg[cell];
-      gr.rows = rows[cell];
-      gr.rows_pad = (rows[cell] + PP_ROW_ALIGN - 1) / PP_ROW_ALIGN * PP_ROW_ALIGN;
+      gr.row_off = S.seg[cell];
+      gr.rows = S.rows[cell];
+      gr.rows_pad = (S.rows[cell] + PP_ROW_ALIGN - 1) / PP_ROW_ALIGN * PP_ROW_ALIGN;
       const bool home = (e / m == me);
       gr.wslot = home ? (e % m) : (m + nrep++);
       gr.expert = e;
@@ -108,21 +128,37 @@ __global__ void __launch_bounds__(kLayoutThreads)
     }
     *num_groups = g;
   }
-  // per local slot j: destination and base row for each expert, then per chunk
-  const int chunks_per_slot = (T / m) / PP_CHUNK;
-  for (int cell = tid; cell < m * E; cell += blockDim.x) {
+  // phase 4: destination + first row of each (local slot, expert), then per chunk
+  const int cps = (T / m) / PP_CHUNK;
+  for (int cell = tid; cell < m * E; cell += nt) {
     const int j = cell / E, e = cell % E;
     const int v = me * m + j;
-    const int dest = comp(v, e);
-    int64_t base = seg[dest * E + e];
+    const int dest = S.comp[v * E + e];
+    int base = S.seg[dest * E + e];
     for (int v2 = 0; v2 < v; ++v2)
-      if (comp(v2, e) == dest) base += counts[(size_t)v2 * E + e];
+      if (S.comp[v2 * E + e] == dest) base += S.counts[v2 * E + e];
     slot_dest[cell] = dest;
-    for (int c = 0; c < chunks_per_slot; ++c) {
-      const int chunk = j * chunks_per_slot + c;
-      chunk_base[(size_t)chunk * E + e] = (int32_t)base;
-      base += chunk_counts[(size_t)chunk * E + e];
+    for (int c = 0; c < cps; ++c) {
+      const int chunk = j * cps + c;
+      chunk_base[(size_t)chunk * E + e] = base;
+      base += S.cc[chunk * E + e];
     }
+  }
+}
+
+// zero rows [row_off+rows, row_off+rows_pad) of every group of this rank (warp per row)
+template <int VPL>
+__device__ __forceinline__ void zero_padding_rows(const pp_group* groups, const int32_t* num_groups,
+                                                  int d, __nv_bfloat16* buf, int warp_global,
+                                                  int nwarps, int lane) {
+  const int G = *num_groups;
+  for (int w = warp_global; w < G * PP_ROW_ALIGN; w += nwarps) {
+    const pp_group gr = groups[w / PP_ROW_ALIGN];
+    const int j = w % PP_ROW_ALIGN;
+    if (j >= gr.rows_pad - gr.rows) continue;
+    uint4* dst = reinterpret_cast<uint4*>(buf + (size_t)(gr.row_off + gr.rows + j) * d);
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) st_v4(dst + lane + 32 * i, make_uint4(0, 0, 0, 0));
   }
 }
 
@@ -132,11 +168,13 @@ __global__ void __launch_bounds__(256)
     dispatch_kernel(const __nv_bfloat16* __restrict__ x, const int32_t* __restrict__ idx,
                     const int32_t* __restrict__ rank, const int32_t* __restrict__ chunk_base,
                     const int32_t* __restrict__ slot_dest, int T, int d, int k, int m, int E,
-                    void* const* recv_ptrs, int32_t* pair_dest, int32_t* pair_row) {
+                    void* const* recv_ptrs, int32_t* pair_dest, int32_t* pair_row,
+                    const pp_group* groups, const int32_t* num_groups, __nv_bfloat16* own) {
   const int lane = threadIdx.x & 31;
   const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
   const int slot_tokens = T / m;
+  zero_padding_rows<VPL>(groups, num_groups, d, own, warp_global, nwarps, lane);
   for (int t = warp_global; t < T; t += nwarps) {
     uint4 v[VPL];
     const uint4* src = reinterpret_cast<const uint4*>(x + (size_t)t * d);
@@ -162,17 +200,7 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-// zero rows [row_off+rows, row_off+rows_pad) of every group of this rank
-__global__ void zero_padding_kernel(const pp_group* groups, const int32_t* num_groups, int d,
-                                    __nv_bfloat16* buf) {
-  const int g = blockIdx.x;
-  if (g >= *num_groups) return;
-  const pp_group gr = groups[g];
-  const size_t begin = (size_t)(gr.row_off + gr.rows) * d;
-  const size_t end = (size_t)(gr.row_off + gr.rows_pad) * d;
-  uint4* p = reinterpret_cast<uint4*>(buf);
-  for (size_t i = begin / 8 + threadIdx.x; i < end / 8; i += blockDim.x) p[i] = make_uint4(0, 0, 0, 0);
-}
+
 
 template <int VPL>
 __global__ void __launch_bounds__(256)
@@ -223,10 +251,12 @@ __global__ void __launch_bounds__(256)
     combine_bwd_kernel(const __nv_bfloat16* __restrict__ dy, void* const* out_ptrs,
                        void* const* dgrad_ptrs, const int32_t* __restrict__ pair_dest,
                        const int32_t* __restrict__ pair_row, const float* __restrict__ w, int T,
-                       int d, int k, float* dw) {
+                       int d, int k, float* dw, const pp_group* groups, const int32_t* num_groups,
+                       __nv_bfloat16* own) {
   const int lane = threadIdx.x & 31;
   const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  zero_padding_rows<VPL>(groups, num_groups, d, own, warp_global, nwarps, lane);
   for (int t = warp_global; t < T; t += nwarps) {
     float g[VPL][8];
     const uint4* src = reinterpret_cast<const uint4*>(dy + (size_t)t * d);
@@ -394,8 +424,17 @@ extern "C" int pp_dispatch_layout(const int64_t* counts, const uint8_t* mask,
   PP_CHECK_ARG(my_rank >= 0 && my_rank < D, "pp_dispatch_layout: bad rank %d", my_rank);
   PP_CHECK_ARG(T % (m * PP_CHUNK) == 0, "pp_dispatch_layout: T=%d not a multiple of m*%d", T,
                PP_CHUNK);
-  const size_t smem = (size_t)D * E * (2 * sizeof(int32_t) + 1);
-  PP_CHECK_ARG(smem <= 48 * 1024, "pp_dispatch_layout: D*E too large");
+  PP_CHECK_ARG(D <= 255, "pp_dispatch_layout: D=%d > 255", D);
+  const size_t smem = layout_smem_bytes(D, m, E, T);
+  PP_CHECK_ARG(smem <= 220 * 1024, "pp_dispatch_layout: E x E and T/128 x E staging too large");
+  static int configured[64] = {0};  // per device: largest smem attribute set so far
+  int dev = 0;
+  PP_CUDA_TRY(cudaGetDevice(&dev));
+  if (dev >= 64 || configured[dev] < (int)smem) {
+    PP_CUDA_TRY(cudaFuncSetAttribute(dispatch_layout_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     220 * 1024));
+    if (dev < 64) configured[dev] = 220 * 1024;
+  }
   dispatch_layout_kernel<<<1, kLayoutThreads, smem, as_stream(stream)>>>(
       counts, mask, chunk_counts, D, m, E, T, my_rank, max_groups, rows_capacity, chunk_base,
       slot_dest, groups, num_groups, total_rows, seg_start, rep_slot);
@@ -413,12 +452,10 @@ extern "C" int pp_dispatch(const void* x, const int32_t* idx, const int32_t* ran
                    num_groups && pair_dest && pair_row,
                "pp_dispatch: null pointer");
   cudaStream_t st = as_stream(stream);
-  zero_padding_kernel<<<max_groups, 256, 0, st>>>(groups, num_groups, d,
-                                                  reinterpret_cast<__nv_bfloat16*>(own_recv));
-  PP_LAUNCH_CHECK();
   PP_VPL_SWITCH(d, (dispatch_kernel<VPL><<<grid_for_tokens(T), 256, 0, st>>>(
                        reinterpret_cast<const __nv_bfloat16*>(x), idx, rank, chunk_base,
-                       slot_dest, T, d, k, m, E, recv_ptrs, pair_dest, pair_row)));
+                       slot_dest, T, d, k, m, E, recv_ptrs, pair_dest, pair_row, groups, num_groups,
+                       reinterpret_cast<__nv_bfloat16*>(own_recv))));
   PP_LAUNCH_CHECK();
   return PP_OK;
 }
@@ -442,12 +479,10 @@ extern "C" int pp_combine_bwd(const void* dy, void* const* out_ptrs, void* const
                    num_groups && dw,
                "pp_combine_bwd: null pointer");
   cudaStream_t st = as_stream(stream);
-  zero_padding_kernel<<<max_groups, 256, 0, st>>>(groups, num_groups, d,
-                                                  reinterpret_cast<__nv_bfloat16*>(own_dgrad));
-  PP_LAUNCH_CHECK();
   PP_VPL_SWITCH(d, (combine_bwd_kernel<VPL><<<grid_for_tokens(T), 256, 0, st>>>(
                        reinterpret_cast<const __nv_bfloat16*>(dy), out_ptrs, dgrad_ptrs,
-                       pair_dest, pair_row, w, T, d, k, dw)));
+                       pair_dest, pair_row, w, T, d, k, dw, groups, num_groups,
+                       reinterpret_cast<__nv_bfloat16*>(own_dgrad))));
   PP_LAUNCH_CHECK();
   return PP_OK;
 }

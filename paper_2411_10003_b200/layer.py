@@ -256,6 +256,7 @@ class MoELayer(torch.nn.Module):
         self.record_history = False
         self.events = {}
         self.gemm_timing = None
+        self.gemm_event_pool = None
         if D > 1:
             torch.cuda.synchronize()
             dist.barrier(group=self.group)
@@ -317,8 +318,12 @@ class MoELayer(torch.nn.Module):
     def _gemm(self, mode, a, b, c, c2=None, stream=None):
         timing = self.gemm_timing
         if timing is not None:
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
+            pool = self.gemm_event_pool
+            if pool and len(pool) >= 2:
+                e0, e1 = pool.pop(), pool.pop()
+            else:
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
             e0.record()
         _device.grouped_gemm(mode, a, b, c, c2, self.groups, self.num_groups, self.max_groups,
                              self.rows_cap, self.slots, self.d, self.f, stream=stream)
