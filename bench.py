@@ -295,6 +295,13 @@ def main() -> None:
     if world > 1:
         dist.barrier()
     launches = _lib.launch_count()
+    # ---- measured phase timeline of two extra steps (not part of the timed value)
+    layer.phase_log = []
+    for i in range(2):
+        step(xs[i % 2].detach(), dy)
+    torch.cuda.synchronize()
+    phases = layer.phase_breakdown()
+    layer.phase_log = None
     ms_total = t0.elapsed_time(t1)
     ms_tensor = torch.tensor([ms_total], dtype=torch.float64, device=dev)
     if world > 1:
@@ -357,6 +364,7 @@ def main() -> None:
             main.wait_event(ev_in[b])
             y = step(xdev[b].detach(), dydev[b])
             ev_free[b].record(main)
+            y.record_stream(back)
             keep[b] = y
             with torch.cuda.stream(back):
                 back.wait_event(ev_free[b])
@@ -427,7 +435,7 @@ def main() -> None:
                        "d_ff": f, "tokens_per_gpu": T, "parallelism": f"ep{world}",
                        "l2": "working set > L2 (activations+weights >> 126 MB), no flush",
                        "routing": "Zipf(1.2) gate bias, random bf16 tokens"},
-            "host_enqueue_ms_per_step": host_ms,
+            "host_enqueue_ms_per_step": host_ms, "phase_ms_rank0": phases,
             "roofline": roofline, "cpu_baseline": cpu_info, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk_summary, "planner": planner_info, "imbalance": imbalance,
         }

@@ -257,6 +257,8 @@ class MoELayer(torch.nn.Module):
         self.events = {}
         self.gemm_timing = None
         self.gemm_event_pool = None
+        self.phase_log = None
+        self._agg_done = None
         if D > 1:
             torch.cuda.synchronize()
             dist.barrier(group=self.group)
@@ -267,6 +269,26 @@ class MoELayer(torch.nn.Module):
 
     def _sp(self):
         return _device.stream_ptr()
+
+    def _mark(self, name: str) -> None:
+        """Measured timeline: when ``phase_log`` is a list, record a CUDA event per
+        phase boundary on the layer's stream (see ``phase_breakdown``)."""
+        if self.phase_log is not None:
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record()
+            self.phase_log.append((name, ev))
+
+    def phase_breakdown(self) -> dict:
+        """Average ms per phase over the recorded steps (phase = time since the
+        previous mark on this rank's stream)."""
+        out, steps, prev = {}, 0, None
+        for name, ev in self.phase_log or []:
+            if name == "fwd_start":
+                steps += 1
+            elif prev is not None:
+                out[name] = out.get(name, 0.0) + prev.elapsed_time(ev)
+            prev = ev
+        return {k: v / max(steps, 1) for k, v in out.items()}
 
     def _route_and_layout(self, x: torch.Tensor) -> None:
         sp = self._sp()
@@ -352,7 +374,12 @@ class MoELayer(torch.nn.Module):
         """Forward without autograd bookkeeping (x: [T, d] bf16 on this device)."""
         assert x.shape == (self.T, self.d) and x.dtype == torch.bfloat16 and x.is_contiguous()
         sp = self._sp()
+        if self._agg_done is not None:  # this forward's WGRADs will overwrite grads Agg still reads
+            torch.cuda.current_stream().wait_event(self._agg_done)
+            self._agg_done = None
+        self._mark("fwd_start")
         self._route_and_layout(x)
+        self._mark("route_layout")
         if self.world > 1 and self.mask_cur is not None:
             # K5 Trans: replicas pull this iteration's planned experts (side stream, overlaps dispatch)
             ev = torch.cuda.Event()
@@ -371,15 +398,21 @@ class MoELayer(torch.nn.Module):
                   self.E, self.xp.ptrs.data_ptr(), self.xp.local.data_ptr(), self.groups.data_ptr(),
                   self.num_groups.data_ptr(), self.max_groups, self.pair_dest.data_ptr(),
                   self.pair_row.data_ptr(), sp)
+        self._mark("dispatch")
         if trans_done is not None:
             torch.cuda.current_stream().wait_event(trans_done)
+        self._mark("trans_wait")
         self.barrier()  # every rank's rows have landed (and replicas' params, via the next barrier use)
+        self._mark("barrier1")
         self._gemm(_lib.PP_GEMM_FWD1, self.xp.local, self.w1_arena.local, self.pre, self.act)
         self._gemm(_lib.PP_GEMM_FWD2, self.act, self.w2_arena.local, self.yp.local)
+        self._mark("fwd_gemms")
         self.barrier()
+        self._mark("barrier2")
         y = torch.empty((self.T, self.d), dtype=torch.bfloat16, device=self.device)
         _lib.call("pp_combine", self.yp.ptrs.data_ptr(), self.pair_dest.data_ptr(), self.pair_row.data_ptr(),
                   self.w.data_ptr(), self.T, self.d, self.k, y.data_ptr(), sp)
+        self._mark("combine")
         self._launch_planner()
         return y
 
@@ -390,25 +423,45 @@ class MoELayer(torch.nn.Module):
                   self.dyp.local.data_ptr(), self.pair_dest.data_ptr(), self.pair_row.data_ptr(),
                   self.w.data_ptr(), self.groups.data_ptr(), self.num_groups.data_ptr(), self.max_groups,
                   self.T, self.d, self.k, self.dw.data_ptr(), sp)
+        self._mark("combine_bwd")
         self.barrier()
+        self._mark("barrier3")
         self._gemm(_lib.PP_GEMM_DGRAD2, self.dyp.local, self.w2_arena.local, self.pre, self.pre)
         self._gemm(_lib.PP_GEMM_WGRAD2, self.dyp.local, self.act, self.g2_arena.local)
         self._gemm(_lib.PP_GEMM_DGRAD1, self.pre, self.w1_arena.local, self.dxp.local)
         self._gemm(_lib.PP_GEMM_WGRAD1, self.pre, self.xp.local, self.g1_arena.local)
+        self._mark("bwd_gemms")
         self.barrier()
+        self._mark("barrier4")
         if self.world > 1 and self.mask_cur is not None:
-            _lib.call("pp_replica_agg", self.g1_arena.ptrs.data_ptr(), self.g2_arena.ptrs.data_ptr(),
-                      self.rep_slot.data_ptr(), self.world, self.E, self.m, self.rank, self.d, self.f,
-                      self.trans_ctas * 4, sp)
+            # K5 Agg on the side stream: overlaps dispatch_bwd and the gate GEMMs
+            ev = torch.cuda.Event()
+            ev.record()
+            with torch.cuda.stream(self.comm_stream):
+                self.comm_stream.wait_event(ev)
+                _lib.call("pp_replica_agg", self.g1_arena.ptrs.data_ptr(), self.g2_arena.ptrs.data_ptr(),
+                          self.rep_slot.data_ptr(), self.world, self.E, self.m, self.rank, self.d, self.f,
+                          self.trans_ctas * 4, _device.stream_ptr(self.comm_stream))
+                self._agg_done = torch.cuda.Event()
+                self._agg_done.record(self.comm_stream)
         dx = torch.empty((self.T, self.d), dtype=torch.bfloat16, device=self.device)
         _lib.call("pp_dispatch_bwd", self.dxp.ptrs.data_ptr(), self.pair_dest.data_ptr(),
                   self.pair_row.data_ptr(), self.idx.data_ptr(), self.probs.data_ptr(), self.dw.data_ptr(),
                   self.T, self.d, self.k, self.E, self.EP, dx.data_ptr(), self.dlogits.data_ptr(), sp)
+        self._mark("dispatch_bwd")
         self.wg.main_grad.zero_()
         _lib.call("pp_gate_bwd", self.dlogits.data_ptr(), self.wg.data_ptr(), x.data_ptr(), self.T, self.d,
                   self.E, self.EP, dx.data_ptr(), self.wg.main_grad.data_ptr(), sp)
+        self._mark("gate_bwd")
         self.iteration += 1
         return dx
+
+    def wait_grads(self, stream=None) -> None:
+        """Make ``stream`` (default: current) wait until the replica gradients have
+        been aggregated into the home experts' ``main_grad`` (call before the
+        optimizer reads them)."""
+        if self._agg_done is not None:
+            (stream or torch.cuda.current_stream()).wait_event(self._agg_done)
 
     def forward(self, x: torch.Tensor) -> torch.Tensor:
         return _MoEFunction.apply(x, self)
