@@ -96,6 +96,14 @@ def greedy_search(load, config: PlannerConfig, cluster, model) -> ExpertPlacemen
     return greedy_search_many([load], config, cluster, model)[0].placement
 
 
+def plan_source_iteration(iter_index: int, reuse_interval: int):
+    """Index of the iteration whose LoadMatrix feeds iteration ``iter_index``'s
+    plan under the reuse policy (None = empty placement).  The MoE layer uses the
+    same rule: after iteration i it plans for i+1 iff (i+1) % F == 0."""
+    anchor = iter_index - iter_index % reuse_interval
+    return None if anchor == 0 else anchor - 1
+
+
 def plan_for_iteration(history: Sequence, iter_index: int, config: PlannerConfig, cluster, model) -> ExpertPlacement:
     """Reuse policy (reference ``planner.py:132-156``): search at multiples of
     ``reuse_interval`` on the previous iteration's load (persistence

@@ -185,7 +185,7 @@ def main() -> None:
         from moebal import LayerCost
         costs = []
         for _ in range(L):
-            v = rng.uniform(0, 4e-3, 5)
+            v = [float(u) for u in rng.uniform(0, 4e-3, 5)]  # Python floats, as JSON configs give
             costs.append(LayerCost(v[0], v[1], 2 * v[1], v[2], v[3], 0.0, 0.0, 0.0, 0.0))
         plan_time = float(rng.uniform(0, 1e-3))
         tl = build_iteration_timeline(costs, plan_time, mo, iteration=i)

@@ -1,0 +1,181 @@
+"""Host-side API mirror vs the reference goldens (CPU only): value types and
+their validation, the scalar cost model, the Algorithm-2 timeline model, metrics."""
+
+import json
+import math
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import paper_2411_10003_b200 as pp
+from paper_2411_10003_b200 import perf_model as pm
+from paper_2411_10003_b200 import planner as pl
+from paper_2411_10003_b200 import scheduler as sc
+
+G = Path(__file__).resolve().parent / "golden"
+
+
+class TestValidation:
+    def test_cluster(self):
+        for args in ((1, 1e9, 1e6), (4, 0, 1e6), (4, 1e9, -1)):
+            with pytest.raises(pp.ValidationError):
+                pp.ClusterSpec(*args)
+
+    def test_model(self):
+        for args, kw in (((4, 1, 5, 1, 1, 1), {}), ((4, 0, 1, 1, 1, 1), {}), ((4, 1, 1, 0, 1, 1), {}),
+                         ((4, 1, 1, 1, 1, 1), {"fnec_time": -0.1})):
+            with pytest.raises(pp.ValidationError):
+                pp.ModelSpec(*args, **kw)
+
+    def test_load_matrix(self):
+        with pytest.raises(pp.ValidationError):
+            pp.LoadMatrix([[1, -1], [0, 2]])
+        with pytest.raises(pp.ValidationError):
+            pp.LoadMatrix([[1, 2], [0, 2]])
+        with pytest.raises(pp.ValidationError):
+            pp.LoadMatrix([1, 2, 3])
+        lm = pp.LoadMatrix([[3, 0, 0], [2, 1, 0], [0, 1, 2]])
+        assert lm.total() == 9 and lm.expert_totals().tolist() == [5, 2, 2]
+        assert not lm.counts.flags.writeable
+        with pytest.raises(AttributeError):
+            lm.counts = None
+
+    def test_placement(self):
+        with pytest.raises(pp.ValidationError):
+            pp.ExpertPlacement(2, 3)
+        with pytest.raises(pp.ValidationError):
+            pp.ExpertPlacement(3, 3, (0, 0), (frozenset({1}), frozenset({2})))
+        with pytest.raises(pp.ValidationError):
+            pp.ExpertPlacement(3, 3, (0,), (frozenset({0}),))  # home excluded
+        with pytest.raises(pp.ValidationError):
+            pp.ExpertPlacement(3, 3, (0, 1), (frozenset({1}), frozenset()))
+        p = pp.ExpertPlacement(3, 3, (0,), (frozenset({2}),))
+        assert p.replicas(0) == frozenset({0, 1}) and p.replicas(1) == frozenset({1}) and p.n == 1
+
+    def test_replica_mask_golden_and_from_mask(self):
+        for c in json.loads((G / "derive_cases.json").read_text()):
+            D, E = np.array(c["counts"]).shape
+            p = pp.ExpertPlacement(D, E, tuple(c["selected"]), tuple(frozenset(x) for x in c["excluded"]))
+            assert p.replica_mask().astype(int).tolist() == c["mask"]
+            if D == E:
+                assert pp.ExpertPlacement.from_mask(p.selected, p.replica_mask()) == p
+
+
+def test_cost_model_golden():
+    for c in json.loads((G / "cost_cases.json").read_text()):
+        cl = pp.ClusterSpec(*c["cluster"])
+        mo = pp.ModelSpec(*c["model"][:6], fnec_time=c["model"][6], bnec_time=c["model"][7])
+        loads = pp.DeviceLoads(np.array(c["H"]), np.array(c["R"]))
+        got = pm.layer_cost_unscheduled(loads, c["s"], c["n"], cl, mo)
+        for k, v in c["cost"].items():
+            assert float(getattr(got, k)).hex() == v, k
+    cl = pp.ClusterSpec(3, 1e9, 1000.0)
+    mo = pp.ModelSpec(3, 1, 1, 1e6, 1e5, 1e5)
+    with pytest.raises(pp.ValidationError):
+        pm.t_trans(0, 3, cl, mo)
+    with pytest.raises(pp.ValidationError):
+        pm.t_agg(4, 0, cl, mo)
+
+
+def test_timeline_golden():
+    for c in json.loads((G / "timeline_cases.json").read_text()):
+        mo = pp.ModelSpec(4, c["L"], 1, 1.0, 1.0, 1.0, fnec_time=c["fnec"], bnec_time=c["bnec"])
+        costs = [pm.LayerCost(a, fe, be, tr, ag, 0.0, 0.0, 0.0, 0.0) for a, fe, be, tr, ag in c["costs"]]
+        tl = pp.build_iteration_timeline(costs, c["plan_time"], mo, iteration=c["iteration"])
+        ts = pp.build_serial_timeline(costs, c["plan_time"], mo, iteration=c["iteration"])
+        assert tl.to_json_obj() == c["overlapped"]
+        assert ts.to_json_obj() == c["serial"]
+        assert tl.phase_totals() == c["phase"]
+        assert tl.exposed_comm_seconds() == c["exposed_comm"]
+
+
+def test_partitions():
+    assert pp.partition_trans(3.0, 1.0, 1.0) == (2.0, 1.0)
+    assert pp.partition_trans(0.5, 1.0, 1.0) == (0.0, 0.5)
+    assert pp.partition_agg(3.0, 1.0, 1.0) == (1.0, 2.0)
+    with pytest.raises(pp.ValidationError):
+        pp.partition_trans(-1.0, 0.0, 0.0)
+    b1, b2 = sc.trans_byte_split(1000, 3.0, 1.0, 1.0)
+    assert (b1, b2) == (667, 333)
+
+
+def test_timeline_errors():
+    mo = pp.ModelSpec(4, 2, 1, 1.0, 1.0, 1.0)
+    c = pm.LayerCost(0, 0, 0, 0, 0, 0, 0, 0, 0)
+    with pytest.raises(pp.ValidationError):
+        pp.build_iteration_timeline([c], 0.0, mo)
+    with pytest.raises(pp.ValidationError):
+        pp.build_iteration_timeline([c, c], -1.0, mo)
+
+
+def test_metrics_golden():
+    for c in json.loads((G / "metric_cases.json").read_text()):
+        assert pp.balance_degree(c["a"]) == c["sigma_a"]
+        a = pp.DeviceLoads(np.array(c["a"]), np.zeros(len(c["a"]), dtype=int))
+        b = pp.DeviceLoads(np.array(c["b"]), np.zeros(len(c["b"]), dtype=int))
+        assert repr(pp.rb_ratio(a, b)) == c["rb"]
+    with pytest.raises(pp.ValidationError):
+        pp.balance_degree([])
+
+
+def test_planner_host_helpers():
+    assert pp.is_balanced([5, 2, 2], 9, 3, 0.5) is False
+    assert pp.is_balanced([3, 3, 3], 9, 3, 1e-9) is True
+    assert pp.is_balanced([4, 3, 2], 9, 3, 1.0) is True
+    with pytest.raises(pp.ValidationError):
+        pp.is_balanced([], 9, 3, 1.0)
+    fig8 = pp.LoadMatrix([[3, 0, 0], [2, 1, 0], [0, 1, 2]])
+    assert pl.bottom_devices(fig8, 0, 1) == frozenset({2})
+    assert pl.bottom_devices(pp.LoadMatrix([[0, 3], [0, 3]]), 0, 1) == frozenset({1})
+    assert pl.bottom_devices(pp.LoadMatrix([[2, 1, 0], [1, 2, 0], [1, 0, 2]]), 2, 1) == frozenset({0})
+    for kw in ({"n": -1}, {"alpha": 0}, {"reuse_interval": 0}):
+        with pytest.raises(pp.ValidationError):
+            pp.PlannerConfig(**kw)
+    with pytest.raises(pp.ValidationError):
+        pp.plan_for_iteration([], -1, pp.PlannerConfig(), pp.ClusterSpec(3, 1e9, 1e3), pp.ModelSpec(3, 1, 1, 1, 1, 1))
+    # iteration 0 (and the whole first interval) never touches the device
+    cfg = pp.PlannerConfig(reuse_interval=3)
+    cl, mo = pp.ClusterSpec(3, 1e9, 1e3), pp.ModelSpec(3, 1, 1, 1, 1, 1)
+    for j in range(3):
+        assert pp.plan_for_iteration([], j, cfg, cl, mo) == pp.ExpertPlacement.empty(3, 3)
+
+
+def test_greedy_validation_happens_on_host():
+    """Precondition errors are raised with the reference's types before any device work."""
+    cl = pp.ClusterSpec(3, 1e9, 1e3)
+    mo = pp.ModelSpec(3, 1, 1, 1e6, 1e5, 1e5)
+    with pytest.raises(pp.ValidationError):
+        pp.greedy_search(pp.LoadMatrix([[1, 2], [2, 1], [0, 3]]), pp.PlannerConfig(), cl, mo)
+    with pytest.raises(pp.DimensionMismatchError):
+        pp.greedy_search(pp.LoadMatrix([[1, 2], [2, 1]]), pp.PlannerConfig(), cl, mo)
+    with pytest.raises(pp.ValidationError):
+        pp.greedy_search(pp.LoadMatrix([[3, 0, 0], [2, 1, 0], [0, 1, 2]]), pp.PlannerConfig(n=3), cl, mo)
+    with pytest.raises(pp.DimensionMismatchError):
+        pp.derive_loads(pp.LoadMatrix([[1, 2], [2, 1]]), pp.ExpertPlacement.empty(3, 3))
+
+
+def test_accepts_reference_objects():
+    from conftest import import_reference
+
+    ref = import_reference()
+    lm = ref.LoadMatrix([[3, 0, 0], [2, 1, 0], [0, 1, 2]])
+    from paper_2411_10003_b200.core import as_counts
+
+    assert as_counts(lm).tolist() == [[3, 0, 0], [2, 1, 0], [0, 1, 2]]
+    rc = ref.ClusterSpec(3, 1e9, 1000.0)
+    rm = ref.ModelSpec(3, 1, 1, 1e6, 1e5, 1e5)
+    assert pm.layer_cost_unscheduled(ref.DeviceLoads([5, 2, 2], [2, 1, 0]), 0, 0, rc, rm).total_unscheduled == \
+        ref.layer_cost_unscheduled(ref.DeviceLoads([5, 2, 2], [2, 1, 0]), 0, 0, rc, rm).total_unscheduled
+
+
+def test_no_cpu_fallback_without_gpu():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(RuntimeError):
+        pp.greedy_search(pp.LoadMatrix([[3, 0, 0], [2, 1, 0], [0, 1, 2]]), pp.PlannerConfig(),
+                         pp.ClusterSpec(3, 1e9, 1e3), pp.ModelSpec(3, 1, 1, 1e6, 1e5, 1e5))
+    with pytest.raises(RuntimeError):
+        pp.MoELayer(256, 512, 16, 2, tokens=2048)
