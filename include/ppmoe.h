@@ -204,6 +204,18 @@ int pp_replica_agg(void* const* g1_ptrs, void* const* g2_ptrs, const int32_t* re
                    int32_t D, int32_t E, int32_t m, int32_t my_rank, int32_t d_model,
                    int32_t d_ff, int32_t max_ctas, void* stream);
 
+/* Copy-engine Trans/Agg: one cudaMemcpyAsync per (dst, src, bytes) triple of
+ * the HOST arrays (peer pointers via IPC: the copy runs on the copy engines over
+ * NVLink and takes no SMs, so it overlaps the tensor-core GEMMs). */
+int pp_copy_batch(void* const* dst, const void* const* src, const uint64_t* bytes, int32_t n,
+                  void* stream);
+
+/* Agg reduce step after the copy-engine pulls: home slot j of g1/g2 (fp32
+ * [m][f][d], [m][d][f]) += staging entries [ranges[j], ranges[j+1]) in order
+ * (entry i = g1 part then g2 part).  ranges: device int32 [m+1]. */
+int pp_agg_accumulate(float* g1_home, float* g2_home, const float* staging, const int32_t* ranges,
+                      int32_t m, int32_t d_model, int32_t d_ff, void* stream);
+
 /* ---- peer memory (CUDA IPC) + device barrier ----------------------------- */
 /* Library-owned cudaMalloc allocations (IPC-exportable as a whole). */
 int pp_device_alloc(uint64_t bytes, void** dev_ptr);

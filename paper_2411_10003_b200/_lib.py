@@ -74,6 +74,8 @@ SIGNATURES = {
     "pp_grouped_gemm": [I, P, P, P, P, P, P, I, I, I, I, I, I, P],
     "pp_replica_trans": [P, P, P, P, I, I, I, I, I, I, P],
     "pp_replica_agg": [P, P, P, I, I, I, I, I, I, I, P],
+    "pp_copy_batch": [P, P, P, I, P],
+    "pp_agg_accumulate": [P, P, P, P, I, I, I, P],
     "pp_device_alloc": [c_uint64, POINTER(c_void_p)],
     "pp_device_free": [P],
     "pp_ipc_export": [P, POINTER(c_uint8)],
@@ -129,7 +131,7 @@ KERNELS_PER_CALL = {
     "pp_plan_greedy": 1, "pp_derive_loads": 1, "pp_route_topk": 1, "pp_slot_histogram": 1,
     "pp_dispatch_layout": 1, "pp_dispatch": 1, "pp_combine": 1, "pp_combine_bwd": 1,
     "pp_dispatch_bwd": 1, "pp_gate_bwd": 2, "pp_grouped_gemm": 1, "pp_replica_trans": 1,
-    "pp_replica_agg": 1, "pp_peer_barrier": 1,
+    "pp_replica_agg": 1, "pp_peer_barrier": 1, "pp_agg_accumulate": 1,
 }
 _launches = [0]
 

@@ -173,3 +173,51 @@ extern "C" int pp_replica_agg(void* const* g1_ptrs, void* const* g2_ptrs, const 
   PP_LAUNCH_CHECK();
   return PP_OK;
 }
+
+// ---- copy-engine Trans/Agg helpers ----------------------------------------------
+namespace pp {
+// home grad slot j += sum of staging entries [ranges[j], ranges[j+1]) (rank order);
+// staging entry i = [g1 part (f*d) | g2 part (d*f)] fp32
+__global__ void agg_accumulate_kernel(float* g1, float* g2, const float* staging,
+                                      const int32_t* ranges, int m, size_t fd) {
+  const size_t vec = fd / 4;
+  const size_t total = (size_t)m * 2 * vec;
+  for (size_t x = (size_t)blockIdx.x * blockDim.x + threadIdx.x; x < total;
+       x += (size_t)gridDim.x * blockDim.x) {
+    const int j = (int)(x / (2 * vec));
+    const size_t rem = x % (2 * vec);
+    const int half = rem >= vec;
+    const size_t v = rem - half * vec;
+    const int b = ranges[j], e = ranges[j + 1];
+    if (b == e) continue;
+    float4* dst = reinterpret_cast<float4*>(half ? g2 : g1) + (size_t)j * vec + v;
+    float4 acc = *dst;
+    for (int i = b; i < e; ++i) {
+      const float4 s = *(reinterpret_cast<const float4*>(staging) + ((size_t)i * 2 + half) * vec + v);
+      acc.x += s.x;
+      acc.y += s.y;
+      acc.z += s.z;
+      acc.w += s.w;
+    }
+    *dst = acc;
+  }
+}
+}  // namespace pp
+
+extern "C" int pp_copy_batch(void* const* dst, const void* const* src, const uint64_t* bytes,
+                             int32_t n, void* stream) {
+  PP_CHECK_ARG(n >= 0 && (n == 0 || (dst && src && bytes)), "pp_copy_batch: bad arguments");
+  for (int i = 0; i < n; ++i)
+    PP_CUDA_TRY(cudaMemcpyAsync(dst[i], src[i], bytes[i], cudaMemcpyDeviceToDevice, as_stream(stream)));
+  return PP_OK;
+}
+
+extern "C" int pp_agg_accumulate(float* g1_home, float* g2_home, const float* staging,
+                                 const int32_t* ranges, int32_t m, int32_t d_model, int32_t d_ff,
+                                 void* stream) {
+  PP_CHECK_ARG(g1_home && g2_home && staging && ranges && m >= 1, "pp_agg_accumulate: bad arguments");
+  agg_accumulate_kernel<<<4 * 148, 256, 0, as_stream(stream)>>>(g1_home, g2_home, staging, ranges, m,
+                                                                (size_t)d_model * d_ff);
+  PP_LAUNCH_CHECK();
+  return PP_OK;
+}

@@ -95,6 +95,7 @@ class PeerBuffer:
                 _lib.check(lib.pp_ipc_import(hh, ctypes.byref(q)), "pp_ipc_import")
                 self._imported.append(q.value)
                 ptrs.append(q.value)
+        self.ptr_list = list(ptrs)  # host copy of the table (copy-engine Trans/Agg)
         self.ptrs = torch.tensor(ptrs, dtype=torch.int64, device=device)
 
     def close(self) -> None:
@@ -159,7 +160,7 @@ class MoELayer(torch.nn.Module):
     def __init__(self, d_model: int, d_ff: int, num_experts: int, top_k: int, tokens: int,
                  group=None, planner: PlannerConfig | None = None, cluster=None, model=None,
                  capacity_rows: int | None = None, max_replicas: int | None = None,
-                 seed: int = 0, device=None, trans_ctas: int = 16) -> None:
+                 seed: int = 0, device=None, trans_ctas: int = 16, replica_engine: str = "copy") -> None:
         super().__init__()
         if not torch.cuda.is_available():
             raise RuntimeError("MoELayer needs a CUDA device (B200); there is no CPU path")
@@ -245,12 +246,27 @@ class MoELayer(torch.nn.Module):
         self.plan_enabled = D > 1
         self.mask_cur = None  # None = vanilla EP for iteration 0
         self._plan_out = _device.PlanBuffers(1, E, dev) if self.plan_enabled else None
-        self._plan_next_ready = None
         self._cm = _device.cost_model(self.cluster, self.model, E) if self.plan_enabled else None
         self._pcfg = _device.planner_cfg(self.planner_cfg)
         self.plan_stream = torch.cuda.Stream(device=dev) if self.plan_enabled else None
         self.comm_stream = torch.cuda.Stream(device=dev) if D > 1 else None
         self.trans_ctas = trans_ctas
+        if replica_engine not in ("copy", "sm"):
+            raise ValidationError(f"replica_engine must be 'copy' or 'sm', got {replica_engine!r}")
+        # 'copy': Trans/Agg pulls run on the copy engines (cudaMemcpyAsync over NVLink,
+        # no SMs taken from the GEMMs); 'sm': device-driven pull kernels (no host
+        # knowledge of the plan needed)
+        self.replica_engine = replica_engine
+        self._plan_pending = None
+        self._mask_host = torch.zeros((E, E), dtype=torch.uint8).pin_memory() if D > 1 else None
+        self.mask_cur_host = None
+        self._trans_list = []     # (dst, src, bytes) of this iteration's Trans
+        self._agg_list = []       # (dst, src, bytes) pulls of replica grads into staging
+        self._agg_ranges = None   # device int32 [m+1]
+        self._agg_staging = None
+        self._trans_done = None
+        self._trans_issued = True
+        self.replica_experts = []  # replica experts held by this rank under the current plan
         self.barrier = _Barrier(self.group, dev)
         self.history = []  # host copies of LoadMatrix per iteration (optional, record_history)
         self.record_history = False
@@ -301,12 +317,6 @@ class MoELayer(torch.nn.Module):
         if self.world > 1:
             mine = self.counts[self.rank * m: (self.rank + 1) * m].clone()
             dist.all_gather_into_tensor(self.counts, mine, group=self.group)
-        # plan for this iteration (computed during the previous one on the side stream)
-        if self._plan_next_ready is not None:
-            torch.cuda.current_stream().wait_event(self._plan_next_ready)
-            self._plan_mask_cur.record_stream(torch.cuda.current_stream())
-            self.mask_cur = self._plan_mask_cur
-            self._plan_next_ready = None
         mask_ptr = self.mask_cur.data_ptr() if self.mask_cur is not None else None
         _lib.call("pp_dispatch_layout", self.counts.data_ptr(), mask_ptr, self.chunk_counts.data_ptr(),
                   self.world, m, E, T, self.rank, self.max_groups, self.rows_cap,
@@ -318,7 +328,9 @@ class MoELayer(torch.nn.Module):
 
     def _launch_planner(self) -> None:
         """plan_for_iteration rule: iteration j+1 searches on iteration j's load
-        when (j+1) % reuse_interval == 0, otherwise it keeps the current plan."""
+        when (j+1) % reuse_interval == 0, otherwise it keeps the current plan.
+        The search runs on a side stream; its mask is also copied to pinned host
+        memory so the copy-engine Trans of j+1 can be issued without a stall."""
         if not self.plan_enabled:
             return
         nxt = self.iteration + 1
@@ -332,10 +344,119 @@ class MoELayer(torch.nn.Module):
             snapshot.record_stream(self.plan_stream)
             _device.launch_plan(snapshot.view(1, self.E, self.E), self._plan_out, self._cm, self._pcfg,
                                 self.plan_stream)
-            self._plan_mask_cur = self._plan_out.mask[0].clone()
+            mask_dev = self._plan_out.mask[0].clone()
+            self._mask_host.copy_(mask_dev, non_blocking=True)
             done = torch.cuda.Event()
             done.record(self.plan_stream)
-        self._plan_next_ready = done
+        self._plan_pending = (done, mask_dev)
+
+    def begin_iteration(self) -> None:
+        """Adopt the plan computed during the previous iteration and derive this
+        rank's replica set, Trans copies and Agg sources from it (same rule as the
+        device layout: replica experts in ascending id get slots m, m+1, ...)."""
+        if self._plan_pending is None:
+            return
+        done, mask_dev = self._plan_pending
+        self._plan_pending = None
+        done.synchronize()  # ~100 us planner launched one iteration ago: normally long done
+        cur = torch.cuda.current_stream()
+        cur.wait_event(done)
+        mask_dev.record_stream(cur)
+        self.mask_cur = mask_dev
+        mh = self._mask_host.numpy().astype(bool)
+        self.mask_cur_host = mh.copy()
+        self._derive_replicas(mh)
+        self._trans_issued = False
+
+    def _derive_replicas(self, mh: np.ndarray) -> None:
+        D, m, E, me = self.world, self.m, self.E, self.rank
+        fd = self.d * self.f
+        reps = [[e for e in range(E) if e // m != r and mh[r * m:(r + 1) * m, e].any()] for r in range(D)]
+        if any(len(r) > self.max_replicas for r in reps):
+            raise ValidationError("plan needs more replica slots than max_replicas")
+        self.replica_experts = reps[me]
+        w1, w2 = self.w1_arena.ptr_list, self.w2_arena.ptr_list
+        self._trans_list = []
+        for i, e in enumerate(reps[me]):
+            home, j = e // m, e % m
+            self._trans_list.append((w1[me] + (m + i) * fd * 2, w1[home] + j * fd * 2, fd * 2))
+            self._trans_list.append((w2[me] + (m + i) * fd * 2, w2[home] + j * fd * 2, fd * 2))
+        # Agg sources: for each home slot j, replicas of expert me*m+j on other ranks (rank order)
+        g1, g2 = self.g1_arena.ptr_list, self.g2_arena.ptr_list
+        srcs, ranges = [], [0]
+        for j in range(m):
+            e = me * m + j
+            for r in range(D):
+                if r != me and e in reps[r]:
+                    slot = m + reps[r].index(e)
+                    srcs.append((g1[r] + slot * fd * 4, g2[r] + slot * fd * 4))
+            ranges.append(len(srcs))
+        self._agg_list = []
+        if srcs:
+            need = len(srcs) * 2 * fd
+            if self._agg_staging is None or self._agg_staging.numel() < need:
+                self._agg_staging = torch.empty(need, dtype=torch.float32, device=self.device)
+            base = self._agg_staging.data_ptr()
+            for i, (s1, s2) in enumerate(srcs):
+                self._agg_list.append((base + (2 * i) * fd * 4, s1, fd * 4))
+                self._agg_list.append((base + (2 * i + 1) * fd * 4, s2, fd * 4))
+        self._agg_ranges = torch.tensor(ranges, dtype=torch.int32).to(self.device, non_blocking=True)
+
+    @staticmethod
+    def _copy_batch(items, stream) -> None:
+        n = len(items)
+        if n == 0:
+            return
+        dst = (ctypes.c_void_p * n)(*[t[0] for t in items])
+        src = (ctypes.c_void_p * n)(*[t[1] for t in items])
+        nb = (ctypes.c_uint64 * n)(*[t[2] for t in items])
+        _lib.call("pp_copy_batch", dst, src, nb, n, _device.stream_ptr(stream))
+
+    def issue_trans(self):
+        """K5 Trans for this iteration's plan on the side stream (once per iteration).
+        Ordered after everything already on the current stream (e.g. an optimizer
+        step); returns the completion event (None if nothing to move)."""
+        if self._trans_issued:
+            return self._trans_done
+        self._trans_issued = True
+        self._trans_done = None
+        if self.world == 1 or self.mask_cur is None or not self.replica_experts:
+            return None
+        ev = torch.cuda.Event()
+        ev.record()
+        with torch.cuda.stream(self.comm_stream):
+            self.comm_stream.wait_event(ev)
+            if self.replica_engine == "copy":
+                self._copy_batch(self._trans_list, self.comm_stream)
+            else:
+                _lib.call("pp_replica_trans", self.w1_arena.ptrs.data_ptr(), self.w2_arena.ptrs.data_ptr(),
+                          self.groups.data_ptr(), self.num_groups.data_ptr(), self.max_groups, self.rank,
+                          self.m, self.d, self.f, self.trans_ctas, _device.stream_ptr(self.comm_stream))
+            self._trans_done = torch.cuda.Event()
+            self._trans_done.record(self.comm_stream)
+        return self._trans_done
+
+    def _issue_agg(self) -> None:
+        """K5 Agg: pull the replicas' grads of this rank's home experts and add
+        them (rank order) into main_grad, on the side stream."""
+        if self.world == 1 or self.mask_cur is None:
+            return
+        ev = torch.cuda.Event()
+        ev.record()
+        with torch.cuda.stream(self.comm_stream):
+            self.comm_stream.wait_event(ev)
+            if self.replica_engine == "copy":
+                if self._agg_list:
+                    self._copy_batch(self._agg_list, self.comm_stream)
+                    _lib.call("pp_agg_accumulate", self.g1_arena.local.data_ptr(), self.g2_arena.local.data_ptr(),
+                              self._agg_staging.data_ptr(), self._agg_ranges.data_ptr(), self.m, self.d, self.f,
+                              _device.stream_ptr(self.comm_stream))
+            else:
+                _lib.call("pp_replica_agg", self.g1_arena.ptrs.data_ptr(), self.g2_arena.ptrs.data_ptr(),
+                          self.rep_slot.data_ptr(), self.world, self.E, self.m, self.rank, self.d, self.f,
+                          self.trans_ctas * 4, _device.stream_ptr(self.comm_stream))
+            self._agg_done = torch.cuda.Event()
+            self._agg_done.record(self.comm_stream)
 
     def _gemm(self, mode, a, b, c, c2=None, stream=None):
         timing = self.gemm_timing
@@ -378,21 +499,13 @@ class MoELayer(torch.nn.Module):
             torch.cuda.current_stream().wait_event(self._agg_done)
             self._agg_done = None
         self._mark("fwd_start")
+        self.begin_iteration()
+        if self.replica_engine == "copy":  # host-derived copies: start before routing
+            trans_done = self.issue_trans()  # no-op if a scheduler already issued it earlier
         self._route_and_layout(x)
+        if self.replica_engine == "sm":  # device-driven pulls read this iteration's group table
+            trans_done = self.issue_trans()
         self._mark("route_layout")
-        if self.world > 1 and self.mask_cur is not None:
-            # K5 Trans: replicas pull this iteration's planned experts (side stream, overlaps dispatch)
-            ev = torch.cuda.Event()
-            ev.record()
-            with torch.cuda.stream(self.comm_stream):
-                self.comm_stream.wait_event(ev)
-                _lib.call("pp_replica_trans", self.w1_arena.ptrs.data_ptr(), self.w2_arena.ptrs.data_ptr(),
-                          self.groups.data_ptr(), self.num_groups.data_ptr(), self.max_groups, self.rank,
-                          self.m, self.d, self.f, self.trans_ctas, _device.stream_ptr(self.comm_stream))
-                trans_done = torch.cuda.Event()
-                trans_done.record(self.comm_stream)
-        else:
-            trans_done = None
         _lib.call("pp_dispatch", x.data_ptr(), self.idx.data_ptr(), self.rank_in_chunk.data_ptr(),
                   self.chunk_base.data_ptr(), self.slot_dest.data_ptr(), self.T, self.d, self.k, self.m,
                   self.E, self.xp.ptrs.data_ptr(), self.xp.local.data_ptr(), self.groups.data_ptr(),
@@ -433,17 +546,7 @@ class MoELayer(torch.nn.Module):
         self._mark("bwd_gemms")
         self.barrier()
         self._mark("barrier4")
-        if self.world > 1 and self.mask_cur is not None:
-            # K5 Agg on the side stream: overlaps dispatch_bwd and the gate GEMMs
-            ev = torch.cuda.Event()
-            ev.record()
-            with torch.cuda.stream(self.comm_stream):
-                self.comm_stream.wait_event(ev)
-                _lib.call("pp_replica_agg", self.g1_arena.ptrs.data_ptr(), self.g2_arena.ptrs.data_ptr(),
-                          self.rep_slot.data_ptr(), self.world, self.E, self.m, self.rank, self.d, self.f,
-                          self.trans_ctas * 4, _device.stream_ptr(self.comm_stream))
-                self._agg_done = torch.cuda.Event()
-                self._agg_done.record(self.comm_stream)
+        self._issue_agg()  # K5 Agg on the side stream: overlaps dispatch_bwd and the gate GEMMs
         dx = torch.empty((self.T, self.d), dtype=torch.bfloat16, device=self.device)
         _lib.call("pp_dispatch_bwd", self.dxp.ptrs.data_ptr(), self.pair_dest.data_ptr(),
                   self.pair_row.data_ptr(), self.idx.data_ptr(), self.probs.data_ptr(), self.dw.data_ptr(),

@@ -37,7 +37,8 @@ def main():
     cl = pp.ClusterSpec(E, 1e11, 1e6)  # cheap transfers: the planner replicates
     mo = pp.ModelSpec(E, 1, k, 2 * d, 1e3, 1e3)
     layer = pp.MoELayer(d, f, E, k, tokens=T, group=dist.group.WORLD,
-                        planner=pp.PlannerConfig(n=1, alpha=0.5), cluster=cl, model=mo, seed=0)
+                        planner=pp.PlannerConfig(n=1, alpha=0.5), cluster=cl, model=mo, seed=0,
+                        replica_engine=os.environ.get("PP_ENGINE", "copy"))
     _, wg = M.exact_inputs(16, d, E, seed=99)
     bias = torch.round(torch.log(torch.tensor([1.0 / (i + 1) ** 1.2 for i in range(E)])) * 4) / 4
     with torch.no_grad():
