@@ -225,6 +225,7 @@ def main() -> None:
     ap.add_argument("--config", default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-only", action="store_true", help="short run for ncu (no CPU legs)")
+    ap.add_argument("--eager", action="store_true", help="no CUDA graph for the N == 1 timed region")
     args = ap.parse_args()
     world_env = int(os.environ.get("WORLD_SIZE", "1"))
     cfg_name = args.config or ("cfg2" if max(args.gpus, world_env) == 1 else "cfg3")
@@ -270,12 +271,21 @@ def main() -> None:
     if world > 1:
         dist.barrier()
 
-    # ---- timed region (device events), GEMM launches timed on their stream
-    layer.gemm_timing = []
-    layer.gemm_event_pool = [torch.cuda.Event(enable_timing=True) for _ in range(2 * 8 * args.steps)]
-    _lib.reset_launch_count()
+    # ---- step function: CUDA-graph replay of fwd+bwd at N == 1 (host cost ~ one
+    # graph launch per step), eager stream-ordered calls at N > 1
+    use_graph = world == 1 and not args.eager
     xs = [x.detach().clone() for _ in range(2)]
+    if use_graph:
+        graphs = [layer.make_graphed_step(xs[b], dy.clone()) for b in range(2)]
+        run_step = lambda i: graphs[i % 2]()  # noqa: E731
+    else:
+        run_step = lambda i: step(xs[i % 2].detach(), dy)  # noqa: E731
+    for i in range(2):
+        run_step(i)
     torch.cuda.synchronize()
+
+    # ---- timed region (device events on the launching stream, max over ranks)
+    _lib.reset_launch_count()
     clk = ClockSampler(dev).start()
     time.sleep(0.1)
     if world > 1:
@@ -287,27 +297,35 @@ def main() -> None:
     t0.record()
     h0 = time.perf_counter()
     for i in range(args.steps):
-        step(xs[i % 2].detach(), dy)
+        run_step(i)
     host_ms = (time.perf_counter() - h0) * 1e3 / args.steps
     t1.record()
     torch.cuda.synchronize()
     clk.mark(w0, time.perf_counter())
     if world > 1:
         dist.barrier()
-    launches = _lib.launch_count()
-    # ---- measured phase timeline of two extra steps (not part of the timed value)
-    layer.phase_log = []
-    for i in range(2):
-        step(xs[i % 2].detach(), dy)
-    torch.cuda.synchronize()
-    phases = layer.phase_breakdown()
-    layer.phase_log = None
     ms_total = t0.elapsed_time(t1)
     ms_tensor = torch.tensor([ms_total], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(ms_tensor, op=dist.ReduceOp.MAX)
     ms_max = float(ms_tensor.item())
     value = world * T * args.steps / (ms_max / 1e3)
+
+    # ---- instrumented eager pass of the same K steps: per-GEMM CUDA events on the
+    # launching stream (graph replays cannot carry timing events) + phase timeline
+    _lib.reset_launch_count()
+    layer.gemm_timing = []
+    layer.gemm_event_pool = [torch.cuda.Event(enable_timing=True) for _ in range(2 * 8 * args.steps)]
+    for i in range(args.steps):
+        step(xs[i % 2].detach(), dy)
+    torch.cuda.synchronize()
+    launches = _lib.launch_count()  # kernels of ours per K steps (same kernels the graph replays)
+    layer.phase_log = []
+    for i in range(2):
+        step(xs[i % 2].detach(), dy)
+    torch.cuda.synchronize()
+    phases = layer.phase_breakdown()
+    layer.phase_log = None
 
     # ---- roofline of the grouped tcgen05 GEMM family (dominant kernel)
     gemm = layer.collect_gemm_timing()
@@ -331,8 +349,12 @@ def main() -> None:
         xh = [x.detach().cpu().pin_memory() for _ in range(2)]
         dyh = [dy.detach().cpu().pin_memory() for _ in range(2)]
         yh = [torch.empty((T, d), dtype=torch.bfloat16).pin_memory() for _ in range(2)]
-        xdev = [torch.empty_like(x) for _ in range(2)]
-        dydev = [torch.empty_like(dy) for _ in range(2)]
+        if use_graph:  # the graphed steps' static buffers receive the H2D copies
+            xdev = [g.x for g in graphs]
+            dydev = [g.dy for g in graphs]
+        else:
+            xdev = [torch.empty_like(x) for _ in range(2)]
+            dydev = [torch.empty_like(dy) for _ in range(2)]
         copy = torch.cuda.Stream(device=dev)   # H2D engine
         back = torch.cuda.Stream(device=dev)   # D2H engine (opposite direction, runs concurrently)
         main = torch.cuda.current_stream()
@@ -362,9 +384,13 @@ def main() -> None:
             if i + 1 < args.steps:
                 h2d(i + 1)
             main.wait_event(ev_in[b])
-            y = step(xdev[b].detach(), dydev[b])
+            if use_graph:
+                y, _ = graphs[b]()
+            else:
+                y = step(xdev[b].detach(), dydev[b])
             ev_free[b].record(main)
-            y.record_stream(back)
+            if not use_graph:
+                y.record_stream(back)
             keep[b] = y
             with torch.cuda.stream(back):
                 back.wait_event(ev_free[b])
@@ -380,8 +406,9 @@ def main() -> None:
             dist.all_reduce(em, op=dist.ReduceOp.MAX)
         e2e = {"value": world * T * args.steps / (float(em.item()) / 1e3), "unit": "tokens/s",
                "h2d_bytes_per_step": 2 * T * d * 2, "d2h_bytes_per_step": T * d * 2,
-               "path": "MoELayer.__call__ + backward (public API); pinned host x/dy in, y out; "
-                       "copies on a side stream, double-buffered (H2D of step i+1, D2H of step i overlap compute)"}
+               "path": ("MoELayer.make_graphed_step replay (public API, CUDA graph of fwd+bwd)" if use_graph
+                                else "MoELayer.__call__ + backward (public API)")
+                       + "; pinned host x/dy in, y out; H2D/D2H on two copy streams, double-buffered"}
 
     # ---- planner + imbalance (device planner vs oracle CPU planner)
     planner_info, imbalance = None, None
@@ -436,6 +463,7 @@ def main() -> None:
                        "l2": "working set > L2 (activations+weights >> 126 MB), no flush",
                        "routing": "Zipf(1.2) gate bias, random bf16 tokens"},
             "host_enqueue_ms_per_step": host_ms, "phase_ms_rank0": phases,
+            "timed_region": "CUDA-graph replay of fwd+bwd" if use_graph else "eager stream-ordered fwd+bwd",
             "roofline": roofline, "cpu_baseline": cpu_info, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk_summary, "planner": planner_info, "imbalance": imbalance,
         }

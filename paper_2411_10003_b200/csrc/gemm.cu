@@ -27,6 +27,7 @@
 
 #include <mutex>
 #include <unordered_map>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -82,6 +83,7 @@ struct SchedSmem {
 
 struct Tile {
   int m0, n0, num_kb, row_off, wslot;
+  bool active;  // CTA pairs: false when this CTA's 128-row half lies past the group's rows
 };
 
 // ---- UMMA descriptors ------------------------------------------------------
@@ -96,7 +98,7 @@ __device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr, uint32_t lbo, uin
   return d;
 }
 
-template <int N, bool A_MN, bool B_MN>
+template <int N, bool A_MN, bool B_MN, int M = BM>
 __host__ __device__ constexpr uint32_t make_idesc() {
   return (1u << 4)                    // D = f32
          | (1u << 7)                  // A = bf16
@@ -104,7 +106,7 @@ __host__ __device__ constexpr uint32_t make_idesc() {
          | ((A_MN ? 1u : 0u) << 15)   // A major
          | ((B_MN ? 1u : 0u) << 16)   // B major
          | ((uint32_t)(N >> 3) << 17) // N
-         | ((uint32_t)(BM >> 4) << 24);
+         | ((uint32_t)(M >> 4) << 24);
 }
 
 __device__ __forceinline__ float gelu_f(float x) {
@@ -123,20 +125,23 @@ __device__ __forceinline__ float dgelu_f(float x) {
   return 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * k0 * (1.f + 3.f * k1 * x * x);
 }
 
-template <int BN>
+// Tile t of the static walk -> (group, rows, cols).  With CTA pairs (CG = 2) a
+// tile is 256 x BN: CTA rank r of the pair owns rows [m0_pair + 128 r, +128).
+template <int BN, int CG>
 __device__ __forceinline__ bool decode_tile(int t, const SchedSmem& s, const GemmParams& p,
-                                            Tile& tile) {
+                                            Tile& tile, int cta_rank) {
   // groups are few (<= experts of one rank); linear scan over the prefix
   int g = 0;
   while (g + 1 <= s.G && s.prefix[g + 1] <= t) ++g;
   if (g >= s.G) return false;
   const int local = t - s.prefix[g];
   const int nt = p.N / BN;
-  tile.m0 = (local / nt) * BM;
+  tile.m0 = (local / nt) * (BM * CG) + BM * cta_rank;
   tile.n0 = (local % nt) * BN;
   tile.row_off = s.row_off[g];
   tile.wslot = s.wslot[g];
   tile.num_kb = p.ragged_k ? (s.rows_pad[g] / BK) : (p.K_fixed / BK);
+  tile.active = p.ragged_k ? true : (tile.m0 < s.rows_pad[g]);
   return true;
 }
 
@@ -283,17 +288,21 @@ __device__ __forceinline__ void epilogue_chunk(const uint32_t (&raw)[32], const 
   }
 }
 
-template <int BN, bool A_MN, bool B_MN, int EPI, int STAGES>
+template <int BN, bool A_MN, bool B_MN, int EPI, int STAGES, int CG>
 __global__ void __launch_bounds__(kThreads, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
                         const __grid_constant__ CUtensorMap tmB,
                         const __grid_constant__ CUtensorMap tmC,
                         const __grid_constant__ CUtensorMap tmC2, const GemmParams p) {
+  // CG = 2: CTA pair (cta_group::2).  Each CTA stages its 128 rows of A and its
+  // half (BN/2 rows) of B; the leader issues 256 x BN MMAs over both CTAs' smem.
+  static_assert(CG == 1 || CG == 2, "CG");
+  constexpr int BNC = BN / CG;  // B rows staged by this CTA
   constexpr uint32_t A_BYTES = BM * BK * 2;
-  constexpr uint32_t B_BYTES = BN * BK * 2;
+  constexpr uint32_t B_BYTES = BNC * BK * 2;
   constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
   constexpr uint32_t TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
-  constexpr uint32_t IDESC = make_idesc<BN, A_MN, B_MN>();
+  constexpr uint32_t IDESC = make_idesc<BN, A_MN, B_MN, BM * CG>();  // pair: M = 256
   // epilogue warps: two per TMEM lane quarter (each takes half of the columns),
   // except the route epilogue which needs a whole logits row per thread
   constexpr int EPI_WARPS = (EPI == EPI_ROUTE) ? 4 : (BN >= 128 ? 8 : 4);
@@ -326,7 +335,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         sched.rows_pad[g] = chunk;
         sched.wslot[g] = 0;
       }
-      sched.prefix[g] = g * (p.ragged_k ? (p.M_fixed / BM) * nt : (chunk / BM) * nt);
+      sched.prefix[g] = g * (p.ragged_k ? (p.M_fixed / (BM * CG)) * nt : ((chunk + BM * CG - 1) / (BM * CG)) * nt);
     }
   } else if (threadIdx.x == 0) {
     int G = *p.num_groups;
@@ -354,7 +363,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int g = 0; g < G; ++g) {
       sched.prefix[g] = acc;
-      acc += p.ragged_k ? (p.M_fixed / BM) * nt : (sched.rows_pad[g] / BM) * nt;
+      acc += p.ragged_k ? (p.M_fixed / (BM * CG)) * nt : ((sched.rows_pad[g] + BM * CG - 1) / (BM * CG)) * nt;
     }
     sched.prefix[G] = acc;
   }
@@ -366,21 +375,26 @@ __global__ void __launch_bounds__(kThreads, 1)
       if constexpr (EPI == EPI_GELU) tma_prefetch_desc(&tmC2);
     }
   }
+  const int cta_rank = CG == 2 ? (int)cluster_ctarank() : 0;
   if (warp == 1 && lane == 0) {
     for (int i = 0; i < STAGES; ++i) {
-      mbar_init(&full_bar[i], 1);
+      mbar_init(&full_bar[i], 1);  // pair: the leader's arrive.expect_tx covers both CTAs' bytes
       mbar_init(&empty_bar[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull_bar[i], 1);
-      mbar_init(&tempty_bar[i], EPI_WARPS);
+      mbar_init(&tempty_bar[i], EPI_WARPS * CG);  // pair: both CTAs' epilogues drain
     }
     for (int i = 0; i < 8; ++i) mbar_init(&pre_bar[i], 1);
     fence_mbar_init();
   }
-  if (warp == 2) tmem_alloc<TMEM_COLS>(&tmem_base_sh);
+  if (warp == 2) {
+    if constexpr (CG == 2) tmem_alloc_2sm<TMEM_COLS>(&tmem_base_sh);
+    else tmem_alloc<TMEM_COLS>(&tmem_base_sh);
+  }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) cluster_sync_all();
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = tmem_base_sh;
   const int total_tiles = sched.prefix[sched.G];
@@ -388,7 +402,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // and dealt in snake order (0..G-1, G-1..0, ...) so long tiles spread evenly.
   const bool snake = p.ragged_k != 0;
   auto tile_of = [&](int it) -> int {
-    const int G = (int)gridDim.x, b = (int)blockIdx.x;
+    const int G = (int)gridDim.x / CG, b = (int)blockIdx.x / CG;  // one walk per CTA pair
     return it * G + ((snake && (it & 1)) ? (G - 1 - b) : b);
   };
 
@@ -399,31 +413,39 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       Tile tl;
       for (int it = 0, t = tile_of(0); t < total_tiles; t = tile_of(++it)) {
-        if (!decode_tile<BN>(t, sched, p, tl)) break;
+        if (!decode_tile<BN, CG>(t, sched, p, tl, cta_rank)) break;
         for (int kb = 0; kb < tl.num_kb; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&full_bar[stage], STAGE_BYTES);
           uint8_t* sa = smem + stage * STAGE_BYTES;
           uint8_t* sb = sa + A_BYTES;
           const int k0 = kb * BK;
+          const int nb = tl.n0 + BNC * cta_rank;  // this CTA's half of the B columns
+          // all TMA of the stage completes on the leader CTA's full barrier
+          const uint32_t bar_c = CG == 2 ? mapa_shared(smem_u32(&full_bar[stage]), 0) : 0u;
+          auto load = [&](void* dst, const CUtensorMap* m, int c0, int c1) {
+            if constexpr (CG == 2) tma_load_2d_2sm(dst, m, bar_c, c0, c1);
+            else tma_load_2d(dst, m, &full_bar[stage], c0, c1);
+          };
+          // pair: only the leader arms the barrier (both CTAs' bytes); the peer's
+          // TMA complete_tx may land first -- the phase cannot complete before the
+          // leader's arrive, and the peer only refills a stage after the MMAs that
+          // consumed it committed, so transactions never cross phases
+          if (CG == 1 || cta_rank == 0) mbar_arrive_expect_tx(&full_bar[stage], STAGE_BYTES * CG);
           if constexpr (!A_MN) {
-            tma_load_2d(sa, &tmA, &full_bar[stage], k0, tl.row_off + tl.m0);
+            load(sa, &tmA, k0, tl.row_off + tl.m0);
           } else {
 #pragma unroll
-            for (int i = 0; i < BM / 64; ++i)
-              tma_load_2d(sa + i * 8192, &tmA, &full_bar[stage], tl.m0 + 64 * i, tl.row_off + k0);
+            for (int i = 0; i < BM / 64; ++i) load(sa + i * 8192, &tmA, tl.m0 + 64 * i, tl.row_off + k0);
           }
           if constexpr (!B_MN) {
-            tma_load_2d(sb, &tmB, &full_bar[stage], k0, tl.wslot * p.N + tl.n0);
+            load(sb, &tmB, k0, tl.wslot * p.N + nb);
           } else if (p.ragged_k) {  // wgrad: B rows are the group's token rows
 #pragma unroll
-            for (int i = 0; i < BN / 64; ++i)
-              tma_load_2d(sb + i * 8192, &tmB, &full_bar[stage], tl.n0 + 64 * i, tl.row_off + k0);
+            for (int i = 0; i < BNC / 64; ++i) load(sb + i * 8192, &tmB, nb + 64 * i, tl.row_off + k0);
           } else {  // dgrad: B = W[slot] stored [K rows][N cols]
 #pragma unroll
-            for (int i = 0; i < BN / 64; ++i)
-              tma_load_2d(sb + i * 8192, &tmB, &full_bar[stage], tl.n0 + 64 * i,
-                          tl.wslot * p.K_fixed + k0);
+            for (int i = 0; i < BNC / 64; ++i)
+              load(sb + i * 8192, &tmB, nb + 64 * i, tl.wslot * p.K_fixed + k0);
           }
           if (++stage == STAGES) {
             stage = 0;
@@ -432,20 +454,23 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-  } else if (warp == 1) {
-    // ================= MMA issuer =================
+  } else if (warp == 1 && cta_rank == 0) {
+    // ================= MMA issuer (leader CTA of a pair) =================
     int stage = 0;
     uint32_t phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
     Tile tl;
     for (int it = 0, t = tile_of(0); t < total_tiles; t = tile_of(++it)) {
-      if (!decode_tile<BN>(t, sched, p, tl)) break;
+      if (!decode_tile<BN, CG>(t, sched, p, tl, cta_rank)) break;
       mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + acc * BN;
-      if (tl.num_kb == 0) {
-        if (lane == 0) mbar_arrive(&tfull_bar[acc]);
+      if (tl.num_kb == 0) {  // empty wgrad group: nothing to accumulate, epilogues write zeros
+        if (lane == 0) {
+          mbar_arrive(&tfull_bar[acc]);
+          if constexpr (CG == 2) mbar_arrive_cluster(mapa_shared(smem_u32(&tfull_bar[acc]), 1));
+        }
       }
       for (int kb = 0; kb < tl.num_kb; ++kb) {
         mbar_wait(&full_bar[stage], phase);
@@ -459,10 +484,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                                      : make_sdesc(sa + kk * 32, 16, 1024);
             const uint64_t bd = B_MN ? make_sdesc(sb + kk * 2048, 8192, 1024)
                                      : make_sdesc(sb + kk * 32, 16, 1024);
-            tc_mma_bf16(d_tmem, ad, bd, IDESC, (kb | kk) != 0);
+            if constexpr (CG == 2) tc_mma_bf16_2sm(d_tmem, ad, bd, IDESC, (kb | kk) != 0);
+            else tc_mma_bf16(d_tmem, ad, bd, IDESC, (kb | kk) != 0);
           }
-          tc_commit(&empty_bar[stage]);
-          if (kb == tl.num_kb - 1) tc_commit(&tfull_bar[acc]);
+          if constexpr (CG == 2) {
+            tc_commit_2sm(&empty_bar[stage], 0x3);
+            if (kb == tl.num_kb - 1) tc_commit_2sm(&tfull_bar[acc], 0x3);
+          } else {
+            tc_commit(&empty_bar[stage]);
+            if (kb == tl.num_kb - 1) tc_commit(&tfull_bar[acc]);
+          }
         }
         __syncwarp();
         if (++stage == STAGES) {
@@ -486,9 +517,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t acc_phase = 0;
     Tile tl;
     for (int it = 0, t = tile_of(0); t < total_tiles; t = tile_of(++it)) {
-      if (!decode_tile<BN>(t, sched, p, tl)) break;
+      if (!decode_tile<BN, CG>(t, sched, p, tl, cta_rank)) break;
       if constexpr (EPI == EPI_DGELU) {  // first pre-activation block, in flight during the MMAs
-        if (lane == 0) {
+        if (lane == 0 && tl.active) {
           mbar_arrive_expect_tx(&pre_bar[warp - 4], 2048);
           tma_load_2d(stage, &tmC, &pre_bar[warp - 4], tl.n0 + col0, tl.row_off + tl.m0 + q * 32);
         }
@@ -497,6 +528,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       const uint32_t t_row = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
       const bool zero = tl.num_kb == 0;
+      // pair: the leader's MMA waits on the leader's tempty barrier for both CTAs
+      const uint32_t tempty_c = CG == 2 ? mapa_shared(smem_u32(&tempty_bar[acc]), 0) : 0u;
+      auto release_acc = [&]() {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if constexpr (CG == 2) mbar_arrive_cluster(tempty_c);
+          else mbar_arrive(&tempty_bar[acc]);
+        }
+      };
 
       if constexpr (EPI == EPI_ROUTE) {
         // one thread = one token; logits row in registers
@@ -606,6 +647,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int u = 0; u < 4; ++u) pre_v[u] = ld_v4(old + 8 * u);
           }
           if constexpr (EPI == EPI_DGELU) {  // pre-activation block (TMA, SWIZZLE_64B)
+            if (tl.active) {
             mbar_wait(&pre_bar[warp - 4], pre_phase);
             pre_phase ^= 1;
 #pragma unroll
@@ -616,6 +658,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               mbar_arrive_expect_tx(&pre_bar[warp - 4], 2048);
               tma_load_2d(stage, &tmC, &pre_bar[warp - 4], tl.n0 + c + 32, tl.row_off + tl.m0 + q * 32);
             }
+            }
           }
           if (!zero) {
             tmem_ld_wait();
@@ -624,12 +667,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int j = 0; j < 32; ++j) cur[j] = 0u;
           }
-          if (i + 1 == NCH) {  // every TMEM read of this tile has completed
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty_bar[acc]);
-          }
-          epilogue_chunk<EPI>(cur, p, tl, r, c, pre_v, stage, &tmC, &tmC2, lane);
+          if (i + 1 == NCH) release_acc();  // every TMEM read of this tile has completed
+          if (tl.active) epilogue_chunk<EPI>(cur, p, tl, r, c, pre_v, stage, &tmC, &tmC2, lane);
         }
       }
       if (++acc == 2) {
@@ -643,8 +682,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp >= 4 && lane == 0) bulk_wait0();
   }
   tc_fence_before();
-  __syncthreads();
-  if (warp == 2) tmem_free<TMEM_COLS>(tmem_base);
+  if constexpr (CG == 2) {
+    cluster_sync_all();  // the peer may still read/commit into this CTA's TMEM and barriers
+    if (warp == 2) tmem_free_2sm<TMEM_COLS>(tmem_base);
+  } else {
+    __syncthreads();
+    if (warp == 2) tmem_free<TMEM_COLS>(tmem_base);
+  }
 }
 
 // ---- host side -------------------------------------------------------------
@@ -740,12 +784,12 @@ static int make_out_tmap_f32(CUtensorMap* m, const void* ptr, uint64_t inner, ui
                    CU_TENSOR_MAP_DATA_TYPE_FLOAT32);
 }
 
-template <int BN, bool A_MN, bool B_MN, int EPI, int STAGES>
+template <int BN, bool A_MN, bool B_MN, int EPI, int STAGES, int CG = 1>
 static int launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, int grid,
                   cudaStream_t st, const CUtensorMap* tc = nullptr, const CUtensorMap* tc2 = nullptr) {
-  auto kern = grouped_gemm_kernel<BN, A_MN, B_MN, EPI, STAGES>;
+  auto kern = grouped_gemm_kernel<BN, A_MN, B_MN, EPI, STAGES, CG>;
   const int staging = tma_out<EPI>() ? 8 * stage_bytes_per_warp<EPI>() : 0;
-  const int smem = STAGES * (BM * BK * 2 + BN * BK * 2) + staging + 1024;
+  const int smem = STAGES * (BM * BK * 2 + (BN / CG) * BK * 2) + staging + 1024;
   static CUtensorMap dummy{};
   static int configured[64] = {0};  // per device: the smem attribute is set once
   int dev = 0;
@@ -754,7 +798,23 @@ static int launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams
     PP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     configured[dev] = 1;
   }
-  kern<<<grid, kThreads, smem, st>>>(ta, tb, tc ? *tc : dummy, tc2 ? *tc2 : dummy, p);
+  if constexpr (CG == 1) {
+    kern<<<grid, kThreads, smem, st>>>(ta, tb, tc ? *tc : dummy, tc2 ? *tc2 : dummy, p);
+  } else {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((grid / 2) * 2);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    PP_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, ta, tb, tc ? *tc : dummy, tc2 ? *tc2 : dummy, p));
+  }
   PP_LAUNCH_CHECK();
   return PP_OK;
 }
@@ -828,6 +888,14 @@ int gate_bwd_gemms(const void* dl, const void* wg, const void* x, int T, int d, 
   return launch<256, true, true, EPI_F32_ATOMIC, 4>(ta, tb, q, grid, st);
 }
 
+static bool use_cta_pair() {
+  static const bool on = [] {
+    const char* v = getenv("PPMOE_GEMM_CTA_PAIR");
+    return v == nullptr || atoi(v) != 0;
+  }();
+  return on;
+}
+
 }  // namespace pp
 
 using namespace pp;
@@ -854,45 +922,53 @@ extern "C" int pp_grouped_gemm(int32_t mode, const void* a, const void* b, void*
   p.c = c;
   p.c2 = c2;
   int rc = PP_OK;
+  // CTA pairs (cta_group::2, 256 x 256 tiles, B split across the pair) unless
+  // PPMOE_GEMM_CTA_PAIR=0; a pair stages 16 KB of A + 16 KB of B per CTA and stage
+  const bool pair = use_cta_pair();
+  const uint32_t bkb = pair ? 128 : 256;  // K-major B rows staged per CTA
+#define PP_LAUNCH(EPI_, AMN_, BMN_, S1_, S2_, ...)                                          \
+  (pair ? launch<256, AMN_, BMN_, EPI_, S2_, 2>(ta, tb, p, grid, st, ##__VA_ARGS__)         \
+        : launch<256, AMN_, BMN_, EPI_, S1_, 1>(ta, tb, p, grid, st, ##__VA_ARGS__))
   switch (mode) {
     case PP_GEMM_FWD1:
       PP_CHECK_ARG(c2, "FWD1 needs the act output");
-      if ((rc = make_tmap(&ta, a, dm, R, BK, BM)) || (rc = make_tmap(&tb, b, dm, (uint64_t)S * df, BK, 256))) return rc;
+      if ((rc = make_tmap(&ta, a, dm, R, BK, BM)) || (rc = make_tmap(&tb, b, dm, (uint64_t)S * df, BK, bkb))) return rc;
       p.N = df; p.K_fixed = dm;
       if ((rc = make_out_tmap(&tc, c, df, R)) || (rc = make_out_tmap(&tc2, c2, df, R))) return rc;
-      return launch<256, false, false, EPI_GELU, 4>(ta, tb, p, grid, st, &tc, &tc2);
+      return PP_LAUNCH(EPI_GELU, false, false, 4, 6, &tc, &tc2);
     case PP_GEMM_FWD2:
-      if ((rc = make_tmap(&ta, a, df, R, BK, BM)) || (rc = make_tmap(&tb, b, df, (uint64_t)S * dm, BK, 256))) return rc;
+      if ((rc = make_tmap(&ta, a, df, R, BK, BM)) || (rc = make_tmap(&tb, b, df, (uint64_t)S * dm, BK, bkb))) return rc;
       p.N = dm; p.K_fixed = df;
       if ((rc = make_out_tmap(&tc, c, dm, R))) return rc;
-      return launch<256, false, false, EPI_BF16, 4>(ta, tb, p, grid, st, &tc);
+      return PP_LAUNCH(EPI_BF16, false, false, 4, 6, &tc);
     case PP_GEMM_DGRAD2:
       PP_CHECK_ARG(c2, "DGRAD2 needs the pre-activation");
       if ((rc = make_tmap(&ta, a, dm, R, BK, BM)) || (rc = make_tmap(&tb, b, df, (uint64_t)S * dm, 64, BK))) return rc;
       p.N = df; p.K_fixed = dm;
       PP_CHECK_ARG(c2 == c, "DGRAD2 runs in place: dPre must alias pre");
       if ((rc = make_out_tmap(&tc, c, df, R))) return rc;
-      return launch<256, false, true, EPI_DGELU, 3>(ta, tb, p, grid, st, &tc);
+      return PP_LAUNCH(EPI_DGELU, false, true, 3, 5, &tc);
     case PP_GEMM_DGRAD1:
       if ((rc = make_tmap(&ta, a, df, R, BK, BM)) || (rc = make_tmap(&tb, b, dm, (uint64_t)S * df, 64, BK))) return rc;
       p.N = dm; p.K_fixed = df;
       if ((rc = make_out_tmap(&tc, c, dm, R))) return rc;
-      return launch<256, false, true, EPI_BF16, 4>(ta, tb, p, grid, st, &tc);
+      return PP_LAUNCH(EPI_BF16, false, true, 4, 6, &tc);
     case PP_GEMM_WGRAD2:
       if ((rc = make_tmap(&ta, a, dm, R, 64, BK)) || (rc = make_tmap(&tb, b, df, R, 64, BK))) return rc;
       p.M_fixed = dm; p.N = df; p.ragged_k = 1;
       if ((rc = make_out_tmap_f32(&tc, c, df, (uint64_t)S * dm))) return rc;
-      return launch<256, true, true, EPI_F32, 3>(ta, tb, p, grid, st, &tc);
+      return PP_LAUNCH(EPI_F32, true, true, 3, 5, &tc);
     case PP_GEMM_WGRAD1:
       if ((rc = make_tmap(&ta, a, df, R, 64, BK)) || (rc = make_tmap(&tb, b, dm, R, 64, BK))) return rc;
       p.M_fixed = df; p.N = dm; p.ragged_k = 1;
       if ((rc = make_out_tmap_f32(&tc, c, dm, (uint64_t)S * df))) return rc;
-      return launch<256, true, true, EPI_F32, 3>(ta, tb, p, grid, st, &tc);
+      return PP_LAUNCH(EPI_F32, true, true, 3, 5, &tc);
     case PP_GEMM_PLAIN:
-      if ((rc = make_tmap(&ta, a, dm, R, BK, BM)) || (rc = make_tmap(&tb, b, dm, (uint64_t)S * df, BK, 256))) return rc;
+      if ((rc = make_tmap(&ta, a, dm, R, BK, BM)) || (rc = make_tmap(&tb, b, dm, (uint64_t)S * df, BK, bkb))) return rc;
       p.N = df; p.K_fixed = dm;
       if ((rc = make_out_tmap(&tc, c, df, R))) return rc;
-      return launch<256, false, false, EPI_BF16, 4>(ta, tb, p, grid, st, &tc);
+      return PP_LAUNCH(EPI_BF16, false, false, 4, 6, &tc);
+#undef PP_LAUNCH
     default:
       return fail(PP_EINVAL, "pp_grouped_gemm: unknown mode %d", mode);
   }

@@ -569,6 +569,17 @@ class MoELayer(torch.nn.Module):
     def forward(self, x: torch.Tensor) -> torch.Tensor:
         return _MoEFunction.apply(x, self)
 
+    def make_graphed_step(self, x: torch.Tensor, dy: torch.Tensor) -> "GraphedStep":
+        """Capture one forward + backward into a CUDA graph (host cost per step
+        drops to one graph launch).  ``x`` / ``dy`` become the static input
+        buffers: copy new data into them, call the returned object, read
+        ``.y`` / ``.dx`` (and the ``main_grad`` tensors).  Single-rank layers
+        only: at D > 1 the plan adoption and copy-engine Trans are host-driven
+        per iteration."""
+        if self.world != 1:
+            raise ValidationError("make_graphed_step: CUDA-graph capture is single-rank only")
+        return GraphedStep(self, x, dy)
+
     # ---- introspection (LoadMatrix / placement of the last call) -------------
     def last_load_matrix(self) -> LoadMatrix:
         return LoadMatrix(self.counts.cpu().numpy())
@@ -602,3 +613,29 @@ class _MoEFunction(torch.autograd.Function):
         (x,) = ctx.saved_tensors
         dx = ctx.layer.backward_raw(x, dy.contiguous().to(torch.bfloat16))
         return dx, None
+
+
+class GraphedStep:
+    """A captured fwd+bwd of one MoELayer over static input buffers."""
+
+    def __init__(self, layer: MoELayer, x: torch.Tensor, dy: torch.Tensor) -> None:
+        self.layer, self.x, self.dy = layer, x, dy
+        saved_timing, saved_phase = layer.gemm_timing, layer.phase_log
+        layer.gemm_timing = layer.phase_log = None  # timing events cannot live in the graph
+        side = torch.cuda.Stream(device=layer.device)
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):  # warm the allocator / lazy state outside capture
+            for _ in range(2):
+                layer.forward_raw(x)
+                layer.backward_raw(x, dy)
+        torch.cuda.current_stream().wait_stream(side)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self.y = layer.forward_raw(x)
+            self.dx = layer.backward_raw(x, dy)
+        layer.gemm_timing, layer.phase_log = saved_timing, saved_phase
+
+    def __call__(self):
+        self.graph.replay()
+        self.layer.iteration += 1
+        return self.y, self.dx

@@ -1,0 +1,48 @@
+"""Standalone timing of the grouped GEMM modes at the cfg2 shape (uniform groups).
+Usage: python scripts/gemm_bench.py [mode ...]   (PPMOE_GEMM_CTA_PAIR=0/1 selects 1-CTA / CTA-pair)"""
+import math
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+import torch
+
+from paper_2411_10003_b200 import _device, _lib
+
+T, k, E, d, f = 16384, 2, 16, 1024, 4096
+rows = [T * k // E] * E
+dev = torch.device("cuda")
+groups, ng, total = _device.groups_tensor(rows, device=dev)
+cap = int(math.ceil((total + 512) / 256) * 256)
+X = torch.randn((cap, d), device=dev).to(torch.bfloat16)
+W1 = (torch.randn((E, f, d), device=dev) / 32).to(torch.bfloat16)
+W2 = (torch.randn((E, d, f), device=dev) / 64).to(torch.bfloat16)
+pre = torch.zeros((cap, f), dtype=torch.bfloat16, device=dev)
+act = torch.zeros((cap, f), dtype=torch.bfloat16, device=dev)
+Y = torch.zeros((cap, d), dtype=torch.bfloat16, device=dev)
+G1 = torch.zeros((E, f, d), dtype=torch.float32, device=dev)
+G2 = torch.zeros((E, d, f), dtype=torch.float32, device=dev)
+modes = {
+    "FWD1": (_lib.PP_GEMM_FWD1, X, W1, pre, act),
+    "FWD2": (_lib.PP_GEMM_FWD2, act, W2, Y, None),
+    "DGRAD2": (_lib.PP_GEMM_DGRAD2, Y, W2, pre, pre),
+    "DGRAD1": (_lib.PP_GEMM_DGRAD1, pre, W1, Y, None),
+    "WGRAD2": (_lib.PP_GEMM_WGRAD2, Y, act, G2, None),
+    "WGRAD1": (_lib.PP_GEMM_WGRAD1, pre, X, G1, None),
+}
+sel = sys.argv[1:] or list(modes)
+flops = 2.0 * T * k * d * f
+for name in sel:
+    mode, a, b, c, c2 = modes[name]
+    run = lambda: _device.grouped_gemm(mode, a, b, c, c2, groups, ng, E, cap, E, d, f)  # noqa: E731
+    for _ in range(3):
+        run()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(10):
+        run()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / 10
+    print(f"{name:7s} {ms*1e3:8.1f} us  {flops/ms/1e9:8.1f} TFLOP/s", flush=True)
