@@ -46,7 +46,7 @@ enum Epi { EPI_BF16 = 0, EPI_GELU = 1, EPI_DGELU = 2, EPI_F32 = 3, EPI_ROUTE = 4
 // 2 KB block that receives the TMA-loaded pre-activation
 template <int EPI>
 constexpr int stage_bytes_per_warp() {
-  return EPI == EPI_F32 ? 4096 : EPI == EPI_DGELU ? 4096 : 2048;
+  return EPI == EPI_F32 ? 4096 : (EPI == EPI_DGELU || EPI == EPI_BF16_ADD) ? 4096 : 2048;
 }
 
 struct GemmParams {
@@ -71,6 +71,7 @@ struct GemmParams {
   int single_rows;  // > 0: implicit groups over rows [0, single_rows), slot 0
   int split_rows;   // with single_rows: split-K chunk size (one implicit group per chunk)
   int m_real;       // EPI_F32_ATOMIC: rows of the output that exist (< M_fixed)
+  unsigned long long* dbg;  // optional per-CTA wait-cycle counters (PPMOE_GEMM_DEBUG)
 };
 
 struct SchedSmem {
@@ -147,7 +148,8 @@ __device__ __forceinline__ bool decode_tile(int t, const SchedSmem& s, const Gem
 
 template <int EPI>
 constexpr bool tma_out() {
-  return EPI == EPI_BF16 || EPI == EPI_GELU || EPI == EPI_DGELU || EPI == EPI_F32;
+  return EPI == EPI_BF16 || EPI == EPI_GELU || EPI == EPI_DGELU || EPI == EPI_F32 ||
+         EPI == EPI_BF16_ADD;
 }
 
 // Stage a 32x32 bf16 block (row = lane, 16-byte chunk j) with the SWIZZLE_64B
@@ -221,13 +223,15 @@ __device__ __forceinline__ void epilogue_chunk(const uint32_t (&raw)[32], const 
       }
       stage_and_store(stage, v, tmC, col, row, lane);
       stage_and_store(stage, g4, tmC2, col, row, lane);
-    } else {  // EPI_DGELU
+    } else {  // EPI_DGELU: acc * GeLU'(pre);  EPI_BF16_ADD: acc + old   (operand TMA-loaded)
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         float x[8], f[8];
         bf16x8_to_f32(pre_v[j], x);
 #pragma unroll
-        for (int u = 0; u < 8; ++u) f[u] = __uint_as_float(raw[8 * j + u]) * dgelu_f(x[u]);
+        for (int u = 0; u < 8; ++u)
+          f[u] = EPI == EPI_DGELU ? __uint_as_float(raw[8 * j + u]) * dgelu_f(x[u])
+                                  : __uint_as_float(raw[8 * j + u]) + x[u];
         v[j] = f32x8_to_bf16(f);
       }
       stage_and_store(stage + 2048, v, tmC, col, row, lane);
@@ -263,16 +267,6 @@ __device__ __forceinline__ void epilogue_chunk(const uint32_t (&raw)[32], const 
         for (int u = 0; u < 8; ++u) g[u] = gelu_f(f[u]);
         st_v4(pre + j, pv);
         st_v4(act + j, f32x8_to_bf16(g));
-      }
-    } else if constexpr (EPI == EPI_BF16_ADD) {  // out += acc (pre_v holds the old out)
-      __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.c) + off;
-#pragma unroll
-      for (int j = 0; j < 32; j += 8) {
-        float x[8], f[8];
-        bf16x8_to_f32(pre_v[j / 8], x);
-#pragma unroll
-        for (int u = 0; u < 8; ++u) f[u] = __uint_as_float(raw[j + u]) + x[u];
-        st_v4(out + j, f32x8_to_bf16(f));
       }
     } else if constexpr (EPI == EPI_DGELU) {
       __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.c) + off;
@@ -456,6 +450,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1 && cta_rank == 0) {
     // ================= MMA issuer (leader CTA of a pair) =================
+    long long wait_tempty = 0, wait_full = 0, t_start = p.dbg ? clock64() : 0;
     int stage = 0;
     uint32_t phase = 0;
     int acc = 0;
@@ -463,7 +458,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     Tile tl;
     for (int it = 0, t = tile_of(0); t < total_tiles; t = tile_of(++it)) {
       if (!decode_tile<BN, CG>(t, sched, p, tl, cta_rank)) break;
+      long long w0 = p.dbg ? clock64() : 0;
       mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+      if (p.dbg) wait_tempty += clock64() - w0;
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + acc * BN;
       if (tl.num_kb == 0) {  // empty wgrad group: nothing to accumulate, epilogues write zeros
@@ -473,7 +470,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       for (int kb = 0; kb < tl.num_kb; ++kb) {
+        long long w1 = p.dbg ? clock64() : 0;
         mbar_wait(&full_bar[stage], phase);
+        if (p.dbg) wait_full += clock64() - w1;
         tc_fence_after();
         if (lane == 0) {
           const uint32_t sa = smem_u32(smem + stage * STAGE_BYTES);
@@ -506,6 +505,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         acc_phase ^= 1;
       }
     }
+    if (p.dbg && lane == 0) {
+      p.dbg[blockIdx.x * 4 + 0] = (unsigned long long)(clock64() - t_start);
+      p.dbg[blockIdx.x * 4 + 1] = (unsigned long long)wait_tempty;
+      p.dbg[blockIdx.x * 4 + 2] = (unsigned long long)wait_full;
+    }
   } else if (warp >= 4 && warp < 4 + EPI_WARPS) {
     // ================= epilogue =================
     const int q = warp & 3;                  // TMEM lane quarter (hardware: warp % 4)
@@ -518,7 +522,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     Tile tl;
     for (int it = 0, t = tile_of(0); t < total_tiles; t = tile_of(++it)) {
       if (!decode_tile<BN, CG>(t, sched, p, tl, cta_rank)) break;
-      if constexpr (EPI == EPI_DGELU) {  // first pre-activation block, in flight during the MMAs
+      if constexpr (EPI == EPI_DGELU || EPI == EPI_BF16_ADD) {  // first operand block, in flight during the MMAs
         if (lane == 0 && tl.active) {
           mbar_arrive_expect_tx(&pre_bar[warp - 4], 2048);
           tma_load_2d(stage, &tmC, &pre_bar[warp - 4], tl.n0 + col0, tl.row_off + tl.m0 + q * 32);
@@ -640,13 +644,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           uint32_t(&nxt)[32] = (i & 1) ? rawA : rawB;
           const int c = col0 + 32 * i;
           uint4 pre_v[4];
-          if constexpr (EPI == EPI_BF16_ADD) {  // old output: loads overlap the TMEM read
-            const __nv_bfloat16* old = reinterpret_cast<const __nv_bfloat16*>(p.c) +
-                                       ((size_t)tl.row_off + tl.m0 + r) * p.N + tl.n0 + c;
-#pragma unroll
-            for (int u = 0; u < 4; ++u) pre_v[u] = ld_v4(old + 8 * u);
-          }
-          if constexpr (EPI == EPI_DGELU) {  // pre-activation block (TMA, SWIZZLE_64B)
+          if constexpr (EPI == EPI_DGELU || EPI == EPI_BF16_ADD) {  // operand block (TMA, SWIZZLE_64B)
             if (tl.active) {
             mbar_wait(&pre_bar[warp - 4], pre_phase);
             pre_phase ^= 1;
@@ -872,7 +870,9 @@ int gate_bwd_gemms(const void* dl, const void* wg, const void* x, int T, int d, 
   p.c = dx;
   if (int rc = make_tmap(&ta, dl, EP, T, BK, BM)) return rc;
   if (int rc = make_tmap(&tb, wg, d, E, 64, BK)) return rc;
-  if (int rc = launch<256, false, true, EPI_BF16_ADD, 4>(ta, tb, p, grid, st)) return rc;
+  CUtensorMap tc;
+  if (int rc = make_out_tmap(&tc, dx, d, T)) return rc;
+  if (int rc = launch<256, false, true, EPI_BF16_ADD, 3>(ta, tb, p, grid, st, &tc)) return rc;
   // dwg[E][d] += dl^T . x  (split-K over token chunks, fp32 atomics; M padded to 128)
   GemmParams q{};
   q.max_groups = 1;
@@ -900,6 +900,15 @@ static bool use_cta_pair() {
 
 using namespace pp;
 
+// Diagnostic (PPMOE_GEMM_DEBUG=1): copies the last GEMM launch's per-CTA MMA-thread
+// cycle counters [cta][total, wait_tempty, wait_full, -] into host memory.
+static unsigned long long* g_dbg_buf = nullptr;
+extern "C" int pp_gemm_debug_read(unsigned long long* host, int32_t ctas) {
+  PP_CHECK_ARG(g_dbg_buf && host && ctas > 0 && ctas <= 1024, "pp_gemm_debug_read: PPMOE_GEMM_DEBUG not set");
+  PP_CUDA_TRY(cudaMemcpy(host, g_dbg_buf, (size_t)ctas * 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+  return PP_OK;
+}
+
 extern "C" int pp_grouped_gemm(int32_t mode, const void* a, const void* b, void* c, void* c2,
                                const pp_group* groups, const int32_t* num_groups,
                                int32_t max_groups, int32_t rows_capacity, int32_t num_slots,
@@ -916,6 +925,9 @@ extern "C" int pp_grouped_gemm(int32_t mode, const void* a, const void* b, void*
   const int R = rows_capacity, S = num_slots, dm = d_model, df = d_ff;
   CUtensorMap ta, tb, tc, tc2;
   GemmParams p{};
+  static const bool dbg_on = getenv("PPMOE_GEMM_DEBUG") != nullptr;
+  if (dbg_on && !g_dbg_buf) cudaMalloc(&g_dbg_buf, 4 * 1024 * sizeof(unsigned long long));
+  p.dbg = dbg_on ? g_dbg_buf : nullptr;
   p.groups = groups;
   p.num_groups = num_groups;
   p.max_groups = max_groups;

@@ -46,3 +46,20 @@ for name in sel:
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / 10
     print(f"{name:7s} {ms*1e3:8.1f} us  {flops/ms/1e9:8.1f} TFLOP/s", flush=True)
+
+if __import__("os").environ.get("PPMOE_GEMM_DEBUG"):
+    import ctypes
+    import numpy as np
+
+    lib = _lib.load()
+    for name in sel:
+        mode, a, b, c, c2 = modes[name]
+        _device.grouped_gemm(mode, a, b, c, c2, groups, ng, E, cap, E, d, f)
+        torch.cuda.synchronize()
+        buf = (ctypes.c_ulonglong * (148 * 4))()
+        lib.pp_gemm_debug_read(buf, 148)
+        arr = np.array(buf).reshape(148, 4)
+        lead = arr[arr[:, 0] > 0]
+        tot, wt, wf = lead[:, 0].mean(), lead[:, 1].mean(), lead[:, 2].mean()
+        print(f"{name:7s} MMA thread: total {tot:10.0f} cyc, wait tempty {wt/tot*100:5.1f}%, wait full {wf/tot*100:5.1f}%, "
+              f"issue+other {(tot-wt-wf)/tot*100:5.1f}%  (CTAs {len(lead)}, max total {lead[:,0].max():.0f})")
