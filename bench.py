@@ -33,6 +33,8 @@ CONFIGS = {
     "cfg2": dict(E=16, k=2, d=1024, f=4096, T=16384, desc="16 experts top-2 d1024 f4096 16K tokens/GPU skewed"),
     "cfg3": dict(E=32, k=2, d=2048, f=4096, T=32768, desc="32 experts top-2 d2048 f4096 32K tokens/GPU EP"),
     "cfg4": dict(E=64, k=2, d=2048, f=4096, T=32768, desc="64 experts top-2 d2048 32K tokens/GPU Zipf drift"),
+    "cfg5": dict(E=64, k=2, d=2048, f=4096, T=8192, L=12, desc="12-block MoE-GPT stack, 64 experts top-2 d2048 f4096, "
+                 "8K tokens/GPU (4 x 2048-token sequences), attention in stock PyTorch, Algorithm-2 overlap"),
 }
 METRIC = "MoE-layer tokens/s fwd+bwd at 1/2/4/8 B200; planner ms/iter; load imbalance"
 
@@ -215,6 +217,67 @@ def run_reference(args, cfg_name: str, cfg: dict) -> None:
     print(json.dumps(out), flush=True)
 
 
+# --------------------------------------------------------------------------- stack (cfg5)
+def run_stack(args, cfg_name: str, cfg: dict, world: int, rank: int, dev, group) -> dict:
+    """Config 5: L-block stack, fwd+bwd per step, eager (host-driven Trans per block),
+    with the measured Algorithm-2 timeline of one iteration."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2411_10003_b200 as pp
+    from paper_2411_10003_b200.stack import MoEStack
+
+    E, k, d, f, T, L = cfg["E"], cfg["k"], cfg["d"], cfg["f"], cfg["T"], cfg["L"]
+    planner = pp.PlannerConfig(n=1, alpha=0.5, reuse_interval=1, overlap_aware=True)
+    stack = MoEStack(L, d, f, E, k, T, group=group, planner=planner, seq_len=2048, n_heads=16)
+    for m in stack.moe:
+        m.set_gate_bias(zipf_bias(E, 1.2, m.block_index))
+    g = torch.Generator(device="cpu").manual_seed(1000 + rank)
+    x = torch.randn((T, d), generator=g).to(dev, torch.bfloat16)
+    dy = (torch.randn((T, d), generator=g) * 0.1).to(dev, torch.bfloat16)
+
+    def step():
+        xin = x.detach().requires_grad_(True)
+        y = stack(xin)
+        y.backward(dy)
+        stack.wait_grads()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for _ in range(args.steps):
+        step()
+    t1.record()
+    torch.cuda.synchronize()
+    ms = torch.tensor([t0.elapsed_time(t1) / args.steps], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms_step = float(ms.item())
+    # one instrumented iteration -> reference-schema measured timeline
+    stack.start_timeline()
+    step()
+    tl = stack.measured_timeline(iteration=0)
+    stack.stop_timeline()
+    mk = tl.makespan()
+    exposed_trans = sum(tl.exposed_trans_seconds(i) for i in range(L))
+    exposed_agg = sum(tl.exposed_agg_seconds(i) for i in range(L))
+    trans_total = sum(o.duration for o in tl.ops if o.kind.value.startswith("SubTrans"))
+    agg_total = sum(o.duration for o in tl.ops if o.kind.value.startswith("SubAgg"))
+    return {"value": world * T / (ms_step / 1e3), "ms_per_step": ms_step,
+            "timeline": {"makespan_ms": mk * 1e3, "phase_totals_ms": {k_: v * 1e3 for k_, v in tl.phase_totals().items()},
+                         "replica_comm_ms": (trans_total + agg_total) * 1e3,
+                         "exposed_replica_comm_ms": (exposed_trans + exposed_agg) * 1e3,
+                         "exposed_replica_comm_frac": (exposed_trans + exposed_agg) / mk if mk > 0 else 0.0,
+                         "definition": "reference IterationTimeline.exposed_*_seconds on the measured CUDA-event timeline",
+                         "replicas_per_block": [len(m.replica_experts) for m in stack.moe]},
+            "timeline_json": tl.to_json_obj()}
+
+
 # --------------------------------------------------------------------------- our arm
 def main() -> None:
     ap = argparse.ArgumentParser()
@@ -250,6 +313,22 @@ def main() -> None:
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
         group = dist.group.WORLD
+    if "L" in cfg:  # config 5: the block stack
+        res = run_stack(args, cfg_name, cfg, world, rank, dev, group)
+        if rank == 0:
+            out = {"metric": METRIC, "value": res["value"], "unit": "tokens/s", "n_gpus": world,
+                   "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["ms_per_step"],
+                   "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+                   "data": "synthetic", "config": {"workload": f"{cfg_name}: {cfg['desc']}",
+                                                   "parallelism": f"ep{world}"},
+                   "stack_timeline": res["timeline"]}
+            print(json.dumps(out), flush=True)
+            Path(ROOT, "gpurun_out").mkdir(exist_ok=True)
+            Path(ROOT, "gpurun_out", f"timeline_{cfg_name}_n{world}.json").write_text(json.dumps(res["timeline_json"]))
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
     E, k, d, f, T = cfg["E"], cfg["k"], cfg["d"], cfg["f"], cfg["T"]
     planner = pp.PlannerConfig(n=1, alpha=0.5, reuse_interval=1, overlap_aware=True)
     layer = pp.MoELayer(d, f, E, k, tokens=T, group=group, planner=planner, seed=0)

@@ -275,6 +275,8 @@ class MoELayer(torch.nn.Module):
         self.gemm_event_pool = None
         self.phase_log = None
         self._agg_done = None
+        self.timeline_log = None  # list -> (kind, lane, start_event, end_event) of side-stream ops
+        self.block_index = 0
         if D > 1:
             torch.cuda.synchronize()
             dist.barrier(group=self.group)
@@ -342,8 +344,10 @@ class MoELayer(torch.nn.Module):
         with torch.cuda.stream(self.plan_stream):
             self.plan_stream.wait_event(ev)
             snapshot.record_stream(self.plan_stream)
+            p0 = self._side_event(self.plan_stream)
             _device.launch_plan(snapshot.view(1, self.E, self.E), self._plan_out, self._cm, self._pcfg,
                                 self.plan_stream)
+            self._log_side("Plan", p0, self._side_event(self.plan_stream))
             mask_dev = self._plan_out.mask[0].clone()
             self._mask_host.copy_(mask_dev, non_blocking=True)
             done = torch.cuda.Event()
@@ -426,15 +430,61 @@ class MoELayer(torch.nn.Module):
         ev.record()
         with torch.cuda.stream(self.comm_stream):
             self.comm_stream.wait_event(ev)
+            t0 = self._side_event(self.comm_stream)
             if self.replica_engine == "copy":
-                self._copy_batch(self._trans_list, self.comm_stream)
+                split = getattr(self, "trans_split_bytes", None)
+                if split:  # Algorithm 2 partition: SubTrans2 (FNEC window) first, then SubTrans1
+                    first, rest = self._split_copies(self._trans_list, split)
+                    self._copy_batch(first, self.comm_stream)
+                    t1 = self._side_event(self.comm_stream)
+                    self._log_side("SubTrans2", t0, t1)
+                    t0 = t1
+                    self._copy_batch(rest, self.comm_stream)
+                else:
+                    self._copy_batch(self._trans_list, self.comm_stream)
             else:
                 _lib.call("pp_replica_trans", self.w1_arena.ptrs.data_ptr(), self.w2_arena.ptrs.data_ptr(),
                           self.groups.data_ptr(), self.num_groups.data_ptr(), self.max_groups, self.rank,
                           self.m, self.d, self.f, self.trans_ctas, _device.stream_ptr(self.comm_stream))
             self._trans_done = torch.cuda.Event()
             self._trans_done.record(self.comm_stream)
+            self._log_side("SubTrans1", t0, self._side_event(self.comm_stream))
         return self._trans_done
+
+    def _side_event(self, stream):
+        if self.timeline_log is None:
+            return None
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record(stream)
+        return ev
+
+    def _log_side(self, kind: str, e0, e1) -> None:
+        if self.timeline_log is not None and e0 is not None and e1 is not None:
+            self.timeline_log.append((kind, e0, e1))
+
+    @staticmethod
+    def _split_copies(items, first_bytes: int):
+        """Split a copy list so that the first part moves ~first_bytes (a copy may
+        be cut in two at a 16-byte boundary)."""
+        first, rest, acc = [], [], 0
+        for dst, src, nb in items:
+            if acc >= first_bytes:
+                rest.append((dst, src, nb))
+                continue
+            take = min(nb, first_bytes - acc)
+            take -= take % 16
+            if take > 0:
+                first.append((dst, src, take))
+            if take < nb:
+                rest.append((dst + take, src + take, nb - take))
+            acc += take
+        return first, rest
+
+    def trans_bytes(self) -> int:
+        return sum(t[2] for t in self._trans_list)
+
+    def agg_bytes(self) -> int:
+        return sum(t[2] for t in self._agg_list)
 
     def _issue_agg(self) -> None:
         """K5 Agg: pull the replicas' grads of this rank's home experts and add
@@ -445,6 +495,7 @@ class MoELayer(torch.nn.Module):
         ev.record()
         with torch.cuda.stream(self.comm_stream):
             self.comm_stream.wait_event(ev)
+            t0 = self._side_event(self.comm_stream)
             if self.replica_engine == "copy":
                 if self._agg_list:
                     self._copy_batch(self._agg_list, self.comm_stream)
@@ -457,6 +508,7 @@ class MoELayer(torch.nn.Module):
                           self.trans_ctas * 4, _device.stream_ptr(self.comm_stream))
             self._agg_done = torch.cuda.Event()
             self._agg_done.record(self.comm_stream)
+            self._log_side("SubAgg2", t0, self._side_event(self.comm_stream))
 
     def _gemm(self, mode, a, b, c, c2=None, stream=None):
         timing = self.gemm_timing
@@ -532,6 +584,7 @@ class MoELayer(torch.nn.Module):
     def backward_raw(self, x: torch.Tensor, dy: torch.Tensor) -> torch.Tensor:
         assert dy.shape == (self.T, self.d) and dy.dtype == torch.bfloat16 and dy.is_contiguous()
         sp = self._sp()
+        self._mark("bwd_begin")
         _lib.call("pp_combine_bwd", dy.data_ptr(), self.yp.ptrs.data_ptr(), self.dyp.ptrs.data_ptr(),
                   self.dyp.local.data_ptr(), self.pair_dest.data_ptr(), self.pair_row.data_ptr(),
                   self.w.data_ptr(), self.groups.data_ptr(), self.num_groups.data_ptr(), self.max_groups,
