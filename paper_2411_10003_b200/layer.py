@@ -276,6 +276,9 @@ class MoELayer(torch.nn.Module):
         self.phase_log = None
         self._agg_done = None
         self.timeline_log = None  # list -> (kind, lane, start_event, end_event) of side-stream ops
+        # persistent-GEMM grid (0 = every SM); leaving a few SMs free lets the side-stream
+        # Agg reduce / planner kernels run under the expert GEMMs instead of after them
+        self.gemm_sms = 0
         self.block_index = 0
         if D > 1:
             torch.cuda.synchronize()
@@ -521,7 +524,7 @@ class MoELayer(torch.nn.Module):
                 e1 = torch.cuda.Event(enable_timing=True)
             e0.record()
         _device.grouped_gemm(mode, a, b, c, c2, self.groups, self.num_groups, self.max_groups,
-                             self.rows_cap, self.slots, self.d, self.f, stream=stream)
+                             self.rows_cap, self.slots, self.d, self.f, num_sms=self.gemm_sms, stream=stream)
         if timing is not None:
             e1.record()
             timing.append((mode, e0, e1))
@@ -558,6 +561,7 @@ class MoELayer(torch.nn.Module):
         if self.replica_engine == "sm":  # device-driven pulls read this iteration's group table
             trans_done = self.issue_trans()
         self._mark("route_layout")
+        self._launch_planner()  # [A2A | Plan(j+1)]: the search overlaps this block's dispatch
         _lib.call("pp_dispatch", x.data_ptr(), self.idx.data_ptr(), self.rank_in_chunk.data_ptr(),
                   self.chunk_base.data_ptr(), self.slot_dest.data_ptr(), self.T, self.d, self.k, self.m,
                   self.E, self.xp.ptrs.data_ptr(), self.xp.local.data_ptr(), self.groups.data_ptr(),
@@ -578,7 +582,6 @@ class MoELayer(torch.nn.Module):
         _lib.call("pp_combine", self.yp.ptrs.data_ptr(), self.pair_dest.data_ptr(), self.pair_row.data_ptr(),
                   self.w.data_ptr(), self.T, self.d, self.k, y.data_ptr(), sp)
         self._mark("combine")
-        self._launch_planner()
         return y
 
     def backward_raw(self, x: torch.Tensor, dy: torch.Tensor) -> torch.Tensor:
@@ -594,12 +597,15 @@ class MoELayer(torch.nn.Module):
         self._mark("barrier3")
         self._gemm(_lib.PP_GEMM_DGRAD2, self.dyp.local, self.w2_arena.local, self.pre, self.pre)
         self._gemm(_lib.PP_GEMM_WGRAD2, self.dyp.local, self.act, self.g2_arena.local)
-        self._gemm(_lib.PP_GEMM_DGRAD1, self.pre, self.w1_arena.local, self.dxp.local)
         self._gemm(_lib.PP_GEMM_WGRAD1, self.pre, self.xp.local, self.g1_arena.local)
+        agg = self.world > 1 and self.mask_cur is not None
+        if agg:  # every rank's replica gradients exist: Agg rides on DGRAD1 (SubAgg | BEC)
+            self.barrier()
+            self._issue_agg()
+        self._gemm(_lib.PP_GEMM_DGRAD1, self.pre, self.w1_arena.local, self.dxp.local)
         self._mark("bwd_gemms")
         self.barrier()
         self._mark("barrier4")
-        self._issue_agg()  # K5 Agg on the side stream: overlaps dispatch_bwd and the gate GEMMs
         dx = torch.empty((self.T, self.d), dtype=torch.bfloat16, device=self.device)
         _lib.call("pp_dispatch_bwd", self.dxp.ptrs.data_ptr(), self.pair_dest.data_ptr(),
                   self.pair_row.data_ptr(), self.idx.data_ptr(), self.probs.data_ptr(), self.dw.data_ptr(),

@@ -31,6 +31,12 @@ from .perf_model import LayerCost
 from .scheduler import IterationTimeline, Lane, OpKind, ScheduledOp, partition_trans
 
 
+def reserve_sms_gemm_grid(reserved: int = 4) -> int:
+    props = torch.cuda.get_device_properties(torch.cuda.current_device())
+    n = props.multi_processor_count - reserved
+    return n - (n % 2)  # CTA pairs
+
+
 class Attention(torch.nn.Module):
     """Pre-LN causal self-attention over [T, d] tokens packed as T/seq sequences."""
 
@@ -91,6 +97,8 @@ class MoEStack(torch.nn.Module):
         for i, m in enumerate(self.moe):
             m.block_index = i
             self.add_module(f"moe{i}", m)
+            if m.world > 1:  # reserve SMs for the Agg reduce / planner kernels (Algorithm 2 overlap)
+                m.gemm_sms = reserve_sms_gemm_grid()
         self.fnec_time, self.bnec_time = fnec_time, bnec_time  # seconds; calibrate() measures them
         self.log = None  # main-stream timeline marks of one iteration
 
@@ -152,13 +160,17 @@ class MoEStack(torch.nn.Module):
             m = self.moe[i]
             ph = m.phase_log or []
             seq = {n: e for n, e in ph}
+            # gate GEMMs + layout count as expert compute (FEC/BEC); the permute /
+            # all-to-all kernels and their barriers are the A2A (network lane)
             groups = [
-                (OpKind.A2A, Lane.NETWORK, "fwd_start", "barrier1"),
+                (OpKind.FEC, Lane.COMPUTE, "fwd_start", "route_layout"),
+                (OpKind.A2A, Lane.NETWORK, "route_layout", "barrier1"),
                 (OpKind.FEC, Lane.COMPUTE, "barrier1", "fwd_gemms"),
                 (OpKind.A2A, Lane.NETWORK, "fwd_gemms", "combine"),
                 (OpKind.A2A, Lane.NETWORK, "bwd_begin", "barrier3"),
                 (OpKind.BEC, Lane.COMPUTE, "barrier3", "bwd_gemms"),
-                (OpKind.A2A, Lane.NETWORK, "bwd_gemms", "gate_bwd"),
+                (OpKind.A2A, Lane.NETWORK, "bwd_gemms", "dispatch_bwd"),
+                (OpKind.BEC, Lane.COMPUTE, "dispatch_bwd", "gate_bwd"),
             ]
             for kind, lane, a, b in groups:
                 if a in seq and b in seq:
