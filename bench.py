@@ -413,8 +413,17 @@ def main() -> None:
     flops_step = 2.0 * rows_real * d * f * 6  # FWD1, FWD2, DGRAD2, DGRAD1, WGRAD2, WGRAD1
     gemm_ms_step = gemm["ms_per_step"]
     achieved = flops_step / (gemm_ms_step / 1e3) / 1e12 if gemm_ms_step > 0 else 0.0
+    traffic = None
+    tf = ROOT / "profiles" / "r01_roofline_traffic.json"
+    if tf.exists():
+        tj = json.loads(tf.read_text()).get(cfg_name)
+        if tj:
+            traffic = tj["gemm_family_dram_bytes_per_step"]
     roofline = {"bound": "tensor", "achieved": achieved, "peak": peaks["tc_sustained"], "unit": "TFLOP/s",
-                "frac": achieved / peaks["tc_sustained"], "traffic": None,
+                "frac": achieved / peaks["tc_sustained"], "traffic": traffic,
+                "traffic_note": "DRAM bytes (read+write) of one step's 6 GEMM launches from the committed ncu "
+                                "--set full capture (profiles/r01_roofline_traffic.json); algorithmic minimum "
+                                "~2.2 GB (operands once + outputs)" if traffic else None,
                 "kernel": "grouped_gemm_kernel (6 launches/step: FWD1 FWD2 DGRAD2 DGRAD1 WGRAD2 WGRAD1)",
                 "peak_source": f"{peaks['source']} bf16_tflops_sustained",
                 "flops_per_step": flops_step, "gemm_ms_per_step": gemm_ms_step,
