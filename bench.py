@@ -7,9 +7,11 @@ One "step" = one forward + backward of one MoE layer over this rank's T tokens
 (synthetic bf16 activations, random-init weights, Zipf-skewed gate bias,
 planner re-planning every iteration when N > 1).  Prints ONE JSON line on rank 0.
 
-Workloads (BASELINE.json configs): N == 1 -> configs[1] ("cfg2": 16 experts,
-top-2, d=1024, f=4096, 16K tokens/GPU); N > 1 -> configs[2] ("cfg3": 32
-experts, top-2, d=2048, f=4096, 32K tokens/GPU, EP across the N GPUs).
+Workload: BASELINE.json configs[1] ("cfg2": 16 experts, top-2, d=1024, f=4096,
+16K tokens/GPU, Zipf-skewed routing) at every N -- weak scaling, the 16 experts
+spread over the N GPUs (E/N per GPU) with the Pro-Prophet planner re-planning
+every iteration when N > 1.  ``--config cfg3|cfg4|cfg5`` runs the other
+BASELINE configs (cfg5 = the 12-block stack with Algorithm-2 overlap).
 """
 
 from __future__ import annotations
@@ -291,7 +293,10 @@ def main() -> None:
     ap.add_argument("--eager", action="store_true", help="no CUDA graph for the N == 1 timed region")
     args = ap.parse_args()
     world_env = int(os.environ.get("WORLD_SIZE", "1"))
-    cfg_name = args.config or ("cfg2" if max(args.gpus, world_env) == 1 else "cfg3")
+    # one bench workload for every N (weak scaling of the same per-GPU work): BASELINE
+    # configs[1] (16 experts, top-2, d=1024, f=4096, 16K tokens/GPU); at N > 1 its 16
+    # experts are spread EP-style over the N GPUs.  Other configs: --config cfg1|cfg3|cfg4|cfg5.
+    cfg_name = args.config or "cfg2"
     cfg = dict(CONFIGS[cfg_name])
     if args.impl == "reference":
         run_reference(args, cfg_name, cfg)

@@ -95,10 +95,12 @@ int pp_route_topk(const void* x, const void* wg, const float* bias,
                   int32_t* idx, float* w, float* probs, int32_t* rank,
                   int32_t* chunk_counts, void* stream);
 
-/* Local virtual-slot histogram: chunk_counts [T/128][E] -> hist [m][E] int64
- * written at row offset `row0` of `out` (out has >= row0+m rows of E). */
+/* This rank's virtual-slot rows of the LoadMatrix: chunk_counts [T/128][E] ->
+ * hist [m][E] int64, stored at row offset `row0` of EVERY rank's LoadMatrix copy
+ * (out_ptrs: device array [D] of peer-mapped [E][E] buffers) -- the histogram
+ * all-gather as plain NVLink stores; follow with pp_peer_barrier. */
 int pp_slot_histogram(const int32_t* chunk_counts, int32_t T, int32_t E, int32_t m,
-                      int64_t* out, int32_t row0, void* stream);
+                      int64_t* const* out_ptrs, int32_t D, int32_t row0, void* stream);
 
 /* ---- dispatch layout / permute / combine (K3) --------------------------- */
 #define PP_CHUNK 128

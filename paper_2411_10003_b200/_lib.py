@@ -64,7 +64,7 @@ SIGNATURES = {
     "pp_plan_greedy": [P, I, I, POINTER(CostModel), POINTER(PlannerCfg), P, P, P, P, P, P, P, P],
     "pp_derive_loads": [P, P, I, I, P, P, P],
     "pp_route_topk": [P, P, P, I, I, I, I, P, P, P, P, P, P],
-    "pp_slot_histogram": [P, I, I, I, P, I, P],
+    "pp_slot_histogram": [P, I, I, I, P, I, I, P],
     "pp_dispatch_layout": [P, P, P, I, I, I, I, I, I, I, P, P, P, P, P, P, P, P],
     "pp_dispatch": [P, P, P, P, P, I, I, I, I, I, P, P, P, P, I, P, P, P],
     "pp_combine": [P, P, P, P, I, I, I, P, P],

@@ -23,15 +23,17 @@ int route_gemm(const void* x, const void* wg, const float* bias, int T, int d, i
                cudaStream_t st);
 
 // ---------------------------------------------------------------------------
+// this rank's m virtual-slot rows of the LoadMatrix, stored into every rank's copy
+// (peer-mapped) -- the all-gather of the histogram without a collective library
 __global__ void slot_histogram_kernel(const int32_t* chunk_counts, int chunks_per_slot, int E,
-                                      int m, int64_t* out) {
+                                      int m, int64_t* const* out_ptrs, int D, int row0) {
   const int cell = blockIdx.x * blockDim.x + threadIdx.x;
   if (cell >= m * E) return;
   const int v = cell / E, e = cell % E;
   int64_t s = 0;
   for (int c = 0; c < chunks_per_slot; ++c)
     s += chunk_counts[(size_t)(v * chunks_per_slot + c) * E + e];
-  out[(size_t)v * E + e] = s;
+  for (int r = 0; r < D; ++r) out_ptrs[r][(size_t)(row0 + v) * E + e] = s;
 }
 
 // ---------------------------------------------------------------------------
@@ -397,15 +399,15 @@ extern "C" int pp_route_topk(const void* x, const void* wg, const float* bias, i
 }
 
 extern "C" int pp_slot_histogram(const int32_t* chunk_counts, int32_t T, int32_t E, int32_t m,
-                                 int64_t* out, int32_t row0, void* stream) {
-  PP_CHECK_ARG(chunk_counts && out, "pp_slot_histogram: null pointer");
+                                 int64_t* const* out_ptrs, int32_t D, int32_t row0, void* stream) {
+  PP_CHECK_ARG(chunk_counts && out_ptrs && D >= 1, "pp_slot_histogram: bad arguments");
   PP_CHECK_ARG(m >= 1 && T % (m * PP_CHUNK) == 0,
                "pp_slot_histogram: T=%d must split into m=%d slots of whole %d-token chunks", T, m,
                PP_CHUNK);
   const int cps = (T / m) / PP_CHUNK;
   const int cells = m * E;
-  slot_histogram_kernel<<<(cells + 255) / 256, 256, 0, as_stream(stream)>>>(
-      chunk_counts, cps, E, m, out + (size_t)row0 * E);
+  slot_histogram_kernel<<<(cells + 255) / 256, 256, 0, as_stream(stream)>>>(chunk_counts, cps, E, m,
+                                                                            out_ptrs, D, row0);
   PP_LAUNCH_CHECK();
   return PP_OK;
 }

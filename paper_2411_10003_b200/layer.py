@@ -220,7 +220,8 @@ class MoELayer(torch.nn.Module):
         self.w = torch.empty((T, k), dtype=torch.float32, device=dev)
         self.probs = torch.empty((T, E), dtype=torch.float32, device=dev)
         self.chunk_counts = torch.empty((C, E), **i32)
-        self.counts = torch.zeros((E, E), dtype=torch.int64, device=dev)  # virtual-slot LoadMatrix
+        self.counts_buf = PeerBuffer((E, E), torch.int64, self.group, dev)  # virtual-slot LoadMatrix
+        self.counts = self.counts_buf.local
         self.chunk_base = torch.empty((C, E), **i32)
         self.slot_dest = torch.empty((self.m, E), **i32)
         self.groups = torch.zeros((self.max_groups, 8), **i32)
@@ -317,11 +318,9 @@ class MoELayer(torch.nn.Module):
         _lib.call("pp_route_topk", x.data_ptr(), self.wg.data_ptr(), self.gate_bias.data_ptr(), T, d,
                   E, k, self.idx.data_ptr(), self.w.data_ptr(), self.probs.data_ptr(),
                   self.rank_in_chunk.data_ptr(), self.chunk_counts.data_ptr(), sp)
-        _lib.call("pp_slot_histogram", self.chunk_counts.data_ptr(), T, E, m, self.counts.data_ptr(),
-                  self.rank * m, sp)
-        if self.world > 1:
-            mine = self.counts[self.rank * m: (self.rank + 1) * m].clone()
-            dist.all_gather_into_tensor(self.counts, mine, group=self.group)
+        _lib.call("pp_slot_histogram", self.chunk_counts.data_ptr(), T, E, m, self.counts_buf.ptrs.data_ptr(),
+                  self.world, self.rank * m, sp)
+        self.barrier()  # every rank's rows of the LoadMatrix have landed
         mask_ptr = self.mask_cur.data_ptr() if self.mask_cur is not None else None
         _lib.call("pp_dispatch_layout", self.counts.data_ptr(), mask_ptr, self.chunk_counts.data_ptr(),
                   self.world, m, E, T, self.rank, self.max_groups, self.rows_cap,
@@ -655,7 +654,8 @@ class MoELayer(torch.nn.Module):
                      expert=int(r[4]), src_rank=int(r[5])) for r in t]
 
     def close(self) -> None:
-        for b in (self.w1_arena, self.w2_arena, self.g1_arena, self.g2_arena, self.xp, self.yp, self.dyp, self.dxp):
+        for b in (self.w1_arena, self.w2_arena, self.g1_arena, self.g2_arena, self.xp, self.yp, self.dyp, self.dxp,
+                  self.counts_buf):
             b.close()
 
 
