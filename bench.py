@@ -291,6 +291,8 @@ def main() -> None:
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-only", action="store_true", help="short run for ncu (no CPU legs)")
     ap.add_argument("--eager", action="store_true", help="no CUDA graph for the N == 1 timed region")
+    ap.add_argument("--policy", default="greedy-overlap",
+                    help="vanilla | top<m> | greedy | greedy-overlap (reference simulator policies)")
     args = ap.parse_args()
     world_env = int(os.environ.get("WORLD_SIZE", "1"))
     # one bench workload for every N (weak scaling of the same per-GPU work): BASELINE
@@ -335,8 +337,8 @@ def main() -> None:
             dist.destroy_process_group()
         return
     E, k, d, f, T = cfg["E"], cfg["k"], cfg["d"], cfg["f"], cfg["T"]
-    planner = pp.PlannerConfig(n=1, alpha=0.5, reuse_interval=1, overlap_aware=True)
-    layer = pp.MoELayer(d, f, E, k, tokens=T, group=group, planner=planner, seed=0)
+    planner = pp.PlannerConfig(n=1, alpha=0.5, reuse_interval=1, overlap_aware=args.policy != "greedy")
+    layer = pp.MoELayer(d, f, E, k, tokens=T, group=group, planner=planner, seed=0, policy=args.policy)
     layer.set_gate_bias(zipf_bias(E, 1.2, 0))
     g = torch.Generator(device="cpu").manual_seed(1000 + rank)
     x = torch.randn((T, d), generator=g).to(dev, torch.bfloat16)
@@ -554,7 +556,7 @@ def main() -> None:
             "config": {"workload": f"{cfg_name}: {cfg['desc']}", "experts": E, "top_k": k, "d_model": d,
                        "d_ff": f, "tokens_per_gpu": T, "parallelism": f"ep{world}",
                        "l2": "working set > L2 (activations+weights >> 126 MB), no flush",
-                       "routing": "Zipf(1.2) gate bias, random bf16 tokens"},
+                       "routing": "Zipf(1.2) gate bias, random bf16 tokens", "policy": args.policy},
             "host_enqueue_ms_per_step": host_ms, "phase_ms_rank0": phases,
             "timed_region": "CUDA-graph replay of fwd+bwd" if use_graph else "eager stream-ordered fwd+bwd",
             "roofline": roofline, "cpu_baseline": cpu_info, "e2e": e2e, "gpu_launches": launches,

@@ -76,6 +76,12 @@ int pp_plan_greedy(const int64_t* counts, int32_t num_layers, int32_t E,
                    uint8_t* mask, int64_t* H, int64_t* R, double* best_cost,
                    void* stream);
 
+/* Top-m baseline (reference simulator._top_m_placement, simulator.py:318-324):
+ * mask [D][E] with the m heaviest experts (column totals, ties -> lower index)
+ * on every device; selected [m] (nullable) in that order. */
+int pp_top_m_mask(const int64_t* counts, int32_t D, int32_t E, int32_t m_top, uint8_t* mask,
+                  int32_t* selected, void* stream);
+
 /* counts [D][E] int64, mask [D][E] uint8 -> H [D], R [D] int64.  E <= D. */
 int pp_derive_loads(const int64_t* counts, const uint8_t* mask, int32_t D, int32_t E,
                     int64_t* H, int64_t* R, void* stream);

@@ -131,6 +131,16 @@ def greedy_search(counts, n: int, alpha: float, overlap_aware: bool, cm: dict) -
             "mask": mask, "H": Hf, "R": Rf}
 
 
+def top_m_mask(counts: np.ndarray, m: int) -> np.ndarray:
+    """reference simulator._top_m_placement (simulator.py:318-324): the m experts
+    with the largest column totals (ties -> lower index) on every device."""
+    counts = np.asarray(counts, dtype=np.int64)
+    D, E = counts.shape
+    totals = counts.sum(axis=0)
+    order = sorted(range(E), key=lambda e: (-int(totals[e]), e))
+    return replica_mask(D, E, tuple(order[:m]), tuple(frozenset() for _ in range(m)))
+
+
 def plan_for_iteration(history, iter_index: int, reuse_interval: int, planner):
     """reference planner.py:132-156; ``planner(counts)`` runs the search."""
     anchor = (iter_index // reuse_interval) * reuse_interval

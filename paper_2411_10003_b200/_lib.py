@@ -63,6 +63,7 @@ SIGNATURES = {
     "pp_version": [],
     "pp_plan_greedy": [P, I, I, POINTER(CostModel), POINTER(PlannerCfg), P, P, P, P, P, P, P, P],
     "pp_derive_loads": [P, P, I, I, P, P, P],
+    "pp_top_m_mask": [P, I, I, I, P, P, P],
     "pp_route_topk": [P, P, P, I, I, I, I, P, P, P, P, P, P],
     "pp_slot_histogram": [P, I, I, I, P, I, I, P],
     "pp_dispatch_layout": [P, P, P, I, I, I, I, I, I, I, P, P, P, P, P, P, P, P],
@@ -128,7 +129,7 @@ def check(rc: int, what: str = "") -> None:
 
 # kernels each entry point launches (for the bench's gpu_launches claim)
 KERNELS_PER_CALL = {
-    "pp_plan_greedy": 1, "pp_derive_loads": 1, "pp_route_topk": 1, "pp_slot_histogram": 1,
+    "pp_plan_greedy": 1, "pp_derive_loads": 1, "pp_top_m_mask": 1, "pp_route_topk": 1, "pp_slot_histogram": 1,
     "pp_dispatch_layout": 1, "pp_dispatch": 1, "pp_combine": 1, "pp_combine_bwd": 1,
     "pp_dispatch_bwd": 1, "pp_gate_bwd": 2, "pp_grouped_gemm": 1, "pp_replica_trans": 1,
     "pp_replica_agg": 1, "pp_peer_barrier": 1, "pp_agg_accumulate": 1,

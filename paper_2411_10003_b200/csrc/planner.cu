@@ -235,9 +235,39 @@ __global__ void derive_loads_kernel(const int64_t* counts, const uint8_t* mask, 
   }
 }
 
+// top-m baseline policy (reference simulator._top_m_placement, simulator.py:318-324):
+// the m experts with the largest column totals (ties -> lower index) go to every
+// device (empty excluded sets); all other experts stay home.
+__global__ void top_m_mask_kernel(const int64_t* counts, int D, int E, int m_top, uint8_t* mask,
+                                  int32_t* selected) {
+  extern __shared__ int64_t tot[];
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    int64_t s = 0;
+    for (int d = 0; d < D; ++d) s += counts[(size_t)d * E + e];
+    tot[e] = s;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    int rank = 0;  // position in the order (-total, e)
+    for (int j = 0; j < E; ++j) rank += (tot[j] > tot[e]) || (tot[j] == tot[e] && j < e);
+    const bool chosen = rank < m_top;
+    if (chosen && selected) selected[rank] = e;
+    for (int d = 0; d < D; ++d) mask[(size_t)d * E + e] = chosen || d == e;
+  }
+}
+
 }  // namespace pp
 
 using namespace pp;
+
+extern "C" int pp_top_m_mask(const int64_t* counts, int32_t D, int32_t E, int32_t m_top,
+                             uint8_t* mask, int32_t* selected, void* stream) {
+  PP_CHECK_ARG(counts && mask && D >= E && E >= 1 && E <= 4096, "pp_top_m_mask: bad arguments");
+  PP_CHECK_ARG(m_top >= 1 && m_top <= E, "top-m policy needs 1 <= m <= E, got %d", m_top);
+  top_m_mask_kernel<<<1, 256, sizeof(int64_t) * E, as_stream(stream)>>>(counts, D, E, m_top, mask, selected);
+  PP_LAUNCH_CHECK();
+  return PP_OK;
+}
 
 extern "C" int pp_plan_greedy(const int64_t* counts, int32_t num_layers, int32_t E,
                               const pp_cost_model* cm, const pp_planner_cfg* cfg,

@@ -160,7 +160,8 @@ class MoELayer(torch.nn.Module):
     def __init__(self, d_model: int, d_ff: int, num_experts: int, top_k: int, tokens: int,
                  group=None, planner: PlannerConfig | None = None, cluster=None, model=None,
                  capacity_rows: int | None = None, max_replicas: int | None = None,
-                 seed: int = 0, device=None, trans_ctas: int = 16, replica_engine: str = "copy") -> None:
+                 seed: int = 0, device=None, trans_ctas: int = 16, replica_engine: str = "copy",
+                 policy: str | None = None) -> None:
         super().__init__()
         if not torch.cuda.is_available():
             raise RuntimeError("MoELayer needs a CUDA device (B200); there is no CPU path")
@@ -258,6 +259,21 @@ class MoELayer(torch.nn.Module):
         # no SMs taken from the GEMMs); 'sm': device-driven pull kernels (no host
         # knowledge of the plan needed)
         self.replica_engine = replica_engine
+        # policy (reference simulator.py:54-103): None/"greedy"/"greedy-overlap" = Pro-Prophet
+        # planner (overlap_aware from `planner`), "vanilla" = plain EP, "top<m>" = the m
+        # heaviest experts of the CURRENT iteration broadcast to every rank (device-side mask)
+        self.top_m = 0
+        if policy is not None and policy not in ("greedy", "greedy-overlap"):
+            if policy == "vanilla":
+                self.plan_enabled = False
+            elif policy.startswith("top") and policy[3:].isdigit() and int(policy[3:]) >= 1:
+                self.plan_enabled = False
+                self.top_m = int(policy[3:])
+                self.replica_engine = "sm"  # the mask only exists on the device mid-forward
+                self._topm_mask = torch.zeros((E, E), dtype=torch.uint8, device=dev)
+            else:
+                raise ValidationError(f"unknown policy {policy!r}; valid: vanilla, top<m>, greedy, greedy-overlap")
+        self.policy = policy or ("greedy-overlap" if self.planner_cfg.overlap_aware else "greedy")
         self._plan_pending = None
         self._mask_host = torch.zeros((E, E), dtype=torch.uint8).pin_memory() if D > 1 else None
         self.mask_cur_host = None
@@ -321,6 +337,10 @@ class MoELayer(torch.nn.Module):
         _lib.call("pp_slot_histogram", self.chunk_counts.data_ptr(), T, E, m, self.counts_buf.ptrs.data_ptr(),
                   self.world, self.rank * m, sp)
         self.barrier()  # every rank's rows of the LoadMatrix have landed
+        if self.top_m and self.world > 1:
+            _lib.call("pp_top_m_mask", self.counts.data_ptr(), E, E, self.top_m, self._topm_mask.data_ptr(),
+                      None, sp)
+            self.mask_cur = self._topm_mask
         mask_ptr = self.mask_cur.data_ptr() if self.mask_cur is not None else None
         _lib.call("pp_dispatch_layout", self.counts.data_ptr(), mask_ptr, self.chunk_counts.data_ptr(),
                   self.world, m, E, T, self.rank, self.max_groups, self.rows_cap,
@@ -426,7 +446,9 @@ class MoELayer(torch.nn.Module):
             return self._trans_done
         self._trans_issued = True
         self._trans_done = None
-        if self.world == 1 or self.mask_cur is None or not self.replica_experts:
+        if self.world == 1 or self.mask_cur is None:
+            return None
+        if self.replica_engine == "copy" and not self.replica_experts:
             return None
         ev = torch.cuda.Event()
         ev.record()
@@ -556,6 +578,8 @@ class MoELayer(torch.nn.Module):
         self.begin_iteration()
         if self.replica_engine == "copy":  # host-derived copies: start before routing
             trans_done = self.issue_trans()  # no-op if a scheduler already issued it earlier
+        if self.top_m:
+            self._trans_issued = False  # a fresh top-m placement every iteration
         self._route_and_layout(x)
         if self.replica_engine == "sm":  # device-driven pulls read this iteration's group table
             trans_done = self.issue_trans()

@@ -38,7 +38,9 @@ def main():
     mo = pp.ModelSpec(E, 1, k, 2 * d, 1e3, 1e3)
     layer = pp.MoELayer(d, f, E, k, tokens=T, group=dist.group.WORLD,
                         planner=pp.PlannerConfig(n=1, alpha=0.5), cluster=cl, model=mo, seed=0,
-                        replica_engine=os.environ.get("PP_ENGINE", "copy"))
+                        replica_engine=os.environ.get("PP_ENGINE", "copy"),
+                        policy=os.environ.get("PP_POLICY") or None)
+    policy = os.environ.get("PP_POLICY") or "greedy"
     _, wg = M.exact_inputs(16, d, E, seed=99)
     bias = torch.round(torch.log(torch.tensor([1.0 / (i + 1) ** 1.2 for i in range(E)])) * 4) / 4
     with torch.no_grad():
@@ -56,7 +58,7 @@ def main():
         dy = (torch.randn((T, d), generator=torch.Generator().manual_seed(7 + it * 31 + rank)) * 0.1).to(torch.bfloat16)
         xd = x.to(dev).requires_grad_(True)
         y = layer(xd)
-        mask_used = layer.current_mask() if it > 0 else None  # the plan this forward ran with
+        mask_used = layer.current_mask() if (it > 0 or policy.startswith("top")) else None  # plan used
         y.backward(dy.to(dev))
         layer.wait_grads()
         torch.cuda.synchronize()
@@ -68,7 +70,14 @@ def main():
         dist.all_gather_object(allrec, rec)
         if rank == 0:
             counts = allrec[0]["counts"].numpy()
-            if it > 0:
+            if policy.startswith("top"):
+                exp_mask = P.top_m_mask(counts, int(policy[3:]))
+                if not np.array_equal(mask_used, exp_mask):
+                    print(f"[it {it}] TOP-M MASK MISMATCH", flush=True)
+                    ok = False
+            elif policy == "vanilla":
+                pass
+            elif it > 0:
                 # plan_for_iteration: iteration it uses greedy(history[it-1])
                 cm = P.cost_model_dict(E, k, 2 * d, 1e3, 1e3, 1e11, 1e6)
                 exp = P.greedy_search(prev_counts, 1, 0.5, False, cm)

@@ -179,3 +179,33 @@ def test_no_cpu_fallback_without_gpu():
                          pp.ClusterSpec(3, 1e9, 1e3), pp.ModelSpec(3, 1, 1, 1e6, 1e5, 1e5))
     with pytest.raises(RuntimeError):
         pp.MoELayer(256, 512, 16, 2, tokens=2048)
+
+
+def test_trace_jsonl_matches_reference_format(tmp_path, rng):
+    from paper_2411_10003_b200 import trace as tr
+
+    recs = []
+    for it in range(3):
+        for layer in range(2):
+            p = rng.dirichlet(np.ones(8))
+            counts = np.stack([rng.multinomial(64, p) for _ in range(8)])
+            recs.append(tr.TraceRecord(it, layer, pp.LoadMatrix(counts)))
+    ours = tmp_path / "ours.jsonl"
+    tr.write_trace(recs, ours)
+    back = tr.read_trace(ours)
+    assert [(r.iteration, r.layer, r.load) for r in back] == [(r.iteration, r.layer, r.load) for r in recs]
+    bad = tmp_path / "bad.jsonl"
+    bad.write_text('{"iter": 0, "layer": 0}\n')
+    with pytest.raises(tr.TraceFormatError):
+        tr.read_trace(bad)
+    from conftest import import_reference
+
+    ref = import_reference()
+    from moebal import workload
+
+    theirs = tmp_path / "theirs.jsonl"
+    workload.write_trace([workload.TraceRecord(r.iteration, r.layer, ref.LoadMatrix(r.load.counts)) for r in recs],
+                         theirs)
+    assert ours.read_bytes() == theirs.read_bytes()  # byte-identical JSONL
+    parsed = workload.read_trace(ours)  # the reference replays our traces
+    assert [r.load.counts.tolist() for r in parsed] == [r.load.counts.tolist() for r in recs]
