@@ -407,10 +407,29 @@ def main() -> None:
     torch.cuda.synchronize()
     launches = _lib.launch_count()  # kernels of ours per K steps (same kernels the graph replays)
     layer.phase_log = []
-    for i in range(2):
+    calib_samples = []
+    n_phase_steps = 6 if world > 1 else 2
+    for i in range(n_phase_steps):
         step(xs[i % 2].detach(), dy)
+        if world > 1:  # loads under the plan this step ran with (device derive_loads)
+            lm = layer.last_load_matrix()
+            mask = layer.current_mask()
+            calib_samples.append((lm.counts.copy(), mask.copy()))
     torch.cuda.synchronize()
     phases = layer.phase_breakdown()
+    calibration = None
+    if world > 1 and not args.profile_only:
+        from paper_2411_10003_b200 import _device as dv
+        from paper_2411_10003_b200 import calibrate
+
+        steps_ph = calibrate.per_step_phases(layer.phase_log)
+        samples = []
+        for (counts_np, mask_np), ph in zip(calib_samples, steps_ph):
+            H, R = dv.derive_loads(counts_np, mask_np.astype("uint8"))  # pp_derive_loads kernel
+            samples.append((H, R, calibrate.measured_costs(ph)))
+        calibration = calibrate.fit(samples, input_bytes=2 * d)
+        calibration["note"] = ("fit of the reference model's B and t to this run's measured phases "
+                               "(virtual-slot H/R, rank 0); plan objective uses these units")
     layer.phase_log = None
 
     # ---- roofline of the grouped tcgen05 GEMM family (dominant kernel)
@@ -561,6 +580,7 @@ def main() -> None:
             "timed_region": "CUDA-graph replay of fwd+bwd" if use_graph else "eager stream-ordered fwd+bwd",
             "roofline": roofline, "cpu_baseline": cpu_info, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk_summary, "planner": planner_info, "imbalance": imbalance,
+            "cost_model_calibration": calibration,
         }
         print(json.dumps(out), flush=True)
     if world > 1:
