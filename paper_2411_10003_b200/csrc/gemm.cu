@@ -155,9 +155,10 @@ constexpr bool tma_out() {
 // Stage a 32x32 bf16 block (row = lane, 16-byte chunk j) with the SWIZZLE_64B
 // pattern the output tensor map uses, then one lane TMA-stores it.  The
 // staging buffer is reused only after the previous store finished reading it.
+template <int PENDING = 0>
 __device__ __forceinline__ void stage_and_store(uint8_t* stage, const uint4 (&v)[4], const void* tmap,
                                                 int col, int row, int lane) {
-  if (lane == 0) bulk_wait_read0();
+  if (lane == 0) bulk_wait_read<PENDING>();
   __syncwarp();
 #pragma unroll
   for (int j = 0; j < 4; ++j)
