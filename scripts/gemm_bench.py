@@ -34,7 +34,8 @@ sel = sys.argv[1:] or list(modes)
 flops = 2.0 * T * k * d * f
 for name in sel:
     mode, a, b, c, c2 = modes[name]
-    run = lambda: _device.grouped_gemm(mode, a, b, c, c2, groups, ng, E, cap, E, d, f)  # noqa: E731
+    nsm = int(__import__("os").environ.get("GEMM_SMS", "0"))
+    run = lambda: _device.grouped_gemm(mode, a, b, c, c2, groups, ng, E, cap, E, d, f, num_sms=nsm)  # noqa: E731
     for _ in range(3):
         run()
     torch.cuda.synchronize()
