@@ -291,6 +291,8 @@ def main() -> None:
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-only", action="store_true", help="short run for ncu (no CPU legs)")
     ap.add_argument("--eager", action="store_true", help="no CUDA graph for the N == 1 timed region")
+    ap.add_argument("--alpha", type=float, default=0.5, help="planner balance coefficient (Eq. 8)")
+    ap.add_argument("--n-excl", type=int, default=1, help="planner n: devices a selected expert skips")
     ap.add_argument("--policy", default="greedy-overlap",
                     help="vanilla | top<m> | greedy | greedy-overlap (reference simulator policies)")
     args = ap.parse_args()
@@ -337,7 +339,8 @@ def main() -> None:
             dist.destroy_process_group()
         return
     E, k, d, f, T = cfg["E"], cfg["k"], cfg["d"], cfg["f"], cfg["T"]
-    planner = pp.PlannerConfig(n=1, alpha=0.5, reuse_interval=1, overlap_aware=args.policy != "greedy")
+    planner = pp.PlannerConfig(n=args.n_excl, alpha=args.alpha, reuse_interval=1,
+                               overlap_aware=args.policy != "greedy")
     layer = pp.MoELayer(d, f, E, k, tokens=T, group=group, planner=planner, seed=0, policy=args.policy)
     layer.set_gate_bias(zipf_bias(E, 1.2, 0))
     g = torch.Generator(device="cpu").manual_seed(1000 + rank)
@@ -431,6 +434,15 @@ def main() -> None:
         calibration["note"] = ("fit of the reference model's B and t to this run's measured phases "
                                "(virtual-slot H/R, rank 0); plan objective uses these units")
     layer.phase_log = None
+
+    # ---- physical balance: expert-GEMM rows computed per rank under the plan used
+    rows_rank = torch.tensor([float(layer.total_real_rows())], dtype=torch.float64, device=dev)
+    if world > 1:
+        all_rows = [torch.zeros_like(rows_rank) for _ in range(world)]
+        dist.all_gather(all_rows, rows_rank)
+        phys_rows = [int(r.item()) for r in all_rows]
+    else:
+        phys_rows = [int(rows_rank.item())]
 
     # ---- roofline of the grouped tcgen05 GEMM family (dominant kernel)
     gemm = layer.collect_gemm_timing()
@@ -575,12 +587,14 @@ def main() -> None:
             "config": {"workload": f"{cfg_name}: {cfg['desc']}", "experts": E, "top_k": k, "d_model": d,
                        "d_ff": f, "tokens_per_gpu": T, "parallelism": f"ep{world}",
                        "l2": "working set > L2 (activations+weights >> 126 MB), no flush",
-                       "routing": "Zipf(1.2) gate bias, random bf16 tokens", "policy": args.policy},
+                       "routing": "Zipf(1.2) gate bias, random bf16 tokens", "policy": args.policy,
+                       "planner": {"n": args.n_excl, "alpha": args.alpha, "reuse_interval": 1}},
             "host_enqueue_ms_per_step": host_ms, "phase_ms_rank0": phases,
             "timed_region": "CUDA-graph replay of fwd+bwd" if use_graph else "eager stream-ordered fwd+bwd",
             "roofline": roofline, "cpu_baseline": cpu_info, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk_summary, "planner": planner_info, "imbalance": imbalance,
             "cost_model_calibration": calibration,
+            "rows_per_rank": {"rows": phys_rows, "max_over_mean": max(phys_rows) / (sum(phys_rows) / len(phys_rows))},
         }
         print(json.dumps(out), flush=True)
     if world > 1:
