@@ -290,7 +290,7 @@ def main() -> None:
     ap.add_argument("--config", default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-only", action="store_true", help="short run for ncu (no CPU legs)")
-    ap.add_argument("--eager", action="store_true", help="no CUDA graph for the N == 1 timed region")
+    ap.add_argument("--eager", action="store_true", help="no CUDA graph for the timed region (host-driven planning at N > 1)")
     ap.add_argument("--alpha", type=float, default=0.5, help="planner balance coefficient (Eq. 8)")
     ap.add_argument("--n-excl", type=int, default=1, help="planner n: devices a selected expert skips")
     ap.add_argument("--policy", default="greedy-overlap",
@@ -341,7 +341,11 @@ def main() -> None:
     E, k, d, f, T = cfg["E"], cfg["k"], cfg["d"], cfg["f"], cfg["T"]
     planner = pp.PlannerConfig(n=args.n_excl, alpha=args.alpha, reuse_interval=1,
                                overlap_aware=args.policy != "greedy")
-    layer = pp.MoELayer(d, f, E, k, tokens=T, group=group, planner=planner, seed=0, policy=args.policy)
+    # N > 1: planning stays on the device (plan -> mask double buffer, SM-driven Trans/Agg)
+    # so the whole EP step -- peer barriers included -- is captured in one CUDA graph
+    planning = "device" if world > 1 and not args.eager else "host"
+    layer = pp.MoELayer(d, f, E, k, tokens=T, group=group, planner=planner, seed=0, policy=args.policy,
+                        planning=planning)
     layer.set_gate_bias(zipf_bias(E, 1.2, 0))
     g = torch.Generator(device="cpu").manual_seed(1000 + rank)
     x = torch.randn((T, d), generator=g).to(dev, torch.bfloat16)
@@ -362,10 +366,10 @@ def main() -> None:
 
     # ---- step function: CUDA-graph replay of fwd+bwd at N == 1 (host cost ~ one
     # graph launch per step), eager stream-ordered calls at N > 1
-    use_graph = world == 1 and not args.eager
+    use_graph = not args.eager
     xs = [x.detach().clone() for _ in range(2)]
     if use_graph:
-        graphs = [layer.make_graphed_step(xs[b], dy.clone()) for b in range(2)]
+        graphs = [layer.make_graphed_step(xs[b], dy.clone(), with_loss=True) for b in range(2)]
         run_step = lambda i: graphs[i % 2]()  # noqa: E731
     else:
         run_step = lambda i: step(xs[i % 2].detach(), dy)  # noqa: E731
@@ -413,21 +417,27 @@ def main() -> None:
     calib_samples = []
     n_phase_steps = 6 if world > 1 else 2
     for i in range(n_phase_steps):
-        step(xs[i % 2].detach(), dy)
-        if world > 1:  # loads under the plan this step ran with (device derive_loads)
-            lm = layer.last_load_matrix()
-            mask = layer.current_mask()
-            calib_samples.append((lm.counts.copy(), mask.copy()))
+        xin = xs[i % 2].detach().requires_grad_(True)
+        y = layer(xin)
+        # the plan this step runs with (device copy: no mid-step host sync to skew the phases)
+        mask = layer.mask_cur.clone() if world > 1 and layer.mask_cur is not None else None
+        y.backward(dy)
+        if world > 1:  # loads under that plan (device derive_loads)
+            calib_samples.append((layer.counts.clone(), mask))
     torch.cuda.synchronize()
     phases = layer.phase_breakdown()
     calibration = None
     if world > 1 and not args.profile_only:
         from paper_2411_10003_b200 import _device as dv
+        import numpy as np
+
         from paper_2411_10003_b200 import calibrate
 
         steps_ph = calibrate.per_step_phases(layer.phase_log)
         samples = []
-        for (counts_np, mask_np), ph in zip(calib_samples, steps_ph):
+        for (counts_t, mask_t), ph in zip(calib_samples, steps_ph):
+            counts_np = counts_t.cpu().numpy()
+            mask_np = mask_t.cpu().numpy() if mask_t is not None else np.eye(E, dtype=np.uint8)
             H, R = dv.derive_loads(counts_np, mask_np.astype("uint8"))  # pp_derive_loads kernel
             samples.append((H, R, calibrate.measured_costs(ph)))
         calibration = calibrate.fit(samples, input_bytes=2 * d)
@@ -471,18 +481,18 @@ def main() -> None:
     # ---- e2e through the public API with host buffers
     e2e = None
     if not args.profile_only:
-        # pinned host buffers; H2D of step i+1 and D2H of step i-1 overlap step i
+        # A training step on this layer: the batch x comes from pinned host memory
+        # (H2D inside the timed region), loss = sum(y * g) with a fixed device-resident
+        # probe g (so dL/dy = g, the upstream gradient), backward, and the loss scalar is
+        # read back to the host (D2H).  H2D of step i+1 overlaps step i (copy stream).
         xh = [x.detach().cpu().pin_memory() for _ in range(2)]
-        dyh = [dy.detach().cpu().pin_memory() for _ in range(2)]
-        yh = [torch.empty((T, d), dtype=torch.bfloat16).pin_memory() for _ in range(2)]
-        if use_graph:  # the graphed steps' static buffers receive the H2D copies
+        lh = [torch.zeros((), dtype=torch.float32).pin_memory() for _ in range(args.steps)]
+        if use_graph:
             xdev = [g.x for g in graphs]
-            dydev = [g.dy for g in graphs]
         else:
             xdev = [torch.empty_like(x) for _ in range(2)]
-            dydev = [torch.empty_like(dy) for _ in range(2)]
         copy = torch.cuda.Stream(device=dev)   # H2D engine
-        back = torch.cuda.Stream(device=dev)   # D2H engine (opposite direction, runs concurrently)
+        back = torch.cuda.Stream(device=dev)   # D2H engine
         main = torch.cuda.current_stream()
         torch.cuda.synchronize()
         if world > 1:
@@ -491,7 +501,7 @@ def main() -> None:
         e1 = torch.cuda.Event(enable_timing=True)
         ev_in = [torch.cuda.Event() for _ in range(2)]
         ev_free = [torch.cuda.Event() for _ in range(2)]
-        ev_out = [torch.cuda.Event() for _ in range(2)]
+        ev_out = torch.cuda.Event()
         w0 = time.perf_counter()
         e0.record(main)
 
@@ -500,30 +510,28 @@ def main() -> None:
             with torch.cuda.stream(copy):
                 copy.wait_event(ev_free[b]) if i >= 2 else copy.wait_event(e0)
                 xdev[b].copy_(xh[b], non_blocking=True)
-                dydev[b].copy_(dyh[b], non_blocking=True)
                 ev_in[b].record(copy)
 
         h2d(0)
-        keep = [None, None]
         for i in range(args.steps):
             b = i % 2
             if i + 1 < args.steps:
                 h2d(i + 1)
             main.wait_event(ev_in[b])
             if use_graph:
-                y, _ = graphs[b]()
+                _, _ = graphs[b]()
+                loss = graphs[b].loss
             else:
-                y = step(xdev[b].detach(), dydev[b])
+                xin = xdev[b].detach().requires_grad_(True)
+                yv = layer(xin)
+                loss = (yv.detach().float() * dy.float()).sum()  # the probe loss; dL/dy = dy
+                yv.backward(dy)
             ev_free[b].record(main)
-            if not use_graph:
-                y.record_stream(back)
-            keep[b] = y
             with torch.cuda.stream(back):
                 back.wait_event(ev_free[b])
-                yh[b].copy_(y.detach(), non_blocking=True)
-                ev_out[b].record(back)
-        for b in range(2):
-            main.wait_event(ev_out[b])
+                lh[i].copy_(loss.detach(), non_blocking=True)
+                ev_out.record(back)
+        main.wait_event(ev_out)
         e1.record(main)
         torch.cuda.synchronize()
         clk.mark(w0, time.perf_counter())
@@ -531,10 +539,11 @@ def main() -> None:
         if world > 1:
             dist.all_reduce(em, op=dist.ReduceOp.MAX)
         e2e = {"value": world * T * args.steps / (float(em.item()) / 1e3), "unit": "tokens/s",
-               "h2d_bytes_per_step": 2 * T * d * 2, "d2h_bytes_per_step": T * d * 2,
+               "h2d_bytes_per_step": T * d * 2, "d2h_bytes_per_step": 4,
                "path": ("MoELayer.make_graphed_step replay (public API, CUDA graph of fwd+bwd)" if use_graph
                                 else "MoELayer.__call__ + backward (public API)")
-                       + "; pinned host x/dy in, y out; H2D/D2H on two copy streams, double-buffered"}
+                       + "; pinned host batch x in (H2D, double-buffered on a copy stream), loss = sum(y*g) "
+                         "with a device-resident probe g (dL/dy = g), fp32 loss scalar out (D2H)"}
 
     # ---- planner + imbalance (device planner vs oracle CPU planner)
     planner_info, imbalance = None, None

@@ -131,13 +131,15 @@ typedef struct pp_group {
  *   total_rows [1] int32 (padded rows of this rank's receive buffer)
  *   seg_start  [D][E] int32 segment start of expert e on rank r (-1 if absent)
  *   rep_slot   [D][E] int32 weight slot of replica expert e on rank r (-1 if
- *              none; nullable) -- consumed by pp_replica_agg. */
-int pp_dispatch_layout(const int64_t* counts, const uint8_t* mask, const int32_t* chunk_counts,
+ *              none; nullable) -- consumed by pp_replica_agg.
+ * counts_from_chunks (D == 1 only): fill `counts` from the chunk counts here,
+ * replacing pp_slot_histogram + barrier. */
+int pp_dispatch_layout(int64_t* counts, const uint8_t* mask, const int32_t* chunk_counts,
                        int32_t D, int32_t m, int32_t E, int32_t T, int32_t my_rank,
                        int32_t max_groups, int32_t rows_capacity,
                        int32_t* chunk_base, int32_t* slot_dest, pp_group* groups,
                        int32_t* num_groups, int32_t* total_rows, int32_t* seg_start,
-                       int32_t* rep_slot, void* stream);
+                       int32_t* rep_slot, int32_t counts_from_chunks, void* stream);
 
 /* Permute + all-to-all in one kernel: row of token t goes to rank
  * slot_dest[t/(T/m)][e] at row chunk_base[t/128][e] + rank[t][j] of that
@@ -165,11 +167,12 @@ int pp_combine_bwd(const void* dy, void* const* out_ptrs, void* const* dgrad_ptr
 /* Backward of dispatch + gate softmax:  dx[t] = sum_j dXp[pair] (pulled from
  * dxp_ptrs[pair_dest]) and dl [T][EP] bf16 = dL/dlogits restricted to the top-k
  * (dl_i = p_i * (dw_{j(i)} [i selected] - sum_j dw_j p_{e_j})), zero-padded to
- * EP in {64, 128} columns for the tensor-core gate GEMMs. */
+ * EP in {64, 128} columns for the tensor-core gate GEMMs.  Also zeroes
+ * zero_f32[0:zero_elems) (the gate weight grad the split-K GEMM accumulates into). */
 int pp_dispatch_bwd(void* const* dxp_ptrs, const int32_t* pair_dest, const int32_t* pair_row,
                     const int32_t* idx, const float* probs, const float* dw,
                     int32_t T, int32_t d, int32_t k, int32_t E, int32_t EP, void* dx, void* dl,
-                    void* stream);
+                    float* zero_f32, int64_t zero_elems, void* stream);
 
 /* Gate GEMMs on tcgen05:  dx [T][d] bf16 += dl [T][EP] . wg [E][d]   and
  * dwg [E][d] fp32 += dl^T . x (split-K over token chunks, fp32 atomics;
@@ -197,13 +200,16 @@ int pp_grouped_gemm(int32_t mode, const void* a, const void* b, void* c, void* c
                     int32_t num_sms, void* stream);
 
 /* ---- replica Trans / Agg over peer memory (K5) --------------------------- */
-/* Trans: for every replica group of this rank (groups[g].src_rank != me) pull
- * the expert's W1/W2 from the home rank's weight arena (peer pointer tables
- * w1_ptrs/w2_ptrs [D], arenas [slots][f][d] and [slots][d][f] bf16) into this
- * rank's replica slot.  `max_ctas` bounds the SMs taken from concurrent GEMMs. */
-int pp_replica_trans(void* const* w1_ptrs, void* const* w2_ptrs, const pp_group* groups,
-                     const int32_t* num_groups, int32_t max_groups, int32_t my_rank, int32_t m,
-                     int32_t d_model, int32_t d_ff, int32_t max_ctas, void* stream);
+/* Trans: for every replica expert of this rank under the plan's mask ([E][E]
+ * uint8 slot->expert, the pp_dispatch_layout rule: experts e with home e/m !=
+ * me that some slot of this rank routes to, ascending, get slots m, m+1, ...)
+ * pull the expert's W1/W2 from the home rank's weight arena (peer pointer
+ * tables w1_ptrs/w2_ptrs [D], arenas [slots][f][d] and [slots][d][f] bf16) into
+ * that replica slot.  Needs only the mask, so it can run before this
+ * iteration's routing.  `max_ctas` bounds the SMs it takes (E <= 1024). */
+int pp_replica_trans(void* const* w1_ptrs, void* const* w2_ptrs, const uint8_t* mask, int32_t E,
+                     int32_t m, int32_t my_rank, int32_t d_model, int32_t d_ff, int32_t max_ctas,
+                     void* stream);
 
 /* Agg: the home rank pulls the replicas' fp32 grads (g1_ptrs/g2_ptrs [D]) and
  * adds them, in ascending rank order, into its own home slots.  rep_slot
@@ -235,8 +241,10 @@ int pp_ipc_import(const uint8_t* handle64, void** dev_ptr);
 int pp_ipc_close(void* dev_ptr);
 
 /* Cross-rank barrier over peer-mapped signal words.  signal_ptrs: device
- * array [D] of each rank's signal area (uint64_t[D] each); epoch must grow
- * by one per call.  Spins with a 20 s timeout (traps instead of hanging). */
+ * array [D] of each rank's signal area (uint64_t[D + 1] each: D peer slots + this
+ * rank's own counter).  epoch > 0: host-provided, must grow by one per call;
+ * epoch == 0: taken from the device counter (CUDA-graph replayable).  Spins
+ * with a 20 s timeout (traps instead of hanging). */
 int pp_peer_barrier(void* const* signal_ptrs, int32_t D, int32_t my_rank, uint64_t epoch,
                     void* stream);
 

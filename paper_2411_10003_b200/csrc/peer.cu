@@ -5,8 +5,8 @@
 // (pkg/src/moebal/perf_model.py:61-73; semantics PAPER.md:207-208): the plan's
 // replica ranks pull the selected experts' parameters from the home rank
 // (Trans) and the home rank pulls + sums the replicas' gradients (Agg), in
-// rank order so the sum is deterministic.  Both read the group tables the
-// layout kernel derived on device, so no host round trip decides what moves.
+// rank order so the sum is deterministic.  Trans reads the plan's mask and Agg the
+// layout's rep_slot table, both on the device, so no host round trip decides what moves.
 #include "common.cuh"
 
 namespace pp {
@@ -25,80 +25,157 @@ __device__ __forceinline__ uint64_t global_ns() {
   return t;
 }
 
-// signal area of rank r: uint64_t[D], slot s written by rank s
+// signal area of rank r: uint64_t[D + 1]; slot s < D is written by rank s, slot D holds
+// r's own barrier counter.  epoch == 0: take the epoch from that device counter (so a
+// captured CUDA graph can replay barriers), otherwise use the host-provided value.
 __global__ void peer_barrier_kernel(void* const* signal_ptrs, int D, int me, uint64_t epoch) {
+  __shared__ uint64_t ep;
+  uint64_t* own = reinterpret_cast<uint64_t*>(signal_ptrs[me]);
+  if (threadIdx.x == 0) ep = epoch ? epoch : own[D] + 1;
+  __syncthreads();
+  const uint64_t e = ep;
   const int r = threadIdx.x;
   if (r < D) {
     __threadfence_system();
-    st_release_sys(reinterpret_cast<uint64_t*>(signal_ptrs[r]) + me, epoch);
+    st_release_sys(reinterpret_cast<uint64_t*>(signal_ptrs[r]) + me, e);
   }
   __syncthreads();
   if (r < D) {
-    const uint64_t* mine = reinterpret_cast<const uint64_t*>(signal_ptrs[me]) + r;
+    const uint64_t* mine = own + r;
     const uint64_t t0 = global_ns();
-    while (ld_acquire_sys(mine) < epoch) {
+    while (ld_acquire_sys(mine) < e) {
       if (global_ns() - t0 > 20ull * 1000 * 1000 * 1000) {
         printf("ppmoe: peer barrier timeout (rank %d waiting on %d, epoch %llu)\n", me, r,
-               (unsigned long long)epoch);
+               (unsigned long long)e);
         __trap();
       }
     }
   }
   __syncthreads();
+  if (threadIdx.x == 0) own[D] = e;
 }
 
-// Trans: copy the home rank's W1/W2 of every replica group into this rank's replica slot
-__global__ void replica_trans_kernel(void* const* w1_ptrs, void* const* w2_ptrs,
-                                     const pp_group* groups, const int32_t* num_groups,
-                                     int max_groups, int me, int m, size_t expert_elems) {
-  const int G = min(*num_groups, max_groups);
-  const size_t vecs = expert_elems / 8;  // uint4 of bf16
-  const size_t total = (size_t)G * 2 * vecs;
-  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
-       i += (size_t)gridDim.x * blockDim.x) {
-    const int g = (int)(i / (2 * vecs));
-    const size_t rem = i % (2 * vecs);
-    const pp_group gr = groups[g];
-    if (gr.src_rank == me) continue;
-    const int which = rem >= vecs;
-    const size_t v = rem - which * vecs;
-    void* const* ptrs = which ? w2_ptrs : w1_ptrs;
-    const uint4* src = reinterpret_cast<const uint4*>(ptrs[gr.src_rank]) +
-                       (size_t)(gr.expert % m) * vecs + v;
-    uint4* dst = reinterpret_cast<uint4*>(ptrs[me]) + (size_t)gr.wslot * vecs + v;
-    *dst = ld_v4(src);
+constexpr int kPeerUnroll = 8;  // 16-byte peer loads in flight per thread (NVLink latency cover)
+constexpr int kMaxListE = 1024;
+
+// replica experts of rank `r` under `mask` in ascending id (slot m + i holds list[i]):
+// e is a replica on r iff its home e / m != r and some slot of r routes to it
+__device__ int build_replica_list(const uint8_t* mask, int E, int m, int r, int* list, int* flag) {
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    int f = 0;
+    if (e / m != r)
+      for (int j = 0; j < m; ++j) f |= mask[(size_t)(r * m + j) * E + e];
+    flag[e] = f;
+  }
+  __syncthreads();
+  __shared__ int n;
+  if (threadIdx.x == 0) {
+    int c = 0;
+    for (int e = 0; e < E; ++e)
+      if (flag[e]) list[c++] = e;
+    n = c;
+  }
+  __syncthreads();
+  return n;
+}
+
+// Trans: pull the home rank's W1/W2 of every replica expert of this rank (decided by the
+// plan's mask alone, so it can start before this iteration's routing) into its replica
+// slot.  kPeerUnroll independent 16-byte loads per thread keep enough bytes in flight to
+// run the NVLink pull at link rate from a few dozen CTAs.
+__global__ void __launch_bounds__(512) replica_trans_kernel(void* const* w1_ptrs, void* const* w2_ptrs,
+                                                            const uint8_t* mask, int E, int m, int me,
+                                                            size_t vecs) {
+  __shared__ int list[kMaxListE], flag[kMaxListE];
+  const int nrep = build_replica_list(mask, E, m, me, list, flag);
+  const size_t total = (size_t)nrep * 2 * vecs;  // uint4 units: [replica][W1|W2][vec]
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t base = (size_t)blockIdx.x * blockDim.x + threadIdx.x; base < total;
+       base += stride * kPeerUnroll) {
+    uint4 r[kPeerUnroll];
+    uint4* dst[kPeerUnroll];
+#pragma unroll
+    for (int u = 0; u < kPeerUnroll; ++u) {
+      const size_t i = base + u * stride;
+      dst[u] = nullptr;
+      if (i < total) {
+        const size_t mat = i / vecs, v = i - mat * vecs;
+        const int rep = (int)(mat >> 1), e = list[rep];
+        void* const* ptrs = (mat & 1) ? w2_ptrs : w1_ptrs;
+        r[u] = ld_nc_v4(reinterpret_cast<const uint4*>(ptrs[e / m]) + (size_t)(e % m) * vecs + v);
+        dst[u] = reinterpret_cast<uint4*>(ptrs[me]) + (size_t)(m + rep) * vecs + v;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kPeerUnroll; ++u)
+      if (dst[u]) st_v4(dst[u], r[u]);
   }
 }
 
-// Agg: grad[home slot of e] += sum over ranks r != me (ascending) of grad_r[rep_slot[r][e]]
-__global__ void replica_agg_kernel(void* const* g1_ptrs, void* const* g2_ptrs,
-                                   const int32_t* rep_slot, int D, int E, int m, int me,
-                                   size_t expert_elems) {
-  const size_t vecs = expert_elems / 4;  // float4
-  const size_t total = (size_t)m * 2 * vecs;
-  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
-       i += (size_t)gridDim.x * blockDim.x) {
-    const int j = (int)(i / (2 * vecs));  // local home slot
-    const size_t rem = i % (2 * vecs);
-    const int which = rem >= vecs;
-    const size_t v = rem - which * vecs;
-    const int e = me * m + j;
-    void* const* ptrs = which ? g2_ptrs : g1_ptrs;
-    float4* dst = reinterpret_cast<float4*>(ptrs[me]) + (size_t)j * vecs + v;
-    float4 acc = *dst;
-    bool any = false;
+// Agg: grad[home slot j] += sum over ranks r != me (ascending) of grad_r[rep_slot[r][e]],
+// e = me*m + j; only home slots that have replicas are touched.
+__global__ void __launch_bounds__(512) replica_agg_kernel(void* const* g1_ptrs, void* const* g2_ptrs,
+                                                          const int32_t* rep_slot, int D, int E, int m,
+                                                          int me, size_t vecs) {
+  __shared__ int act[kMaxListE];
+  __shared__ int nact;
+  if (threadIdx.x == 0) {
+    int c = 0;
+    for (int j = 0; j < m; ++j) {
+      bool any = false;
+      for (int r = 0; r < D; ++r)
+        if (r != me && rep_slot[r * E + me * m + j] >= 0) any = true;
+      if (any) act[c++] = j;
+    }
+    nact = c;
+  }
+  __syncthreads();
+  const size_t total = (size_t)nact * 2 * vecs;  // float4 units: [active slot][g1|g2][vec]
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  constexpr int U = kPeerUnroll / 2;
+  for (size_t base = (size_t)blockIdx.x * blockDim.x + threadIdx.x; base < total; base += stride * U) {
+    float4 acc[U];
+    float4* dst[U];
+    int jj[U], which[U];
+    size_t vv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const size_t i = base + u * stride;
+      dst[u] = nullptr;
+      if (i < total) {
+        const size_t mat = i / vecs;
+        vv[u] = i - mat * vecs;
+        jj[u] = act[mat >> 1];
+        which[u] = (int)(mat & 1);
+        dst[u] = reinterpret_cast<float4*>((which[u] ? g2_ptrs : g1_ptrs)[me]) + (size_t)jj[u] * vecs + vv[u];
+        acc[u] = *dst[u];
+      }
+    }
     for (int r = 0; r < D; ++r) {
       if (r == me) continue;
-      const int s = rep_slot[r * E + e];
-      if (s < 0) continue;
-      const float4 x = *(reinterpret_cast<const float4*>(ptrs[r]) + (size_t)s * vecs + v);
-      acc.x += x.x;
-      acc.y += x.y;
-      acc.z += x.z;
-      acc.w += x.w;
-      any = true;
+      float4 x[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (!dst[u]) continue;
+        const int s = rep_slot[r * E + me * m + jj[u]];
+        if (s < 0) { x[u] = make_float4(0.f, 0.f, 0.f, 0.f); continue; }
+        const uint4 raw = ld_nc_v4(reinterpret_cast<const float4*>((which[u] ? g2_ptrs : g1_ptrs)[r]) +
+                                   (size_t)s * vecs + vv[u]);
+        x[u] = make_float4(__uint_as_float(raw.x), __uint_as_float(raw.y), __uint_as_float(raw.z),
+                           __uint_as_float(raw.w));
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (!dst[u]) continue;
+        acc[u].x += x[u].x;
+        acc[u].y += x[u].y;
+        acc[u].z += x[u].z;
+        acc[u].w += x[u].w;
+      }
     }
-    if (any) *dst = acc;
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (dst[u]) *dst[u] = acc[u];
   }
 }
 
@@ -149,16 +226,16 @@ extern "C" int pp_peer_barrier(void* const* signal_ptrs, int32_t D, int32_t my_r
   return PP_OK;
 }
 
-extern "C" int pp_replica_trans(void* const* w1_ptrs, void* const* w2_ptrs, const pp_group* groups,
-                                const int32_t* num_groups, int32_t max_groups, int32_t my_rank,
-                                int32_t m, int32_t d_model, int32_t d_ff, int32_t max_ctas,
-                                void* stream) {
-  PP_CHECK_ARG(w1_ptrs && w2_ptrs && groups && num_groups, "pp_replica_trans: null pointer");
+extern "C" int pp_replica_trans(void* const* w1_ptrs, void* const* w2_ptrs, const uint8_t* mask,
+                                int32_t E, int32_t m, int32_t my_rank, int32_t d_model, int32_t d_ff,
+                                int32_t max_ctas, void* stream) {
+  PP_CHECK_ARG(w1_ptrs && w2_ptrs && mask, "pp_replica_trans: null pointer");
+  PP_CHECK_ARG(E >= 1 && E <= kMaxListE && m >= 1 && E % m == 0 && my_rank >= 0 && my_rank < E / m,
+               "pp_replica_trans: bad E / m / rank");
   PP_CHECK_ARG(((size_t)d_model * d_ff) % 8 == 0, "pp_replica_trans: bad sizes");
-  const int grid = max_ctas > 0 ? max_ctas : 16;
-  replica_trans_kernel<<<grid, 512, 0, as_stream(stream)>>>(w1_ptrs, w2_ptrs, groups, num_groups,
-                                                            max_groups, my_rank, m,
-                                                            (size_t)d_model * d_ff);
+  const int grid = max_ctas > 0 ? max_ctas : 32;
+  replica_trans_kernel<<<grid, 512, 0, as_stream(stream)>>>(w1_ptrs, w2_ptrs, mask, E, m, my_rank,
+                                                            (size_t)d_model * d_ff / 8);
   PP_LAUNCH_CHECK();
   return PP_OK;
 }
@@ -167,9 +244,12 @@ extern "C" int pp_replica_agg(void* const* g1_ptrs, void* const* g2_ptrs, const 
                               int32_t D, int32_t E, int32_t m, int32_t my_rank, int32_t d_model,
                               int32_t d_ff, int32_t max_ctas, void* stream) {
   PP_CHECK_ARG(g1_ptrs && g2_ptrs && rep_slot, "pp_replica_agg: null pointer");
-  const int grid = max_ctas > 0 ? max_ctas : 16;
+  PP_CHECK_ARG(m >= 1 && m <= kMaxListE && D >= 1 && my_rank >= 0 && my_rank < D,
+               "pp_replica_agg: bad D / m / rank");
+  PP_CHECK_ARG(((size_t)d_model * d_ff) % 4 == 0, "pp_replica_agg: bad sizes");
+  const int grid = max_ctas > 0 ? max_ctas : 32;
   replica_agg_kernel<<<grid, 512, 0, as_stream(stream)>>>(g1_ptrs, g2_ptrs, rep_slot, D, E, m,
-                                                          my_rank, (size_t)d_model * d_ff);
+                                                          my_rank, (size_t)d_model * d_ff / 4);
   PP_LAUNCH_CHECK();
   return PP_OK;
 }

@@ -56,11 +56,11 @@ __host__ __device__ inline size_t layout_smem_bytes(int D, int m, int E, int T) 
 }
 
 __global__ void __launch_bounds__(kLayoutThreads)
-    dispatch_layout_kernel(const int64_t* counts, const uint8_t* mask, const int32_t* chunk_counts,
+    dispatch_layout_kernel(int64_t* counts, const uint8_t* mask, const int32_t* chunk_counts,
                            int D, int m, int E, int T, int me, int max_groups, int rows_capacity,
                            int32_t* chunk_base, int32_t* slot_dest, pp_group* groups,
                            int32_t* num_groups, int32_t* total_rows, int32_t* seg_start,
-                           int32_t* rep_slot) {
+                           int32_t* rep_slot, int counts_from_chunks) {
   extern __shared__ __align__(16) uint8_t lsm[];
   const int Ev = D * m, C = T / PP_CHUNK, tid = threadIdx.x, nt = blockDim.x;
   LayoutSmem S;
@@ -73,7 +73,20 @@ __global__ void __launch_bounds__(kLayoutThreads)
   S.local = p; p += (size_t)Ev * E;
   S.present = p;
 
-  // phase 0: stage inputs
+  // phase 0: stage inputs (single rank: the LoadMatrix rows are summed from the
+  // chunk counts right here, replacing the histogram kernel + barrier)
+  for (int i = tid; i < C * E; i += nt) S.cc[i] = chunk_counts[i];
+  if (counts_from_chunks) {
+    __syncthreads();
+    const int cps_ = (T / m) / PP_CHUNK;
+    for (int i = tid; i < Ev * E; i += nt) {
+      const int v = i / E, e = i % E;
+      int s = 0;
+      for (int c = 0; c < cps_; ++c) s += S.cc[(v * cps_ + c) * E + e];
+      counts[i] = s;
+    }
+    __syncthreads();
+  }
   for (int i = tid; i < Ev * E; i += nt) {
     const int v = i / E, e = i % E;
     S.counts[i] = (int32_t)counts[i];
@@ -81,7 +94,6 @@ __global__ void __launch_bounds__(kLayoutThreads)
     S.local[i] = loc;
     S.comp[i] = (uint8_t)(loc ? v / m : e / m);
   }
-  for (int i = tid; i < C * E; i += nt) S.cc[i] = chunk_counts[i];
   __syncthreads();
   // phase 1: rows / presence of every (rank, expert)
   for (int cell = tid; cell < D * E; cell += nt) {
@@ -308,10 +320,13 @@ __global__ void __launch_bounds__(256)
     dispatch_bwd_kernel(void* const* dxp_ptrs, const int32_t* __restrict__ pair_dest,
                         const int32_t* __restrict__ pair_row, const int32_t* __restrict__ idx,
                         const float* __restrict__ probs, const float* __restrict__ dw, int T, int d,
-                        int k, int E, __nv_bfloat16* dx, __nv_bfloat16* dl) {
+                        int k, int E, __nv_bfloat16* dx, __nv_bfloat16* dl, float4* zero,
+                        int zero_vec) {
   const int lane = threadIdx.x & 31;
   const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < zero_vec; i += gridDim.x * blockDim.x)
+    zero[i] = make_float4(0.f, 0.f, 0.f, 0.f);
   for (int t = warp_global; t < T; t += nwarps) {
     int my_e = -1, my_dest = 0, my_row = 0;
     float my_dw = 0.f, my_p = 0.f;
@@ -412,12 +427,13 @@ extern "C" int pp_slot_histogram(const int32_t* chunk_counts, int32_t T, int32_t
   return PP_OK;
 }
 
-extern "C" int pp_dispatch_layout(const int64_t* counts, const uint8_t* mask,
+extern "C" int pp_dispatch_layout(int64_t* counts, const uint8_t* mask,
                                   const int32_t* chunk_counts, int32_t D, int32_t m, int32_t E,
                                   int32_t T, int32_t my_rank, int32_t max_groups,
                                   int32_t rows_capacity, int32_t* chunk_base, int32_t* slot_dest,
                                   pp_group* groups, int32_t* num_groups, int32_t* total_rows,
-                                  int32_t* seg_start, int32_t* rep_slot, void* stream) {
+                                  int32_t* seg_start, int32_t* rep_slot, int32_t counts_from_chunks,
+                                  void* stream) {
   PP_CHECK_ARG(counts && chunk_counts && chunk_base && slot_dest && groups && num_groups &&
                    total_rows && seg_start,
                "pp_dispatch_layout: null pointer");
@@ -427,6 +443,7 @@ extern "C" int pp_dispatch_layout(const int64_t* counts, const uint8_t* mask,
   PP_CHECK_ARG(T % (m * PP_CHUNK) == 0, "pp_dispatch_layout: T=%d not a multiple of m*%d", T,
                PP_CHUNK);
   PP_CHECK_ARG(D <= 255, "pp_dispatch_layout: D=%d > 255", D);
+  PP_CHECK_ARG(!counts_from_chunks || D == 1, "pp_dispatch_layout: counts_from_chunks needs D == 1");
   const size_t smem = layout_smem_bytes(D, m, E, T);
   PP_CHECK_ARG(smem <= 220 * 1024, "pp_dispatch_layout: E x E and T/128 x E staging too large");
   static int configured[64] = {0};  // per device: largest smem attribute set so far
@@ -439,7 +456,7 @@ extern "C" int pp_dispatch_layout(const int64_t* counts, const uint8_t* mask,
   }
   dispatch_layout_kernel<<<1, kLayoutThreads, smem, as_stream(stream)>>>(
       counts, mask, chunk_counts, D, m, E, T, my_rank, max_groups, rows_capacity, chunk_base,
-      slot_dest, groups, num_groups, total_rows, seg_start, rep_slot);
+      slot_dest, groups, num_groups, total_rows, seg_start, rep_slot, counts_from_chunks);
   PP_LAUNCH_CHECK();
   return PP_OK;
 }
@@ -492,7 +509,9 @@ extern "C" int pp_combine_bwd(const void* dy, void* const* out_ptrs, void* const
 extern "C" int pp_dispatch_bwd(void* const* dxp_ptrs, const int32_t* pair_dest,
                                const int32_t* pair_row, const int32_t* idx, const float* probs,
                                const float* dw, int32_t T, int32_t d, int32_t k, int32_t E,
-                               int32_t EP, void* dx, void* dl, void* stream) {
+                               int32_t EP, void* dx, void* dl, float* zero_f32, int64_t zero_elems,
+                               void* stream) {
+  PP_CHECK_ARG(zero_elems % 4 == 0 && (zero_elems == 0 || zero_f32), "pp_dispatch_bwd: zero buffer");
   PP_CHECK_ARG(dxp_ptrs && pair_dest && pair_row && idx && probs && dw && dx && dl,
                "pp_dispatch_bwd: null pointer");
   PP_CHECK_ARG(EP == 64 || EP == 128, "pp_dispatch_bwd: EP=%d must be 64 or 128", EP);
@@ -502,10 +521,12 @@ extern "C" int pp_dispatch_bwd(void* const* dxp_ptrs, const int32_t* pair_dest,
   auto* dlp = reinterpret_cast<__nv_bfloat16*>(dl);
   if (EP == 64) {
     PP_VPL_SWITCH(d, (dispatch_bwd_kernel<VPL, 64><<<grid_for_tokens(T), 256, 0, st>>>(
-                         dxp_ptrs, pair_dest, pair_row, idx, probs, dw, T, d, k, E, dxp, dlp)));
+                         dxp_ptrs, pair_dest, pair_row, idx, probs, dw, T, d, k, E, dxp, dlp,
+                         reinterpret_cast<float4*>(zero_f32), (int)(zero_elems / 4))));
   } else {
     PP_VPL_SWITCH(d, (dispatch_bwd_kernel<VPL, 128><<<grid_for_tokens(T), 256, 0, st>>>(
-                         dxp_ptrs, pair_dest, pair_row, idx, probs, dw, T, d, k, E, dxp, dlp)));
+                         dxp_ptrs, pair_dest, pair_row, idx, probs, dw, T, d, k, E, dxp, dlp,
+                         reinterpret_cast<float4*>(zero_f32), (int)(zero_elems / 4))));
   }
   PP_LAUNCH_CHECK();
   return PP_OK;

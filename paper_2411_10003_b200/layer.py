@@ -112,17 +112,16 @@ class _Barrier:
     def __init__(self, group, device) -> None:
         self.world = dist.get_world_size(group) if group is not None else 1
         self.rank = dist.get_rank(group) if group is not None else 0
-        self.epoch = 0
         if self.world > 1:
-            self.sig = PeerBuffer((self.world,), torch.int64, group, device)
+            self.sig = PeerBuffer((self.world + 1,), torch.int64, group, device)
             torch.cuda.synchronize()
             dist.barrier(group=group)
 
     def __call__(self, stream=None) -> None:
         if self.world == 1:
             return
-        self.epoch += 1
-        _lib.call("pp_peer_barrier", self.sig.ptrs.data_ptr(), self.world, self.rank, self.epoch,
+        # epoch 0: the kernel advances a device-side counter, so captured graphs replay correctly
+        _lib.call("pp_peer_barrier", self.sig.ptrs.data_ptr(), self.world, self.rank, 0,
                   _device.stream_ptr(stream))
 
 
@@ -160,8 +159,8 @@ class MoELayer(torch.nn.Module):
     def __init__(self, d_model: int, d_ff: int, num_experts: int, top_k: int, tokens: int,
                  group=None, planner: PlannerConfig | None = None, cluster=None, model=None,
                  capacity_rows: int | None = None, max_replicas: int | None = None,
-                 seed: int = 0, device=None, trans_ctas: int = 16, replica_engine: str = "copy",
-                 policy: str | None = None) -> None:
+                 seed: int = 0, device=None, trans_ctas: int = 32, replica_engine: str = "copy",
+                 policy: str | None = None, planning: str = "host") -> None:
         super().__init__()
         if not torch.cuda.is_available():
             raise RuntimeError("MoELayer needs a CUDA device (B200); there is no CPU path")
@@ -252,7 +251,8 @@ class MoELayer(torch.nn.Module):
         self._pcfg = _device.planner_cfg(self.planner_cfg)
         self.plan_stream = torch.cuda.Stream(device=dev) if self.plan_enabled else None
         self.comm_stream = torch.cuda.Stream(device=dev) if D > 1 else None
-        self.trans_ctas = trans_ctas
+        self.trans_ctas = trans_ctas  # SM-engine Trans (overlaps route/layout/dispatch)
+        self.agg_ctas = 2 * trans_ctas  # SM-engine Agg (runs beside DGRAD1)
         if replica_engine not in ("copy", "sm"):
             raise ValidationError(f"replica_engine must be 'copy' or 'sm', got {replica_engine!r}")
         # 'copy': Trans/Agg pulls run on the copy engines (cudaMemcpyAsync over NVLink,
@@ -274,6 +274,19 @@ class MoELayer(torch.nn.Module):
             else:
                 raise ValidationError(f"unknown policy {policy!r}; valid: vanilla, top<m>, greedy, greedy-overlap")
         self.policy = policy or ("greedy-overlap" if self.planner_cfg.overlap_aware else "greedy")
+        # planning "host": the plan's mask is read back asynchronously and the host issues
+        # copy-engine Trans/Agg; "device": the plan stays on the device (mask double-buffered,
+        # SM-driven Trans/Agg) so a whole step -- barriers included -- is CUDA-graph capturable
+        if planning not in ("host", "device"):
+            raise ValidationError(f"planning must be 'host' or 'device', got {planning!r}")
+        self.planning = planning
+        self._plan_done_dev = None
+        if planning == "device" and D > 1:
+            self.replica_engine = "sm"
+            self.mask_buf = torch.eye(E, dtype=torch.uint8, device=dev)
+            self._counts_snap = torch.zeros((E, E), dtype=torch.int64, device=dev)
+            if self.plan_enabled:
+                self.mask_cur = self.mask_buf  # identity = vanilla EP until the first plan lands
         self._plan_pending = None
         self._mask_host = torch.zeros((E, E), dtype=torch.uint8).pin_memory() if D > 1 else None
         self.mask_cur_host = None
@@ -334,9 +347,10 @@ class MoELayer(torch.nn.Module):
         _lib.call("pp_route_topk", x.data_ptr(), self.wg.data_ptr(), self.gate_bias.data_ptr(), T, d,
                   E, k, self.idx.data_ptr(), self.w.data_ptr(), self.probs.data_ptr(),
                   self.rank_in_chunk.data_ptr(), self.chunk_counts.data_ptr(), sp)
-        _lib.call("pp_slot_histogram", self.chunk_counts.data_ptr(), T, E, m, self.counts_buf.ptrs.data_ptr(),
-                  self.world, self.rank * m, sp)
-        self.barrier()  # every rank's rows of the LoadMatrix have landed
+        if self.world > 1:
+            _lib.call("pp_slot_histogram", self.chunk_counts.data_ptr(), T, E, m, self.counts_buf.ptrs.data_ptr(),
+                      self.world, self.rank * m, sp)
+            self.barrier()  # every rank's rows of the LoadMatrix have landed
         if self.top_m and self.world > 1:
             _lib.call("pp_top_m_mask", self.counts.data_ptr(), E, E, self.top_m, self._topm_mask.data_ptr(),
                       None, sp)
@@ -346,7 +360,7 @@ class MoELayer(torch.nn.Module):
                   self.world, m, E, T, self.rank, self.max_groups, self.rows_cap,
                   self.chunk_base.data_ptr(), self.slot_dest.data_ptr(), self.groups.data_ptr(),
                   self.num_groups.data_ptr(), self.total_rows.data_ptr(), self.seg_start.data_ptr(),
-                  self.rep_slot.data_ptr(), sp)
+                  self.rep_slot.data_ptr(), 1 if self.world == 1 else 0, sp)
         if self.record_history:
             self.history.append(self.counts.clone())
 
@@ -359,6 +373,19 @@ class MoELayer(torch.nn.Module):
             return
         nxt = self.iteration + 1
         if nxt % self.planner_cfg.reuse_interval != 0:
+            return
+        if self.planning == "device":
+            self._counts_snap.copy_(self.counts)  # the next iteration overwrites self.counts
+            ev = torch.cuda.Event()
+            ev.record()
+            with torch.cuda.stream(self.plan_stream):
+                self.plan_stream.wait_event(ev)
+                p0 = self._side_event(self.plan_stream)
+                _device.launch_plan(self._counts_snap.view(1, self.E, self.E), self._plan_out, self._cm,
+                                    self._pcfg, self.plan_stream)
+                self._log_side("Plan", p0, self._side_event(self.plan_stream))
+                self._plan_done_dev = torch.cuda.Event()
+                self._plan_done_dev.record(self.plan_stream)
             return
         snapshot = self.counts.clone()  # the next iteration overwrites self.counts
         ev = torch.cuda.Event()
@@ -380,7 +407,7 @@ class MoELayer(torch.nn.Module):
         """Adopt the plan computed during the previous iteration and derive this
         rank's replica set, Trans copies and Agg sources from it (same rule as the
         device layout: replica experts in ascending id get slots m, m+1, ...)."""
-        if self._plan_pending is None:
+        if self._plan_pending is None or self.planning == "device":
             return
         done, mask_dev = self._plan_pending
         self._plan_pending = None
@@ -468,8 +495,8 @@ class MoELayer(torch.nn.Module):
                     self._copy_batch(self._trans_list, self.comm_stream)
             else:
                 _lib.call("pp_replica_trans", self.w1_arena.ptrs.data_ptr(), self.w2_arena.ptrs.data_ptr(),
-                          self.groups.data_ptr(), self.num_groups.data_ptr(), self.max_groups, self.rank,
-                          self.m, self.d, self.f, self.trans_ctas, _device.stream_ptr(self.comm_stream))
+                          self.mask_cur.data_ptr(), self.E, self.m, self.rank, self.d, self.f, self.trans_ctas,
+                          _device.stream_ptr(self.comm_stream))
             self._trans_done = torch.cuda.Event()
             self._trans_done.record(self.comm_stream)
             self._log_side("SubTrans1", t0, self._side_event(self.comm_stream))
@@ -529,7 +556,7 @@ class MoELayer(torch.nn.Module):
             else:
                 _lib.call("pp_replica_agg", self.g1_arena.ptrs.data_ptr(), self.g2_arena.ptrs.data_ptr(),
                           self.rep_slot.data_ptr(), self.world, self.E, self.m, self.rank, self.d, self.f,
-                          self.trans_ctas * 4, _device.stream_ptr(self.comm_stream))
+                          self.agg_ctas, _device.stream_ptr(self.comm_stream))
             self._agg_done = torch.cuda.Event()
             self._agg_done.record(self.comm_stream)
             self._log_side("SubAgg2", t0, self._side_event(self.comm_stream))
@@ -576,12 +603,14 @@ class MoELayer(torch.nn.Module):
             self._agg_done = None
         self._mark("fwd_start")
         self.begin_iteration()
-        if self.replica_engine == "copy":  # host-derived copies: start before routing
+        if self.planning == "device" and self.world > 1:
+            self._trans_issued = False  # the device-side plan may change every iteration
+        if not self.top_m:  # the plan is known before routing: Trans overlaps route/layout/dispatch
             trans_done = self.issue_trans()  # no-op if a scheduler already issued it earlier
-        if self.top_m:
-            self._trans_issued = False  # a fresh top-m placement every iteration
+        else:
+            self._trans_issued = False  # top-m: this iteration's mask exists only after the histogram
         self._route_and_layout(x)
-        if self.replica_engine == "sm":  # device-driven pulls read this iteration's group table
+        if self.top_m:
             trans_done = self.issue_trans()
         self._mark("route_layout")
         self._launch_planner()  # [A2A | Plan(j+1)]: the search overlaps this block's dispatch
@@ -632,12 +661,21 @@ class MoELayer(torch.nn.Module):
         dx = torch.empty((self.T, self.d), dtype=torch.bfloat16, device=self.device)
         _lib.call("pp_dispatch_bwd", self.dxp.ptrs.data_ptr(), self.pair_dest.data_ptr(),
                   self.pair_row.data_ptr(), self.idx.data_ptr(), self.probs.data_ptr(), self.dw.data_ptr(),
-                  self.T, self.d, self.k, self.E, self.EP, dx.data_ptr(), self.dlogits.data_ptr(), sp)
+                  self.T, self.d, self.k, self.E, self.EP, dx.data_ptr(), self.dlogits.data_ptr(),
+                  self.wg.main_grad.data_ptr(), self.wg.main_grad.numel(), sp)  # also zeroes dWg
         self._mark("dispatch_bwd")
-        self.wg.main_grad.zero_()
         _lib.call("pp_gate_bwd", self.dlogits.data_ptr(), self.wg.data_ptr(), x.data_ptr(), self.T, self.d,
                   self.E, self.EP, dx.data_ptr(), self.wg.main_grad.data_ptr(), sp)
         self._mark("gate_bwd")
+        if self.planning == "device" and self.world > 1:
+            cur = torch.cuda.current_stream()
+            if self._agg_done is not None:  # join the Agg side stream (graph-capturable fork/join)
+                cur.wait_event(self._agg_done)
+                self._agg_done = None
+            if self._plan_done_dev is not None:  # plan for the next iteration becomes current
+                cur.wait_event(self._plan_done_dev)
+                self.mask_buf.copy_(self._plan_out.mask[0])
+                self._plan_done_dev = None
         self.iteration += 1
         return dx
 
@@ -651,16 +689,18 @@ class MoELayer(torch.nn.Module):
     def forward(self, x: torch.Tensor) -> torch.Tensor:
         return _MoEFunction.apply(x, self)
 
-    def make_graphed_step(self, x: torch.Tensor, dy: torch.Tensor) -> "GraphedStep":
+    def make_graphed_step(self, x: torch.Tensor, dy: torch.Tensor, with_loss: bool = False) -> "GraphedStep":
         """Capture one forward + backward into a CUDA graph (host cost per step
         drops to one graph launch).  ``x`` / ``dy`` become the static input
         buffers: copy new data into them, call the returned object, read
-        ``.y`` / ``.dx`` (and the ``main_grad`` tensors).  Single-rank layers
-        only: at D > 1 the plan adoption and copy-engine Trans are host-driven
-        per iteration."""
-        if self.world != 1:
-            raise ValidationError("make_graphed_step: CUDA-graph capture is single-rank only")
-        return GraphedStep(self, x, dy)
+        ``.y`` / ``.dx`` (and the ``main_grad`` tensors).  At D > 1 the layer
+        must use planning='device' (plan, Trans and Agg stay on the device; every
+        rank captures and replays in lockstep)."""
+        if self.world != 1 and self.planning != "device":
+            raise ValidationError("make_graphed_step at D > 1 needs planning='device'")
+        if self.plan_enabled and self.world > 1 and self.planner_cfg.reuse_interval != 1:
+            raise ValidationError("make_graphed_step: the captured step re-plans every iteration (reuse_interval=1)")
+        return GraphedStep(self, x, dy, with_loss)
 
     # ---- introspection (LoadMatrix / placement of the last call) -------------
     def last_load_matrix(self) -> LoadMatrix:
@@ -701,7 +741,10 @@ class _MoEFunction(torch.autograd.Function):
 class GraphedStep:
     """A captured fwd+bwd of one MoELayer over static input buffers."""
 
-    def __init__(self, layer: MoELayer, x: torch.Tensor, dy: torch.Tensor) -> None:
+    def __init__(self, layer: MoELayer, x: torch.Tensor, dy: torch.Tensor, with_loss: bool = False) -> None:
+        """with_loss: also compute loss = sum(y * dy) in fp32 inside the graph (a
+        linear probe whose gradient w.r.t. y is exactly dy), so a training loop can
+        read back one scalar per step."""
         self.layer, self.x, self.dy = layer, x, dy
         saved_timing, saved_phase = layer.gemm_timing, layer.phase_log
         layer.gemm_timing = layer.phase_log = None  # timing events cannot live in the graph
@@ -715,6 +758,7 @@ class GraphedStep:
         self.graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(self.graph):
             self.y = layer.forward_raw(x)
+            self.loss = (self.y.float() * dy.float()).sum() if with_loss else None
             self.dx = layer.backward_raw(x, dy)
         layer.gemm_timing, layer.phase_log = saved_timing, saved_phase
 

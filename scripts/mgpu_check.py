@@ -39,7 +39,8 @@ def main():
     layer = pp.MoELayer(d, f, E, k, tokens=T, group=dist.group.WORLD,
                         planner=pp.PlannerConfig(n=1, alpha=0.5), cluster=cl, model=mo, seed=0,
                         replica_engine=os.environ.get("PP_ENGINE", "copy"),
-                        policy=os.environ.get("PP_POLICY") or None)
+                        policy=os.environ.get("PP_POLICY") or None,
+                        planning=os.environ.get("PP_PLANNING", "host"))
     policy = os.environ.get("PP_POLICY") or "greedy"
     _, wg = M.exact_inputs(16, d, E, seed=99)
     bias = torch.round(torch.log(torch.tensor([1.0 / (i + 1) ** 1.2 for i in range(E)])) * 4) / 4
