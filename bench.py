@@ -292,9 +292,15 @@ def main() -> None:
     ap.add_argument("--profile-only", action="store_true", help="short run for ncu (no CPU legs)")
     ap.add_argument("--eager", action="store_true", help="no CUDA graph for the timed region (host-driven planning at N > 1)")
     ap.add_argument("--alpha", type=float, default=0.5, help="planner balance coefficient (Eq. 8)")
-    ap.add_argument("--n-excl", type=int, default=1, help="planner n: devices a selected expert skips")
+    ap.add_argument("--n-excl", type=int, default=None,
+                    help="planner n: devices a selected expert skips (default 1 virtual, 0 physical)")
     ap.add_argument("--policy", default="greedy-overlap",
                     help="vanilla | top<m> | greedy | greedy-overlap (reference simulator policies)")
+    ap.add_argument("--placement", default="physical", choices=["virtual", "physical"],
+                    help="planner over physical devices (E = m*D generalisation, 8(f) row 4; == the reference "
+                         "search when E == D) or over E x E virtual expert slots (the reference search verbatim)")
+    ap.add_argument("--trans-ctas", type=int, default=None, help="SMs of the SM-engine Trans push")
+    ap.add_argument("--agg-ctas", type=int, default=None, help="SMs of the SM-engine Agg push/reduce")
     args = ap.parse_args()
     world_env = int(os.environ.get("WORLD_SIZE", "1"))
     # one bench workload for every N (weak scaling of the same per-GPU work): BASELINE
@@ -339,13 +345,19 @@ def main() -> None:
             dist.destroy_process_group()
         return
     E, k, d, f, T = cfg["E"], cfg["k"], cfg["d"], cfg["f"], cfg["T"]
+    if args.n_excl is None:
+        args.n_excl = 0 if args.placement == "physical" else 1
     planner = pp.PlannerConfig(n=args.n_excl, alpha=args.alpha, reuse_interval=1,
                                overlap_aware=args.policy != "greedy")
     # N > 1: planning stays on the device (plan -> mask double buffer, SM-driven Trans/Agg)
     # so the whole EP step -- peer barriers included -- is captured in one CUDA graph
     planning = "device" if world > 1 and not args.eager else "host"
     layer = pp.MoELayer(d, f, E, k, tokens=T, group=group, planner=planner, seed=0, policy=args.policy,
-                        planning=planning)
+                        planning=planning, placement=args.placement if world > 1 else "virtual")
+    if args.trans_ctas:
+        layer.trans_ctas = args.trans_ctas
+    if args.agg_ctas:
+        layer.agg_ctas = args.agg_ctas
     layer.set_gate_bias(zipf_bias(E, 1.2, 0))
     g = torch.Generator(device="cpu").manual_seed(1000 + rank)
     x = torch.randn((T, d), generator=g).to(dev, torch.bfloat16)
@@ -414,6 +426,7 @@ def main() -> None:
     torch.cuda.synchronize()
     launches = _lib.launch_count()  # kernels of ours per K steps (same kernels the graph replays)
     layer.phase_log = []
+    layer.timeline_log = [] if world > 1 else None  # side-stream ops: Plan, Trans, Agg
     calib_samples = []
     n_phase_steps = 6 if world > 1 else 2
     for i in range(n_phase_steps):
@@ -426,6 +439,19 @@ def main() -> None:
             calib_samples.append((layer.counts.clone(), mask))
     torch.cuda.synchronize()
     phases = layer.phase_breakdown()
+    side_ms = None
+    if layer.timeline_log:
+        acc = {}
+        for kind, e0, e1 in layer.timeline_log:
+            acc.setdefault(kind, []).append(e0.elapsed_time(e1))
+        side_ms = {k: sum(v) / len(v) for k, v in acc.items()}
+        layer.timeline_log = None
+    if os.environ.get("PP_DEBUG_PHASES"):
+        from paper_2411_10003_b200 import calibrate as _cal
+
+        for i, ph in enumerate(_cal.per_step_phases(layer.phase_log)):
+            print(f"[rank {rank}] step {i} phases {json.dumps({k: round(v, 3) for k, v in ph.items()})}",
+                  file=sys.stderr, flush=True)
     calibration = None
     if world > 1 and not args.profile_only:
         from paper_2411_10003_b200 import _device as dv
@@ -444,6 +470,14 @@ def main() -> None:
         calibration["note"] = ("fit of the reference model's B and t to this run's measured phases "
                                "(virtual-slot H/R, rank 0); plan objective uses these units")
     layer.phase_log = None
+
+    replica_traffic = None
+    if world > 1 and calib_samples and calib_samples[-1][1] is not None:
+        replica_traffic = layer.replica_traffic(calib_samples[-1][1].cpu().numpy())
+        if side_ms:  # achieved NVLink rate of the busiest rank's pushes (rank 0's timing)
+            for kind, key in (("SubTrans1", "trans_out_bytes"), ("SubAgg2", "agg_out_bytes")):
+                if side_ms.get(kind):
+                    replica_traffic[f"{kind}_rank0_GBps"] = replica_traffic[key][rank] / (side_ms[kind] / 1e3) / 1e9
 
     # ---- physical balance: expert-GEMM rows computed per rank under the plan used
     rows_rank = torch.tensor([float(layer.total_real_rows())], dtype=torch.float64, device=dev)
@@ -597,8 +631,11 @@ def main() -> None:
                        "d_ff": f, "tokens_per_gpu": T, "parallelism": f"ep{world}",
                        "l2": "working set > L2 (activations+weights >> 126 MB), no flush",
                        "routing": "Zipf(1.2) gate bias, random bf16 tokens", "policy": args.policy,
-                       "planner": {"n": args.n_excl, "alpha": args.alpha, "reuse_interval": 1}},
+                       "planner": {"n": args.n_excl, "alpha": args.alpha, "reuse_interval": 1,
+                                   "placement": layer.placement, "planning": layer.planning,
+                                   "replica_engine": layer.replica_engine}},
             "host_enqueue_ms_per_step": host_ms, "phase_ms_rank0": phases,
+            "side_stream_ms_rank0": side_ms, "replica_traffic": replica_traffic,
             "timed_region": "CUDA-graph replay of fwd+bwd" if use_graph else "eager stream-ordered fwd+bwd",
             "roofline": roofline, "cpu_baseline": cpu_info, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk_summary, "planner": planner_info, "imbalance": imbalance,

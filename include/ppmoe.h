@@ -14,6 +14,8 @@
  * "moebal" package, /root/reference/pkg/src/moebal):
  *   pp_plan_greedy    <- planner.greedy_search        planner.py:80-129
  *                        (+ derive_loads core.py:255-275, cost _build perf_model.py:86-107)
+ *   pp_plan_physical  <- greedy_search generalised to E = m*D (opt-in; equals
+ *                        pp_plan_greedy at m = 1; planner.py:88-90 lifts E == D)
  *   pp_derive_loads   <- core.derive_loads             core.py:255-275
  *   pp_route_topk     <- the gate that produces LoadMatrix rows (core.py:88-95;
  *                        gate described in PAPER.md:106-108); no reference code
@@ -22,7 +24,7 @@
  *                     <- routing rule of derive_loads core.py:267-274 realised on
  *                        tokens; A2A modelled by t_a2a perf_model.py:36-39
  *   pp_grouped_gemm   <- expert compute modelled by t_fec/t_bec perf_model.py:42-51
- *   pp_replica_trans / pp_replica_agg
+ *   pp_replica_trans / pp_replica_agg / pp_replica_agg_reduce
  *                     <- Trans/Agg modelled by t_trans/t_agg perf_model.py:61-73,
  *                        split by partition_trans/agg scheduler.py:91-108
  */
@@ -75,6 +77,19 @@ int pp_plan_greedy(const int64_t* counts, int32_t num_layers, int32_t E,
                    int32_t* selected, int32_t* num_selected, int32_t* num_explored,
                    uint8_t* mask, int64_t* H, int64_t* R, double* best_cost,
                    void* stream);
+
+/* Physically-faithful E > D planner (opt-in): Algorithm 1
+ * generalised to m = E/D experts per device (home of e = device e/m, physical
+ * LoadMatrix rows); identical to pp_plan_greedy when E == D.  counts:
+ * [L][rows][E] int64 with rows = D (physical) or any multiple (rows/D slot rows
+ * per device, summed on load).  Outputs: selected [L][E], num_selected [L],
+ * num_explored [L], mask [L][rows][E] (each device's row repeated over its slot
+ * rows, so the layout consumes it as a slot mask), H/R [L][D], best_cost [L].
+ * cm->num_devices must be D and cm->num_experts E; D*E <= 4096. */
+int pp_plan_physical(const int64_t* counts, int32_t num_layers, int32_t rows, int32_t D, int32_t E,
+                     const pp_cost_model* cm, const pp_planner_cfg* cfg, int32_t* selected,
+                     int32_t* num_selected, int32_t* num_explored, uint8_t* mask, int64_t* H,
+                     int64_t* R, double* best_cost, void* stream);
 
 /* Top-m baseline (reference simulator._top_m_placement, simulator.py:318-324):
  * mask [D][E] with the m heaviest experts (column totals, ties -> lower index)
@@ -131,7 +146,7 @@ typedef struct pp_group {
  *   total_rows [1] int32 (padded rows of this rank's receive buffer)
  *   seg_start  [D][E] int32 segment start of expert e on rank r (-1 if absent)
  *   rep_slot   [D][E] int32 weight slot of replica expert e on rank r (-1 if
- *              none; nullable) -- consumed by pp_replica_agg.
+ *              none; nullable).
  * counts_from_chunks (D == 1 only): fill `counts` from the chunk counts here,
  * replacing pp_slot_histogram + barrier. */
 int pp_dispatch_layout(int64_t* counts, const uint8_t* mask, const int32_t* chunk_counts,
@@ -200,23 +215,33 @@ int pp_grouped_gemm(int32_t mode, const void* a, const void* b, void* c, void* c
                     int32_t num_sms, void* stream);
 
 /* ---- replica Trans / Agg over peer memory (K5) --------------------------- */
-/* Trans: for every replica expert of this rank under the plan's mask ([E][E]
- * uint8 slot->expert, the pp_dispatch_layout rule: experts e with home e/m !=
- * me that some slot of this rank routes to, ascending, get slots m, m+1, ...)
- * pull the expert's W1/W2 from the home rank's weight arena (peer pointer
- * tables w1_ptrs/w2_ptrs [D], arenas [slots][f][d] and [slots][d][f] bf16) into
- * that replica slot.  Needs only the mask, so it can run before this
- * iteration's routing.  `max_ctas` bounds the SMs it takes (E <= 1024). */
+/* Trans (home side, SM engine): push each of this rank's home experts' W1/W2
+ * (weight arenas [slots][f][d] and [slots][d][f] bf16, peer pointer tables
+ * w1_ptrs/w2_ptrs [D]) into the replica slot of every rank that holds it under
+ * the plan's mask ([E][E] uint8 slot->expert; D = E/m).  Replica slot rule (=
+ * pp_dispatch_layout's): the experts e with home e/m != r that some slot of r
+ * routes to, ascending, get slots m, m+1, ... on r.  Needs only the mask, so it
+ * can run before this iteration's routing; every rank must have passed the
+ * previous backward's last peer barrier.  `max_ctas` = SMs it occupies
+ * (E <= 1024, D*E <= 16384). */
 int pp_replica_trans(void* const* w1_ptrs, void* const* w2_ptrs, const uint8_t* mask, int32_t E,
                      int32_t m, int32_t my_rank, int32_t d_model, int32_t d_ff, int32_t max_ctas,
                      void* stream);
 
-/* Agg: the home rank pulls the replicas' fp32 grads (g1_ptrs/g2_ptrs [D]) and
- * adds them, in ascending rank order, into its own home slots.  rep_slot
- * [D][E] from pp_dispatch_layout. */
-int pp_replica_agg(void* const* g1_ptrs, void* const* g2_ptrs, const int32_t* rep_slot,
-                   int32_t D, int32_t E, int32_t m, int32_t my_rank, int32_t d_model,
+/* Agg phase 1 (replica side): push the fp32 grads of this rank's replica slots
+ * (g1_ptrs/g2_ptrs [D] grad arenas) into the home rank's staging area
+ * stage_ptrs[home] laid out [m][D-1][2][d_ff*d_model] fp32 (index r' = this
+ * rank's position among the home's D-1 peers). */
+int pp_replica_agg(void* const* g1_ptrs, void* const* g2_ptrs, void* const* stage_ptrs,
+                   const uint8_t* mask, int32_t E, int32_t m, int32_t my_rank, int32_t d_model,
                    int32_t d_ff, int32_t max_ctas, void* stream);
+
+/* Agg phase 2 (home side, after a peer barrier): grad[j] += stage[j][r'] for
+ * every rank holding expert my_rank*m + j, in ascending rank order (the
+ * oracle's summation order).  g1/g2/stage are this rank's local buffers. */
+int pp_replica_agg_reduce(float* g1, float* g2, const float* stage, const uint8_t* mask, int32_t E,
+                          int32_t m, int32_t my_rank, int32_t d_model, int32_t d_ff,
+                          int32_t max_ctas, void* stream);
 
 /* Copy-engine Trans/Agg: one cudaMemcpyAsync per (dst, src, bytes) triple of
  * the HOST arrays (peer pointers via IPC: the copy runs on the copy engines over

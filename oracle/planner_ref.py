@@ -131,6 +131,97 @@ def greedy_search(counts, n: int, alpha: float, overlap_aware: bool, cm: dict) -
             "mask": mask, "H": Hf, "R": Rf}
 
 
+# ---- physically-faithful E > D planner (parity pinned at m = 1) ----
+#
+# The reference search needs E == D (planner.py:88-90).  With m = E / D experts per
+# device, expert e's home is device e // m and the LoadMatrix rows are physical
+# devices.  Generalisation (reduces to greedy_search exactly when m == 1):
+#   * derive_loads: a (d, e) batch stays on d when d holds e, otherwise it is
+#     computed and received at home(e)                      (core.py:255-275 with homes e // m)
+#   * is_balanced threshold alpha * total_inputs / D         (planner.py:63-68; E == D there)
+#   * i = first argmax(H) is a DEVICE; the expert to replicate is the unused expert
+#     homed on i that currently sends it the most rows (ties -> lower id); stop when
+#     i has no unused expert                                  (planner.py:115-117)
+#   * excluded = n non-home devices with the fewest rows of that expert, key
+#     (count, index), on the original matrix                 (planner.py:71-77)
+#   * the cost model is the reference's with num_devices = D (perf_model.py:36-107)
+
+
+def replica_mask_physical(D: int, E: int, selected, excluded) -> np.ndarray:
+    m = E // D
+    mask = np.zeros((D, E), dtype=bool)
+    for e in range(E):
+        mask[e // m, e] = True
+    for e, ex in zip(selected, excluded):
+        mask[:, e] = True
+        for dv in ex:
+            mask[dv, e] = False
+    return mask
+
+
+def derive_loads_physical(counts: np.ndarray, mask: np.ndarray):
+    counts = np.asarray(counts, dtype=np.int64)
+    D, E = counts.shape
+    m = E // D
+    H = np.zeros(D, dtype=np.int64)
+    R = np.zeros(D, dtype=np.int64)
+    for d in range(D):
+        for e in range(E):
+            c = int(counts[d, e])
+            if mask[d, e]:
+                H[d] += c
+            else:
+                H[e // m] += c
+                R[e // m] += c
+    return H, R
+
+
+def bottom_devices_physical(counts: np.ndarray, expert: int, n: int, home: int) -> frozenset:
+    col = counts[:, expert]
+    cands = sorted((int(col[d]), d) for d in range(counts.shape[0]) if d != home)
+    return frozenset(d for _, d in cands[:n])
+
+
+def greedy_search_physical(counts, n: int, alpha: float, overlap_aware: bool, cm: dict) -> dict:
+    counts = np.asarray(counts, dtype=np.int64)
+    D, E = counts.shape
+    assert E % D == 0 and cm["num_devices"] == D
+    m = E // D
+    total_inputs = int(counts.sum()) // cm["top_k"]
+    mask = replica_mask_physical(D, E, (), ())
+    H, R = derive_loads_physical(counts, mask)
+    best = objective(H, R, 0, 0, cm, overlap_aware)
+    selected, bottoms, used = [], [], set()
+    cnt = 0
+    while not (float(H.max() - H.min()) < alpha * total_inputs / D):
+        i = int(np.argmax(H))
+        cand = None
+        for e in range(i * m, (i + 1) * m):
+            if e in used:
+                continue
+            sent = int(sum(int(counts[d, e]) for d in range(D) if not mask[d, e]))
+            if cand is None or sent > cand[0]:
+                cand = (sent, e)
+        if cand is None:
+            break
+        e = cand[1]
+        used.add(e)
+        selected.append(e)
+        bottoms.append(bottom_devices_physical(counts, e, n, i))
+        mask = replica_mask_physical(D, E, selected, bottoms)
+        H, R = derive_loads_physical(counts, mask)
+        changed = objective(H, R, len(selected), n, cm, overlap_aware)
+        if changed < best:
+            best = changed
+            cnt = len(selected)
+    sel = tuple(selected[:cnt])
+    exc = tuple(bottoms[:cnt])
+    mask = replica_mask_physical(D, E, sel, exc)
+    Hf, Rf = derive_loads_physical(counts, mask)
+    return {"selected": sel, "excluded": exc, "best": best, "explored": len(selected),
+            "mask": mask, "H": Hf, "R": Rf}
+
+
 def top_m_mask(counts: np.ndarray, m: int) -> np.ndarray:
     """reference simulator._top_m_placement (simulator.py:318-324): the m experts
     with the largest column totals (ties -> lower index) on every device."""

@@ -13,7 +13,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .core import ExpertPlacement
+from .core import ExpertPlacement, PhysicalPlacement
 
 
 def _require_cuda() -> torch.device:
@@ -21,6 +21,10 @@ def _require_cuda() -> torch.device:
         raise RuntimeError("paper_2411_10003_b200 needs a CUDA device (B200); there is no CPU path")
     _lib.load()
     return torch.device("cuda", torch.cuda.current_device())
+
+
+def num_sms(device) -> int:
+    return torch.cuda.get_device_properties(device).multi_processor_count
 
 
 def stream_ptr(stream=None) -> int:
@@ -69,8 +73,17 @@ class PlanBuffers:
         self.best = torch.empty((L,), dtype=torch.float64, device=device)
 
 
-def launch_plan(counts_dev: torch.Tensor, out: PlanBuffers, cm, cfg, stream=None) -> None:
-    L, E, _ = counts_dev.shape
+def launch_plan(counts_dev: torch.Tensor, out: PlanBuffers, cm, cfg, stream=None, physical_devices: int = 0) -> None:
+    """physical_devices = D > 0: the physically-faithful search (pp_plan_physical) over
+    D devices; counts_dev rows may be D physical rows or virtual-slot rows."""
+    L, rows, E = counts_dev.shape
+    if physical_devices:
+        _lib.call(
+            "pp_plan_physical", counts_dev.data_ptr(), L, rows, physical_devices, E, ctypes.byref(cm),
+            ctypes.byref(cfg), out.selected.data_ptr(), out.num_selected.data_ptr(), out.num_explored.data_ptr(),
+            out.mask.data_ptr(), out.H.data_ptr(), out.R.data_ptr(), out.best.data_ptr(), stream_ptr(stream),
+        )
+        return
     _lib.call(
         "pp_plan_greedy", counts_dev.data_ptr(), L, E, ctypes.byref(cm), ctypes.byref(cfg),
         out.selected.data_ptr(), out.num_selected.data_ptr(), out.num_explored.data_ptr(),
@@ -97,6 +110,29 @@ def plan_greedy(counts: np.ndarray, config, cluster, model) -> list:
         chosen = [int(x) for x in sel[l, : nsel[l]]]
         placement = ExpertPlacement.from_mask(chosen, mask[l])
         results.append(PlanResult(placement, float(best[l]), int(nexp[l]), H[l].copy(), R[l].copy()))
+    return results
+
+
+def plan_physical(counts: np.ndarray, config, cluster, model) -> list:
+    """counts [L][D][E] physical LoadMatrices -> PlanResult per layer (mask [D][E])."""
+    from .planner import PlanResult
+
+    dev = _require_cuda()
+    L, D, E = counts.shape
+    counts_dev = torch.from_numpy(np.ascontiguousarray(counts, dtype=np.int64)).to(dev)
+    out = PlanBuffers(L, E, dev)
+    out.mask = torch.empty((L, D, E), dtype=torch.uint8, device=dev)
+    launch_plan(counts_dev, out, cost_model(cluster, model), planner_cfg(config), physical_devices=D)
+    sel = out.selected.cpu().numpy()
+    nsel = out.num_selected.cpu().numpy()
+    nexp = out.num_explored.cpu().numpy()
+    mask = out.mask.cpu().numpy().astype(bool)
+    H, R, best = out.H.cpu().numpy(), out.R.cpu().numpy(), out.best.cpu().numpy()
+    results = []
+    for l in range(L):
+        chosen = [int(x) for x in sel[l, : nsel[l]]]
+        results.append(PlanResult(PhysicalPlacement.from_mask(chosen, mask[l]), float(best[l]), int(nexp[l]),
+                                  H[l, :D].copy(), R[l, :D].copy()))
     return results
 
 

@@ -62,6 +62,7 @@ I = c_int32
 SIGNATURES = {
     "pp_version": [],
     "pp_plan_greedy": [P, I, I, POINTER(CostModel), POINTER(PlannerCfg), P, P, P, P, P, P, P, P],
+    "pp_plan_physical": [P, I, I, I, I, POINTER(CostModel), POINTER(PlannerCfg), P, P, P, P, P, P, P, P],
     "pp_derive_loads": [P, P, I, I, P, P, P],
     "pp_top_m_mask": [P, I, I, I, P, P, P],
     "pp_route_topk": [P, P, P, I, I, I, I, P, P, P, P, P, P],
@@ -74,7 +75,8 @@ SIGNATURES = {
     "pp_gate_bwd": [P, P, P, I, I, I, I, P, P, P],
     "pp_grouped_gemm": [I, P, P, P, P, P, P, I, I, I, I, I, I, P],
     "pp_replica_trans": [P, P, P, I, I, I, I, I, I, P],
-    "pp_replica_agg": [P, P, P, I, I, I, I, I, I, I, P],
+    "pp_replica_agg": [P, P, P, P, I, I, I, I, I, I, P],
+    "pp_replica_agg_reduce": [P, P, P, P, I, I, I, I, I, I, P],
     "pp_copy_batch": [P, P, P, I, P],
     "pp_agg_accumulate": [P, P, P, P, I, I, I, P],
     "pp_device_alloc": [c_uint64, POINTER(c_void_p)],
@@ -129,10 +131,10 @@ def check(rc: int, what: str = "") -> None:
 
 # kernels each entry point launches (for the bench's gpu_launches claim)
 KERNELS_PER_CALL = {
-    "pp_plan_greedy": 1, "pp_derive_loads": 1, "pp_top_m_mask": 1, "pp_route_topk": 1, "pp_slot_histogram": 1,
+    "pp_plan_greedy": 1, "pp_plan_physical": 1, "pp_derive_loads": 1, "pp_top_m_mask": 1, "pp_route_topk": 1, "pp_slot_histogram": 1,
     "pp_dispatch_layout": 1, "pp_dispatch": 1, "pp_combine": 1, "pp_combine_bwd": 1,
     "pp_dispatch_bwd": 1, "pp_gate_bwd": 2, "pp_grouped_gemm": 1, "pp_replica_trans": 1,
-    "pp_replica_agg": 1, "pp_peer_barrier": 1, "pp_agg_accumulate": 1,
+    "pp_replica_agg": 1, "pp_replica_agg_reduce": 1, "pp_peer_barrier": 1, "pp_agg_accumulate": 1,
 }
 _launches = [0]
 

@@ -55,118 +55,164 @@ __global__ void peer_barrier_kernel(void* const* signal_ptrs, int D, int me, uin
   if (threadIdx.x == 0) own[D] = e;
 }
 
-constexpr int kPeerUnroll = 8;  // 16-byte peer loads in flight per thread (NVLink latency cover)
-constexpr int kMaxListE = 1024;
+// Peer traffic is PUSHED: remote 16-byte stores are posted, so ~16 CTAs fill an NVLink 5
+// port (measured 700 GB/s push vs 240 GB/s pull at 16 CTAs; scripts/micro/p2p_bw.cu).
+constexpr int kPushUnroll = 4;
+constexpr int kReduceUnroll = 8;
+constexpr int kMaxFlags = 16384;  // D * E
+constexpr int kMaxItems = 1024;   // E
 
-// replica experts of rank `r` under `mask` in ascending id (slot m + i holds list[i]):
-// e is a replica on r iff its home e / m != r and some slot of r routes to it
-__device__ int build_replica_list(const uint8_t* mask, int E, int m, int r, int* list, int* flag) {
-  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+// flag[r*E + e] = 1 iff expert e is a replica on rank r under mask: home e/m != r and some
+// slot of r routes to e.  A replica's weight slot is m + #{e' < e : flag[r*E + e']}, the
+// same rule pp_dispatch_layout uses for its group table and rep_slot.
+__device__ void replica_flags(const uint8_t* mask, int D, int E, int m, uint8_t* flag) {
+  for (int t = threadIdx.x; t < D * E; t += blockDim.x) {
+    const int r = t / E, e = t - (t / E) * E;
     int f = 0;
     if (e / m != r)
       for (int j = 0; j < m; ++j) f |= mask[(size_t)(r * m + j) * E + e];
-    flag[e] = f;
+    flag[t] = (uint8_t)f;
   }
   __syncthreads();
-  __shared__ int n;
-  if (threadIdx.x == 0) {
-    int c = 0;
-    for (int e = 0; e < E; ++e)
-      if (flag[e]) list[c++] = e;
-    n = c;
-  }
-  __syncthreads();
-  return n;
 }
 
-// Trans: pull the home rank's W1/W2 of every replica expert of this rank (decided by the
-// plan's mask alone, so it can start before this iteration's routing) into its replica
-// slot.  kPeerUnroll independent 16-byte loads per thread keep enough bytes in flight to
-// run the NVLink pull at link rate from a few dozen CTAs.
+__device__ __forceinline__ int replica_index(const uint8_t* flag, int E, int r, int e) {
+  int c = 0;
+  for (int x = 0; x < e; ++x) c += flag[r * E + x];
+  return c;
+}
+
+// deterministic compaction of per-thread candidates (same order in every CTA)
+__device__ int compact_items(const int* cand, int n, int* items) {
+  __shared__ int cnt;
+  if (threadIdx.x == 0) {
+    int c = 0;
+    for (int t = 0; t < n; ++t)
+      if (cand[t] >= 0) items[c++] = cand[t];
+    cnt = c;
+  }
+  __syncthreads();
+  return cnt;
+}
+
+// 16-byte copy of `nmat` matrices of `vecs` uint4 each, addresses from addr(item, W1|W2):
+// CTAs stride over (matrix, chunk) pairs -- one 32-bit division per chunk, none per
+// element -- and each thread keeps U independent loads in flight.
+template <int U, class Addr>
+__device__ __forceinline__ void push_copy(int nmat, size_t vecs, Addr addr) {
+  constexpr int kThreads = 512;
+  const size_t chunk = (size_t)kThreads * U;
+  const int per_mat = (int)((vecs + chunk - 1) / chunk);
+  const int nchunks = nmat * per_mat;
+  for (int c = blockIdx.x; c < nchunks; c += gridDim.x) {
+    const int mat = c / per_mat;
+    const size_t off = (size_t)(c - mat * per_mat) * chunk + threadIdx.x;
+    const uint4* src;
+    uint4* dst;
+    addr(mat >> 1, mat & 1, src, dst);
+    uint4 r[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (off + u * kThreads < vecs) r[u] = ld_nc_v4(src + off + u * kThreads);
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (off + u * kThreads < vecs) st_v4(dst + off + u * kThreads, r[u]);
+  }
+}
+
+// Trans (home side): push each of this rank's home experts to every rank holding it as a
+// replica, into that rank's replica slot.  The receivers' previous use of those slots
+// ended before the last peer barrier of their backward, which this rank has passed.
 __global__ void __launch_bounds__(512) replica_trans_kernel(void* const* w1_ptrs, void* const* w2_ptrs,
                                                             const uint8_t* mask, int E, int m, int me,
                                                             size_t vecs) {
-  __shared__ int list[kMaxListE], flag[kMaxListE];
-  const int nrep = build_replica_list(mask, E, m, me, list, flag);
-  const size_t total = (size_t)nrep * 2 * vecs;  // uint4 units: [replica][W1|W2][vec]
-  const size_t stride = (size_t)gridDim.x * blockDim.x;
-  for (size_t base = (size_t)blockIdx.x * blockDim.x + threadIdx.x; base < total;
-       base += stride * kPeerUnroll) {
-    uint4 r[kPeerUnroll];
-    uint4* dst[kPeerUnroll];
-#pragma unroll
-    for (int u = 0; u < kPeerUnroll; ++u) {
-      const size_t i = base + u * stride;
-      dst[u] = nullptr;
-      if (i < total) {
-        const size_t mat = i / vecs, v = i - mat * vecs;
-        const int rep = (int)(mat >> 1), e = list[rep];
-        void* const* ptrs = (mat & 1) ? w2_ptrs : w1_ptrs;
-        r[u] = ld_nc_v4(reinterpret_cast<const uint4*>(ptrs[e / m]) + (size_t)(e % m) * vecs + v);
-        dst[u] = reinterpret_cast<uint4*>(ptrs[me]) + (size_t)(m + rep) * vecs + v;
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < kPeerUnroll; ++u)
-      if (dst[u]) st_v4(dst[u], r[u]);
-  }
-}
-
-// Agg: grad[home slot j] += sum over ranks r != me (ascending) of grad_r[rep_slot[r][e]],
-// e = me*m + j; only home slots that have replicas are touched.
-__global__ void __launch_bounds__(512) replica_agg_kernel(void* const* g1_ptrs, void* const* g2_ptrs,
-                                                          const int32_t* rep_slot, int D, int E, int m,
-                                                          int me, size_t vecs) {
-  __shared__ int act[kMaxListE];
-  __shared__ int nact;
-  if (threadIdx.x == 0) {
-    int c = 0;
-    for (int j = 0; j < m; ++j) {
-      bool any = false;
-      for (int r = 0; r < D; ++r)
-        if (r != me && rep_slot[r * E + me * m + j] >= 0) any = true;
-      if (any) act[c++] = j;
-    }
-    nact = c;
+  __shared__ uint8_t flag[kMaxFlags];
+  __shared__ int cand[kMaxItems], items[kMaxItems];
+  const int D = E / m;
+  replica_flags(mask, D, E, m, flag);
+  for (int t = threadIdx.x; t < D * m; t += blockDim.x) {  // t = (receiver r, home slot j)
+    const int r = t / m, j = t - (t / m) * m, e = me * m + j;
+    cand[t] = (r != me && flag[r * E + e]) ? ((r * m + j) << 10 | replica_index(flag, E, r, e)) : -1;
   }
   __syncthreads();
-  const size_t total = (size_t)nact * 2 * vecs;  // float4 units: [active slot][g1|g2][vec]
-  const size_t stride = (size_t)gridDim.x * blockDim.x;
-  constexpr int U = kPeerUnroll / 2;
-  for (size_t base = (size_t)blockIdx.x * blockDim.x + threadIdx.x; base < total; base += stride * U) {
-    float4 acc[U];
-    float4* dst[U];
-    int jj[U], which[U];
-    size_t vv[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const size_t i = base + u * stride;
-      dst[u] = nullptr;
-      if (i < total) {
-        const size_t mat = i / vecs;
-        vv[u] = i - mat * vecs;
-        jj[u] = act[mat >> 1];
-        which[u] = (int)(mat & 1);
-        dst[u] = reinterpret_cast<float4*>((which[u] ? g2_ptrs : g1_ptrs)[me]) + (size_t)jj[u] * vecs + vv[u];
-        acc[u] = *dst[u];
-      }
-    }
-    for (int r = 0; r < D; ++r) {
+  const int n = compact_items(cand, D * m, items);
+  push_copy<kPushUnroll>(n * 2, vecs, [&](int it, int mat, const uint4*& src, uint4*& dst) {
+    const int code = items[it], rj = code >> 10, i = code & 1023;
+    const int r = rj / m, j = rj - (rj / m) * m;
+    void* const* ptrs = mat ? w2_ptrs : w1_ptrs;
+    src = reinterpret_cast<const uint4*>(ptrs[me]) + (size_t)j * vecs;
+    dst = reinterpret_cast<uint4*>(ptrs[r]) + (size_t)(m + i) * vecs;
+  });
+}
+
+// Agg, phase 1 (replica side): push the fp32 grads of every replica slot of this rank into
+// the home rank's staging area stage[j][r'][W1|W2] (r' = this rank's index among the
+// home's D-1 peers), so the home can sum its sources in rank order.
+__global__ void __launch_bounds__(512) replica_agg_push_kernel(void* const* g1_ptrs, void* const* g2_ptrs,
+                                                               void* const* stage_ptrs, const uint8_t* mask,
+                                                               int E, int m, int me, size_t vecs) {
+  __shared__ uint8_t flag[kMaxFlags];
+  __shared__ int cand[kMaxItems], items[kMaxItems];
+  const int D = E / m;
+  replica_flags(mask, D, E, m, flag);
+  for (int e = threadIdx.x; e < E; e += blockDim.x)
+    cand[e] = flag[me * E + e] ? (e << 10 | replica_index(flag, E, me, e)) : -1;
+  __syncthreads();
+  const int n = compact_items(cand, E, items);
+  push_copy<kPushUnroll>(n * 2, vecs, [&](int it, int mat, const uint4*& src, uint4*& dst) {
+    const int code = items[it], e = code >> 10, i = code & 1023;
+    const int h = e / m, j = e - h * m, rp = me < h ? me : me - 1;
+    src = reinterpret_cast<const uint4*>((mat ? g2_ptrs : g1_ptrs)[me]) + (size_t)(m + i) * vecs;
+    dst = reinterpret_cast<uint4*>(stage_ptrs[h]) + ((size_t)(j * (D - 1) + rp) * 2 + mat) * vecs;
+  });
+}
+
+// Agg, phase 2 (home side, local HBM): grad[j] += stage[j][r'] for the ranks r != me that
+// hold expert me*m + j, ascending r (deterministic, = the oracle's rank-order sum).
+__global__ void __launch_bounds__(512, 1) replica_agg_reduce_kernel(float* g1, float* g2, const float* stage,
+                                                                    const uint8_t* mask, int E, int m, int me,
+                                                                    size_t vecs) {
+  __shared__ uint8_t flag[kMaxFlags];
+  __shared__ int cand[kMaxItems], items[kMaxItems];
+  __shared__ uint32_t srcmask[kMaxItems];
+  const int D = E / m;
+  replica_flags(mask, D, E, m, flag);
+  for (int j = threadIdx.x; j < m; j += blockDim.x) {
+    uint32_t bits = 0;
+    for (int r = 0, rp = 0; r < D; ++r) {
       if (r == me) continue;
+      if (flag[r * E + me * m + j]) bits |= 1u << rp;
+      ++rp;
+    }
+    srcmask[j] = bits;
+    cand[j] = bits ? j : -1;
+  }
+  __syncthreads();
+  const int n = compact_items(cand, m, items);
+  constexpr int U = kReduceUnroll, kThreads = 512;
+  const size_t chunk = (size_t)kThreads * U;
+  const int per_mat = (int)((vecs + chunk - 1) / chunk);
+  const int nchunks = n * 2 * per_mat;
+  for (int c = blockIdx.x; c < nchunks; c += gridDim.x) {  // (active slot, g1|g2, chunk)
+    const int mat = c / per_mat;
+    const size_t off = (size_t)(c - mat * per_mat) * chunk + threadIdx.x;
+    const int j = items[mat >> 1], w = mat & 1;
+    const uint32_t bits = srcmask[j];
+    float4* dst = reinterpret_cast<float4*>(w ? g2 : g1) + (size_t)j * vecs + off;
+    const float4* src = reinterpret_cast<const float4*>(stage) + (size_t)j * (D - 1) * 2 * vecs + w * vecs + off;
+    float4 acc[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (off + u * kThreads < vecs) acc[u] = dst[u * kThreads];
+    for (int rp = 0; rp < D - 1; ++rp) {
+      if (!(bits >> rp & 1)) continue;
+      const float4* sp = src + (size_t)rp * 2 * vecs;
       float4 x[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        if (!dst[u]) continue;
-        const int s = rep_slot[r * E + me * m + jj[u]];
-        if (s < 0) { x[u] = make_float4(0.f, 0.f, 0.f, 0.f); continue; }
-        const uint4 raw = ld_nc_v4(reinterpret_cast<const float4*>((which[u] ? g2_ptrs : g1_ptrs)[r]) +
-                                   (size_t)s * vecs + vv[u]);
-        x[u] = make_float4(__uint_as_float(raw.x), __uint_as_float(raw.y), __uint_as_float(raw.z),
-                           __uint_as_float(raw.w));
-      }
+      for (int u = 0; u < U; ++u)
+        if (off + u * kThreads < vecs) x[u] = __ldcs(sp + u * kThreads);
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        if (!dst[u]) continue;
         acc[u].x += x[u].x;
         acc[u].y += x[u].y;
         acc[u].z += x[u].z;
@@ -175,7 +221,7 @@ __global__ void __launch_bounds__(512) replica_agg_kernel(void* const* g1_ptrs, 
     }
 #pragma unroll
     for (int u = 0; u < U; ++u)
-      if (dst[u]) *dst[u] = acc[u];
+      if (off + u * kThreads < vecs) dst[u * kThreads] = acc[u];
   }
 }
 
@@ -230,26 +276,43 @@ extern "C" int pp_replica_trans(void* const* w1_ptrs, void* const* w2_ptrs, cons
                                 int32_t E, int32_t m, int32_t my_rank, int32_t d_model, int32_t d_ff,
                                 int32_t max_ctas, void* stream) {
   PP_CHECK_ARG(w1_ptrs && w2_ptrs && mask, "pp_replica_trans: null pointer");
-  PP_CHECK_ARG(E >= 1 && E <= kMaxListE && m >= 1 && E % m == 0 && my_rank >= 0 && my_rank < E / m,
+  PP_CHECK_ARG(E >= 1 && E <= kMaxItems && m >= 1 && E % m == 0 && (E / m) * E <= kMaxFlags &&
+                   my_rank >= 0 && my_rank < E / m,
                "pp_replica_trans: bad E / m / rank");
   PP_CHECK_ARG(((size_t)d_model * d_ff) % 8 == 0, "pp_replica_trans: bad sizes");
-  const int grid = max_ctas > 0 ? max_ctas : 32;
+  const int grid = max_ctas > 0 ? max_ctas : 16;
   replica_trans_kernel<<<grid, 512, 0, as_stream(stream)>>>(w1_ptrs, w2_ptrs, mask, E, m, my_rank,
                                                             (size_t)d_model * d_ff / 8);
   PP_LAUNCH_CHECK();
   return PP_OK;
 }
 
-extern "C" int pp_replica_agg(void* const* g1_ptrs, void* const* g2_ptrs, const int32_t* rep_slot,
-                              int32_t D, int32_t E, int32_t m, int32_t my_rank, int32_t d_model,
-                              int32_t d_ff, int32_t max_ctas, void* stream) {
-  PP_CHECK_ARG(g1_ptrs && g2_ptrs && rep_slot, "pp_replica_agg: null pointer");
-  PP_CHECK_ARG(m >= 1 && m <= kMaxListE && D >= 1 && my_rank >= 0 && my_rank < D,
-               "pp_replica_agg: bad D / m / rank");
+extern "C" int pp_replica_agg(void* const* g1_ptrs, void* const* g2_ptrs, void* const* stage_ptrs,
+                              const uint8_t* mask, int32_t E, int32_t m, int32_t my_rank,
+                              int32_t d_model, int32_t d_ff, int32_t max_ctas, void* stream) {
+  PP_CHECK_ARG(g1_ptrs && g2_ptrs && stage_ptrs && mask, "pp_replica_agg: null pointer");
+  PP_CHECK_ARG(E >= 1 && E <= kMaxItems && m >= 1 && E % m == 0 && (E / m) * E <= kMaxFlags &&
+                   my_rank >= 0 && my_rank < E / m,
+               "pp_replica_agg: bad E / m / rank");
   PP_CHECK_ARG(((size_t)d_model * d_ff) % 4 == 0, "pp_replica_agg: bad sizes");
-  const int grid = max_ctas > 0 ? max_ctas : 32;
-  replica_agg_kernel<<<grid, 512, 0, as_stream(stream)>>>(g1_ptrs, g2_ptrs, rep_slot, D, E, m,
-                                                          my_rank, (size_t)d_model * d_ff / 4);
+  const int grid = max_ctas > 0 ? max_ctas : 16;
+  replica_agg_push_kernel<<<grid, 512, 0, as_stream(stream)>>>(g1_ptrs, g2_ptrs, stage_ptrs, mask, E, m,
+                                                               my_rank, (size_t)d_model * d_ff / 4);
+  PP_LAUNCH_CHECK();
+  return PP_OK;
+}
+
+extern "C" int pp_replica_agg_reduce(float* g1, float* g2, const float* stage, const uint8_t* mask,
+                                     int32_t E, int32_t m, int32_t my_rank, int32_t d_model,
+                                     int32_t d_ff, int32_t max_ctas, void* stream) {
+  PP_CHECK_ARG(g1 && g2 && stage && mask, "pp_replica_agg_reduce: null pointer");
+  PP_CHECK_ARG(E >= 1 && E <= kMaxItems && m >= 1 && E % m == 0 && (E / m) * E <= kMaxFlags &&
+                   E / m <= 33 && my_rank >= 0 && my_rank < E / m,
+               "pp_replica_agg_reduce: bad E / m / rank (D <= 33)");
+  PP_CHECK_ARG(((size_t)d_model * d_ff) % 4 == 0, "pp_replica_agg_reduce: bad sizes");
+  const int grid = max_ctas > 0 ? max_ctas : 16;
+  replica_agg_reduce_kernel<<<grid, 512, 0, as_stream(stream)>>>(g1, g2, stage, mask, E, m, my_rank,
+                                                                  (size_t)d_model * d_ff / 4);
   PP_LAUNCH_CHECK();
   return PP_OK;
 }

@@ -220,6 +220,163 @@ __global__ void __launch_bounds__(kMaxPlanThreads) plan_greedy_kernel(PlanArgs a
   }
 }
 
+// ---- physically-faithful E > D planner -------------------------
+// Generalises Algorithm 1 to m = E / D experts per device (home of e = device e / m,
+// physical LoadMatrix rows); reduces to plan_greedy_kernel bit-for-bit when m == 1:
+//   * balance threshold alpha * total_inputs / D (planner.py:63-68 has E == D)
+//   * i = first argmax(H) is a device; the expert to replicate is its unused home
+//     expert that currently sends it the most rows (ties -> lower id); stop when i
+//     has none left (planner.py:115-117)
+//   * excluded = n non-home devices with the fewest rows of that expert on the
+//     original matrix, key (count, index) (planner.py:71-77)
+//   * objective = perf_model._build with num_devices = D, strict improvement accepts
+// counts may be virtual-slot rows (rows = E, rows / D slots per device): they are
+// summed per device on load; the emitted mask has `rows` rows (device row repeated).
+struct PhysArgs {
+  const int64_t* counts;
+  int rows, D, E;
+  pp_cost_model cm;
+  pp_planner_cfg cfg;
+  int32_t* selected;
+  int32_t* num_selected;
+  int32_t* num_explored;
+  uint8_t* mask;
+  int64_t* H;
+  int64_t* R;
+  double* best_cost;
+};
+
+__global__ void __launch_bounds__(kMaxPlanThreads) plan_physical_kernel(PhysArgs a) {
+  const int L = blockIdx.x;
+  const int D = a.D, E = a.E, m = E / D, rpd = a.rows / D;
+  const int t = threadIdx.x;
+  const int n = a.cfg.n;
+  const bool overlap = a.cfg.overlap_aware != 0;
+  extern __shared__ int64_t dyn[];
+  int64_t* phys = dyn;                                        // [D][E]
+  int64_t* sent = phys + (size_t)D * E;                       // [E] rows each expert's home receives
+  uint8_t* pmask = reinterpret_cast<uint8_t*>(sent + E);      // [D][E]
+  uint8_t* used = pmask + (size_t)D * E;                      // [E]
+  __shared__ Red scratch[kMaxWarps];
+  __shared__ int32_t sel_list[kMaxPlanThreads];
+  __shared__ int cand_e;
+
+  const int64_t* counts = a.counts + (size_t)L * a.rows * E;
+  for (int x = t; x < D * E; x += blockDim.x) {
+    const int d = x / E, e = x - (x / E) * E;
+    int64_t c = 0;
+    for (int r = 0; r < rpd; ++r) c += counts[(size_t)(d * rpd + r) * E + e];
+    phys[x] = c;
+    pmask[x] = (e / m == d);
+  }
+  for (int e = t; e < E; e += blockDim.x) used[e] = 0;
+  __syncthreads();
+
+  int64_t rowsum = 0;
+  if (t < D)
+    for (int e = 0; e < E; ++e) rowsum += phys[(size_t)t * E + e];
+  const int64_t total = block_reduce(Red{rowsum, 0}, SumOp(), scratch).v;
+  const int64_t total_inputs = total / a.cm.top_k;
+  const double threshold = __ddiv_rn(__dmul_rn(a.cfg.alpha, (double)total_inputs), (double)D);
+  const Red neutral_max{INT64_MIN, 0x7fffffff};
+  const Red neutral_min{INT64_MAX, 0x7fffffff};
+
+  // H/R of the current pmask: sent[e] by thread e, then device d sums its kept + home rows
+  auto loads = [&](int64_t& h, int64_t& r) {
+    for (int e = t; e < E; e += blockDim.x) {
+      int64_t s = 0;
+      for (int d = 0; d < D; ++d)
+        if (!pmask[(size_t)d * E + e]) s += phys[(size_t)d * E + e];
+      sent[e] = s;
+    }
+    __syncthreads();
+    h = 0;
+    r = 0;
+    if (t < D) {
+      for (int e = 0; e < E; ++e)
+        if (pmask[(size_t)t * E + e]) h += phys[(size_t)t * E + e];
+      for (int e = t * m; e < (t + 1) * m; ++e) r += sent[e];
+      h += r;
+    }
+  };
+  auto reduce3 = [&](int64_t h, int64_t r, Red& hmax, Red& hmin, Red& rmax) {
+    const bool act = t < D;
+    hmax = block_reduce(act ? Red{h, t} : neutral_max, MaxFirst(), scratch);
+    hmin = block_reduce(act ? Red{h, t} : neutral_min, MinOp(), scratch);
+    rmax = block_reduce(act ? Red{r, t} : neutral_max, MaxFirst(), scratch);
+  };
+  // replicate expert e: every non-home device except the n with the fewest rows of e
+  auto apply = [&](int e) {
+    const int home = e / m;
+    if (t < D && t != home) {
+      const int64_t c = phys[(size_t)t * E + e];
+      int rank = 0;
+      for (int j = 0; j < D; ++j) {
+        if (j == home || j == t) continue;
+        const int64_t cj = phys[(size_t)j * E + e];
+        rank += (cj < c) || (cj == c && j < t);
+      }
+      pmask[(size_t)t * E + e] = rank >= n;
+    }
+    __syncthreads();
+  };
+
+  int64_t h, r;
+  Red hmax, hmin, rmax;
+  loads(h, r);
+  reduce3(h, r, hmax, hmin, rmax);
+  double best = objective(a.cm, overlap, rmax.v, hmax.v, 0, 0);
+  int cnt = 0, s = 0;
+  while (true) {
+    if ((double)(hmax.v - hmin.v) < threshold) break;  // is_balanced
+    const int i = hmax.i;
+    __syncthreads();
+    if (t == 0) {
+      int ce = -1;
+      for (int e = i * m; e < (i + 1) * m; ++e)
+        if (!used[e] && (ce < 0 || sent[e] > sent[ce])) ce = e;
+      cand_e = ce;
+      if (ce >= 0) {
+        used[ce] = 1;
+        sel_list[s] = ce;
+      }
+    }
+    __syncthreads();
+    const int e = cand_e;
+    if (e < 0) break;
+    ++s;
+    apply(e);
+    loads(h, r);
+    reduce3(h, r, hmax, hmin, rmax);
+    const double changed = objective(a.cm, overlap, rmax.v, hmax.v, s, n);
+    if (changed < best) {
+      best = changed;
+      cnt = s;
+    }
+  }
+  __syncthreads();
+  // replay the accepted prefix, emit mask rows / H / R / selected
+  for (int x = t; x < D * E; x += blockDim.x) pmask[x] = ((x - (x / E) * E) / m == x / E);
+  __syncthreads();
+  for (int p = 0; p < cnt; ++p) apply(sel_list[p]);
+  loads(h, r);
+  if (t < D) {
+    a.H[(size_t)L * D + t] = h;
+    a.R[(size_t)L * D + t] = r;
+  }
+  uint8_t* mask = a.mask + (size_t)L * a.rows * E;
+  for (int x = t; x < a.rows * E; x += blockDim.x) {
+    const int v = x / E, e = x - (x / E) * E;
+    mask[x] = pmask[(size_t)(v / rpd) * E + e];
+  }
+  for (int e = t; e < E; e += blockDim.x) a.selected[(size_t)L * E + e] = e < cnt ? sel_list[e] : -1;
+  if (t == 0) {
+    a.num_selected[L] = cnt;
+    a.num_explored[L] = s;
+    a.best_cost[L] = best;
+  }
+}
+
 __global__ void derive_loads_kernel(const int64_t* counts, const uint8_t* mask, int D, int E,
                                     int64_t* H, int64_t* R) {
   for (int x = threadIdx.x; x < D; x += blockDim.x) {
@@ -288,6 +445,32 @@ extern "C" int pp_plan_greedy(const int64_t* counts, int32_t num_layers, int32_t
   PlanArgs a{counts, E, *cm, *cfg, selected, num_selected, num_explored, mask, H, R, best_cost};
   const int threads = ((E + 31) / 32) * 32;
   plan_greedy_kernel<<<num_layers, threads, sizeof(int64_t) * E, as_stream(stream)>>>(a);
+  PP_LAUNCH_CHECK();
+  return PP_OK;
+}
+
+extern "C" int pp_plan_physical(const int64_t* counts, int32_t num_layers, int32_t rows, int32_t D,
+                                int32_t E, const pp_cost_model* cm, const pp_planner_cfg* cfg,
+                                int32_t* selected, int32_t* num_selected, int32_t* num_explored,
+                                uint8_t* mask, int64_t* H, int64_t* R, double* best_cost,
+                                void* stream) {
+  PP_CHECK_ARG(counts && cm && cfg && selected && num_selected && num_explored && mask && H && R &&
+                   best_cost,
+               "pp_plan_physical: null pointer");
+  PP_CHECK_ARG(num_layers >= 1, "pp_plan_physical: num_layers must be >= 1, got %d", num_layers);
+  PP_CHECK_ARG(D >= 1 && E >= D && E % D == 0 && E <= kMaxPlanThreads,
+               "pp_plan_physical: need E a multiple of D and E <= %d (D=%d, E=%d)", kMaxPlanThreads, D, E);
+  PP_CHECK_ARG((int64_t)D * E <= 4096, "pp_plan_physical: D*E must be <= 4096, got %d", D * E);
+  PP_CHECK_ARG(rows >= D && rows % D == 0, "pp_plan_physical: rows (%d) must be a multiple of D (%d)", rows, D);
+  if (cm->num_devices != D || cm->num_experts != E)
+    return fail(PP_EDIM, "pp_plan_physical: cost model is %dx%d, load is %dx%d", cm->num_devices,
+                cm->num_experts, D, E);
+  PP_CHECK_ARG(cfg->n >= 0 && cfg->n < D, "n must be < num_devices=%d, got %d", D, cfg->n);
+  PP_CHECK_ARG(cm->top_k >= 1, "top_k must be >= 1");
+  PhysArgs a{counts, rows, D, E, *cm, *cfg, selected, num_selected, num_explored, mask, H, R, best_cost};
+  const int threads = ((E + 31) / 32) * 32;
+  const size_t smem = sizeof(int64_t) * ((size_t)D * E + E) + (size_t)D * E + E;
+  plan_physical_kernel<<<num_layers, threads, smem, as_stream(stream)>>>(a);
   PP_LAUNCH_CHECK();
   return PP_OK;
 }

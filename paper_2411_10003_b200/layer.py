@@ -160,7 +160,7 @@ class MoELayer(torch.nn.Module):
                  group=None, planner: PlannerConfig | None = None, cluster=None, model=None,
                  capacity_rows: int | None = None, max_replicas: int | None = None,
                  seed: int = 0, device=None, trans_ctas: int = 32, replica_engine: str = "copy",
-                 policy: str | None = None, planning: str = "host") -> None:
+                 policy: str | None = None, planning: str = "host", placement: str = "virtual") -> None:
         super().__init__()
         if not torch.cuda.is_available():
             raise RuntimeError("MoELayer needs a CUDA device (B200); there is no CPU path")
@@ -247,12 +247,24 @@ class MoELayer(torch.nn.Module):
         self.plan_enabled = D > 1
         self.mask_cur = None  # None = vanilla EP for iteration 0
         self._plan_out = _device.PlanBuffers(1, E, dev) if self.plan_enabled else None
+        # placement "virtual": the reference search, bit-exact, over E x E virtual expert
+        # slots; "physical": the opt-in E = m*D generalisation over D devices (pp_plan_physical,
+        # SURVEY 8(f) row 4) -- its [E][E] output mask repeats each device row over its slots
+        if placement not in ("virtual", "physical"):
+            raise ValidationError(f"placement must be 'virtual' or 'physical', got {placement!r}")
+        self.placement = placement
         self._cm = _device.cost_model(self.cluster, self.model, E) if self.plan_enabled else None
+        if self._cm is not None and placement == "physical":
+            if self.planner_cfg.n >= D:
+                raise ValidationError(f"physical placement needs planner n < world size {D}, got {self.planner_cfg.n}")
+            self._cm.num_devices = D
         self._pcfg = _device.planner_cfg(self.planner_cfg)
         self.plan_stream = torch.cuda.Stream(device=dev) if self.plan_enabled else None
         self.comm_stream = torch.cuda.Stream(device=dev) if D > 1 else None
         self.trans_ctas = trans_ctas  # SM-engine Trans (overlaps route/layout/dispatch)
-        self.agg_ctas = 2 * trans_ctas  # SM-engine Agg (runs beside DGRAD1)
+        # SM-engine Agg runs beside DGRAD1 on agg_ctas SMs (one CTA per SM); DGRAD1 then
+        # launches its persistent grid on the remaining SMs so neither waits for the other
+        self.agg_ctas = 32
         if replica_engine not in ("copy", "sm"):
             raise ValidationError(f"replica_engine must be 'copy' or 'sm', got {replica_engine!r}")
         # 'copy': Trans/Agg pulls run on the copy engines (cudaMemcpyAsync over NVLink,
@@ -287,6 +299,13 @@ class MoELayer(torch.nn.Module):
             self._counts_snap = torch.zeros((E, E), dtype=torch.int64, device=dev)
             if self.plan_enabled:
                 self.mask_cur = self.mask_buf  # identity = vanilla EP until the first plan lands
+        # SM-engine Agg: replicas push their grads into the home's staging area
+        # [m][D-1][W1|W2][d*f] fp32, the home sums them in rank order after a barrier on
+        # the comm stream (its own barrier object: its epochs advance on that stream)
+        self.agg_stage = None
+        if D > 1 and self.replica_engine == "sm":
+            self.agg_stage = PeerBuffer((self.m, D - 1, 2, d_ff * d_model), torch.float32, self.group, dev)
+            self.comm_barrier = _Barrier(self.group, dev)
         self._plan_pending = None
         self._mask_host = torch.zeros((E, E), dtype=torch.uint8).pin_memory() if D > 1 else None
         self.mask_cur_host = None
@@ -382,7 +401,7 @@ class MoELayer(torch.nn.Module):
                 self.plan_stream.wait_event(ev)
                 p0 = self._side_event(self.plan_stream)
                 _device.launch_plan(self._counts_snap.view(1, self.E, self.E), self._plan_out, self._cm,
-                                    self._pcfg, self.plan_stream)
+                                    self._pcfg, self.plan_stream, physical_devices=self._phys_devices())
                 self._log_side("Plan", p0, self._side_event(self.plan_stream))
                 self._plan_done_dev = torch.cuda.Event()
                 self._plan_done_dev.record(self.plan_stream)
@@ -395,13 +414,16 @@ class MoELayer(torch.nn.Module):
             snapshot.record_stream(self.plan_stream)
             p0 = self._side_event(self.plan_stream)
             _device.launch_plan(snapshot.view(1, self.E, self.E), self._plan_out, self._cm, self._pcfg,
-                                self.plan_stream)
+                                self.plan_stream, physical_devices=self._phys_devices())
             self._log_side("Plan", p0, self._side_event(self.plan_stream))
             mask_dev = self._plan_out.mask[0].clone()
             self._mask_host.copy_(mask_dev, non_blocking=True)
             done = torch.cuda.Event()
             done.record(self.plan_stream)
         self._plan_pending = (done, mask_dev)
+
+    def _phys_devices(self) -> int:
+        return self.world if self.placement == "physical" else 0
 
     def begin_iteration(self) -> None:
         """Adopt the plan computed during the previous iteration and derive this
@@ -554,14 +576,19 @@ class MoELayer(torch.nn.Module):
                               self._agg_staging.data_ptr(), self._agg_ranges.data_ptr(), self.m, self.d, self.f,
                               _device.stream_ptr(self.comm_stream))
             else:
+                cs = _device.stream_ptr(self.comm_stream)
                 _lib.call("pp_replica_agg", self.g1_arena.ptrs.data_ptr(), self.g2_arena.ptrs.data_ptr(),
-                          self.rep_slot.data_ptr(), self.world, self.E, self.m, self.rank, self.d, self.f,
-                          self.agg_ctas, _device.stream_ptr(self.comm_stream))
+                          self.agg_stage.ptrs.data_ptr(), self.mask_cur.data_ptr(), self.E, self.m, self.rank,
+                          self.d, self.f, self.agg_ctas, cs)
+                self.comm_barrier(self.comm_stream)  # every replica's grads have landed here
+                _lib.call("pp_replica_agg_reduce", self.g1_arena.local.data_ptr(), self.g2_arena.local.data_ptr(),
+                          self.agg_stage.local.data_ptr(), self.mask_cur.data_ptr(), self.E, self.m, self.rank,
+                          self.d, self.f, self.agg_ctas, cs)
             self._agg_done = torch.cuda.Event()
             self._agg_done.record(self.comm_stream)
             self._log_side("SubAgg2", t0, self._side_event(self.comm_stream))
 
-    def _gemm(self, mode, a, b, c, c2=None, stream=None):
+    def _gemm(self, mode, a, b, c, c2=None, stream=None, num_sms=None):
         timing = self.gemm_timing
         if timing is not None:
             pool = self.gemm_event_pool
@@ -572,7 +599,8 @@ class MoELayer(torch.nn.Module):
                 e1 = torch.cuda.Event(enable_timing=True)
             e0.record()
         _device.grouped_gemm(mode, a, b, c, c2, self.groups, self.num_groups, self.max_groups,
-                             self.rows_cap, self.slots, self.d, self.f, num_sms=self.gemm_sms, stream=stream)
+                             self.rows_cap, self.slots, self.d, self.f,
+                             num_sms=self.gemm_sms if num_sms is None else num_sms, stream=stream)
         if timing is not None:
             e1.record()
             timing.append((mode, e0, e1))
@@ -651,10 +679,15 @@ class MoELayer(torch.nn.Module):
         self._gemm(_lib.PP_GEMM_WGRAD2, self.dyp.local, self.act, self.g2_arena.local)
         self._gemm(_lib.PP_GEMM_WGRAD1, self.pre, self.xp.local, self.g1_arena.local)
         agg = self.world > 1 and self.mask_cur is not None
-        if agg:  # every rank's replica gradients exist: Agg rides on DGRAD1 (SubAgg | BEC)
-            self.barrier()
+        dgrad1_sms = None
+        if agg:  # Agg rides on DGRAD1 (SubAgg | BEC)
+            if self.replica_engine == "copy":
+                self.barrier()  # the home pulls: every rank's replica gradients must exist
             self._issue_agg()
-        self._gemm(_lib.PP_GEMM_DGRAD1, self.pre, self.w1_arena.local, self.dxp.local)
+            if self.replica_engine == "sm":
+                total = self.gemm_sms or _device.num_sms(self.device)
+                dgrad1_sms = max(2, (total - self.agg_ctas) // 2 * 2)
+        self._gemm(_lib.PP_GEMM_DGRAD1, self.pre, self.w1_arena.local, self.dxp.local, num_sms=dgrad1_sms)
         self._mark("bwd_gemms")
         self.barrier()
         self._mark("barrier4")
@@ -711,6 +744,19 @@ class MoELayer(torch.nn.Module):
             return np.eye(self.E, dtype=bool)
         return self.mask_cur.cpu().numpy().astype(bool)
 
+    def replica_traffic(self, mask: np.ndarray | None = None) -> dict:
+        """NVLink bytes of one iteration's Trans (bf16 W1+W2) and Agg (fp32 grads) per
+        rank under `mask` (default: the current plan): out = pushed by the home,
+        in = received by the replica holder (Trans); Agg the reverse direction."""
+        mh = self.current_mask() if mask is None else np.asarray(mask, dtype=bool)
+        D, m, E = self.world, self.m, self.E
+        reps = [[e for e in range(E) if e // m != r and mh[r * m:(r + 1) * m, e].any()] for r in range(D)]
+        w = 2 * self.d * self.f * 2  # W1 + W2 bf16
+        t_out = [sum(w for r in range(D) for e in reps[r] if e // m == h) for h in range(D)]
+        t_in = [len(reps[r]) * w for r in range(D)]
+        return {"replicas_per_rank": [len(x) for x in reps], "trans_out_bytes": t_out, "trans_in_bytes": t_in,
+                "agg_out_bytes": [2 * b for b in t_in], "agg_in_bytes": [2 * b for b in t_out]}
+
     def group_table(self) -> list:
         n = int(self.num_groups.item())
         t = self.groups[:n].cpu().numpy()
@@ -719,8 +765,9 @@ class MoELayer(torch.nn.Module):
 
     def close(self) -> None:
         for b in (self.w1_arena, self.w2_arena, self.g1_arena, self.g2_arena, self.xp, self.yp, self.dyp, self.dxp,
-                  self.counts_buf):
-            b.close()
+                  self.counts_buf, self.agg_stage):
+            if b is not None:
+                b.close()
 
 
 class _MoEFunction(torch.autograd.Function):

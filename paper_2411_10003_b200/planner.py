@@ -96,6 +96,34 @@ def greedy_search(load, config: PlannerConfig, cluster, model) -> ExpertPlacemen
     return greedy_search_many([load], config, cluster, model)[0].placement
 
 
+def greedy_search_physical_many(loads: Sequence, config: PlannerConfig, cluster, model) -> list:
+    """Physically-faithful search (opt-in) for L layers: loads are
+    [D][E] with E = m * D (expert e homed on device e // m).  Identical to
+    ``greedy_search_many`` when E == D; for m > 1 the rule generalisation is documented
+    in ``csrc/planner.cu`` and pinned only by that reduction (the reference requires
+    E == D, planner.py:88-90)."""
+    counts = [as_counts(x) for x in loads]
+    if not counts:
+        return []
+    for c in counts:
+        D, E = c.shape
+        if E % D:
+            raise ValidationError(f"num_experts must be a multiple of num_devices, got D={D}, E={E}")
+        if (cluster.num_devices, model.num_experts) != (D, E):
+            raise DimensionMismatchError(
+                f"cluster/model are {cluster.num_devices}/{model.num_experts}, load is {D}x{E}")
+        if config.n >= D:
+            raise ValidationError(f"n must be < num_devices={D}, got {config.n}")
+    from . import _device
+
+    return _device.plan_physical(np.stack(counts), config, cluster, model)
+
+
+def greedy_search_physical(load, config: PlannerConfig, cluster, model):
+    """One layer of ``greedy_search_physical_many``; returns a PhysicalPlacement."""
+    return greedy_search_physical_many([load], config, cluster, model)[0].placement
+
+
 def plan_source_iteration(iter_index: int, reuse_interval: int):
     """Index of the iteration whose LoadMatrix feeds iteration ``iter_index``'s
     plan under the reuse policy (None = empty placement).  The MoE layer uses the

@@ -36,8 +36,11 @@ def main():
     m = E // world
     cl = pp.ClusterSpec(E, 1e11, 1e6)  # cheap transfers: the planner replicates
     mo = pp.ModelSpec(E, 1, k, 2 * d, 1e3, 1e3)
+    placement = os.environ.get("PP_PLACEMENT", "virtual")
+    n_excl = int(os.environ.get("PP_N", "1" if placement == "virtual" else "0"))
     layer = pp.MoELayer(d, f, E, k, tokens=T, group=dist.group.WORLD,
-                        planner=pp.PlannerConfig(n=1, alpha=0.5), cluster=cl, model=mo, seed=0,
+                        planner=pp.PlannerConfig(n=n_excl, alpha=0.5), cluster=cl, model=mo, seed=0,
+                        placement=placement,
                         replica_engine=os.environ.get("PP_ENGINE", "copy"),
                         policy=os.environ.get("PP_POLICY") or None,
                         planning=os.environ.get("PP_PLANNING", "host"))
@@ -80,8 +83,14 @@ def main():
                 pass
             elif it > 0:
                 # plan_for_iteration: iteration it uses greedy(history[it-1])
-                cm = P.cost_model_dict(E, k, 2 * d, 1e3, 1e3, 1e11, 1e6)
-                exp = P.greedy_search(prev_counts, 1, 0.5, False, cm)
+                if placement == "physical":
+                    cm = P.cost_model_dict(world, k, 2 * d, 1e3, 1e3, 1e11, 1e6)
+                    phys = prev_counts.reshape(world, m, E).sum(axis=1)
+                    exp = P.greedy_search_physical(phys, n_excl, 0.5, False, cm)
+                    exp["mask"] = np.repeat(exp["mask"], m, axis=0)
+                else:
+                    cm = P.cost_model_dict(E, k, 2 * d, 1e3, 1e3, 1e11, 1e6)
+                    exp = P.greedy_search(prev_counts, n_excl, 0.5, False, cm)
                 if not np.array_equal(mask_used, exp["mask"]):
                     print(f"[it {it}] MASK MISMATCH: plan {exp['selected']}", flush=True)
                     ok = False
@@ -116,6 +125,28 @@ def main():
         okt = torch.tensor([1 if ok else 0], device=dev)
         dist.broadcast(okt, 0)
         ok = bool(okt.item())
+    if layer.planning == "device":
+        # graph replay of the whole EP step (barriers, plan, Trans/Agg inside) == eager, bit-exact
+        x, _ = M.exact_inputs(T, d, E, seed=4242 + rank)
+        xd = x.to(dev)
+        dyd = (torch.randn((T, d), generator=torch.Generator().manual_seed(5 + rank)) * 0.1).to(dev, torch.bfloat16)
+        for _ in range(3):  # same batch every step: the plan reaches its fixed point
+            xe = xd.clone().requires_grad_(True)
+            ye = layer(xe)
+            ye.backward(dyd)
+        torch.cuda.synchronize()
+        ref_out = (ye.detach().clone(), xe.grad.clone(), layer.w1.main_grad.clone(), layer.w2.main_grad.clone())
+        gs = layer.make_graphed_step(xd.clone(), dyd.clone())
+        for _ in range(2):
+            yg, dxg = gs()
+        torch.cuda.synchronize()
+        got = (yg, dxg, layer.w1.main_grad, layer.w2.main_grad)
+        same = all(torch.equal(a, b) for a, b in zip(ref_out, got))
+        flag = torch.tensor([1 if same else 0], device=dev)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if rank == 0:
+            print(f"[graph] replay == eager on {world} ranks: {'OK' if flag.item() else 'FAIL'}", flush=True)
+        ok = ok and bool(flag.item())
     layer.close()
     dist.barrier()
     dist.destroy_process_group()

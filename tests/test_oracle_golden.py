@@ -115,3 +115,44 @@ def test_oracle_against_live_reference(rng):
         res = P.greedy_search(counts, n, 0.5, ov, cm)
         assert res["selected"] == pl.selected
         assert tuple(frozenset(x) for x in res["excluded"]) == pl.excluded
+
+
+def test_physical_planner_reduces_to_reference_at_m1():
+    """The physically-faithful E > D search is parity-pinned by
+    reduction: at m = E / D = 1 it must reproduce every reference golden plan."""
+    for c, counts in load_cases():
+        res = P.greedy_search_physical(counts, c["n"], c["alpha"], c["overlap"], cm_of(c))
+        check_plan(res, c)
+        assert res["explored"] == P.greedy_search(counts, c["n"], c["alpha"], c["overlap"], cm_of(c))["explored"]
+
+
+def test_physical_derive_loads_rules(rng):
+    """Physical derive_loads (homes e // m) == the slot-level rule summed per device, and
+    at m = 1 == the reference derive_loads restatement."""
+    for _ in range(50):
+        D = int(rng.integers(2, 6))
+        m = int(rng.integers(1, 4))
+        E = D * m
+        counts = rng.integers(0, 9, size=(D, E))
+        mask = rng.random((D, E)) < 0.3
+        for e in range(E):
+            mask[e // m, e] = True
+        H, R = P.derive_loads_physical(counts, mask)
+        assert H.sum() == counts.sum() and R.sum() == sum(int(counts[d, e]) for d in range(D) for e in range(E)
+                                                          if not mask[d, e])
+        if m == 1:
+            H1, R1 = P.derive_loads(counts, mask)
+            assert H.tolist() == H1.tolist() and R.tolist() == R1.tolist()
+    # fuzz over m > 1: the returned plan never costs more than vanilla EP, conserves rows, keeps homes
+    for i in range(40):
+        D = int(rng.integers(2, 9))
+        m = int(rng.integers(2, 5))
+        E = D * m
+        probs = rng.dirichlet(np.ones(E) * 0.3)
+        counts = np.stack([rng.multinomial(512, probs) for _ in range(D)])
+        cm = P.cost_model_dict(D, 2, 2048, 1.6e7, 3.2e7, 4e11, 1e8 * (1 + i % 4))
+        res = P.greedy_search_physical(counts, int(rng.integers(0, D)), 0.5, bool(i % 2), cm)
+        H0, R0 = P.derive_loads_physical(counts, P.replica_mask_physical(D, E, (), ()))
+        assert res["best"] <= P.objective(H0, R0, 0, 0, cm, bool(i % 2))  # strict improvements only
+        assert res["H"].sum() == counts.sum()
+        assert all(e // m != d or res["mask"][d, e] for d in range(D) for e in range(E))

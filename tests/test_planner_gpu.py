@@ -119,3 +119,72 @@ def test_plan_for_iteration_reuse():
     assert pp.plan_for_iteration(hist, 4, cfg, cl, mo) == pp.greedy_search(flat, cfg, cl, mo)
     with pytest.raises(pp.ValidationError):
         pp.plan_for_iteration(hist, 6, cfg, cl, mo)
+
+
+# ---- physically-faithful E > D planner (pp_plan_physical) ----------
+
+def test_physical_planner_equals_reference_at_m1():
+    """At m = E / D = 1 the physical search is the reference search, bit for bit."""
+    cases = json.loads((G / "planner_cases.json").read_text())
+    counts = np.load(G / "planner_counts.npz")
+    for c in cases:
+        k = counts[f"arr_{c['counts_index']}"]
+        cl, mo = specs(c["cm"], k.shape[0])
+        cfg = pp.PlannerConfig(n=c["n"], alpha=c["alpha"], overlap_aware=c["overlap"])
+        res = pp.greedy_search_physical_many([k], cfg, cl, mo)[0]
+        assert_same(res, c)
+        assert res.explored == pp.greedy_search_many([k], cfg, cl, mo)[0].explored
+
+
+@pytest.mark.parametrize("D,m", [(2, 2), (2, 8), (4, 4), (8, 2), (8, 8), (16, 4), (3, 5)])
+def test_physical_planner_fuzz_vs_oracle(D, m):
+    E = D * m
+    rng = np.random.default_rng(77 + D * 100 + m)
+    mats, cfgs = [], []
+    for i in range(60):
+        probs = rng.dirichlet(np.ones(E) * (0.2 + 0.3 * (i % 4)))
+        mats.append(np.stack([rng.multinomial(256 * m, probs) for _ in range(D)]).astype(np.int64))
+    for i, k in enumerate(mats):
+        n = int(i % D) if D > 1 else 0
+        ov = bool(i % 2)
+        cm = P.cost_model_dict(D, 2, 2048, 1.6e7 * (1 + i % 3), 3.2e7, 4e11 / (1 + i % 5), 1e8 * (1 + i % 4),
+                               1e-4 * (i % 3), 2e-4)
+        cl = pp.ClusterSpec(D, cm["avg_bandwidth"], cm["compute_throughput"])
+        mo = pp.ModelSpec(E, 1, 2, cm["input_bytes"], cm["expert_param_bytes"], cm["expert_grad_bytes"],
+                          fnec_time=cm["fnec_time"], bnec_time=cm["bnec_time"])
+        cfg = pp.PlannerConfig(n=n, alpha=0.5 if i % 3 else 0.1, overlap_aware=ov)
+        res = pp.greedy_search_physical_many([k], cfg, cl, mo)[0]
+        exp = P.greedy_search_physical(k, n, cfg.alpha, ov, cm)
+        assert list(res.placement.selected) == list(exp["selected"]), i
+        assert [sorted(x) for x in res.placement.excluded] == [sorted(x) for x in exp["excluded"]]
+        assert res.placement.replica_mask().tolist() == exp["mask"].tolist()
+        assert res.H.tolist() == exp["H"].tolist() and res.R.tolist() == exp["R"].tolist()
+        assert float(res.best_cost).hex() == float(exp["best"]).hex()
+        assert res.explored == exp["explored"]
+
+
+def test_physical_planner_slot_rows_input():
+    """Virtual-slot rows (rows = E, m per device) are summed per device on load and the
+    emitted mask repeats each device row over its slots (the layout's slot mask)."""
+    import torch
+
+    from paper_2411_10003_b200 import _device
+
+    D, m = 4, 4
+    E = D * m
+    rng = np.random.default_rng(5)
+    slot = np.stack([rng.multinomial(512, rng.dirichlet(np.ones(E) * 0.3)) for _ in range(E)]).astype(np.int64)
+    phys = slot.reshape(D, m, E).sum(axis=1)
+    cm = P.cost_model_dict(D, 2, 2048, 1.6e7, 3.2e7, 4e11, 1e8)
+    exp = P.greedy_search_physical(phys, 1, 0.5, True, cm)
+    cl = pp.ClusterSpec(D, cm["avg_bandwidth"], cm["compute_throughput"])
+    mo = pp.ModelSpec(E, 1, 2, cm["input_bytes"], cm["expert_param_bytes"], cm["expert_grad_bytes"])
+    out = _device.PlanBuffers(1, E, torch.device("cuda", 0))
+    _device.launch_plan(torch.from_numpy(slot).cuda().view(1, E, E), out, _device.cost_model(cl, mo),
+                        _device.planner_cfg(pp.PlannerConfig(n=1, alpha=0.5, overlap_aware=True)),
+                        physical_devices=D)
+    torch.cuda.synchronize()
+    assert out.mask[0].cpu().numpy().astype(bool).tolist() == np.repeat(exp["mask"], m, axis=0).tolist()
+    assert out.H[0, :D].cpu().tolist() == exp["H"].tolist()
+    with pytest.raises(pp.ValidationError):
+        pp.greedy_search_physical(pp.LoadMatrix(phys[:, :E - 1]), pp.PlannerConfig(), cl, mo)
