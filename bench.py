@@ -558,7 +558,7 @@ def main() -> None:
             else:
                 xin = xdev[b].detach().requires_grad_(True)
                 yv = layer(xin)
-                loss = (yv.detach().float() * dy.float()).sum()  # the probe loss; dL/dy = dy
+                loss = layer.probe_loss(yv.detach(), dy)  # the probe loss; dL/dy = dy
                 yv.backward(dy)
             ev_free[b].record(main)
             with torch.cuda.stream(back):

@@ -214,6 +214,14 @@ int pp_grouped_gemm(int32_t mode, const void* a, const void* b, void* c, void* c
                     int32_t rows_capacity, int32_t num_slots, int32_t d_model, int32_t d_ff,
                     int32_t num_sms, void* stream);
 
+/* Probe loss of the training-step API: out[0] = sum(a[i] * b[i]) over n bf16
+ * elements (n % 8 == 0, 16-byte aligned) in fp32, deterministic (per-CTA
+ * partials in a fixed order, then one CTA).  partial: >= PP_DOT_PARTIALS floats
+ * of device scratch.  The loss sum(y * g) has dL/dy = g, so a training loop
+ * that feeds g as the upstream gradient reads back one scalar per step. */
+#define PP_DOT_PARTIALS 592
+int pp_dot_bf16(const void* a, const void* b, int64_t n, float* partial, float* out, void* stream);
+
 /* ---- replica Trans / Agg over peer memory (K5) --------------------------- */
 /* Trans (home side, SM engine): push each of this rank's home experts' W1/W2
  * (weight arenas [slots][f][d] and [slots][d][f] bf16, peer pointer tables

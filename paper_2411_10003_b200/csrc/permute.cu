@@ -549,3 +549,63 @@ extern "C" int pp_gate_bwd(const void* dl, const void* wg, const void* x, int32_
   if (T % split) split = T;
   return gate_bwd_gemms(dl, wg, x, T, d, E, EP, dx, dwg, split, as_stream(stream));
 }
+
+// ---------------------------------------------------------------------------
+// probe loss sum(a * b) over n bf16 elements in fp32: per-CTA partial sums in a fixed
+// element order, then one CTA adds the partials in CTA order (deterministic; one HBM
+// pass over both operands).
+namespace pp {
+constexpr int kDotCtas = 592;  // 4 per SM
+
+__global__ void __launch_bounds__(512) dot_bf16_partial_kernel(const uint4* a, const uint4* b, int64_t nvec,
+                                                               float* partial) {
+  float s = 0.f;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nvec; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint4 x = ld_nc_v4(a + i), y = ld_nc_v4(b + i);
+    const uint32_t xs[4] = {x.x, x.y, x.z, x.w}, ys[4] = {y.x, y.y, y.z, y.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 fx = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xs[j]));
+      const float2 fy = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ys[j]));
+      s = fmaf(fx.x, fy.x, s);
+      s = fmaf(fx.y, fy.y, s);
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  __shared__ float ws[16];
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = 0.f;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += ws[w];
+    partial[blockIdx.x] = t;
+  }
+}
+
+__global__ void dot_bf16_final_kernel(const float* partial, int n, float* out) {
+  __shared__ float ws[32];
+  float s = 0.f;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s += partial[i];
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = 0.f;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += ws[w];
+    *out = t;
+  }
+}
+}  // namespace pp
+
+extern "C" int pp_dot_bf16(const void* a, const void* b, int64_t n, float* partial, float* out,
+                           void* stream) {
+  PP_CHECK_ARG(a && b && partial && out, "pp_dot_bf16: null pointer");
+  PP_CHECK_ARG(n >= 0 && n % 8 == 0, "pp_dot_bf16: n=%lld must be a multiple of 8", (long long)n);
+  PP_CHECK_ARG(((uintptr_t)a | (uintptr_t)b) % 16 == 0, "pp_dot_bf16: operands must be 16-byte aligned");
+  cudaStream_t st = as_stream(stream);
+  dot_bf16_partial_kernel<<<kDotCtas, 512, 0, st>>>(reinterpret_cast<const uint4*>(a),
+                                                    reinterpret_cast<const uint4*>(b), n / 8, partial);
+  dot_bf16_final_kernel<<<1, 1024, 0, st>>>(partial, kDotCtas, out);
+  PP_LAUNCH_CHECK();
+  return PP_OK;
+}

@@ -744,6 +744,17 @@ class MoELayer(torch.nn.Module):
             return np.eye(self.E, dtype=bool)
         return self.mask_cur.cpu().numpy().astype(bool)
 
+    def probe_loss(self, y: torch.Tensor, g: torch.Tensor) -> torch.Tensor:
+        """loss = sum(y * g) in fp32 (one fused pass, pp_dot_bf16): a linear probe whose
+        gradient w.r.t. y is exactly g -- the scalar a training loop reads back per step."""
+        assert y.shape == g.shape and y.dtype == g.dtype == torch.bfloat16
+        if getattr(self, "_dot_partial", None) is None:
+            self._dot_partial = torch.empty(_lib.PP_DOT_PARTIALS, dtype=torch.float32, device=self.device)
+        out = torch.empty((), dtype=torch.float32, device=self.device)
+        _lib.call("pp_dot_bf16", y.data_ptr(), g.data_ptr(), y.numel(), self._dot_partial.data_ptr(),
+                  out.data_ptr(), self._sp())
+        return out
+
     def replica_traffic(self, mask: np.ndarray | None = None) -> dict:
         """NVLink bytes of one iteration's Trans (bf16 W1+W2) and Agg (fp32 grads) per
         rank under `mask` (default: the current plan): out = pushed by the home,
@@ -805,7 +816,7 @@ class GraphedStep:
         self.graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(self.graph):
             self.y = layer.forward_raw(x)
-            self.loss = (self.y.float() * dy.float()).sum() if with_loss else None
+            self.loss = layer.probe_loss(self.y, dy) if with_loss else None
             self.dx = layer.backward_raw(x, dy)
         layer.gemm_timing, layer.phase_log = saved_timing, saved_phase
 

@@ -110,3 +110,22 @@ def test_layer_repeatable_and_iteration_counter():
     assert layer.iteration == 1
     lm = layer.last_load_matrix()
     assert lm.total() == 2048 * 2
+
+
+def test_probe_loss_and_graphed_step():
+    """pp_dot_bf16 (the training-step probe loss) vs a torch fp32 reference (rel 1e-4, fp32
+    accumulation-order tolerance), deterministic across calls; a captured CUDA-graph step
+    reproduces the eager step bit-exactly and its in-graph loss equals probe_loss."""
+    layer, x, wg, dy, y1, dx1 = run_layer(2048, 256, 512, 16, 2, seed=3)
+    dev = layer.device
+    yv, g = y1.to(dev), dy.to(dev)
+    l1, l2 = layer.probe_loss(yv, g), layer.probe_loss(yv, g)
+    ref = (yv.double() * g.double()).sum().item()
+    assert torch.equal(l1, l2)
+    assert abs(l1.item() - ref) <= 1e-4 * max(1.0, abs(ref)) + 1e-3
+    xs, dys = x.to(dev).contiguous(), dy.to(dev).contiguous()
+    gs = layer.make_graphed_step(xs.clone(), dys.clone(), with_loss=True)
+    ya, dxa = gs()
+    torch.cuda.synchronize()
+    assert torch.equal(ya, y1.to(dev)) and torch.equal(dxa, dx1.to(dev))
+    assert torch.equal(gs.loss, layer.probe_loss(ya, dys))
