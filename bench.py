@@ -299,6 +299,8 @@ def main() -> None:
     ap.add_argument("--placement", default="physical", choices=["virtual", "physical"],
                     help="planner over physical devices (E = m*D generalisation, 8(f) row 4; == the reference "
                          "search when E == D) or over E x E virtual expert slots (the reference search verbatim)")
+    ap.add_argument("--avg-bandwidth", type=float, default=None,
+                    help="planner cost model B (bytes/s; default layer.default_specs' 450e9)")
     ap.add_argument("--trans-ctas", type=int, default=None, help="SMs of the SM-engine Trans push")
     ap.add_argument("--agg-ctas", type=int, default=None, help="SMs of the SM-engine Agg push/reduce")
     args = ap.parse_args()
@@ -352,7 +354,13 @@ def main() -> None:
     # N > 1: planning stays on the device (plan -> mask double buffer, SM-driven Trans/Agg)
     # so the whole EP step -- peer barriers included -- is captured in one CUDA graph
     planning = "device" if world > 1 and not args.eager else "host"
-    layer = pp.MoELayer(d, f, E, k, tokens=T, group=group, planner=planner, seed=0, policy=args.policy,
+    specs = {}
+    if args.avg_bandwidth:
+        from paper_2411_10003_b200.layer import default_specs
+
+        cl_, mo_ = default_specs(E, k, d, f, T * world, avg_bandwidth=args.avg_bandwidth)
+        specs = {"cluster": cl_, "model": mo_}
+    layer = pp.MoELayer(d, f, E, k, tokens=T, group=group, planner=planner, seed=0, policy=args.policy, **specs,
                         planning=planning, placement=args.placement if world > 1 else "virtual")
     if args.trans_ctas:
         layer.trans_ctas = args.trans_ctas
@@ -632,6 +640,7 @@ def main() -> None:
                        "l2": "working set > L2 (activations+weights >> 126 MB), no flush",
                        "routing": "Zipf(1.2) gate bias, random bf16 tokens", "policy": args.policy,
                        "planner": {"n": args.n_excl, "alpha": args.alpha, "reuse_interval": 1,
+                                   "avg_bandwidth": layer.cluster.avg_bandwidth,
                                    "placement": layer.placement, "planning": layer.planning,
                                    "replica_engine": layer.replica_engine}},
             "host_enqueue_ms_per_step": host_ms, "phase_ms_rank0": phases,

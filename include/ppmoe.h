@@ -239,16 +239,18 @@ int pp_replica_trans(void* const* w1_ptrs, void* const* w2_ptrs, const uint8_t* 
 /* Agg phase 1 (replica side): push the fp32 grads of this rank's replica slots
  * (g1_ptrs/g2_ptrs [D] grad arenas) into the home rank's staging area
  * stage_ptrs[home] laid out [m][D-1][2][d_ff*d_model] fp32 (index r' = this
- * rank's position among the home's D-1 peers). */
+ * rank's position among the home's D-1 peers).  parts: 1 = W1 grads, 2 = W2
+ * grads, 3 = both (the layer pushes W2's as soon as WGRAD2 is done, W1's after
+ * WGRAD1). */
 int pp_replica_agg(void* const* g1_ptrs, void* const* g2_ptrs, void* const* stage_ptrs,
                    const uint8_t* mask, int32_t E, int32_t m, int32_t my_rank, int32_t d_model,
-                   int32_t d_ff, int32_t max_ctas, void* stream);
+                   int32_t d_ff, int32_t parts, int32_t max_ctas, void* stream);
 
 /* Agg phase 2 (home side, after a peer barrier): grad[j] += stage[j][r'] for
  * every rank holding expert my_rank*m + j, in ascending rank order (the
  * oracle's summation order).  g1/g2/stage are this rank's local buffers. */
 int pp_replica_agg_reduce(float* g1, float* g2, const float* stage, const uint8_t* mask, int32_t E,
-                          int32_t m, int32_t my_rank, int32_t d_model, int32_t d_ff,
+                          int32_t m, int32_t my_rank, int32_t d_model, int32_t d_ff, int32_t parts,
                           int32_t max_ctas, void* stream);
 
 /* Copy-engine Trans/Agg: one cudaMemcpyAsync per (dst, src, bytes) triple of

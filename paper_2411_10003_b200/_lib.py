@@ -76,9 +76,9 @@ SIGNATURES = {
     "pp_gate_bwd": [P, P, P, I, I, I, I, P, P, P],
     "pp_grouped_gemm": [I, P, P, P, P, P, P, I, I, I, I, I, I, P],
     "pp_replica_trans": [P, P, P, I, I, I, I, I, I, P],
-    "pp_replica_agg": [P, P, P, P, I, I, I, I, I, I, P],
+    "pp_replica_agg": [P, P, P, P, I, I, I, I, I, I, I, P],
     "pp_dot_bf16": [P, P, ctypes.c_int64, P, P, P],
-    "pp_replica_agg_reduce": [P, P, P, P, I, I, I, I, I, I, P],
+    "pp_replica_agg_reduce": [P, P, P, P, I, I, I, I, I, I, I, P],
     "pp_copy_batch": [P, P, P, I, P],
     "pp_agg_accumulate": [P, P, P, P, I, I, I, P],
     "pp_device_alloc": [c_uint64, POINTER(c_void_p)],

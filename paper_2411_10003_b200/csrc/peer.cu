@@ -95,7 +95,7 @@ __device__ int compact_items(const int* cand, int n, int* items) {
   return cnt;
 }
 
-// 16-byte copy of `nmat` matrices of `vecs` uint4 each, addresses from addr(item, W1|W2):
+// 16-byte copy of `nmat` matrices of `vecs` uint4 each, addresses from addr(matrix index):
 // CTAs stride over (matrix, chunk) pairs -- one 32-bit division per chunk, none per
 // element -- and each thread keeps U independent loads in flight.
 template <int U, class Addr>
@@ -109,7 +109,7 @@ __device__ __forceinline__ void push_copy(int nmat, size_t vecs, Addr addr) {
     const size_t off = (size_t)(c - mat * per_mat) * chunk + threadIdx.x;
     const uint4* src;
     uint4* dst;
-    addr(mat >> 1, mat & 1, src, dst);
+    addr(mat, 0, src, dst);
     uint4 r[U];
 #pragma unroll
     for (int u = 0; u < U; ++u)
@@ -136,7 +136,8 @@ __global__ void __launch_bounds__(512) replica_trans_kernel(void* const* w1_ptrs
   }
   __syncthreads();
   const int n = compact_items(cand, D * m, items);
-  push_copy<kPushUnroll>(n * 2, vecs, [&](int it, int mat, const uint4*& src, uint4*& dst) {
+  push_copy<kPushUnroll>(n * 2, vecs, [&](int it2, int, const uint4*& src, uint4*& dst) {
+    const int it = it2 >> 1, mat = it2 & 1;
     const int code = items[it], rj = code >> 10, i = code & 1023;
     const int r = rj / m, j = rj - (rj / m) * m;
     void* const* ptrs = mat ? w2_ptrs : w1_ptrs;
@@ -150,7 +151,7 @@ __global__ void __launch_bounds__(512) replica_trans_kernel(void* const* w1_ptrs
 // home's D-1 peers), so the home can sum its sources in rank order.
 __global__ void __launch_bounds__(512) replica_agg_push_kernel(void* const* g1_ptrs, void* const* g2_ptrs,
                                                                void* const* stage_ptrs, const uint8_t* mask,
-                                                               int E, int m, int me, size_t vecs) {
+                                                               int E, int m, int me, size_t vecs, int parts) {
   __shared__ uint8_t flag[kMaxFlags];
   __shared__ int cand[kMaxItems], items[kMaxItems];
   const int D = E / m;
@@ -159,7 +160,9 @@ __global__ void __launch_bounds__(512) replica_agg_push_kernel(void* const* g1_p
     cand[e] = flag[me * E + e] ? (e << 10 | replica_index(flag, E, me, e)) : -1;
   __syncthreads();
   const int n = compact_items(cand, E, items);
-  push_copy<kPushUnroll>(n * 2, vecs, [&](int it, int mat, const uint4*& src, uint4*& dst) {
+  const int np = parts == 3 ? 2 : 1;  // bit 0: W1 grads, bit 1: W2 grads
+  push_copy<kPushUnroll>(n * np, vecs, [&](int it2, int, const uint4*& src, uint4*& dst) {
+    const int it = np == 2 ? it2 >> 1 : it2, mat = np == 2 ? (it2 & 1) : (parts >> 1);
     const int code = items[it], e = code >> 10, i = code & 1023;
     const int h = e / m, j = e - h * m, rp = me < h ? me : me - 1;
     src = reinterpret_cast<const uint4*>((mat ? g2_ptrs : g1_ptrs)[me]) + (size_t)(m + i) * vecs;
@@ -171,7 +174,7 @@ __global__ void __launch_bounds__(512) replica_agg_push_kernel(void* const* g1_p
 // hold expert me*m + j, ascending r (deterministic, = the oracle's rank-order sum).
 __global__ void __launch_bounds__(512, 1) replica_agg_reduce_kernel(float* g1, float* g2, const float* stage,
                                                                     const uint8_t* mask, int E, int m, int me,
-                                                                    size_t vecs) {
+                                                                    size_t vecs, int parts) {
   __shared__ uint8_t flag[kMaxFlags];
   __shared__ int cand[kMaxItems], items[kMaxItems];
   __shared__ uint32_t srcmask[kMaxItems];
@@ -192,11 +195,12 @@ __global__ void __launch_bounds__(512, 1) replica_agg_reduce_kernel(float* g1, f
   constexpr int U = kReduceUnroll, kThreads = 512;
   const size_t chunk = (size_t)kThreads * U;
   const int per_mat = (int)((vecs + chunk - 1) / chunk);
-  const int nchunks = n * 2 * per_mat;
+  const int np = parts == 3 ? 2 : 1;  // bit 0: W1 grads, bit 1: W2 grads
+  const int nchunks = n * np * per_mat;
   for (int c = blockIdx.x; c < nchunks; c += gridDim.x) {  // (active slot, g1|g2, chunk)
     const int mat = c / per_mat;
     const size_t off = (size_t)(c - mat * per_mat) * chunk + threadIdx.x;
-    const int j = items[mat >> 1], w = mat & 1;
+    const int j = items[np == 2 ? mat >> 1 : mat], w = np == 2 ? (mat & 1) : (parts >> 1);
     const uint32_t bits = srcmask[j];
     float4* dst = reinterpret_cast<float4*>(w ? g2 : g1) + (size_t)j * vecs + off;
     const float4* src = reinterpret_cast<const float4*>(stage) + (size_t)j * (D - 1) * 2 * vecs + w * vecs + off;
@@ -289,7 +293,9 @@ extern "C" int pp_replica_trans(void* const* w1_ptrs, void* const* w2_ptrs, cons
 
 extern "C" int pp_replica_agg(void* const* g1_ptrs, void* const* g2_ptrs, void* const* stage_ptrs,
                               const uint8_t* mask, int32_t E, int32_t m, int32_t my_rank,
-                              int32_t d_model, int32_t d_ff, int32_t max_ctas, void* stream) {
+                              int32_t d_model, int32_t d_ff, int32_t parts, int32_t max_ctas,
+                              void* stream) {
+  PP_CHECK_ARG(parts >= 1 && parts <= 3, "pp_replica_agg: parts must be 1 (W1), 2 (W2) or 3, got %d", parts);
   PP_CHECK_ARG(g1_ptrs && g2_ptrs && stage_ptrs && mask, "pp_replica_agg: null pointer");
   PP_CHECK_ARG(E >= 1 && E <= kMaxItems && m >= 1 && E % m == 0 && (E / m) * E <= kMaxFlags &&
                    my_rank >= 0 && my_rank < E / m,
@@ -297,14 +303,15 @@ extern "C" int pp_replica_agg(void* const* g1_ptrs, void* const* g2_ptrs, void* 
   PP_CHECK_ARG(((size_t)d_model * d_ff) % 4 == 0, "pp_replica_agg: bad sizes");
   const int grid = max_ctas > 0 ? max_ctas : 16;
   replica_agg_push_kernel<<<grid, 512, 0, as_stream(stream)>>>(g1_ptrs, g2_ptrs, stage_ptrs, mask, E, m,
-                                                               my_rank, (size_t)d_model * d_ff / 4);
+                                                               my_rank, (size_t)d_model * d_ff / 4, parts);
   PP_LAUNCH_CHECK();
   return PP_OK;
 }
 
 extern "C" int pp_replica_agg_reduce(float* g1, float* g2, const float* stage, const uint8_t* mask,
                                      int32_t E, int32_t m, int32_t my_rank, int32_t d_model,
-                                     int32_t d_ff, int32_t max_ctas, void* stream) {
+                                     int32_t d_ff, int32_t parts, int32_t max_ctas, void* stream) {
+  PP_CHECK_ARG(parts >= 1 && parts <= 3, "pp_replica_agg_reduce: parts must be 1, 2 or 3, got %d", parts);
   PP_CHECK_ARG(g1 && g2 && stage && mask, "pp_replica_agg_reduce: null pointer");
   PP_CHECK_ARG(E >= 1 && E <= kMaxItems && m >= 1 && E % m == 0 && (E / m) * E <= kMaxFlags &&
                    E / m <= 33 && my_rank >= 0 && my_rank < E / m,
@@ -312,7 +319,7 @@ extern "C" int pp_replica_agg_reduce(float* g1, float* g2, const float* stage, c
   PP_CHECK_ARG(((size_t)d_model * d_ff) % 4 == 0, "pp_replica_agg_reduce: bad sizes");
   const int grid = max_ctas > 0 ? max_ctas : 16;
   replica_agg_reduce_kernel<<<grid, 512, 0, as_stream(stream)>>>(g1, g2, stage, mask, E, m, my_rank,
-                                                                  (size_t)d_model * d_ff / 4);
+                                                                  (size_t)d_model * d_ff / 4, parts);
   PP_LAUNCH_CHECK();
   return PP_OK;
 }

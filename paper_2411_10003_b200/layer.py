@@ -262,9 +262,10 @@ class MoELayer(torch.nn.Module):
         self.plan_stream = torch.cuda.Stream(device=dev) if self.plan_enabled else None
         self.comm_stream = torch.cuda.Stream(device=dev) if D > 1 else None
         self.trans_ctas = trans_ctas  # SM-engine Trans (overlaps route/layout/dispatch)
-        # SM-engine Agg runs beside DGRAD1 on agg_ctas SMs (one CTA per SM); DGRAD1 then
-        # launches its persistent grid on the remaining SMs so neither waits for the other
-        self.agg_ctas = 32
+        # SM-engine Agg runs beside the backward GEMMs on agg_ctas SMs (one CTA per SM);
+        # those GEMMs launch their persistent grids on the remaining SMs so neither waits
+        # for the other (pushes reach NVLink rate from ~16 CTAs)
+        self.agg_ctas = 16
         if replica_engine not in ("copy", "sm"):
             raise ValidationError(f"replica_engine must be 'copy' or 'sm', got {replica_engine!r}")
         # 'copy': Trans/Agg pulls run on the copy engines (cudaMemcpyAsync over NVLink,
@@ -559,9 +560,10 @@ class MoELayer(torch.nn.Module):
     def agg_bytes(self) -> int:
         return sum(t[2] for t in self._agg_list)
 
-    def _issue_agg(self) -> None:
-        """K5 Agg: pull the replicas' grads of this rank's home experts and add
-        them (rank order) into main_grad, on the side stream."""
+    def _issue_agg(self, parts: int = 3) -> None:
+        """K5 Agg on the side stream: the replicas' grads of this rank's home experts
+        are added (rank order) into main_grad.  parts (SM engine): 1 = W1 grads, 2 = W2
+        grads, 3 = both; the copy engine always moves both."""
         if self.world == 1 or self.mask_cur is None:
             return
         ev = torch.cuda.Event()
@@ -579,14 +581,14 @@ class MoELayer(torch.nn.Module):
                 cs = _device.stream_ptr(self.comm_stream)
                 _lib.call("pp_replica_agg", self.g1_arena.ptrs.data_ptr(), self.g2_arena.ptrs.data_ptr(),
                           self.agg_stage.ptrs.data_ptr(), self.mask_cur.data_ptr(), self.E, self.m, self.rank,
-                          self.d, self.f, self.agg_ctas, cs)
+                          self.d, self.f, parts, self.agg_ctas, cs)
                 self.comm_barrier(self.comm_stream)  # every replica's grads have landed here
                 _lib.call("pp_replica_agg_reduce", self.g1_arena.local.data_ptr(), self.g2_arena.local.data_ptr(),
                           self.agg_stage.local.data_ptr(), self.mask_cur.data_ptr(), self.E, self.m, self.rank,
-                          self.d, self.f, self.agg_ctas, cs)
+                          self.d, self.f, parts, self.agg_ctas, cs)
             self._agg_done = torch.cuda.Event()
             self._agg_done.record(self.comm_stream)
-            self._log_side("SubAgg2", t0, self._side_event(self.comm_stream))
+            self._log_side("SubAgg1" if parts == 2 else "SubAgg2", t0, self._side_event(self.comm_stream))
 
     def _gemm(self, mode, a, b, c, c2=None, stream=None, num_sms=None):
         timing = self.gemm_timing
@@ -675,19 +677,28 @@ class MoELayer(torch.nn.Module):
         self._mark("combine_bwd")
         self.barrier()
         self._mark("barrier3")
-        self._gemm(_lib.PP_GEMM_DGRAD2, self.dyp.local, self.w2_arena.local, self.pre, self.pre)
-        self._gemm(_lib.PP_GEMM_WGRAD2, self.dyp.local, self.act, self.g2_arena.local)
-        self._gemm(_lib.PP_GEMM_WGRAD1, self.pre, self.xp.local, self.g1_arena.local)
         agg = self.world > 1 and self.mask_cur is not None
-        dgrad1_sms = None
-        if agg:  # Agg rides on DGRAD1 (SubAgg | BEC)
-            if self.replica_engine == "copy":
-                self.barrier()  # the home pulls: every rank's replica gradients must exist
-            self._issue_agg()
-            if self.replica_engine == "sm":
-                total = self.gemm_sms or _device.num_sms(self.device)
-                dgrad1_sms = max(2, (total - self.agg_ctas) // 2 * 2)
-        self._gemm(_lib.PP_GEMM_DGRAD1, self.pre, self.w1_arena.local, self.dxp.local, num_sms=dgrad1_sms)
+        if agg and self.replica_engine == "sm":
+            # SM engine: WGRAD2 first, so the replicas' W2 grads are pushed home while
+            # DGRAD2 and WGRAD1 run, and the W1 grads while DGRAD1 runs; those GEMMs leave
+            # agg_ctas SMs to the push/reduce kernels (SubAgg | BEC)
+            total = self.gemm_sms or _device.num_sms(self.device)
+            side_sms = max(2, (total - self.agg_ctas) // 2 * 2)
+            self._gemm(_lib.PP_GEMM_WGRAD2, self.dyp.local, self.act, self.g2_arena.local)
+            self._issue_agg(parts=2)
+            self._gemm(_lib.PP_GEMM_DGRAD2, self.dyp.local, self.w2_arena.local, self.pre, self.pre,
+                       num_sms=side_sms)
+            self._gemm(_lib.PP_GEMM_WGRAD1, self.pre, self.xp.local, self.g1_arena.local, num_sms=side_sms)
+            self._issue_agg(parts=1)
+            self._gemm(_lib.PP_GEMM_DGRAD1, self.pre, self.w1_arena.local, self.dxp.local, num_sms=side_sms)
+        else:
+            self._gemm(_lib.PP_GEMM_DGRAD2, self.dyp.local, self.w2_arena.local, self.pre, self.pre)
+            self._gemm(_lib.PP_GEMM_WGRAD2, self.dyp.local, self.act, self.g2_arena.local)
+            self._gemm(_lib.PP_GEMM_WGRAD1, self.pre, self.xp.local, self.g1_arena.local)
+            if agg:  # copy engine: the home pulls once every rank's replica grads exist; rides on DGRAD1
+                self.barrier()
+                self._issue_agg()
+            self._gemm(_lib.PP_GEMM_DGRAD1, self.pre, self.w1_arena.local, self.dxp.local)
         self._mark("bwd_gemms")
         self.barrier()
         self._mark("barrier4")
