@@ -41,12 +41,23 @@ constexpr int kMaxGroups = 256;
 
 enum Epi { EPI_BF16 = 0, EPI_GELU = 1, EPI_DGELU = 2, EPI_F32 = 3, EPI_ROUTE = 4, EPI_BF16_ADD = 5, EPI_F32_ATOMIC = 6 };
 
-// per-epilogue-warp staging for the TMA-store epilogue: one 32x32 block
-// (bf16: 2 KB, SWIZZLE_64B; fp32: 4 KB, SWIZZLE_128B); DGELU adds a second
-// 2 KB block that receives the TMA-loaded pre-activation
+// per-epilogue-warp staging for the TMA-store epilogue: a ring of out_bufs 32x32
+// blocks (bf16: 2 KB, SWIZZLE_64B; fp32: one 4 KB block, SWIZZLE_128B), so a warp
+// stages the next block while up to out_bufs-1 earlier TMA stores still read theirs;
+// DGELU / BF16_ADD put a 2 KB block for the TMA-loaded operand in front of the ring.
+// The short-K GEMMs with heavy epilogues (FWD1: two outputs + GeLU; DGRAD2: operand
+// load + GeLU') get deeper rings; the long-K ones keep one block and more stages.
+template <int EPI>
+constexpr int out_bufs() {
+  return EPI == EPI_GELU ? 3 : EPI == EPI_DGELU ? 2 : 1;
+}
+template <int EPI>
+constexpr int out_base() {
+  return (EPI == EPI_DGELU || EPI == EPI_BF16_ADD) ? 2048 : 0;
+}
 template <int EPI>
 constexpr int stage_bytes_per_warp() {
-  return EPI == EPI_F32 ? 4096 : (EPI == EPI_DGELU || EPI == EPI_BF16_ADD) ? 4096 : 2048;
+  return EPI == EPI_F32 ? 4096 : out_base<EPI>() + out_bufs<EPI>() * 2048;
 }
 
 struct GemmParams {
@@ -193,8 +204,14 @@ __device__ __forceinline__ void stage_and_store_f32(uint8_t* stage, const uint32
 template <int EPI>
 __device__ __forceinline__ void epilogue_chunk(const uint32_t (&raw)[32], const GemmParams& p,
                                                const Tile& tl, int r, int c, const uint4 (&pre_v)[4],
-                                               uint8_t* stage, const CUtensorMap* tmC,
+                                               uint8_t* stage, int& sbuf, const CUtensorMap* tmC,
                                                const CUtensorMap* tmC2, int lane) {
+  constexpr int NB = out_bufs<EPI>();
+  auto next_buf = [&]() -> uint8_t* {  // ring slot for the next staged 32x32 bf16 block
+    uint8_t* b = stage + out_base<EPI>() + sbuf * 2048;
+    if (++sbuf == NB) sbuf = 0;
+    return b;
+  };
   if constexpr (EPI == EPI_F32) {
     stage_and_store_f32(stage, raw, tmC, tl.n0 + c, tl.wslot * p.M_fixed + tl.m0 + (r & ~31), lane);
   } else if constexpr (tma_out<EPI>()) {
@@ -209,7 +226,7 @@ __device__ __forceinline__ void epilogue_chunk(const uint32_t (&raw)[32], const 
         for (int u = 0; u < 8; ++u) f[u] = __uint_as_float(raw[8 * j + u]);
         v[j] = f32x8_to_bf16(f);
       }
-      stage_and_store(stage, v, tmC, col, row, lane);
+      stage_and_store<NB - 1>(next_buf(), v, tmC, col, row, lane);
     } else if constexpr (EPI == EPI_GELU) {
       uint4 g4[4];
 #pragma unroll
@@ -223,8 +240,8 @@ __device__ __forceinline__ void epilogue_chunk(const uint32_t (&raw)[32], const 
         for (int u = 0; u < 8; ++u) g[u] = gelu_f(f[u]);
         g4[j] = f32x8_to_bf16(g);
       }
-      stage_and_store(stage, v, tmC, col, row, lane);
-      stage_and_store(stage, g4, tmC2, col, row, lane);
+      stage_and_store<NB - 1>(next_buf(), v, tmC, col, row, lane);
+      stage_and_store<NB - 1>(next_buf(), g4, tmC2, col, row, lane);
     } else {  // EPI_DGELU: acc * GeLU'(pre);  EPI_BF16_ADD: acc + old   (operand TMA-loaded)
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
@@ -236,7 +253,7 @@ __device__ __forceinline__ void epilogue_chunk(const uint32_t (&raw)[32], const 
                                   : __uint_as_float(raw[8 * j + u]) + x[u];
         v[j] = f32x8_to_bf16(f);
       }
-      stage_and_store(stage + 2048, v, tmC, col, row, lane);
+      stage_and_store<NB - 1>(next_buf(), v, tmC, col, row, lane);
     }
   } else if constexpr (EPI == EPI_F32_ATOMIC) {  // split-K partial: out[m][n] += acc
     if (tl.m0 + r < p.m_real) {
@@ -526,6 +543,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int col0 = ((warp - 4) >> 2) * EPI_COLS;  // column slice of this warp
     uint8_t* stage = smem + STAGES * STAGE_BYTES + (warp - 4) * stage_bytes_per_warp<EPI>();
     uint32_t pre_phase = 0;  // DGELU: parity of this warp's pre-activation TMA barrier
+    int sbuf = 0;            // ring slot of the next staged output block
     const int r = q * 32 + lane;
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -676,7 +694,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int j = 0; j < 32; ++j) cur[j] = 0u;
           }
           if (i + 1 == NCH) release_acc();  // every TMEM read of this tile has completed
-          if (tl.active) epilogue_chunk<EPI>(cur, p, tl, r, c, pre_v, stage, &tmC, &tmC2, lane);
+          if (tl.active) epilogue_chunk<EPI>(cur, p, tl, r, c, pre_v, stage, sbuf, &tmC, &tmC2, lane);
         }
       }
       if (++acc == 2) {
@@ -959,7 +977,7 @@ extern "C" int pp_grouped_gemm(int32_t mode, const void* a, const void* b, void*
       if ((rc = make_tmap(&ta, a, dm, R, BK, BM)) || (rc = make_tmap(&tb, b, dm, (uint64_t)S * df, BK, bkb))) return rc;
       p.N = df; p.K_fixed = dm;
       if ((rc = make_out_tmap(&tc, c, df, R)) || (rc = make_out_tmap(&tc2, c2, df, R))) return rc;
-      return PP_LAUNCH(EPI_GELU, false, false, 4, 6, &tc, &tc2);
+      return PP_LAUNCH(EPI_GELU, false, false, 4, 5, &tc, &tc2);
     case PP_GEMM_FWD2:
       if ((rc = make_tmap(&ta, a, df, R, BK, BM)) || (rc = make_tmap(&tb, b, df, (uint64_t)S * dm, BK, bkb))) return rc;
       p.N = dm; p.K_fixed = df;
