@@ -284,7 +284,7 @@ def run_stack(args, cfg_name: str, cfg: dict, world: int, rank: int, dev, group)
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default=None)
@@ -299,6 +299,8 @@ def main() -> None:
     ap.add_argument("--placement", default="physical", choices=["virtual", "physical"],
                     help="planner over physical devices (E = m*D generalisation, 8(f) row 4; == the reference "
                          "search when E == D) or over E x E virtual expert slots (the reference search verbatim)")
+    ap.add_argument("--refine-slots", type=int, default=1,
+                    help="physical placement: slot-level refinement of the plan (1/0; beyond the paper)")
     ap.add_argument("--avg-bandwidth", type=float, default=None,
                     help="planner cost model B (bytes/s; default layer.default_specs' 450e9)")
     ap.add_argument("--trans-ctas", type=int, default=None, help="SMs of the SM-engine Trans push")
@@ -361,7 +363,8 @@ def main() -> None:
         cl_, mo_ = default_specs(E, k, d, f, T * world, avg_bandwidth=args.avg_bandwidth)
         specs = {"cluster": cl_, "model": mo_}
     layer = pp.MoELayer(d, f, E, k, tokens=T, group=group, planner=planner, seed=0, policy=args.policy, **specs,
-                        planning=planning, placement=args.placement if world > 1 else "virtual")
+                        planning=planning, placement=args.placement if world > 1 else "virtual",
+                        refine_slots=bool(args.refine_slots) and args.placement == "physical" and world > 1)
     if args.trans_ctas:
         layer.trans_ctas = args.trans_ctas
     if args.agg_ctas:
@@ -641,7 +644,8 @@ def main() -> None:
                        "routing": "Zipf(1.2) gate bias, random bf16 tokens", "policy": args.policy,
                        "planner": {"n": args.n_excl, "alpha": args.alpha, "reuse_interval": 1,
                                    "avg_bandwidth": layer.cluster.avg_bandwidth,
-                                   "placement": layer.placement, "planning": layer.planning,
+                                   "placement": layer.placement, "refine_slots": layer.refine_slots,
+                                   "planning": layer.planning,
                                    "replica_engine": layer.replica_engine}},
             "host_enqueue_ms_per_step": host_ms, "phase_ms_rank0": phases,
             "side_stream_ms_rank0": side_ms, "replica_traffic": replica_traffic,

@@ -85,9 +85,15 @@ int pp_plan_greedy(const int64_t* counts, int32_t num_layers, int32_t E,
  * per device, summed on load).  Outputs: selected [L][E], num_selected [L],
  * num_explored [L], mask [L][rows][E] (each device's row repeated over its slot
  * rows, so the layout consumes it as a slot mask), H/R [L][D], best_cost [L].
- * cm->num_devices must be D and cm->num_experts E; D*E <= 4096. */
+ * cm->num_devices must be D and cm->num_experts E; D*E <= 4096.
+ * refine_slots (needs rows/D > 1 slot rows per device; an extension beyond the
+ * paper): afterwards the heaviest device repeatedly sends one of its replica
+ * slot batches back to the expert's home when that lowers the pair's maximum
+ * (ties: lower slot, lower expert); the mask then differs between a device's
+ * slot rows, H/R are recomputed, selected/best_cost describe the search. */
 int pp_plan_physical(const int64_t* counts, int32_t num_layers, int32_t rows, int32_t D, int32_t E,
-                     const pp_cost_model* cm, const pp_planner_cfg* cfg, int32_t* selected,
+                     const pp_cost_model* cm, const pp_planner_cfg* cfg, int32_t refine_slots,
+                     int32_t* selected,
                      int32_t* num_selected, int32_t* num_explored, uint8_t* mask, int64_t* H,
                      int64_t* R, double* best_cost, void* stream);
 

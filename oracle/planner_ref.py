@@ -222,6 +222,52 @@ def greedy_search_physical(counts, n: int, alpha: float, overlap_aware: bool, cm
             "mask": mask, "H": Hf, "R": Rf}
 
 
+def refine_slots(slot_counts: np.ndarray, pmask: np.ndarray):
+    """Opt-in slot-level refinement of a physical plan (our extension, not in the paper):
+    a replica holder may keep sending some of its m token slots to the expert's home.
+    Repeatedly take the heaviest device h (first argmax of H); among its slots v that
+    compute a non-home expert e locally with C[v][e] > 0, un-route the one minimising
+    max(H[h] - C[v][e], H[home(e)] + C[v][e]) (ties: lower v, then lower e) if that is
+    below H[h]; stop when h cannot improve.  Returns the [E][E] slot mask and H, R."""
+    C = np.asarray(slot_counts, dtype=np.int64)
+    E = C.shape[0]
+    D = pmask.shape[0]
+    m = E // D
+    S = np.repeat(np.asarray(pmask, dtype=bool), m, axis=0)
+
+    def loads():
+        H = np.zeros(D, dtype=np.int64)
+        R = np.zeros(D, dtype=np.int64)
+        for v in range(E):
+            for e in range(E):
+                c = int(C[v, e])
+                if S[v, e]:
+                    H[v // m] += c
+                else:
+                    H[e // m] += c
+                    R[e // m] += c
+        return H, R
+
+    H, R = loads()
+    for _ in range(E * E):
+        h = int(np.argmax(H))
+        best = None
+        for v in range(h * m, (h + 1) * m):
+            for e in range(E):
+                c = int(C[v, e])
+                if not S[v, e] or e // m == h or c == 0:
+                    continue
+                val = max(int(H[h]) - c, int(H[e // m]) + c)
+                if val < H[h] and (best is None or val < best[0]):
+                    best = (val, v, e)
+        if best is None:
+            break
+        _, v, e = best
+        S[v, e] = False
+        H, R = loads()
+    return S, H, R
+
+
 def top_m_mask(counts: np.ndarray, m: int) -> np.ndarray:
     """reference simulator._top_m_placement (simulator.py:318-324): the m experts
     with the largest column totals (ties -> lower index) on every device."""

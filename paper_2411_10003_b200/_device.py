@@ -73,14 +73,16 @@ class PlanBuffers:
         self.best = torch.empty((L,), dtype=torch.float64, device=device)
 
 
-def launch_plan(counts_dev: torch.Tensor, out: PlanBuffers, cm, cfg, stream=None, physical_devices: int = 0) -> None:
+def launch_plan(counts_dev: torch.Tensor, out: PlanBuffers, cm, cfg, stream=None, physical_devices: int = 0,
+                refine_slots: bool = False) -> None:
     """physical_devices = D > 0: the physically-faithful search (pp_plan_physical) over
-    D devices; counts_dev rows may be D physical rows or virtual-slot rows."""
+    D devices; counts_dev rows may be D physical rows or virtual-slot rows (then
+    refine_slots may trim replica routing per slot)."""
     L, rows, E = counts_dev.shape
     if physical_devices:
         _lib.call(
             "pp_plan_physical", counts_dev.data_ptr(), L, rows, physical_devices, E, ctypes.byref(cm),
-            ctypes.byref(cfg), out.selected.data_ptr(), out.num_selected.data_ptr(), out.num_explored.data_ptr(),
+            ctypes.byref(cfg), 1 if refine_slots else 0, out.selected.data_ptr(), out.num_selected.data_ptr(), out.num_explored.data_ptr(),
             out.mask.data_ptr(), out.H.data_ptr(), out.R.data_ptr(), out.best.data_ptr(), stream_ptr(stream),
         )
         return

@@ -63,7 +63,7 @@ I = c_int32
 SIGNATURES = {
     "pp_version": [],
     "pp_plan_greedy": [P, I, I, POINTER(CostModel), POINTER(PlannerCfg), P, P, P, P, P, P, P, P],
-    "pp_plan_physical": [P, I, I, I, I, POINTER(CostModel), POINTER(PlannerCfg), P, P, P, P, P, P, P, P],
+    "pp_plan_physical": [P, I, I, I, I, POINTER(CostModel), POINTER(PlannerCfg), I, P, P, P, P, P, P, P, P],
     "pp_derive_loads": [P, P, I, I, P, P, P],
     "pp_top_m_mask": [P, I, I, I, P, P, P],
     "pp_route_topk": [P, P, P, I, I, I, I, P, P, P, P, P, P],

@@ -235,6 +235,7 @@ __global__ void __launch_bounds__(kMaxPlanThreads) plan_greedy_kernel(PlanArgs a
 struct PhysArgs {
   const int64_t* counts;
   int rows, D, E;
+  int refine;
   pp_cost_model cm;
   pp_planner_cfg cfg;
   int32_t* selected;
@@ -375,6 +376,55 @@ __global__ void __launch_bounds__(kMaxPlanThreads) plan_physical_kernel(PhysArgs
     a.num_explored[L] = s;
     a.best_cost[L] = best;
   }
+  if (!a.refine || rpd < 2) return;
+  // Opt-in slot refinement (not in the paper; oracle refine_slots): the heaviest device h
+  // un-routes the (slot v of h, non-home expert e) batch that minimises
+  // max(H[h] - C[v][e], H[home e] + C[v][e]) while that is below H[h]; ties -> lower v, e.
+  // Works on the emitted slot mask in global memory.
+  int64_t* Hs = sent;  // [D] device loads of the current slot mask (E >= D)
+  const int rows = a.rows;
+  auto slot_loads = [&](int64_t& hh, int64_t& rr) {
+    __syncthreads();
+    hh = 0;
+    rr = 0;
+    if (t < D) {
+      for (int v = t * rpd; v < (t + 1) * rpd; ++v)
+        for (int e = 0; e < E; ++e)
+          if (mask[(size_t)v * E + e]) hh += counts[(size_t)v * E + e];
+      for (int e = t * m; e < (t + 1) * m; ++e)
+        for (int v = 0; v < rows; ++v)
+          if (!mask[(size_t)v * E + e]) rr += counts[(size_t)v * E + e];
+      hh += rr;
+      Hs[t] = hh;
+    }
+    __syncthreads();
+  };
+  for (int iter = 0; iter < rows * E; ++iter) {
+    int64_t hh, rr;
+    slot_loads(hh, rr);
+    const Red hm = block_reduce(t < D ? Red{hh, t} : neutral_max, MaxFirst(), scratch);
+    const int hd = hm.i;
+    Red cand{INT64_MAX, 0x7fffffff};
+    for (int x = t; x < rpd * E; x += blockDim.x) {
+      const int v = hd * rpd + x / E, e = x - (x / E) * E;
+      const int64_t c = counts[(size_t)v * E + e];
+      if (!mask[(size_t)v * E + e] || e / m == hd || c == 0) continue;
+      const int64_t lo = hm.v - c, hi = Hs[e / m] + c;
+      const int64_t val = lo > hi ? lo : hi;
+      if (val >= hm.v) continue;
+      const int64_t key = (val << 20) | (int64_t)(v * E + e);
+      if (key < cand.v) cand.v = key;
+    }
+    cand = block_reduce(cand, MinOp(), scratch);
+    if (cand.v == INT64_MAX) break;
+    if (t == 0) mask[cand.v & ((1 << 20) - 1)] = 0;
+  }
+  int64_t hh, rr;
+  slot_loads(hh, rr);
+  if (t < D) {
+    a.H[(size_t)L * D + t] = hh;
+    a.R[(size_t)L * D + t] = rr;
+  }
 }
 
 __global__ void derive_loads_kernel(const int64_t* counts, const uint8_t* mask, int D, int E,
@@ -451,7 +501,7 @@ extern "C" int pp_plan_greedy(const int64_t* counts, int32_t num_layers, int32_t
 
 extern "C" int pp_plan_physical(const int64_t* counts, int32_t num_layers, int32_t rows, int32_t D,
                                 int32_t E, const pp_cost_model* cm, const pp_planner_cfg* cfg,
-                                int32_t* selected, int32_t* num_selected, int32_t* num_explored,
+                                int32_t refine_slots, int32_t* selected, int32_t* num_selected, int32_t* num_explored,
                                 uint8_t* mask, int64_t* H, int64_t* R, double* best_cost,
                                 void* stream) {
   PP_CHECK_ARG(counts && cm && cfg && selected && num_selected && num_explored && mask && H && R &&
@@ -467,7 +517,10 @@ extern "C" int pp_plan_physical(const int64_t* counts, int32_t num_layers, int32
                 cm->num_experts, D, E);
   PP_CHECK_ARG(cfg->n >= 0 && cfg->n < D, "n must be < num_devices=%d, got %d", D, cfg->n);
   PP_CHECK_ARG(cm->top_k >= 1, "top_k must be >= 1");
-  PhysArgs a{counts, rows, D, E, *cm, *cfg, selected, num_selected, num_explored, mask, H, R, best_cost};
+  PP_CHECK_ARG(!refine_slots || (int64_t)rows * E <= (1 << 20),
+               "pp_plan_physical: slot refinement needs rows*E <= 2^20");
+  PhysArgs a{counts, rows, D, E, refine_slots ? 1 : 0, *cm, *cfg, selected, num_selected, num_explored,
+             mask, H, R, best_cost};
   const int threads = ((E + 31) / 32) * 32;
   const size_t smem = sizeof(int64_t) * ((size_t)D * E + E) + (size_t)D * E + E;
   plan_physical_kernel<<<num_layers, threads, smem, as_stream(stream)>>>(a);

@@ -160,7 +160,8 @@ class MoELayer(torch.nn.Module):
                  group=None, planner: PlannerConfig | None = None, cluster=None, model=None,
                  capacity_rows: int | None = None, max_replicas: int | None = None,
                  seed: int = 0, device=None, trans_ctas: int = 32, replica_engine: str = "copy",
-                 policy: str | None = None, planning: str = "host", placement: str = "virtual") -> None:
+                 policy: str | None = None, planning: str = "host", placement: str = "virtual",
+                 refine_slots: bool = False) -> None:
         super().__init__()
         if not torch.cuda.is_available():
             raise RuntimeError("MoELayer needs a CUDA device (B200); there is no CPU path")
@@ -253,6 +254,12 @@ class MoELayer(torch.nn.Module):
         if placement not in ("virtual", "physical"):
             raise ValidationError(f"placement must be 'virtual' or 'physical', got {placement!r}")
         self.placement = placement
+        # opt-in (physical placement only; beyond the paper): a replica holder may keep
+        # sending some of its token slots to the expert's home when that lowers the
+        # heaviest device's rows (pp_plan_physical refine_slots, oracle refine_slots)
+        if refine_slots and placement != "physical":
+            raise ValidationError("refine_slots needs placement='physical'")
+        self.refine_slots = bool(refine_slots) and self.m > 1
         self._cm = _device.cost_model(self.cluster, self.model, E) if self.plan_enabled else None
         if self._cm is not None and placement == "physical":
             if self.planner_cfg.n >= D:
@@ -402,7 +409,8 @@ class MoELayer(torch.nn.Module):
                 self.plan_stream.wait_event(ev)
                 p0 = self._side_event(self.plan_stream)
                 _device.launch_plan(self._counts_snap.view(1, self.E, self.E), self._plan_out, self._cm,
-                                    self._pcfg, self.plan_stream, physical_devices=self._phys_devices())
+                                    self._pcfg, self.plan_stream, physical_devices=self._phys_devices(),
+                                    refine_slots=self.refine_slots)
                 self._log_side("Plan", p0, self._side_event(self.plan_stream))
                 self._plan_done_dev = torch.cuda.Event()
                 self._plan_done_dev.record(self.plan_stream)
@@ -415,13 +423,17 @@ class MoELayer(torch.nn.Module):
             snapshot.record_stream(self.plan_stream)
             p0 = self._side_event(self.plan_stream)
             _device.launch_plan(snapshot.view(1, self.E, self.E), self._plan_out, self._cm, self._pcfg,
-                                self.plan_stream, physical_devices=self._phys_devices())
+                                self.plan_stream, physical_devices=self._phys_devices(),
+                                refine_slots=self.refine_slots)
             self._log_side("Plan", p0, self._side_event(self.plan_stream))
             mask_dev = self._plan_out.mask[0].clone()
             self._mask_host.copy_(mask_dev, non_blocking=True)
             done = torch.cuda.Event()
             done.record(self.plan_stream)
         self._plan_pending = (done, mask_dev)
+
+    def _plan_inflight(self) -> bool:
+        return self.planning == "device" and self._plan_done_dev is not None or self._plan_pending is not None
 
     def _phys_devices(self) -> int:
         return self.world if self.placement == "physical" else 0
@@ -655,8 +667,13 @@ class MoELayer(torch.nn.Module):
         self._mark("trans_wait")
         self.barrier()  # every rank's rows have landed (and replicas' params, via the next barrier use)
         self._mark("barrier1")
-        self._gemm(_lib.PP_GEMM_FWD1, self.xp.local, self.w1_arena.local, self.pre, self.act)
-        self._gemm(_lib.PP_GEMM_FWD2, self.act, self.w2_arena.local, self.yp.local)
+        # a planner launched this iteration may still occupy an SM: the forward GEMMs leave
+        # one CTA pair's SMs free so their static persistent walk never waits on it
+        fwd_sms = None
+        if self._plan_inflight():
+            fwd_sms = max(2, (self.gemm_sms or _device.num_sms(self.device)) - 2)
+        self._gemm(_lib.PP_GEMM_FWD1, self.xp.local, self.w1_arena.local, self.pre, self.act, num_sms=fwd_sms)
+        self._gemm(_lib.PP_GEMM_FWD2, self.act, self.w2_arena.local, self.yp.local, num_sms=fwd_sms)
         self._mark("fwd_gemms")
         self.barrier()
         self._mark("barrier2")

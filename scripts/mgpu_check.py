@@ -40,7 +40,7 @@ def main():
     n_excl = int(os.environ.get("PP_N", "1" if placement == "virtual" else "0"))
     layer = pp.MoELayer(d, f, E, k, tokens=T, group=dist.group.WORLD,
                         planner=pp.PlannerConfig(n=n_excl, alpha=0.5), cluster=cl, model=mo, seed=0,
-                        placement=placement,
+                        placement=placement, refine_slots=os.environ.get("PP_REFINE") == "1",
                         replica_engine=os.environ.get("PP_ENGINE", "copy"),
                         policy=os.environ.get("PP_POLICY") or None,
                         planning=os.environ.get("PP_PLANNING", "host"))
@@ -87,7 +87,10 @@ def main():
                     cm = P.cost_model_dict(world, k, 2 * d, 1e3, 1e3, 1e11, 1e6)
                     phys = prev_counts.reshape(world, m, E).sum(axis=1)
                     exp = P.greedy_search_physical(phys, n_excl, 0.5, False, cm)
-                    exp["mask"] = np.repeat(exp["mask"], m, axis=0)
+                    if os.environ.get("PP_REFINE") == "1":
+                        exp["mask"] = P.refine_slots(prev_counts, exp["mask"])[0]
+                    else:
+                        exp["mask"] = np.repeat(exp["mask"], m, axis=0)
                 else:
                     cm = P.cost_model_dict(E, k, 2 * d, 1e3, 1e3, 1e11, 1e6)
                     exp = P.greedy_search(prev_counts, n_excl, 0.5, False, cm)

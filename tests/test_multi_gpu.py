@@ -25,10 +25,13 @@ def _ngpus():
 @pytest.mark.skipif(_ngpus() < 2, reason="needs >= 2 GPUs")
 @pytest.mark.parametrize("planning,engine,policy,placement", [
     ("host", "copy", "", "virtual"), ("device", "sm", "", "virtual"), ("host", "sm", "top2", "virtual"),
-    ("host", "copy", "vanilla", "virtual"), ("device", "sm", "", "physical"), ("host", "copy", "", "physical")])
+    ("host", "copy", "vanilla", "virtual"), ("device", "sm", "", "physical"), ("host", "copy", "", "physical"),
+    ("device", "sm", "", "physical+refine")])
 def test_ep_layer_parity(planning, engine, policy, placement):
     n = min(_ngpus(), 4)
-    env = dict(os.environ, PP_PLANNING=planning, PP_ENGINE=engine, PP_POLICY=policy, PP_PLACEMENT=placement)
+    refine = placement.endswith("+refine")
+    env = dict(os.environ, PP_PLANNING=planning, PP_ENGINE=engine, PP_POLICY=policy,
+               PP_PLACEMENT=placement.split("+")[0], PP_REFINE="1" if refine else "0")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--standalone", "--nproc-per-node", str(n),
            str(ROOT / "scripts" / "mgpu_check.py")]
     r = subprocess.run(cmd, env=env, cwd=ROOT, capture_output=True, text=True, timeout=600)

@@ -156,3 +156,25 @@ def test_physical_derive_loads_rules(rng):
         assert res["best"] <= P.objective(H0, R0, 0, 0, cm, bool(i % 2))  # strict improvements only
         assert res["H"].sum() == counts.sum()
         assert all(e // m != d or res["mask"][d, e] for d in range(D) for e in range(E))
+
+
+def test_slot_refinement_properties(rng):
+    """refine_slots (opt-in extension): conserves rows, keeps every home slot local,
+    only un-routes replica slots, and never raises the heaviest device."""
+    for i in range(30):
+        D = int(rng.integers(2, 6))
+        m = int(rng.integers(2, 5))
+        E = D * m
+        p = rng.dirichlet(np.ones(E) * 0.3)
+        slot = np.stack([rng.multinomial(128, p) for _ in range(E)]).astype(np.int64)
+        phys = slot.reshape(D, m, E).sum(axis=1)
+        cm = P.cost_model_dict(D, 2, 2048, 1.6e7, 3.2e7, 4e11, 1e8)
+        plan = P.greedy_search_physical(phys, 0, 0.5, bool(i % 2), cm)
+        S, H, R = P.refine_slots(slot, plan["mask"])
+        full = np.repeat(plan["mask"], m, axis=0)
+        assert H.sum() == slot.sum() and H.max() <= plan["H"].max()
+        assert not (S & ~full).any()  # only removals
+        for v in range(E):
+            for e in range(E):
+                if e // m == v // m:
+                    assert S[v, e] == full[v, e]  # home slots untouched

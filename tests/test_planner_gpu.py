@@ -188,3 +188,35 @@ def test_physical_planner_slot_rows_input():
     assert out.H[0, :D].cpu().tolist() == exp["H"].tolist()
     with pytest.raises(pp.ValidationError):
         pp.greedy_search_physical(pp.LoadMatrix(phys[:, :E - 1]), pp.PlannerConfig(), cl, mo)
+
+
+@pytest.mark.parametrize("D,m", [(2, 8), (4, 4), (8, 2), (4, 8)])
+def test_physical_planner_slot_refinement_vs_oracle(D, m):
+    """refine_slots (beyond the paper): the device's slot mask and H/R equal the oracle's
+    refine_slots applied to the oracle's physical plan, and never raise the heaviest device."""
+    import torch
+
+    from paper_2411_10003_b200 import _device
+
+    E = D * m
+    rng = np.random.default_rng(900 + D * 10 + m)
+    for i in range(25):
+        p = rng.dirichlet(np.ones(E) * (0.15 + 0.2 * (i % 3)))
+        slot = np.stack([rng.multinomial(256 * 2, p) for _ in range(E)]).astype(np.int64)
+        phys = slot.reshape(D, m, E).sum(axis=1)
+        n = i % D
+        ov = bool(i % 2)
+        cm = P.cost_model_dict(D, 2, 2048, 1.6e7, 3.2e7, 4e11 / (1 + i % 3), 1e8)
+        exp = P.greedy_search_physical(phys, n, 0.5, ov, cm)
+        S, H, R = P.refine_slots(slot, exp["mask"])
+        assert H.max() <= exp["H"].max()
+        cl = pp.ClusterSpec(D, cm["avg_bandwidth"], cm["compute_throughput"])
+        mo = pp.ModelSpec(E, 1, 2, cm["input_bytes"], cm["expert_param_bytes"], cm["expert_grad_bytes"])
+        out = _device.PlanBuffers(1, E, torch.device("cuda", 0))
+        _device.launch_plan(torch.from_numpy(slot).cuda().view(1, E, E), out, _device.cost_model(cl, mo),
+                            _device.planner_cfg(pp.PlannerConfig(n=n, alpha=0.5, overlap_aware=ov)),
+                            physical_devices=D, refine_slots=True)
+        torch.cuda.synchronize()
+        assert out.mask[0].cpu().numpy().astype(bool).tolist() == S.tolist(), i
+        assert out.H[0, :D].cpu().tolist() == H.tolist() and out.R[0, :D].cpu().tolist() == R.tolist()
+        assert out.selected[0, : int(out.num_selected[0])].cpu().tolist() == list(exp["selected"])
