@@ -36,6 +36,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 
 import numpy as np
 import torch
@@ -269,6 +270,8 @@ class MoELayer(torch.nn.Module):
         self.plan_stream = torch.cuda.Stream(device=dev) if self.plan_enabled else None
         self.comm_stream = torch.cuda.Stream(device=dev) if D > 1 else None
         self.trans_ctas = trans_ctas  # SM-engine Trans (overlaps route/layout/dispatch)
+        # where the forward issues Trans: "start" (before the gate GEMM) or "after_route"
+        self.trans_point = os.environ.get("PPMOE_TRANS_POINT", "start")
         # SM-engine Agg runs beside the backward GEMMs on agg_ctas SMs (one CTA per SM);
         # those GEMMs launch their persistent grids on the remaining SMs so neither waits
         # for the other (pushes reach NVLink rate from ~16 CTAs)
@@ -374,10 +377,14 @@ class MoELayer(torch.nn.Module):
         _lib.call("pp_route_topk", x.data_ptr(), self.wg.data_ptr(), self.gate_bias.data_ptr(), T, d,
                   E, k, self.idx.data_ptr(), self.w.data_ptr(), self.probs.data_ptr(),
                   self.rank_in_chunk.data_ptr(), self.chunk_counts.data_ptr(), sp)
+        if self.trans_point == "after_route" and not self.top_m:
+            self.issue_trans()  # overlaps histogram, barrier, layout and dispatch, not the gate GEMM
         if self.world > 1:
             _lib.call("pp_slot_histogram", self.chunk_counts.data_ptr(), T, E, m, self.counts_buf.ptrs.data_ptr(),
                       self.world, self.rank * m, sp)
+            self._mark("route_hist")
             self.barrier()  # every rank's rows of the LoadMatrix have landed
+            self._mark("hist_barrier")
         if self.top_m and self.world > 1:
             _lib.call("pp_top_m_mask", self.counts.data_ptr(), E, E, self.top_m, self._topm_mask.data_ptr(),
                       None, sp)
@@ -647,13 +654,14 @@ class MoELayer(torch.nn.Module):
         self.begin_iteration()
         if self.planning == "device" and self.world > 1:
             self._trans_issued = False  # the device-side plan may change every iteration
-        if not self.top_m:  # the plan is known before routing: Trans overlaps route/layout/dispatch
+        trans_done = None
+        if not self.top_m and self.trans_point == "start":  # plan known before routing
             trans_done = self.issue_trans()  # no-op if a scheduler already issued it earlier
-        else:
+        elif self.top_m:
             self._trans_issued = False  # top-m: this iteration's mask exists only after the histogram
         self._route_and_layout(x)
-        if self.top_m:
-            trans_done = self.issue_trans()
+        if self.top_m or self.trans_point == "after_route":
+            trans_done = self.issue_trans() if trans_done is None else trans_done
         self._mark("route_layout")
         self._launch_planner()  # [A2A | Plan(j+1)]: the search overlaps this block's dispatch
         _lib.call("pp_dispatch", x.data_ptr(), self.idx.data_ptr(), self.rank_in_chunk.data_ptr(),

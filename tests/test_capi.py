@@ -55,3 +55,37 @@ def test_validation_before_any_device_work():
     rc = lib.pp_grouped_gemm(99, z, z, z, z, z, z, 1, 128, 1, 256, 256, 0, None)
     assert rc == _lib.PP_EINVAL
     assert b"unknown mode" in lib.pp_last_error()
+
+
+def test_new_entry_points_validate_before_device_work():
+    """pp_plan_physical / pp_replica_* / pp_dot_bf16 reject bad shapes with the reference
+    exception types, without touching (fake) device pointers."""
+    lib = _lib.load()
+    z = ctypes.c_void_p(8)
+    cm, cfg = _lib.CostModel(), _lib.PlannerCfg()
+    cm.top_k = 2
+    cm.num_devices, cm.num_experts = 4, 16
+    cfg.n = 0
+    # E not a multiple of D
+    rc = lib.pp_plan_physical(z, 1, 4, 4, 15, ctypes.byref(cm), ctypes.byref(cfg), 0, z, z, z, z, z, z, z, None)
+    assert rc == _lib.PP_EINVAL
+    # cost model dims disagree with the load
+    cm.num_devices = 8
+    rc = lib.pp_plan_physical(z, 1, 4, 4, 16, ctypes.byref(cm), ctypes.byref(cfg), 0, z, z, z, z, z, z, z, None)
+    assert rc == _lib.PP_EDIM
+    cm.num_devices = 4
+    cfg.n = 4  # n must be < D
+    rc = lib.pp_plan_physical(z, 1, 4, 4, 16, ctypes.byref(cm), ctypes.byref(cfg), 0, z, z, z, z, z, z, z, None)
+    assert rc == _lib.PP_EINVAL
+    cfg.n = 0
+    rc = lib.pp_plan_physical(z, 1, 6, 4, 16, ctypes.byref(cm), ctypes.byref(cfg), 0, z, z, z, z, z, z, z, None)
+    assert rc == _lib.PP_EINVAL  # rows not a multiple of D
+    # replica kernels: rank out of range, bad parts
+    assert lib.pp_replica_trans(z, z, z, 16, 4, 4, 256, 256, 0, None) == _lib.PP_EINVAL
+    assert lib.pp_replica_agg(z, z, z, z, 16, 4, 0, 256, 256, 4, 0, None) == _lib.PP_EINVAL
+    assert lib.pp_replica_agg_reduce(z, z, z, z, 16, 4, 0, 256, 256, 0, 0, None) == _lib.PP_EINVAL
+    assert lib.pp_replica_agg(None, z, z, z, 16, 4, 0, 256, 256, 3, 0, None) == _lib.PP_EINVAL
+    # probe loss: n must be a multiple of 8, operands 16-byte aligned
+    assert lib.pp_dot_bf16(z, z, 12, z, z, None) == _lib.PP_EINVAL
+    assert lib.pp_dot_bf16(ctypes.c_void_p(24), z, 16, z, z, None) == _lib.PP_EINVAL
+    assert b"aligned" in lib.pp_last_error()
