@@ -301,6 +301,8 @@ def main() -> None:
                          "search when E == D) or over E x E virtual expert slots (the reference search verbatim)")
     ap.add_argument("--refine-slots", type=int, default=1,
                     help="physical placement: slot-level refinement of the plan (1/0; beyond the paper)")
+    ap.add_argument("--fused-a2a", type=int, default=1,
+                    help="N > 1: combine / dispatch-backward fused into the FWD2 / DGRAD1 epilogues (1/0)")
     ap.add_argument("--avg-bandwidth", type=float, default=None,
                     help="planner cost model B (bytes/s; default layer.default_specs' 450e9)")
     ap.add_argument("--trans-ctas", type=int, default=None, help="SMs of the SM-engine Trans push")
@@ -364,7 +366,8 @@ def main() -> None:
         specs = {"cluster": cl_, "model": mo_}
     layer = pp.MoELayer(d, f, E, k, tokens=T, group=group, planner=planner, seed=0, policy=args.policy, **specs,
                         planning=planning, placement=args.placement if world > 1 else "virtual",
-                        refine_slots=bool(args.refine_slots) and args.placement == "physical" and world > 1)
+                        refine_slots=bool(args.refine_slots) and args.placement == "physical" and world > 1,
+                        fused_a2a=bool(args.fused_a2a) and world > 1)
     if args.trans_ctas:
         layer.trans_ctas = args.trans_ctas
     if args.agg_ctas:
@@ -645,6 +648,7 @@ def main() -> None:
                        "planner": {"n": args.n_excl, "alpha": args.alpha, "reuse_interval": 1,
                                    "avg_bandwidth": layer.cluster.avg_bandwidth,
                                    "placement": layer.placement, "refine_slots": layer.refine_slots,
+                                   "fused_a2a": layer.fused_a2a,
                                    "planning": layer.planning,
                                    "replica_engine": layer.replica_engine}},
             "host_enqueue_ms_per_step": host_ms, "phase_ms_rank0": phases,

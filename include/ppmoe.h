@@ -172,28 +172,35 @@ int pp_dispatch(const void* x, const int32_t* idx, const int32_t* rank,
                 int32_t T, int32_t d, int32_t k, int32_t m, int32_t E,
                 void* const* recv_ptrs, void* own_recv,
                 const pp_group* groups, const int32_t* num_groups, int32_t max_groups,
-                int32_t* pair_dest, int32_t* pair_row, void* stream);
+                int32_t* pair_dest, int32_t* pair_row, void* const* origin_ptrs,
+                int32_t my_rank, void* stream);
 
-/* y[t] = sum_j w[t][j] * out_ptrs[pair_dest][pair_row] (fp32 accumulate, bf16 out). */
+/* y[t] = sum_j w[t][j] * out_ptrs[pair_dest][pair_row] (fp32 accumulate, bf16 out).
+ * Fused-A2A mode (comb != NULL, out_ptrs may be NULL): the expert outputs were
+ * already pushed to this rank by pp_grouped_gemm_scatter as comb [T*k][d] bf16 in
+ * pair order (t*k + j), so the gather is local. */
 int pp_combine(void* const* out_ptrs, const int32_t* pair_dest, const int32_t* pair_row,
-               const float* w, int32_t T, int32_t d, int32_t k, void* y, void* stream);
+               const float* w, int32_t T, int32_t d, int32_t k, void* y, const void* comb,
+               void* stream);
 
 /* Backward of combine: dw[t][j] = <dy[t], Yp[pair]> ; dYp[pair] = w[t][j]*dy[t]
- * (pushed to dgrad_ptrs[pair_dest]); zero-fills own padding rows of own_dgrad. */
+ * (pushed to dgrad_ptrs[pair_dest]); zero-fills own padding rows of own_dgrad.
+ * comb != NULL: Yp[pair] is read locally from comb[t*k + j] (fused-A2A mode). */
 int pp_combine_bwd(const void* dy, void* const* out_ptrs, void* const* dgrad_ptrs, void* own_dgrad,
                    const int32_t* pair_dest, const int32_t* pair_row, const float* w,
                    const pp_group* groups, const int32_t* num_groups, int32_t max_groups,
-                   int32_t T, int32_t d, int32_t k, float* dw, void* stream);
+                   int32_t T, int32_t d, int32_t k, float* dw, const void* comb, void* stream);
 
 /* Backward of dispatch + gate softmax:  dx[t] = sum_j dXp[pair] (pulled from
  * dxp_ptrs[pair_dest]) and dl [T][EP] bf16 = dL/dlogits restricted to the top-k
  * (dl_i = p_i * (dw_{j(i)} [i selected] - sum_j dw_j p_{e_j})), zero-padded to
- * EP in {64, 128} columns for the tensor-core gate GEMMs.  Also zeroes
+ * EP in {64, 128} columns for the tensor-core gate GEMMs.  comb != NULL: the
+ * dXp rows were pushed here by the DGRAD1 epilogue, comb[t*k + j] (local).  Also zeroes
  * zero_f32[0:zero_elems) (the gate weight grad the split-K GEMM accumulates into). */
 int pp_dispatch_bwd(void* const* dxp_ptrs, const int32_t* pair_dest, const int32_t* pair_row,
                     const int32_t* idx, const float* probs, const float* dw,
                     int32_t T, int32_t d, int32_t k, int32_t E, int32_t EP, void* dx, void* dl,
-                    float* zero_f32, int64_t zero_elems, void* stream);
+                    float* zero_f32, int64_t zero_elems, const void* comb, void* stream);
 
 /* Gate GEMMs on tcgen05:  dx [T][d] bf16 += dl [T][EP] . wg [E][d]   and
  * dwg [E][d] fp32 += dl^T . x (split-K over token chunks, fp32 atomics;
@@ -227,6 +234,19 @@ int pp_grouped_gemm(int32_t mode, const void* a, const void* b, void* c, void* c
  * that feeds g as the upstream gradient reads back one scalar per step. */
 #define PP_DOT_PARTIALS 592
 int pp_dot_bf16(const void* a, const void* b, int64_t n, float* partial, float* out, void* stream);
+
+/* Fused GEMM + all-to-all (FWD2 -> combine, DGRAD1 -> dispatch backward):
+ * same GEMM as pp_grouped_gemm(mode), but the epilogue stores output row r of
+ * the receive layout straight into the rank that owns the pair, over NVLink:
+ * row (o % pairs_per_rank) of scatter_ptrs[o / pairs_per_rank] ([T*k][d] bf16),
+ * o = origin[r] as written by pp_dispatch (origin_ptrs; padding rows -1, not
+ * stored).  The transfer overlaps the remaining tiles' MMAs; pp_combine /
+ * pp_dispatch_bwd then read comb locally.  mode: PP_GEMM_FWD2 or PP_GEMM_DGRAD1. */
+int pp_grouped_gemm_scatter(int32_t mode, const void* a, const void* b, const pp_group* groups,
+                            const int32_t* num_groups, int32_t max_groups, int32_t rows_capacity,
+                            int32_t num_slots, int32_t d_model, int32_t d_ff, const int32_t* origin,
+                            void* const* scatter_ptrs, int32_t pairs_per_rank, int32_t num_sms,
+                            void* stream);
 
 /* ---- replica Trans / Agg over peer memory (K5) --------------------------- */
 /* Trans (home side, SM engine): push each of this rank's home experts' W1/W2

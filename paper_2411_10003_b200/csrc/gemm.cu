@@ -84,6 +84,13 @@ struct GemmParams {
   int m_real;       // EPI_F32_ATOMIC: rows of the output that exist (< M_fixed)
   unsigned long long* dbg;  // optional per-CTA wait-cycle counters (PPMOE_GEMM_DEBUG)
   int dbg_noload;           // diagnostic: skip operand TMA (MMA + epilogue only)
+  // fused combine / dispatch-backward (EPI_BF16 only): output row r goes to pair
+  // origin[r] = src_rank * pairs_per_rank + t*k + j, i.e. row (t*k+j) of scatter_ptrs[src_rank]
+  // (peer memory over NVLink), instead of this rank's receive-layout buffer; origin < 0
+  // marks padding rows (not stored)
+  const int32_t* origin;
+  void* const* scatter_ptrs;
+  int scatter_tk;
 };
 
 struct SchedSmem {
@@ -226,7 +233,24 @@ __device__ __forceinline__ void epilogue_chunk(const uint32_t (&raw)[32], const 
         for (int u = 0; u < 8; ++u) f[u] = __uint_as_float(raw[8 * j + u]);
         v[j] = f32x8_to_bf16(f);
       }
-      stage_and_store<NB - 1>(next_buf(), v, tmC, col, row, lane);
+      if (p.origin) {
+        // fused A2A: this thread's 64 B of row r go to the pair's owner as one bulk copy
+        // (TMA engine, smem -> local or peer global), so the LSUs stay with the epilogue
+        const int o = p.origin[tl.row_off + tl.m0 + r];
+        uint8_t* buf = next_buf() + lane * 64;
+        bulk_wait_read<NB - 1>();  // this lane's previous copy out of the slot has read it
+#pragma unroll
+        for (int j = 0; j < 4; ++j) *reinterpret_cast<uint4*>(buf + 16 * j) = v[j];
+        fence_async_shared();
+        if (o >= 0) {
+          const int src = o / p.scatter_tk;
+          bulk_store_s2g(reinterpret_cast<__nv_bfloat16*>(p.scatter_ptrs[src]) +
+                             (size_t)(o - src * p.scatter_tk) * p.N + col, buf, 64);
+        }
+        bulk_commit();
+      } else {
+        stage_and_store<NB - 1>(next_buf(), v, tmC, col, row, lane);
+      }
     } else if constexpr (EPI == EPI_GELU) {
       uint4 g4[4];
 #pragma unroll
@@ -705,7 +729,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 
   if constexpr (tma_out<EPI>()) {
-    if (warp >= 4 && lane == 0) bulk_wait0();
+    if (warp >= 4) bulk_wait0();  // every lane: scatter epilogues issue per-lane bulk copies
   }
   tc_fence_before();
   if constexpr (CG == 2) {
@@ -937,10 +961,45 @@ extern "C" int pp_gemm_debug_read(unsigned long long* host, int32_t ctas) {
   return PP_OK;
 }
 
+struct ScatterArgs {
+  const int32_t* origin;
+  void* const* ptrs;
+  int tk;
+};
+
+static int grouped_gemm_impl(int32_t mode, const void* a, const void* b, void* c, void* c2,
+                             const pp_group* groups, const int32_t* num_groups, int32_t max_groups,
+                             int32_t rows_capacity, int32_t num_slots, int32_t d_model,
+                             int32_t d_ff, int32_t num_sms, void* stream, const ScatterArgs* sc);
+
 extern "C" int pp_grouped_gemm(int32_t mode, const void* a, const void* b, void* c, void* c2,
                                const pp_group* groups, const int32_t* num_groups,
                                int32_t max_groups, int32_t rows_capacity, int32_t num_slots,
                                int32_t d_model, int32_t d_ff, int32_t num_sms, void* stream) {
+  PP_CHECK_ARG(c, "pp_grouped_gemm: null pointer");
+  return grouped_gemm_impl(mode, a, b, c, c2, groups, num_groups, max_groups, rows_capacity,
+                           num_slots, d_model, d_ff, num_sms, stream, nullptr);
+}
+
+extern "C" int pp_grouped_gemm_scatter(int32_t mode, const void* a, const void* b,
+                                       const pp_group* groups, const int32_t* num_groups,
+                                       int32_t max_groups, int32_t rows_capacity, int32_t num_slots,
+                                       int32_t d_model, int32_t d_ff, const int32_t* origin,
+                                       void* const* scatter_ptrs, int32_t pairs_per_rank,
+                                       int32_t num_sms, void* stream) {
+  PP_CHECK_ARG(mode == PP_GEMM_FWD2 || mode == PP_GEMM_DGRAD1,
+               "pp_grouped_gemm_scatter: only FWD2 (combine) and DGRAD1 (dispatch backward), got %d", mode);
+  PP_CHECK_ARG(origin && scatter_ptrs && pairs_per_rank > 0, "pp_grouped_gemm_scatter: bad scatter arguments");
+  ScatterArgs sc{origin, scatter_ptrs, pairs_per_rank};
+  // the unused output tensor map is built over the A operand (>= rows x d_model elements)
+  return grouped_gemm_impl(mode, a, b, const_cast<void*>(a), nullptr, groups, num_groups, max_groups,
+                           rows_capacity, num_slots, d_model, d_ff, num_sms, stream, &sc);
+}
+
+static int grouped_gemm_impl(int32_t mode, const void* a, const void* b, void* c, void* c2,
+                             const pp_group* groups, const int32_t* num_groups, int32_t max_groups,
+                             int32_t rows_capacity, int32_t num_slots, int32_t d_model,
+                             int32_t d_ff, int32_t num_sms, void* stream, const ScatterArgs* sc) {
   PP_CHECK_ARG(a && b && c && groups && num_groups, "pp_grouped_gemm: null pointer");
   PP_CHECK_ARG(max_groups >= 1 && max_groups <= kMaxGroups, "pp_grouped_gemm: max_groups=%d",
                max_groups);
@@ -963,6 +1022,11 @@ extern "C" int pp_grouped_gemm(int32_t mode, const void* a, const void* b, void*
   p.max_groups = max_groups;
   p.c = c;
   p.c2 = c2;
+  if (sc) {
+    p.origin = sc->origin;
+    p.scatter_ptrs = sc->ptrs;
+    p.scatter_tk = sc->tk;
+  }
   int rc = PP_OK;
   // CTA pairs (cta_group::2, 256 x 256 tiles, B split across the pair) unless
   // PPMOE_GEMM_CTA_PAIR=0; a pair stages 16 KB of A + 16 KB of B per CTA and stage

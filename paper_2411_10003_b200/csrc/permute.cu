@@ -164,7 +164,7 @@ __global__ void __launch_bounds__(kLayoutThreads)
 template <int VPL>
 __device__ __forceinline__ void zero_padding_rows(const pp_group* groups, const int32_t* num_groups,
                                                   int d, __nv_bfloat16* buf, int warp_global,
-                                                  int nwarps, int lane) {
+                                                  int nwarps, int lane, int32_t* origin = nullptr) {
   const int G = *num_groups;
   for (int w = warp_global; w < G * PP_ROW_ALIGN; w += nwarps) {
     const pp_group gr = groups[w / PP_ROW_ALIGN];
@@ -173,6 +173,7 @@ __device__ __forceinline__ void zero_padding_rows(const pp_group* groups, const 
     uint4* dst = reinterpret_cast<uint4*>(buf + (size_t)(gr.row_off + gr.rows + j) * d);
 #pragma unroll
     for (int i = 0; i < VPL; ++i) st_v4(dst + lane + 32 * i, make_uint4(0, 0, 0, 0));
+    if (origin && lane == 0) origin[gr.row_off + gr.rows + j] = -1;  // padding: no source pair
   }
 }
 
@@ -183,12 +184,14 @@ __global__ void __launch_bounds__(256)
                     const int32_t* __restrict__ rank, const int32_t* __restrict__ chunk_base,
                     const int32_t* __restrict__ slot_dest, int T, int d, int k, int m, int E,
                     void* const* recv_ptrs, int32_t* pair_dest, int32_t* pair_row,
-                    const pp_group* groups, const int32_t* num_groups, __nv_bfloat16* own) {
+                    const pp_group* groups, const int32_t* num_groups, __nv_bfloat16* own,
+                    void* const* origin_ptrs, int me) {
   const int lane = threadIdx.x & 31;
   const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
   const int slot_tokens = T / m;
-  zero_padding_rows<VPL>(groups, num_groups, d, own, warp_global, nwarps, lane);
+  zero_padding_rows<VPL>(groups, num_groups, d, own, warp_global, nwarps, lane,
+                         origin_ptrs ? reinterpret_cast<int32_t*>(origin_ptrs[me]) : nullptr);
   for (int t = warp_global; t < T; t += nwarps) {
     uint4 v[VPL];
     const uint4* src = reinterpret_cast<const uint4*>(x + (size_t)t * d);
@@ -210,6 +213,9 @@ __global__ void __launch_bounds__(256)
                                             (size_t)row * d);
 #pragma unroll
       for (int i = 0; i < VPL; ++i) st_v4(dst + lane + 32 * i, v[i]);
+      // fused A2A: the computing rank's GEMM epilogue sends this row's result straight back
+      if (origin_ptrs && lane == 0)
+        reinterpret_cast<int32_t*>(origin_ptrs[dest])[row] = me * T * k + t * k + j;
     }
   }
 }
@@ -220,7 +226,7 @@ template <int VPL>
 __global__ void __launch_bounds__(256)
     combine_kernel(void* const* out_ptrs, const int32_t* __restrict__ pair_dest,
                    const int32_t* __restrict__ pair_row, const float* __restrict__ w, int T, int d,
-                   int k, __nv_bfloat16* y) {
+                   int k, __nv_bfloat16* y, const __nv_bfloat16* __restrict__ comb) {
   const int lane = threadIdx.x & 31;
   const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -241,8 +247,10 @@ __global__ void __launch_bounds__(256)
       const int dest = __shfl_sync(0xffffffffu, my_dest, j);
       const int row = __shfl_sync(0xffffffffu, my_row, j);
       const float wj = __shfl_sync(0xffffffffu, my_w, j);
+      // fused A2A: the expert outputs were pushed here by the GEMM epilogue, in pair order
       const uint4* src = reinterpret_cast<const uint4*>(
-          reinterpret_cast<const __nv_bfloat16*>(out_ptrs[dest]) + (size_t)row * d);
+          comb ? comb + (size_t)(t * k + j) * d
+               : reinterpret_cast<const __nv_bfloat16*>(out_ptrs[dest]) + (size_t)row * d);
       uint4 v[VPL];
 #pragma unroll
       for (int i = 0; i < VPL; ++i) v[i] = ld_v4(src + lane + 32 * i);
@@ -266,7 +274,7 @@ __global__ void __launch_bounds__(256)
                        void* const* dgrad_ptrs, const int32_t* __restrict__ pair_dest,
                        const int32_t* __restrict__ pair_row, const float* __restrict__ w, int T,
                        int d, int k, float* dw, const pp_group* groups, const int32_t* num_groups,
-                       __nv_bfloat16* own) {
+                       __nv_bfloat16* own, const __nv_bfloat16* __restrict__ comb) {
   const int lane = threadIdx.x & 31;
   const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -289,8 +297,8 @@ __global__ void __launch_bounds__(256)
       const int row = __shfl_sync(0xffffffffu, my_row, j);
       const float wj = __shfl_sync(0xffffffffu, my_w, j);
       const size_t off = (size_t)row * d;
-      const uint4* ysrc =
-          reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(out_ptrs[dest]) + off);
+      const uint4* ysrc = reinterpret_cast<const uint4*>(
+          comb ? comb + (size_t)(t * k + j) * d : reinterpret_cast<const __nv_bfloat16*>(out_ptrs[dest]) + off);
       uint4* gdst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(dgrad_ptrs[dest]) + off);
       float dot = 0.f;
 #pragma unroll
@@ -321,7 +329,7 @@ __global__ void __launch_bounds__(256)
                         const int32_t* __restrict__ pair_row, const int32_t* __restrict__ idx,
                         const float* __restrict__ probs, const float* __restrict__ dw, int T, int d,
                         int k, int E, __nv_bfloat16* dx, __nv_bfloat16* dl, float4* zero,
-                        int zero_vec) {
+                        int zero_vec, const __nv_bfloat16* __restrict__ comb) {
   const int lane = threadIdx.x & 31;
   const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -347,7 +355,8 @@ __global__ void __launch_bounds__(256)
       const int dest = __shfl_sync(0xffffffffu, my_dest, j);
       const int row = __shfl_sync(0xffffffffu, my_row, j);
       const uint4* src = reinterpret_cast<const uint4*>(
-          reinterpret_cast<const __nv_bfloat16*>(dxp_ptrs[dest]) + (size_t)row * d);
+          comb ? comb + (size_t)(t * k + j) * d
+               : reinterpret_cast<const __nv_bfloat16*>(dxp_ptrs[dest]) + (size_t)row * d);
       uint4 v[VPL];
 #pragma unroll
       for (int i = 0; i < VPL; ++i) v[i] = ld_v4(src + lane + 32 * i);
@@ -466,25 +475,27 @@ extern "C" int pp_dispatch(const void* x, const int32_t* idx, const int32_t* ran
                            int32_t d, int32_t k, int32_t m, int32_t E, void* const* recv_ptrs,
                            void* own_recv, const pp_group* groups, const int32_t* num_groups,
                            int32_t max_groups, int32_t* pair_dest, int32_t* pair_row,
-                           void* stream) {
+                           void* const* origin_ptrs, int32_t my_rank, void* stream) {
   PP_CHECK_ARG(x && idx && rank && chunk_base && slot_dest && recv_ptrs && own_recv && groups &&
                    num_groups && pair_dest && pair_row,
                "pp_dispatch: null pointer");
+  PP_CHECK_ARG(my_rank >= 0 && (int64_t)(my_rank + 1) * T * k < (1ll << 31), "pp_dispatch: bad my_rank");
   cudaStream_t st = as_stream(stream);
   PP_VPL_SWITCH(d, (dispatch_kernel<VPL><<<grid_for_tokens(T), 256, 0, st>>>(
                        reinterpret_cast<const __nv_bfloat16*>(x), idx, rank, chunk_base,
                        slot_dest, T, d, k, m, E, recv_ptrs, pair_dest, pair_row, groups, num_groups,
-                       reinterpret_cast<__nv_bfloat16*>(own_recv))));
+                       reinterpret_cast<__nv_bfloat16*>(own_recv), origin_ptrs, my_rank)));
   PP_LAUNCH_CHECK();
   return PP_OK;
 }
 
 extern "C" int pp_combine(void* const* out_ptrs, const int32_t* pair_dest, const int32_t* pair_row,
-                          const float* w, int32_t T, int32_t d, int32_t k, void* y, void* stream) {
-  PP_CHECK_ARG(out_ptrs && pair_dest && pair_row && w && y, "pp_combine: null pointer");
+                          const float* w, int32_t T, int32_t d, int32_t k, void* y, const void* comb,
+                          void* stream) {
+  PP_CHECK_ARG((out_ptrs || comb) && pair_dest && pair_row && w && y, "pp_combine: null pointer");
   PP_VPL_SWITCH(d, (combine_kernel<VPL><<<grid_for_tokens(T), 256, 0, as_stream(stream)>>>(
                        out_ptrs, pair_dest, pair_row, w, T, d, k,
-                       reinterpret_cast<__nv_bfloat16*>(y))));
+                       reinterpret_cast<__nv_bfloat16*>(y), reinterpret_cast<const __nv_bfloat16*>(comb))));
   PP_LAUNCH_CHECK();
   return PP_OK;
 }
@@ -493,15 +504,16 @@ extern "C" int pp_combine_bwd(const void* dy, void* const* out_ptrs, void* const
                               void* own_dgrad, const int32_t* pair_dest, const int32_t* pair_row,
                               const float* w, const pp_group* groups, const int32_t* num_groups,
                               int32_t max_groups, int32_t T, int32_t d, int32_t k, float* dw,
-                              void* stream) {
-  PP_CHECK_ARG(dy && out_ptrs && dgrad_ptrs && own_dgrad && pair_dest && pair_row && w && groups &&
-                   num_groups && dw,
+                              const void* comb, void* stream) {
+  PP_CHECK_ARG(dy && (out_ptrs || comb) && dgrad_ptrs && own_dgrad && pair_dest && pair_row && w &&
+                   groups && num_groups && dw,
                "pp_combine_bwd: null pointer");
   cudaStream_t st = as_stream(stream);
   PP_VPL_SWITCH(d, (combine_bwd_kernel<VPL><<<grid_for_tokens(T), 256, 0, st>>>(
                        reinterpret_cast<const __nv_bfloat16*>(dy), out_ptrs, dgrad_ptrs,
                        pair_dest, pair_row, w, T, d, k, dw, groups, num_groups,
-                       reinterpret_cast<__nv_bfloat16*>(own_dgrad))));
+                       reinterpret_cast<__nv_bfloat16*>(own_dgrad),
+                       reinterpret_cast<const __nv_bfloat16*>(comb))));
   PP_LAUNCH_CHECK();
   return PP_OK;
 }
@@ -510,9 +522,9 @@ extern "C" int pp_dispatch_bwd(void* const* dxp_ptrs, const int32_t* pair_dest,
                                const int32_t* pair_row, const int32_t* idx, const float* probs,
                                const float* dw, int32_t T, int32_t d, int32_t k, int32_t E,
                                int32_t EP, void* dx, void* dl, float* zero_f32, int64_t zero_elems,
-                               void* stream) {
+                               const void* comb, void* stream) {
   PP_CHECK_ARG(zero_elems % 4 == 0 && (zero_elems == 0 || zero_f32), "pp_dispatch_bwd: zero buffer");
-  PP_CHECK_ARG(dxp_ptrs && pair_dest && pair_row && idx && probs && dw && dx && dl,
+  PP_CHECK_ARG((dxp_ptrs || comb) && pair_dest && pair_row && idx && probs && dw && dx && dl,
                "pp_dispatch_bwd: null pointer");
   PP_CHECK_ARG(EP == 64 || EP == 128, "pp_dispatch_bwd: EP=%d must be 64 or 128", EP);
   PP_CHECK_ARG(E <= EP, "pp_dispatch_bwd: E=%d > EP=%d", E, EP);
@@ -522,11 +534,13 @@ extern "C" int pp_dispatch_bwd(void* const* dxp_ptrs, const int32_t* pair_dest,
   if (EP == 64) {
     PP_VPL_SWITCH(d, (dispatch_bwd_kernel<VPL, 64><<<grid_for_tokens(T), 256, 0, st>>>(
                          dxp_ptrs, pair_dest, pair_row, idx, probs, dw, T, d, k, E, dxp, dlp,
-                         reinterpret_cast<float4*>(zero_f32), (int)(zero_elems / 4))));
+                         reinterpret_cast<float4*>(zero_f32), (int)(zero_elems / 4),
+                         reinterpret_cast<const __nv_bfloat16*>(comb))));
   } else {
     PP_VPL_SWITCH(d, (dispatch_bwd_kernel<VPL, 128><<<grid_for_tokens(T), 256, 0, st>>>(
                          dxp_ptrs, pair_dest, pair_row, idx, probs, dw, T, d, k, E, dxp, dlp,
-                         reinterpret_cast<float4*>(zero_f32), (int)(zero_elems / 4))));
+                         reinterpret_cast<float4*>(zero_f32), (int)(zero_elems / 4),
+                         reinterpret_cast<const __nv_bfloat16*>(comb))));
   }
   PP_LAUNCH_CHECK();
   return PP_OK;

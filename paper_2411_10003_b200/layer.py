@@ -162,7 +162,7 @@ class MoELayer(torch.nn.Module):
                  capacity_rows: int | None = None, max_replicas: int | None = None,
                  seed: int = 0, device=None, trans_ctas: int = 32, replica_engine: str = "copy",
                  policy: str | None = None, planning: str = "host", placement: str = "virtual",
-                 refine_slots: bool = False) -> None:
+                 refine_slots: bool = False, fused_a2a: bool = False) -> None:
         super().__init__()
         if not torch.cuda.is_available():
             raise RuntimeError("MoELayer needs a CUDA device (B200); there is no CPU path")
@@ -242,6 +242,12 @@ class MoELayer(torch.nn.Module):
         self.yp = PeerBuffer((R, d_model), torch.bfloat16, self.group, dev)
         self.dyp = PeerBuffer((R, d_model), torch.bfloat16, self.group, dev)
         self.dxp = PeerBuffer((R, d_model), torch.bfloat16, self.group, dev)
+        # fused A2A (FWD2 -> combine, DGRAD1 -> dispatch backward in the GEMM epilogue):
+        # pp_dispatch records each received row's origin pair; the epilogues push results
+        # straight into the owning rank's comb [T*k][d] (pair order), read locally after
+        self.fused_a2a = bool(fused_a2a)
+        self.origin = PeerBuffer((R,), torch.int32, self.group, dev) if self.fused_a2a else None
+        self.comb = PeerBuffer((tokens * top_k, d_model), torch.bfloat16, self.group, dev) if self.fused_a2a else None
         self.pre = torch.zeros((R, d_ff), dtype=torch.bfloat16, device=dev)
         self.act = torch.zeros((R, d_ff), dtype=torch.bfloat16, device=dev)
         # ---- planning state -------------------------------------------------
@@ -439,6 +445,9 @@ class MoELayer(torch.nn.Module):
             done.record(self.plan_stream)
         self._plan_pending = (done, mask_dev)
 
+    def _comb_local(self):
+        return self.comb.local.data_ptr() if self.fused_a2a else None
+
     def _plan_inflight(self) -> bool:
         return self.planning == "device" and self._plan_done_dev is not None or self._plan_pending is not None
 
@@ -609,7 +618,7 @@ class MoELayer(torch.nn.Module):
             self._agg_done.record(self.comm_stream)
             self._log_side("SubAgg1" if parts == 2 else "SubAgg2", t0, self._side_event(self.comm_stream))
 
-    def _gemm(self, mode, a, b, c, c2=None, stream=None, num_sms=None):
+    def _gemm(self, mode, a, b, c, c2=None, stream=None, num_sms=None, scatter=False):
         timing = self.gemm_timing
         if timing is not None:
             pool = self.gemm_event_pool
@@ -619,9 +628,15 @@ class MoELayer(torch.nn.Module):
                 e0 = torch.cuda.Event(enable_timing=True)
                 e1 = torch.cuda.Event(enable_timing=True)
             e0.record()
-        _device.grouped_gemm(mode, a, b, c, c2, self.groups, self.num_groups, self.max_groups,
-                             self.rows_cap, self.slots, self.d, self.f,
-                             num_sms=self.gemm_sms if num_sms is None else num_sms, stream=stream)
+        nsm = self.gemm_sms if num_sms is None else num_sms
+        if scatter:  # fused A2A epilogue: rows go to their source rank's comb buffer
+            _lib.call("pp_grouped_gemm_scatter", mode, a.data_ptr(), b.data_ptr(), self.groups.data_ptr(),
+                      self.num_groups.data_ptr(), self.max_groups, self.rows_cap, self.slots, self.d, self.f,
+                      self.origin.local.data_ptr(), self.comb.ptrs.data_ptr(), self.T * self.k, nsm,
+                      _device.stream_ptr(stream))
+        else:
+            _device.grouped_gemm(mode, a, b, c, c2, self.groups, self.num_groups, self.max_groups,
+                                 self.rows_cap, self.slots, self.d, self.f, num_sms=nsm, stream=stream)
         if timing is not None:
             e1.record()
             timing.append((mode, e0, e1))
@@ -668,7 +683,8 @@ class MoELayer(torch.nn.Module):
                   self.chunk_base.data_ptr(), self.slot_dest.data_ptr(), self.T, self.d, self.k, self.m,
                   self.E, self.xp.ptrs.data_ptr(), self.xp.local.data_ptr(), self.groups.data_ptr(),
                   self.num_groups.data_ptr(), self.max_groups, self.pair_dest.data_ptr(),
-                  self.pair_row.data_ptr(), sp)
+                  self.pair_row.data_ptr(), self.origin.ptrs.data_ptr() if self.fused_a2a else None,
+                  self.rank, sp)
         self._mark("dispatch")
         if trans_done is not None:
             torch.cuda.current_stream().wait_event(trans_done)
@@ -681,13 +697,14 @@ class MoELayer(torch.nn.Module):
         if self._plan_inflight():
             fwd_sms = max(2, (self.gemm_sms or _device.num_sms(self.device)) - 2)
         self._gemm(_lib.PP_GEMM_FWD1, self.xp.local, self.w1_arena.local, self.pre, self.act, num_sms=fwd_sms)
-        self._gemm(_lib.PP_GEMM_FWD2, self.act, self.w2_arena.local, self.yp.local, num_sms=fwd_sms)
+        self._gemm(_lib.PP_GEMM_FWD2, self.act, self.w2_arena.local, self.yp.local, num_sms=fwd_sms,
+                   scatter=self.fused_a2a)
         self._mark("fwd_gemms")
         self.barrier()
         self._mark("barrier2")
         y = torch.empty((self.T, self.d), dtype=torch.bfloat16, device=self.device)
         _lib.call("pp_combine", self.yp.ptrs.data_ptr(), self.pair_dest.data_ptr(), self.pair_row.data_ptr(),
-                  self.w.data_ptr(), self.T, self.d, self.k, y.data_ptr(), sp)
+                  self.w.data_ptr(), self.T, self.d, self.k, y.data_ptr(), self._comb_local(), sp)
         self._mark("combine")
         return y
 
@@ -698,7 +715,7 @@ class MoELayer(torch.nn.Module):
         _lib.call("pp_combine_bwd", dy.data_ptr(), self.yp.ptrs.data_ptr(), self.dyp.ptrs.data_ptr(),
                   self.dyp.local.data_ptr(), self.pair_dest.data_ptr(), self.pair_row.data_ptr(),
                   self.w.data_ptr(), self.groups.data_ptr(), self.num_groups.data_ptr(), self.max_groups,
-                  self.T, self.d, self.k, self.dw.data_ptr(), sp)
+                  self.T, self.d, self.k, self.dw.data_ptr(), self._comb_local(), sp)
         self._mark("combine_bwd")
         self.barrier()
         self._mark("barrier3")
@@ -715,7 +732,8 @@ class MoELayer(torch.nn.Module):
                        num_sms=side_sms)
             self._gemm(_lib.PP_GEMM_WGRAD1, self.pre, self.xp.local, self.g1_arena.local, num_sms=side_sms)
             self._issue_agg(parts=1)
-            self._gemm(_lib.PP_GEMM_DGRAD1, self.pre, self.w1_arena.local, self.dxp.local, num_sms=side_sms)
+            self._gemm(_lib.PP_GEMM_DGRAD1, self.pre, self.w1_arena.local, self.dxp.local, num_sms=side_sms,
+                       scatter=self.fused_a2a)
         else:
             self._gemm(_lib.PP_GEMM_DGRAD2, self.dyp.local, self.w2_arena.local, self.pre, self.pre)
             self._gemm(_lib.PP_GEMM_WGRAD2, self.dyp.local, self.act, self.g2_arena.local)
@@ -723,7 +741,8 @@ class MoELayer(torch.nn.Module):
             if agg:  # copy engine: the home pulls once every rank's replica grads exist; rides on DGRAD1
                 self.barrier()
                 self._issue_agg()
-            self._gemm(_lib.PP_GEMM_DGRAD1, self.pre, self.w1_arena.local, self.dxp.local)
+            self._gemm(_lib.PP_GEMM_DGRAD1, self.pre, self.w1_arena.local, self.dxp.local,
+                       scatter=self.fused_a2a)
         self._mark("bwd_gemms")
         self.barrier()
         self._mark("barrier4")
@@ -731,7 +750,8 @@ class MoELayer(torch.nn.Module):
         _lib.call("pp_dispatch_bwd", self.dxp.ptrs.data_ptr(), self.pair_dest.data_ptr(),
                   self.pair_row.data_ptr(), self.idx.data_ptr(), self.probs.data_ptr(), self.dw.data_ptr(),
                   self.T, self.d, self.k, self.E, self.EP, dx.data_ptr(), self.dlogits.data_ptr(),
-                  self.wg.main_grad.data_ptr(), self.wg.main_grad.numel(), sp)  # also zeroes dWg
+                  self.wg.main_grad.data_ptr(), self.wg.main_grad.numel(), self._comb_local(),
+                  sp)  # also zeroes dWg
         self._mark("dispatch_bwd")
         _lib.call("pp_gate_bwd", self.dlogits.data_ptr(), self.wg.data_ptr(), x.data_ptr(), self.T, self.d,
                   self.E, self.EP, dx.data_ptr(), self.wg.main_grad.data_ptr(), sp)
@@ -812,7 +832,7 @@ class MoELayer(torch.nn.Module):
 
     def close(self) -> None:
         for b in (self.w1_arena, self.w2_arena, self.g1_arena, self.g2_arena, self.xp, self.yp, self.dyp, self.dxp,
-                  self.counts_buf, self.agg_stage):
+                  self.counts_buf, self.agg_stage, self.origin, self.comb):
             if b is not None:
                 b.close()
 

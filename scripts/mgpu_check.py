@@ -41,6 +41,7 @@ def main():
     layer = pp.MoELayer(d, f, E, k, tokens=T, group=dist.group.WORLD,
                         planner=pp.PlannerConfig(n=n_excl, alpha=0.5), cluster=cl, model=mo, seed=0,
                         placement=placement, refine_slots=os.environ.get("PP_REFINE") == "1",
+                        fused_a2a=os.environ.get("PP_FUSED") == "1",
                         replica_engine=os.environ.get("PP_ENGINE", "copy"),
                         policy=os.environ.get("PP_POLICY") or None,
                         planning=os.environ.get("PP_PLANNING", "host"))

@@ -50,8 +50,8 @@ def test_route_exact(T, d, E, k):
     torch.testing.assert_close(probs.cpu(), rprobs, rtol=1e-5, atol=1e-7)
 
 
-def run_layer(T, d, f, E, k, bias=None, seed=0):
-    layer = pp.MoELayer(d, f, E, k, tokens=T, seed=seed)
+def run_layer(T, d, f, E, k, bias=None, seed=0, **kw):
+    layer = pp.MoELayer(d, f, E, k, tokens=T, seed=seed, **kw)
     x, wg = M.exact_inputs(T, d, E, seed=seed + 11)
     with torch.no_grad():
         layer.wg.copy_(wg.to(layer.device))
@@ -66,11 +66,14 @@ def run_layer(T, d, f, E, k, bias=None, seed=0):
     return layer, x, wg, dy, y, xd.grad
 
 
+@pytest.mark.parametrize("fused", [False, True])
 @pytest.mark.parametrize("T,d,f,E,k", [(2048, 256, 512, 16, 2), (1024, 256, 256, 8, 1), (4096, 512, 768, 32, 2)])
-def test_layer_vs_oracle(T, d, f, E, k):
+def test_layer_vs_oracle(T, d, f, E, k, fused):
+    """fused=True: FWD2 / DGRAD1 epilogues push rows to the pair's owner (pp_grouped_gemm_scatter)
+    and combine / dispatch-backward read them locally -- same contract, same tolerances."""
     bias = torch.log(torch.tensor([1.0 / (i + 1) ** 1.2 for i in range(E)]))  # Zipf skew
     bias = torch.round(bias * 4) / 4  # keep logits exact
-    layer, x, wg, dy, y, dx = run_layer(T, d, f, E, k, bias=bias, seed=E)
+    layer, x, wg, dy, y, dx = run_layer(T, d, f, E, k, bias=bias, seed=E, fused_a2a=fused)
     w1 = layer.w1.detach().cpu()
     w2 = layer.w2.detach().cpu()
     ref = M.LayerRef(w1, w2, wg, bias, k, D=1)
@@ -129,3 +132,22 @@ def test_probe_loss_and_graphed_step():
     torch.cuda.synchronize()
     assert torch.equal(ya, y1.to(dev)) and torch.equal(dxa, dx1.to(dev))
     assert torch.equal(gs.loss, layer.probe_loss(ya, dys))
+
+
+def test_fused_a2a_bit_identical_to_unfused():
+    """The fused epilogue path changes where rows travel, not the arithmetic: y, dx and
+    every gradient are bit-identical to the unfused layer on the same inputs."""
+    outs = []
+    for fused in (False, True):
+        layer, x, wg, dy, y, dx = run_layer(2048, 256, 512, 16, 2, seed=5, fused_a2a=fused)
+        outs.append((y.detach().clone(), dx.clone(), layer.w1.main_grad.clone(), layer.w2.main_grad.clone(),
+                     layer.dw.clone()))
+        if fused:  # every pair's row recorded once (pair index t*k+j), padding rows marked -1
+            org = layer.origin.local.cpu()
+            seen = []
+            for g in layer.group_table():
+                seen += org[g["row_off"]:g["row_off"] + g["rows"]].tolist()
+                assert (org[g["row_off"] + g["rows"]:g["row_off"] + g["rows_pad"]] == -1).all()
+            assert sorted(seen) == list(range(2048 * 2))
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)

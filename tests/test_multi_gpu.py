@@ -26,12 +26,14 @@ def _ngpus():
 @pytest.mark.parametrize("planning,engine,policy,placement", [
     ("host", "copy", "", "virtual"), ("device", "sm", "", "virtual"), ("host", "sm", "top2", "virtual"),
     ("host", "copy", "vanilla", "virtual"), ("device", "sm", "", "physical"), ("host", "copy", "", "physical"),
-    ("device", "sm", "", "physical+refine")])
+    ("device", "sm", "", "physical+refine"), ("device", "sm", "", "physical+refine+fused"),
+    ("host", "copy", "", "virtual+fused")])
 def test_ep_layer_parity(planning, engine, policy, placement):
     n = min(_ngpus(), 4)
-    refine = placement.endswith("+refine")
+    opts = placement.split("+")[1:]
     env = dict(os.environ, PP_PLANNING=planning, PP_ENGINE=engine, PP_POLICY=policy,
-               PP_PLACEMENT=placement.split("+")[0], PP_REFINE="1" if refine else "0")
+               PP_PLACEMENT=placement.split("+")[0], PP_REFINE="1" if "refine" in opts else "0",
+               PP_FUSED="1" if "fused" in opts else "0")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--standalone", "--nproc-per-node", str(n),
            str(ROOT / "scripts" / "mgpu_check.py")]
     r = subprocess.run(cmd, env=env, cwd=ROOT, capture_output=True, text=True, timeout=600)
