@@ -413,6 +413,7 @@ def main() -> None:
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     w0 = time.perf_counter()
+    layer.barrier()  # device-side peer barrier: the ranks' timed regions start together
     t0.record()
     h0 = time.perf_counter()
     for i in range(args.steps):
@@ -551,6 +552,7 @@ def main() -> None:
         ev_free = [torch.cuda.Event() for _ in range(2)]
         ev_out = torch.cuda.Event()
         w0 = time.perf_counter()
+        layer.barrier()  # device-side peer barrier: every rank's clock starts together
         e0.record(main)
 
         def h2d(i):
