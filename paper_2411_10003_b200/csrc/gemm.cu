@@ -83,7 +83,6 @@ struct GemmParams {
   int split_rows;   // with single_rows: split-K chunk size (one implicit group per chunk)
   int m_real;       // EPI_F32_ATOMIC: rows of the output that exist (< M_fixed)
   unsigned long long* dbg;  // optional per-CTA wait-cycle counters (PPMOE_GEMM_DEBUG)
-  int dbg_noload;           // diagnostic: skip operand TMA (MMA + epilogue only)
   // fused combine / dispatch-backward (EPI_BF16 only): output row r goes to pair
   // origin[r] = src_rank * pairs_per_rank + t*k + j, i.e. row (t*k+j) of scatter_ptrs[src_rank]
   // (peer memory over NVLink), instead of this rank's receive-layout buffer; origin < 0
@@ -467,14 +466,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           // TMA complete_tx may land first -- the phase cannot complete before the
           // leader's arrive, and the peer only refills a stage after the MMAs that
           // consumed it committed, so transactions never cross phases
-          if (p.dbg_noload) {  // diagnostic: MMAs run on whatever the stage holds
-            if (CG == 1 || cta_rank == 0) mbar_arrive(&full_bar[stage]);
-            if (++stage == STAGES) {
-              stage = 0;
-              phase ^= 1;
-            }
-            continue;
-          }
           if (CG == 1 || cta_rank == 0) mbar_arrive_expect_tx(&full_bar[stage], STAGE_BYTES * CG);
           if constexpr (!A_MN) {
             load(sa, &tmA, k0, tl.row_off + tl.m0);
@@ -1015,8 +1006,6 @@ static int grouped_gemm_impl(int32_t mode, const void* a, const void* b, void* c
   static const bool dbg_on = getenv("PPMOE_GEMM_DEBUG") != nullptr;
   if (dbg_on && !g_dbg_buf) cudaMalloc(&g_dbg_buf, 4 * 1024 * sizeof(unsigned long long));
   p.dbg = dbg_on ? g_dbg_buf : nullptr;
-  static const int noload = getenv("PPMOE_GEMM_NOLOAD") ? atoi(getenv("PPMOE_GEMM_NOLOAD")) : 0;
-  p.dbg_noload = noload;
   p.groups = groups;
   p.num_groups = num_groups;
   p.max_groups = max_groups;

@@ -1,3 +1,2 @@
 cd $GRAFT_REPO_ROOT
 echo "== normal + debug counters"; PPMOE_GEMM_DEBUG=1 timeout 300 python scripts/gemm_bench.py 2>&1 | tail -12
-echo "== no operand loads (MMA + epilogue only)"; PPMOE_GEMM_NOLOAD=1 PPMOE_GEMM_DEBUG=1 timeout 300 python scripts/gemm_bench.py 2>&1 | tail -12
