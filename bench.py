@@ -41,6 +41,21 @@ CONFIGS = {
 METRIC = "MoE-layer tokens/s fwd+bwd at 1/2/4/8 B200; planner ms/iter; load imbalance"
 
 
+def bind_cpu_to_gpu(device_index: int) -> None:
+    """Pin this process to the CPU cores NVML reports as local to its GPU, so the pinned
+    host buffers of the e2e loop are first-touched on the GPU's NUMA node and the H2D
+    copies do not cross the inter-socket link (what NCCL / launchers do per rank)."""
+    try:
+        import pynvml
+        import torch
+
+        pynvml.nvmlInit()
+        uuid = "GPU-" + str(torch.cuda.get_device_properties(device_index).uuid)
+        pynvml.nvmlDeviceSetCpuAffinity(pynvml.nvmlDeviceGetHandleByUUID(uuid.encode()))
+    except Exception:  # no NVML / no affinity support: keep the default placement
+        pass
+
+
 def zipf_bias(E: int, skew: float, seed: int):
     """Per-expert logit bias log(p_e), p = Zipf(skew) in a seeded random order
     (the popularity shape of the reference generator, workload.py:89-95)."""
@@ -303,6 +318,8 @@ def main() -> None:
                     help="physical placement: slot-level refinement of the plan (1/0; beyond the paper)")
     ap.add_argument("--fused-a2a", type=int, default=1,
                     help="N > 1: combine / dispatch-backward fused into the FWD2 / DGRAD1 epilogues (1/0)")
+    ap.add_argument("--trans-gate", type=int, default=None,
+                    help="SM-engine Trans overlapped with FWD1 via per-tile gates (1) or awaited before it (0)")
     ap.add_argument("--avg-bandwidth", type=float, default=None,
                     help="planner cost model B (bytes/s; default layer.default_specs' 450e9)")
     ap.add_argument("--trans-ctas", type=int, default=None, help="SMs of the SM-engine Trans push")
@@ -329,6 +346,7 @@ def main() -> None:
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local_rank)
+    bind_cpu_to_gpu(local_rank)  # pinned host batches then live on the GPU's NUMA node
     dev = torch.device("cuda", local_rank)
     group = None
     if world > 1:
@@ -372,6 +390,8 @@ def main() -> None:
         layer.trans_ctas = args.trans_ctas
     if args.agg_ctas:
         layer.agg_ctas = args.agg_ctas
+    if args.trans_gate is not None:
+        layer.trans_gate = bool(args.trans_gate)
     layer.set_gate_bias(zipf_bias(E, 1.2, 0))
     g = torch.Generator(device="cpu").manual_seed(1000 + rank)
     x = torch.randn((T, d), generator=g).to(dev, torch.bfloat16)

@@ -177,7 +177,7 @@ int pp_dispatch(const void* x, const int32_t* idx, const int32_t* rank,
 
 /* y[t] = sum_j w[t][j] * out_ptrs[pair_dest][pair_row] (fp32 accumulate, bf16 out).
  * Fused-A2A mode (comb != NULL, out_ptrs may be NULL): the expert outputs were
- * already pushed to this rank by pp_grouped_gemm_scatter as comb [T*k][d] bf16 in
+ * already pushed to this rank by pp_grouped_gemm_ex as comb [T*k][d] bf16 in
  * pair order (t*k + j), so the gather is local. */
 int pp_combine(void* const* out_ptrs, const int32_t* pair_dest, const int32_t* pair_row,
                const float* w, int32_t T, int32_t d, int32_t k, void* y, const void* comb,
@@ -235,18 +235,25 @@ int pp_grouped_gemm(int32_t mode, const void* a, const void* b, void* c, void* c
 #define PP_DOT_PARTIALS 592
 int pp_dot_bf16(const void* a, const void* b, int64_t n, float* partial, float* out, void* stream);
 
-/* Fused GEMM + all-to-all (FWD2 -> combine, DGRAD1 -> dispatch backward):
- * same GEMM as pp_grouped_gemm(mode), but the epilogue stores output row r of
- * the receive layout straight into the rank that owns the pair, over NVLink:
- * row (o % pairs_per_rank) of scatter_ptrs[o / pairs_per_rank] ([T*k][d] bf16),
- * o = origin[r] as written by pp_dispatch (origin_ptrs; padding rows -1, not
- * stored).  The transfer overlaps the remaining tiles' MMAs; pp_combine /
- * pp_dispatch_bwd then read comb locally.  mode: PP_GEMM_FWD2 or PP_GEMM_DGRAD1. */
-int pp_grouped_gemm_scatter(int32_t mode, const void* a, const void* b, const pp_group* groups,
-                            const int32_t* num_groups, int32_t max_groups, int32_t rows_capacity,
-                            int32_t num_slots, int32_t d_model, int32_t d_ff, const int32_t* origin,
-                            void* const* scatter_ptrs, int32_t pairs_per_rank, int32_t num_sms,
-                            void* stream);
+/* pp_grouped_gemm with two optional fusions (NULL disables each):
+ * Fused GEMM + all-to-all (origin != NULL; FWD2 -> combine, DGRAD1 -> dispatch
+ *   backward): the epilogue stores output row r of the receive layout straight
+ *   into the rank that owns the pair, over NVLink: row (o % pairs_per_rank) of
+ *   scatter_ptrs[o / pairs_per_rank] ([T*k][d] bf16), o = origin[r] as written
+ *   by pp_dispatch (origin_ptrs; padding rows -1, not stored) -- one 64-B bulk
+ *   copy per row chunk from the staging smem, overlapping the remaining tiles'
+ *   MMAs; pp_combine / pp_dispatch_bwd then read comb locally.  c may be NULL.
+ * Replica gate (gate_flags != NULL; FWD1 / FWD2 while Trans is in flight): the
+ *   home groups (wslot < first_replica_slot) are scheduled first; before the
+ *   first replica tile's loads the TMA producer waits until gate_flags[r] >=
+ *   *gate_epoch for every peer r != my_rank (the completion flags of
+ *   pp_replica_trans; gate_flags = this rank's [D] uint64 row).  20 s -> trap. */
+int pp_grouped_gemm_ex(int32_t mode, const void* a, const void* b, void* c, void* c2,
+                       const pp_group* groups, const int32_t* num_groups, int32_t max_groups,
+                       int32_t rows_capacity, int32_t num_slots, int32_t d_model, int32_t d_ff,
+                       const int32_t* origin, void* const* scatter_ptrs, int32_t pairs_per_rank,
+                       const uint64_t* gate_flags, const uint64_t* gate_epoch, int32_t my_rank,
+                       int32_t D, int32_t first_replica_slot, int32_t num_sms, void* stream);
 
 /* ---- replica Trans / Agg over peer memory (K5) --------------------------- */
 /* Trans (home side, SM engine): push each of this rank's home experts' W1/W2
@@ -257,10 +264,16 @@ int pp_grouped_gemm_scatter(int32_t mode, const void* a, const void* b, const pp
  * routes to, ascending, get slots m, m+1, ... on r.  Needs only the mask, so it
  * can run before this iteration's routing; every rank must have passed the
  * previous backward's last peer barrier.  `max_ctas` = SMs it occupies
- * (E <= 1024, D*E <= 16384). */
+ * (E <= 1024, D*E <= 16384).  parts: 1 = W1 only, 2 = W2 only, 3 = both.
+ * flag_ptrs (nullable; peer table of [rows][D] uint64 flag arrays): when every
+ * CTA is done, the last one stores *epoch (device value, e.g. the peer-barrier
+ * counter) into flag_ptrs[r][flag_row*D + my_rank] of every peer r with release
+ * semantics -- the completion signal the pp_grouped_gemm_ex gate waits on;
+ * done_ctr is a zeroed uint32 scratch word (left zeroed). */
 int pp_replica_trans(void* const* w1_ptrs, void* const* w2_ptrs, const uint8_t* mask, int32_t E,
-                     int32_t m, int32_t my_rank, int32_t d_model, int32_t d_ff, int32_t max_ctas,
-                     void* stream);
+                     int32_t m, int32_t my_rank, int32_t d_model, int32_t d_ff, int32_t parts,
+                     void* const* flag_ptrs, int32_t flag_row, const uint64_t* epoch,
+                     uint32_t* done_ctr, int32_t max_ctas, void* stream);
 
 /* Agg phase 1 (replica side): push the fp32 grads of this rank's replica slots
  * (g1_ptrs/g2_ptrs [D] grad arenas) into the home rank's staging area

@@ -75,8 +75,8 @@ SIGNATURES = {
     "pp_dispatch_bwd": [P, P, P, P, P, P, I, I, I, I, I, P, P, P, ctypes.c_int64, P, P],
     "pp_gate_bwd": [P, P, P, I, I, I, I, P, P, P],
     "pp_grouped_gemm": [I, P, P, P, P, P, P, I, I, I, I, I, I, P],
-    "pp_grouped_gemm_scatter": [I, P, P, P, P, I, I, I, I, I, P, P, I, I, P],
-    "pp_replica_trans": [P, P, P, I, I, I, I, I, I, P],
+    "pp_grouped_gemm_ex": [I, P, P, P, P, P, P, I, I, I, I, I, P, P, I, P, P, I, I, I, I, P],
+    "pp_replica_trans": [P, P, P, I, I, I, I, I, I, P, I, P, P, I, P],
     "pp_replica_agg": [P, P, P, P, I, I, I, I, I, I, I, P],
     "pp_dot_bf16": [P, P, ctypes.c_int64, P, P, P],
     "pp_replica_agg_reduce": [P, P, P, P, I, I, I, I, I, I, I, P],
@@ -136,7 +136,7 @@ def check(rc: int, what: str = "") -> None:
 KERNELS_PER_CALL = {
     "pp_plan_greedy": 1, "pp_plan_physical": 1, "pp_derive_loads": 1, "pp_top_m_mask": 1, "pp_route_topk": 1, "pp_slot_histogram": 1,
     "pp_dispatch_layout": 1, "pp_dispatch": 1, "pp_combine": 1, "pp_combine_bwd": 1,
-    "pp_dispatch_bwd": 1, "pp_gate_bwd": 2, "pp_grouped_gemm": 1, "pp_grouped_gemm_scatter": 1, "pp_replica_trans": 1,
+    "pp_dispatch_bwd": 1, "pp_gate_bwd": 2, "pp_grouped_gemm": 1, "pp_grouped_gemm_ex": 1, "pp_replica_trans": 1,
     "pp_replica_agg": 1, "pp_replica_agg_reduce": 1, "pp_dot_bf16": 2, "pp_peer_barrier": 1, "pp_agg_accumulate": 1,
 }
 _launches = [0]

@@ -90,6 +90,12 @@ struct GemmParams {
   const int32_t* origin;
   void* const* scatter_ptrs;
   int scatter_tk;
+  // replica gate (FWD1 while Trans is in flight): groups with wslot >= gate_slot0 are
+  // scheduled after the home groups and their B loads wait until every peer's Trans
+  // completion flag gate_flags[r] (r != gate_me) reaches *gate_epoch
+  const uint64_t* gate_flags;
+  const uint64_t* gate_epoch;
+  int gate_me, gate_D, gate_slot0;
 };
 
 struct SchedSmem {
@@ -380,11 +386,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     sched.G = G;
     int acc = 0;
     const int nt = p.N / BN;
+    int next_home = 0;
+    if (p.gate_flags && !p.ragged_k)  // home groups first: the gated replica tiles go last
+      for (int g = 0; g < G; ++g) next_home += p.groups[g].wslot < p.gate_slot0;
+    int next_rep = next_home;
+    next_home = 0;
     for (int g = 0; g < G; ++g) {
       const pp_group gr = p.groups[g];
       // ragged-K (wgrad): keep groups sorted by K descending so the static
       // round-robin tile walk hands out the long tiles first (LPT balance)
       int pos = g;
+      if (p.gate_flags && !p.ragged_k) pos = gr.wslot < p.gate_slot0 ? next_home++ : next_rep++;
       if (p.ragged_k) {
         while (pos > 0 && sched.rows_pad[pos - 1] < gr.rows_pad) {
           sched.row_off[pos] = sched.row_off[pos - 1];
@@ -447,9 +459,25 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
+      bool gate_pending = p.gate_flags != nullptr;
       Tile tl;
       for (int it = 0, t = tile_of(0); t < total_tiles; t = tile_of(++it)) {
         if (!decode_tile<BN, CG>(t, sched, p, tl, cta_rank)) break;
+        if (gate_pending && tl.wslot >= p.gate_slot0) {  // first replica tile: Trans must have landed
+          const uint64_t e = *p.gate_epoch;
+          const uint64_t t0 = globaltimer_ns();
+          for (int r = 0; r < p.gate_D; ++r) {
+            if (r == p.gate_me) continue;
+            while (ld_acquire_sys_u64(p.gate_flags + r) < e) {
+              if (globaltimer_ns() - t0 > 20ull * 1000 * 1000 * 1000) {
+                printf("ppmoe: replica gate timeout (rank %d waiting on %d)\n", p.gate_me, r);
+                __trap();
+              }
+            }
+          }
+          fence_proxy_async_global();
+          gate_pending = false;
+        }
         for (int kb = 0; kb < tl.num_kb; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sa = smem + stage * STAGE_BYTES;
@@ -958,10 +986,17 @@ struct ScatterArgs {
   int tk;
 };
 
+struct GateArgs {
+  const uint64_t* flags;
+  const uint64_t* epoch;
+  int me, D, slot0;
+};
+
 static int grouped_gemm_impl(int32_t mode, const void* a, const void* b, void* c, void* c2,
                              const pp_group* groups, const int32_t* num_groups, int32_t max_groups,
                              int32_t rows_capacity, int32_t num_slots, int32_t d_model,
-                             int32_t d_ff, int32_t num_sms, void* stream, const ScatterArgs* sc);
+                             int32_t d_ff, int32_t num_sms, void* stream, const ScatterArgs* sc,
+                             const GateArgs* gate = nullptr);
 
 extern "C" int pp_grouped_gemm(int32_t mode, const void* a, const void* b, void* c, void* c2,
                                const pp_group* groups, const int32_t* num_groups,
@@ -972,25 +1007,35 @@ extern "C" int pp_grouped_gemm(int32_t mode, const void* a, const void* b, void*
                            num_slots, d_model, d_ff, num_sms, stream, nullptr);
 }
 
-extern "C" int pp_grouped_gemm_scatter(int32_t mode, const void* a, const void* b,
-                                       const pp_group* groups, const int32_t* num_groups,
-                                       int32_t max_groups, int32_t rows_capacity, int32_t num_slots,
-                                       int32_t d_model, int32_t d_ff, const int32_t* origin,
-                                       void* const* scatter_ptrs, int32_t pairs_per_rank,
-                                       int32_t num_sms, void* stream) {
-  PP_CHECK_ARG(mode == PP_GEMM_FWD2 || mode == PP_GEMM_DGRAD1,
-               "pp_grouped_gemm_scatter: only FWD2 (combine) and DGRAD1 (dispatch backward), got %d", mode);
-  PP_CHECK_ARG(origin && scatter_ptrs && pairs_per_rank > 0, "pp_grouped_gemm_scatter: bad scatter arguments");
+extern "C" int pp_grouped_gemm_ex(int32_t mode, const void* a, const void* b, void* c, void* c2,
+                                  const pp_group* groups, const int32_t* num_groups, int32_t max_groups,
+                                  int32_t rows_capacity, int32_t num_slots, int32_t d_model, int32_t d_ff,
+                                  const int32_t* origin, void* const* scatter_ptrs, int32_t pairs_per_rank,
+                                  const uint64_t* gate_flags, const uint64_t* gate_epoch, int32_t my_rank,
+                                  int32_t D, int32_t first_replica_slot, int32_t num_sms, void* stream) {
   ScatterArgs sc{origin, scatter_ptrs, pairs_per_rank};
-  // the unused output tensor map is built over the A operand (>= rows x d_model elements)
-  return grouped_gemm_impl(mode, a, b, const_cast<void*>(a), nullptr, groups, num_groups, max_groups,
-                           rows_capacity, num_slots, d_model, d_ff, num_sms, stream, &sc);
+  GateArgs gt{gate_flags, gate_epoch, my_rank, D, first_replica_slot};
+  if (origin) {
+    PP_CHECK_ARG(mode == PP_GEMM_FWD2 || mode == PP_GEMM_DGRAD1,
+                 "pp_grouped_gemm_ex: the fused A2A epilogue serves FWD2 and DGRAD1, got mode %d", mode);
+    PP_CHECK_ARG(scatter_ptrs && pairs_per_rank > 0, "pp_grouped_gemm_ex: bad scatter arguments");
+    if (!c) c = const_cast<void*>(a);  // the unused output tensor map is built over A (>= rows x d_model)
+  }
+  if (gate_flags) {
+    PP_CHECK_ARG(mode == PP_GEMM_FWD1 || mode == PP_GEMM_FWD2,
+                 "pp_grouped_gemm_ex: the replica gate serves FWD1 and FWD2, got mode %d", mode);
+    PP_CHECK_ARG(gate_epoch && D >= 1 && my_rank >= 0 && my_rank < D && first_replica_slot >= 1,
+                 "pp_grouped_gemm_ex: bad gate arguments");
+  }
+  return grouped_gemm_impl(mode, a, b, c, c2, groups, num_groups, max_groups, rows_capacity, num_slots,
+                           d_model, d_ff, num_sms, stream, origin ? &sc : nullptr, gate_flags ? &gt : nullptr);
 }
 
 static int grouped_gemm_impl(int32_t mode, const void* a, const void* b, void* c, void* c2,
                              const pp_group* groups, const int32_t* num_groups, int32_t max_groups,
                              int32_t rows_capacity, int32_t num_slots, int32_t d_model,
-                             int32_t d_ff, int32_t num_sms, void* stream, const ScatterArgs* sc) {
+                             int32_t d_ff, int32_t num_sms, void* stream, const ScatterArgs* sc,
+                             const GateArgs* gate) {
   PP_CHECK_ARG(a && b && c && groups && num_groups, "pp_grouped_gemm: null pointer");
   PP_CHECK_ARG(max_groups >= 1 && max_groups <= kMaxGroups, "pp_grouped_gemm: max_groups=%d",
                max_groups);
@@ -1015,6 +1060,13 @@ static int grouped_gemm_impl(int32_t mode, const void* a, const void* b, void* c
     p.origin = sc->origin;
     p.scatter_ptrs = sc->ptrs;
     p.scatter_tk = sc->tk;
+  }
+  if (gate) {
+    p.gate_flags = gate->flags;
+    p.gate_epoch = gate->epoch;
+    p.gate_me = gate->me;
+    p.gate_D = gate->D;
+    p.gate_slot0 = gate->slot0;
   }
   int rc = PP_OK;
   // CTA pairs (cta_group::2, 256 x 256 tiles, B split across the pair) unless

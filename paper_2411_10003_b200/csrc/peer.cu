@@ -125,7 +125,9 @@ __device__ __forceinline__ void push_copy(int nmat, size_t vecs, Addr addr) {
 // ended before the last peer barrier of their backward, which this rank has passed.
 __global__ void __launch_bounds__(512) replica_trans_kernel(void* const* w1_ptrs, void* const* w2_ptrs,
                                                             const uint8_t* mask, int E, int m, int me,
-                                                            size_t vecs) {
+                                                            size_t vecs, int parts, void* const* flag_ptrs,
+                                                            int flag_row, const uint64_t* epoch,
+                                                            unsigned int* done_ctr) {
   __shared__ uint8_t flag[kMaxFlags];
   __shared__ int cand[kMaxItems], items[kMaxItems];
   const int D = E / m;
@@ -136,14 +138,32 @@ __global__ void __launch_bounds__(512) replica_trans_kernel(void* const* w1_ptrs
   }
   __syncthreads();
   const int n = compact_items(cand, D * m, items);
-  push_copy<kPushUnroll>(n * 2, vecs, [&](int it2, int, const uint4*& src, uint4*& dst) {
-    const int it = it2 >> 1, mat = it2 & 1;
+  const int np = parts == 3 ? 2 : 1;
+  push_copy<kPushUnroll>(n * np, vecs, [&](int it2, int, const uint4*& src, uint4*& dst) {
+    const int it = np == 2 ? it2 >> 1 : it2, mat = np == 2 ? (it2 & 1) : (parts >> 1);
     const int code = items[it], rj = code >> 10, i = code & 1023;
     const int r = rj / m, j = rj - (rj / m) * m;
     void* const* ptrs = mat ? w2_ptrs : w1_ptrs;
     src = reinterpret_cast<const uint4*>(ptrs[me]) + (size_t)j * vecs;
     dst = reinterpret_cast<uint4*>(ptrs[r]) + (size_t)(m + i) * vecs;
   });
+  if (!flag_ptrs) return;
+  // completion signal: the last CTA to finish tells every peer "my pushes for epoch
+  // *epoch have landed" (release after all CTAs' system-scope fences), so a receiver's
+  // FWD1 can start on its home experts and gate only its replica tiles on the flags
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    const unsigned int prev = atomicAdd(done_ctr, 1u);
+    if (prev == gridDim.x - 1) {
+      __threadfence_system();
+      const uint64_t e = *epoch;
+      const int D = E / m;
+      for (int r = 0; r < D; ++r)
+        if (r != me) st_release_sys(reinterpret_cast<uint64_t*>(flag_ptrs[r]) + (size_t)flag_row * D + me, e);
+      *done_ctr = 0;  // ready for the next launch (stream-ordered)
+    }
+  }
 }
 
 // Agg, phase 1 (replica side): push the fp32 grads of every replica slot of this rank into
@@ -278,7 +298,11 @@ extern "C" int pp_peer_barrier(void* const* signal_ptrs, int32_t D, int32_t my_r
 
 extern "C" int pp_replica_trans(void* const* w1_ptrs, void* const* w2_ptrs, const uint8_t* mask,
                                 int32_t E, int32_t m, int32_t my_rank, int32_t d_model, int32_t d_ff,
-                                int32_t max_ctas, void* stream) {
+                                int32_t parts, void* const* flag_ptrs, int32_t flag_row,
+                                const uint64_t* epoch, uint32_t* done_ctr, int32_t max_ctas,
+                                void* stream) {
+  PP_CHECK_ARG(parts >= 1 && parts <= 3 && flag_row >= 0, "pp_replica_trans: bad parts / flag_row");
+  PP_CHECK_ARG(!flag_ptrs || (epoch && done_ctr), "pp_replica_trans: flags need epoch and done_ctr");
   PP_CHECK_ARG(w1_ptrs && w2_ptrs && mask, "pp_replica_trans: null pointer");
   PP_CHECK_ARG(E >= 1 && E <= kMaxItems && m >= 1 && E % m == 0 && (E / m) * E <= kMaxFlags &&
                    my_rank >= 0 && my_rank < E / m,
@@ -286,7 +310,8 @@ extern "C" int pp_replica_trans(void* const* w1_ptrs, void* const* w2_ptrs, cons
   PP_CHECK_ARG(((size_t)d_model * d_ff) % 8 == 0, "pp_replica_trans: bad sizes");
   const int grid = max_ctas > 0 ? max_ctas : 16;
   replica_trans_kernel<<<grid, 512, 0, as_stream(stream)>>>(w1_ptrs, w2_ptrs, mask, E, m, my_rank,
-                                                            (size_t)d_model * d_ff / 8);
+                                                            (size_t)d_model * d_ff / 8, parts, flag_ptrs,
+                                                            flag_row, epoch, done_ctr);
   PP_LAUNCH_CHECK();
   return PP_OK;
 }

@@ -36,7 +36,6 @@ from __future__ import annotations
 
 import ctypes
 import math
-import os
 
 import numpy as np
 import torch
@@ -160,7 +159,7 @@ class MoELayer(torch.nn.Module):
     def __init__(self, d_model: int, d_ff: int, num_experts: int, top_k: int, tokens: int,
                  group=None, planner: PlannerConfig | None = None, cluster=None, model=None,
                  capacity_rows: int | None = None, max_replicas: int | None = None,
-                 seed: int = 0, device=None, trans_ctas: int = 32, replica_engine: str = "copy",
+                 seed: int = 0, device=None, trans_ctas: int = 16, replica_engine: str = "copy",
                  policy: str | None = None, planning: str = "host", placement: str = "virtual",
                  refine_slots: bool = False, fused_a2a: bool = False) -> None:
         super().__init__()
@@ -275,9 +274,11 @@ class MoELayer(torch.nn.Module):
         self._pcfg = _device.planner_cfg(self.planner_cfg)
         self.plan_stream = torch.cuda.Stream(device=dev) if self.plan_enabled else None
         self.comm_stream = torch.cuda.Stream(device=dev) if D > 1 else None
-        self.trans_ctas = trans_ctas  # SM-engine Trans (overlaps route/layout/dispatch)
-        # where the forward issues Trans: "start" (before the gate GEMM) or "after_route"
-        self.trans_point = os.environ.get("PPMOE_TRANS_POINT", "start")
+        self.trans_ctas = trans_ctas  # SM-engine Trans pushes
+        # SM engine: True = Trans issued after barrier 1, overlapping FWD1/FWD2 on the home
+        # experts with the replica tiles gated on completion flags; False = issued at the
+        # start of the forward and awaited before barrier 1
+        self.trans_gate = True
         # SM-engine Agg runs beside the backward GEMMs on agg_ctas SMs (one CTA per SM);
         # those GEMMs launch their persistent grids on the remaining SMs so neither waits
         # for the other (pushes reach NVLink rate from ~16 CTAs)
@@ -320,7 +321,11 @@ class MoELayer(torch.nn.Module):
         # [m][D-1][W1|W2][d*f] fp32, the home sums them in rank order after a barrier on
         # the comm stream (its own barrier object: its epochs advance on that stream)
         self.agg_stage = None
+        self.trans_flags = None
         if D > 1 and self.replica_engine == "sm":
+            # Trans completion flags (slot r written by rank r) + the pushers' CTA counter
+            self.trans_flags = PeerBuffer((2, D), torch.int64, self.group, dev)  # rows: W1, W2
+            self._trans_ctr = torch.zeros(1, dtype=torch.int32, device=dev)
             self.agg_stage = PeerBuffer((self.m, D - 1, 2, d_ff * d_model), torch.float32, self.group, dev)
             self.comm_barrier = _Barrier(self.group, dev)
         self._plan_pending = None
@@ -383,8 +388,6 @@ class MoELayer(torch.nn.Module):
         _lib.call("pp_route_topk", x.data_ptr(), self.wg.data_ptr(), self.gate_bias.data_ptr(), T, d,
                   E, k, self.idx.data_ptr(), self.w.data_ptr(), self.probs.data_ptr(),
                   self.rank_in_chunk.data_ptr(), self.chunk_counts.data_ptr(), sp)
-        if self.trans_point == "after_route" and not self.top_m:
-            self.issue_trans()  # overlaps histogram, barrier, layout and dispatch, not the gate GEMM
         if self.world > 1:
             _lib.call("pp_slot_histogram", self.chunk_counts.data_ptr(), T, E, m, self.counts_buf.ptrs.data_ptr(),
                       self.world, self.rank * m, sp)
@@ -444,6 +447,11 @@ class MoELayer(torch.nn.Module):
             done = torch.cuda.Event()
             done.record(self.plan_stream)
         self._plan_pending = (done, mask_dev)
+
+    def _epoch_ptr(self) -> int:
+        """Device address of the main peer barrier's epoch counter: equal on every rank after
+        the same barrier, so it names this iteration's Trans completion."""
+        return self.barrier.sig.local.data_ptr() + 8 * self.world
 
     def _comb_local(self):
         return self.comb.local.data_ptr() if self.fused_a2a else None
@@ -545,9 +553,12 @@ class MoELayer(torch.nn.Module):
                 else:
                     self._copy_batch(self._trans_list, self.comm_stream)
             else:
-                _lib.call("pp_replica_trans", self.w1_arena.ptrs.data_ptr(), self.w2_arena.ptrs.data_ptr(),
-                          self.mask_cur.data_ptr(), self.E, self.m, self.rank, self.d, self.f, self.trans_ctas,
-                          _device.stream_ptr(self.comm_stream))
+                # W1 first (FWD1's replica tiles wait on flag row 0), then W2 (FWD2's, row 1)
+                for part, row in ((1, 0), (2, 1)):
+                    _lib.call("pp_replica_trans", self.w1_arena.ptrs.data_ptr(), self.w2_arena.ptrs.data_ptr(),
+                              self.mask_cur.data_ptr(), self.E, self.m, self.rank, self.d, self.f, part,
+                              self.trans_flags.ptrs.data_ptr(), row, self._epoch_ptr(),
+                              self._trans_ctr.data_ptr(), self.trans_ctas, _device.stream_ptr(self.comm_stream))
             self._trans_done = torch.cuda.Event()
             self._trans_done.record(self.comm_stream)
             self._log_side("SubTrans1", t0, self._side_event(self.comm_stream))
@@ -618,7 +629,7 @@ class MoELayer(torch.nn.Module):
             self._agg_done.record(self.comm_stream)
             self._log_side("SubAgg1" if parts == 2 else "SubAgg2", t0, self._side_event(self.comm_stream))
 
-    def _gemm(self, mode, a, b, c, c2=None, stream=None, num_sms=None, scatter=False):
+    def _gemm(self, mode, a, b, c, c2=None, stream=None, num_sms=None, scatter=False, gate=False):
         timing = self.gemm_timing
         if timing is not None:
             pool = self.gemm_event_pool
@@ -629,10 +640,17 @@ class MoELayer(torch.nn.Module):
                 e1 = torch.cuda.Event(enable_timing=True)
             e0.record()
         nsm = self.gemm_sms if num_sms is None else num_sms
-        if scatter:  # fused A2A epilogue: rows go to their source rank's comb buffer
-            _lib.call("pp_grouped_gemm_scatter", mode, a.data_ptr(), b.data_ptr(), self.groups.data_ptr(),
+        if gate or scatter:
+            # fused A2A epilogue (rows go to their source rank's comb buffer) and/or replica
+            # gate (replica tiles wait for the pushers' Trans completion flags: W1 row for
+            # FWD1, W2 row for FWD2)
+            flags = (self.trans_flags.local[0 if mode == _lib.PP_GEMM_FWD1 else 1].data_ptr() if gate else None)
+            _lib.call("pp_grouped_gemm_ex", mode, a.data_ptr(), b.data_ptr(), None if scatter else c.data_ptr(),
+                      c2.data_ptr() if c2 is not None else None, self.groups.data_ptr(),
                       self.num_groups.data_ptr(), self.max_groups, self.rows_cap, self.slots, self.d, self.f,
-                      self.origin.local.data_ptr(), self.comb.ptrs.data_ptr(), self.T * self.k, nsm,
+                      self.origin.local.data_ptr() if scatter else None,
+                      self.comb.ptrs.data_ptr() if scatter else None, self.T * self.k, flags,
+                      self._epoch_ptr() if gate else None, self.rank, self.world, self.m, nsm,
                       _device.stream_ptr(stream))
         else:
             _device.grouped_gemm(mode, a, b, c, c2, self.groups, self.num_groups, self.max_groups,
@@ -669,14 +687,14 @@ class MoELayer(torch.nn.Module):
         self.begin_iteration()
         if self.planning == "device" and self.world > 1:
             self._trans_issued = False  # the device-side plan may change every iteration
-        trans_done = None
-        if not self.top_m and self.trans_point == "start":  # plan known before routing
-            trans_done = self.issue_trans()  # no-op if a scheduler already issued it earlier
-        elif self.top_m:
+        if self.top_m:
             self._trans_issued = False  # top-m: this iteration's mask exists only after the histogram
+        # copy engine: host-derived copies start before routing and must land before FEC;
+        # SM engine: the home ranks push after barrier 1, overlapping FWD1 on the home experts,
+        # and each receiver's FWD1 gates only its replica tiles on the pushers' completion flags
+        sm_gate = self.replica_engine == "sm" and self.world > 1 and self.trans_gate
+        trans_done = None if sm_gate else self.issue_trans()  # no-op if a scheduler issued it earlier
         self._route_and_layout(x)
-        if self.top_m or self.trans_point == "after_route":
-            trans_done = self.issue_trans() if trans_done is None else trans_done
         self._mark("route_layout")
         self._launch_planner()  # [A2A | Plan(j+1)]: the search overlaps this block's dispatch
         _lib.call("pp_dispatch", x.data_ptr(), self.idx.data_ptr(), self.rank_in_chunk.data_ptr(),
@@ -689,16 +707,22 @@ class MoELayer(torch.nn.Module):
         if trans_done is not None:
             torch.cuda.current_stream().wait_event(trans_done)
         self._mark("trans_wait")
-        self.barrier()  # every rank's rows have landed (and replicas' params, via the next barrier use)
+        self.barrier()  # every rank's rows have landed
         self._mark("barrier1")
-        # a planner launched this iteration may still occupy an SM: the forward GEMMs leave
-        # one CTA pair's SMs free so their static persistent walk never waits on it
-        fwd_sms = None
-        if self._plan_inflight():
-            fwd_sms = max(2, (self.gemm_sms or _device.num_sms(self.device)) - 2)
-        self._gemm(_lib.PP_GEMM_FWD1, self.xp.local, self.w1_arena.local, self.pre, self.act, num_sms=fwd_sms)
+        if sm_gate:
+            trans_done = self.issue_trans()
+        total = self.gemm_sms or _device.num_sms(self.device)
+        reserve = self.trans_ctas if (sm_gate and trans_done is not None) else 0
+        if self._plan_inflight():  # the planner's CTA: keep its SM out of the static GEMM walk
+            reserve += 2
+        fwd_sms = max(2, (total - reserve) // 2 * 2) if reserve else None
+        gated = sm_gate and trans_done is not None
+        self._gemm(_lib.PP_GEMM_FWD1, self.xp.local, self.w1_arena.local, self.pre, self.act, num_sms=fwd_sms,
+                   gate=gated)
         self._gemm(_lib.PP_GEMM_FWD2, self.act, self.w2_arena.local, self.yp.local, num_sms=fwd_sms,
-                   scatter=self.fused_a2a)
+                   scatter=self.fused_a2a, gate=gated)
+        if gated:  # join the side stream (its pushes have landed: FWD2 waited for every flag)
+            torch.cuda.current_stream().wait_event(trans_done)
         self._mark("fwd_gemms")
         self.barrier()
         self._mark("barrier2")
@@ -832,7 +856,7 @@ class MoELayer(torch.nn.Module):
 
     def close(self) -> None:
         for b in (self.w1_arena, self.w2_arena, self.g1_arena, self.g2_arena, self.xp, self.yp, self.dyp, self.dxp,
-                  self.counts_buf, self.agg_stage, self.origin, self.comb):
+                  self.counts_buf, self.agg_stage, self.origin, self.comb, self.trans_flags):
             if b is not None:
                 b.close()
 

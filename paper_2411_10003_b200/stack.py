@@ -105,6 +105,8 @@ class MoEStack(torch.nn.Module):
     # ---- Algorithm 2 ---------------------------------------------------------
     def _schedule_trans(self, i: int, fec_time: float | None) -> None:
         m = self.moe[i]
+        if m.replica_engine != "copy":  # SM pushes are issued by the layer itself, gated into FWD1
+            return
         m.begin_iteration()
         if self.fnec_time is not None and fec_time is not None and m.trans_bytes() > 0:
             # bytes of Trans(i) the FNEC window of block i-1 can hide go first (SubTrans2)

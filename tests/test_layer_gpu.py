@@ -69,7 +69,7 @@ def run_layer(T, d, f, E, k, bias=None, seed=0, **kw):
 @pytest.mark.parametrize("fused", [False, True])
 @pytest.mark.parametrize("T,d,f,E,k", [(2048, 256, 512, 16, 2), (1024, 256, 256, 8, 1), (4096, 512, 768, 32, 2)])
 def test_layer_vs_oracle(T, d, f, E, k, fused):
-    """fused=True: FWD2 / DGRAD1 epilogues push rows to the pair's owner (pp_grouped_gemm_scatter)
+    """fused=True: FWD2 / DGRAD1 epilogues push rows to the pair's owner (pp_grouped_gemm_ex)
     and combine / dispatch-backward read them locally -- same contract, same tolerances."""
     bias = torch.log(torch.tensor([1.0 / (i + 1) ** 1.2 for i in range(E)]))  # Zipf skew
     bias = torch.round(bias * 4) / 4  # keep logits exact
