@@ -7,19 +7,22 @@ the reference's objects are its interface:
 
   forward  (per rank, stream-ordered, no host sync)
     K1 pp_route_topk       gate GEMM on tcgen05 + softmax/top-k/chunk ranks
-       pp_slot_histogram   this rank's virtual-slot rows of the LoadMatrix
-       all-gather          -> LoadMatrix [E x E] on every rank (tiny)
+       pp_slot_histogram   this rank's virtual-slot rows of the LoadMatrix, stored
+                           into every rank's copy (peer stores) + barrier
     K3 pp_dispatch_layout  receive layout from LoadMatrix + replica mask
-    K5 pp_replica_trans    (D>1) replicas pull the planned experts' params
     K3 pp_dispatch         permute + all-to-all in one kernel (peer stores)
        barrier
-    K4 FWD1, FWD2          grouped tcgen05 GEMMs (GeLU fused)
+    K5 pp_replica_trans    (D>1) copy engine: replicas pull before the barrier;
+                           SM engine: homes push W1/W2 + completion flags
+    K4 FWD1, FWD2          grouped tcgen05 GEMMs (GeLU fused); replica tiles gated
+                           on the Trans flags; FWD2 may push rows straight to the
+                           pairs' owners (fused A2A)
        barrier
-    K3 pp_combine          weighted gather back (peer loads)
-    K2 pp_plan_greedy      (D>1, side stream) plan for iteration j+1 on this
-                           iteration's LoadMatrix (plan_for_iteration rule)
-  backward mirrors it: combine_bwd (push), DGRAD2/WGRAD2/DGRAD1/WGRAD1,
-  dispatch_bwd (pull) + gate grads, K5 pp_replica_agg (D>1).
+    K3 pp_combine          weighted gather back (peer loads, or local after fused A2A)
+    K2 pp_plan_greedy /    (D>1, side stream) plan for iteration j+1 on this
+       pp_plan_physical    iteration's LoadMatrix (plan_for_iteration rule)
+  backward mirrors it: combine_bwd (push), WGRAD2/DGRAD2/WGRAD1/DGRAD1 (order
+  depends on the replica engine), dispatch_bwd + gate grads, K5 Agg (D>1).
 
 Virtual expert slots: with m = E/D experts per rank, each
 rank's T tokens are cut into m contiguous slots; slot v = rank*m + j is a
@@ -154,6 +157,16 @@ class MoELayer(torch.nn.Module):
       cluster/model: cost-model specs for the planner (default: default_specs).
       capacity_rows: receive-buffer rows (default: worst case world*tokens*k + E*128,
         i.e. no token is ever dropped).
+      max_replicas: replica weight slots per rank (default E - m: any plan fits).
+      replica_engine: "copy" (copy-engine peer copies, host-derived from the plan) or
+        "sm" (NVLink pushes from SMs, fully device-driven).
+      policy: None/"greedy"/"greedy-overlap" (Pro-Prophet), "vanilla", "top<m>".
+      planning: "host" (plan mask read back asynchronously) or "device" (plan stays on
+        the GPU; forces the SM engine; the whole step is CUDA-graph capturable at any N).
+      placement: "virtual" (reference search over E x E virtual slots, bit-exact) or
+        "physical" (E = m*D generalisation, pp_plan_physical).
+      refine_slots: physical placement only -- slot-level refinement of the plan.
+      fused_a2a: combine / dispatch backward fused into the FWD2 / DGRAD1 epilogues.
     """
 
     def __init__(self, d_model: int, d_ff: int, num_experts: int, top_k: int, tokens: int,
