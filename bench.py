@@ -324,6 +324,7 @@ def main() -> None:
                     help="planner cost model B (bytes/s; default layer.default_specs' 450e9)")
     ap.add_argument("--trans-ctas", type=int, default=None, help="SMs of the SM-engine Trans push")
     ap.add_argument("--agg-ctas", type=int, default=None, help="SMs of the SM-engine Agg push/reduce")
+    ap.add_argument("--agg-ctas-w2", type=int, default=None, help="SMs of the Agg's W2 half (beside DGRAD2/WGRAD1)")
     args = ap.parse_args()
     world_env = int(os.environ.get("WORLD_SIZE", "1"))
     # one bench workload for every N (weak scaling of the same per-GPU work): BASELINE
@@ -390,6 +391,8 @@ def main() -> None:
         layer.trans_ctas = args.trans_ctas
     if args.agg_ctas:
         layer.agg_ctas = args.agg_ctas
+    if args.agg_ctas_w2:
+        layer.agg_ctas_w2 = args.agg_ctas_w2
     if args.trans_gate is not None:
         layer.trans_gate = bool(args.trans_gate)
     layer.set_gate_bias(zipf_bias(E, 1.2, 0))

@@ -296,6 +296,7 @@ class MoELayer(torch.nn.Module):
         # those GEMMs launch their persistent grids on the remaining SMs so neither waits
         # for the other (pushes reach NVLink rate from ~16 CTAs)
         self.agg_ctas = 16
+        self.agg_ctas_w2 = 16  # the W2 half has DGRAD2 + WGRAD1 to hide under: may use fewer SMs
         if replica_engine not in ("copy", "sm"):
             raise ValidationError(f"replica_engine must be 'copy' or 'sm', got {replica_engine!r}")
         # 'copy': Trans/Agg pulls run on the copy engines (cudaMemcpyAsync over NVLink,
@@ -631,13 +632,14 @@ class MoELayer(torch.nn.Module):
                               _device.stream_ptr(self.comm_stream))
             else:
                 cs = _device.stream_ptr(self.comm_stream)
+                nctas = self.agg_ctas_w2 if parts == 2 else self.agg_ctas
                 _lib.call("pp_replica_agg", self.g1_arena.ptrs.data_ptr(), self.g2_arena.ptrs.data_ptr(),
                           self.agg_stage.ptrs.data_ptr(), self.mask_cur.data_ptr(), self.E, self.m, self.rank,
-                          self.d, self.f, parts, self.agg_ctas, cs)
+                          self.d, self.f, parts, nctas, cs)
                 self.comm_barrier(self.comm_stream)  # every replica's grads have landed here
                 _lib.call("pp_replica_agg_reduce", self.g1_arena.local.data_ptr(), self.g2_arena.local.data_ptr(),
                           self.agg_stage.local.data_ptr(), self.mask_cur.data_ptr(), self.E, self.m, self.rank,
-                          self.d, self.f, parts, self.agg_ctas, cs)
+                          self.d, self.f, parts, nctas, cs)
             self._agg_done = torch.cuda.Event()
             self._agg_done.record(self.comm_stream)
             self._log_side("SubAgg1" if parts == 2 else "SubAgg2", t0, self._side_event(self.comm_stream))
@@ -763,11 +765,12 @@ class MoELayer(torch.nn.Module):
             # agg_ctas SMs to the push/reduce kernels (SubAgg | BEC)
             total = self.gemm_sms or _device.num_sms(self.device)
             side_sms = max(2, (total - self.agg_ctas) // 2 * 2)
+            side_sms_w2 = max(2, (total - self.agg_ctas_w2) // 2 * 2)
             self._gemm(_lib.PP_GEMM_WGRAD2, self.dyp.local, self.act, self.g2_arena.local)
             self._issue_agg(parts=2)
             self._gemm(_lib.PP_GEMM_DGRAD2, self.dyp.local, self.w2_arena.local, self.pre, self.pre,
-                       num_sms=side_sms)
-            self._gemm(_lib.PP_GEMM_WGRAD1, self.pre, self.xp.local, self.g1_arena.local, num_sms=side_sms)
+                       num_sms=side_sms_w2)
+            self._gemm(_lib.PP_GEMM_WGRAD1, self.pre, self.xp.local, self.g1_arena.local, num_sms=side_sms_w2)
             self._issue_agg(parts=1)
             self._gemm(_lib.PP_GEMM_DGRAD1, self.pre, self.w1_arena.local, self.dxp.local, num_sms=side_sms,
                        scatter=self.fused_a2a)
