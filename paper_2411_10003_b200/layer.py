@@ -384,17 +384,18 @@ class MoELayer(torch.nn.Module):
             ev.record()
             self.phase_log.append((name, ev))
 
-    def phase_breakdown(self) -> dict:
-        """Average ms per phase over the recorded steps (phase = time since the
-        previous mark on this rank's stream)."""
-        out, steps, prev = {}, 0, None
+    def phase_breakdown(self, stat: str = "median") -> dict:
+        """Per-phase ms over the recorded steps (phase = time since the previous mark on
+        this rank's stream); the median by default, so a host hiccup in one eager step
+        (allocator, GC) does not masquerade as a slow phase."""
+        per, prev = {}, None
         for name, ev in self.phase_log or []:
-            if name == "fwd_start":
-                steps += 1
-            elif prev is not None:
-                out[name] = out.get(name, 0.0) + prev.elapsed_time(ev)
+            if name != "fwd_start" and prev is not None:
+                per.setdefault(name, []).append(prev.elapsed_time(ev))
             prev = ev
-        return {k: v / max(steps, 1) for k, v in out.items()}
+        if stat == "mean":
+            return {k: sum(v) / len(v) for k, v in per.items()}
+        return {k: float(np.median(v)) for k, v in per.items()}
 
     def _route_and_layout(self, x: torch.Tensor) -> None:
         sp = self._sp()
