@@ -819,7 +819,8 @@ class MoELayer(torch.nn.Module):
     def forward(self, x: torch.Tensor) -> torch.Tensor:
         return _MoEFunction.apply(x, self)
 
-    def make_graphed_step(self, x: torch.Tensor, dy: torch.Tensor, with_loss: bool = False) -> "GraphedStep":
+    def make_graphed_step(self, x: torch.Tensor, dy: torch.Tensor, with_loss: bool = False,
+                          gemm_events: bool = False) -> "GraphedStep":
         """Capture one forward + backward into a CUDA graph (host cost per step
         drops to one graph launch).  ``x`` / ``dy`` become the static input
         buffers: copy new data into them, call the returned object, read
@@ -830,7 +831,7 @@ class MoELayer(torch.nn.Module):
             raise ValidationError("make_graphed_step at D > 1 needs planning='device'")
         if self.plan_enabled and self.world > 1 and self.planner_cfg.reuse_interval != 1:
             raise ValidationError("make_graphed_step: the captured step re-plans every iteration (reuse_interval=1)")
-        return GraphedStep(self, x, dy, with_loss)
+        return GraphedStep(self, x, dy, with_loss, gemm_events)
 
     # ---- introspection (LoadMatrix / placement of the last call) -------------
     def last_load_matrix(self) -> LoadMatrix:
@@ -896,13 +897,16 @@ class _MoEFunction(torch.autograd.Function):
 class GraphedStep:
     """A captured fwd+bwd of one MoELayer over static input buffers."""
 
-    def __init__(self, layer: MoELayer, x: torch.Tensor, dy: torch.Tensor, with_loss: bool = False) -> None:
+    def __init__(self, layer: MoELayer, x: torch.Tensor, dy: torch.Tensor, with_loss: bool = False,
+                 gemm_events: bool = False) -> None:
         """with_loss: also compute loss = sum(y * dy) in fp32 inside the graph (a
         linear probe whose gradient w.r.t. y is exactly dy), so a training loop can
-        read back one scalar per step."""
+        read back one scalar per step.  gemm_events: capture a timing-event pair
+        around each grouped GEMM (event-record nodes); after a replay,
+        ``gemm_times()`` gives that replay's per-GEMM durations."""
         self.layer, self.x, self.dy = layer, x, dy
-        saved_timing, saved_phase = layer.gemm_timing, layer.phase_log
-        layer.gemm_timing = layer.phase_log = None  # timing events cannot live in the graph
+        saved_timing, saved_phase, saved_pool = layer.gemm_timing, layer.phase_log, layer.gemm_event_pool
+        layer.gemm_timing = layer.phase_log = None  # host-side timing lists cannot live in the graph
         side = torch.cuda.Stream(device=layer.device)
         side.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(side):  # warm the allocator / lazy state outside capture
@@ -911,11 +915,21 @@ class GraphedStep:
                 layer.backward_raw(x, dy)
         torch.cuda.current_stream().wait_stream(side)
         self.graph = torch.cuda.CUDAGraph()
+        self.gemm_events = None
+        if gemm_events:  # external events: recorded as graph nodes on every replay
+            layer.gemm_timing = []
+            layer.gemm_event_pool = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(32)]
         with torch.cuda.graph(self.graph):
             self.y = layer.forward_raw(x)
             self.loss = layer.probe_loss(self.y, dy) if with_loss else None
             self.dx = layer.backward_raw(x, dy)
-        layer.gemm_timing, layer.phase_log = saved_timing, saved_phase
+        if gemm_events:
+            self.gemm_events = layer.gemm_timing
+        layer.gemm_timing, layer.phase_log, layer.gemm_event_pool = saved_timing, saved_phase, saved_pool
+
+    def gemm_times(self) -> list:
+        """(mode, ms) of each grouped GEMM in the most recent replay (call after it finished)."""
+        return [(mode, e0.elapsed_time(e1)) for mode, e0, e1 in self.gemm_events or []]
 
     def __call__(self):
         self.graph.replay()
