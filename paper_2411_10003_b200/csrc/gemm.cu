@@ -37,6 +37,7 @@ constexpr int BM = 128;
 constexpr int BK = 64;  // 64 bf16 = 128 B = one SWIZZLE_128B span
 constexpr int kThreads = 384;  // 4 non-epilogue warps + up to 8 epilogue warps
 constexpr int kMaxGroups = 256;
+constexpr int kTraceSteps = 1024;
 
 
 enum Epi { EPI_BF16 = 0, EPI_GELU = 1, EPI_DGELU = 2, EPI_F32 = 3, EPI_ROUTE = 4, EPI_BF16_ADD = 5, EPI_F32_ATOMIC = 6 };
@@ -83,6 +84,9 @@ struct GemmParams {
   int split_rows;   // with single_rows: split-K chunk size (one implicit group per chunk)
   int m_real;       // EPI_F32_ATOMIC: rows of the output that exist (< M_fixed)
   unsigned long long* dbg;  // optional per-CTA wait-cycle counters (PPMOE_GEMM_DEBUG)
+  // PPMOE_GEMM_DEBUG=2: per-k-step globaltimer trace of CTAs 0..3 (first kTraceSteps steps):
+  // [cta][step][0..1] producer before/after the empty wait, [2..3] MMA before/after the full wait
+  unsigned long long* trace;
   // fused combine / dispatch-backward (EPI_BF16 only): output row r goes to pair
   // origin[r] = src_rank * pairs_per_rank + t*k + j, i.e. row (t*k+j) of scatter_ptrs[src_rank]
   // (peer memory over NVLink), instead of this rank's receive-layout buffer; origin < 0
@@ -460,6 +464,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       bool gate_pending = p.gate_flags != nullptr;
+      int pstep = 0;  // trace index
       Tile tl;
       for (int it = 0, t = tile_of(0); t < total_tiles; t = tile_of(++it)) {
         if (!decode_tile<BN, CG>(t, sched, p, tl, cta_rank)) break;
@@ -479,7 +484,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           gate_pending = false;
         }
         for (int kb = 0; kb < tl.num_kb; ++kb) {
+          const bool tr = p.trace && blockIdx.x < 4 && pstep < kTraceSteps;
+          if (tr) p.trace[((size_t)blockIdx.x * kTraceSteps + pstep) * 4 + 0] = globaltimer_ns();
           mbar_wait(&empty_bar[stage], phase ^ 1);
+          if (tr) p.trace[((size_t)blockIdx.x * kTraceSteps + pstep) * 4 + 1] = globaltimer_ns();
+          ++pstep;
           uint8_t* sa = smem + stage * STAGE_BYTES;
           uint8_t* sb = sa + A_BYTES;
           const int k0 = kb * BK;
@@ -521,6 +530,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 1 && cta_rank == 0) {
     // ================= MMA issuer (leader CTA of a pair) =================
     long long wait_tempty = 0, wait_full = 0, t_start = p.dbg ? clock64() : 0;
+    int mstep = 0;  // trace index
     int stage = 0;
     uint32_t phase = 0;
     int acc = 0;
@@ -541,7 +551,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       for (int kb = 0; kb < tl.num_kb; ++kb) {
         long long w1 = p.dbg ? clock64() : 0;
+        const bool tr = p.trace && blockIdx.x < 4 && mstep < kTraceSteps && lane == 0;
+        if (tr) p.trace[((size_t)blockIdx.x * kTraceSteps + mstep) * 4 + 2] = globaltimer_ns();
         mbar_wait(&full_bar[stage], phase);
+        if (tr) p.trace[((size_t)blockIdx.x * kTraceSteps + mstep) * 4 + 3] = globaltimer_ns();
+        ++mstep;
         if (p.dbg) wait_full += clock64() - w1;
         tc_fence_after();
         if (lane == 0) {
@@ -975,7 +989,8 @@ using namespace pp;
 // cycle counters [cta][total, wait_tempty, wait_full, -] into host memory.
 static unsigned long long* g_dbg_buf = nullptr;
 extern "C" int pp_gemm_debug_read(unsigned long long* host, int32_t ctas) {
-  PP_CHECK_ARG(g_dbg_buf && host && ctas > 0 && ctas <= 1024, "pp_gemm_debug_read: PPMOE_GEMM_DEBUG not set");
+  PP_CHECK_ARG(g_dbg_buf && host && ctas > 0 && ctas <= 1024 + kTraceSteps * 4,
+               "pp_gemm_debug_read: PPMOE_GEMM_DEBUG not set");
   PP_CUDA_TRY(cudaMemcpy(host, g_dbg_buf, (size_t)ctas * 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
   return PP_OK;
 }
@@ -1048,9 +1063,12 @@ static int grouped_gemm_impl(int32_t mode, const void* a, const void* b, void* c
   const int R = rows_capacity, S = num_slots, dm = d_model, df = d_ff;
   CUtensorMap ta, tb, tc, tc2;
   GemmParams p{};
-  static const bool dbg_on = getenv("PPMOE_GEMM_DEBUG") != nullptr;
-  if (dbg_on && !g_dbg_buf) cudaMalloc(&g_dbg_buf, 4 * 1024 * sizeof(unsigned long long));
-  p.dbg = dbg_on ? g_dbg_buf : nullptr;
+  static const int dbg_level = getenv("PPMOE_GEMM_DEBUG") ? atoi(getenv("PPMOE_GEMM_DEBUG")) : 0;
+  // [1024 CTAs][4] counters, then (level 2) the [4][kTraceSteps][4] timestamp trace
+  if (dbg_level && !g_dbg_buf)
+    cudaMalloc(&g_dbg_buf, (4 * 1024 + 4 * kTraceSteps * 4) * sizeof(unsigned long long));
+  p.dbg = dbg_level ? g_dbg_buf : nullptr;
+  p.trace = dbg_level >= 2 ? g_dbg_buf + 4 * 1024 : nullptr;
   p.groups = groups;
   p.num_groups = num_groups;
   p.max_groups = max_groups;
