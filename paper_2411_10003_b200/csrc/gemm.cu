@@ -347,8 +347,17 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr uint32_t A_BYTES = BM * BK * 2;
   constexpr uint32_t B_BYTES = BNC * BK * 2;
   constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
-  constexpr uint32_t TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
-  constexpr uint32_t IDESC = make_idesc<BN, A_MN, B_MN, BM * CG>();  // pair: M = 256
+  // BN = 512 (CTA pairs, long-K modes): a 256 x 512 tile is two N = 256 MMAs per K step that
+  // share the A operand -- 25 % fewer operand bytes per FLOP for a feed-bound mainloop -- and
+  // fills all 512 TMEM columns, so the accumulator is single-buffered
+  constexpr int NSUB = BN > 256 ? 2 : 1;      // MMAs per K step (N halves)
+  constexpr int BN_MMA = BN / NSUB;
+  constexpr int NACC = (2 * BN <= 512) ? 2 : 1;  // TMEM accumulator buffers
+  constexpr uint32_t TMEM_COLS = (NACC * BN <= 32) ? 32 : (NACC * BN <= 64) ? 64 : (NACC * BN <= 128) ? 128
+                                 : (NACC * BN <= 256) ? 256 : 512;
+  static_assert(NACC * BN <= 512, "TMEM holds 512 fp32 columns");
+  static_assert(NSUB == 1 || CG == 2, "BN = 512 tiles are CTA-pair only");
+  constexpr uint32_t IDESC = make_idesc<BN_MMA, A_MN, B_MN, BM * CG>();  // pair: M = 256
   // epilogue warps: two per TMEM lane quarter (each takes half of the columns),
   // except the route epilogue which needs a whole logits row per thread
   constexpr int EPI_WARPS = (EPI == EPI_ROUTE) ? 4 : (BN >= 128 ? 8 : 4);
@@ -492,7 +501,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           uint8_t* sa = smem + stage * STAGE_BYTES;
           uint8_t* sb = sa + A_BYTES;
           const int k0 = kb * BK;
-          const int nb = tl.n0 + BNC * cta_rank;  // this CTA's half of the B columns
+          // B columns staged by this CTA: for each N half s (one MMA), the pair splits the
+          // half's BN_MMA columns, this CTA taking [s*BN_MMA + rank*BNC/NSUB, +BNC/NSUB)
+          auto bcol = [&](int j) {  // tile-relative column of this CTA's staged B row/col j
+            constexpr int H = BNC / NSUB;
+            return tl.n0 + (j / H) * BN_MMA + cta_rank * H + (j % H);
+          };
           // all TMA of the stage completes on the leader CTA's full barrier
           const uint32_t bar_c = CG == 2 ? mapa_shared(smem_u32(&full_bar[stage]), 0) : 0u;
           auto load = [&](void* dst, const CUtensorMap* m, int c0, int c1) {
@@ -510,15 +524,17 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int i = 0; i < BM / 64; ++i) load(sa + i * 8192, &tmA, tl.m0 + 64 * i, tl.row_off + k0);
           }
-          if constexpr (!B_MN) {
-            load(sb, &tmB, k0, tl.wslot * p.N + nb);
+          if constexpr (!B_MN) {  // K-major B: one box of BNC/NSUB rows per N half
+#pragma unroll
+            for (int s = 0; s < NSUB; ++s)
+              load(sb + s * (BNC / NSUB) * 128, &tmB, k0, tl.wslot * p.N + bcol(s * (BNC / NSUB)));
           } else if (p.ragged_k) {  // wgrad: B rows are the group's token rows
 #pragma unroll
-            for (int i = 0; i < BNC / 64; ++i) load(sb + i * 8192, &tmB, nb + 64 * i, tl.row_off + k0);
+            for (int i = 0; i < BNC / 64; ++i) load(sb + i * 8192, &tmB, bcol(64 * i), tl.row_off + k0);
           } else {  // dgrad: B = W[slot] stored [K rows][N cols]
 #pragma unroll
             for (int i = 0; i < BNC / 64; ++i)
-              load(sb + i * 8192, &tmB, nb + 64 * i, tl.wslot * p.K_fixed + k0);
+              load(sb + i * 8192, &tmB, bcol(64 * i), tl.wslot * p.K_fixed + k0);
           }
           if (++stage == STAGES) {
             stage = 0;
@@ -565,10 +581,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int kk = 0; kk < BK / 16; ++kk) {
             const uint64_t ad = A_MN ? make_sdesc(sa + kk * 2048, 8192, 1024)
                                      : make_sdesc(sa + kk * 32, 16, 1024);
-            const uint64_t bd = B_MN ? make_sdesc(sb + kk * 2048, 8192, 1024)
-                                     : make_sdesc(sb + kk * 32, 16, 1024);
-            if constexpr (CG == 2) tc_mma_bf16_2sm(d_tmem, ad, bd, IDESC, (kb | kk) != 0);
-            else tc_mma_bf16(d_tmem, ad, bd, IDESC, (kb | kk) != 0);
+#pragma unroll
+            for (int s = 0; s < NSUB; ++s) {
+              // N half s: this CTA's B rows [s*BNC/NSUB, +BNC/NSUB) (K-major: 128 B per row;
+              // MN-major: 8 KB per 64-column chunk) into TMEM columns [s*BN_MMA, +BN_MMA)
+              const uint32_t sbs = sb + s * (B_MN ? (BNC / NSUB / 64) * 8192 : (BNC / NSUB) * 128);
+              const uint64_t bd = B_MN ? make_sdesc(sbs + kk * 2048, 8192, 1024)
+                                       : make_sdesc(sbs + kk * 32, 16, 1024);
+              if constexpr (CG == 2) tc_mma_bf16_2sm(d_tmem + s * BN_MMA, ad, bd, IDESC, (kb | kk) != 0);
+              else tc_mma_bf16(d_tmem + s * BN_MMA, ad, bd, IDESC, (kb | kk) != 0);
+            }
           }
           if constexpr (CG == 2) {
             tc_commit_2sm(&empty_bar[stage], 0x3);
@@ -584,7 +606,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           phase ^= 1;
         }
       }
-      if (++acc == 2) {
+      if (++acc == NACC) {
         acc = 0;
         acc_phase ^= 1;
       }
@@ -754,7 +776,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (tl.active) epilogue_chunk<EPI>(cur, p, tl, r, c, pre_v, stage, sbuf, &tmC, &tmC2, lane);
         }
       }
-      if (++acc == 2) {
+      if (++acc == NACC) {
         acc = 0;
         acc_phase ^= 1;
       }
@@ -1091,6 +1113,10 @@ static int grouped_gemm_impl(int32_t mode, const void* a, const void* b, void* c
   // PPMOE_GEMM_CTA_PAIR=0; a pair stages 16 KB of A + 16 KB of B per CTA and stage
   const bool pair = use_cta_pair();
   const uint32_t bkb = pair ? 128 : 256;  // K-major B rows staged per CTA
+  // 256 x 512 pair tiles for the long-K modes when N allows (PPMOE_GEMM_WIDE=0 disables)
+  static const bool wide_env = !getenv("PPMOE_GEMM_WIDE") || atoi(getenv("PPMOE_GEMM_WIDE")) != 0;
+  const bool wide_dm = pair && wide_env && dm % 512 == 0, wide_df = pair && wide_env && df % 512 == 0;
+#define PP_LAUNCH_W(EPI_, AMN_, BMN_, S_, ...) launch<512, AMN_, BMN_, EPI_, S_, 2>(ta, tb, p, grid, st, ##__VA_ARGS__)
 #define PP_LAUNCH(EPI_, AMN_, BMN_, S1_, S2_, ...)                                          \
   (pair ? launch<256, AMN_, BMN_, EPI_, S2_, 2>(ta, tb, p, grid, st, ##__VA_ARGS__)         \
         : launch<256, AMN_, BMN_, EPI_, S1_, 1>(ta, tb, p, grid, st, ##__VA_ARGS__))
@@ -1102,9 +1128,12 @@ static int grouped_gemm_impl(int32_t mode, const void* a, const void* b, void* c
       if ((rc = make_out_tmap(&tc, c, df, R)) || (rc = make_out_tmap(&tc2, c2, df, R))) return rc;
       return PP_LAUNCH(EPI_GELU, false, false, 4, 5, &tc, &tc2);
     case PP_GEMM_FWD2:
-      if ((rc = make_tmap(&ta, a, df, R, BK, BM)) || (rc = make_tmap(&tb, b, df, (uint64_t)S * dm, BK, bkb))) return rc;
+      if ((rc = make_tmap(&ta, a, df, R, BK, BM)) ||
+          (rc = make_tmap(&tb, b, df, (uint64_t)S * dm, BK, bkb)))
+        return rc;
       p.N = dm; p.K_fixed = df;
       if ((rc = make_out_tmap(&tc, c, dm, R))) return rc;
+      if (wide_dm) return PP_LAUNCH_W(EPI_BF16, false, false, 4, &tc);
       return PP_LAUNCH(EPI_BF16, false, false, 4, 6, &tc);
     case PP_GEMM_DGRAD2:
       PP_CHECK_ARG(c2, "DGRAD2 needs the pre-activation");
@@ -1117,16 +1146,19 @@ static int grouped_gemm_impl(int32_t mode, const void* a, const void* b, void* c
       if ((rc = make_tmap(&ta, a, df, R, BK, BM)) || (rc = make_tmap(&tb, b, dm, (uint64_t)S * df, 64, BK))) return rc;
       p.N = dm; p.K_fixed = df;
       if ((rc = make_out_tmap(&tc, c, dm, R))) return rc;
+      if (wide_dm) return PP_LAUNCH_W(EPI_BF16, false, true, 4, &tc);
       return PP_LAUNCH(EPI_BF16, false, true, 4, 6, &tc);
     case PP_GEMM_WGRAD2:
       if ((rc = make_tmap(&ta, a, dm, R, 64, BK)) || (rc = make_tmap(&tb, b, df, R, 64, BK))) return rc;
       p.M_fixed = dm; p.N = df; p.ragged_k = 1;
       if ((rc = make_out_tmap_f32(&tc, c, df, (uint64_t)S * dm))) return rc;
+      if (wide_df) return PP_LAUNCH_W(EPI_F32, true, true, 3, &tc);
       return PP_LAUNCH(EPI_F32, true, true, 3, 5, &tc);
     case PP_GEMM_WGRAD1:
       if ((rc = make_tmap(&ta, a, df, R, 64, BK)) || (rc = make_tmap(&tb, b, dm, R, 64, BK))) return rc;
       p.M_fixed = df; p.N = dm; p.ragged_k = 1;
       if ((rc = make_out_tmap_f32(&tc, c, dm, (uint64_t)S * df))) return rc;
+      if (wide_dm) return PP_LAUNCH_W(EPI_F32, true, true, 3, &tc);
       return PP_LAUNCH(EPI_F32, true, true, 3, 5, &tc);
     case PP_GEMM_PLAIN:
       if ((rc = make_tmap(&ta, a, dm, R, BK, BM)) || (rc = make_tmap(&tb, b, dm, (uint64_t)S * df, BK, bkb))) return rc;
@@ -1134,6 +1166,7 @@ static int grouped_gemm_impl(int32_t mode, const void* a, const void* b, void* c
       if ((rc = make_out_tmap(&tc, c, df, R))) return rc;
       return PP_LAUNCH(EPI_BF16, false, false, 4, 6, &tc);
 #undef PP_LAUNCH
+#undef PP_LAUNCH_W
     default:
       return fail(PP_EINVAL, "pp_grouped_gemm: unknown mode %d", mode);
   }

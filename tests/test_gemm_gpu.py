@@ -55,8 +55,11 @@ def make_case(rows, d, f, slots=None, seed=0):
     return dict(groups=groups, ng=ng, cap=cap, X=X, segs=segs, W1=W1, W2=W2, G=G, slots=slots)
 
 
-@pytest.mark.parametrize("rows,d,f", [([300, 0, 128, 77, 1], 256, 512), ([2048, 1000], 512, 1024), ([130] * 6, 1024, 768)])
+@pytest.mark.parametrize("rows,d,f", [([300, 0, 128, 77, 1], 256, 512), ([2048, 1000], 512, 1024), ([130] * 6, 1024, 768),
+                                      ([2048, 1000, 4100, 0, 129], 1024, 4096)])
 def test_fwd_bwd_modes(rows, d, f):
+    """All six modes vs fp32 torch.  N % 512 == 0 runs the 256 x 512 CTA-pair tiles (FWD2 / DGRAD1 /
+    WGRAD1 at d = 512, 1024; WGRAD2 at f = 512, 1024, 4096), the rest the 256 x 256 ones."""
     c = make_case(rows, d, f)
     dev = torch.device("cuda")
     cap, G, S = c["cap"], c["G"], c["slots"]
