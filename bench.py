@@ -316,8 +316,9 @@ def main() -> None:
                          "search when E == D) or over E x E virtual expert slots (the reference search verbatim)")
     ap.add_argument("--refine-slots", type=int, default=1,
                     help="physical placement: slot-level refinement of the plan (1/0; beyond the paper)")
-    ap.add_argument("--fused-a2a", type=int, default=None,
-                    help="combine / dispatch-backward fused into the FWD2 / DGRAD1 epilogues (1/0; default: N > 1)")
+    ap.add_argument("--fused-a2a", type=int, default=0,
+                    help="combine / dispatch-backward fused into the FWD2 / DGRAD1 epilogues (1/0; default 0: with "
+                         "the 256x512 tiles the unfused path measured 3 % faster at 2 and 4 GPUs)")
     ap.add_argument("--trans-gate", type=int, default=None,
                     help="SM-engine Trans overlapped with FWD1 via per-tile gates (1) or awaited before it (0)")
     ap.add_argument("--avg-bandwidth", type=float, default=None,
@@ -386,7 +387,7 @@ def main() -> None:
     layer = pp.MoELayer(d, f, E, k, tokens=T, group=group, planner=planner, seed=0, policy=args.policy, **specs,
                         planning=planning, placement=args.placement if world > 1 else "virtual",
                         refine_slots=bool(args.refine_slots) and args.placement == "physical" and world > 1,
-                        fused_a2a=(world > 1) if args.fused_a2a is None else bool(args.fused_a2a))
+                        fused_a2a=bool(args.fused_a2a))
     if args.trans_ctas:
         layer.trans_ctas = args.trans_ctas
     if args.agg_ctas:

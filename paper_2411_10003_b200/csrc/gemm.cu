@@ -1115,7 +1115,9 @@ static int grouped_gemm_impl(int32_t mode, const void* a, const void* b, void* c
   const uint32_t bkb = pair ? 128 : 256;  // K-major B rows staged per CTA
   // 256 x 512 pair tiles for the long-K modes when N allows (PPMOE_GEMM_WIDE=0 disables)
   static const bool wide_env = !getenv("PPMOE_GEMM_WIDE") || atoi(getenv("PPMOE_GEMM_WIDE")) != 0;
-  const bool wide_dm = pair && wide_env && dm % 512 == 0, wide_df = pair && wide_env && df % 512 == 0;
+  // (not with the fused-A2A scatter epilogue: its per-row copies are heavier, and the single-buffered
+  // 512-column accumulator would expose them)
+  const bool wide_dm = pair && wide_env && !sc && dm % 512 == 0, wide_df = pair && wide_env && !sc && df % 512 == 0;
 #define PP_LAUNCH_W(EPI_, AMN_, BMN_, S_, ...) launch<512, AMN_, BMN_, EPI_, S_, 2>(ta, tb, p, grid, st, ##__VA_ARGS__)
 #define PP_LAUNCH(EPI_, AMN_, BMN_, S1_, S2_, ...)                                          \
   (pair ? launch<256, AMN_, BMN_, EPI_, S2_, 2>(ta, tb, p, grid, st, ##__VA_ARGS__)         \
