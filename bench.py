@@ -326,6 +326,8 @@ def main() -> None:
     ap.add_argument("--trans-ctas", type=int, default=None, help="SMs of the SM-engine Trans push")
     ap.add_argument("--agg-ctas", type=int, default=None, help="SMs of the SM-engine Agg push/reduce")
     ap.add_argument("--agg-ctas-w2", type=int, default=None, help="SMs of the Agg's W2 half (beside DGRAD2/WGRAD1)")
+    ap.add_argument("--res-per-replica", type=int, default=None,
+                    help="SMs the GEMMs leave to Trans/Agg per replica sent or received (device-adaptive)")
     args = ap.parse_args()
     world_env = int(os.environ.get("WORLD_SIZE", "1"))
     # one bench workload for every N (weak scaling of the same per-GPU work): BASELINE
@@ -394,6 +396,8 @@ def main() -> None:
         layer.agg_ctas = args.agg_ctas
     if args.agg_ctas_w2:
         layer.agg_ctas_w2 = args.agg_ctas_w2
+    if args.res_per_replica:
+        layer.res_per_replica = args.res_per_replica
     if args.trans_gate is not None:
         layer.trans_gate = bool(args.trans_gate)
     layer.set_gate_bias(zipf_bias(E, 1.2, 0))

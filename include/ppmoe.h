@@ -154,13 +154,16 @@ typedef struct pp_group {
  *   rep_slot   [D][E] int32 weight slot of replica expert e on rank r (-1 if
  *              none; nullable).
  * counts_from_chunks (D == 1 only): fill `counts` from the chunk counts here,
- * replacing pp_slot_histogram + barrier. */
+ * replacing pp_slot_histogram + barrier.  replica_stats (nullable, int32[2]):
+ * [0] replicas of this rank's home experts held elsewhere, [1] replicas this
+ * rank holds -- the device-side volume hints for SM reservation around Trans/Agg. */
 int pp_dispatch_layout(int64_t* counts, const uint8_t* mask, const int32_t* chunk_counts,
                        int32_t D, int32_t m, int32_t E, int32_t T, int32_t my_rank,
                        int32_t max_groups, int32_t rows_capacity,
                        int32_t* chunk_base, int32_t* slot_dest, pp_group* groups,
                        int32_t* num_groups, int32_t* total_rows, int32_t* seg_start,
-                       int32_t* rep_slot, int32_t counts_from_chunks, void* stream);
+                       int32_t* rep_slot, int32_t counts_from_chunks, int32_t* replica_stats,
+                       void* stream);
 
 /* Permute + all-to-all in one kernel: row of token t goes to rank
  * slot_dest[t/(T/m)][e] at row chunk_base[t/128][e] + rank[t][j] of that
@@ -247,13 +250,21 @@ int pp_dot_bf16(const void* a, const void* b, int64_t n, float* partial, float* 
  *   home groups (wslot < first_replica_slot) are scheduled first; before the
  *   first replica tile's loads the TMA producer waits until gate_flags[r] >=
  *   *gate_epoch for every peer r != my_rank (the completion flags of
- *   pp_replica_trans; gate_flags = this rank's [D] uint64 row).  20 s -> trap. */
+ *   pp_replica_trans; gate_flags = this rank's [D] uint64 row).  20 s -> trap.
+ * Device-adaptive SM reservation (res_stats != NULL, pp_dispatch_layout's
+ *   replica_stats): the persistent walk leaves clamp(res_per_unit * (stats[0] +
+ *   (res_both ? stats[1] : 0)), res_lo, res_hi) of the num_sms SMs to concurrent
+ *   side kernels sized by this iteration's replica volume; the other CTAs exit at
+ *   once.  Keep res_lo >= 2 when gating, so this rank's own Trans kernel (whose
+ *   completion signal the peers wait on) can always run. */
 int pp_grouped_gemm_ex(int32_t mode, const void* a, const void* b, void* c, void* c2,
                        const pp_group* groups, const int32_t* num_groups, int32_t max_groups,
                        int32_t rows_capacity, int32_t num_slots, int32_t d_model, int32_t d_ff,
                        const int32_t* origin, void* const* scatter_ptrs, int32_t pairs_per_rank,
                        const uint64_t* gate_flags, const uint64_t* gate_epoch, int32_t my_rank,
-                       int32_t D, int32_t first_replica_slot, int32_t num_sms, void* stream);
+                       int32_t D, int32_t first_replica_slot, const int32_t* res_stats,
+                       int32_t res_both, int32_t res_per_unit, int32_t res_lo, int32_t res_hi,
+                       int32_t num_sms, void* stream);
 
 /* ---- replica Trans / Agg over peer memory (K5) --------------------------- */
 /* Trans (home side, SM engine): push each of this rank's home experts' W1/W2

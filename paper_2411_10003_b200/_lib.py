@@ -68,14 +68,14 @@ SIGNATURES = {
     "pp_top_m_mask": [P, I, I, I, P, P, P],
     "pp_route_topk": [P, P, P, I, I, I, I, P, P, P, P, P, P],
     "pp_slot_histogram": [P, I, I, I, P, I, I, P],
-    "pp_dispatch_layout": [P, P, P, I, I, I, I, I, I, I, P, P, P, P, P, P, P, I, P],
+    "pp_dispatch_layout": [P, P, P, I, I, I, I, I, I, I, P, P, P, P, P, P, P, I, P, P],
     "pp_dispatch": [P, P, P, P, P, I, I, I, I, I, P, P, P, P, I, P, P, P, I, P],
     "pp_combine": [P, P, P, P, I, I, I, P, P, P],
     "pp_combine_bwd": [P, P, P, P, P, P, P, P, P, I, I, I, I, P, P, P],
     "pp_dispatch_bwd": [P, P, P, P, P, P, I, I, I, I, I, P, P, P, ctypes.c_int64, P, P],
     "pp_gate_bwd": [P, P, P, I, I, I, I, P, P, P],
     "pp_grouped_gemm": [I, P, P, P, P, P, P, I, I, I, I, I, I, P],
-    "pp_grouped_gemm_ex": [I, P, P, P, P, P, P, I, I, I, I, I, P, P, I, P, P, I, I, I, I, P],
+    "pp_grouped_gemm_ex": [I, P, P, P, P, P, P, I, I, I, I, I, P, P, I, P, P, I, I, I, P, I, I, I, I, I, P],
     "pp_replica_trans": [P, P, P, I, I, I, I, I, I, P, I, P, P, I, P],
     "pp_replica_agg": [P, P, P, P, I, I, I, I, I, I, I, P],
     "pp_dot_bf16": [P, P, ctypes.c_int64, P, P, P],

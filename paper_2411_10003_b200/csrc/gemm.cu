@@ -100,6 +100,11 @@ struct GemmParams {
   const uint64_t* gate_flags;
   const uint64_t* gate_epoch;
   int gate_me, gate_D, gate_slot0;
+  // device-adaptive SM reservation: the persistent walk leaves
+  // clamp(res_per_unit * (res_stats[0] + (res_both ? res_stats[1] : 0)), res_lo, res_hi) SMs
+  // to concurrent side kernels (Trans / Agg), sized by this iteration's replica volume
+  const int32_t* res_stats;
+  int res_both, res_per_unit, res_lo, res_hi;
 };
 
 struct SchedSmem {
@@ -462,8 +467,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   // Static persistent walk.  Ragged-K (wgrad) tiles are sorted by K descending
   // and dealt in snake order (0..G-1, G-1..0, ...) so long tiles spread evenly.
   const bool snake = p.ragged_k != 0;
+  int G_walk = (int)gridDim.x / CG;  // one walk per CTA pair
+  if (p.res_stats) {
+    int r = p.res_per_unit * (p.res_stats[0] + (p.res_both ? p.res_stats[1] : 0));
+    r = r < p.res_lo ? p.res_lo : (r > p.res_hi ? p.res_hi : r);
+    G_walk = max(1, G_walk - (r + CG - 1) / CG);
+  }
   auto tile_of = [&](int it) -> int {
-    const int G = (int)gridDim.x / CG, b = (int)blockIdx.x / CG;  // one walk per CTA pair
+    const int G = G_walk, b = (int)blockIdx.x / CG;
+    if (b >= G) return total_tiles;  // reserved: no tiles, the CTA exits after the prologue
     return it * G + ((snake && (it & 1)) ? (G - 1 - b) : b);
   };
 
@@ -1027,6 +1039,8 @@ struct GateArgs {
   const uint64_t* flags;
   const uint64_t* epoch;
   int me, D, slot0;
+  const int32_t* res_stats;
+  int res_both, res_per_unit, res_lo, res_hi;
 };
 
 static int grouped_gemm_impl(int32_t mode, const void* a, const void* b, void* c, void* c2,
@@ -1049,9 +1063,14 @@ extern "C" int pp_grouped_gemm_ex(int32_t mode, const void* a, const void* b, vo
                                   int32_t rows_capacity, int32_t num_slots, int32_t d_model, int32_t d_ff,
                                   const int32_t* origin, void* const* scatter_ptrs, int32_t pairs_per_rank,
                                   const uint64_t* gate_flags, const uint64_t* gate_epoch, int32_t my_rank,
-                                  int32_t D, int32_t first_replica_slot, int32_t num_sms, void* stream) {
+                                  int32_t D, int32_t first_replica_slot, const int32_t* res_stats,
+                                  int32_t res_both, int32_t res_per_unit, int32_t res_lo, int32_t res_hi,
+                                  int32_t num_sms, void* stream) {
   ScatterArgs sc{origin, scatter_ptrs, pairs_per_rank};
-  GateArgs gt{gate_flags, gate_epoch, my_rank, D, first_replica_slot};
+  GateArgs gt{gate_flags, gate_epoch, my_rank, D, first_replica_slot, res_stats, res_both, res_per_unit,
+              res_lo, res_hi};
+  PP_CHECK_ARG(!res_stats || (res_per_unit >= 0 && res_lo >= 0 && res_hi >= res_lo),
+               "pp_grouped_gemm_ex: bad reservation arguments");
   if (origin) {
     PP_CHECK_ARG(mode == PP_GEMM_FWD2 || mode == PP_GEMM_DGRAD1,
                  "pp_grouped_gemm_ex: the fused A2A epilogue serves FWD2 and DGRAD1, got mode %d", mode);
@@ -1065,7 +1084,8 @@ extern "C" int pp_grouped_gemm_ex(int32_t mode, const void* a, const void* b, vo
                  "pp_grouped_gemm_ex: bad gate arguments");
   }
   return grouped_gemm_impl(mode, a, b, c, c2, groups, num_groups, max_groups, rows_capacity, num_slots,
-                           d_model, d_ff, num_sms, stream, origin ? &sc : nullptr, gate_flags ? &gt : nullptr);
+                           d_model, d_ff, num_sms, stream, origin ? &sc : nullptr,
+                           (gate_flags || res_stats) ? &gt : nullptr);
 }
 
 static int grouped_gemm_impl(int32_t mode, const void* a, const void* b, void* c, void* c2,
@@ -1107,6 +1127,11 @@ static int grouped_gemm_impl(int32_t mode, const void* a, const void* b, void* c
     p.gate_me = gate->me;
     p.gate_D = gate->D;
     p.gate_slot0 = gate->slot0;
+    p.res_stats = gate->res_stats;
+    p.res_both = gate->res_both;
+    p.res_per_unit = gate->res_per_unit;
+    p.res_lo = gate->res_lo;
+    p.res_hi = gate->res_hi;
   }
   int rc = PP_OK;
   // CTA pairs (cta_group::2, 256 x 256 tiles, B split across the pair) unless

@@ -60,7 +60,7 @@ __global__ void __launch_bounds__(kLayoutThreads)
                            int D, int m, int E, int T, int me, int max_groups, int rows_capacity,
                            int32_t* chunk_base, int32_t* slot_dest, pp_group* groups,
                            int32_t* num_groups, int32_t* total_rows, int32_t* seg_start,
-                           int32_t* rep_slot, int counts_from_chunks) {
+                           int32_t* rep_slot, int counts_from_chunks, int32_t* replica_stats) {
   extern __shared__ __align__(16) uint8_t lsm[];
   const int Ev = D * m, C = T / PP_CHUNK, tid = threadIdx.x, nt = blockDim.x;
   LayoutSmem S;
@@ -123,6 +123,17 @@ __global__ void __launch_bounds__(kLayoutThreads)
     if (r == me) *total_rows = off;
   }
   __syncthreads();
+  if (replica_stats && tid == 0) {
+    // [0] replicas of this rank's home experts held elsewhere (Trans pushes out, Agg sources in)
+    // [1] replicas this rank holds (Agg pushes out)
+    int out = 0, held = 0;
+    for (int r = 0; r < D; ++r)
+      if (r != me)
+        for (int e = me * m; e < (me + 1) * m; ++e) out += S.present[r * E + e];
+    for (int e = 0; e < E; ++e) held += (e / m != me) && S.present[me * E + e];
+    replica_stats[0] = out;
+    replica_stats[1] = held;
+  }
   // phase 3: this rank's group table
   if (tid == 0) {
     int g = 0, nrep = 0;
@@ -442,7 +453,7 @@ extern "C" int pp_dispatch_layout(int64_t* counts, const uint8_t* mask,
                                   int32_t rows_capacity, int32_t* chunk_base, int32_t* slot_dest,
                                   pp_group* groups, int32_t* num_groups, int32_t* total_rows,
                                   int32_t* seg_start, int32_t* rep_slot, int32_t counts_from_chunks,
-                                  void* stream) {
+                                  int32_t* replica_stats, void* stream) {
   PP_CHECK_ARG(counts && chunk_counts && chunk_base && slot_dest && groups && num_groups &&
                    total_rows && seg_start,
                "pp_dispatch_layout: null pointer");
@@ -465,7 +476,7 @@ extern "C" int pp_dispatch_layout(int64_t* counts, const uint8_t* mask,
   }
   dispatch_layout_kernel<<<1, kLayoutThreads, smem, as_stream(stream)>>>(
       counts, mask, chunk_counts, D, m, E, T, my_rank, max_groups, rows_capacity, chunk_base,
-      slot_dest, groups, num_groups, total_rows, seg_start, rep_slot, counts_from_chunks);
+      slot_dest, groups, num_groups, total_rows, seg_start, rep_slot, counts_from_chunks, replica_stats);
   PP_LAUNCH_CHECK();
   return PP_OK;
 }

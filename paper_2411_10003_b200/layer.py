@@ -297,6 +297,9 @@ class MoELayer(torch.nn.Module):
         # for the other (pushes reach NVLink rate from ~16 CTAs)
         self.agg_ctas = 16
         self.agg_ctas_w2 = 16  # the W2 half has DGRAD2 + WGRAD1 to hide under: may use fewer SMs
+        # SMs the GEMMs leave to Trans / Agg per replica this rank sends or receives (device-side,
+        # clamped to [2, trans_ctas / agg_ctas])
+        self.res_per_replica = 4
         if replica_engine not in ("copy", "sm"):
             raise ValidationError(f"replica_engine must be 'copy' or 'sm', got {replica_engine!r}")
         # 'copy': Trans/Agg pulls run on the copy engines (cudaMemcpyAsync over NVLink,
@@ -340,6 +343,9 @@ class MoELayer(torch.nn.Module):
             # Trans completion flags (slot r written by rank r) + the pushers' CTA counter
             self.trans_flags = PeerBuffer((2, D), torch.int64, self.group, dev)  # rows: W1, W2
             self._trans_ctr = torch.zeros(1, dtype=torch.int32, device=dev)
+            # layout output: [replicas of my home experts elsewhere, replicas I hold] -> the
+            # GEMMs size their SM reservation for Trans / Agg from it, on device
+            self.replica_stats = torch.zeros(2, dtype=torch.int32, device=dev)
             self.agg_stage = PeerBuffer((self.m, D - 1, 2, d_ff * d_model), torch.float32, self.group, dev)
             self.comm_barrier = _Barrier(self.group, dev)
         self._plan_pending = None
@@ -418,7 +424,8 @@ class MoELayer(torch.nn.Module):
                   self.world, m, E, T, self.rank, self.max_groups, self.rows_cap,
                   self.chunk_base.data_ptr(), self.slot_dest.data_ptr(), self.groups.data_ptr(),
                   self.num_groups.data_ptr(), self.total_rows.data_ptr(), self.seg_start.data_ptr(),
-                  self.rep_slot.data_ptr(), 1 if self.world == 1 else 0, sp)
+                  self.rep_slot.data_ptr(), 1 if self.world == 1 else 0,
+                  self.replica_stats.data_ptr() if self.trans_flags is not None else None, sp)
         if self.record_history:
             self.history.append(self.counts.clone())
 
@@ -645,7 +652,7 @@ class MoELayer(torch.nn.Module):
             self._agg_done.record(self.comm_stream)
             self._log_side("SubAgg1" if parts == 2 else "SubAgg2", t0, self._side_event(self.comm_stream))
 
-    def _gemm(self, mode, a, b, c, c2=None, stream=None, num_sms=None, scatter=False, gate=False):
+    def _gemm(self, mode, a, b, c, c2=None, stream=None, num_sms=None, scatter=False, gate=False, res=None):
         timing = self.gemm_timing
         if timing is not None:
             pool = self.gemm_event_pool
@@ -656,7 +663,7 @@ class MoELayer(torch.nn.Module):
                 e1 = torch.cuda.Event(enable_timing=True)
             e0.record()
         nsm = self.gemm_sms if num_sms is None else num_sms
-        if gate or scatter:
+        if gate or scatter or res:
             # fused A2A epilogue (rows go to their source rank's comb buffer) and/or replica
             # gate (replica tiles wait for the pushers' Trans completion flags: W1 row for
             # FWD1, W2 row for FWD2)
@@ -666,7 +673,8 @@ class MoELayer(torch.nn.Module):
                       self.num_groups.data_ptr(), self.max_groups, self.rows_cap, self.slots, self.d, self.f,
                       self.origin.local.data_ptr() if scatter else None,
                       self.comb.ptrs.data_ptr() if scatter else None, self.T * self.k, flags,
-                      self._epoch_ptr() if gate else None, self.rank, self.world, self.m, nsm,
+                      self._epoch_ptr() if gate else None, self.rank, self.world, self.m,
+                      self.replica_stats.data_ptr() if res else None, *(res or (0, 0, 0, 0)), nsm,
                       _device.stream_ptr(stream))
         else:
             _device.grouped_gemm(mode, a, b, c, c2, self.groups, self.num_groups, self.max_groups,
@@ -728,15 +736,17 @@ class MoELayer(torch.nn.Module):
         if sm_gate:
             trans_done = self.issue_trans()
         total = self.gemm_sms or _device.num_sms(self.device)
-        reserve = self.trans_ctas if (sm_gate and trans_done is not None) else 0
-        if self._plan_inflight():  # the planner's CTA: keep its SM out of the static GEMM walk
-            reserve += 2
-        fwd_sms = max(2, (total - reserve) // 2 * 2) if reserve else None
         gated = sm_gate and trans_done is not None
+        plan_sms = 2 if self._plan_inflight() else 0  # the planner's CTA stays out of the static walk
+        fwd_sms, fwd_res = None, None
+        if gated:  # leave ~2 SMs per replica this rank pushes (>= 2: its own signal-only Trans must run)
+            fwd_res = (0, self.res_per_replica, 2 + plan_sms, self.trans_ctas + plan_sms)
+        elif plan_sms:
+            fwd_sms = max(2, (total - plan_sms) // 2 * 2)
         self._gemm(_lib.PP_GEMM_FWD1, self.xp.local, self.w1_arena.local, self.pre, self.act, num_sms=fwd_sms,
-                   gate=gated)
+                   gate=gated, res=fwd_res)
         self._gemm(_lib.PP_GEMM_FWD2, self.act, self.w2_arena.local, self.yp.local, num_sms=fwd_sms,
-                   scatter=self.fused_a2a, gate=gated)
+                   scatter=self.fused_a2a, gate=gated, res=fwd_res)
         if gated:  # join the side stream (its pushes have landed: FWD2 waited for every flag)
             torch.cuda.current_stream().wait_event(trans_done)
         self._mark("fwd_gemms")
@@ -764,17 +774,16 @@ class MoELayer(torch.nn.Module):
             # SM engine: WGRAD2 first, so the replicas' W2 grads are pushed home while
             # DGRAD2 and WGRAD1 run, and the W1 grads while DGRAD1 runs; those GEMMs leave
             # agg_ctas SMs to the push/reduce kernels (SubAgg | BEC)
-            total = self.gemm_sms or _device.num_sms(self.device)
-            side_sms = max(2, (total - self.agg_ctas) // 2 * 2)
-            side_sms_w2 = max(2, (total - self.agg_ctas_w2) // 2 * 2)
+            # ~2 SMs per replica this rank sends or receives, on device (layout's replica_stats)
+            res_w2 = (1, self.res_per_replica, 2, self.agg_ctas_w2)
+            res_w1 = (1, self.res_per_replica, 2, self.agg_ctas)
             self._gemm(_lib.PP_GEMM_WGRAD2, self.dyp.local, self.act, self.g2_arena.local)
             self._issue_agg(parts=2)
-            self._gemm(_lib.PP_GEMM_DGRAD2, self.dyp.local, self.w2_arena.local, self.pre, self.pre,
-                       num_sms=side_sms_w2)
-            self._gemm(_lib.PP_GEMM_WGRAD1, self.pre, self.xp.local, self.g1_arena.local, num_sms=side_sms_w2)
+            self._gemm(_lib.PP_GEMM_DGRAD2, self.dyp.local, self.w2_arena.local, self.pre, self.pre, res=res_w2)
+            self._gemm(_lib.PP_GEMM_WGRAD1, self.pre, self.xp.local, self.g1_arena.local, res=res_w2)
             self._issue_agg(parts=1)
-            self._gemm(_lib.PP_GEMM_DGRAD1, self.pre, self.w1_arena.local, self.dxp.local, num_sms=side_sms,
-                       scatter=self.fused_a2a)
+            self._gemm(_lib.PP_GEMM_DGRAD1, self.pre, self.w1_arena.local, self.dxp.local,
+                       scatter=self.fused_a2a, res=res_w1)
         else:
             self._gemm(_lib.PP_GEMM_DGRAD2, self.dyp.local, self.w2_arena.local, self.pre, self.pre)
             self._gemm(_lib.PP_GEMM_WGRAD2, self.dyp.local, self.act, self.g2_arena.local)

@@ -84,16 +84,17 @@ def test_new_entry_points_validate_before_device_work():
     assert lib.pp_replica_trans(z, z, z, 16, 4, 4, 256, 256, 3, None, 0, None, None, 0, None) == _lib.PP_EINVAL
     assert lib.pp_replica_trans(z, z, z, 16, 4, 0, 256, 256, 3, z, 0, None, None, 0, None) == _lib.PP_EINVAL
     assert lib.pp_replica_trans(z, z, z, 16, 4, 0, 256, 256, 4, None, 0, None, None, 0, None) == _lib.PP_EINVAL
-    # pp_grouped_gemm_ex: the gate serves FWD1/FWD2 and needs its epoch; the scatter FWD2/DGRAD1
-    assert lib.pp_grouped_gemm_ex(0, z, z, z, z, z, z, 1, 128, 1, 256, 256, None, None, 0, z, None, 0, 2, 1, 0,
-                                  None) == _lib.PP_EINVAL
-    assert lib.pp_grouped_gemm_ex(2, z, z, z, z, z, z, 1, 128, 1, 256, 256, None, None, 0, z, z, 0, 2, 1, 0,
-                                  None) == _lib.PP_EINVAL
-    assert lib.pp_grouped_gemm_ex(0, z, z, z, z, z, z, 1, 128, 1, 256, 256, z, z, 4096, None, None, 0, 2, 1, 0,
-                                  None) == _lib.PP_EINVAL
-    assert lib.pp_replica_agg(z, z, z, z, 16, 4, 0, 256, 256, 4, 0, None) == _lib.PP_EINVAL
-    assert lib.pp_replica_agg_reduce(z, z, z, z, 16, 4, 0, 256, 256, 0, 0, None) == _lib.PP_EINVAL
-    assert lib.pp_replica_agg(None, z, z, z, 16, 4, 0, 256, 256, 3, 0, None) == _lib.PP_EINVAL
+    # pp_grouped_gemm_ex: the gate serves FWD1/FWD2 and needs its epoch; the scatter FWD2/DGRAD1;
+    # the adaptive reservation needs hi >= lo
+    nores = (None, 0, 0, 0, 0)
+    assert lib.pp_grouped_gemm_ex(0, z, z, z, z, z, z, 1, 128, 1, 256, 256, None, None, 0, z, None, 0, 2, 1,
+                                  *nores, 0, None) == _lib.PP_EINVAL
+    assert lib.pp_grouped_gemm_ex(2, z, z, z, z, z, z, 1, 128, 1, 256, 256, None, None, 0, z, z, 0, 2, 1,
+                                  *nores, 0, None) == _lib.PP_EINVAL
+    assert lib.pp_grouped_gemm_ex(0, z, z, z, z, z, z, 1, 128, 1, 256, 256, z, z, 4096, None, None, 0, 2, 1,
+                                  *nores, 0, None) == _lib.PP_EINVAL
+    assert lib.pp_grouped_gemm_ex(0, z, z, z, z, z, z, 1, 128, 1, 256, 256, None, None, 0, None, None, 0, 2, 1,
+                                  z, 1, 2, 8, 4, 0, None) == _lib.PP_EINVAL
     # probe loss: n must be a multiple of 8, operands 16-byte aligned
     assert lib.pp_dot_bf16(z, z, 12, z, z, None) == _lib.PP_EINVAL
     assert lib.pp_dot_bf16(ctypes.c_void_p(24), z, 16, z, z, None) == _lib.PP_EINVAL
