@@ -739,7 +739,7 @@ class MoELayer(torch.nn.Module):
         gated = sm_gate and trans_done is not None
         plan_sms = 2 if self._plan_inflight() else 0  # the planner's CTA stays out of the static walk
         fwd_sms, fwd_res = None, None
-        if gated:  # leave ~2 SMs per replica this rank pushes (>= 2: its own signal-only Trans must run)
+        if gated:  # res_per_replica SMs per replica this rank pushes (>= 2: its signal-only Trans must run)
             fwd_res = (0, self.res_per_replica, 2 + plan_sms, self.trans_ctas + plan_sms)
         elif plan_sms:
             fwd_sms = max(2, (total - plan_sms) // 2 * 2)
@@ -774,7 +774,7 @@ class MoELayer(torch.nn.Module):
             # SM engine: WGRAD2 first, so the replicas' W2 grads are pushed home while
             # DGRAD2 and WGRAD1 run, and the W1 grads while DGRAD1 runs; those GEMMs leave
             # agg_ctas SMs to the push/reduce kernels (SubAgg | BEC)
-            # ~2 SMs per replica this rank sends or receives, on device (layout's replica_stats)
+            # res_per_replica SMs per replica this rank sends or receives, on device (layout replica_stats)
             res_w2 = (1, self.res_per_replica, 2, self.agg_ctas_w2)
             res_w1 = (1, self.res_per_replica, 2, self.agg_ctas)
             self._gemm(_lib.PP_GEMM_WGRAD2, self.dyp.local, self.act, self.g2_arena.local)
