@@ -1153,7 +1153,7 @@ static int grouped_gemm_impl(int32_t mode, const void* a, const void* b, void* c
       if ((rc = make_tmap(&ta, a, dm, R, BK, BM)) || (rc = make_tmap(&tb, b, dm, (uint64_t)S * df, BK, bkb))) return rc;
       p.N = df; p.K_fixed = dm;
       if ((rc = make_out_tmap(&tc, c, df, R)) || (rc = make_out_tmap(&tc2, c2, df, R))) return rc;
-      return PP_LAUNCH(EPI_GELU, false, false, 4, 5, &tc, &tc2);
+      return PP_LAUNCH(EPI_GELU, false, false, 3, 5, &tc, &tc2);
     case PP_GEMM_FWD2:
       if ((rc = make_tmap(&ta, a, df, R, BK, BM)) ||
           (rc = make_tmap(&tb, b, df, (uint64_t)S * dm, BK, bkb)))
