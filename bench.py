@@ -421,12 +421,13 @@ def main() -> None:
     # ---- step function: CUDA-graph replay of fwd+bwd at N == 1 (host cost ~ one
     # graph launch per step), eager stream-ordered calls at N > 1
     use_graph = not args.eager
-    xs = [x.detach().clone() for _ in range(2)]
+    NB = int(os.environ.get("PP_BENCH_NBUF", "2"))  # input buffers / graphs: e2e stages H2D NB-1 steps ahead
+    xs = [x.detach().clone() for _ in range(NB)]
     if use_graph:
-        graphs = [layer.make_graphed_step(xs[b], dy.clone(), with_loss=True) for b in range(2)]
-        run_step = lambda i: graphs[i % 2]()  # noqa: E731
+        graphs = [layer.make_graphed_step(xs[b], dy.clone(), with_loss=True) for b in range(NB)]
+        run_step = lambda i: graphs[i % NB]()  # noqa: E731
     else:
-        run_step = lambda i: step(xs[i % 2].detach(), dy)  # noqa: E731
+        run_step = lambda i: step(xs[i % NB].detach(), dy)  # noqa: E731
     for i in range(2):
         run_step(i)
     torch.cuda.synchronize()
@@ -581,13 +582,14 @@ def main() -> None:
         # A training step on this layer: the batch x comes from pinned host memory
         # (H2D inside the timed region), loss = sum(y * g) with a fixed device-resident
         # probe g (so dL/dy = g, the upstream gradient), backward, and the loss scalar is
-        # read back to the host (D2H).  H2D of step i+1 overlaps step i (copy stream).
-        xh = [x.detach().cpu().pin_memory() for _ in range(2)]
+        # read back to the host (D2H).  The H2D of step i+NB-1 overlaps the steps before it (copy stream;
+        # NB = 2 and 3 measured the same e2e at 4 GPUs).
+        xh = [x.detach().cpu().pin_memory() for _ in range(NB)]
         lh = [torch.zeros((), dtype=torch.float32).pin_memory() for _ in range(args.steps)]
         if use_graph:
             xdev = [g.x for g in graphs]
         else:
-            xdev = [torch.empty_like(x) for _ in range(2)]
+            xdev = [torch.empty_like(x) for _ in range(NB)]
         copy = torch.cuda.Stream(device=dev)   # H2D engine
         back = torch.cuda.Stream(device=dev)   # D2H engine
         main = torch.cuda.current_stream()
@@ -596,25 +598,26 @@ def main() -> None:
             dist.barrier()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
-        ev_in = [torch.cuda.Event() for _ in range(2)]
-        ev_free = [torch.cuda.Event() for _ in range(2)]
+        ev_in = [torch.cuda.Event() for _ in range(NB)]
+        ev_free = [torch.cuda.Event() for _ in range(NB)]
         ev_out = torch.cuda.Event()
         w0 = time.perf_counter()
         layer.barrier()  # device-side peer barrier: every rank's clock starts together
         e0.record(main)
 
         def h2d(i):
-            b = i % 2
+            b = i % NB
             with torch.cuda.stream(copy):
-                copy.wait_event(ev_free[b]) if i >= 2 else copy.wait_event(e0)
+                copy.wait_event(ev_free[b]) if i >= NB else copy.wait_event(e0)
                 xdev[b].copy_(xh[b], non_blocking=True)
                 ev_in[b].record(copy)
 
-        h2d(0)
+        for i in range(min(NB - 1, args.steps)):
+            h2d(i)
         for i in range(args.steps):
-            b = i % 2
-            if i + 1 < args.steps:
-                h2d(i + 1)
+            b = i % NB
+            if i + NB - 1 < args.steps:
+                h2d(i + NB - 1)  # two steps ahead: its buffer was freed by step i-1
             main.wait_event(ev_in[b])
             if use_graph:
                 _, _ = graphs[b]()
