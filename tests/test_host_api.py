@@ -209,3 +209,28 @@ def test_trace_jsonl_matches_reference_format(tmp_path, rng):
     assert ours.read_bytes() == theirs.read_bytes()  # byte-identical JSONL
     parsed = workload.read_trace(ours)  # the reference replays our traces
     assert [r.load.counts.tolist() for r in parsed] == [r.load.counts.tolist() for r in recs]
+
+
+def test_cost_model_calibration_fit():
+    """calibrate.fit recovers B and t from phase timings generated by the model itself and
+    reports ~0 held-out error; measured_costs sums the four A2A spans and the GEMM phases."""
+    from paper_2411_10003_b200 import calibrate
+
+    t_true, B_true, ib = 5e7, 4e11, 2048.0
+    rng = np.random.default_rng(0)
+    samples = []
+    for _ in range(8):
+        H = rng.integers(20000, 40000, size=4)
+        R = rng.integers(5000, 15000, size=4)
+        fec = H.max() / t_true
+        a2a = R.max() * ib / B_true
+        samples.append((H, R, {"a2a_total": 4 * a2a, "fec": fec, "bec": 2 * fec, "layer": 4 * a2a + 3 * fec}))
+    fit = calibrate.fit(samples, input_bytes=ib)
+    assert abs(fit["compute_throughput"] / t_true - 1) < 1e-9
+    assert abs(fit["avg_bandwidth"] / B_true - 1) < 1e-9
+    assert fit["mean_abs_rel_error"] < 1e-9 and fit["train_iters"] == 4 and fit["test_iters"] == 4
+    step = {"route_layout": 0.1, "barrier1": 0.3, "fwd_gemms": 1.0, "combine": 1.2, "bwd_begin": 1.25,
+            "barrier3": 1.4, "bwd_gemms": 3.0, "dispatch_bwd": 3.2}
+    m = calibrate.measured_costs(step)
+    assert abs(m["fec"] - 0.7e-3) < 1e-12 and abs(m["bec"] - 1.6e-3) < 1e-12
+    assert abs(m["a2a_total"] - (0.2 + 0.2 + 0.15 + 0.2) * 1e-3) < 1e-12
