@@ -234,3 +234,19 @@ def test_cost_model_calibration_fit():
     m = calibrate.measured_costs(step)
     assert abs(m["fec"] - 0.7e-3) < 1e-12 and abs(m["bec"] - 1.6e-3) < 1e-12
     assert abs(m["a2a_total"] - (0.2 + 0.2 + 0.15 + 0.2) * 1e-3) < 1e-12
+
+
+def test_physical_placement_value_type():
+    """PhysicalPlacement (E = m*D, homes e // m): validation, replica sets, the [D][E] mask,
+    the [E][E] slot mask the layout consumes, and equality with ExpertPlacement at m = 1."""
+    p = pp.PhysicalPlacement(2, 4, (1,), (frozenset(),))
+    assert p.home(3) == 1 and p.replicas(1) == frozenset({0, 1}) and p.replicas(2) == frozenset({1})
+    assert p.replica_mask().astype(int).tolist() == [[1, 1, 0, 0], [0, 1, 1, 1]]
+    assert p.slot_mask().astype(int).tolist() == [[1, 1, 0, 0], [1, 1, 0, 0], [0, 1, 1, 1], [0, 1, 1, 1]]
+    with pytest.raises(pp.ValidationError):
+        pp.PhysicalPlacement(3, 4)  # E not a multiple of D
+    with pytest.raises(pp.ValidationError):
+        pp.PhysicalPlacement(2, 4, (1,), (frozenset({0}),))  # home of expert 1 is device 0
+    q = pp.PhysicalPlacement(3, 3, (0,), (frozenset({2}),))
+    r = pp.ExpertPlacement(3, 3, (0,), (frozenset({2}),))
+    assert q.replica_mask().tolist() == r.replica_mask().tolist()
