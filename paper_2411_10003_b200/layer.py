@@ -120,6 +120,10 @@ class _Barrier:
             torch.cuda.synchronize()
             dist.barrier(group=group)
 
+    def close(self) -> None:
+        if self.world > 1:
+            self.sig.close()
+
     def __call__(self, stream=None) -> None:
         if self.world == 1:
             return
@@ -883,7 +887,8 @@ class MoELayer(torch.nn.Module):
 
     def close(self) -> None:
         for b in (self.w1_arena, self.w2_arena, self.g1_arena, self.g2_arena, self.xp, self.yp, self.dyp, self.dxp,
-                  self.counts_buf, self.agg_stage, self.origin, self.comb, self.trans_flags):
+                  self.counts_buf, self.agg_stage, self.origin, self.comb, self.trans_flags,
+                  self.barrier, getattr(self, "comm_barrier", None)):
             if b is not None:
                 b.close()
 
