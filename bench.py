@@ -522,14 +522,25 @@ def main() -> None:
 
         steps_ph = calibrate.per_step_phases(layer.phase_log)
         samples = []
+        m_ = E // world
         for (counts_t, mask_t), ph in zip(calib_samples, steps_ph):
             counts_np = counts_t.cpu().numpy()
             mask_np = mask_t.cpu().numpy() if mask_t is not None else np.eye(E, dtype=np.uint8)
-            H, R = dv.derive_loads(counts_np, mask_np.astype("uint8"))  # pp_derive_loads kernel
+            if layer.placement == "physical":
+                # per-device loads under the slot routing rule the layout applies: pair (slot v,
+                # expert e) is computed on v's device if mask[v][e], else on e's home device
+                dev_of_slot = np.arange(E) // m_
+                comp = np.where(mask_np.astype(bool), dev_of_slot[:, None], (np.arange(E) // m_)[None, :])
+                H = np.bincount(comp.ravel(), weights=counts_np.ravel(), minlength=world)
+                remote = comp != dev_of_slot[:, None]
+                R = np.bincount(comp[remote], weights=counts_np[remote], minlength=world)
+            else:
+                H, R = dv.derive_loads(counts_np, mask_np.astype("uint8"))  # pp_derive_loads kernel
             samples.append((H, R, calibrate.measured_costs(ph)))
         calibration = calibrate.fit(samples, input_bytes=2 * d)
-        calibration["note"] = ("fit of the reference model's B and t to this run's measured phases "
-                               "(virtual-slot H/R, rank 0); plan objective uses these units")
+        calibration["note"] = ("fit of the reference model's B and t to this run's measured phases ("
+                               + ("per-device H/R" if layer.placement == "physical" else "virtual-slot H/R")
+                               + ", rank 0); plan objective uses these units")
     layer.phase_log = None
 
     replica_traffic = None
