@@ -318,7 +318,7 @@ def main() -> None:
                     help="physical placement: slot-level refinement of the plan (1/0; beyond the paper)")
     ap.add_argument("--fused-a2a", type=int, default=0,
                     help="combine / dispatch-backward fused into the FWD2 / DGRAD1 epilogues (1/0; default 0: with "
-                         "the 256x512 tiles the unfused path measured 3 % faster at 2 and 4 GPUs)")
+                         "the 256x512 tiles the unfused path measured 3 %% faster at 2 and 4 GPUs)")
     ap.add_argument("--trans-gate", type=int, default=None,
                     help="SM-engine Trans overlapped with FWD1 via per-tile gates (1) or awaited before it (0)")
     ap.add_argument("--avg-bandwidth", type=float, default=None,
