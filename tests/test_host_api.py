@@ -250,3 +250,15 @@ def test_physical_placement_value_type():
     q = pp.PhysicalPlacement(3, 3, (0,), (frozenset({2}),))
     r = pp.ExpertPlacement(3, 3, (0,), (frozenset({2}),))
     assert q.replica_mask().tolist() == r.replica_mask().tolist()
+
+
+def test_bench_cli_parses():
+    """bench.py's argument parser (the driver's entry point) builds and prints its help."""
+    import subprocess
+    import sys
+
+    root = Path(__file__).resolve().parent.parent
+    r = subprocess.run([sys.executable, str(root / "bench.py"), "--help"], capture_output=True, text=True,
+                       timeout=120)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert "--gpus" in r.stdout and "--impl" in r.stdout
