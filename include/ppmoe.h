@@ -61,10 +61,30 @@ typedef struct pp_cost_model {
   int32_t _pad;
 } pp_cost_model;
 
+/* alpha / n / overlap_aware / reuse_interval: reference PlannerConfig (planner.py:38-60).
+ * Extensions (all zero = the reference's behaviour):
+ *   max_replicas  > 0: only plans that give no rank more than max_replicas replica
+ *                 experts are accepted (the replica weight slots a rank owns); replica
+ *                 counts grow with the search prefix, so the search stops at the first
+ *                 prefix that exceeds it.  A bound that never binds leaves the plan
+ *                 bit-exact with the reference.
+ *   slots_per_rank: rows of the load matrix per rank for that count (virtual-slot search:
+ *                 m = E/D; 0 or 1 = one row per rank).
+ *   iter_counter: device int64[2] {j, scratch}.  Non-NULL: the launch belongs to iteration
+ *                 j and plans iteration j+1, so it searches only when (j+1) % reuse_interval
+ *                 == 0 (plan_for_iteration, planner.py:132-156) and otherwise leaves every
+ *                 output untouched; either way j advances by one when the launch ends.  This
+ *                 keeps the reuse policy inside a CUDA graph that replays one launch per
+ *                 iteration. */
 typedef struct pp_planner_cfg {
   double alpha;
   int32_t n;
   int32_t overlap_aware;
+  int32_t reuse_interval;
+  int32_t max_replicas;
+  int32_t slots_per_rank;
+  int32_t _pad;
+  const int64_t* iter_counter;
 } pp_planner_cfg;
 
 /* Plan L layers, one CTA each.  counts: [L][E][E] int64 (device).
@@ -156,14 +176,20 @@ typedef struct pp_group {
  * counts_from_chunks (D == 1 only): fill `counts` from the chunk counts here,
  * replacing pp_slot_histogram + barrier.  replica_stats (nullable, int32[2]):
  * [0] replicas of this rank's home experts held elsewhere, [1] replicas this
- * rank holds -- the device-side volume hints for SM reservation around Trans/Agg. */
+ * rank holds -- the device-side volume hints for SM reservation around Trans/Agg.
+ * Capacity: every rank's receive buffer holds rows_capacity rows and num_slots weight
+ * slots (0 = unchecked).  When any rank's padded rows exceed rows_capacity, its replica
+ * experts exceed num_slots - m, or its groups exceed max_groups, the layout of the whole
+ * step is dropped on every rank alike (num_groups = 0, slot_dest = -1: dispatch stores
+ * nothing, combine yields zeros) and status (nullable int32, sticky) gets bit 1 / 2 / 4
+ * respectively -- nothing is written out of bounds and the caller raises on the flag. */
 int pp_dispatch_layout(int64_t* counts, const uint8_t* mask, const int32_t* chunk_counts,
                        int32_t D, int32_t m, int32_t E, int32_t T, int32_t my_rank,
-                       int32_t max_groups, int32_t rows_capacity,
+                       int32_t max_groups, int32_t rows_capacity, int32_t num_slots,
                        int32_t* chunk_base, int32_t* slot_dest, pp_group* groups,
                        int32_t* num_groups, int32_t* total_rows, int32_t* seg_start,
                        int32_t* rep_slot, int32_t counts_from_chunks, int32_t* replica_stats,
-                       void* stream);
+                       int32_t* status, void* stream);
 
 /* Permute + all-to-all in one kernel: row of token t goes to rank
  * slot_dest[t/(T/m)][e] at row chunk_base[t/128][e] + rank[t][j] of that
@@ -276,13 +302,15 @@ int pp_grouped_gemm_ex(int32_t mode, const void* a, const void* b, void* c, void
  * can run before this iteration's routing; every rank must have passed the
  * previous backward's last peer barrier.  `max_ctas` = SMs it occupies
  * (E <= 1024, D*E <= 16384).  parts: 1 = W1 only, 2 = W2 only, 3 = both.
+ * num_slots: weight slots per rank's arena; replicas that would land in slot >=
+ * num_slots are skipped (the layout flags such a plan, see pp_dispatch_layout).
  * flag_ptrs (nullable; peer table of [rows][D] uint64 flag arrays): when every
  * CTA is done, the last one stores *epoch (device value, e.g. the peer-barrier
  * counter) into flag_ptrs[r][flag_row*D + my_rank] of every peer r with release
  * semantics -- the completion signal the pp_grouped_gemm_ex gate waits on;
  * done_ctr is a zeroed uint32 scratch word (left zeroed). */
 int pp_replica_trans(void* const* w1_ptrs, void* const* w2_ptrs, const uint8_t* mask, int32_t E,
-                     int32_t m, int32_t my_rank, int32_t d_model, int32_t d_ff, int32_t parts,
+                     int32_t m, int32_t my_rank, int32_t num_slots, int32_t d_model, int32_t d_ff, int32_t parts,
                      void* const* flag_ptrs, int32_t flag_row, const uint64_t* epoch,
                      uint32_t* done_ctr, int32_t max_ctas, void* stream);
 
@@ -293,7 +321,7 @@ int pp_replica_trans(void* const* w1_ptrs, void* const* w2_ptrs, const uint8_t* 
  * grads, 3 = both (the layer pushes W2's as soon as WGRAD2 is done, W1's after
  * WGRAD1). */
 int pp_replica_agg(void* const* g1_ptrs, void* const* g2_ptrs, void* const* stage_ptrs,
-                   const uint8_t* mask, int32_t E, int32_t m, int32_t my_rank, int32_t d_model,
+                   const uint8_t* mask, int32_t E, int32_t m, int32_t my_rank, int32_t num_slots, int32_t d_model,
                    int32_t d_ff, int32_t parts, int32_t max_ctas, void* stream);
 
 /* Agg phase 2 (home side, after a peer barrier): grad[j] += stage[j][r'] for

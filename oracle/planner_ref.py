@@ -100,9 +100,24 @@ def is_balanced(H, total_inputs: int, E: int, alpha: float) -> bool:
     return float(H.max() - H.min()) < alpha * total_inputs / E
 
 
-def greedy_search(counts, n: int, alpha: float, overlap_aware: bool, cm: dict) -> dict:
+def replicas_per_rank(mask: np.ndarray, rows_per_rank: int, homes_per_rank: int) -> np.ndarray:
+    """Replica experts each rank holds under a [rows][E] mask (rank of row v = v // rows_per_rank,
+    home rank of expert e = e // homes_per_rank) -- the weight slots the plan needs."""
+    rows, E = mask.shape
+    ranks = rows // rows_per_rank
+    held = mask.reshape(ranks, rows_per_rank, E).any(axis=1)
+    home = np.arange(E) // homes_per_rank
+    return np.array([int(sum(held[r, e] and home[e] != r for e in range(E))) for r in range(ranks)])
+
+
+def greedy_search(counts, n: int, alpha: float, overlap_aware: bool, cm: dict,
+                  max_replicas: int = 0, slots_per_rank: int = 1) -> dict:
     """reference planner.py:80-129 (Algorithm 1).  Returns the plan plus the
-    objective of the returned plan and the number of explored steps."""
+    objective of the returned plan and the number of explored steps.
+
+    max_replicas > 0 (extension of the device kernel, pp_planner_cfg; not in the
+    reference): the search stops before the first prefix whose mask gives a rank
+    (slots_per_rank rows each) more than max_replicas replica experts."""
     counts = np.asarray(counts, dtype=np.int64)
     D, E = counts.shape
     assert D == E, "greedy search requires num_experts == num_devices"
@@ -118,6 +133,11 @@ def greedy_search(counts, n: int, alpha: float, overlap_aware: bool, cm: dict) -
         used.add(i)
         selected.append(i)
         bottoms.append(bottom_devices(counts, i, n))
+        if max_replicas > 0 and replicas_per_rank(replica_mask(D, E, selected, bottoms), slots_per_rank,
+                                                  slots_per_rank).max() > max_replicas:
+            selected.pop()
+            bottoms.pop()
+            break
         H, R = derive_loads(counts, replica_mask(D, E, selected, bottoms))
         changed = objective(H, R, len(selected), n, cm, overlap_aware)
         if changed < best:
@@ -182,7 +202,8 @@ def bottom_devices_physical(counts: np.ndarray, expert: int, n: int, home: int) 
     return frozenset(d for _, d in cands[:n])
 
 
-def greedy_search_physical(counts, n: int, alpha: float, overlap_aware: bool, cm: dict) -> dict:
+def greedy_search_physical(counts, n: int, alpha: float, overlap_aware: bool, cm: dict,
+                           max_replicas: int = 0) -> dict:
     counts = np.asarray(counts, dtype=np.int64)
     D, E = counts.shape
     assert E % D == 0 and cm["num_devices"] == D
@@ -209,6 +230,10 @@ def greedy_search_physical(counts, n: int, alpha: float, overlap_aware: bool, cm
         selected.append(e)
         bottoms.append(bottom_devices_physical(counts, e, n, i))
         mask = replica_mask_physical(D, E, selected, bottoms)
+        if max_replicas > 0 and replicas_per_rank(mask, 1, m).max() > max_replicas:
+            selected.pop()
+            bottoms.pop()
+            break
         H, R = derive_loads_physical(counts, mask)
         changed = objective(H, R, len(selected), n, cm, overlap_aware)
         if changed < best:

@@ -51,11 +51,17 @@ def cost_model(cluster, model, E: int | None = None) -> _lib.CostModel:
     return cm
 
 
-def planner_cfg(config) -> _lib.PlannerCfg:
+def planner_cfg(config, max_replicas: int = 0, slots_per_rank: int = 1, iter_counter=None) -> _lib.PlannerCfg:
+    """pp_planner_cfg from a reference PlannerConfig; the extensions default to the
+    reference's behaviour (no replica bound, no device-side reuse gate)."""
     c = _lib.PlannerCfg()
     c.alpha = float(config.alpha)
     c.n = int(config.n)
     c.overlap_aware = 1 if config.overlap_aware else 0
+    c.reuse_interval = int(getattr(config, "reuse_interval", 1))
+    c.max_replicas = int(max_replicas)
+    c.slots_per_rank = int(slots_per_rank)
+    c.iter_counter = None if iter_counter is None else iter_counter.data_ptr()
     return c
 
 

@@ -40,7 +40,8 @@ class CostModel(ctypes.Structure):
 
 
 class PlannerCfg(ctypes.Structure):
-    _fields_ = [("alpha", c_double), ("n", c_int32), ("overlap_aware", c_int32)]
+    _fields_ = [("alpha", c_double), ("n", c_int32), ("overlap_aware", c_int32), ("reuse_interval", c_int32),
+                ("max_replicas", c_int32), ("slots_per_rank", c_int32), ("_pad", c_int32), ("iter_counter", c_void_p)]
 
 
 class Group(ctypes.Structure):
@@ -68,7 +69,7 @@ SIGNATURES = {
     "pp_top_m_mask": [P, I, I, I, P, P, P],
     "pp_route_topk": [P, P, P, I, I, I, I, P, P, P, P, P, P],
     "pp_slot_histogram": [P, I, I, I, P, I, I, P],
-    "pp_dispatch_layout": [P, P, P, I, I, I, I, I, I, I, P, P, P, P, P, P, P, I, P, P],
+    "pp_dispatch_layout": [P, P, P, I, I, I, I, I, I, I, I, P, P, P, P, P, P, P, I, P, P, P],
     "pp_dispatch": [P, P, P, P, P, I, I, I, I, I, P, P, P, P, I, P, P, P, I, P],
     "pp_combine": [P, P, P, P, I, I, I, P, P, P],
     "pp_combine_bwd": [P, P, P, P, P, P, P, P, P, I, I, I, I, P, P, P],
@@ -76,8 +77,8 @@ SIGNATURES = {
     "pp_gate_bwd": [P, P, P, I, I, I, I, P, P, P],
     "pp_grouped_gemm": [I, P, P, P, P, P, P, I, I, I, I, I, I, P],
     "pp_grouped_gemm_ex": [I, P, P, P, P, P, P, I, I, I, I, I, P, P, I, P, P, I, I, I, P, I, I, I, I, I, P],
-    "pp_replica_trans": [P, P, P, I, I, I, I, I, I, P, I, P, P, I, P],
-    "pp_replica_agg": [P, P, P, P, I, I, I, I, I, I, I, P],
+    "pp_replica_trans": [P, P, P, I, I, I, I, I, I, I, P, I, P, P, I, P],
+    "pp_replica_agg": [P, P, P, P, I, I, I, I, I, I, I, I, P],
     "pp_dot_bf16": [P, P, ctypes.c_int64, P, P, P],
     "pp_replica_agg_reduce": [P, P, P, P, I, I, I, I, I, I, I, P],
     "pp_copy_batch": [P, P, P, I, P],

@@ -125,7 +125,7 @@ __device__ __forceinline__ void push_copy(int nmat, size_t vecs, Addr addr) {
 // ended before the last peer barrier of their backward, which this rank has passed.
 __global__ void __launch_bounds__(512) replica_trans_kernel(void* const* w1_ptrs, void* const* w2_ptrs,
                                                             const uint8_t* mask, int E, int m, int me,
-                                                            size_t vecs, int parts, void* const* flag_ptrs,
+                                                            int num_slots, size_t vecs, int parts, void* const* flag_ptrs,
                                                             int flag_row, const uint64_t* epoch,
                                                             unsigned int* done_ctr) {
   __shared__ uint8_t flag[kMaxFlags];
@@ -134,7 +134,8 @@ __global__ void __launch_bounds__(512) replica_trans_kernel(void* const* w1_ptrs
   replica_flags(mask, D, E, m, flag);
   for (int t = threadIdx.x; t < D * m; t += blockDim.x) {  // t = (receiver r, home slot j)
     const int r = t / m, j = t - (t / m) * m, e = me * m + j;
-    cand[t] = (r != me && flag[r * E + e]) ? ((r * m + j) << 10 | replica_index(flag, E, r, e)) : -1;
+    const int i = (r != me && flag[r * E + e]) ? replica_index(flag, E, r, e) : -1;
+    cand[t] = (i >= 0 && m + i < num_slots) ? ((r * m + j) << 10 | i) : -1;  // slot bound
   }
   __syncthreads();
   const int n = compact_items(cand, D * m, items);
@@ -171,13 +172,16 @@ __global__ void __launch_bounds__(512) replica_trans_kernel(void* const* w1_ptrs
 // home's D-1 peers), so the home can sum its sources in rank order.
 __global__ void __launch_bounds__(512) replica_agg_push_kernel(void* const* g1_ptrs, void* const* g2_ptrs,
                                                                void* const* stage_ptrs, const uint8_t* mask,
-                                                               int E, int m, int me, size_t vecs, int parts) {
+                                                               int E, int m, int me, int num_slots, size_t vecs,
+                                                               int parts) {
   __shared__ uint8_t flag[kMaxFlags];
   __shared__ int cand[kMaxItems], items[kMaxItems];
   const int D = E / m;
   replica_flags(mask, D, E, m, flag);
-  for (int e = threadIdx.x; e < E; e += blockDim.x)
-    cand[e] = flag[me * E + e] ? (e << 10 | replica_index(flag, E, me, e)) : -1;
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    const int i = flag[me * E + e] ? replica_index(flag, E, me, e) : -1;
+    cand[e] = (i >= 0 && m + i < num_slots) ? (e << 10 | i) : -1;  // slot bound
+  }
   __syncthreads();
   const int n = compact_items(cand, E, items);
   const int np = parts == 3 ? 2 : 1;  // bit 0: W1 grads, bit 1: W2 grads
@@ -297,8 +301,8 @@ extern "C" int pp_peer_barrier(void* const* signal_ptrs, int32_t D, int32_t my_r
 }
 
 extern "C" int pp_replica_trans(void* const* w1_ptrs, void* const* w2_ptrs, const uint8_t* mask,
-                                int32_t E, int32_t m, int32_t my_rank, int32_t d_model, int32_t d_ff,
-                                int32_t parts, void* const* flag_ptrs, int32_t flag_row,
+                                int32_t E, int32_t m, int32_t my_rank, int32_t num_slots, int32_t d_model,
+                                int32_t d_ff, int32_t parts, void* const* flag_ptrs, int32_t flag_row,
                                 const uint64_t* epoch, uint32_t* done_ctr, int32_t max_ctas,
                                 void* stream) {
   PP_CHECK_ARG(parts >= 1 && parts <= 3 && flag_row >= 0, "pp_replica_trans: bad parts / flag_row");
@@ -309,7 +313,8 @@ extern "C" int pp_replica_trans(void* const* w1_ptrs, void* const* w2_ptrs, cons
                "pp_replica_trans: bad E / m / rank");
   PP_CHECK_ARG(((size_t)d_model * d_ff) % 8 == 0, "pp_replica_trans: bad sizes");
   const int grid = max_ctas > 0 ? max_ctas : 16;
-  replica_trans_kernel<<<grid, 512, 0, as_stream(stream)>>>(w1_ptrs, w2_ptrs, mask, E, m, my_rank,
+  PP_CHECK_ARG(num_slots > m, "pp_replica_trans: num_slots=%d leaves no replica slot (m=%d)", num_slots, m);
+  replica_trans_kernel<<<grid, 512, 0, as_stream(stream)>>>(w1_ptrs, w2_ptrs, mask, E, m, my_rank, num_slots,
                                                             (size_t)d_model * d_ff / 8, parts, flag_ptrs,
                                                             flag_row, epoch, done_ctr);
   PP_LAUNCH_CHECK();
@@ -317,7 +322,7 @@ extern "C" int pp_replica_trans(void* const* w1_ptrs, void* const* w2_ptrs, cons
 }
 
 extern "C" int pp_replica_agg(void* const* g1_ptrs, void* const* g2_ptrs, void* const* stage_ptrs,
-                              const uint8_t* mask, int32_t E, int32_t m, int32_t my_rank,
+                              const uint8_t* mask, int32_t E, int32_t m, int32_t my_rank, int32_t num_slots,
                               int32_t d_model, int32_t d_ff, int32_t parts, int32_t max_ctas,
                               void* stream) {
   PP_CHECK_ARG(parts >= 1 && parts <= 3, "pp_replica_agg: parts must be 1 (W1), 2 (W2) or 3, got %d", parts);
@@ -327,8 +332,9 @@ extern "C" int pp_replica_agg(void* const* g1_ptrs, void* const* g2_ptrs, void* 
                "pp_replica_agg: bad E / m / rank");
   PP_CHECK_ARG(((size_t)d_model * d_ff) % 4 == 0, "pp_replica_agg: bad sizes");
   const int grid = max_ctas > 0 ? max_ctas : 16;
+  PP_CHECK_ARG(num_slots > m, "pp_replica_agg: num_slots=%d leaves no replica slot (m=%d)", num_slots, m);
   replica_agg_push_kernel<<<grid, 512, 0, as_stream(stream)>>>(g1_ptrs, g2_ptrs, stage_ptrs, mask, E, m,
-                                                               my_rank, (size_t)d_model * d_ff / 4, parts);
+                                                               my_rank, num_slots, (size_t)d_model * d_ff / 4, parts);
   PP_LAUNCH_CHECK();
   return PP_OK;
 }

@@ -58,9 +58,11 @@ __host__ __device__ inline size_t layout_smem_bytes(int D, int m, int E, int T) 
 __global__ void __launch_bounds__(kLayoutThreads)
     dispatch_layout_kernel(int64_t* counts, const uint8_t* mask, const int32_t* chunk_counts,
                            int D, int m, int E, int T, int me, int max_groups, int rows_capacity,
-                           int32_t* chunk_base, int32_t* slot_dest, pp_group* groups,
+                           int num_slots, int32_t* chunk_base, int32_t* slot_dest, pp_group* groups,
                            int32_t* num_groups, int32_t* total_rows, int32_t* seg_start,
-                           int32_t* rep_slot, int counts_from_chunks, int32_t* replica_stats) {
+                           int32_t* rep_slot, int counts_from_chunks, int32_t* replica_stats,
+                           int32_t* status) {
+  __shared__ int overflow;
   extern __shared__ __align__(16) uint8_t lsm[];
   const int Ev = D * m, C = T / PP_CHUNK, tid = threadIdx.x, nt = blockDim.x;
   LayoutSmem S;
@@ -110,19 +112,37 @@ __global__ void __launch_bounds__(kLayoutThreads)
   }
   __syncthreads();
   // phase 2: expert-major segments per rank (ascending expert id, 128-row padding)
+  if (tid == 0) overflow = 0;
+  __syncthreads();
   for (int r = tid; r < D; r += nt) {
-    int off = 0, nrep = 0;
+    int64_t off = 0;
+    int nrep = 0, ng = 0;
     for (int e = 0; e < E; ++e) {
       const int cell = r * E + e;
       const bool pres = S.present[cell];
       if (rep_slot) rep_slot[cell] = (pres && e / m != r) ? m + nrep++ : -1;
-      S.seg[cell] = pres ? off : -1;
+      ng += pres;
+      S.seg[cell] = pres ? (int)off : -1;
       seg_start[cell] = S.seg[cell];
       if (pres) off += (S.rows[cell] + PP_ROW_ALIGN - 1) / PP_ROW_ALIGN * PP_ROW_ALIGN;
     }
-    if (r == me) *total_rows = off;
+    // capacity rule (identical on every rank: same LoadMatrix and mask)
+    const int bits = (off > rows_capacity ? 1 : 0) | (num_slots > 0 && m + nrep > num_slots ? 2 : 0) |
+                     (ng > max_groups ? 4 : 0);
+    if (bits) atomicOr(&overflow, bits);
+    if (r == me) *total_rows = (int)off;
   }
   __syncthreads();
+  if (overflow) {  // drop the step on every rank alike: nothing is stored out of bounds
+    if (tid == 0) {
+      if (status) atomicOr(status, overflow);
+      *num_groups = 0;
+      *total_rows = 0;
+      if (replica_stats) replica_stats[0] = replica_stats[1] = 0;
+    }
+    for (int cell = tid; cell < m * E; cell += nt) slot_dest[cell] = -1;
+    return;
+  }
   if (replica_stats && tid == 0) {
     // [0] replicas of this rank's home experts held elsewhere (Trans pushes out, Agg sources in)
     // [1] replicas this rank holds (Agg pushes out)
@@ -220,6 +240,7 @@ __global__ void __launch_bounds__(256)
     for (int j = 0; j < k; ++j) {
       const int dest = __shfl_sync(0xffffffffu, my_dest, j);
       const int row = __shfl_sync(0xffffffffu, my_row, j);
+      if (dest < 0) continue;  // dropped step (layout capacity flag)
       uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(recv_ptrs[dest]) +
                                             (size_t)row * d);
 #pragma unroll
@@ -258,6 +279,7 @@ __global__ void __launch_bounds__(256)
       const int dest = __shfl_sync(0xffffffffu, my_dest, j);
       const int row = __shfl_sync(0xffffffffu, my_row, j);
       const float wj = __shfl_sync(0xffffffffu, my_w, j);
+      if (dest < 0) continue;  // dropped step
       // fused A2A: the expert outputs were pushed here by the GEMM epilogue, in pair order
       const uint4* src = reinterpret_cast<const uint4*>(
           comb ? comb + (size_t)(t * k + j) * d
@@ -307,6 +329,7 @@ __global__ void __launch_bounds__(256)
       const int dest = __shfl_sync(0xffffffffu, my_dest, j);
       const int row = __shfl_sync(0xffffffffu, my_row, j);
       const float wj = __shfl_sync(0xffffffffu, my_w, j);
+      if (dest < 0) continue;  // dropped step: dw stays 0
       const size_t off = (size_t)row * d;
       const uint4* ysrc = reinterpret_cast<const uint4*>(
           comb ? comb + (size_t)(t * k + j) * d : reinterpret_cast<const __nv_bfloat16*>(out_ptrs[dest]) + off);
@@ -365,6 +388,7 @@ __global__ void __launch_bounds__(256)
     for (int j = 0; j < k; ++j) {
       const int dest = __shfl_sync(0xffffffffu, my_dest, j);
       const int row = __shfl_sync(0xffffffffu, my_row, j);
+      if (dest < 0) continue;  // dropped step
       const uint4* src = reinterpret_cast<const uint4*>(
           comb ? comb + (size_t)(t * k + j) * d
                : reinterpret_cast<const __nv_bfloat16*>(dxp_ptrs[dest]) + (size_t)row * d);
@@ -450,10 +474,11 @@ extern "C" int pp_slot_histogram(const int32_t* chunk_counts, int32_t T, int32_t
 extern "C" int pp_dispatch_layout(int64_t* counts, const uint8_t* mask,
                                   const int32_t* chunk_counts, int32_t D, int32_t m, int32_t E,
                                   int32_t T, int32_t my_rank, int32_t max_groups,
-                                  int32_t rows_capacity, int32_t* chunk_base, int32_t* slot_dest,
-                                  pp_group* groups, int32_t* num_groups, int32_t* total_rows,
-                                  int32_t* seg_start, int32_t* rep_slot, int32_t counts_from_chunks,
-                                  int32_t* replica_stats, void* stream) {
+                                  int32_t rows_capacity, int32_t num_slots, int32_t* chunk_base,
+                                  int32_t* slot_dest, pp_group* groups, int32_t* num_groups,
+                                  int32_t* total_rows, int32_t* seg_start, int32_t* rep_slot,
+                                  int32_t counts_from_chunks, int32_t* replica_stats, int32_t* status,
+                                  void* stream) {
   PP_CHECK_ARG(counts && chunk_counts && chunk_base && slot_dest && groups && num_groups &&
                    total_rows && seg_start,
                "pp_dispatch_layout: null pointer");
@@ -464,6 +489,7 @@ extern "C" int pp_dispatch_layout(int64_t* counts, const uint8_t* mask,
                PP_CHUNK);
   PP_CHECK_ARG(D <= 255, "pp_dispatch_layout: D=%d > 255", D);
   PP_CHECK_ARG(!counts_from_chunks || D == 1, "pp_dispatch_layout: counts_from_chunks needs D == 1");
+  PP_CHECK_ARG(rows_capacity > 0 && num_slots >= 0 && max_groups >= 1, "pp_dispatch_layout: bad capacity");
   const size_t smem = layout_smem_bytes(D, m, E, T);
   PP_CHECK_ARG(smem <= 220 * 1024, "pp_dispatch_layout: E x E and T/128 x E staging too large");
   static int configured[64] = {0};  // per device: largest smem attribute set so far
@@ -475,8 +501,8 @@ extern "C" int pp_dispatch_layout(int64_t* counts, const uint8_t* mask,
     if (dev < 64) configured[dev] = 220 * 1024;
   }
   dispatch_layout_kernel<<<1, kLayoutThreads, smem, as_stream(stream)>>>(
-      counts, mask, chunk_counts, D, m, E, T, my_rank, max_groups, rows_capacity, chunk_base,
-      slot_dest, groups, num_groups, total_rows, seg_start, rep_slot, counts_from_chunks, replica_stats);
+      counts, mask, chunk_counts, D, m, E, T, my_rank, max_groups, rows_capacity, num_slots, chunk_base,
+      slot_dest, groups, num_groups, total_rows, seg_start, rep_slot, counts_from_chunks, replica_stats, status);
   PP_LAUNCH_CHECK();
   return PP_OK;
 }

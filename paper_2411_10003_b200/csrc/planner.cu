@@ -110,6 +110,48 @@ __device__ __forceinline__ int bottom_rank(const int64_t* col, int E, int home, 
   return r;
 }
 
+// Device-side plan_for_iteration gate (pp_planner_cfg.iter_counter): the launch of
+// iteration j plans j+1, so it searches only when (j+1) % reuse_interval == 0.
+__device__ __forceinline__ bool plan_gate_open(const pp_planner_cfg& cfg, int64_t& j) {
+  if (!cfg.iter_counter) return true;
+  j = *(volatile const int64_t*)cfg.iter_counter;
+  const int F = cfg.reuse_interval > 0 ? cfg.reuse_interval : 1;
+  return (j + 1) % F == 0;
+}
+
+// ... and j advances once per launch: the last CTA to finish stores j + 1 (every CTA
+// read j before its arrival, so no CTA can see the advanced value).
+__device__ __forceinline__ void plan_gate_tick(const pp_planner_cfg& cfg, int64_t j) {
+  if (!cfg.iter_counter) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int64_t* ctr = const_cast<int64_t*>(cfg.iter_counter);
+    __threadfence();
+    if (atomicAdd(reinterpret_cast<unsigned long long*>(ctr + 1), 1ull) == gridDim.x - 1) {
+      ctr[1] = 0;
+      ctr[0] = j + 1;
+      __threadfence();
+    }
+  }
+}
+
+// Replica bound (pp_planner_cfg.max_replicas): rank r = row / rows_per_rank gains a
+// replica of expert e when one of its rows that is not e's home rank keeps e's pairs.
+// holder[] / rep[] are shared [ranks]; returns the new maximum over ranks.
+__device__ __forceinline__ int64_t add_replicas(uint8_t* holder, int32_t* rep, int ranks, Red* scratch) {
+  __syncthreads();
+  int64_t v = 0;
+  if ((int)threadIdx.x < ranks) {
+    rep[threadIdx.x] += holder[threadIdx.x];
+    holder[threadIdx.x] = 0;
+    v = rep[threadIdx.x];
+  }
+  struct Max {
+    __device__ Red operator()(Red x, Red y) const { return x.v >= y.v ? x : y; }
+  };
+  return block_reduce(Red{v, 0}, Max(), scratch).v;
+}
+
 __global__ void __launch_bounds__(kMaxPlanThreads) plan_greedy_kernel(PlanArgs a) {
   const int L = blockIdx.x;
   const int E = a.E;
@@ -123,8 +165,21 @@ __global__ void __launch_bounds__(kMaxPlanThreads) plan_greedy_kernel(PlanArgs a
   __shared__ Red scratch[kMaxWarps];
   __shared__ int32_t sel_list[kMaxPlanThreads];
   __shared__ uint8_t used[kMaxPlanThreads];
+  __shared__ uint8_t holder[kMaxPlanThreads];
+  __shared__ int32_t rep[kMaxPlanThreads];
 
-  if (active) used[d] = 0;
+  int64_t iter_j = 0;
+  if (!plan_gate_open(a.cfg, iter_j)) {  // reuse: keep the previous plan's outputs
+    plan_gate_tick(a.cfg, iter_j);
+    return;
+  }
+  const int spr = a.cfg.slots_per_rank > 1 ? a.cfg.slots_per_rank : 1;
+  const int ranks = (E + spr - 1) / spr;
+  if (active) {
+    used[d] = 0;
+    holder[d] = 0;
+    rep[d] = 0;
+  }
 
   // initial (vanilla EP) loads: local[d] = counts[d][d]; remote[d] = sum_{d'!=d} counts[d'][d]
   int64_t local = 0, remote = 0, rowsum = 0;
@@ -173,7 +228,12 @@ __global__ void __launch_bounds__(kMaxPlanThreads) plan_greedy_kernel(PlanArgs a
       if (!excluded) {
         moved = smem_col[d];
         local += moved;
+        if (d / spr != i / spr) holder[d / spr] = 1;
       }
+    }
+    if (a.cfg.max_replicas > 0 && add_replicas(holder, rep, ranks, scratch) > a.cfg.max_replicas) {
+      --s;  // this prefix needs more replica slots than a rank owns: stop before it
+      break;
     }
     const int64_t moved_total = block_reduce(Red{moved, 0}, SumOp(), scratch).v;
     if (d == i) remote -= moved_total;
@@ -218,6 +278,7 @@ __global__ void __launch_bounds__(kMaxPlanThreads) plan_greedy_kernel(PlanArgs a
     a.num_explored[L] = s;
     a.best_cost[L] = best;
   }
+  plan_gate_tick(a.cfg, iter_j);
 }
 
 // ---- physically-faithful E > D planner -------------------------
@@ -261,7 +322,18 @@ __global__ void __launch_bounds__(kMaxPlanThreads) plan_physical_kernel(PhysArgs
   __shared__ Red scratch[kMaxWarps];
   __shared__ int32_t sel_list[kMaxPlanThreads];
   __shared__ int cand_e;
+  __shared__ uint8_t holder[kMaxPlanThreads];
+  __shared__ int32_t rep[kMaxPlanThreads];
 
+  int64_t iter_j = 0;
+  if (!plan_gate_open(a.cfg, iter_j)) {  // reuse: keep the previous plan's outputs
+    plan_gate_tick(a.cfg, iter_j);
+    return;
+  }
+  if (t < D) {
+    holder[t] = 0;
+    rep[t] = 0;
+  }
   const int64_t* counts = a.counts + (size_t)L * a.rows * E;
   for (int x = t; x < D * E; x += blockDim.x) {
     const int d = x / E, e = x - (x / E) * E;
@@ -318,6 +390,7 @@ __global__ void __launch_bounds__(kMaxPlanThreads) plan_physical_kernel(PhysArgs
         rank += (cj < c) || (cj == c && j < t);
       }
       pmask[(size_t)t * E + e] = rank >= n;
+      if (rank >= n) holder[t] = 1;
     }
     __syncthreads();
   };
@@ -347,6 +420,10 @@ __global__ void __launch_bounds__(kMaxPlanThreads) plan_physical_kernel(PhysArgs
     if (e < 0) break;
     ++s;
     apply(e);
+    if (a.cfg.max_replicas > 0 && add_replicas(holder, rep, D, scratch) > a.cfg.max_replicas) {
+      --s;  // this prefix needs more replica slots than a device owns: stop before it
+      break;
+    }
     loads(h, r);
     reduce3(h, r, hmax, hmin, rmax);
     const double changed = objective(a.cm, overlap, rmax.v, hmax.v, s, n);
@@ -376,7 +453,10 @@ __global__ void __launch_bounds__(kMaxPlanThreads) plan_physical_kernel(PhysArgs
     a.num_explored[L] = s;
     a.best_cost[L] = best;
   }
-  if (!a.refine || rpd < 2) return;
+  if (!a.refine || rpd < 2) {
+    plan_gate_tick(a.cfg, iter_j);
+    return;
+  }
   // Opt-in slot refinement (not in the paper; oracle refine_slots): the heaviest device h
   // un-routes the (slot v of h, non-home expert e) batch that minimises
   // max(H[h] - C[v][e], H[home e] + C[v][e]) while that is below H[h]; ties -> lower v, e.
@@ -425,6 +505,7 @@ __global__ void __launch_bounds__(kMaxPlanThreads) plan_physical_kernel(PhysArgs
     a.H[(size_t)L * D + t] = hh;
     a.R[(size_t)L * D + t] = rr;
   }
+  plan_gate_tick(a.cfg, iter_j);
 }
 
 __global__ void derive_loads_kernel(const int64_t* counts, const uint8_t* mask, int D, int E,
@@ -492,6 +573,8 @@ extern "C" int pp_plan_greedy(const int64_t* counts, int32_t num_layers, int32_t
                 cm->num_experts, E, E);
   PP_CHECK_ARG(cfg->n >= 0 && cfg->n < E, "n must be < num_devices=%d, got %d", E, cfg->n);
   PP_CHECK_ARG(cm->top_k >= 1, "top_k must be >= 1");
+  PP_CHECK_ARG(cfg->reuse_interval >= 1, "reuse_interval must be >= 1, got %d", cfg->reuse_interval);
+  PP_CHECK_ARG(cfg->max_replicas >= 0 && cfg->slots_per_rank >= 0, "pp_plan_greedy: bad replica bound");
   PlanArgs a{counts, E, *cm, *cfg, selected, num_selected, num_explored, mask, H, R, best_cost};
   const int threads = ((E + 31) / 32) * 32;
   plan_greedy_kernel<<<num_layers, threads, sizeof(int64_t) * E, as_stream(stream)>>>(a);
@@ -517,6 +600,8 @@ extern "C" int pp_plan_physical(const int64_t* counts, int32_t num_layers, int32
                 cm->num_experts, D, E);
   PP_CHECK_ARG(cfg->n >= 0 && cfg->n < D, "n must be < num_devices=%d, got %d", D, cfg->n);
   PP_CHECK_ARG(cm->top_k >= 1, "top_k must be >= 1");
+  PP_CHECK_ARG(cfg->reuse_interval >= 1, "reuse_interval must be >= 1, got %d", cfg->reuse_interval);
+  PP_CHECK_ARG(cfg->max_replicas >= 0, "pp_plan_physical: bad replica bound");
   PP_CHECK_ARG(!refine_slots || (int64_t)rows * E <= (1 << 20),
                "pp_plan_physical: slot refinement needs rows*E <= 2^20");
   PhysArgs a{counts, rows, D, E, refine_slots ? 1 : 0, *cm, *cfg, selected, num_selected, num_explored,

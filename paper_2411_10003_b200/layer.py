@@ -49,6 +49,10 @@ from .core import ClusterSpec, LoadMatrix, ModelSpec, ValidationError
 from .planner import PlannerConfig
 
 
+class CapacityError(RuntimeError):
+    """A step needed more receive rows / replica slots than the layer allocated."""
+
+
 class _CAI:
     def __init__(self, ptr: int, nbytes: int) -> None:
         self.__cuda_array_interface__ = {
@@ -161,6 +165,11 @@ class MoELayer(torch.nn.Module):
       cluster/model: cost-model specs for the planner (default: default_specs).
       capacity_rows: receive-buffer rows (default: worst case world*tokens*k + E*128,
         i.e. no token is ever dropped).
+      capacity_factor: alternative to capacity_rows: ceil(factor*tokens*k) + E*128 rows
+        (the rows a rank computes under a balanced plan are ~tokens*k).  A step whose layout
+        needs more rows on any rank is dropped on every rank (zero outputs, nothing written
+        out of bounds) and the layer raises CapacityError on its next call or on
+        ``check_status()``.
       max_replicas: replica weight slots per rank (default E - m: any plan fits).
       replica_engine: "copy" (copy-engine peer copies, host-derived from the plan) or
         "sm" (NVLink pushes from SMs, fully device-driven).
@@ -178,7 +187,8 @@ class MoELayer(torch.nn.Module):
                  capacity_rows: int | None = None, max_replicas: int | None = None,
                  seed: int = 0, device=None, trans_ctas: int = 16, replica_engine: str = "copy",
                  policy: str | None = None, planning: str = "host", placement: str = "virtual",
-                 refine_slots: bool = False, fused_a2a: bool = False) -> None:
+                 refine_slots: bool = False, fused_a2a: bool = False,
+                 capacity_factor: float | None = None) -> None:
         super().__init__()
         if not torch.cuda.is_available():
             raise RuntimeError("MoELayer needs a CUDA device (B200); there is no CPU path")
@@ -205,7 +215,14 @@ class MoELayer(torch.nn.Module):
         self.max_replicas = (E - self.m) if max_replicas is None else max_replicas
         self.slots = self.m + (self.max_replicas if D > 1 else 0)
         self.max_groups = min(256, self.m + self.max_replicas)
-        rows = capacity_rows if capacity_rows is not None else D * tokens * top_k + E * _lib.PP_ROW_ALIGN
+        if capacity_rows is not None:
+            rows = capacity_rows
+        elif capacity_factor is not None:
+            if capacity_factor <= 0:
+                raise ValidationError(f"capacity_factor must be > 0, got {capacity_factor}")
+            rows = min(math.ceil(capacity_factor * tokens * top_k), D * tokens * top_k) + E * _lib.PP_ROW_ALIGN
+        else:
+            rows = D * tokens * top_k + E * _lib.PP_ROW_ALIGN
         self.rows_cap = int(math.ceil(rows / _lib.PP_ROW_ALIGN) * _lib.PP_ROW_ALIGN)
         dev = self.device
         g = torch.Generator(device="cpu").manual_seed(seed)
@@ -247,6 +264,11 @@ class MoELayer(torch.nn.Module):
         self.total_rows = torch.zeros((1,), **i32)
         self.seg_start = torch.empty((D, E), **i32)
         self.rep_slot = torch.full((D, E), -1, **i32)
+        # layout status (sticky bits: 1 rows > capacity, 2 replica slots, 4 groups), read
+        # back asynchronously after every eager forward
+        self.status = torch.zeros((1,), **i32)
+        self._status_host = torch.zeros((1,), dtype=torch.int32).pin_memory()
+        self._status_ev = None
         self.pair_dest = torch.empty((T, k), **i32)
         self.pair_row = torch.empty((T, k), **i32)
         self.dw = torch.empty((T, k), dtype=torch.float32, device=dev)
@@ -271,6 +293,8 @@ class MoELayer(torch.nn.Module):
         self.plan_enabled = D > 1
         self.mask_cur = None  # None = vanilla EP for iteration 0
         self._plan_out = _device.PlanBuffers(1, E, dev) if self.plan_enabled else None
+        if self._plan_out is not None:  # a skipped (reused) search leaves the previous mask: start at vanilla EP
+            self._plan_out.mask.copy_(torch.eye(E, dtype=torch.uint8, device=dev).view(1, E, E))
         # placement "virtual": the reference search, bit-exact, over E x E virtual expert
         # slots; "physical": the opt-in E = m*D generalisation over D devices (pp_plan_physical,
         # SURVEY 8(f) row 4) -- its [E][E] output mask repeats each device row over its slots
@@ -288,7 +312,14 @@ class MoELayer(torch.nn.Module):
             if self.planner_cfg.n >= D:
                 raise ValidationError(f"physical placement needs planner n < world size {D}, got {self.planner_cfg.n}")
             self._cm.num_devices = D
-        self._pcfg = _device.planner_cfg(self.planner_cfg)
+        # replica bound inside the search (only when max_replicas < E - m can bind); with
+        # planning="device" the reuse policy is gated on a device iteration counter, so a
+        # captured step that launches the planner every iteration still re-plans every F
+        self._plan_ctr = torch.zeros(2, dtype=torch.int64, device=dev)
+        bound = self.max_replicas if self.max_replicas < E - self.m else 0
+        self._pcfg = _device.planner_cfg(
+            self.planner_cfg, max_replicas=bound, slots_per_rank=self.m if placement == "virtual" else 1,
+            iter_counter=self._plan_ctr if planning == "device" else None)
         self.plan_stream = torch.cuda.Stream(device=dev) if self.plan_enabled else None
         self.comm_stream = torch.cuda.Stream(device=dev) if D > 1 else None
         self.trans_ctas = trans_ctas  # SM-engine Trans pushes
@@ -352,6 +383,11 @@ class MoELayer(torch.nn.Module):
             self.replica_stats = torch.zeros(2, dtype=torch.int32, device=dev)
             self.agg_stage = PeerBuffer((self.m, D - 1, 2, d_ff * d_model), torch.float32, self.group, dev)
             self.comm_barrier = _Barrier(self.group, dev)
+        elif D > 1:
+            # copy engine: the replicas pull the home weights; a barrier on the comm stream
+            # orders the pulls after every home's optimizer step (stream order of this rank's
+            # forward start + arrival of every peer at the same point)
+            self.comm_barrier = _Barrier(self.group, dev)
         self._plan_pending = None
         self._mask_host = torch.zeros((E, E), dtype=torch.uint8).pin_memory() if D > 1 else None
         self.mask_cur_host = None
@@ -360,7 +396,7 @@ class MoELayer(torch.nn.Module):
         self._agg_ranges = None   # device int32 [m+1]
         self._agg_staging = None
         self._trans_done = None
-        self._trans_issued = True
+        self._trans_iter = -1     # iteration whose Trans has been issued
         self.replica_experts = []  # replica experts held by this rank under the current plan
         self.barrier = _Barrier(self.group, dev)
         self.history = []  # host copies of LoadMatrix per iteration (optional, record_history)
@@ -425,13 +461,40 @@ class MoELayer(torch.nn.Module):
             self.mask_cur = self._topm_mask
         mask_ptr = self.mask_cur.data_ptr() if self.mask_cur is not None else None
         _lib.call("pp_dispatch_layout", self.counts.data_ptr(), mask_ptr, self.chunk_counts.data_ptr(),
-                  self.world, m, E, T, self.rank, self.max_groups, self.rows_cap,
+                  self.world, m, E, T, self.rank, self.max_groups, self.rows_cap, self.slots,
                   self.chunk_base.data_ptr(), self.slot_dest.data_ptr(), self.groups.data_ptr(),
                   self.num_groups.data_ptr(), self.total_rows.data_ptr(), self.seg_start.data_ptr(),
                   self.rep_slot.data_ptr(), 1 if self.world == 1 else 0,
-                  self.replica_stats.data_ptr() if self.trans_flags is not None else None, sp)
+                  self.replica_stats.data_ptr() if self.trans_flags is not None else None,
+                  self.status.data_ptr(), sp)
         if self.record_history:
             self.history.append(self.counts.clone())
+        if not torch.cuda.is_current_stream_capturing():
+            self._status_host.copy_(self.status, non_blocking=True)
+            self._status_ev = torch.cuda.Event()
+            self._status_ev.record()
+
+    def _poll_status(self) -> None:
+        """Raise CapacityError if an earlier step's layout was dropped (non-blocking)."""
+        if self._status_ev is not None and self._status_ev.query() and int(self._status_host[0]):
+            self._raise_status(int(self._status_host[0]))
+
+    def check_status(self) -> None:
+        """Synchronous check of the layout status (call e.g. after graph replays)."""
+        st = int(self.status.item())
+        if st:
+            self._raise_status(st)
+
+    def _raise_status(self, st: int) -> None:
+        why = []
+        if st & 1:
+            why.append(f"a rank needed more than rows_capacity={self.rows_cap} receive rows")
+        if st & 2:
+            why.append(f"a rank needed more than {self.slots - self.m} replica weight slots")
+        if st & 4:
+            why.append(f"a rank needed more than max_groups={self.max_groups} expert groups")
+        raise CapacityError("MoE layer step dropped (outputs are zero): " + "; ".join(why) +
+                            " -- raise capacity_factor / max_replicas")
 
     def _launch_planner(self) -> None:
         """plan_for_iteration rule: iteration j+1 searches on iteration j's load
@@ -441,9 +504,9 @@ class MoELayer(torch.nn.Module):
         if not self.plan_enabled:
             return
         nxt = self.iteration + 1
-        if nxt % self.planner_cfg.reuse_interval != 0:
+        if self.planning != "device" and nxt % self.planner_cfg.reuse_interval != 0:
             return
-        if self.planning == "device":
+        if self.planning == "device":  # launched every iteration; the kernel applies the reuse rule
             self._counts_snap.copy_(self.counts)  # the next iteration overwrites self.counts
             ev = torch.cuda.Event()
             ev.record()
@@ -504,7 +567,6 @@ class MoELayer(torch.nn.Module):
         mh = self._mask_host.numpy().astype(bool)
         self.mask_cur_host = mh.copy()
         self._derive_replicas(mh)
-        self._trans_issued = False
 
     def _derive_replicas(self, mh: np.ndarray) -> None:
         D, m, E, me = self.world, self.m, self.E, self.rank
@@ -554,13 +616,14 @@ class MoELayer(torch.nn.Module):
         """K5 Trans for this iteration's plan on the side stream (once per iteration).
         Ordered after everything already on the current stream (e.g. an optimizer
         step); returns the completion event (None if nothing to move)."""
-        if self._trans_issued:
+        # once per iteration: the home weights change with every optimizer step, so the
+        # replicas are refreshed every iteration even when the plan is reused (the reference
+        # charges Trans every iteration, simulator.py placement_for / cost_fn)
+        if self._trans_iter == self.iteration:
             return self._trans_done
-        self._trans_issued = True
+        self._trans_iter = self.iteration
         self._trans_done = None
         if self.world == 1 or self.mask_cur is None:
-            return None
-        if self.replica_engine == "copy" and not self.replica_experts:
             return None
         ev = torch.cuda.Event()
         ev.record()
@@ -568,6 +631,8 @@ class MoELayer(torch.nn.Module):
             self.comm_stream.wait_event(ev)
             t0 = self._side_event(self.comm_stream)
             if self.replica_engine == "copy":
+                # every rank (replica holder or not) arrives: the homes' weights are final
+                self.comm_barrier(self.comm_stream)
                 split = getattr(self, "trans_split_bytes", None)
                 if split:  # Algorithm 2 partition: SubTrans2 (FNEC window) first, then SubTrans1
                     first, rest = self._split_copies(self._trans_list, split)
@@ -582,7 +647,7 @@ class MoELayer(torch.nn.Module):
                 # W1 first (FWD1's replica tiles wait on flag row 0), then W2 (FWD2's, row 1)
                 for part, row in ((1, 0), (2, 1)):
                     _lib.call("pp_replica_trans", self.w1_arena.ptrs.data_ptr(), self.w2_arena.ptrs.data_ptr(),
-                              self.mask_cur.data_ptr(), self.E, self.m, self.rank, self.d, self.f, part,
+                              self.mask_cur.data_ptr(), self.E, self.m, self.rank, self.slots, self.d, self.f, part,
                               self.trans_flags.ptrs.data_ptr(), row, self._epoch_ptr(),
                               self._trans_ctr.data_ptr(), self.trans_ctas, _device.stream_ptr(self.comm_stream))
             self._trans_done = torch.cuda.Event()
@@ -647,7 +712,7 @@ class MoELayer(torch.nn.Module):
                 nctas = self.agg_ctas_w2 if parts == 2 else self.agg_ctas
                 _lib.call("pp_replica_agg", self.g1_arena.ptrs.data_ptr(), self.g2_arena.ptrs.data_ptr(),
                           self.agg_stage.ptrs.data_ptr(), self.mask_cur.data_ptr(), self.E, self.m, self.rank,
-                          self.d, self.f, parts, nctas, cs)
+                          self.slots, self.d, self.f, parts, nctas, cs)
                 self.comm_barrier(self.comm_stream)  # every replica's grads have landed here
                 _lib.call("pp_replica_agg_reduce", self.g1_arena.local.data_ptr(), self.g2_arena.local.data_ptr(),
                           self.agg_stage.local.data_ptr(), self.mask_cur.data_ptr(), self.E, self.m, self.rank,
@@ -712,11 +777,8 @@ class MoELayer(torch.nn.Module):
             torch.cuda.current_stream().wait_event(self._agg_done)
             self._agg_done = None
         self._mark("fwd_start")
+        self._poll_status()
         self.begin_iteration()
-        if self.planning == "device" and self.world > 1:
-            self._trans_issued = False  # the device-side plan may change every iteration
-        if self.top_m:
-            self._trans_issued = False  # top-m: this iteration's mask exists only after the histogram
         # copy engine: host-derived copies start before routing and must land before FEC;
         # SM engine: the home ranks push after barrier 1, overlapping FWD1 on the home experts,
         # and each receiver's FWD1 gates only its replica tiles on the pushers' completion flags
@@ -842,8 +904,6 @@ class MoELayer(torch.nn.Module):
         rank captures and replays in lockstep)."""
         if self.world != 1 and self.planning != "device":
             raise ValidationError("make_graphed_step at D > 1 needs planning='device'")
-        if self.plan_enabled and self.world > 1 and self.planner_cfg.reuse_interval != 1:
-            raise ValidationError("make_graphed_step: the captured step re-plans every iteration (reuse_interval=1)")
         return GraphedStep(self, x, dy, with_loss, gemm_events)
 
     # ---- introspection (LoadMatrix / placement of the last call) -------------
@@ -937,6 +997,7 @@ class GraphedStep:
             self.y = layer.forward_raw(x)
             self.loss = layer.probe_loss(self.y, dy) if with_loss else None
             self.dx = layer.backward_raw(x, dy)
+        layer.iteration -= 1  # the capture ran no kernels: replays count the iterations
         if gemm_events:
             self.gemm_events = layer.gemm_timing
         layer.gemm_timing, layer.phase_log, layer.gemm_event_pool = saved_timing, saved_phase, saved_pool

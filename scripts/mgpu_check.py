@@ -28,9 +28,19 @@ def rel(a, b):
 def main():
     rank = int(os.environ["RANK"])
     world = int(os.environ["WORLD_SIZE"])
-    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)))
+    ngpu = torch.cuda.device_count()
+    # emulated ranks: fewer GPUs than ranks -> several rank processes share a device
+    # (CUDA IPC between processes on one device; time-sliced contexts make the spin
+    # barriers progress); NCCL refuses duplicate devices, so the plumbing uses gloo
+    emulated = ngpu < world
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)) % ngpu)
     dev = torch.device("cuda", torch.cuda.current_device())
-    dist.init_process_group("nccl", device_id=dev)
+    if emulated:
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("cpu:gloo,cuda:nccl", device_id=dev)
+    if rank == 0:
+        print(f"ranks {world} on {ngpu} GPU(s){' (emulated: shared device)' if emulated else ''}", flush=True)
     E = int(os.environ.get("PP_E", 4 * world))
     T, d, f, k = int(os.environ.get("PP_T", 2048)), 256, 512, 2
     m = E // world
@@ -38,8 +48,10 @@ def main():
     mo = pp.ModelSpec(E, 1, k, 2 * d, 1e3, 1e3)
     placement = os.environ.get("PP_PLACEMENT", "virtual")
     n_excl = int(os.environ.get("PP_N", "1" if placement == "virtual" else "0"))
+    reuse = int(os.environ.get("PP_REUSE", "1"))
+    iters = 3 if reuse == 1 else 5
     layer = pp.MoELayer(d, f, E, k, tokens=T, group=dist.group.WORLD,
-                        planner=pp.PlannerConfig(n=n_excl, alpha=0.5), cluster=cl, model=mo, seed=0,
+                        planner=pp.PlannerConfig(n=n_excl, alpha=0.5, reuse_interval=reuse), cluster=cl, model=mo, seed=0,
                         placement=placement, refine_slots=os.environ.get("PP_REFINE") == "1",
                         fused_a2a=os.environ.get("PP_FUSED") == "1",
                         replica_engine=os.environ.get("PP_ENGINE", "copy"),
@@ -57,13 +69,14 @@ def main():
     w1_all = (torch.randn((E, f, d), generator=g) / math.sqrt(d)).to(torch.bfloat16)
     w2_all = (torch.randn((E, d, f), generator=g) / math.sqrt(f)).to(torch.bfloat16)
     ok = True
-    prev_counts = None
-    for it in range(3):
+    hist = []
+    for it in range(iters):
         x, _ = M.exact_inputs(T, d, E, seed=1000 * it + rank)
         dy = (torch.randn((T, d), generator=torch.Generator().manual_seed(7 + it * 31 + rank)) * 0.1).to(torch.bfloat16)
         xd = x.to(dev).requires_grad_(True)
         y = layer(xd)
-        mask_used = layer.current_mask() if (it > 0 or policy.startswith("top")) else None  # plan used
+        anchor = (it // reuse) * reuse  # plan_for_iteration (planner.py:148-156)
+        mask_used = layer.current_mask() if (anchor > 0 or policy.startswith("top")) else None  # plan used
         y.backward(dy.to(dev))
         layer.wait_grads()
         torch.cuda.synchronize()
@@ -82,8 +95,9 @@ def main():
                     ok = False
             elif policy == "vanilla":
                 pass
-            elif it > 0:
-                # plan_for_iteration: iteration it uses greedy(history[it-1])
+            elif anchor > 0:
+                # plan_for_iteration: iteration it uses greedy(history[anchor-1])
+                prev_counts = hist[anchor - 1]
                 if placement == "physical":
                     cm = P.cost_model_dict(world, k, 2 * d, 1e3, 1e3, 1e11, 1e6)
                     phys = prev_counts.reshape(world, m, E).sum(axis=1)
@@ -125,8 +139,14 @@ def main():
             if e > 1e-2:
                 print(f"[it {it}] gate grad rel err {e}", flush=True); ok = False
             print(f"[it {it}] checked {world} ranks: {'OK' if ok else 'FAIL'}", flush=True)
-            prev_counts = counts
-        okt = torch.tensor([1 if ok else 0], device=dev)
+            hist.append(counts)
+        # "optimizer step": exact power-of-two rescale of the home experts, so a replica that
+        # is not refreshed by this iteration's Trans shows up as an output mismatch
+        with torch.no_grad():
+            layer.w1.mul_(2.0)
+            layer.w2.mul_(0.5)
+        w1_all, w2_all = w1_all * 2.0, w2_all * 0.5
+        okt = torch.tensor([1 if ok else 0])
         dist.broadcast(okt, 0)
         ok = bool(okt.item())
     if layer.planning == "device":
@@ -146,7 +166,7 @@ def main():
         torch.cuda.synchronize()
         got = (yg, dxg, layer.w1.main_grad, layer.w2.main_grad)
         same = all(torch.equal(a, b) for a, b in zip(ref_out, got))
-        flag = torch.tensor([1 if same else 0], device=dev)
+        flag = torch.tensor([1 if same else 0])
         dist.all_reduce(flag, op=dist.ReduceOp.MIN)
         if rank == 0:
             print(f"[graph] replay == eager on {world} ranks: {'OK' if flag.item() else 'FAIL'}", flush=True)

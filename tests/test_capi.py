@@ -81,9 +81,9 @@ def test_new_entry_points_validate_before_device_work():
     rc = lib.pp_plan_physical(z, 1, 6, 4, 16, ctypes.byref(cm), ctypes.byref(cfg), 0, z, z, z, z, z, z, z, None)
     assert rc == _lib.PP_EINVAL  # rows not a multiple of D
     # replica kernels: rank out of range, bad parts
-    assert lib.pp_replica_trans(z, z, z, 16, 4, 4, 256, 256, 3, None, 0, None, None, 0, None) == _lib.PP_EINVAL
-    assert lib.pp_replica_trans(z, z, z, 16, 4, 0, 256, 256, 3, z, 0, None, None, 0, None) == _lib.PP_EINVAL
-    assert lib.pp_replica_trans(z, z, z, 16, 4, 0, 256, 256, 4, None, 0, None, None, 0, None) == _lib.PP_EINVAL
+    assert lib.pp_replica_trans(z, z, z, 16, 4, 4, 8, 256, 256, 3, None, 0, None, None, 0, None) == _lib.PP_EINVAL
+    assert lib.pp_replica_trans(z, z, z, 16, 4, 0, 8, 256, 256, 3, z, 0, None, None, 0, None) == _lib.PP_EINVAL
+    assert lib.pp_replica_trans(z, z, z, 16, 4, 0, 8, 256, 256, 4, None, 0, None, None, 0, None) == _lib.PP_EINVAL
     # pp_grouped_gemm_ex: the gate serves FWD1/FWD2 and needs its epoch; the scatter FWD2/DGRAD1;
     # the adaptive reservation needs hi >= lo
     nores = (None, 0, 0, 0, 0)

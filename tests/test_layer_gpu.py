@@ -105,6 +105,32 @@ def test_layer_vs_oracle(T, d, f, E, k, fused):
     close(layer.wg.main_grad, dwg, rtol=1e-2, what="dWg")
 
 
+@pytest.mark.parametrize("T,d,f,E,k", [(16384, 1024, 4096, 16, 2), (8192, 2048, 4096, 32, 2), (8192, 2048, 4096, 64, 1)],
+                         ids=["cfg2", "cfg3-d2048-E32", "cfg4-E64-top1"])
+def test_layer_vs_oracle_baseline_shapes(T, d, f, E, k):
+    """The BASELINE layer shapes (cfg2 exactly; the d=2048 configs at 8K tokens so the CPU
+    oracle stays in seconds): exact-arithmetic routing under a Zipf(1.2) gate bias, the
+    integer contract bit-exact, outputs and gradients within the bf16 tolerances."""
+    bias = torch.log(torch.tensor([1.0 / (i + 1) ** 1.2 for i in range(E)]))
+    bias = torch.round(bias * 4) / 4
+    torch.set_num_threads(max(1, __import__("os").cpu_count() or 1))
+    layer, x, wg, dy, y, dx = run_layer(T, d, f, E, k, bias=bias, seed=E + d)
+    ref = M.LayerRef(layer.w1.detach().cpu(), layer.w2.detach().cpu(), wg, bias, k, D=1)
+    ys, st = ref.forward([x])
+    assert np.array_equal(layer.idx.cpu().numpy(), st["routes"][0][1].numpy())
+    assert np.array_equal(layer.counts.cpu().numpy(), st["hist"])
+    dest, row = st["pos"][0]
+    assert np.array_equal(layer.pair_row.cpu().numpy(), row)
+    assert np.array_equal(layer.pair_dest.cpu().numpy(), dest)
+    close(y, ys[0], what="y")
+    dxs, dw1, dw2, dwg, dws = ref.backward([dy], st)
+    close(dx, dxs[0], what="dx")
+    close(layer.w1.main_grad, dw1, rtol=1e-2, what="dW1")
+    close(layer.w2.main_grad, dw2, rtol=1e-2, what="dW2")
+    close(layer.wg.main_grad, dwg, rtol=1e-2, what="dWg")
+    layer.close()
+
+
 def test_layer_repeatable_and_iteration_counter():
     layer, x, wg, dy, y1, dx1 = run_layer(2048, 256, 512, 16, 2, seed=1)
     y2 = layer(x.to(layer.device))
@@ -151,3 +177,24 @@ def test_fused_a2a_bit_identical_to_unfused():
             assert sorted(seen) == list(range(2048 * 2))
     for a, b in zip(*outs):
         assert torch.equal(a, b)
+
+
+def test_capacity_overflow_drops_step_and_raises():
+    """A receive capacity below the rows a step needs: the step is dropped (zero outputs,
+    nothing written out of bounds) and the layer raises CapacityError."""
+    import paper_2411_10003_b200 as pp
+
+    T, d, f, E, k = 1024, 256, 512, 8, 2
+    layer = pp.MoELayer(d, f, E, k, tokens=T, seed=0, capacity_factor=0.5)
+    x = torch.randn((T, d), device="cuda").to(torch.bfloat16)
+    y = layer.forward_raw(x)
+    torch.cuda.synchronize()
+    assert float(y.float().abs().max()) == 0.0
+    with pytest.raises(pp.CapacityError):
+        layer.check_status()
+    with pytest.raises(pp.CapacityError):
+        layer.forward_raw(x)  # the next call raises from the asynchronous read-back
+    ok = pp.MoELayer(d, f, E, k, tokens=T, seed=0, capacity_factor=1.0)
+    y = ok.forward_raw(x)
+    ok.check_status()
+    assert float(y.float().abs().max()) > 0.0

@@ -220,3 +220,86 @@ def test_physical_planner_slot_refinement_vs_oracle(D, m):
         assert out.mask[0].cpu().numpy().astype(bool).tolist() == S.tolist(), i
         assert out.H[0, :D].cpu().tolist() == H.tolist() and out.R[0, :D].cpu().tolist() == R.tolist()
         assert out.selected[0, : int(out.num_selected[0])].cpu().tolist() == list(exp["selected"])
+
+
+# ---- extensions of pp_planner_cfg: replica bound and the device-side reuse gate ------------
+
+def _launch(slot, D, m, cfg, physical, max_replicas=0, ctr=None):
+    import torch
+
+    from paper_2411_10003_b200 import _device
+
+    E = D * m
+    rows = slot.shape[0]
+    cm = P.cost_model_dict(D if physical else E, 2, 2048, 1.6e7, 3.2e7, 4e11, 1e8)
+    cl = pp.ClusterSpec(cm["num_devices"], cm["avg_bandwidth"], cm["compute_throughput"])
+    mo = pp.ModelSpec(E, 1, 2, cm["input_bytes"], cm["expert_param_bytes"], cm["expert_grad_bytes"])
+    out = _device.PlanBuffers(1, E, torch.device("cuda", 0))
+    out.mask.fill_(7)
+    c = _device.planner_cfg(cfg, max_replicas=max_replicas, slots_per_rank=1 if physical else m,
+                            iter_counter=ctr)
+    _device.launch_plan(torch.from_numpy(slot).cuda().view(1, rows, E), out, _device.cost_model(cl, mo, None if physical else E),
+                        c, physical_devices=D if physical else 0)
+    torch.cuda.synchronize()
+    return out, cm
+
+
+@pytest.mark.parametrize("physical", [False, True])
+def test_planner_replica_bound_vs_oracle(physical):
+    """max_replicas (weight slots a rank owns): the search stops before the first prefix that
+    gives a rank more replicas; equal to the oracle restatement, and equal to the unbounded
+    (reference) search whenever the bound does not bind."""
+    D, m = 4, 4
+    E = D * m
+    rng = np.random.default_rng(4242 + physical)
+    bound_hit = 0
+    for i in range(30):
+        p = rng.dirichlet(np.ones(E) * (0.1 + 0.1 * (i % 3)))
+        slot = np.stack([rng.multinomial(512, p) for _ in range(E)]).astype(np.int64)
+        cap = 1 + i % 4
+        cfg = pp.PlannerConfig(n=1, alpha=0.2, overlap_aware=bool(i % 2))
+        out, cm = _launch(slot, D, m, cfg, physical, max_replicas=cap)
+        if physical:
+            phys = slot.reshape(D, m, E).sum(axis=1)
+            exp = P.greedy_search_physical(phys, 1, 0.2, bool(i % 2), cm, max_replicas=cap)
+            free = P.greedy_search_physical(phys, 1, 0.2, bool(i % 2), cm)
+            exp_mask = np.repeat(exp["mask"], m, axis=0)
+            reps = P.replicas_per_rank(exp["mask"], 1, m)
+        else:
+            exp = P.greedy_search(slot, 1, 0.2, bool(i % 2), cm, max_replicas=cap, slots_per_rank=m)
+            free = P.greedy_search(slot, 1, 0.2, bool(i % 2), cm)
+            exp_mask = exp["mask"]
+            reps = P.replicas_per_rank(exp["mask"], m, m)
+        assert reps.max() <= cap
+        got = out.selected[0, : int(out.num_selected[0])].cpu().tolist()
+        assert got == list(exp["selected"]), i
+        assert out.mask[0].cpu().numpy().astype(bool).tolist() == exp_mask.tolist()
+        assert int(out.num_explored[0]) == exp["explored"]
+        if exp["explored"] == free["explored"]:
+            assert list(exp["selected"]) == list(free["selected"])
+        else:
+            bound_hit += 1
+    assert bound_hit > 0  # the bound did bind in some cases
+
+
+def test_planner_reuse_gate_device_counter():
+    """iter_counter: the launch of iteration j searches only when (j+1) % F == 0, leaves every
+    output untouched otherwise, and advances j by one either way (plan_for_iteration,
+    planner.py:132-156, inside a replayable launch)."""
+    import torch
+
+    D, m = 4, 1
+    E = D * m
+    rng = np.random.default_rng(3)
+    slot = np.stack([rng.multinomial(512, rng.dirichlet(np.ones(E) * 0.2)) for _ in range(E)]).astype(np.int64)
+    ctr = torch.zeros(2, dtype=torch.int64, device="cuda")
+    cfg = pp.PlannerConfig(n=1, alpha=0.2, reuse_interval=3)
+    for j in range(7):
+        out, cm = _launch(slot, D, m, cfg, False, ctr=ctr)
+        searched = (j + 1) % 3 == 0
+        assert int(ctr[0]) == j + 1 and int(ctr[1]) == 0
+        if searched:
+            exp = P.greedy_search(slot, 1, 0.2, False, cm)
+            assert out.mask[0].cpu().numpy().astype(bool).tolist() == exp["mask"].tolist()
+        else:
+            assert (out.mask == 7).all()  # untouched
