@@ -212,30 +212,35 @@ int pp_combine(void* const* out_ptrs, const int32_t* pair_dest, const int32_t* p
                const float* w, int32_t T, int32_t d, int32_t k, void* y, const void* comb,
                void* stream);
 
-/* Backward of combine: dw[t][j] = <dy[t], Yp[pair]> ; dYp[pair] = w[t][j]*dy[t]
- * (pushed to dgrad_ptrs[pair_dest]); zero-fills own padding rows of own_dgrad.
+/* Backward of combine + gate softmax: dw[t][j] = <dy[t], Yp[pair]> ; dYp[pair] = w[t][j]*dy[t]
+ * (pushed to dgrad_ptrs[pair_dest]); zero-fills own padding rows of own_dgrad; and
+ * dl [T][EP] bf16 = dL/dlogits restricted to the top-k (dl_i = p_i * (dw_{j(i)} [i
+ * selected] - sum_j dw_j p_{e_j})), zero-padded to EP in {64, 128} columns for the
+ * tensor-core gate GEMMs (idx [T][k], probs [T][E]).
  * comb != NULL: Yp[pair] is read locally from comb[t*k + j] (fused-A2A mode). */
 int pp_combine_bwd(const void* dy, void* const* out_ptrs, void* const* dgrad_ptrs, void* own_dgrad,
                    const int32_t* pair_dest, const int32_t* pair_row, const float* w,
                    const pp_group* groups, const int32_t* num_groups, int32_t max_groups,
-                   int32_t T, int32_t d, int32_t k, float* dw, const void* comb, void* stream);
+                   int32_t T, int32_t d, int32_t k, float* dw, const void* comb,
+                   const int32_t* idx, const float* probs, int32_t E, int32_t EP, void* dl, void* stream);
 
-/* Backward of dispatch + gate softmax:  dx[t] = sum_j dXp[pair] (pulled from
- * dxp_ptrs[pair_dest]) and dl [T][EP] bf16 = dL/dlogits restricted to the top-k
- * (dl_i = p_i * (dw_{j(i)} [i selected] - sum_j dw_j p_{e_j})), zero-padded to
- * EP in {64, 128} columns for the tensor-core gate GEMMs.  comb != NULL: the
- * dXp rows were pushed here by the DGRAD1 epilogue, comb[t*k + j] (local).  Also zeroes
- * zero_f32[0:zero_elems) (the gate weight grad the split-K GEMM accumulates into). */
-int pp_dispatch_bwd(void* const* dxp_ptrs, const int32_t* pair_dest, const int32_t* pair_row,
-                    const int32_t* idx, const float* probs, const float* dw,
-                    int32_t T, int32_t d, int32_t k, int32_t E, int32_t EP, void* dx, void* dl,
-                    float* zero_f32, int64_t zero_elems, const void* comb, void* stream);
+/* Backward of dispatch + the gate's input gradient in ONE tcgen05 kernel:
+ *   dx [T][d] bf16 = dl [T][EP] . wg [E][d]  +  sum_j dXp[pair(t, j)]
+ * the MMA gives the gate term in TMEM, the epilogue gathers the k expert-input
+ * gradient rows (peer loads from dxp_ptrs[pair_dest] at pair_row, or comb[t*k + j]
+ * locally in fused-A2A mode), adds in fp32 and stores dx once.  Pairs with
+ * pair_dest < 0 (dropped step) contribute nothing. */
+int pp_gate_dx(const void* dl, const void* wg, void* const* dxp_ptrs, const void* comb,
+               const int32_t* pair_dest, const int32_t* pair_row, int32_t T, int32_t d, int32_t k,
+               int32_t E, int32_t EP, void* dx, void* stream);
 
-/* Gate GEMMs on tcgen05:  dx [T][d] bf16 += dl [T][EP] . wg [E][d]   and
- * dwg [E][d] fp32 += dl^T . x (split-K over token chunks, fp32 atomics;
- * caller zeroes dwg). */
-int pp_gate_bwd(const void* dl, const void* wg, const void* x, int32_t T, int32_t d, int32_t E,
-                int32_t EP, void* dx, float* dwg, void* stream);
+/* Gate weight gradient, deterministic: dwg [E][d] fp32 = dl^T . x, split-K over
+ * token chunks on tcgen05 into workspace [splits][128][d] fp32 (no atomics), then
+ * the splits are summed in a fixed order (overwrites dwg).  workspace must hold
+ * pp_gate_dw_workspace_bytes(T, d) bytes. */
+int pp_gate_dw(const void* dl, const void* x, int32_t T, int32_t d, int32_t E, int32_t EP,
+               float* workspace, float* dwg, void* stream);
+int64_t pp_gate_dw_workspace_bytes(int32_t T, int32_t d);
 
 /* ---- grouped expert GEMM on tcgen05 (K4) -------------------------------- */
 #define PP_GEMM_FWD1 0   /* pre,act[rows][f] = GeLU-split( Xp[rows][d] . W1[slot][f][d]^T ) */
@@ -271,7 +276,7 @@ int pp_dot_bf16(const void* a, const void* b, int64_t n, float* partial, float* 
  *   scatter_ptrs[o / pairs_per_rank] ([T*k][d] bf16), o = origin[r] as written
  *   by pp_dispatch (origin_ptrs; padding rows -1, not stored) -- one 64-B bulk
  *   copy per row chunk from the staging smem, overlapping the remaining tiles'
- *   MMAs; pp_combine / pp_dispatch_bwd then read comb locally.  c may be NULL.
+ *   MMAs; pp_combine / pp_gate_dx then read comb locally.  c may be NULL.
  * Replica gate (gate_flags != NULL; FWD1 / FWD2 while Trans is in flight): the
  *   home groups (wslot < first_replica_slot) are scheduled first; before the
  *   first replica tile's loads the TMA producer waits until gate_flags[r] >=

@@ -72,9 +72,10 @@ SIGNATURES = {
     "pp_dispatch_layout": [P, P, P, I, I, I, I, I, I, I, I, P, P, P, P, P, P, P, I, P, P, P],
     "pp_dispatch": [P, P, P, P, P, I, I, I, I, I, P, P, P, P, I, P, P, P, I, P],
     "pp_combine": [P, P, P, P, I, I, I, P, P, P],
-    "pp_combine_bwd": [P, P, P, P, P, P, P, P, P, I, I, I, I, P, P, P],
-    "pp_dispatch_bwd": [P, P, P, P, P, P, I, I, I, I, I, P, P, P, ctypes.c_int64, P, P],
-    "pp_gate_bwd": [P, P, P, I, I, I, I, P, P, P],
+    "pp_combine_bwd": [P, P, P, P, P, P, P, P, P, I, I, I, I, P, P, P, P, I, I, P, P],
+    "pp_gate_dx": [P, P, P, P, P, P, I, I, I, I, I, P, P],
+    "pp_gate_dw": [P, P, I, I, I, I, P, P, P],
+    "pp_gate_dw_workspace_bytes": [I, I],
     "pp_grouped_gemm": [I, P, P, P, P, P, P, I, I, I, I, I, I, P],
     "pp_grouped_gemm_ex": [I, P, P, P, P, P, P, I, I, I, I, I, P, P, I, P, P, I, I, I, P, I, I, I, I, I, P],
     "pp_replica_trans": [P, P, P, I, I, I, I, I, I, I, P, I, P, P, I, P],
@@ -90,6 +91,8 @@ SIGNATURES = {
     "pp_ipc_close": [P],
     "pp_peer_barrier": [P, I, I, c_uint64, P],
 }
+
+RESTYPE_I64 = {"pp_gate_dw_workspace_bytes"}
 
 _lib = None
 
@@ -110,7 +113,7 @@ def load():
     for name, argtypes in SIGNATURES.items():
         fn = getattr(lib, name)
         fn.argtypes = argtypes
-        fn.restype = c_int32
+        fn.restype = ctypes.c_int64 if name in RESTYPE_I64 else c_int32
     _lib = lib
     return lib
 
@@ -137,7 +140,7 @@ def check(rc: int, what: str = "") -> None:
 KERNELS_PER_CALL = {
     "pp_plan_greedy": 1, "pp_plan_physical": 1, "pp_derive_loads": 1, "pp_top_m_mask": 1, "pp_route_topk": 1, "pp_slot_histogram": 1,
     "pp_dispatch_layout": 1, "pp_dispatch": 1, "pp_combine": 1, "pp_combine_bwd": 1,
-    "pp_dispatch_bwd": 1, "pp_gate_bwd": 2, "pp_grouped_gemm": 1, "pp_grouped_gemm_ex": 1, "pp_replica_trans": 1,
+    "pp_gate_dx": 1, "pp_gate_dw": 2, "pp_grouped_gemm": 1, "pp_grouped_gemm_ex": 1, "pp_replica_trans": 1,
     "pp_replica_agg": 1, "pp_replica_agg_reduce": 1, "pp_dot_bf16": 2, "pp_peer_barrier": 1, "pp_agg_accumulate": 1,
 }
 _launches = [0]

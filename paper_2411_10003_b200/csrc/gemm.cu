@@ -40,7 +40,8 @@ constexpr int kMaxGroups = 256;
 constexpr int kTraceSteps = 1024;
 
 
-enum Epi { EPI_BF16 = 0, EPI_GELU = 1, EPI_DGELU = 2, EPI_F32 = 3, EPI_ROUTE = 4, EPI_BF16_ADD = 5, EPI_F32_ATOMIC = 6 };
+enum Epi { EPI_BF16 = 0, EPI_GELU = 1, EPI_DGELU = 2, EPI_F32 = 3, EPI_ROUTE = 4, EPI_BF16_ADD = 5, EPI_F32_ATOMIC = 6,
+           EPI_GATHER = 7 };
 
 // per-epilogue-warp staging for the TMA-store epilogue: a ring of out_bufs 32x32
 // blocks (bf16: 2 KB, SWIZZLE_64B; fp32: one 4 KB block, SWIZZLE_128B), so a warp
@@ -50,7 +51,7 @@ enum Epi { EPI_BF16 = 0, EPI_GELU = 1, EPI_DGELU = 2, EPI_F32 = 3, EPI_ROUTE = 4
 // load + GeLU') get deeper rings; the long-K ones keep one block and more stages.
 template <int EPI>
 constexpr int out_bufs() {
-  return EPI == EPI_GELU ? 3 : EPI == EPI_DGELU ? 2 : 1;
+  return EPI == EPI_GELU ? 3 : (EPI == EPI_DGELU || EPI == EPI_GATHER) ? 2 : 1;
 }
 template <int EPI>
 constexpr int out_base() {
@@ -100,6 +101,17 @@ struct GemmParams {
   const uint64_t* gate_flags;
   const uint64_t* gate_epoch;
   int gate_me, gate_D, gate_slot0;
+  // EPI_GATHER (gate dX + dispatch backward): output row t also receives sum_j of the
+  // rows pair (t, j) points at: gather_ptrs[pair_dest][pair_row] (peer memory), or
+  // gather_comb[t*topk + j] when the rows were pushed here (fused A2A)
+  void* const* gather_ptrs;
+  const __nv_bfloat16* gather_comb;
+  const int32_t* pair_dest;
+  const int32_t* pair_row;
+  // bf16 epilogue I/O through the LSUs (st.global / ld.global via an smem transpose)
+  // instead of TMA stores / loads: the SM's TMA unit moves ~42 B/clk of loads + stores
+  // together, and the operand loads alone need more than that at the MMA rate
+  int lsu_epi;
   // device-adaptive SM reservation: the persistent walk leaves
   // clamp(res_per_unit * (res_stats[0] + (res_both ? res_stats[1] : 0)), res_lo, res_hi) SMs
   // to concurrent side kernels (Trans / Agg), sized by this iteration's replica volume
@@ -182,7 +194,7 @@ __device__ __forceinline__ bool decode_tile(int t, const SchedSmem& s, const Gem
 template <int EPI>
 constexpr bool tma_out() {
   return EPI == EPI_BF16 || EPI == EPI_GELU || EPI == EPI_DGELU || EPI == EPI_F32 ||
-         EPI == EPI_BF16_ADD;
+         EPI == EPI_BF16_ADD || EPI == EPI_GATHER;
 }
 
 // Stage a 32x32 bf16 block (row = lane, 16-byte chunk j) with the SWIZZLE_64B
@@ -202,6 +214,42 @@ __device__ __forceinline__ void stage_and_store(uint8_t* stage, const uint4 (&v)
     tma_store_2d(tmap, stage, col, row);
     bulk_commit();
   }
+}
+
+// LSU variant: the same conflict-free staging, then 4 coalesced 16-byte stores per lane
+// (each instruction writes 8 rows x 64 B) -- the SM's TMA unit stays with the operand loads
+__device__ __forceinline__ void stage_and_store_lsu(uint8_t* stage, const uint4 (&v)[4], __nv_bfloat16* out,
+                                                    int ld, int col, int row, int lane) {
+  __syncwarp();  // the previous block's reads of the staging buffer are done
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+    *reinterpret_cast<uint4*>(stage + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4)) = v[j];
+  __syncwarp();
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int rr = q * 8 + (lane >> 2), c = lane & 3;
+    const uint4 w = *reinterpret_cast<const uint4*>(stage + rr * 64 + ((c ^ ((rr >> 1) & 3)) << 4));
+    st_v4(out + (size_t)(row + rr) * ld + col + c * 8, w);
+  }
+}
+
+// coalesced load of a 32x32 bf16 block (lane: rows q*8 + lane/4, 16-byte chunk lane%4) ...
+__device__ __forceinline__ void blk_load_lsu(uint4 (&r)[4], const __nv_bfloat16* src, int ld, int col, int row,
+                                             int lane) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) r[q] = ld_nc_v4(src + (size_t)(row + q * 8 + (lane >> 2)) * ld + col + (lane & 3) * 8);
+}
+// ... and its transpose through smem into "row = lane" order
+__device__ __forceinline__ void blk_rows_lsu(uint8_t* stage, const uint4 (&r)[4], uint4 (&out)[4], int lane) {
+  __syncwarp();
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int rr = q * 8 + (lane >> 2), c = lane & 3;
+    *reinterpret_cast<uint4*>(stage + rr * 64 + ((c ^ ((rr >> 1) & 3)) << 4)) = r[q];
+  }
+  __syncwarp();
+#pragma unroll
+  for (int j = 0; j < 4; ++j) out[j] = *reinterpret_cast<const uint4*>(stage + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4));
 }
 
 // fp32 variant: 32 rows x 128 B, SWIZZLE_128B (16-byte chunk j of row l at j ^ (l & 7))
@@ -238,6 +286,13 @@ __device__ __forceinline__ void epilogue_chunk(const uint32_t (&raw)[32], const 
   } else if constexpr (tma_out<EPI>()) {
     const int col = tl.n0 + c;
     const int row = tl.row_off + tl.m0 + (r & ~31);
+    // one 32x32 bf16 output block of this warp: TMA store from the ring, or LSU stores
+    auto put = [&](const uint4 (&blk)[4], const CUtensorMap* tm, void* base) {
+      if (p.lsu_epi)
+        stage_and_store_lsu(stage + out_base<EPI>(), blk, reinterpret_cast<__nv_bfloat16*>(base), p.N, col, row, lane);
+      else
+        stage_and_store<NB - 1>(next_buf(), blk, tm, col, row, lane);
+    };
     uint4 v[4];
     if constexpr (EPI == EPI_BF16) {
 #pragma unroll
@@ -263,8 +318,53 @@ __device__ __forceinline__ void epilogue_chunk(const uint32_t (&raw)[32], const 
         }
         bulk_commit();
       } else {
-        stage_and_store<NB - 1>(next_buf(), v, tmC, col, row, lane);
+        put(v, tmC, p.c);
       }
+    } else if constexpr (EPI == EPI_GATHER) {
+      // dx[t] = (dl . wg)[t] + sum_j dXp[pair(t, j)]: all k rows' 64-byte pieces are loaded
+      // before any is consumed (k * 4 independent 16-byte loads in flight per thread)
+      const int t = tl.row_off + tl.m0 + r;
+      float acc[32];
+#pragma unroll
+      for (int u = 0; u < 32; ++u) acc[u] = __uint_as_float(raw[u]);
+      for (int j0 = 0; j0 < p.topk; j0 += 2) {
+        uint4 g[2][4];
+        bool have[2];
+#pragma unroll
+        for (int jj = 0; jj < 2; ++jj) {
+          const int j = j0 + jj;
+          const int pi = t * p.topk + j;
+          const int dest = j < p.topk ? p.pair_dest[pi] : -1;
+          have[jj] = dest >= 0;
+          if (have[jj]) {
+            const __nv_bfloat16* src =
+                p.gather_comb ? p.gather_comb + (size_t)pi * p.N + col
+                              : reinterpret_cast<const __nv_bfloat16*>(p.gather_ptrs[dest]) +
+                                    (size_t)p.pair_row[pi] * p.N + col;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) g[jj][u] = ld_v4(src + 8 * u);
+          }
+        }
+#pragma unroll
+        for (int jj = 0; jj < 2; ++jj) {
+          if (!have[jj]) continue;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            float f[8];
+            bf16x8_to_f32(g[jj][u], f);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) acc[8 * u + q] += f[q];
+          }
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float f[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) f[u] = acc[8 * j + u];
+        v[j] = f32x8_to_bf16(f);
+      }
+      put(v, tmC, p.c);
     } else if constexpr (EPI == EPI_GELU) {
       uint4 g4[4];
 #pragma unroll
@@ -278,8 +378,8 @@ __device__ __forceinline__ void epilogue_chunk(const uint32_t (&raw)[32], const 
         for (int u = 0; u < 8; ++u) g[u] = gelu_f(f[u]);
         g4[j] = f32x8_to_bf16(g);
       }
-      stage_and_store<NB - 1>(next_buf(), v, tmC, col, row, lane);
-      stage_and_store<NB - 1>(next_buf(), g4, tmC2, col, row, lane);
+      put(v, tmC, p.c);
+      put(g4, tmC2, p.c2);
     } else {  // EPI_DGELU: acc * GeLU'(pre);  EPI_BF16_ADD: acc + old   (operand TMA-loaded)
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
@@ -291,7 +391,7 @@ __device__ __forceinline__ void epilogue_chunk(const uint32_t (&raw)[32], const 
                                   : __uint_as_float(raw[8 * j + u]) + x[u];
         v[j] = f32x8_to_bf16(f);
       }
-      stage_and_store<NB - 1>(next_buf(), v, tmC, col, row, lane);
+      put(v, tmC, p.c);
     }
   } else if constexpr (EPI == EPI_F32_ATOMIC) {  // split-K partial: out[m][n] += acc
     if (tl.m0 + r < p.m_real) {
@@ -393,7 +493,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (g < G) {
         sched.row_off[g] = g * chunk;
         sched.rows_pad[g] = chunk;
-        sched.wslot[g] = 0;
+        sched.wslot[g] = g;  // split-K: partial g goes to its own output slice (EPI_F32)
       }
       sched.prefix[g] = g * (p.ragged_k ? (p.M_fixed / (BM * CG)) * nt : ((chunk + BM * CG - 1) / (BM * CG)) * nt);
     }
@@ -641,8 +741,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     Tile tl;
     for (int it = 0, t = tile_of(0); t < total_tiles; t = tile_of(++it)) {
       if (!decode_tile<BN, CG>(t, sched, p, tl, cta_rank)) break;
+      uint4 pre_r[4];  // LSU path: next operand block in registers (coalesced layout)
       if constexpr (EPI == EPI_DGELU || EPI == EPI_BF16_ADD) {  // first operand block, in flight during the MMAs
-        if (lane == 0 && tl.active) {
+        if (p.lsu_epi) {
+          if (tl.active)
+            blk_load_lsu(pre_r, reinterpret_cast<const __nv_bfloat16*>(p.c), p.N, tl.n0 + col0,
+                         tl.row_off + tl.m0 + q * 32, lane);
+        } else if (lane == 0 && tl.active) {
           mbar_arrive_expect_tx(&pre_bar[warp - 4], 2048);
           tma_load_2d(stage, &tmC, &pre_bar[warp - 4], tl.n0 + col0, tl.row_off + tl.m0 + q * 32);
         }
@@ -763,8 +868,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           uint32_t(&nxt)[32] = (i & 1) ? rawA : rawB;
           const int c = col0 + 32 * i;
           uint4 pre_v[4];
-          if constexpr (EPI == EPI_DGELU || EPI == EPI_BF16_ADD) {  // operand block (TMA, SWIZZLE_64B)
-            if (tl.active) {
+          if constexpr (EPI == EPI_DGELU || EPI == EPI_BF16_ADD) {  // operand block (LSU or TMA, SWIZZLE_64B)
+            if (tl.active && p.lsu_epi) {
+              blk_rows_lsu(stage, pre_r, pre_v, lane);
+              if (i + 1 < NCH)  // next block's loads overlap this chunk's math and stores
+                blk_load_lsu(pre_r, reinterpret_cast<const __nv_bfloat16*>(p.c), p.N, tl.n0 + c + 32,
+                             tl.row_off + tl.m0 + q * 32, lane);
+            } else if (tl.active) {
             mbar_wait(&pre_bar[warp - 4], pre_phase);
             pre_phase ^= 1;
 #pragma unroll
@@ -936,6 +1046,11 @@ static int launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams
   return PP_OK;
 }
 
+static int lsu_epilogue() {  // PPMOE_GEMM_LSU_EPI=0: TMA-store epilogues (A/B switch)
+  static const int on = !getenv("PPMOE_GEMM_LSU_EPI") || atoi(getenv("PPMOE_GEMM_LSU_EPI")) != 0;
+  return on;
+}
+
 static int sm_count() {
   static int n = 0;
   if (!n) {
@@ -976,35 +1091,70 @@ int route_gemm(const void* x, const void* wg, const float* bias, int T, int d, i
   }
 }
 
-int gate_bwd_gemms(const void* dl, const void* wg, const void* x, int T, int d, int E, int EP,
-                   void* dx, float* dwg, int split, cudaStream_t st) {
-  const int grid = sm_count();
-  CUtensorMap ta, tb;
-  // dx[T][d] += dl[T][EP] . wg[E][d]      (K = EP; wg rows >= E read as zeros)
+// dx[T][d] = dl[T][EP] . wg[E][d] + gathered expert-input grads (EPI_GATHER; K = EP,
+// wg rows >= E read as zeros by the TMA)
+int gate_dx_gemm(const void* dl, const void* wg, void* const* dxp_ptrs, const void* comb,
+                 const int32_t* pair_dest, const int32_t* pair_row, int T, int d, int k, int E, int EP,
+                 void* dx, cudaStream_t st) {
+  CUtensorMap ta, tb, tc;
   GemmParams p{};
   p.max_groups = 1;
   p.single_rows = T;
   p.N = d;
   p.K_fixed = EP;
   p.c = dx;
+  p.topk = k;
+  p.gather_ptrs = dxp_ptrs;
+  p.gather_comb = reinterpret_cast<const __nv_bfloat16*>(comb);
+  p.pair_dest = pair_dest;
+  p.pair_row = pair_row;
+  p.lsu_epi = lsu_epilogue();
   if (int rc = make_tmap(&ta, dl, EP, T, BK, BM)) return rc;
   if (int rc = make_tmap(&tb, wg, d, E, 64, BK)) return rc;
-  CUtensorMap tc;
   if (int rc = make_out_tmap(&tc, dx, d, T)) return rc;
-  if (int rc = launch<256, false, true, EPI_BF16_ADD, 3>(ta, tb, p, grid, st, &tc)) return rc;
-  // dwg[E][d] += dl^T . x  (split-K over token chunks, fp32 atomics; M padded to 128)
+  return launch<256, false, true, EPI_GATHER, 3>(ta, tb, p, sm_count(), st, &tc);
+}
+
+__global__ void splitk_reduce_kernel(const float4* __restrict__ ws, int splits, int rows, int slice_rows,
+                                     int vec_per_row, float4* __restrict__ out) {
+  const int n = rows * vec_per_row;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int rr = i / vec_per_row, c = i - rr * vec_per_row;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int sp = 0; sp < splits; ++sp) {  // fixed order: bit-deterministic
+      const float4 v = __ldcs(ws + ((size_t)sp * slice_rows + rr) * vec_per_row + c);
+      acc.x += v.x;
+      acc.y += v.y;
+      acc.z += v.z;
+      acc.w += v.w;
+    }
+    out[i] = acc;
+  }
+}
+
+// dwg[E][d] = dl^T . x: split-K over token chunks, partial s -> ws[s][128][d] (EPI_F32 TMA
+// stores, no atomics), then a fixed-order sum of the E real rows
+int gate_dw_gemm(const void* dl, const void* x, int T, int d, int E, int EP, int split, float* ws,
+                 float* dwg, cudaStream_t st) {
+  const int S = T / split;
+  CUtensorMap ta, tb, tc;
   GemmParams q{};
   q.max_groups = 1;
   q.single_rows = T;
   q.split_rows = split;
   q.ragged_k = 1;
   q.M_fixed = BM;
-  q.m_real = E;
   q.N = d;
-  q.c = dwg;
+  q.c = ws;
   if (int rc = make_tmap(&ta, dl, EP, T, 64, BK)) return rc;
   if (int rc = make_tmap(&tb, x, d, T, 64, BK)) return rc;
-  return launch<256, true, true, EPI_F32_ATOMIC, 4>(ta, tb, q, grid, st);
+  if (int rc = make_out_tmap_f32(&tc, ws, d, (uint64_t)S * BM)) return rc;
+  if (int rc = launch<256, true, true, EPI_F32, 4>(ta, tb, q, sm_count(), st, &tc)) return rc;
+  const int nvec = E * d / 4;
+  splitk_reduce_kernel<<<(nvec + 255) / 256 < 4 * 148 ? (nvec + 255) / 256 : 4 * 148, 256, 0, st>>>(
+      reinterpret_cast<const float4*>(ws), S, E, BM, d / 4, reinterpret_cast<float4*>(dwg));
+  PP_LAUNCH_CHECK();
+  return PP_OK;
 }
 
 static bool use_cta_pair() {
@@ -1116,6 +1266,7 @@ static int grouped_gemm_impl(int32_t mode, const void* a, const void* b, void* c
   p.max_groups = max_groups;
   p.c = c;
   p.c2 = c2;
+  p.lsu_epi = lsu_epilogue();
   if (sc) {
     p.origin = sc->origin;
     p.scatter_ptrs = sc->ptrs;

@@ -301,13 +301,15 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-template <int VPL>
+template <int VPL, int EP>
 __global__ void __launch_bounds__(256)
     combine_bwd_kernel(const __nv_bfloat16* __restrict__ dy, void* const* out_ptrs,
                        void* const* dgrad_ptrs, const int32_t* __restrict__ pair_dest,
                        const int32_t* __restrict__ pair_row, const float* __restrict__ w, int T,
                        int d, int k, float* dw, const pp_group* groups, const int32_t* num_groups,
-                       __nv_bfloat16* own, const __nv_bfloat16* __restrict__ comb) {
+                       __nv_bfloat16* own, const __nv_bfloat16* __restrict__ comb,
+                       const int32_t* __restrict__ idx, const float* __restrict__ probs, int E,
+                       __nv_bfloat16* dl) {
   const int lane = threadIdx.x & 31;
   const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -351,64 +353,10 @@ __global__ void __launch_bounds__(256)
       if (lane == j) my_dw = dot;
     }
     if (lane < k) dw[(size_t)t * k + lane] = my_dw;
-  }
-}
-
-// dx[t] = sum_j dXp[pair]  and  dl[t][:] = softmax backward of the gate (bf16,
-// padded to EP columns with zeros); the gate GEMMs (dx += dl.wg, dwg += dl^T.x)
-// then run on tensor cores (gate_bwd_gemms in gemm.cu).
-template <int VPL, int EP>
-__global__ void __launch_bounds__(256)
-    dispatch_bwd_kernel(void* const* dxp_ptrs, const int32_t* __restrict__ pair_dest,
-                        const int32_t* __restrict__ pair_row, const int32_t* __restrict__ idx,
-                        const float* __restrict__ probs, const float* __restrict__ dw, int T, int d,
-                        int k, int E, __nv_bfloat16* dx, __nv_bfloat16* dl, float4* zero,
-                        int zero_vec, const __nv_bfloat16* __restrict__ comb) {
-  const int lane = threadIdx.x & 31;
-  const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int nwarps = (gridDim.x * blockDim.x) >> 5;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < zero_vec; i += gridDim.x * blockDim.x)
-    zero[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int t = warp_global; t < T; t += nwarps) {
-    int my_e = -1, my_dest = 0, my_row = 0;
-    float my_dw = 0.f, my_p = 0.f;
-    if (lane < k) {
-      my_e = idx[(size_t)t * k + lane];
-      my_dest = pair_dest[(size_t)t * k + lane];
-      my_row = pair_row[(size_t)t * k + lane];
-      my_dw = dw[(size_t)t * k + lane];
-      my_p = probs[(size_t)t * E + my_e];
-    }
-    // gather the expert-input grads first (long-latency loads in flight)
-    float acc[VPL][8];
-#pragma unroll
-    for (int i = 0; i < VPL; ++i)
-#pragma unroll
-      for (int u = 0; u < 8; ++u) acc[i][u] = 0.f;
-    for (int j = 0; j < k; ++j) {
-      const int dest = __shfl_sync(0xffffffffu, my_dest, j);
-      const int row = __shfl_sync(0xffffffffu, my_row, j);
-      if (dest < 0) continue;  // dropped step
-      const uint4* src = reinterpret_cast<const uint4*>(
-          comb ? comb + (size_t)(t * k + j) * d
-               : reinterpret_cast<const __nv_bfloat16*>(dxp_ptrs[dest]) + (size_t)row * d);
-      uint4 v[VPL];
-#pragma unroll
-      for (int i = 0; i < VPL; ++i) v[i] = ld_v4(src + lane + 32 * i);
-#pragma unroll
-      for (int i = 0; i < VPL; ++i) {
-        float f[8];
-        bf16x8_to_f32(v[i], f);
-#pragma unroll
-        for (int u = 0; u < 8; ++u) acc[i][u] += f[u];
-      }
-    }
-    uint4* dst = reinterpret_cast<uint4*>(dx + (size_t)t * d);
-#pragma unroll
-    for (int i = 0; i < VPL; ++i) st_v4(dst + lane + 32 * i, f32x8_to_bf16(acc[i]));
-    // softmax backward restricted to the selected experts:
+    // gate softmax backward restricted to the selected experts (dw is complete here):
     //   dl_i = p_i * (dw_{j(i)} [i selected] - sum_j dw_j p_{e_j})
-    float gsum = my_dw * my_p;
+    const int my_e = lane < k ? idx[(size_t)t * k + lane] : -1;
+    float gsum = lane < k ? my_dw * probs[(size_t)t * E + my_e] : 0.f;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) gsum += __shfl_xor_sync(0xffffffffu, gsum, o);
 #pragma unroll
@@ -541,64 +489,71 @@ extern "C" int pp_combine_bwd(const void* dy, void* const* out_ptrs, void* const
                               void* own_dgrad, const int32_t* pair_dest, const int32_t* pair_row,
                               const float* w, const pp_group* groups, const int32_t* num_groups,
                               int32_t max_groups, int32_t T, int32_t d, int32_t k, float* dw,
-                              const void* comb, void* stream) {
+                              const void* comb, const int32_t* idx, const float* probs, int32_t E,
+                              int32_t EP, void* dl, void* stream) {
   PP_CHECK_ARG(dy && (out_ptrs || comb) && dgrad_ptrs && own_dgrad && pair_dest && pair_row && w &&
-                   groups && num_groups && dw,
+                   groups && num_groups && dw && idx && probs && dl,
                "pp_combine_bwd: null pointer");
+  PP_CHECK_ARG(EP == 64 || EP == 128, "pp_combine_bwd: EP=%d must be 64 or 128", EP);
+  PP_CHECK_ARG(E >= 1 && E <= EP && k >= 1 && k <= 8, "pp_combine_bwd: E=%d / k=%d", E, k);
   cudaStream_t st = as_stream(stream);
-  PP_VPL_SWITCH(d, (combine_bwd_kernel<VPL><<<grid_for_tokens(T), 256, 0, st>>>(
-                       reinterpret_cast<const __nv_bfloat16*>(dy), out_ptrs, dgrad_ptrs,
-                       pair_dest, pair_row, w, T, d, k, dw, groups, num_groups,
-                       reinterpret_cast<__nv_bfloat16*>(own_dgrad),
-                       reinterpret_cast<const __nv_bfloat16*>(comb))));
-  PP_LAUNCH_CHECK();
-  return PP_OK;
-}
-
-extern "C" int pp_dispatch_bwd(void* const* dxp_ptrs, const int32_t* pair_dest,
-                               const int32_t* pair_row, const int32_t* idx, const float* probs,
-                               const float* dw, int32_t T, int32_t d, int32_t k, int32_t E,
-                               int32_t EP, void* dx, void* dl, float* zero_f32, int64_t zero_elems,
-                               const void* comb, void* stream) {
-  PP_CHECK_ARG(zero_elems % 4 == 0 && (zero_elems == 0 || zero_f32), "pp_dispatch_bwd: zero buffer");
-  PP_CHECK_ARG((dxp_ptrs || comb) && pair_dest && pair_row && idx && probs && dw && dx && dl,
-               "pp_dispatch_bwd: null pointer");
-  PP_CHECK_ARG(EP == 64 || EP == 128, "pp_dispatch_bwd: EP=%d must be 64 or 128", EP);
-  PP_CHECK_ARG(E <= EP, "pp_dispatch_bwd: E=%d > EP=%d", E, EP);
-  cudaStream_t st = as_stream(stream);
-  auto* dxp = reinterpret_cast<__nv_bfloat16*>(dx);
   auto* dlp = reinterpret_cast<__nv_bfloat16*>(dl);
+  auto* ddy = reinterpret_cast<const __nv_bfloat16*>(dy);
+  auto* own = reinterpret_cast<__nv_bfloat16*>(own_dgrad);
+  auto* cb = reinterpret_cast<const __nv_bfloat16*>(comb);
   if (EP == 64) {
-    PP_VPL_SWITCH(d, (dispatch_bwd_kernel<VPL, 64><<<grid_for_tokens(T), 256, 0, st>>>(
-                         dxp_ptrs, pair_dest, pair_row, idx, probs, dw, T, d, k, E, dxp, dlp,
-                         reinterpret_cast<float4*>(zero_f32), (int)(zero_elems / 4),
-                         reinterpret_cast<const __nv_bfloat16*>(comb))));
+    PP_VPL_SWITCH(d, (combine_bwd_kernel<VPL, 64><<<grid_for_tokens(T), 256, 0, st>>>(
+                         ddy, out_ptrs, dgrad_ptrs, pair_dest, pair_row, w, T, d, k, dw, groups, num_groups,
+                         own, cb, idx, probs, E, dlp)));
   } else {
-    PP_VPL_SWITCH(d, (dispatch_bwd_kernel<VPL, 128><<<grid_for_tokens(T), 256, 0, st>>>(
-                         dxp_ptrs, pair_dest, pair_row, idx, probs, dw, T, d, k, E, dxp, dlp,
-                         reinterpret_cast<float4*>(zero_f32), (int)(zero_elems / 4),
-                         reinterpret_cast<const __nv_bfloat16*>(comb))));
+    PP_VPL_SWITCH(d, (combine_bwd_kernel<VPL, 128><<<grid_for_tokens(T), 256, 0, st>>>(
+                         ddy, out_ptrs, dgrad_ptrs, pair_dest, pair_row, w, T, d, k, dw, groups, num_groups,
+                         own, cb, idx, probs, E, dlp)));
   }
   PP_LAUNCH_CHECK();
   return PP_OK;
 }
 
 namespace pp {
-int gate_bwd_gemms(const void* dl, const void* wg, const void* x, int T, int d, int E, int EP,
-                   void* dx, float* dwg, int split, cudaStream_t st);
+int gate_dx_gemm(const void* dl, const void* wg, void* const* dxp_ptrs, const void* comb,
+                 const int32_t* pair_dest, const int32_t* pair_row, int T, int d, int k, int E, int EP,
+                 void* dx, cudaStream_t st);
+int gate_dw_gemm(const void* dl, const void* x, int T, int d, int E, int EP, int split, float* ws,
+                 float* dwg, cudaStream_t st);
+
+// split-K chunk of the gate weight GEMM: ~one wave of (split, 256-column) tiles, a
+// multiple of 128 that divides T
+static int gate_dw_split(int T, int d) {
+  const int want_splits = (148 + d / 256 - 1) / (d / 256);
+  int split = 128;
+  while (split * 2 <= T && T % (split * 2) == 0 && T / (split * 2) >= want_splits) split *= 2;
+  return split;
+}
+}  // namespace pp
+
+extern "C" int pp_gate_dx(const void* dl, const void* wg, void* const* dxp_ptrs, const void* comb,
+                          const int32_t* pair_dest, const int32_t* pair_row, int32_t T, int32_t d, int32_t k,
+                          int32_t E, int32_t EP, void* dx, void* stream) {
+  PP_CHECK_ARG(dl && wg && (dxp_ptrs || comb) && pair_dest && pair_row && dx, "pp_gate_dx: null pointer");
+  PP_CHECK_ARG(d % 256 == 0, "pp_gate_dx: d=%d must be a multiple of 256", d);
+  PP_CHECK_ARG(T > 0 && T % PP_CHUNK == 0, "pp_gate_dx: T=%d must be a multiple of %d", T, PP_CHUNK);
+  PP_CHECK_ARG((EP == 64 || EP == 128) && E >= 1 && E <= EP, "pp_gate_dx: bad E=%d/EP=%d", E, EP);
+  PP_CHECK_ARG(k >= 1 && k <= 8, "pp_gate_dx: k=%d", k);
+  return gate_dx_gemm(dl, wg, dxp_ptrs, comb, pair_dest, pair_row, T, d, k, E, EP, dx, as_stream(stream));
 }
 
-extern "C" int pp_gate_bwd(const void* dl, const void* wg, const void* x, int32_t T, int32_t d,
-                           int32_t E, int32_t EP, void* dx, float* dwg, void* stream) {
-  PP_CHECK_ARG(dl && wg && x && dx && dwg, "pp_gate_bwd: null pointer");
-  PP_CHECK_ARG(d % 256 == 0, "pp_gate_bwd: d=%d must be a multiple of 256", d);
-  PP_CHECK_ARG(T % PP_CHUNK == 0, "pp_gate_bwd: T=%d must be a multiple of %d", T, PP_CHUNK);
-  PP_CHECK_ARG((EP == 64 || EP == 128) && E <= EP, "pp_gate_bwd: bad E=%d/EP=%d", E, EP);
-  // split-K chunk: ~4 chunks per SM-row of output tiles, multiple of 128 dividing T
-  int split = 1024;
-  while (split > 128 && T % split) split >>= 1;
-  if (T % split) split = T;
-  return gate_bwd_gemms(dl, wg, x, T, d, E, EP, dx, dwg, split, as_stream(stream));
+extern "C" int64_t pp_gate_dw_workspace_bytes(int32_t T, int32_t d) {
+  if (T <= 0 || T % PP_CHUNK || d <= 0 || d % 256) return -1;
+  return (int64_t)(T / gate_dw_split(T, d)) * 128 * d * 4;
+}
+
+extern "C" int pp_gate_dw(const void* dl, const void* x, int32_t T, int32_t d, int32_t E, int32_t EP,
+                          float* workspace, float* dwg, void* stream) {
+  PP_CHECK_ARG(dl && x && workspace && dwg, "pp_gate_dw: null pointer");
+  PP_CHECK_ARG(d % 256 == 0, "pp_gate_dw: d=%d must be a multiple of 256", d);
+  PP_CHECK_ARG(T > 0 && T % PP_CHUNK == 0, "pp_gate_dw: T=%d must be a multiple of %d", T, PP_CHUNK);
+  PP_CHECK_ARG((EP == 64 || EP == 128) && E >= 1 && E <= EP, "pp_gate_dw: bad E=%d/EP=%d", E, EP);
+  return gate_dw_gemm(dl, x, T, d, E, EP, gate_dw_split(T, d), workspace, dwg, as_stream(stream));
 }
 
 // ---------------------------------------------------------------------------

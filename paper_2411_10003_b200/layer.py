@@ -21,8 +21,9 @@ the reference's objects are its interface:
     K3 pp_combine          weighted gather back (peer loads, or local after fused A2A)
     K2 pp_plan_greedy /    (D>1, side stream) plan for iteration j+1 on this
        pp_plan_physical    iteration's LoadMatrix (plan_for_iteration rule)
-  backward mirrors it: combine_bwd (push), WGRAD2/DGRAD2/WGRAD1/DGRAD1 (order
-  depends on the replica engine), dispatch_bwd + gate grads, K5 Agg (D>1).
+  backward mirrors it: combine_bwd (push; also dL/dlogits), gate dW (deterministic
+  split-K), WGRAD2/DGRAD2/WGRAD1/DGRAD1 (order depends on the replica engine), then
+  pp_gate_dx = dispatch backward + gate dX in one tcgen05 kernel, K5 Agg (D>1).
 
 Virtual expert slots: with m = E/D experts per rank, each
 rank's T tokens are cut into m contiguous slots; slot v = rank*m + j is a
@@ -274,6 +275,10 @@ class MoELayer(torch.nn.Module):
         self.dw = torch.empty((T, k), dtype=torch.float32, device=dev)
         self.EP = 64 if E <= 64 else 128
         self.dlogits = torch.zeros((T, self.EP), dtype=torch.bfloat16, device=dev)  # gate dL/dlogits
+        ws_bytes = _lib.load().pp_gate_dw_workspace_bytes(T, d_model)
+        if ws_bytes < 0:
+            raise ValidationError(f"gate backward: unsupported T={T} / d_model={d_model}")
+        self.gate_ws = torch.empty((ws_bytes // 4,), dtype=torch.float32, device=dev)  # split-K partials of dWg
         # ---- expert activations ---------------------------------------------
         R = self.rows_cap
         self.xp = PeerBuffer((R, d_model), torch.bfloat16, self.group, dev)
@@ -476,7 +481,9 @@ class MoELayer(torch.nn.Module):
 
     def _poll_status(self) -> None:
         """Raise CapacityError if an earlier step's layout was dropped (non-blocking)."""
-        if self._status_ev is not None and self._status_ev.query() and int(self._status_host[0]):
+        if self._status_ev is None or torch.cuda.is_current_stream_capturing():
+            return
+        if self._status_ev.query() and int(self._status_host[0]):
             self._raise_status(int(self._status_host[0]))
 
     def check_status(self) -> None:
@@ -831,8 +838,14 @@ class MoELayer(torch.nn.Module):
         _lib.call("pp_combine_bwd", dy.data_ptr(), self.yp.ptrs.data_ptr(), self.dyp.ptrs.data_ptr(),
                   self.dyp.local.data_ptr(), self.pair_dest.data_ptr(), self.pair_row.data_ptr(),
                   self.w.data_ptr(), self.groups.data_ptr(), self.num_groups.data_ptr(), self.max_groups,
-                  self.T, self.d, self.k, self.dw.data_ptr(), self._comb_local(), sp)
+                  self.T, self.d, self.k, self.dw.data_ptr(), self._comb_local(), self.idx.data_ptr(),
+                  self.probs.data_ptr(), self.E, self.EP, self.dlogits.data_ptr(), sp)
         self._mark("combine_bwd")
+        # gate weight grad (deterministic split-K; needs only x and dL/dlogits): at N > 1 it
+        # fills the wait for the slowest rank's combine_bwd at the next barrier
+        _lib.call("pp_gate_dw", self.dlogits.data_ptr(), x.data_ptr(), self.T, self.d, self.E, self.EP,
+                  self.gate_ws.data_ptr(), self.wg.main_grad.data_ptr(), sp)
+        self._mark("gate_dw")
         self.barrier()
         self._mark("barrier3")
         agg = self.world > 1 and self.mask_cur is not None
@@ -863,15 +876,12 @@ class MoELayer(torch.nn.Module):
         self.barrier()
         self._mark("barrier4")
         dx = torch.empty((self.T, self.d), dtype=torch.bfloat16, device=self.device)
-        _lib.call("pp_dispatch_bwd", self.dxp.ptrs.data_ptr(), self.pair_dest.data_ptr(),
-                  self.pair_row.data_ptr(), self.idx.data_ptr(), self.probs.data_ptr(), self.dw.data_ptr(),
-                  self.T, self.d, self.k, self.E, self.EP, dx.data_ptr(), self.dlogits.data_ptr(),
-                  self.wg.main_grad.data_ptr(), self.wg.main_grad.numel(), self._comb_local(),
-                  sp)  # also zeroes dWg
-        self._mark("dispatch_bwd")
-        _lib.call("pp_gate_bwd", self.dlogits.data_ptr(), self.wg.data_ptr(), x.data_ptr(), self.T, self.d,
-                  self.E, self.EP, dx.data_ptr(), self.wg.main_grad.data_ptr(), sp)
-        self._mark("gate_bwd")
+        # dispatch backward + gate input grad in one tcgen05 kernel: dx = dl . Wg + sum_j dXp[pair]
+        _lib.call("pp_gate_dx", self.dlogits.data_ptr(), self.wg.data_ptr(),
+                  None if self.fused_a2a else self.dxp.ptrs.data_ptr(), self._comb_local(),
+                  self.pair_dest.data_ptr(), self.pair_row.data_ptr(), self.T, self.d, self.k, self.E, self.EP,
+                  dx.data_ptr(), sp)
+        self._mark("gate_dx")
         if self.planning == "device" and self.world > 1:
             cur = torch.cuda.current_stream()
             if self._agg_done is not None:  # join the Agg side stream (graph-capturable fork/join)

@@ -169,10 +169,11 @@ class MoEStack(torch.nn.Module):
                 (OpKind.A2A, Lane.NETWORK, "route_layout", "barrier1"),
                 (OpKind.FEC, Lane.COMPUTE, "barrier1", "fwd_gemms"),
                 (OpKind.A2A, Lane.NETWORK, "fwd_gemms", "combine"),
-                (OpKind.A2A, Lane.NETWORK, "bwd_begin", "barrier3"),
+                (OpKind.A2A, Lane.NETWORK, "bwd_begin", "combine_bwd"),
+                (OpKind.BEC, Lane.COMPUTE, "combine_bwd", "gate_dw"),
+                (OpKind.A2A, Lane.NETWORK, "gate_dw", "barrier3"),
                 (OpKind.BEC, Lane.COMPUTE, "barrier3", "bwd_gemms"),
-                (OpKind.A2A, Lane.NETWORK, "bwd_gemms", "dispatch_bwd"),
-                (OpKind.BEC, Lane.COMPUTE, "dispatch_bwd", "gate_bwd"),
+                (OpKind.A2A, Lane.NETWORK, "bwd_gemms", "gate_dx"),
             ]
             for kind, lane, a, b in groups:
                 if a in seq and b in seq:

@@ -29,7 +29,9 @@ modes = {
     "DGRAD1": (_lib.PP_GEMM_DGRAD1, pre, W1, Y, None),
     "WGRAD2": (_lib.PP_GEMM_WGRAD2, Y, act, G2, None),
     "WGRAD1": (_lib.PP_GEMM_WGRAD1, pre, X, G1, None),
+    "PLAIN": (_lib.PP_GEMM_PLAIN, X, W1, pre, None),  # FWD1's shape, single bf16 output, no GeLU
 }
+times = {}
 sel = sys.argv[1:] or list(modes)
 flops = 2.0 * T * k * d * f
 for name in sel:
@@ -46,6 +48,7 @@ for name in sel:
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / 10
+    times[name] = ms
     print(f"{name:7s} {ms*1e3:8.1f} us  {flops/ms/1e9:8.1f} TFLOP/s", flush=True)
 
 if __import__("os").environ.get("PPMOE_GEMM_DEBUG"):
@@ -55,12 +58,16 @@ if __import__("os").environ.get("PPMOE_GEMM_DEBUG"):
     lib = _lib.load()
     for name in sel:
         mode, a, b, c, c2 = modes[name]
-        _device.grouped_gemm(mode, a, b, c, c2, groups, ng, E, cap, E, d, f)
+        _device.grouped_gemm(mode, a, b, c, c2, groups, ng, E, cap, E, d, f, num_sms=int(__import__("os").environ.get("GEMM_SMS", "0")))
         torch.cuda.synchronize()
         buf = (ctypes.c_ulonglong * (148 * 4))()
         lib.pp_gemm_debug_read(buf, 148)
         arr = np.array(buf).reshape(148, 4)
         lead = arr[arr[:, 0] > 0]
         tot, wt, wf = lead[:, 0].mean(), lead[:, 1].mean(), lead[:, 2].mean()
+        nsm_used = int(__import__("os").environ.get("GEMM_SMS", "0")) or 148
+        fpc = flops / nsm_used / lead[:, 0].max()
+        print(f"{name:7s} {fpc:7.0f} FLOP/cycle/SM over the MMA thread's window "
+              f"({fpc / 8192 * 100:5.1f}% of 8192), implied SM clock {lead[:, 0].max() / (times.get(name, 1) * 1e-3) / 1e9:5.2f} GHz")
         print(f"{name:7s} MMA thread: total {tot:10.0f} cyc, wait tempty {wt/tot*100:5.1f}%, wait full {wf/tot*100:5.1f}%, "
               f"issue+other {(tot-wt-wf)/tot*100:5.1f}%  (CTAs {len(lead)}, max total {lead[:,0].max():.0f})")

@@ -159,12 +159,13 @@ def main():
             ye = layer(xe)
             ye.backward(dyd)
         torch.cuda.synchronize()
-        ref_out = (ye.detach().clone(), xe.grad.clone(), layer.w1.main_grad.clone(), layer.w2.main_grad.clone())
+        ref_out = (ye.detach().clone(), xe.grad.clone(), layer.w1.main_grad.clone(), layer.w2.main_grad.clone(),
+                   layer.wg.main_grad.clone())
         gs = layer.make_graphed_step(xd.clone(), dyd.clone())
         for _ in range(2):
             yg, dxg = gs()
         torch.cuda.synchronize()
-        got = (yg, dxg, layer.w1.main_grad, layer.w2.main_grad)
+        got = (yg, dxg, layer.w1.main_grad, layer.w2.main_grad, layer.wg.main_grad)
         same = all(torch.equal(a, b) for a, b in zip(ref_out, got))
         flag = torch.tensor([1 if same else 0])
         dist.all_reduce(flag, op=dist.ReduceOp.MIN)

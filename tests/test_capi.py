@@ -15,7 +15,7 @@ HEADER = Path(__file__).resolve().parent.parent / "include" / "ppmoe.h"
 
 def declared_symbols():
     text = HEADER.read_text()
-    return sorted(set(re.findall(r"^(?:int|const char\*)\s+(pp_\w+)\s*\(", text, flags=re.M)))
+    return sorted(set(re.findall(r"^(?:int|int64_t|const char\*)\s+(pp_\w+)\s*\(", text, flags=re.M)))
 
 
 def test_header_symbols_exported():

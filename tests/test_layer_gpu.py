@@ -146,6 +146,7 @@ def test_probe_loss_and_graphed_step():
     accumulation-order tolerance), deterministic across calls; a captured CUDA-graph step
     reproduces the eager step bit-exactly and its in-graph loss equals probe_loss."""
     layer, x, wg, dy, y1, dx1 = run_layer(2048, 256, 512, 16, 2, seed=3)
+    gw1 = layer.wg.main_grad.clone()  # deterministic gate dW (fixed-order split-K)
     dev = layer.device
     yv, g = y1.to(dev), dy.to(dev)
     l1, l2 = layer.probe_loss(yv, g), layer.probe_loss(yv, g)
@@ -157,6 +158,7 @@ def test_probe_loss_and_graphed_step():
     ya, dxa = gs()
     torch.cuda.synchronize()
     assert torch.equal(ya, y1.to(dev)) and torch.equal(dxa, dx1.to(dev))
+    assert torch.equal(layer.wg.main_grad, gw1)
     assert torch.equal(gs.loss, layer.probe_loss(ya, dys))
 
 
