@@ -55,7 +55,7 @@ constexpr int out_bufs() {
 }
 template <int EPI>
 constexpr int out_base() {
-  return (EPI == EPI_DGELU || EPI == EPI_BF16_ADD) ? 2048 : 0;
+  return (EPI == EPI_DGELU || EPI == EPI_BF16_ADD || EPI == EPI_GATHER) ? 2048 : 0;
 }
 template <int EPI>
 constexpr int stage_bytes_per_warp() {
@@ -270,11 +270,34 @@ __device__ __forceinline__ void stage_and_store_f32(uint8_t* stage, const uint32
 }
 
 // Epilogue of one 32-column chunk of one accumulator row (thread = row r).
+// EPI_GATHER: coalesced loads of the gathered rows of one warp's 32x32 output block, for
+// pair slots j = 0, 1 (lane: rows qq*8 + lane/4, 16-byte piece lane%4; zero for dropped pairs)
+__device__ __forceinline__ void gather_issue(uint4 (&g)[2][4], const GemmParams& p, int row0, int col, int lane) {
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+#pragma unroll
+    for (int qq = 0; qq < 4; ++qq) {
+      g[j][qq] = make_uint4(0, 0, 0, 0);
+      if (j < p.topk) {
+        const int t = row0 + qq * 8 + (lane >> 2);
+        const int pi = t * p.topk + j;
+        const int dest = p.pair_dest[pi];
+        if (dest >= 0) {
+          const __nv_bfloat16* src =
+              p.gather_comb ? p.gather_comb + (size_t)pi * p.N
+                            : reinterpret_cast<const __nv_bfloat16*>(p.gather_ptrs[dest]) + (size_t)p.pair_row[pi] * p.N;
+          g[j][qq] = ld_v4(src + col + (lane & 3) * 8);
+        }
+      }
+    }
+  }
+}
+
 template <int EPI>
 __device__ __forceinline__ void epilogue_chunk(const uint32_t (&raw)[32], const GemmParams& p,
                                                const Tile& tl, int r, int c, const uint4 (&pre_v)[4],
                                                uint8_t* stage, int& sbuf, const CUtensorMap* tmC,
-                                               const CUtensorMap* tmC2, int lane) {
+                                               const CUtensorMap* tmC2, int lane, const float* gx = nullptr) {
   constexpr int NB = out_bufs<EPI>();
   auto next_buf = [&]() -> uint8_t* {  // ring slot for the next staged 32x32 bf16 block
     uint8_t* b = stage + out_base<EPI>() + sbuf * 2048;
@@ -321,47 +344,12 @@ __device__ __forceinline__ void epilogue_chunk(const uint32_t (&raw)[32], const 
         put(v, tmC, p.c);
       }
     } else if constexpr (EPI == EPI_GATHER) {
-      // dx[t] = (dl . wg)[t] + sum_j dXp[pair(t, j)]: all k rows' 64-byte pieces are loaded
-      // before any is consumed (k * 4 independent 16-byte loads in flight per thread)
-      const int t = tl.row_off + tl.m0 + r;
-      float acc[32];
-#pragma unroll
-      for (int u = 0; u < 32; ++u) acc[u] = __uint_as_float(raw[u]);
-      for (int j0 = 0; j0 < p.topk; j0 += 2) {
-        uint4 g[2][4];
-        bool have[2];
-#pragma unroll
-        for (int jj = 0; jj < 2; ++jj) {
-          const int j = j0 + jj;
-          const int pi = t * p.topk + j;
-          const int dest = j < p.topk ? p.pair_dest[pi] : -1;
-          have[jj] = dest >= 0;
-          if (have[jj]) {
-            const __nv_bfloat16* src =
-                p.gather_comb ? p.gather_comb + (size_t)pi * p.N + col
-                              : reinterpret_cast<const __nv_bfloat16*>(p.gather_ptrs[dest]) +
-                                    (size_t)p.pair_row[pi] * p.N + col;
-#pragma unroll
-            for (int u = 0; u < 4; ++u) g[jj][u] = ld_v4(src + 8 * u);
-          }
-        }
-#pragma unroll
-        for (int jj = 0; jj < 2; ++jj) {
-          if (!have[jj]) continue;
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            float f[8];
-            bf16x8_to_f32(g[jj][u], f);
-#pragma unroll
-            for (int q = 0; q < 8; ++q) acc[8 * u + q] += f[q];
-          }
-        }
-      }
+      // dx[t] = (dl . wg)[t] + sum_j dXp[pair(t, j)]  (gx: the gathered sum, fp32)
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         float f[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) f[u] = acc[8 * j + u];
+        for (int u = 0; u < 8; ++u) f[u] = __uint_as_float(raw[8 * j + u]) + gx[8 * j + u];
         v[j] = f32x8_to_bf16(f);
       }
       put(v, tmC, p.c);
@@ -861,6 +849,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         // software-pipelined: the TMEM read of chunk i+1 is in flight while chunk i is processed
         constexpr int NCH = EPI_COLS / 32;
         uint32_t rawA[32], rawB[32];
+        // EPI_GATHER: the gathered rows of chunk i+1 are in flight while chunk i is processed
+        constexpr int GB = (EPI == EPI_GATHER) ? 2 : 1;
+        uint4 gbuf[GB][2][4];
+        const int grow0 = tl.row_off + tl.m0 + q * 32;
+        if constexpr (EPI == EPI_GATHER) {
+          if (tl.active) gather_issue(gbuf[0], p, grow0, tl.n0 + col0, lane);
+        }
         if (!zero) tmem_ld_32x32b_x32(t_row + col0, rawA);
 #pragma unroll
         for (int i = 0; i < NCH; ++i) {
@@ -894,8 +889,43 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int j = 0; j < 32; ++j) cur[j] = 0u;
           }
+          float gx[(EPI == EPI_GATHER) ? 32 : 1];
+          if constexpr (EPI == EPI_GATHER) {
+            if (tl.active) {
+              if (i + 1 < NCH) gather_issue(gbuf[(i + 1) & 1], p, grow0, c + 32, lane);
+#pragma unroll
+              for (int u = 0; u < 32; ++u) gx[u] = 0.f;
+#pragma unroll
+              for (int j = 0; j < 2; ++j) {
+                if (j >= p.topk) break;
+                uint4 rv[4];
+                blk_rows_lsu(stage, gbuf[i & 1][j], rv, lane);  // coalesced pieces -> this lane's row
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                  float f[8];
+                  bf16x8_to_f32(rv[u], f);
+#pragma unroll
+                  for (int w = 0; w < 8; ++w) gx[8 * u + w] += f[w];
+                }
+              }
+              for (int j0 = 2; j0 < p.topk; ++j0) {  // top-k > 2: remaining pairs, one at a time
+                const int t = grow0 + lane, pi = t * p.topk + j0, dest = p.pair_dest[pi];
+                if (dest < 0) continue;
+                const __nv_bfloat16* src =
+                    p.gather_comb ? p.gather_comb + (size_t)pi * p.N
+                                  : reinterpret_cast<const __nv_bfloat16*>(p.gather_ptrs[dest]) + (size_t)p.pair_row[pi] * p.N;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                  float f[8];
+                  bf16x8_to_f32(ld_v4(src + c + 8 * u), f);
+#pragma unroll
+                  for (int w = 0; w < 8; ++w) gx[8 * u + w] += f[w];
+                }
+              }
+            }
+          }
           if (i + 1 == NCH) release_acc();  // every TMEM read of this tile has completed
-          if (tl.active) epilogue_chunk<EPI>(cur, p, tl, r, c, pre_v, stage, sbuf, &tmC, &tmC2, lane);
+          if (tl.active) epilogue_chunk<EPI>(cur, p, tl, r, c, pre_v, stage, sbuf, &tmC, &tmC2, lane, gx);
         }
       }
       if (++acc == NACC) {
@@ -1046,9 +1076,15 @@ static int launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams
   return PP_OK;
 }
 
-static int lsu_epilogue() {  // PPMOE_GEMM_LSU_EPI=0: TMA-store epilogues (A/B switch)
-  static const int on = !getenv("PPMOE_GEMM_LSU_EPI") || atoi(getenv("PPMOE_GEMM_LSU_EPI")) != 0;
+// PPMOE_GEMM_LSU_EPI=1: bf16 epilogue I/O through the LSUs instead of TMA (A/B switch; measured
+// slower: the SM's L2 port, not the TMA unit, carries loads and stores either way)
+static int lsu_epilogue() {
+  static const int on = getenv("PPMOE_GEMM_LSU_EPI") && atoi(getenv("PPMOE_GEMM_LSU_EPI")) != 0;
   return on;
+}
+static int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v ? atoi(v) : dflt;
 }
 
 static int sm_count() {
@@ -1115,25 +1151,30 @@ int gate_dx_gemm(const void* dl, const void* wg, void* const* dxp_ptrs, const vo
   return launch<256, false, true, EPI_GATHER, 3>(ta, tb, p, sm_count(), st, &tc);
 }
 
-__global__ void splitk_reduce_kernel(const float4* __restrict__ ws, int splits, int rows, int slice_rows,
-                                     int vec_per_row, float4* __restrict__ out) {
-  const int n = rows * vec_per_row;
+// dwg[e][c] = sum_s ws[s][c][e] (fixed order over the splits: bit-deterministic); thread per
+// (c, e), every split's value loaded before the adds
+__global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, int d, int EP, int E,
+                                     float* __restrict__ out) {
+  const int n = d * E;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const int rr = i / vec_per_row, c = i - rr * vec_per_row;
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int sp = 0; sp < splits; ++sp) {  // fixed order: bit-deterministic
-      const float4 v = __ldcs(ws + ((size_t)sp * slice_rows + rr) * vec_per_row + c);
-      acc.x += v.x;
-      acc.y += v.y;
-      acc.z += v.z;
-      acc.w += v.w;
+    const int c = i / E, e = i - (i / E) * E;
+    const float* src = ws + (size_t)c * EP + e;
+    const size_t stride = (size_t)d * EP;
+    float acc = 0.f;
+    for (int s0 = 0; s0 < splits; s0 += 8) {
+      float v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = s0 + u < splits ? __ldcs(src + (size_t)(s0 + u) * stride) : 0.f;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc += v[u];
     }
-    out[i] = acc;
+    out[(size_t)e * d + c] = acc;
   }
 }
 
-// dwg[E][d] = dl^T . x: split-K over token chunks, partial s -> ws[s][128][d] (EPI_F32 TMA
-// stores, no atomics), then a fixed-order sum of the E real rows
+// dwg[E][d] = dl^T . x, computed transposed: dwg^T[d][EP] = x^T . dl with M = d (128-row
+// tiles of x^T), N = EP, split-K over token chunks; partial s -> ws[s][d][EP] (EPI_F32 TMA
+// stores, no atomics), then the fixed-order reduce (transposing back)
 int gate_dw_gemm(const void* dl, const void* x, int T, int d, int E, int EP, int split, float* ws,
                  float* dwg, cudaStream_t st) {
   const int S = T / split;
@@ -1143,16 +1184,17 @@ int gate_dw_gemm(const void* dl, const void* x, int T, int d, int E, int EP, int
   q.single_rows = T;
   q.split_rows = split;
   q.ragged_k = 1;
-  q.M_fixed = BM;
-  q.N = d;
+  q.M_fixed = d;
+  q.N = EP;
   q.c = ws;
-  if (int rc = make_tmap(&ta, dl, EP, T, 64, BK)) return rc;
-  if (int rc = make_tmap(&tb, x, d, T, 64, BK)) return rc;
-  if (int rc = make_out_tmap_f32(&tc, ws, d, (uint64_t)S * BM)) return rc;
-  if (int rc = launch<256, true, true, EPI_F32, 4>(ta, tb, q, sm_count(), st, &tc)) return rc;
-  const int nvec = E * d / 4;
-  splitk_reduce_kernel<<<(nvec + 255) / 256 < 4 * 148 ? (nvec + 255) / 256 : 4 * 148, 256, 0, st>>>(
-      reinterpret_cast<const float4*>(ws), S, E, BM, d / 4, reinterpret_cast<float4*>(dwg));
+  if (int rc = make_tmap(&ta, x, d, T, 64, BK)) return rc;   // A = x^T (MN-major: d contiguous)
+  if (int rc = make_tmap(&tb, dl, EP, T, 64, BK)) return rc; // B = dl (MN-major: experts contiguous)
+  if (int rc = make_out_tmap_f32(&tc, ws, EP, (uint64_t)S * d)) return rc;
+  int rc = EP == 64 ? launch<64, true, true, EPI_F32, 6>(ta, tb, q, sm_count(), st, &tc)
+                    : launch<128, true, true, EPI_F32, 5>(ta, tb, q, sm_count(), st, &tc);
+  if (rc) return rc;
+  const int n = E * d;
+  splitk_reduce_kernel<<<(n + 255) / 256, 256, 0, st>>>(ws, S, d, EP, E, dwg);
   PP_LAUNCH_CHECK();
   return PP_OK;
 }
@@ -1304,6 +1346,7 @@ static int grouped_gemm_impl(int32_t mode, const void* a, const void* b, void* c
       if ((rc = make_tmap(&ta, a, dm, R, BK, BM)) || (rc = make_tmap(&tb, b, dm, (uint64_t)S * df, BK, bkb))) return rc;
       p.N = df; p.K_fixed = dm;
       if ((rc = make_out_tmap(&tc, c, df, R)) || (rc = make_out_tmap(&tc2, c2, df, R))) return rc;
+      if (wide_df && env_int("PPMOE_GEMM_FWD1_WIDE", 0)) return PP_LAUNCH_W(EPI_GELU, false, false, 3, &tc, &tc2);
       return PP_LAUNCH(EPI_GELU, false, false, 3, 5, &tc, &tc2);
     case PP_GEMM_FWD2:
       if ((rc = make_tmap(&ta, a, df, R, BK, BM)) ||
@@ -1319,6 +1362,7 @@ static int grouped_gemm_impl(int32_t mode, const void* a, const void* b, void* c
       p.N = df; p.K_fixed = dm;
       PP_CHECK_ARG(c2 == c, "DGRAD2 runs in place: dPre must alias pre");
       if ((rc = make_out_tmap(&tc, c, df, R))) return rc;
+      if (wide_df && env_int("PPMOE_GEMM_DGRAD2_WIDE", 0)) return PP_LAUNCH_W(EPI_DGELU, false, true, 3, &tc);
       return PP_LAUNCH(EPI_DGELU, false, true, 3, 5, &tc);
     case PP_GEMM_DGRAD1:
       if ((rc = make_tmap(&ta, a, df, R, BK, BM)) || (rc = make_tmap(&tb, b, dm, (uint64_t)S * df, 64, BK))) return rc;

@@ -275,24 +275,35 @@ __global__ void __launch_bounds__(256)
       my_row = pair_row[(size_t)t * k + lane];
       my_w = w[(size_t)t * k + lane];
     }
-    for (int j = 0; j < k; ++j) {
-      const int dest = __shfl_sync(0xffffffffu, my_dest, j);
-      const int row = __shfl_sync(0xffffffffu, my_row, j);
-      const float wj = __shfl_sync(0xffffffffu, my_w, j);
-      if (dest < 0) continue;  // dropped step
-      // fused A2A: the expert outputs were pushed here by the GEMM epilogue, in pair order
-      const uint4* src = reinterpret_cast<const uint4*>(
-          comb ? comb + (size_t)(t * k + j) * d
-               : reinterpret_cast<const __nv_bfloat16*>(out_ptrs[dest]) + (size_t)row * d);
-      uint4 v[VPL];
+    for (int j0 = 0; j0 < k; j0 += 2) {  // two pairs' rows in flight at a time
+      uint4 v[2][VPL];
+      int dest[2];
+      float wj[2];
 #pragma unroll
-      for (int i = 0; i < VPL; ++i) v[i] = ld_v4(src + lane + 32 * i);
+      for (int jj = 0; jj < 2; ++jj) {
+        const int j = j0 + jj < k ? j0 + jj : j0;
+        dest[jj] = __shfl_sync(0xffffffffu, my_dest, j);
+        const int row = __shfl_sync(0xffffffffu, my_row, j);
+        wj[jj] = __shfl_sync(0xffffffffu, my_w, j);
+        if (j0 + jj >= k) dest[jj] = -1;
+        if (dest[jj] < 0) continue;  // beyond k, or dropped step
+        // fused A2A: the expert outputs were pushed here by the GEMM epilogue, in pair order
+        const uint4* src = reinterpret_cast<const uint4*>(
+            comb ? comb + (size_t)(t * k + j) * d
+                 : reinterpret_cast<const __nv_bfloat16*>(out_ptrs[dest[jj]]) + (size_t)row * d);
 #pragma unroll
-      for (int i = 0; i < VPL; ++i) {
-        float f[8];
-        bf16x8_to_f32(v[i], f);
+        for (int i = 0; i < VPL; ++i) v[jj][i] = ld_v4(src + lane + 32 * i);
+      }
 #pragma unroll
-        for (int u = 0; u < 8; ++u) acc[i][u] = fmaf(wj, f[u], acc[i][u]);
+      for (int jj = 0; jj < 2; ++jj) {
+        if (dest[jj] < 0) continue;
+#pragma unroll
+        for (int i = 0; i < VPL; ++i) {
+          float f[8];
+          bf16x8_to_f32(v[jj][i], f);
+#pragma unroll
+          for (int u = 0; u < 8; ++u) acc[i][u] = fmaf(wj[jj], f[u], acc[i][u]);
+        }
       }
     }
     uint4* dst = reinterpret_cast<uint4*>(y + (size_t)t * d);
@@ -315,48 +326,75 @@ __global__ void __launch_bounds__(256)
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
   zero_padding_rows<VPL>(groups, num_groups, d, own, warp_global, nwarps, lane);
   for (int t = warp_global; t < T; t += nwarps) {
-    float g[VPL][8];
-    const uint4* src = reinterpret_cast<const uint4*>(dy + (size_t)t * d);
-#pragma unroll
-    for (int i = 0; i < VPL; ++i) bf16x8_to_f32(ld_nc_v4(src + lane + 32 * i), g[i]);
-    int my_dest = 0, my_row = 0;
+    // everything this token needs is requested up front: pair info, the gate's probabilities
+    // (dL/dlogits below), dy, and the Yp rows of two pairs at a time
+    int my_dest = 0, my_row = 0, my_e = -1;
     float my_w = 0.f;
     if (lane < k) {
       my_dest = pair_dest[(size_t)t * k + lane];
       my_row = pair_row[(size_t)t * k + lane];
       my_w = w[(size_t)t * k + lane];
+      my_e = idx[(size_t)t * k + lane];
     }
+    float pq[EP / 32];
+#pragma unroll
+    for (int q = 0; q < EP / 32; ++q) pq[q] = lane + 32 * q < E ? probs[(size_t)t * E + lane + 32 * q] : 0.f;
+    float g[VPL][8];
+    const uint4* src = reinterpret_cast<const uint4*>(dy + (size_t)t * d);
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) bf16x8_to_f32(ld_nc_v4(src + lane + 32 * i), g[i]);
     float my_dw = 0.f;
-    for (int j = 0; j < k; ++j) {
-      const int dest = __shfl_sync(0xffffffffu, my_dest, j);
-      const int row = __shfl_sync(0xffffffffu, my_row, j);
-      const float wj = __shfl_sync(0xffffffffu, my_w, j);
-      if (dest < 0) continue;  // dropped step: dw stays 0
-      const size_t off = (size_t)row * d;
-      const uint4* ysrc = reinterpret_cast<const uint4*>(
-          comb ? comb + (size_t)(t * k + j) * d : reinterpret_cast<const __nv_bfloat16*>(out_ptrs[dest]) + off);
-      uint4* gdst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(dgrad_ptrs[dest]) + off);
-      float dot = 0.f;
+    for (int j0 = 0; j0 < k; j0 += 2) {
+      uint4 yv[2][VPL];
+      int dest[2], row[2];
+      float wj[2];
 #pragma unroll
-      for (int i = 0; i < VPL; ++i) {
-        float yv[8], o[8];
-        bf16x8_to_f32(ld_v4(ysrc + lane + 32 * i), yv);
+      for (int jj = 0; jj < 2; ++jj) {
+        const int j = j0 + jj < k ? j0 + jj : j0;
+        dest[jj] = __shfl_sync(0xffffffffu, my_dest, j);
+        row[jj] = __shfl_sync(0xffffffffu, my_row, j);
+        wj[jj] = __shfl_sync(0xffffffffu, my_w, j);
+        if (j0 + jj >= k) dest[jj] = -1;
+        if (dest[jj] >= 0) {
+          const uint4* ysrc = reinterpret_cast<const uint4*>(
+              comb ? comb + (size_t)(t * k + j) * d
+                   : reinterpret_cast<const __nv_bfloat16*>(out_ptrs[dest[jj]]) + (size_t)row[jj] * d);
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          dot = fmaf(g[i][u], yv[u], dot);
-          o[u] = wj * g[i][u];
+          for (int i = 0; i < VPL; ++i) yv[jj][i] = ld_v4(ysrc + lane + 32 * i);
         }
-        st_v4(gdst + lane + 32 * i, f32x8_to_bf16(o));
       }
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
-      if (lane == j) my_dw = dot;
+      for (int jj = 0; jj < 2; ++jj) {
+        if (dest[jj] < 0) continue;  // beyond k, or dropped step: dw stays 0
+        uint4* gdst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(dgrad_ptrs[dest[jj]]) +
+                                               (size_t)row[jj] * d);
+        float dot = 0.f;
+#pragma unroll
+        for (int i = 0; i < VPL; ++i) {
+          float y8[8], o[8];
+          bf16x8_to_f32(yv[jj][i], y8);
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            dot = fmaf(g[i][u], y8[u], dot);
+            o[u] = wj[jj] * g[i][u];
+          }
+          st_v4(gdst + lane + 32 * i, f32x8_to_bf16(o));
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+        if (lane == j0 + jj) my_dw = dot;
+      }
     }
     if (lane < k) dw[(size_t)t * k + lane] = my_dw;
     // gate softmax backward restricted to the selected experts (dw is complete here):
     //   dl_i = p_i * (dw_{j(i)} [i selected] - sum_j dw_j p_{e_j})
-    const int my_e = lane < k ? idx[(size_t)t * k + lane] : -1;
-    float gsum = lane < k ? my_dw * probs[(size_t)t * E + my_e] : 0.f;
+    float p_sel = 0.f;  // p_{e_j} for lane j < k, from the lane holding expert e_j
+#pragma unroll
+    for (int q = 0; q < EP / 32; ++q) {
+      const float v = __shfl_sync(0xffffffffu, pq[q], my_e & 31);
+      if (lane < k && (my_e >> 5) == q) p_sel = v;
+    }
+    float gsum = lane < k ? my_dw * p_sel : 0.f;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) gsum += __shfl_xor_sync(0xffffffffu, gsum, o);
 #pragma unroll
@@ -368,8 +406,7 @@ __global__ void __launch_bounds__(256)
         const float dwj = __shfl_sync(0xffffffffu, my_dw, j);
         if (ej == i) sel_dw = dwj;
       }
-      const float v = i < E ? probs[(size_t)t * E + i] * (sel_dw - gsum) : 0.f;
-      dl[(size_t)t * EP + i] = __float2bfloat16_rn(v);
+      dl[(size_t)t * EP + i] = __float2bfloat16_rn(i < E ? pq[q] * (sel_dw - gsum) : 0.f);
     }
   }
 }
@@ -521,10 +558,10 @@ int gate_dx_gemm(const void* dl, const void* wg, void* const* dxp_ptrs, const vo
 int gate_dw_gemm(const void* dl, const void* x, int T, int d, int E, int EP, int split, float* ws,
                  float* dwg, cudaStream_t st);
 
-// split-K chunk of the gate weight GEMM: ~one wave of (split, 256-column) tiles, a
+// split-K chunk of the gate weight GEMM: ~one wave of (split, 128-row of d) tiles, a
 // multiple of 128 that divides T
 static int gate_dw_split(int T, int d) {
-  const int want_splits = (148 + d / 256 - 1) / (d / 256);
+  const int want_splits = (148 + d / 128 - 1) / (d / 128);
   int split = 128;
   while (split * 2 <= T && T % (split * 2) == 0 && T / (split * 2) >= want_splits) split *= 2;
   return split;
@@ -544,7 +581,7 @@ extern "C" int pp_gate_dx(const void* dl, const void* wg, void* const* dxp_ptrs,
 
 extern "C" int64_t pp_gate_dw_workspace_bytes(int32_t T, int32_t d) {
   if (T <= 0 || T % PP_CHUNK || d <= 0 || d % 256) return -1;
-  return (int64_t)(T / gate_dw_split(T, d)) * 128 * d * 4;
+  return (int64_t)(T / gate_dw_split(T, d)) * d * 128 * 4;  // [splits][d][EP <= 128] fp32
 }
 
 extern "C" int pp_gate_dw(const void* dl, const void* x, int32_t T, int32_t d, int32_t E, int32_t EP,

@@ -45,9 +45,65 @@ import numpy as np
 import torch
 import torch.distributed as dist
 
-from . import _device, _lib
+from . import _device, _lib, memory
 from .core import ClusterSpec, LoadMatrix, ModelSpec, ValidationError
 from .planner import PlannerConfig
+
+
+def layer_plan(d_model: int, d_ff: int, num_experts: int, top_k: int, tokens: int, world: int,
+               capacity_factor: float | None = None, capacity_rows: int | None = None,
+               max_replicas: int | None = None, replica_engine: str = "copy", planning: str = "host",
+               policy: str | None = None, fused_a2a: bool = False) -> dict:
+    """Allocation rule of one MoELayer (shared by MoELayer and MoEStack's Workspace)."""
+    E, D = num_experts, world
+    m = E // D
+    reps = (E - m) if max_replicas is None else int(max_replicas)
+    if reps < 0:
+        raise ValidationError(f"max_replicas must be >= 0, got {max_replicas}")
+    if str(policy or "").startswith("top") and policy[3:].isdigit() and D > 1 and int(policy[3:]) > reps:
+        raise ValidationError(f"policy {policy} needs max_replicas >= {int(policy[3:])}, got {reps}")
+    slots = m + (reps if D > 1 else 0)
+    max_groups = min(256, m + reps)
+    try:
+        rows = memory.rows_capacity(tokens, top_k, E, D, capacity_factor, capacity_rows)
+    except ValueError as exc:
+        raise ValidationError(str(exc)) from None
+    sm_engine = D > 1 and (replica_engine == "sm" or planning == "device" or str(policy or "").startswith("top"))
+    plan = memory.buffer_plan(d_model, d_ff, E, top_k, tokens, D, rows, slots, max_groups,
+                              fused_a2a=bool(fused_a2a), sm_engine=sm_engine)
+    return {"plan": plan, "rows_cap": rows, "slots": slots, "max_groups": max_groups, "max_replicas": reps,
+            "sm_engine": sm_engine}
+
+
+class Workspace:
+    """Buffers that live only inside one block's backward (memory.buffer_plan scope
+    "shared"/"shared2"): dYp / dXp (peer-mapped), dL/dw, dL/dlogits, the gate dW split-K
+    partials, and the Agg staging (two copies when blocks share it: ``agg_copies``).
+    One per MoEStack; a standalone MoELayer builds its own.  Collective at D > 1."""
+
+    def __init__(self, plan, group, device, agg_copies: int = 1) -> None:
+        b = {x.name: x for x in plan}
+        self._shapes = {n: b[n].shape for n in ("dyp", "dxp", "dw", "dlogits", "gate_ws")}
+        self.dyp = PeerBuffer(b["dyp"].shape, torch.bfloat16, group, device)
+        self.dxp = PeerBuffer(b["dxp"].shape, torch.bfloat16, group, device)
+        self.dw = torch.empty(b["dw"].shape, dtype=torch.float32, device=device)
+        self.dlogits = torch.zeros(b["dlogits"].shape, dtype=torch.bfloat16, device=device)
+        self.gate_ws = torch.empty(b["gate_ws"].shape, dtype=torch.float32, device=device).view(-1)
+        self.agg_stage = []
+        if "agg_stage" in b:
+            self._shapes["agg_stage"] = b["agg_stage"].shape
+            self.agg_stage = [PeerBuffer(b["agg_stage"].shape, torch.float32, group, device) for _ in range(agg_copies)]
+
+    def check(self, plan) -> None:
+        b = {x.name: x for x in plan}
+        for n, shp in self._shapes.items():
+            if n not in b or tuple(b[n].shape) != tuple(shp):
+                raise ValidationError(f"workspace buffer {n} {shp} does not fit this layer")
+
+    def close(self) -> None:
+        for x in (self.dyp, self.dxp, *self.agg_stage):
+            x.close()
+        self.agg_stage = []
 
 
 class CapacityError(RuntimeError):
@@ -189,7 +245,7 @@ class MoELayer(torch.nn.Module):
                  seed: int = 0, device=None, trans_ctas: int = 16, replica_engine: str = "copy",
                  policy: str | None = None, planning: str = "host", placement: str = "virtual",
                  refine_slots: bool = False, fused_a2a: bool = False,
-                 capacity_factor: float | None = None) -> None:
+                 capacity_factor: float | None = None, workspace: "Workspace | None" = None) -> None:
         super().__init__()
         if not torch.cuda.is_available():
             raise RuntimeError("MoELayer needs a CUDA device (B200); there is no CPU path")
@@ -213,19 +269,22 @@ class MoELayer(torch.nn.Module):
         if cluster is None or model is None:
             cluster, model = default_specs(E, top_k, d_model, d_ff, tokens * D)
         self.cluster, self.model = cluster, model
-        self.max_replicas = (E - self.m) if max_replicas is None else max_replicas
-        self.slots = self.m + (self.max_replicas if D > 1 else 0)
-        self.max_groups = min(256, self.m + self.max_replicas)
-        if capacity_rows is not None:
-            rows = capacity_rows
-        elif capacity_factor is not None:
-            if capacity_factor <= 0:
-                raise ValidationError(f"capacity_factor must be > 0, got {capacity_factor}")
-            rows = min(math.ceil(capacity_factor * tokens * top_k), D * tokens * top_k) + E * _lib.PP_ROW_ALIGN
-        else:
-            rows = D * tokens * top_k + E * _lib.PP_ROW_ALIGN
-        self.rows_cap = int(math.ceil(rows / _lib.PP_ROW_ALIGN) * _lib.PP_ROW_ALIGN)
+        # the HBM plan (memory.buffer_plan) this layer allocates from; buffers that live only
+        # inside one block's backward come from a Workspace, shared by the blocks of a stack
+        lp = layer_plan(d_model, d_ff, E, top_k, tokens, D, capacity_factor=capacity_factor,
+                        capacity_rows=capacity_rows, max_replicas=max_replicas, replica_engine=replica_engine,
+                        planning=planning, policy=policy, fused_a2a=fused_a2a)
+        self.max_replicas, self.slots, self.max_groups, self.rows_cap = (
+            lp["max_replicas"], lp["slots"], lp["max_groups"], lp["rows_cap"])
+        self.buffer_plan = lp["plan"]
         dev = self.device
+        if workspace is None:
+            workspace = Workspace(self.buffer_plan, self.group, dev)
+            self._own_workspace = True
+        else:
+            workspace.check(self.buffer_plan)
+            self._own_workspace = False
+        self.workspace = workspace
         g = torch.Generator(device="cpu").manual_seed(seed)
 
         # ---- parameters (bf16) in peer-visible arenas -------------------------
@@ -272,19 +331,17 @@ class MoELayer(torch.nn.Module):
         self._status_ev = None
         self.pair_dest = torch.empty((T, k), **i32)
         self.pair_row = torch.empty((T, k), **i32)
-        self.dw = torch.empty((T, k), dtype=torch.float32, device=dev)
         self.EP = 64 if E <= 64 else 128
-        self.dlogits = torch.zeros((T, self.EP), dtype=torch.bfloat16, device=dev)  # gate dL/dlogits
         ws_bytes = _lib.load().pp_gate_dw_workspace_bytes(T, d_model)
-        if ws_bytes < 0:
+        if ws_bytes < 0 or ws_bytes != workspace.gate_ws.numel() * 4:
             raise ValidationError(f"gate backward: unsupported T={T} / d_model={d_model}")
-        self.gate_ws = torch.empty((ws_bytes // 4,), dtype=torch.float32, device=dev)  # split-K partials of dWg
+        # transient backward buffers (shared): dL/dw, dL/dlogits, dWg split-K partials, dYp, dXp
+        self.dw, self.dlogits, self.gate_ws = workspace.dw, workspace.dlogits, workspace.gate_ws
+        self.dyp, self.dxp = workspace.dyp, workspace.dxp
         # ---- expert activations ---------------------------------------------
         R = self.rows_cap
         self.xp = PeerBuffer((R, d_model), torch.bfloat16, self.group, dev)
         self.yp = PeerBuffer((R, d_model), torch.bfloat16, self.group, dev)
-        self.dyp = PeerBuffer((R, d_model), torch.bfloat16, self.group, dev)
-        self.dxp = PeerBuffer((R, d_model), torch.bfloat16, self.group, dev)
         # fused A2A (FWD2 -> combine, DGRAD1 -> dispatch backward in the GEMM epilogue):
         # pp_dispatch records each received row's origin pair; the epilogues push results
         # straight into the owning rank's comb [T*k][d] (pair order), read locally after
@@ -377,16 +434,16 @@ class MoELayer(torch.nn.Module):
         # SM-engine Agg: replicas push their grads into the home's staging area
         # [m][D-1][W1|W2][d*f] fp32, the home sums them in rank order after a barrier on
         # the comm stream (its own barrier object: its epochs advance on that stream)
-        self.agg_stage = None
         self.trans_flags = None
         if D > 1 and self.replica_engine == "sm":
+            if not workspace.agg_stage:
+                raise ValidationError("the workspace has no Agg staging (built for another replica engine)")
             # Trans completion flags (slot r written by rank r) + the pushers' CTA counter
             self.trans_flags = PeerBuffer((2, D), torch.int64, self.group, dev)  # rows: W1, W2
             self._trans_ctr = torch.zeros(1, dtype=torch.int32, device=dev)
             # layout output: [replicas of my home experts elsewhere, replicas I hold] -> the
             # GEMMs size their SM reservation for Trans / Agg from it, on device
             self.replica_stats = torch.zeros(2, dtype=torch.int32, device=dev)
-            self.agg_stage = PeerBuffer((self.m, D - 1, 2, d_ff * d_model), torch.float32, self.group, dev)
             self.comm_barrier = _Barrier(self.group, dev)
         elif D > 1:
             # copy engine: the replicas pull the home weights; a barrier on the comm stream
@@ -419,6 +476,13 @@ class MoELayer(torch.nn.Module):
         if D > 1:
             torch.cuda.synchronize()
             dist.barrier(group=self.group)
+
+    @property
+    def agg_stage(self):
+        """Agg staging of this block: alternates by block parity in a shared workspace (block
+        i's Agg may still run on the side stream while block i-1's backward starts)."""
+        st = self.workspace.agg_stage
+        return st[self.block_index % len(st)] if st else None
 
     # ------------------------------------------------------------------------
     def set_gate_bias(self, bias) -> None:
@@ -956,11 +1020,13 @@ class MoELayer(torch.nn.Module):
                      expert=int(r[4]), src_rank=int(r[5])) for r in t]
 
     def close(self) -> None:
-        for b in (self.w1_arena, self.w2_arena, self.g1_arena, self.g2_arena, self.xp, self.yp, self.dyp, self.dxp,
-                  self.counts_buf, self.agg_stage, self.origin, self.comb, self.trans_flags,
+        for b in (self.w1_arena, self.w2_arena, self.g1_arena, self.g2_arena, self.xp, self.yp,
+                  self.counts_buf, self.origin, self.comb, self.trans_flags,
                   self.barrier, getattr(self, "comm_barrier", None)):
             if b is not None:
                 b.close()
+        if self._own_workspace:
+            self.workspace.close()
 
 
 class _MoEFunction(torch.autograd.Function):

@@ -26,7 +26,9 @@ import math
 import torch
 import torch.nn.functional as F
 
-from .layer import MoELayer
+import torch.distributed as dist
+
+from .layer import MoELayer, Workspace, layer_plan
 from .perf_model import LayerCost
 from .scheduler import IterationTimeline, Lane, OpKind, ScheduledOp, partition_trans
 
@@ -92,8 +94,16 @@ class MoEStack(torch.nn.Module):
             [Attention(d_model, n_heads, seq_len, dev, seed + 1000 + i) for i in range(num_blocks)])
         self.ln2 = torch.nn.ModuleList(
             [torch.nn.LayerNorm(d_model, device=dev, dtype=torch.bfloat16) for _ in range(num_blocks)])
+        # transient backward buffers (dYp, dXp, dL/dlogits, gate dW partials) and the Agg staging
+        # (two, alternating by block parity) are shared by all blocks: memory.py, DESIGN.md section 5
+        world = dist.get_world_size(group) if (group is not None and dist.is_initialized()) else 1
+        lp = layer_plan(d_model, d_ff, num_experts, top_k, tokens, world,
+                        **{k: v for k, v in layer_kwargs.items()
+                           if k in ("capacity_factor", "capacity_rows", "max_replicas", "replica_engine",
+                                    "planning", "policy", "fused_a2a")})
+        self.workspace = Workspace(lp["plan"], group if world > 1 else None, dev, agg_copies=2)
         self.moe = [MoELayer(d_model, d_ff, num_experts, top_k, tokens, group=group, planner=planner,
-                             seed=seed + i, **layer_kwargs) for i in range(num_blocks)]
+                             seed=seed + i, workspace=self.workspace, **layer_kwargs) for i in range(num_blocks)]
         for i, m in enumerate(self.moe):
             m.block_index = i
             self.add_module(f"moe{i}", m)
@@ -132,6 +142,12 @@ class MoEStack(torch.nn.Module):
     def wait_grads(self) -> None:
         for m in self.moe:
             m.wait_grads()
+
+    def close(self) -> None:
+        torch.cuda.synchronize()
+        for m in self.moe:
+            m.close()
+        self.workspace.close()
 
     # ---- measurement -----------------------------------------------------------
     def start_timeline(self) -> None:
