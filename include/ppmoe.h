@@ -224,15 +224,18 @@ int pp_combine_bwd(const void* dy, void* const* out_ptrs, void* const* dgrad_ptr
                    int32_t T, int32_t d, int32_t k, float* dw, const void* comb,
                    const int32_t* idx, const float* probs, int32_t E, int32_t EP, void* dl, void* stream);
 
-/* Backward of dispatch + the gate's input gradient in ONE tcgen05 kernel:
- *   dx [T][d] bf16 = dl [T][EP] . wg [E][d]  +  sum_j dXp[pair(t, j)]
- * the MMA gives the gate term in TMEM, the epilogue gathers the k expert-input
- * gradient rows (peer loads from dxp_ptrs[pair_dest] at pair_row, or comb[t*k + j]
- * locally in fused-A2A mode), adds in fp32 and stores dx once.  Pairs with
- * pair_dest < 0 (dropped step) contribute nothing. */
-int pp_gate_dx(const void* dl, const void* wg, void* const* dxp_ptrs, const void* comb,
-               const int32_t* pair_dest, const int32_t* pair_row, int32_t T, int32_t d, int32_t k,
-               int32_t E, int32_t EP, void* dx, void* stream);
+/* The gate's input gradient on tcgen05:  dx [T][d] bf16 = dl [T][EP] . wg [E][d]
+ * (overwrites dx; wg rows >= E read as zeros).  Runs early in the backward (dl comes
+ * from pp_combine_bwd); pp_dispatch_bwd adds the expert-input gradients at the end. */
+int pp_gate_dx(const void* dl, const void* wg, int32_t T, int32_t d, int32_t E, int32_t EP, void* dx,
+               void* stream);
+
+/* Backward of dispatch:  dx[t] += sum_j dXp[pair(t, j)]  (fp32 sum, one bf16 rounding),
+ * the k rows pulled from dxp_ptrs[pair_dest] at pair_row (peer loads), or from
+ * comb[t*k + j] locally when the DGRAD1 epilogue pushed them here (fused A2A).  Pairs
+ * with pair_dest < 0 (dropped step) contribute nothing. */
+int pp_dispatch_bwd(void* const* dxp_ptrs, const void* comb, const int32_t* pair_dest,
+                    const int32_t* pair_row, int32_t T, int32_t d, int32_t k, void* dx, void* stream);
 
 /* Gate weight gradient, deterministic: dwg [E][d] fp32 = dl^T . x, split-K over
  * token chunks on tcgen05 into workspace [splits][128][d] fp32 (no atomics), then

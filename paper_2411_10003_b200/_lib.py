@@ -73,7 +73,8 @@ SIGNATURES = {
     "pp_dispatch": [P, P, P, P, P, I, I, I, I, I, P, P, P, P, I, P, P, P, I, P],
     "pp_combine": [P, P, P, P, I, I, I, P, P, P],
     "pp_combine_bwd": [P, P, P, P, P, P, P, P, P, I, I, I, I, P, P, P, P, I, I, P, P],
-    "pp_gate_dx": [P, P, P, P, P, P, I, I, I, I, I, P, P],
+    "pp_gate_dx": [P, P, I, I, I, I, P, P],
+    "pp_dispatch_bwd": [P, P, P, P, I, I, I, P, P],
     "pp_gate_dw": [P, P, I, I, I, I, P, P, P],
     "pp_gate_dw_workspace_bytes": [I, I],
     "pp_grouped_gemm": [I, P, P, P, P, P, P, I, I, I, I, I, I, P],
@@ -140,7 +141,7 @@ def check(rc: int, what: str = "") -> None:
 KERNELS_PER_CALL = {
     "pp_plan_greedy": 1, "pp_plan_physical": 1, "pp_derive_loads": 1, "pp_top_m_mask": 1, "pp_route_topk": 1, "pp_slot_histogram": 1,
     "pp_dispatch_layout": 1, "pp_dispatch": 1, "pp_combine": 1, "pp_combine_bwd": 1,
-    "pp_gate_dx": 1, "pp_gate_dw": 2, "pp_grouped_gemm": 1, "pp_grouped_gemm_ex": 1, "pp_replica_trans": 1,
+    "pp_gate_dx": 1, "pp_dispatch_bwd": 1, "pp_gate_dw": 2, "pp_grouped_gemm": 1, "pp_grouped_gemm_ex": 1, "pp_replica_trans": 1,
     "pp_replica_agg": 1, "pp_replica_agg_reduce": 1, "pp_dot_bf16": 2, "pp_peer_barrier": 1, "pp_agg_accumulate": 1,
 }
 _launches = [0]

@@ -7,8 +7,7 @@ CUDA-event times of the real layer and reports the model's prediction error on
 held-out iterations (the paper reports < 5 % mean error, ``PAPER.md:741``).
 
 Per iteration j with device-derived loads (H, R) under the plan actually used:
-    measured A2A  = dispatch + combine + combine_bwd + (dispatch backward fused with the gate dX,
-                    pp_gate_dx) phases (4 A2As)
+    measured A2A  = dispatch + combine + combine_bwd + dispatch_bwd phases (4 A2As)
     measured FEC  = forward expert GEMMs,  measured BEC = backward expert GEMMs
     model: a2a = max(R) * input_bytes / B,  fec = max(H) / t,  bec = 2 fec
 Fit (least squares through the origin): t = sum(maxH^2) / sum(maxH * FEC);
@@ -21,7 +20,7 @@ from __future__ import annotations
 import numpy as np
 
 A2A_PHASES = (("route_layout", "barrier1"), ("fwd_gemms", "combine"), ("bwd_begin", "combine_bwd"),
-              ("gate_dw", "barrier3"), ("bwd_gemms", "gate_dx"))
+              ("gate_dw", "barrier3"), ("bwd_gemms", "dispatch_bwd"))
 
 
 def per_step_phases(phase_log) -> list:

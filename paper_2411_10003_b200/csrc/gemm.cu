@@ -40,8 +40,7 @@ constexpr int kMaxGroups = 256;
 constexpr int kTraceSteps = 1024;
 
 
-enum Epi { EPI_BF16 = 0, EPI_GELU = 1, EPI_DGELU = 2, EPI_F32 = 3, EPI_ROUTE = 4, EPI_BF16_ADD = 5, EPI_F32_ATOMIC = 6,
-           EPI_GATHER = 7 };
+enum Epi { EPI_BF16 = 0, EPI_GELU = 1, EPI_DGELU = 2, EPI_F32 = 3, EPI_ROUTE = 4, EPI_BF16_ADD = 5, EPI_F32_ATOMIC = 6 };
 
 // per-epilogue-warp staging for the TMA-store epilogue: a ring of out_bufs 32x32
 // blocks (bf16: 2 KB, SWIZZLE_64B; fp32: one 4 KB block, SWIZZLE_128B), so a warp
@@ -51,15 +50,18 @@ enum Epi { EPI_BF16 = 0, EPI_GELU = 1, EPI_DGELU = 2, EPI_F32 = 3, EPI_ROUTE = 4
 // load + GeLU') get deeper rings; the long-K ones keep one block and more stages.
 template <int EPI>
 constexpr int out_bufs() {
-  return EPI == EPI_GELU ? 3 : (EPI == EPI_DGELU || EPI == EPI_GATHER) ? 2 : 1;
+  return EPI == EPI_GELU ? 3 : EPI == EPI_DGELU ? 2 : 1;
 }
 template <int EPI>
 constexpr int out_base() {
-  return (EPI == EPI_DGELU || EPI == EPI_BF16_ADD || EPI == EPI_GATHER) ? 2048 : 0;
+  return (EPI == EPI_DGELU || EPI == EPI_BF16_ADD) ? 2048 : 0;
 }
-template <int EPI>
+// LSU = true: the epilogue's bf16 blocks go out through the LSUs (stage_and_store_lsu), so a
+// warp needs one 2 KB transpose block instead of a ring of TMA-store blocks -- the smem saved
+// buys operand stages (256 x 512 tiles: 4 instead of 3)
+template <int EPI, bool LSU = false>
 constexpr int stage_bytes_per_warp() {
-  return EPI == EPI_F32 ? 4096 : out_base<EPI>() + out_bufs<EPI>() * 2048;
+  return EPI == EPI_F32 ? 4096 : out_base<EPI>() + (LSU ? 1 : out_bufs<EPI>()) * 2048;
 }
 
 struct GemmParams {
@@ -101,17 +103,11 @@ struct GemmParams {
   const uint64_t* gate_flags;
   const uint64_t* gate_epoch;
   int gate_me, gate_D, gate_slot0;
-  // EPI_GATHER (gate dX + dispatch backward): output row t also receives sum_j of the
-  // rows pair (t, j) points at: gather_ptrs[pair_dest][pair_row] (peer memory), or
-  // gather_comb[t*topk + j] when the rows were pushed here (fused A2A)
-  void* const* gather_ptrs;
-  const __nv_bfloat16* gather_comb;
-  const int32_t* pair_dest;
-  const int32_t* pair_row;
   // bf16 epilogue I/O through the LSUs (st.global / ld.global via an smem transpose)
   // instead of TMA stores / loads: the SM's TMA unit moves ~42 B/clk of loads + stores
   // together, and the operand loads alone need more than that at the MMA rate
   int lsu_epi;
+  int fast_gelu;  // FWD1 GeLU / DGRAD2 GeLU' in packed bf16x2 arithmetic (on the bf16 pre-activation)
   // device-adaptive SM reservation: the persistent walk leaves
   // clamp(res_per_unit * (res_stats[0] + (res_both ? res_stats[1] : 0)), res_lo, res_hi) SMs
   // to concurrent side kernels (Trans / Agg), sized by this iteration's replica volume
@@ -163,6 +159,41 @@ __device__ __forceinline__ float gelu_f(float x) {
   return 0.5f * x * (1.f + t);
 }
 
+// GeLU of two bf16 values in packed bf16x2 arithmetic (HFMA2.BF16 + MUFU.TANH.BF16x2): half the
+// FP32-pipe and MUFU work of gelu_f per element, ~1 bf16 ulp more error
+__device__ __forceinline__ uint32_t gelu_bf16x2(uint32_t xv) {
+  const __nv_bfloat162 x = *reinterpret_cast<const __nv_bfloat162*>(&xv);
+  const __nv_bfloat162 c0 = __float2bfloat162_rn(0.7978845608028654f);
+  const __nv_bfloat162 c1 = __float2bfloat162_rn(0.7978845608028654f * 0.044715f);
+  const __nv_bfloat162 half = __float2bfloat162_rn(0.5f);
+  const __nv_bfloat162 u = __hmul2(x, __hfma2(__hmul2(x, x), c1, c0));
+  uint32_t ur = *reinterpret_cast<const uint32_t*>(&u), tr;
+  asm("tanh.approx.bf16x2 %0, %1;" : "=r"(tr) : "r"(ur));
+  const __nv_bfloat162 t = *reinterpret_cast<const __nv_bfloat162*>(&tr);
+  const __nv_bfloat162 hx = __hmul2(x, half);
+  const __nv_bfloat162 g = __hfma2(hx, t, hx);
+  return *reinterpret_cast<const uint32_t*>(&g);
+}
+
+// GeLU'(x) of two bf16 values in packed bf16x2 arithmetic (DGRAD2's epilogue)
+__device__ __forceinline__ uint32_t dgelu_bf16x2(uint32_t xv) {
+  const __nv_bfloat162 x = *reinterpret_cast<const __nv_bfloat162*>(&xv);
+  const __nv_bfloat162 c0 = __float2bfloat162_rn(0.7978845608028654f);
+  const __nv_bfloat162 c1 = __float2bfloat162_rn(0.7978845608028654f * 0.044715f);
+  const __nv_bfloat162 c3 = __float2bfloat162_rn(3.f * 0.7978845608028654f * 0.044715f);
+  const __nv_bfloat162 half = __float2bfloat162_rn(0.5f);
+  const __nv_bfloat162 one = __float2bfloat162_rn(1.f);
+  const __nv_bfloat162 x2 = __hmul2(x, x);
+  const __nv_bfloat162 u = __hmul2(x, __hfma2(x2, c1, c0));
+  uint32_t ur = *reinterpret_cast<const uint32_t*>(&u), tr;
+  asm("tanh.approx.bf16x2 %0, %1;" : "=r"(tr) : "r"(ur));
+  const __nv_bfloat162 t = *reinterpret_cast<const __nv_bfloat162*>(&tr);
+  const __nv_bfloat162 omt2 = __hfma2(__hneg2(t), t, one);   // 1 - t^2
+  const __nv_bfloat162 slope = __hfma2(x2, c3, c0);          // k0 (1 + 3 k1 x^2)
+  const __nv_bfloat162 g = __hfma2(__hmul2(__hmul2(x, half), omt2), slope, __hfma2(half, t, half));
+  return *reinterpret_cast<const uint32_t*>(&g);
+}
+
 __device__ __forceinline__ float dgelu_f(float x) {
   const float k0 = 0.7978845608028654f, k1 = 0.044715f;
   float u = k0 * (x + k1 * x * x * x);
@@ -194,7 +225,7 @@ __device__ __forceinline__ bool decode_tile(int t, const SchedSmem& s, const Gem
 template <int EPI>
 constexpr bool tma_out() {
   return EPI == EPI_BF16 || EPI == EPI_GELU || EPI == EPI_DGELU || EPI == EPI_F32 ||
-         EPI == EPI_BF16_ADD || EPI == EPI_GATHER;
+         EPI == EPI_BF16_ADD;
 }
 
 // Stage a 32x32 bf16 block (row = lane, 16-byte chunk j) with the SWIZZLE_64B
@@ -270,34 +301,11 @@ __device__ __forceinline__ void stage_and_store_f32(uint8_t* stage, const uint32
 }
 
 // Epilogue of one 32-column chunk of one accumulator row (thread = row r).
-// EPI_GATHER: coalesced loads of the gathered rows of one warp's 32x32 output block, for
-// pair slots j = 0, 1 (lane: rows qq*8 + lane/4, 16-byte piece lane%4; zero for dropped pairs)
-__device__ __forceinline__ void gather_issue(uint4 (&g)[2][4], const GemmParams& p, int row0, int col, int lane) {
-#pragma unroll
-  for (int j = 0; j < 2; ++j) {
-#pragma unroll
-    for (int qq = 0; qq < 4; ++qq) {
-      g[j][qq] = make_uint4(0, 0, 0, 0);
-      if (j < p.topk) {
-        const int t = row0 + qq * 8 + (lane >> 2);
-        const int pi = t * p.topk + j;
-        const int dest = p.pair_dest[pi];
-        if (dest >= 0) {
-          const __nv_bfloat16* src =
-              p.gather_comb ? p.gather_comb + (size_t)pi * p.N
-                            : reinterpret_cast<const __nv_bfloat16*>(p.gather_ptrs[dest]) + (size_t)p.pair_row[pi] * p.N;
-          g[j][qq] = ld_v4(src + col + (lane & 3) * 8);
-        }
-      }
-    }
-  }
-}
-
 template <int EPI>
 __device__ __forceinline__ void epilogue_chunk(const uint32_t (&raw)[32], const GemmParams& p,
                                                const Tile& tl, int r, int c, const uint4 (&pre_v)[4],
                                                uint8_t* stage, int& sbuf, const CUtensorMap* tmC,
-                                               const CUtensorMap* tmC2, int lane, const float* gx = nullptr) {
+                                               const CUtensorMap* tmC2, int lane) {
   constexpr int NB = out_bufs<EPI>();
   auto next_buf = [&]() -> uint8_t* {  // ring slot for the next staged 32x32 bf16 block
     uint8_t* b = stage + out_base<EPI>() + sbuf * 2048;
@@ -343,16 +351,6 @@ __device__ __forceinline__ void epilogue_chunk(const uint32_t (&raw)[32], const 
       } else {
         put(v, tmC, p.c);
       }
-    } else if constexpr (EPI == EPI_GATHER) {
-      // dx[t] = (dl . wg)[t] + sum_j dXp[pair(t, j)]  (gx: the gathered sum, fp32)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        float f[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) f[u] = __uint_as_float(raw[8 * j + u]) + gx[8 * j + u];
-        v[j] = f32x8_to_bf16(f);
-      }
-      put(v, tmC, p.c);
     } else if constexpr (EPI == EPI_GELU) {
       uint4 g4[4];
 #pragma unroll
@@ -361,6 +359,10 @@ __device__ __forceinline__ void epilogue_chunk(const uint32_t (&raw)[32], const 
 #pragma unroll
         for (int u = 0; u < 8; ++u) f[u] = __uint_as_float(raw[8 * j + u]);
         v[j] = f32x8_to_bf16(f);
+        if (p.fast_gelu) {  // packed bf16x2 GeLU of the bf16 pre-activation
+          g4[j] = make_uint4(gelu_bf16x2(v[j].x), gelu_bf16x2(v[j].y), gelu_bf16x2(v[j].z), gelu_bf16x2(v[j].w));
+          continue;
+        }
         bf16x8_to_f32(v[j], f);  // GeLU of the bf16-rounded pre-activation, as the backward sees it
 #pragma unroll
         for (int u = 0; u < 8; ++u) g[u] = gelu_f(f[u]);
@@ -372,6 +374,15 @@ __device__ __forceinline__ void epilogue_chunk(const uint32_t (&raw)[32], const 
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         float x[8], f[8];
+        if (EPI == EPI_DGELU && p.fast_gelu) {  // GeLU' in packed bf16x2, product in fp32
+          const uint4 gp = make_uint4(dgelu_bf16x2(pre_v[j].x), dgelu_bf16x2(pre_v[j].y), dgelu_bf16x2(pre_v[j].z),
+                                      dgelu_bf16x2(pre_v[j].w));
+          bf16x8_to_f32(gp, x);
+#pragma unroll
+          for (int u = 0; u < 8; ++u) f[u] = __uint_as_float(raw[8 * j + u]) * x[u];
+          v[j] = f32x8_to_bf16(f);
+          continue;
+        }
         bf16x8_to_f32(pre_v[j], x);
 #pragma unroll
         for (int u = 0; u < 8; ++u)
@@ -427,7 +438,7 @@ __device__ __forceinline__ void epilogue_chunk(const uint32_t (&raw)[32], const 
   }
 }
 
-template <int BN, bool A_MN, bool B_MN, int EPI, int STAGES, int CG>
+template <int BN, bool A_MN, bool B_MN, int EPI, int STAGES, int CG, bool LSU = false>
 __global__ void __launch_bounds__(kThreads, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
                         const __grid_constant__ CUtensorMap tmB,
@@ -720,7 +731,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ================= epilogue =================
     const int q = warp & 3;                  // TMEM lane quarter (hardware: warp % 4)
     const int col0 = ((warp - 4) >> 2) * EPI_COLS;  // column slice of this warp
-    uint8_t* stage = smem + STAGES * STAGE_BYTES + (warp - 4) * stage_bytes_per_warp<EPI>();
+    uint8_t* stage = smem + STAGES * STAGE_BYTES + (warp - 4) * stage_bytes_per_warp<EPI, LSU>();
     uint32_t pre_phase = 0;  // DGELU: parity of this warp's pre-activation TMA barrier
     int sbuf = 0;            // ring slot of the next staged output block
     const int r = q * 32 + lane;
@@ -849,13 +860,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         // software-pipelined: the TMEM read of chunk i+1 is in flight while chunk i is processed
         constexpr int NCH = EPI_COLS / 32;
         uint32_t rawA[32], rawB[32];
-        // EPI_GATHER: the gathered rows of chunk i+1 are in flight while chunk i is processed
-        constexpr int GB = (EPI == EPI_GATHER) ? 2 : 1;
-        uint4 gbuf[GB][2][4];
-        const int grow0 = tl.row_off + tl.m0 + q * 32;
-        if constexpr (EPI == EPI_GATHER) {
-          if (tl.active) gather_issue(gbuf[0], p, grow0, tl.n0 + col0, lane);
-        }
         if (!zero) tmem_ld_32x32b_x32(t_row + col0, rawA);
 #pragma unroll
         for (int i = 0; i < NCH; ++i) {
@@ -889,43 +893,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int j = 0; j < 32; ++j) cur[j] = 0u;
           }
-          float gx[(EPI == EPI_GATHER) ? 32 : 1];
-          if constexpr (EPI == EPI_GATHER) {
-            if (tl.active) {
-              if (i + 1 < NCH) gather_issue(gbuf[(i + 1) & 1], p, grow0, c + 32, lane);
-#pragma unroll
-              for (int u = 0; u < 32; ++u) gx[u] = 0.f;
-#pragma unroll
-              for (int j = 0; j < 2; ++j) {
-                if (j >= p.topk) break;
-                uint4 rv[4];
-                blk_rows_lsu(stage, gbuf[i & 1][j], rv, lane);  // coalesced pieces -> this lane's row
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                  float f[8];
-                  bf16x8_to_f32(rv[u], f);
-#pragma unroll
-                  for (int w = 0; w < 8; ++w) gx[8 * u + w] += f[w];
-                }
-              }
-              for (int j0 = 2; j0 < p.topk; ++j0) {  // top-k > 2: remaining pairs, one at a time
-                const int t = grow0 + lane, pi = t * p.topk + j0, dest = p.pair_dest[pi];
-                if (dest < 0) continue;
-                const __nv_bfloat16* src =
-                    p.gather_comb ? p.gather_comb + (size_t)pi * p.N
-                                  : reinterpret_cast<const __nv_bfloat16*>(p.gather_ptrs[dest]) + (size_t)p.pair_row[pi] * p.N;
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                  float f[8];
-                  bf16x8_to_f32(ld_v4(src + c + 8 * u), f);
-#pragma unroll
-                  for (int w = 0; w < 8; ++w) gx[8 * u + w] += f[w];
-                }
-              }
-            }
-          }
           if (i + 1 == NCH) release_acc();  // every TMEM read of this tile has completed
-          if (tl.active) epilogue_chunk<EPI>(cur, p, tl, r, c, pre_v, stage, sbuf, &tmC, &tmC2, lane, gx);
+          if (tl.active) epilogue_chunk<EPI>(cur, p, tl, r, c, pre_v, stage, sbuf, &tmC, &tmC2, lane);
         }
       }
       if (++acc == NACC) {
@@ -1041,11 +1010,12 @@ static int make_out_tmap_f32(CUtensorMap* m, const void* ptr, uint64_t inner, ui
                    CU_TENSOR_MAP_DATA_TYPE_FLOAT32);
 }
 
-template <int BN, bool A_MN, bool B_MN, int EPI, int STAGES, int CG = 1>
+template <int BN, bool A_MN, bool B_MN, int EPI, int STAGES, int CG = 1, bool LSU = false>
 static int launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, int grid,
                   cudaStream_t st, const CUtensorMap* tc = nullptr, const CUtensorMap* tc2 = nullptr) {
-  auto kern = grouped_gemm_kernel<BN, A_MN, B_MN, EPI, STAGES, CG>;
-  const int staging = tma_out<EPI>() ? 8 * stage_bytes_per_warp<EPI>() : 0;
+  auto kern = grouped_gemm_kernel<BN, A_MN, B_MN, EPI, STAGES, CG, LSU>;
+  const int staging = tma_out<EPI>() ? 8 * stage_bytes_per_warp<EPI, LSU>() : 0;
+  if (LSU && !p.lsu_epi) return fail(PP_EINVAL, "gemm: LSU-staged variant launched without lsu_epi");
   const int smem = STAGES * (BM * BK * 2 + (BN / CG) * BK * 2) + staging + 1024;
   static CUtensorMap dummy{};
   static int configured[64] = {0};  // per device: the smem attribute is set once
@@ -1127,11 +1097,9 @@ int route_gemm(const void* x, const void* wg, const float* bias, int T, int d, i
   }
 }
 
-// dx[T][d] = dl[T][EP] . wg[E][d] + gathered expert-input grads (EPI_GATHER; K = EP,
-// wg rows >= E read as zeros by the TMA)
-int gate_dx_gemm(const void* dl, const void* wg, void* const* dxp_ptrs, const void* comb,
-                 const int32_t* pair_dest, const int32_t* pair_row, int T, int d, int k, int E, int EP,
-                 void* dx, cudaStream_t st) {
+// dx[T][d] = dl[T][EP] . wg[E][d]: the gate's input gradient (K = EP; wg rows >= E read
+// as zeros by the TMA); pp_dispatch_bwd then adds the expert-input gradients
+int gate_dx_gemm(const void* dl, const void* wg, int T, int d, int E, int EP, void* dx, cudaStream_t st) {
   CUtensorMap ta, tb, tc;
   GemmParams p{};
   p.max_groups = 1;
@@ -1139,16 +1107,10 @@ int gate_dx_gemm(const void* dl, const void* wg, void* const* dxp_ptrs, const vo
   p.N = d;
   p.K_fixed = EP;
   p.c = dx;
-  p.topk = k;
-  p.gather_ptrs = dxp_ptrs;
-  p.gather_comb = reinterpret_cast<const __nv_bfloat16*>(comb);
-  p.pair_dest = pair_dest;
-  p.pair_row = pair_row;
-  p.lsu_epi = lsu_epilogue();
   if (int rc = make_tmap(&ta, dl, EP, T, BK, BM)) return rc;
   if (int rc = make_tmap(&tb, wg, d, E, 64, BK)) return rc;
   if (int rc = make_out_tmap(&tc, dx, d, T)) return rc;
-  return launch<256, false, true, EPI_GATHER, 3>(ta, tb, p, sm_count(), st, &tc);
+  return launch<256, false, true, EPI_BF16, 4>(ta, tb, p, sm_count(), st, &tc);
 }
 
 // dwg[e][c] = sum_s ws[s][c][e] (fixed order over the splits: bit-deterministic); thread per
@@ -1309,6 +1271,8 @@ static int grouped_gemm_impl(int32_t mode, const void* a, const void* b, void* c
   p.c = c;
   p.c2 = c2;
   p.lsu_epi = lsu_epilogue();
+  // GeLU / GeLU' in packed bf16x2 arithmetic (FWD1 -4 %, DGRAD2 -8 % at cfg2; PPMOE_GEMM_FAST_GELU=0: fp32)
+  p.fast_gelu = env_int("PPMOE_GEMM_FAST_GELU", 1);
   if (sc) {
     p.origin = sc->origin;
     p.scatter_ptrs = sc->ptrs;
@@ -1346,7 +1310,10 @@ static int grouped_gemm_impl(int32_t mode, const void* a, const void* b, void* c
       if ((rc = make_tmap(&ta, a, dm, R, BK, BM)) || (rc = make_tmap(&tb, b, dm, (uint64_t)S * df, BK, bkb))) return rc;
       p.N = df; p.K_fixed = dm;
       if ((rc = make_out_tmap(&tc, c, df, R)) || (rc = make_out_tmap(&tc2, c2, df, R))) return rc;
-      if (wide_df && env_int("PPMOE_GEMM_FWD1_WIDE", 0)) return PP_LAUNCH_W(EPI_GELU, false, false, 3, &tc, &tc2);
+      if (wide_df && env_int("PPMOE_GEMM_FWD1_WIDE", 0)) {
+        if (p.lsu_epi) return launch<512, false, false, EPI_GELU, 4, 2, true>(ta, tb, p, grid, st, &tc, &tc2);
+        return PP_LAUNCH_W(EPI_GELU, false, false, 3, &tc, &tc2);
+      }
       return PP_LAUNCH(EPI_GELU, false, false, 3, 5, &tc, &tc2);
     case PP_GEMM_FWD2:
       if ((rc = make_tmap(&ta, a, df, R, BK, BM)) ||

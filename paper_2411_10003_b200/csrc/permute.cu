@@ -552,9 +552,60 @@ extern "C" int pp_combine_bwd(const void* dy, void* const* out_ptrs, void* const
 }
 
 namespace pp {
-int gate_dx_gemm(const void* dl, const void* wg, void* const* dxp_ptrs, const void* comb,
-                 const int32_t* pair_dest, const int32_t* pair_row, int T, int d, int k, int E, int EP,
-                 void* dx, cudaStream_t st);
+int gate_dx_gemm(const void* dl, const void* wg, int T, int d, int E, int EP, void* dx, cudaStream_t st);
+
+// dx[t] += sum_j dXp[pair(t, j)]: warp per token, 16-byte vectors, the k rows of two pairs
+// in flight at a time (peer loads over NVLink), fp32 sum with the gate term already in dx
+template <int VPL>
+__global__ void __launch_bounds__(256)
+    dispatch_bwd_kernel(void* const* dxp_ptrs, const __nv_bfloat16* __restrict__ comb,
+                        const int32_t* __restrict__ pair_dest, const int32_t* __restrict__ pair_row,
+                        int T, int d, int k, __nv_bfloat16* dx) {
+  const int lane = threadIdx.x & 31;
+  const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int t = warp_global; t < T; t += nwarps) {
+    int my_dest = -1, my_row = 0;
+    if (lane < k) {
+      my_dest = pair_dest[(size_t)t * k + lane];
+      my_row = pair_row[(size_t)t * k + lane];
+    }
+    uint4* drow = reinterpret_cast<uint4*>(dx + (size_t)t * d);
+    float acc[VPL][8];
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) bf16x8_to_f32(ld_v4(drow + lane + 32 * i), acc[i]);
+    for (int j0 = 0; j0 < k; j0 += 2) {
+      uint4 v[2][VPL];
+      int dest[2];
+#pragma unroll
+      for (int jj = 0; jj < 2; ++jj) {
+        const int j = j0 + jj < k ? j0 + jj : j0;
+        dest[jj] = __shfl_sync(0xffffffffu, my_dest, j);
+        const int row = __shfl_sync(0xffffffffu, my_row, j);
+        if (j0 + jj >= k) dest[jj] = -1;
+        if (dest[jj] < 0) continue;
+        const uint4* src = reinterpret_cast<const uint4*>(
+            comb ? comb + (size_t)(t * k + j) * d
+                 : reinterpret_cast<const __nv_bfloat16*>(dxp_ptrs[dest[jj]]) + (size_t)row * d);
+#pragma unroll
+        for (int i = 0; i < VPL; ++i) v[jj][i] = ld_v4(src + lane + 32 * i);
+      }
+#pragma unroll
+      for (int jj = 0; jj < 2; ++jj) {
+        if (dest[jj] < 0) continue;
+#pragma unroll
+        for (int i = 0; i < VPL; ++i) {
+          float f[8];
+          bf16x8_to_f32(v[jj][i], f);
+#pragma unroll
+          for (int u = 0; u < 8; ++u) acc[i][u] += f[u];
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) st_v4(drow + lane + 32 * i, f32x8_to_bf16(acc[i]));
+  }
+}
 int gate_dw_gemm(const void* dl, const void* x, int T, int d, int E, int EP, int split, float* ws,
                  float* dwg, cudaStream_t st);
 
@@ -568,15 +619,25 @@ static int gate_dw_split(int T, int d) {
 }
 }  // namespace pp
 
-extern "C" int pp_gate_dx(const void* dl, const void* wg, void* const* dxp_ptrs, const void* comb,
-                          const int32_t* pair_dest, const int32_t* pair_row, int32_t T, int32_t d, int32_t k,
-                          int32_t E, int32_t EP, void* dx, void* stream) {
-  PP_CHECK_ARG(dl && wg && (dxp_ptrs || comb) && pair_dest && pair_row && dx, "pp_gate_dx: null pointer");
+extern "C" int pp_gate_dx(const void* dl, const void* wg, int32_t T, int32_t d, int32_t E, int32_t EP, void* dx,
+                          void* stream) {
+  PP_CHECK_ARG(dl && wg && dx, "pp_gate_dx: null pointer");
   PP_CHECK_ARG(d % 256 == 0, "pp_gate_dx: d=%d must be a multiple of 256", d);
   PP_CHECK_ARG(T > 0 && T % PP_CHUNK == 0, "pp_gate_dx: T=%d must be a multiple of %d", T, PP_CHUNK);
   PP_CHECK_ARG((EP == 64 || EP == 128) && E >= 1 && E <= EP, "pp_gate_dx: bad E=%d/EP=%d", E, EP);
-  PP_CHECK_ARG(k >= 1 && k <= 8, "pp_gate_dx: k=%d", k);
-  return gate_dx_gemm(dl, wg, dxp_ptrs, comb, pair_dest, pair_row, T, d, k, E, EP, dx, as_stream(stream));
+  return gate_dx_gemm(dl, wg, T, d, E, EP, dx, as_stream(stream));
+}
+
+extern "C" int pp_dispatch_bwd(void* const* dxp_ptrs, const void* comb, const int32_t* pair_dest,
+                               const int32_t* pair_row, int32_t T, int32_t d, int32_t k, void* dx, void* stream) {
+  PP_CHECK_ARG((dxp_ptrs || comb) && pair_dest && pair_row && dx, "pp_dispatch_bwd: null pointer");
+  PP_CHECK_ARG(k >= 1 && k <= 8, "pp_dispatch_bwd: k=%d", k);
+  cudaStream_t st = as_stream(stream);
+  PP_VPL_SWITCH(d, (dispatch_bwd_kernel<VPL><<<grid_for_tokens(T), 256, 0, st>>>(
+                       dxp_ptrs, reinterpret_cast<const __nv_bfloat16*>(comb), pair_dest, pair_row, T, d, k,
+                       reinterpret_cast<__nv_bfloat16*>(dx))));
+  PP_LAUNCH_CHECK();
+  return PP_OK;
 }
 
 extern "C" int64_t pp_gate_dw_workspace_bytes(int32_t T, int32_t d) {

@@ -22,8 +22,8 @@ the reference's objects are its interface:
     K2 pp_plan_greedy /    (D>1, side stream) plan for iteration j+1 on this
        pp_plan_physical    iteration's LoadMatrix (plan_for_iteration rule)
   backward mirrors it: combine_bwd (push; also dL/dlogits), gate dW (deterministic
-  split-K), WGRAD2/DGRAD2/WGRAD1/DGRAD1 (order depends on the replica engine), then
-  pp_gate_dx = dispatch backward + gate dX in one tcgen05 kernel, K5 Agg (D>1).
+  split-K) and gate dX (tcgen05, writes dx), WGRAD2/DGRAD2/WGRAD1/DGRAD1 (order depends
+  on the replica engine), then pp_dispatch_bwd adds the expert-input grads, K5 Agg (D>1).
 
 Virtual expert slots: with m = E/D experts per rank, each
 rank's T tokens are cut into m contiguous slots; slot v = rank*m + j is a
@@ -909,6 +909,10 @@ class MoELayer(torch.nn.Module):
         # fills the wait for the slowest rank's combine_bwd at the next barrier
         _lib.call("pp_gate_dw", self.dlogits.data_ptr(), x.data_ptr(), self.T, self.d, self.E, self.EP,
                   self.gate_ws.data_ptr(), self.wg.main_grad.data_ptr(), sp)
+        # the gate's input gradient dx = dL/dlogits . Wg (tcgen05); the dispatch backward adds to it
+        dx = torch.empty((self.T, self.d), dtype=torch.bfloat16, device=self.device)
+        _lib.call("pp_gate_dx", self.dlogits.data_ptr(), self.wg.data_ptr(), self.T, self.d, self.E, self.EP,
+                  dx.data_ptr(), sp)
         self._mark("gate_dw")
         self.barrier()
         self._mark("barrier3")
@@ -939,13 +943,10 @@ class MoELayer(torch.nn.Module):
         self._mark("bwd_gemms")
         self.barrier()
         self._mark("barrier4")
-        dx = torch.empty((self.T, self.d), dtype=torch.bfloat16, device=self.device)
-        # dispatch backward + gate input grad in one tcgen05 kernel: dx = dl . Wg + sum_j dXp[pair]
-        _lib.call("pp_gate_dx", self.dlogits.data_ptr(), self.wg.data_ptr(),
-                  None if self.fused_a2a else self.dxp.ptrs.data_ptr(), self._comb_local(),
-                  self.pair_dest.data_ptr(), self.pair_row.data_ptr(), self.T, self.d, self.k, self.E, self.EP,
-                  dx.data_ptr(), sp)
-        self._mark("gate_dx")
+        # dispatch backward: dx += sum_j dXp[pair] (peer loads; fused A2A: local comb)
+        _lib.call("pp_dispatch_bwd", None if self.fused_a2a else self.dxp.ptrs.data_ptr(), self._comb_local(),
+                  self.pair_dest.data_ptr(), self.pair_row.data_ptr(), self.T, self.d, self.k, dx.data_ptr(), sp)
+        self._mark("dispatch_bwd")
         if self.planning == "device" and self.world > 1:
             cur = torch.cuda.current_stream()
             if self._agg_done is not None:  # join the Agg side stream (graph-capturable fork/join)

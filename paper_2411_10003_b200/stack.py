@@ -189,7 +189,7 @@ class MoEStack(torch.nn.Module):
                 (OpKind.BEC, Lane.COMPUTE, "combine_bwd", "gate_dw"),
                 (OpKind.A2A, Lane.NETWORK, "gate_dw", "barrier3"),
                 (OpKind.BEC, Lane.COMPUTE, "barrier3", "bwd_gemms"),
-                (OpKind.A2A, Lane.NETWORK, "bwd_gemms", "gate_dx"),
+                (OpKind.A2A, Lane.NETWORK, "bwd_gemms", "dispatch_bwd"),
             ]
             for kind, lane, a, b in groups:
                 if a in seq and b in seq:

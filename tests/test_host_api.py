@@ -230,10 +230,10 @@ def test_cost_model_calibration_fit():
     assert abs(fit["avg_bandwidth"] / B_true - 1) < 1e-9
     assert fit["mean_abs_rel_error"] < 1e-9 and fit["train_iters"] == 4 and fit["test_iters"] == 4
     step = {"route_layout": 0.1, "barrier1": 0.3, "fwd_gemms": 1.0, "combine": 1.2, "bwd_begin": 1.25,
-            "combine_bwd": 1.3, "gate_dw": 1.35, "barrier3": 1.4, "bwd_gemms": 3.0, "gate_dx": 3.2}
+            "combine_bwd": 1.3, "gate_dw": 1.35, "barrier3": 1.4, "bwd_gemms": 3.0, "dispatch_bwd": 3.2}
     m = calibrate.measured_costs(step)
     assert abs(m["fec"] - 0.7e-3) < 1e-12 and abs(m["bec"] - 1.6e-3) < 1e-12
-    # A2A spans: dispatch, combine, combine_bwd (without the gate dW), dispatch bwd (gate_dx)
+    # A2A spans: dispatch, combine, combine_bwd (without the gate dW / dX), dispatch bwd
     assert abs(m["a2a_total"] - (0.2 + 0.2 + (0.05 + 0.05) + 0.2) * 1e-3) < 1e-12
 
 
