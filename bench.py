@@ -34,7 +34,10 @@ CONFIGS = {
     "cfg1": dict(E=8, k=2, d=512, f=1024, T=1024, desc="8 experts top-2 d512 4096 tokens over 4 ranks"),
     "cfg2": dict(E=16, k=2, d=1024, f=4096, T=16384, desc="16 experts top-2 d1024 f4096 16K tokens/GPU skewed"),
     "cfg3": dict(E=32, k=2, d=2048, f=4096, T=32768, desc="32 experts top-2 d2048 f4096 32K tokens/GPU EP"),
-    "cfg4": dict(E=64, k=2, d=2048, f=4096, T=32768, desc="64 experts top-2 d2048 32K tokens/GPU Zipf drift"),
+    "cfg4": dict(E=64, k=2, d=2048, f=4096, T=32768, drift=0.05,
+                 desc="64 experts top-2 d2048 32K tokens/GPU, Zipf(1.2) popularity drifting every iteration"),
+    "cfg4k1": dict(E=64, k=1, d=2048, f=4096, T=32768, drift=0.05,
+                   desc="64 experts top-1 d2048 32K tokens/GPU, Zipf(1.2) popularity drifting every iteration"),
     "cfg5": dict(E=64, k=2, d=2048, f=4096, T=8192, L=12, desc="12-block MoE-GPT stack, 64 experts top-2 d2048 f4096, "
                  "8K tokens/GPU (4 x 2048-token sequences), attention in stock PyTorch, Algorithm-2 overlap"),
 }
@@ -67,6 +70,39 @@ def zipf_bias(E: int, skew: float, seed: int):
     p = np.empty(E)
     p[perm] = w
     return np.log(p)
+
+
+class PopularityDrift:
+    """Per-iteration expert popularity of the reference trace generator (workload.py:89-136):
+    base = Zipf(skew) in a seeded random order, then every iteration
+    p <- (1 - drift) p + drift * Dirichlet(base * 10 * E), renormalised.  The bench turns p into
+    the gate's per-expert logit bias log p, so the routed load drifts like the reference's."""
+
+    def __init__(self, E: int, skew: float = 1.2, drift: float = 0.05, seed: int = 0) -> None:
+        import numpy as np
+
+        master = np.random.default_rng(seed)
+        self.rng = np.random.default_rng(master.integers(0, 2**63 - 1))
+        w = np.arange(1, E + 1, dtype=np.float64) ** -skew
+        w /= w.sum()
+        perm = self.rng.permutation(E)
+        self.base = np.empty(E)
+        self.base[perm] = w
+        self.p = self.base.copy()
+        self.drift, self.E = drift, E
+
+    def step(self):
+        fresh = self.rng.dirichlet(self.base * 10.0 * self.E)
+        p = self.p
+        if self.drift > 0.0:
+            self.p = (1.0 - self.drift) * p + self.drift * fresh
+            self.p /= self.p.sum()
+        return p
+
+    def log_bias_schedule(self, n: int):
+        import numpy as np
+
+        return np.log(np.stack([self.step() for _ in range(n)]))
 
 
 class ClockSampler:
@@ -178,21 +214,32 @@ def cpu_baseline(cfg: dict, budget_s: float = 15.0) -> dict:
                       f"torch-CPU fp32 oracle (oracle/moe_ref.cpu_layer_step), {el:.1f}s"}
 
 
-def cpu_planner_ms(E: int, k: int, T: int, d: int, f: int) -> dict:
-    """Oracle planner (restatement of reference greedy_search, pinned to its
-    goldens) on a Zipf-skewed virtual-slot LoadMatrix, 1 core."""
+def cpu_planner_leg(recs, dev_masks, cluster, model, cfg, E: int, k: int, calib_samples, placement: str,
+                    world: int) -> dict:
+    """CPU baseline of the planner: the oracle restatement of reference greedy_search (pinned to
+    the reference's goldens, 1 core) on the SAME recorded LoadMatrices the device searched,
+    plus the parity checks: device plans == oracle plans on those matrices, and (N > 1,
+    virtual slots) the plan each recorded iteration ran with == the oracle's plan on the
+    previous iteration's LoadMatrix (plan_for_iteration, planner.py:132-156)."""
     import numpy as np
 
     from oracle import planner_ref as P
 
-    rng = np.random.default_rng(0)
-    p = np.exp(zipf_bias(E, 1.2, 0))
-    mats = [np.stack([rng.multinomial(T * k // E if E else 0, p) for _ in range(E)]) for _ in range(8)]
-    cm = P.cost_model_dict(E, k, 2 * d, 4 * d * f, 8 * d * f, 450e9, 1.2e15 / (6.0 * d * f))
+    cm = P.cost_model_dict(E, k, model.input_bytes, model.expert_param_bytes, model.expert_grad_bytes,
+                           cluster.avg_bandwidth, cluster.compute_throughput, model.fnec_time, model.bnec_time)
     t0 = time.perf_counter()
-    for mm in mats:
-        P.greedy_search(mm, 1, 0.5, False, cm)
-    return {"ms_per_layer": (time.perf_counter() - t0) / len(mats) * 1e3, "mats": mats, "cm": cm}
+    plans = [P.greedy_search(m_, cfg.n, cfg.alpha, cfg.overlap_aware, cm) for m_ in recs]
+    ms = (time.perf_counter() - t0) / len(recs) * 1e3
+    equal = sum(int(np.array_equal(pl["mask"], dm)) for pl, dm in zip(plans, dev_masks))
+    res = {"cpu_oracle_ms_per_layer": ms, "cpu_cores": 1,
+           "device_vs_oracle_plans_equal": f"{equal}/{len(recs)}"}
+    if world > 1 and placement == "virtual" and len(calib_samples) > 1:
+        ok = 0
+        for (c_prev, _), (_, m_used) in zip(calib_samples[:-1], calib_samples[1:]):
+            exp = P.greedy_search(c_prev.cpu().numpy(), cfg.n, cfg.alpha, cfg.overlap_aware, cm)
+            ok += int(np.array_equal(exp["mask"], m_used.cpu().numpy().astype(bool)))
+        res["in_loop_plan_parity"] = f"{ok}/{len(calib_samples) - 1}"
+    return res
 
 
 # --------------------------------------------------------------------------- reference arm
@@ -236,63 +283,92 @@ def run_reference(args, cfg_name: str, cfg: dict) -> None:
 
 # --------------------------------------------------------------------------- stack (cfg5)
 def run_stack(args, cfg_name: str, cfg: dict, world: int, rank: int, dev, group) -> dict:
-    """Config 5: L-block stack, fwd+bwd per step, eager (host-driven Trans per block),
-    with the measured Algorithm-2 timeline of one iteration."""
+    """Config 5: L-block stack, fwd+bwd per step.  N > 1: device-planned layers (plan, SM-engine
+    Trans/Agg, barriers all on the device), the whole iteration one CUDA graph; Trans of block i
+    starts with its attention (Algorithm 2's FNEC window) and finishes under FWD1's home tiles.
+    The exposure metric comes from timing events captured inside a second graph of the step."""
     import torch
     import torch.distributed as dist
 
     import paper_2411_10003_b200 as pp
-    from paper_2411_10003_b200.stack import MoEStack
+    from paper_2411_10003_b200.stack import MoEStack, exposure_summary
 
     E, k, d, f, T, L = cfg["E"], cfg["k"], cfg["d"], cfg["f"], cfg["T"], cfg["L"]
     planner = pp.PlannerConfig(n=1, alpha=0.5, reuse_interval=1, overlap_aware=True)
-    stack = MoEStack(L, d, f, E, k, T, group=group, planner=planner, seq_len=2048, n_heads=16)
+    kw = dict(planning="device", capacity_factor=args.capacity_factor, max_replicas=args.max_replicas) \
+        if world > 1 else {}
+    stack = MoEStack(L, d, f, E, k, T, group=group, planner=planner, seq_len=2048, n_heads=16, **kw)
     for m in stack.moe:
         m.set_gate_bias(zipf_bias(E, 1.2, m.block_index))
     g = torch.Generator(device="cpu").manual_seed(1000 + rank)
     x = torch.randn((T, d), generator=g).to(dev, torch.bfloat16)
     dy = (torch.randn((T, d), generator=g) * 0.1).to(dev, torch.bfloat16)
+    use_graph = not args.eager
 
-    def step():
+    def step_eager():
         xin = x.detach().requires_grad_(True)
         y = stack(xin)
         y.backward(dy)
         stack.wait_grads()
 
     for _ in range(args.warmup):
-        step()
+        step_eager()
+    torch.cuda.synchronize()
+    sg = stack.make_graphed_step(x, dy) if use_graph else None
+    run = sg if use_graph else step_eager
+    for _ in range(2):
+        run()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        stack.moe[0].barrier()  # the ranks' timed regions start together
     t0.record()
     for _ in range(args.steps):
-        step()
+        run()
     t1.record()
     torch.cuda.synchronize()
     ms = torch.tensor([t0.elapsed_time(t1) / args.steps], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     ms_step = float(ms.item())
-    # one instrumented iteration -> reference-schema measured timeline
-    stack.start_timeline()
-    step()
-    tl = stack.measured_timeline(iteration=0)
-    stack.stop_timeline()
-    mk = tl.makespan()
-    exposed_trans = sum(tl.exposed_trans_seconds(i) for i in range(L))
-    exposed_agg = sum(tl.exposed_agg_seconds(i) for i in range(L))
-    trans_total = sum(o.duration for o in tl.ops if o.kind.value.startswith("SubTrans"))
-    agg_total = sum(o.duration for o in tl.ops if o.kind.value.startswith("SubAgg"))
-    return {"value": world * T / (ms_step / 1e3), "ms_per_step": ms_step,
-            "timeline": {"makespan_ms": mk * 1e3, "phase_totals_ms": {k_: v * 1e3 for k_, v in tl.phase_totals().items()},
-                         "replica_comm_ms": (trans_total + agg_total) * 1e3,
-                         "exposed_replica_comm_ms": (exposed_trans + exposed_agg) * 1e3,
-                         "exposed_replica_comm_frac": (exposed_trans + exposed_agg) / mk if mk > 0 else 0.0,
-                         "definition": "reference IterationTimeline.exposed_*_seconds on the measured CUDA-event timeline",
-                         "replicas_per_block": [len(m.replica_experts) for m in stack.moe]},
-            "timeline_json": tl.to_json_obj()}
+    # one instrumented iteration -> reference-schema measured timeline (graph nodes when graphed)
+    if use_graph:
+        tg = stack.make_graphed_step(x, dy, timeline_events=True)
+        tls = []
+        for _ in range(5):
+            run()
+            tg()
+            torch.cuda.synchronize()
+            tls.append(tg.timeline(iteration=0))
+        tls.sort(key=lambda t_: exposure_summary(t_, L)["exposed_replica_comm_frac"])
+        tl = tls[len(tls) // 2]
+    else:
+        stack.start_timeline()
+        step_eager()
+        tl = stack.measured_timeline(iteration=0)
+        stack.stop_timeline()
+    ex = exposure_summary(tl, L)
+    fr = torch.tensor([ex["exposed_replica_comm_frac"]], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(fr, op=dist.ReduceOp.MAX)
+    ex["exposed_replica_comm_frac_max_over_ranks"] = float(fr.item())
+    ex["phase_totals_ms"] = {k_: v * 1e3 for k_, v in tl.phase_totals().items()}
+    ex["source"] = "CUDA events captured inside a graph of the step (median of 5 replays)" if use_graph \
+        else "eager instrumented iteration"
+    from paper_2411_10003_b200 import memory
+
+    fp = memory.stack_footprint(L, d, f, E, k, T, world, args.capacity_factor if world > 1 else None,
+                                args.max_replicas if world > 1 else None, sm_engine=world > 1)
+    res = {"value": world * T / (ms_step / 1e3), "ms_per_step": ms_step, "timeline": ex,
+           "timeline_json": tl.to_json_obj(), "graphed": use_graph,
+           "hbm_plan_gb": {"total": fp["total"] / 1e9, "per_layer": fp["per_layer"] / 1e9,
+                           "shared": fp["shared"] / 1e9, "rows_capacity": fp["rows_capacity"], "slots": fp["slots"]},
+           "torch_max_allocated_gb": torch.cuda.max_memory_allocated() / 1e9}
+    stack.close()
+    return res
 
 
 # --------------------------------------------------------------------------- our arm
@@ -311,11 +387,19 @@ def main() -> None:
                     help="planner n: devices a selected expert skips (default 1 virtual, 0 physical)")
     ap.add_argument("--policy", default="greedy-overlap",
                     help="vanilla | top<m> | greedy | greedy-overlap (reference simulator policies)")
-    ap.add_argument("--placement", default="physical", choices=["virtual", "physical"],
+    ap.add_argument("--placement", default="virtual", choices=["virtual", "physical"],
                     help="planner over physical devices (E = m*D generalisation, 8(f) row 4; == the reference "
                          "search when E == D) or over E x E virtual expert slots (the reference search verbatim)")
-    ap.add_argument("--refine-slots", type=int, default=1,
+    ap.add_argument("--refine-slots", type=int, default=0,
                     help="physical placement: slot-level refinement of the plan (1/0; beyond the paper)")
+    ap.add_argument("--capacity-factor", type=float, default=2.0,
+                    help="cfg5 stack at N > 1: receive rows per rank = factor * T * k (+ padding); overflow is "
+                         "detected on device (CapacityError)")
+    ap.add_argument("--max-replicas", type=int, default=16,
+                    help="cfg5 stack at N > 1: replica weight slots per rank (the planner never exceeds it)")
+    ap.add_argument("--alt-placement", type=int, default=1,
+                    help="N > 1: also time the physically-faithful planner with slot refinement (the extension "
+                         "of 8(f) row 4) and report it beside the headline reference-search number")
     ap.add_argument("--fused-a2a", type=int, default=0,
                     help="combine / dispatch-backward fused into the FWD2 / DGRAD1 epilogues (1/0; default 0: with "
                          "the 256x512 tiles the unfused path measured 3 %% faster at 2 and 4 GPUs)")
@@ -349,12 +433,18 @@ def main() -> None:
     world = world_env
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    ngpu = torch.cuda.device_count()
+    emulated = world > ngpu  # ranks sharing a GPU (functional check only; numbers meaningless)
+    local_rank = local_rank % ngpu
     torch.cuda.set_device(local_rank)
     bind_cpu_to_gpu(local_rank)  # pinned host batches then live on the GPU's NUMA node
     dev = torch.device("cuda", local_rank)
     group = None
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if emulated:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
         group = dist.group.WORLD
     if "L" in cfg:  # config 5: the block stack
         res = run_stack(args, cfg_name, cfg, world, rank, dev, group)
@@ -364,7 +454,8 @@ def main() -> None:
                    "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
                    "data": "synthetic", "config": {"workload": f"{cfg_name}: {cfg['desc']}",
                                                    "parallelism": f"ep{world}"},
-                   "stack_timeline": res["timeline"]}
+                   "stack_timeline": res["timeline"], "graphed": res["graphed"], "hbm_plan_gb": res["hbm_plan_gb"],
+                   "torch_max_allocated_gb": res["torch_max_allocated_gb"]}
             print(json.dumps(out), flush=True)
             Path(ROOT, "gpurun_out").mkdir(exist_ok=True)
             Path(ROOT, "gpurun_out", f"timeline_{cfg_name}_n{world}.json").write_text(json.dumps(res["timeline_json"]))
@@ -400,12 +491,26 @@ def main() -> None:
         layer.res_per_replica = args.res_per_replica
     if args.trans_gate is not None:
         layer.trans_gate = bool(args.trans_gate)
-    layer.set_gate_bias(zipf_bias(E, 1.2, 0))
+    drift = None
+    if cfg.get("drift"):  # cfg4: popularity drifting every iteration (reference workload.py:113-136)
+        drift = PopularityDrift(E, skew=1.2, drift=cfg["drift"], seed=0)
+        bias_host = torch.from_numpy(drift.log_bias_schedule(args.warmup + 8 + 4 * args.steps + 64)).float()
+        bias_host = bias_host.pin_memory()
+        bias_pos = [0]
+
+        def next_bias():
+            layer.gate_bias.copy_(bias_host[bias_pos[0] % bias_host.shape[0]], non_blocking=True)
+            bias_pos[0] += 1
+        layer.set_gate_bias(bias_host[0])
+    else:
+        layer.set_gate_bias(zipf_bias(E, 1.2, 0))
     g = torch.Generator(device="cpu").manual_seed(1000 + rank)
     x = torch.randn((T, d), generator=g).to(dev, torch.bfloat16)
     dy = (torch.randn((T, d), generator=g) * 0.1).to(dev, torch.bfloat16)
 
     def step(xin, dyin):
+        if drift is not None:
+            next_bias()
         xin.requires_grad_(True)
         y = layer(xin)
         y.backward(dyin)
@@ -425,7 +530,11 @@ def main() -> None:
     xs = [x.detach().clone() for _ in range(NB)]
     if use_graph:
         graphs = [layer.make_graphed_step(xs[b], dy.clone(), with_loss=True) for b in range(NB)]
-        run_step = lambda i: graphs[i % NB]()  # noqa: E731
+
+        def run_step(i):
+            if drift is not None:  # this iteration's gate popularity (256 B H2D, stream-ordered)
+                next_bias()
+            return graphs[i % NB]()
     else:
         run_step = lambda i: step(xs[i % NB].detach(), dy)  # noqa: E731
     for i in range(2):
@@ -482,6 +591,35 @@ def main() -> None:
         pm = {names.get(m, str(m)): statistics.median(v) for m, v in per.items()}
         gemm_graph = {"ms_per_step": sum(pm.values()), "per_mode_ms": pm}
 
+    # ---- exposed replica communication of the graphed EP step: the reference's metric
+    # (IterationTimeline.exposed_*, scheduler.py:134-169) on CUDA events captured as graph
+    # nodes, replayed between timed-graph replays; median replay, max over ranks
+    exposure = None
+    if use_graph and world > 1:
+        from paper_2411_10003_b200.stack import exposure_summary
+
+        from paper_2411_10003_b200 import calibrate as _cal
+
+        tlg = layer.make_graphed_step(xs[0].clone(), dy.clone(), with_loss=True, timeline_events=True)
+        samples_exp, graph_calib = [], []
+        for _ in range(24):
+            for i in range(3):
+                run_step(i)
+            mask_before = layer.mask_buf.clone()  # the plan this replay runs with
+            tlg()
+            counts_r = layer.counts.clone()       # its LoadMatrix (stream-ordered, before the next step)
+            run_step(0)
+            torch.cuda.synchronize()
+            samples_exp.append(exposure_summary(tlg.timeline()))
+            graph_calib.append((counts_r, mask_before, _cal.per_step_phases(tlg.phase_log)[0]))
+        del tlg
+        samples_exp.sort(key=lambda e_: e_["exposed_replica_comm_frac"])
+        exposure = samples_exp[len(samples_exp) // 2]
+        fr = torch.tensor([exposure["exposed_replica_comm_frac"]], dtype=torch.float64, device=dev)
+        dist.all_reduce(fr, op=dist.ReduceOp.MAX)
+        exposure["exposed_replica_comm_frac_max_over_ranks"] = float(fr.item())
+        exposure["source"] = "rank 0 median of 24 instrumented graph replays (external events as graph nodes)"
+
     # ---- instrumented eager pass of the same K steps: per-GEMM CUDA events on the
     # launching stream (graph replays cannot carry timing events) + phase timeline
     _lib.reset_launch_count()
@@ -494,13 +632,15 @@ def main() -> None:
     layer.phase_log = []
     layer.timeline_log = [] if world > 1 else None  # side-stream ops: Plan, Trans, Agg
     calib_samples = []
-    n_phase_steps = 6 if world > 1 else 2
+    recorded = []  # this run's LoadMatrices (virtual E x E) for the planner legs
+    n_phase_steps = 12
     for i in range(n_phase_steps):
         xin = xs[i % 2].detach().requires_grad_(True)
         y = layer(xin)
         # the plan this step runs with (device copy: no mid-step host sync to skew the phases)
         mask = layer.mask_cur.clone() if world > 1 and layer.mask_cur is not None else None
         y.backward(dy)
+        recorded.append(layer.counts.clone())
         if world > 1:  # loads under that plan (device derive_loads)
             calib_samples.append((layer.counts.clone(), mask))
     torch.cuda.synchronize()
@@ -525,10 +665,13 @@ def main() -> None:
 
         from paper_2411_10003_b200 import calibrate
 
-        steps_ph = calibrate.per_step_phases(layer.phase_log)
+        # graph-timed phases of the instrumented replays (no host launch gaps); 3 independent fits
+        # of 8 replays each (fit on 4, held-out error on 4) give the spread of the model error
         samples = []
         m_ = E // world
-        for (counts_t, mask_t), ph in zip(calib_samples, steps_ph):
+        src = graph_calib if exposure is not None else [
+            (c_, m2_, ph) for (c_, m2_), ph in zip(calib_samples, calibrate.per_step_phases(layer.phase_log))]
+        for counts_t, mask_t, ph in src:
             counts_np = counts_t.cpu().numpy()
             mask_np = mask_t.cpu().numpy() if mask_t is not None else np.eye(E, dtype=np.uint8)
             if layer.placement == "physical":
@@ -542,7 +685,14 @@ def main() -> None:
             else:
                 H, R = dv.derive_loads(counts_np, mask_np.astype("uint8"))  # pp_derive_loads kernel
             samples.append((H, R, calibrate.measured_costs(ph)))
-        calibration = calibrate.fit(samples, input_bytes=2 * d)
+        fits = [calibrate.fit(samples[8 * j:8 * j + 8], input_bytes=2 * d) for j in range(len(samples) // 8)] \
+            if len(samples) >= 16 else [calibrate.fit(samples, input_bytes=2 * d)]
+        calibration = dict(fits[0])
+        errs_ = [f_["mean_abs_rel_error"] for f_ in fits]
+        calibration["fits"] = [{"compute_throughput": f_["compute_throughput"], "avg_bandwidth": f_["avg_bandwidth"],
+                                "mean_abs_rel_error": f_["mean_abs_rel_error"]} for f_ in fits]
+        calibration["mean_abs_rel_error_spread"] = [min(errs_), max(errs_)]
+        calibration["phase_source"] = "graph replays" if exposure is not None else "eager steps"
         calibration["note"] = ("fit of the reference model's B and t to this run's measured phases ("
                                + ("per-device H/R" if layer.placement == "physical" else "virtual-slot H/R")
                                + ", rank 0); plan objective uses these units")
@@ -652,6 +802,8 @@ def main() -> None:
             if i + NB - 1 < args.steps:
                 h2d(i + NB - 1)  # two steps ahead: its buffer was freed by step i-1
             main.wait_event(ev_in[b])
+            if drift is not None:
+                next_bias()
             if use_graph:
                 _, _ = graphs[b]()
                 loss = graphs[b].loss
@@ -679,20 +831,28 @@ def main() -> None:
                        + "; pinned host batch x in (H2D, double-buffered on a copy stream), loss = sum(y*g) "
                          "with a device-resident probe g (dL/dy = g), fp32 loss scalar out (D2H)"}
 
-    # ---- planner + imbalance (device planner vs oracle CPU planner)
+    # ---- planner on this run's recorded LoadMatrices: the device search,
+    # one launch over all of them, vs the CPU oracle (reference greedy_search restated,
+    # pinned to its goldens) on the same matrices; in-loop plan parity at N > 1
     planner_info, imbalance = None, None
     if rank == 0 and not args.profile_only:
-        Ev = E
-        cpu = cpu_planner_ms(Ev, k, T * world, d, f)
-        cl = pp.ClusterSpec(Ev, cpu["cm"]["avg_bandwidth"], cpu["cm"]["compute_throughput"])
-        mo = pp.ModelSpec(Ev, 1, k, cpu["cm"]["input_bytes"], cpu["cm"]["expert_param_bytes"],
-                          cpu["cm"]["expert_grad_bytes"])
-        from paper_2411_10003_b200 import _device
         import numpy as np
 
-        counts_dev = torch.from_numpy(np.stack(cpu["mats"])).to(dev)
-        out = _device.PlanBuffers(len(cpu["mats"]), Ev, dev)
-        cmd, pcfg = _device.cost_model(cl, mo, Ev), _device.planner_cfg(pp.PlannerConfig(n=1, alpha=0.5))
+        from paper_2411_10003_b200 import _device
+        from paper_2411_10003_b200 import metrics as pm
+        from paper_2411_10003_b200.layer import default_specs
+
+        recs = np.stack([r.cpu().numpy() for r in recorded])  # [n][E][E] int64
+        if layer.plan_enabled:
+            cl_p, mo_p = layer.cluster, layer.model
+        else:  # N = 1 runs no planner in the step; price the search with the layer's default specs
+            cl_p, mo_p = default_specs(E, k, d, f, T * world)
+        L_rec = recs.shape[0]
+        counts_dev = torch.from_numpy(recs).to(dev)
+        out = _device.PlanBuffers(L_rec, E, dev)
+        pcfg_ = pp.PlannerConfig(n=args.n_excl if args.placement == "virtual" else 1, alpha=args.alpha,
+                                 overlap_aware=args.policy != "greedy")
+        cmd, pcfg = _device.cost_model(cl_p, mo_p, E), _device.planner_cfg(pcfg_)
         for _ in range(3):
             _device.launch_plan(counts_dev, out, cmd, pcfg)
         p0 = torch.cuda.Event(enable_timing=True)
@@ -702,19 +862,66 @@ def main() -> None:
             _device.launch_plan(counts_dev, out, cmd, pcfg)
         p1.record()
         torch.cuda.synchronize()
-        planner_info = {"device_us_per_launch": p0.elapsed_time(p1) / 20 * 1e3,
-                        "layers_per_launch": len(cpu["mats"]), "E_virtual": Ev,
-                        "cpu_oracle_ms_per_layer": cpu["ms_per_layer"]}
-        lm = layer.last_load_matrix()
-        H0, _ = np.asarray(lm.counts).sum(axis=0), None
-        imbalance = {"virtual_slot_H_sigma_vanilla": float(np.std(H0)),
+        dev_masks = out.mask.cpu().numpy().astype(bool)
+        us_launch = p0.elapsed_time(p1) / 20 * 1e3
+        planner_info = {"device_us_per_launch": us_launch, "layers_per_launch": L_rec,
+                        "device_us_per_layer_equiv": us_launch / L_rec, "E_virtual": E,
+                        "matrices": "this run's recorded LoadMatrices (one per instrumented iteration)",
+                        "config": {"n": pcfg_.n, "alpha": pcfg_.alpha, "overlap_aware": pcfg_.overlap_aware}}
+        H0 = recs[-1].sum(axis=0)
+        imbalance = {"virtual_slot_H_sigma_vanilla": pm.balance_degree(H0),
                      "max_over_mean_vanilla": float(H0.max() / max(H0.mean(), 1e-9))}
-        if world > 1:
-            mask = layer.current_mask()
-            from oracle import planner_ref as P
-            Hp, _ = P.derive_loads(lm.counts, mask)
-            imbalance.update({"virtual_slot_H_sigma_planned": float(np.std(Hp)),
-                              "rb": P.rb_ratio(H0, Hp)})
+        if world > 1 and calib_samples and calib_samples[-1][1] is not None:
+            mask_np = calib_samples[-1][1].cpu().numpy().astype("uint8")
+            Hp, _ = _device.derive_loads(calib_samples[-1][0].cpu().numpy(), mask_np)
+            imbalance.update({"virtual_slot_H_sigma_planned": pm.balance_degree(Hp),
+                              "rb": pm.balance_degree(H0) / max(pm.balance_degree(Hp), 1e-12)})
+        if not args.no_cpu_baseline:
+            planner_info.update(cpu_planner_leg(recs, dev_masks, cl_p, mo_p, pcfg_, E, k, calib_samples,
+                                                layer.placement, world))
+
+    # ---- N > 1: the same step under the physically-faithful planner with slot refinement
+    # (beyond the paper), beside the headline reference search
+    alt = None
+    if world > 1 and args.alt_placement and args.placement == "virtual" and use_graph and not args.profile_only:
+        del graphs
+        torch.cuda.synchronize()
+        dist.barrier()
+        layer.close()
+        lay2 = pp.MoELayer(d, f, E, k, tokens=T, group=group, planner=pp.PlannerConfig(
+            n=0, alpha=args.alpha, reuse_interval=1, overlap_aware=args.policy != "greedy"), seed=0,
+            policy=args.policy, **specs, planning="device", placement="physical", refine_slots=True)
+        if drift is not None:
+            lay2.set_gate_bias(bias_host[0])
+        else:
+            lay2.set_gate_bias(zipf_bias(E, 1.2, 0))
+        for _ in range(args.warmup):
+            xin = xs[0].detach().clone().requires_grad_(True)
+            lay2(xin).backward(dy)
+        g2 = [lay2.make_graphed_step(xs[b], dy.clone(), with_loss=True) for b in range(NB)]
+        for i in range(2):
+            g2[i % NB]()
+        torch.cuda.synchronize()
+        dist.barrier()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        lay2.barrier()
+        a0.record()
+        for i in range(args.steps):
+            g2[i % NB]()
+        a1.record()
+        torch.cuda.synchronize()
+        am = torch.tensor([a0.elapsed_time(a1)], dtype=torch.float64, device=dev)
+        dist.all_reduce(am, op=dist.ReduceOp.MAX)
+        rows2 = torch.tensor([float(lay2.total_real_rows())], dtype=torch.float64, device=dev)
+        allr = [torch.zeros_like(rows2) for _ in range(world)]
+        dist.all_gather(allr, rows2)
+        r2 = [int(r_.item()) for r_ in allr]
+        alt = {"placement": "physical+refine_slots (8(f) row 4 extension; plans not pinned by the reference)",
+               "value": world * T * args.steps / (float(am.item()) / 1e3), "unit": "tokens/s",
+               "ms_per_step": float(am.item()) / args.steps,
+               "rows_per_rank_max_over_mean": max(r2) / (sum(r2) / len(r2))}
+        del g2
+        lay2.close()
 
     clk.stop()
     clk_summary = clk.summary()
@@ -742,7 +949,8 @@ def main() -> None:
             "timed_region": "CUDA-graph replay of fwd+bwd" if use_graph else "eager stream-ordered fwd+bwd",
             "roofline": roofline, "cpu_baseline": cpu_info, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk_summary, "planner": planner_info, "imbalance": imbalance,
-            "cost_model_calibration": calibration,
+            "cost_model_calibration": calibration, "exposure": exposure, "alt_placement": alt,
+            "emulated_ranks_on_one_gpu": emulated or None,
             "rows_per_rank": {"rows": phys_rows, "max_over_mean": max(phys_rows) / (sum(phys_rows) / len(phys_rows))},
         }
         print(json.dumps(out), flush=True)

@@ -107,7 +107,10 @@ struct GemmParams {
   // instead of TMA stores / loads: the SM's TMA unit moves ~42 B/clk of loads + stores
   // together, and the operand loads alone need more than that at the MMA rate
   int lsu_epi;
-  int fast_gelu;  // FWD1 GeLU / DGRAD2 GeLU' in packed bf16x2 arithmetic (on the bf16 pre-activation)
+  int fast_gelu;   // FWD1: GeLU in packed bf16x2 arithmetic (on the bf16 pre-activation)
+  // DGRAD2: GeLU' in packed bf16x2 -- off by default: 1 - tanh^2 cancels in bf16 where the
+  // tanh saturates (dW1 error 1.1 % vs 0.3 % at 4x-scaled weights in the EP parity runs)
+  int fast_dgelu;
   // device-adaptive SM reservation: the persistent walk leaves
   // clamp(res_per_unit * (res_stats[0] + (res_both ? res_stats[1] : 0)), res_lo, res_hi) SMs
   // to concurrent side kernels (Trans / Agg), sized by this iteration's replica volume
@@ -374,7 +377,7 @@ __device__ __forceinline__ void epilogue_chunk(const uint32_t (&raw)[32], const 
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         float x[8], f[8];
-        if (EPI == EPI_DGELU && p.fast_gelu) {  // GeLU' in packed bf16x2, product in fp32
+        if (EPI == EPI_DGELU && p.fast_dgelu) {  // GeLU' in packed bf16x2, product in fp32
           const uint4 gp = make_uint4(dgelu_bf16x2(pre_v[j].x), dgelu_bf16x2(pre_v[j].y), dgelu_bf16x2(pre_v[j].z),
                                       dgelu_bf16x2(pre_v[j].w));
           bf16x8_to_f32(gp, x);
@@ -1271,8 +1274,9 @@ static int grouped_gemm_impl(int32_t mode, const void* a, const void* b, void* c
   p.c = c;
   p.c2 = c2;
   p.lsu_epi = lsu_epilogue();
-  // GeLU / GeLU' in packed bf16x2 arithmetic (FWD1 -4 %, DGRAD2 -8 % at cfg2; PPMOE_GEMM_FAST_GELU=0: fp32)
+  // GeLU in packed bf16x2 arithmetic (FWD1 -4 % at cfg2; PPMOE_GEMM_FAST_GELU=0: fp32)
   p.fast_gelu = env_int("PPMOE_GEMM_FAST_GELU", 1);
+  p.fast_dgelu = env_int("PPMOE_GEMM_FAST_DGELU", 0);
   if (sc) {
     p.origin = sc->origin;
     p.scatter_ptrs = sc->ptrs;

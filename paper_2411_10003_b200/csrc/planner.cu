@@ -479,10 +479,14 @@ __global__ void __launch_bounds__(kMaxPlanThreads) plan_physical_kernel(PhysArgs
     }
     __syncthreads();
   };
-  for (int iter = 0; iter < rows * E; ++iter) {
+  // loads once, then updated incrementally: un-routing batch (v, e) of c rows moves c from
+  // device hd (computed locally) to e's home (received + computed there)
+  {
     int64_t hh, rr;
     slot_loads(hh, rr);
-    const Red hm = block_reduce(t < D ? Red{hh, t} : neutral_max, MaxFirst(), scratch);
+  }
+  for (int iter = 0; iter < rows * E; ++iter) {
+    const Red hm = block_reduce(t < D ? Red{Hs[t], t} : neutral_max, MaxFirst(), scratch);
     const int hd = hm.i;
     Red cand{INT64_MAX, 0x7fffffff};
     for (int x = t; x < rpd * E; x += blockDim.x) {
@@ -497,7 +501,14 @@ __global__ void __launch_bounds__(kMaxPlanThreads) plan_physical_kernel(PhysArgs
     }
     cand = block_reduce(cand, MinOp(), scratch);
     if (cand.v == INT64_MAX) break;
-    if (t == 0) mask[cand.v & ((1 << 20) - 1)] = 0;
+    if (t == 0) {
+      const int cell = (int)(cand.v & ((1 << 20) - 1));
+      const int64_t c = counts[cell];
+      mask[cell] = 0;
+      Hs[hd] -= c;
+      Hs[(cell % E) / m] += c;
+    }
+    __syncthreads();
   }
   int64_t hh, rr;
   slot_loads(hh, rr);

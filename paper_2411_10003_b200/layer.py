@@ -441,6 +441,7 @@ class MoELayer(torch.nn.Module):
             # Trans completion flags (slot r written by rank r) + the pushers' CTA counter
             self.trans_flags = PeerBuffer((2, D), torch.int64, self.group, dev)  # rows: W1, W2
             self._trans_ctr = torch.zeros(1, dtype=torch.int32, device=dev)
+            self._trans_epoch = torch.zeros(1, dtype=torch.int64, device=dev)
             # layout output: [replicas of my home experts elsewhere, replicas I hold] -> the
             # GEMMs size their SM reservation for Trans / Agg from it, on device
             self.replica_stats = torch.zeros(2, dtype=torch.int32, device=dev)
@@ -469,6 +470,7 @@ class MoELayer(torch.nn.Module):
         self.phase_log = None
         self._agg_done = None
         self.timeline_log = None  # list -> (kind, lane, start_event, end_event) of side-stream ops
+        self._ext_events = False  # timing events recorded as graph nodes (capture of a timeline)
         # persistent-GEMM grid (0 = every SM); leaving a few SMs free lets the side-stream
         # Agg reduce / planner kernels run under the expert GEMMs instead of after them
         self.gemm_sms = 0
@@ -495,7 +497,7 @@ class MoELayer(torch.nn.Module):
         """Measured timeline: when ``phase_log`` is a list, record a CUDA event per
         phase boundary on the layer's stream (see ``phase_breakdown``)."""
         if self.phase_log is not None:
-            ev = torch.cuda.Event(enable_timing=True)
+            ev = torch.cuda.Event(enable_timing=True, external=self._ext_events)
             ev.record()
             self.phase_log.append((name, ev))
 
@@ -609,9 +611,11 @@ class MoELayer(torch.nn.Module):
         self._plan_pending = (done, mask_dev)
 
     def _epoch_ptr(self) -> int:
-        """Device address of the main peer barrier's epoch counter: equal on every rank after
-        the same barrier, so it names this iteration's Trans completion."""
-        return self.barrier.sig.local.data_ptr() + 8 * self.world
+        """Device address of this layer's Trans epoch: advanced by one on the main stream every
+        time the iteration's Trans is issued (every rank issues it once per iteration), so it
+        is equal on every rank and names this iteration's Trans completion -- also when the
+        Trans is issued ahead of the block's barriers (MoEStack: during the attention)."""
+        return self._trans_epoch.data_ptr()
 
     def _comb_local(self):
         return self.comb.local.data_ptr() if self.fused_a2a else None
@@ -696,6 +700,8 @@ class MoELayer(torch.nn.Module):
         self._trans_done = None
         if self.world == 1 or self.mask_cur is None:
             return None
+        if self.replica_engine == "sm":
+            self._trans_epoch.add_(1)  # stream-ordered before this rank's FWD1 / FWD2 gates
         ev = torch.cuda.Event()
         ev.record()
         with torch.cuda.stream(self.comm_stream):
@@ -729,7 +735,7 @@ class MoELayer(torch.nn.Module):
     def _side_event(self, stream):
         if self.timeline_log is None:
             return None
-        ev = torch.cuda.Event(enable_timing=True)
+        ev = torch.cuda.Event(enable_timing=True, external=self._ext_events)
         ev.record(stream)
         return ev
 
@@ -970,7 +976,7 @@ class MoELayer(torch.nn.Module):
         return _MoEFunction.apply(x, self)
 
     def make_graphed_step(self, x: torch.Tensor, dy: torch.Tensor, with_loss: bool = False,
-                          gemm_events: bool = False) -> "GraphedStep":
+                          gemm_events: bool = False, timeline_events: bool = False) -> "GraphedStep":
         """Capture one forward + backward into a CUDA graph (host cost per step
         drops to one graph launch).  ``x`` / ``dy`` become the static input
         buffers: copy new data into them, call the returned object, read
@@ -979,7 +985,7 @@ class MoELayer(torch.nn.Module):
         rank captures and replays in lockstep)."""
         if self.world != 1 and self.planning != "device":
             raise ValidationError("make_graphed_step at D > 1 needs planning='device'")
-        return GraphedStep(self, x, dy, with_loss, gemm_events)
+        return GraphedStep(self, x, dy, with_loss, gemm_events, timeline_events)
 
     # ---- introspection (LoadMatrix / placement of the last call) -------------
     def last_load_matrix(self) -> LoadMatrix:
@@ -1049,12 +1055,14 @@ class GraphedStep:
     """A captured fwd+bwd of one MoELayer over static input buffers."""
 
     def __init__(self, layer: MoELayer, x: torch.Tensor, dy: torch.Tensor, with_loss: bool = False,
-                 gemm_events: bool = False) -> None:
+                 gemm_events: bool = False, timeline_events: bool = False) -> None:
         """with_loss: also compute loss = sum(y * dy) in fp32 inside the graph (a
         linear probe whose gradient w.r.t. y is exactly dy), so a training loop can
         read back one scalar per step.  gemm_events: capture a timing-event pair
         around each grouped GEMM (event-record nodes); after a replay,
-        ``gemm_times()`` gives that replay's per-GEMM durations."""
+        ``gemm_times()`` gives that replay's per-GEMM durations.  timeline_events:
+        capture the phase marks and the side-stream Plan/Trans/Agg events as graph nodes;
+        after a replay, ``timeline()`` is that replay's reference-schema timeline."""
         self.layer, self.x, self.dy = layer, x, dy
         saved_timing, saved_phase, saved_pool = layer.gemm_timing, layer.phase_log, layer.gemm_event_pool
         layer.gemm_timing = layer.phase_log = None  # host-side timing lists cannot live in the graph
@@ -1067,6 +1075,11 @@ class GraphedStep:
         torch.cuda.current_stream().wait_stream(side)
         self.graph = torch.cuda.CUDAGraph()
         self.gemm_events = None
+        self.phase_log = self.timeline_log = None
+        saved_tl = layer.timeline_log
+        layer.timeline_log = None
+        if timeline_events:
+            layer.phase_log, layer.timeline_log, layer._ext_events = [], [], True
         if gemm_events:  # external events: recorded as graph nodes on every replay
             layer.gemm_timing = []
             layer.gemm_event_pool = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(32)]
@@ -1075,9 +1088,19 @@ class GraphedStep:
             self.loss = layer.probe_loss(self.y, dy) if with_loss else None
             self.dx = layer.backward_raw(x, dy)
         layer.iteration -= 1  # the capture ran no kernels: replays count the iterations
+        layer._trans_iter = -1  # an eager step after the capture issues its own Trans
+        if timeline_events:
+            self.phase_log, self.timeline_log = layer.phase_log, layer.timeline_log
+        layer._ext_events, layer.timeline_log = False, saved_tl
         if gemm_events:
             self.gemm_events = layer.gemm_timing
         layer.gemm_timing, layer.phase_log, layer.gemm_event_pool = saved_timing, saved_phase, saved_pool
+
+    def timeline(self, iteration: int = 0):
+        """Reference-schema IterationTimeline of the most recent replay (timeline_events)."""
+        from .stack import layer_timeline
+
+        return layer_timeline(self.phase_log, self.timeline_log, iteration)
 
     def gemm_times(self) -> list:
         """(mode, ms) of each grouped GEMM in the most recent replay (call after it finished)."""

@@ -65,8 +65,8 @@ class _Mark(torch.autograd.Function):
     @staticmethod
     def forward(ctx, x, log, fwd_name, bwd_name):
         ctx.log, ctx.bwd_name = log, bwd_name
-        if log is not None:
-            ev = torch.cuda.Event(enable_timing=True)
+        if log is not None:  # external: recorded as a graph node when captured
+            ev = torch.cuda.Event(enable_timing=True, external=torch.cuda.is_current_stream_capturing())
             ev.record()
             log.append((fwd_name, ev))
         return x.view_as(x)
@@ -74,10 +74,71 @@ class _Mark(torch.autograd.Function):
     @staticmethod
     def backward(ctx, g):
         if ctx.log is not None:
-            ev = torch.cuda.Event(enable_timing=True)
+            ev = torch.cuda.Event(enable_timing=True, external=torch.cuda.is_current_stream_capturing())
             ev.record()
             ctx.log.append((ctx.bwd_name, ev))
         return g, None, None, None
+
+
+# phase marks of MoELayer -> reference timeline ops: gate GEMMs + layout count as expert
+# compute (FEC/BEC); the permute / all-to-all kernels and their barriers are the A2A
+# (network lane); side-stream Plan / Trans / Agg come from the layer's timeline_log
+LAYER_PHASE_OPS = [
+    (OpKind.FEC, Lane.COMPUTE, "fwd_start", "route_layout"),
+    (OpKind.A2A, Lane.NETWORK, "route_layout", "barrier1"),
+    (OpKind.FEC, Lane.COMPUTE, "barrier1", "fwd_gemms"),
+    (OpKind.A2A, Lane.NETWORK, "fwd_gemms", "combine"),
+    (OpKind.A2A, Lane.NETWORK, "bwd_begin", "combine_bwd"),
+    (OpKind.BEC, Lane.COMPUTE, "combine_bwd", "gate_dw"),
+    (OpKind.A2A, Lane.NETWORK, "gate_dw", "barrier3"),
+    (OpKind.BEC, Lane.COMPUTE, "barrier3", "bwd_gemms"),
+    (OpKind.A2A, Lane.NETWORK, "bwd_gemms", "dispatch_bwd"),
+]
+SIDE_KINDS = {"Plan": OpKind.PLAN, "SubTrans1": OpKind.SUB_TRANS1, "SubTrans2": OpKind.SUB_TRANS2,
+              "SubAgg2": OpKind.SUB_AGG2, "SubAgg1": OpKind.SUB_AGG1}
+
+
+def add_layer_ops(add, block: int, phase_log, timeline_log) -> None:
+    """Feed one MoELayer step's recorded events to add(kind, block, lane, e0, e1)."""
+    seq = {n: e for n, e in (phase_log or [])}
+    for kind, lane, a, b in LAYER_PHASE_OPS:
+        if a in seq and b in seq:
+            add(kind, block, lane, seq[a], seq[b])
+    for kind, e0, e1 in timeline_log or []:
+        k = SIDE_KINDS[kind]
+        add(k, block, Lane.COMPUTE if k is OpKind.PLAN else Lane.NETWORK, e0, e1)
+
+
+def layer_timeline(phase_log, timeline_log, iteration: int = 0) -> IterationTimeline:
+    """Reference-schema timeline (seconds from the step's first mark) of one MoELayer step,
+    e.g. the events a CUDA-graph capture recorded (``make_graphed_step(timeline_events=True)``),
+    so the reference's exposure metric (``scheduler.py:134-169``) applies to a graphed EP step."""
+    t0 = phase_log[0][1]
+    ops = []
+
+    def add(kind, block, lane, e0, e1):
+        st = t0.elapsed_time(e0) / 1e3
+        dur = e0.elapsed_time(e1) / 1e3
+        if dur > 0:
+            ops.append(ScheduledOp(kind, block, iteration, lane, st, dur))
+
+    add_layer_ops(add, 0, phase_log, timeline_log)
+    ops.sort(key=lambda o: (o.start, o.lane.value))
+    return IterationTimeline(iteration, tuple(ops))
+
+
+def exposure_summary(tl: IterationTimeline, blocks: int = 1) -> dict:
+    """Exposed (not overlapped by the compute lane) replica communication of a timeline,
+    reference IterationTimeline.exposed_{trans,agg}_seconds (scheduler.py:134-169)."""
+    mk = tl.makespan()
+    et = sum(tl.exposed_trans_seconds(i) for i in range(blocks))
+    ea = sum(tl.exposed_agg_seconds(i) for i in range(blocks))
+    tt = sum(o.duration for o in tl.ops if o.kind.value.startswith("SubTrans"))
+    ta = sum(o.duration for o in tl.ops if o.kind.value.startswith("SubAgg"))
+    return {"makespan_ms": mk * 1e3, "replica_comm_ms": (tt + ta) * 1e3, "exposed_trans_ms": et * 1e3,
+            "exposed_agg_ms": ea * 1e3, "exposed_replica_comm_ms": (et + ea) * 1e3,
+            "exposed_replica_comm_frac": (et + ea) / mk if mk > 0 else 0.0,
+            "definition": "reference IterationTimeline.exposed_{trans,agg}_seconds / makespan on measured CUDA events"}
 
 
 class MoEStack(torch.nn.Module):
@@ -115,7 +176,7 @@ class MoEStack(torch.nn.Module):
     # ---- Algorithm 2 ---------------------------------------------------------
     def _schedule_trans(self, i: int, fec_time: float | None) -> None:
         m = self.moe[i]
-        if m.replica_engine != "copy":  # SM pushes are issued by the layer itself, gated into FWD1
+        if m.replica_engine != "copy":
             return
         m.begin_iteration()
         if self.fnec_time is not None and fec_time is not None and m.trans_bytes() > 0:
@@ -133,6 +194,12 @@ class MoEStack(torch.nn.Module):
         for i in range(self.L):
             if i + 1 < self.L:  # Trans(i+1) rides on block i
                 self._schedule_trans(i + 1, getattr(self, "_fec_est", None))
+            m = self.moe[i]
+            if m.replica_engine == "sm" and m.world > 1:
+                # SM engine (device-planned, graph-capturable): block i's pushes start with its
+                # attention (the FNEC window, SubTrans2 of Algorithm 2) and run on into FWD1's home
+                # tiles (SubTrans1); FWD1/FWD2's replica tiles wait on the completion flags
+                m.issue_trans()
             x = _Mark.apply(x, log, f"FNEC_start:{i}", f"BNEC_end:{i}")
             h = x + self.attn[i](x)
             h = _Mark.apply(h, log, f"FNEC_end:{i}", f"BNEC_start:{i}")
@@ -142,6 +209,12 @@ class MoEStack(torch.nn.Module):
     def wait_grads(self) -> None:
         for m in self.moe:
             m.wait_grads()
+
+    def make_graphed_step(self, x: torch.Tensor, dy: torch.Tensor, timeline_events: bool = False) -> "StackGraph":
+        """Capture one whole iteration (forward + autograd backward of every block, the
+        device planners, Trans/Agg side streams, barriers) into ONE CUDA graph.  Needs the
+        layers' planning='device' at D > 1.  x / dy become static input buffers."""
+        return StackGraph(self, x, dy, timeline_events)
 
     def close(self) -> None:
         torch.cuda.synchronize()
@@ -176,29 +249,7 @@ class MoEStack(torch.nn.Module):
             if f"BNEC_start:{i}" in marks:
                 add(OpKind.BNEC, i, Lane.COMPUTE, marks[f"BNEC_start:{i}"], marks[f"BNEC_end:{i}"])
             m = self.moe[i]
-            ph = m.phase_log or []
-            seq = {n: e for n, e in ph}
-            # gate GEMMs + layout count as expert compute (FEC/BEC); the permute /
-            # all-to-all kernels and their barriers are the A2A (network lane)
-            groups = [
-                (OpKind.FEC, Lane.COMPUTE, "fwd_start", "route_layout"),
-                (OpKind.A2A, Lane.NETWORK, "route_layout", "barrier1"),
-                (OpKind.FEC, Lane.COMPUTE, "barrier1", "fwd_gemms"),
-                (OpKind.A2A, Lane.NETWORK, "fwd_gemms", "combine"),
-                (OpKind.A2A, Lane.NETWORK, "bwd_begin", "combine_bwd"),
-                (OpKind.BEC, Lane.COMPUTE, "combine_bwd", "gate_dw"),
-                (OpKind.A2A, Lane.NETWORK, "gate_dw", "barrier3"),
-                (OpKind.BEC, Lane.COMPUTE, "barrier3", "bwd_gemms"),
-                (OpKind.A2A, Lane.NETWORK, "bwd_gemms", "dispatch_bwd"),
-            ]
-            for kind, lane, a, b in groups:
-                if a in seq and b in seq:
-                    add(kind, i, lane, seq[a], seq[b])
-            for kind, e0, e1 in m.timeline_log or []:
-                k = {"Plan": OpKind.PLAN, "SubTrans1": OpKind.SUB_TRANS1, "SubTrans2": OpKind.SUB_TRANS2,
-                     "SubAgg2": OpKind.SUB_AGG2, "SubAgg1": OpKind.SUB_AGG1}[kind]
-                lane = Lane.COMPUTE if k is OpKind.PLAN else Lane.NETWORK
-                add(k, i, lane, e0, e1)
+            add_layer_ops(add, i, m.phase_log, m.timeline_log)
         ops.sort(key=lambda o: (o.start, o.lane.value))
         return IterationTimeline(iteration, tuple(ops))
 
@@ -221,3 +272,62 @@ class MoEStack(torch.nn.Module):
             agg = tot(OpKind.SUB_AGG1) + tot(OpKind.SUB_AGG2)
             out.append(LayerCost(a2a, fec, bec, trans, agg, 0.0, 0.0, 0.0, 0.0))
         return out
+
+
+class StackGraph:
+    """One captured MoEStack iteration (``MoEStack.make_graphed_step``)."""
+
+    def __init__(self, stack: MoEStack, x: torch.Tensor, dy: torch.Tensor, timeline_events: bool = False) -> None:
+        for m in stack.moe:
+            if m.world > 1 and m.planning != "device":
+                raise ValueError("MoEStack.make_graphed_step at D > 1 needs the layers' planning='device'")
+        self.stack, self.x, self.dy = stack, x.detach().requires_grad_(True), dy
+
+        def once():
+            y = stack(self.x)
+            y.backward(self.dy)
+            return y
+
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):  # allocator / autograd / lazy-state warm-up outside capture
+            for _ in range(2):
+                once()
+        torch.cuda.current_stream().wait_stream(side)
+        self.graph = torch.cuda.CUDAGraph()
+        self.timeline_events = timeline_events
+        if timeline_events:
+            stack.log = []
+            for m in stack.moe:
+                m.phase_log, m.timeline_log, m._ext_events = [], [], True
+        with torch.cuda.graph(self.graph):
+            self.y = once()
+        if timeline_events:
+            self.log = stack.log
+            self.layer_logs = [(m.phase_log, m.timeline_log) for m in stack.moe]
+            stack.log = None
+            for m in stack.moe:
+                m.phase_log, m.timeline_log, m._ext_events = None, None, False
+        for m in stack.moe:
+            m.iteration -= 1  # the capture ran no kernels
+            m._trans_iter = -1  # an eager step after the capture issues its own Trans
+
+    def __call__(self) -> torch.Tensor:
+        self.graph.replay()
+        for m in self.stack.moe:
+            m.iteration += 1
+        return self.y
+
+    def timeline(self, iteration: int = 0) -> IterationTimeline:
+        """Reference-schema timeline of the most recent replay (timeline_events=True)."""
+        st = self.stack
+        saved = st.log, [(m.phase_log, m.timeline_log) for m in st.moe]
+        st.log = self.log
+        for m, (pl, tl) in zip(st.moe, self.layer_logs):
+            m.phase_log, m.timeline_log = pl, tl
+        try:
+            return st.measured_timeline(iteration)
+        finally:
+            st.log = saved[0]
+            for m, (pl, tl) in zip(st.moe, saved[1]):
+                m.phase_log, m.timeline_log = pl, tl
