@@ -42,6 +42,7 @@ CONFIGS = {
                  "8K tokens/GPU (4 x 2048-token sequences), attention in stock PyTorch, Algorithm-2 overlap"),
 }
 METRIC = "MoE-layer tokens/s fwd+bwd at 1/2/4/8 B200; planner ms/iter; load imbalance"
+CPU_SAMPLE_TOKENS = 2048  # tokens per CPU step, both in cpu_baseline and in the --impl reference arm
 
 
 def bind_cpu_to_gpu(device_index: int) -> None:
@@ -194,7 +195,7 @@ def cpu_baseline(cfg: dict, budget_s: float = 15.0) -> dict:
     threads = os.cpu_count() or 1
     torch.set_num_threads(threads)
     E, k, d, f = cfg["E"], cfg["k"], cfg["d"], cfg["f"]
-    Ts = min(cfg["T"], 2048)
+    Ts = min(cfg["T"], CPU_SAMPLE_TOKENS)
     g = torch.Generator().manual_seed(0)
     x = torch.randn((Ts, d), generator=g).to(torch.bfloat16)
     dy = (torch.randn((Ts, d), generator=g) * 0.1).to(torch.bfloat16)
@@ -253,7 +254,7 @@ def run_reference(args, cfg_name: str, cfg: dict) -> None:
 
     torch.set_num_threads(os.cpu_count() or 1)
     E, k, d, f = cfg["E"], cfg["k"], cfg["d"], cfg["f"]
-    Ts = min(cfg["T"], 1024)
+    Ts = min(cfg["T"], CPU_SAMPLE_TOKENS)  # the same token sample as our arm's cpu_baseline
     g = torch.Generator().manual_seed(0)
     x = torch.randn((Ts, d), generator=g).to(torch.bfloat16)
     dy = (torch.randn((Ts, d), generator=g) * 0.1).to(torch.bfloat16)

@@ -727,9 +727,9 @@ class MoELayer(torch.nn.Module):
                               self.mask_cur.data_ptr(), self.E, self.m, self.rank, self.slots, self.d, self.f, part,
                               self.trans_flags.ptrs.data_ptr(), row, self._epoch_ptr(),
                               self._trans_ctr.data_ptr(), self.trans_ctas, _device.stream_ptr(self.comm_stream))
+            self._log_side("SubTrans1", t0, self._side_event(self.comm_stream))  # before the join event
             self._trans_done = torch.cuda.Event()
             self._trans_done.record(self.comm_stream)
-            self._log_side("SubTrans1", t0, self._side_event(self.comm_stream))
         return self._trans_done
 
     def _side_event(self, stream):
@@ -794,9 +794,9 @@ class MoELayer(torch.nn.Module):
                 _lib.call("pp_replica_agg_reduce", self.g1_arena.local.data_ptr(), self.g2_arena.local.data_ptr(),
                           self.agg_stage.local.data_ptr(), self.mask_cur.data_ptr(), self.E, self.m, self.rank,
                           self.d, self.f, parts, nctas, cs)
+            self._log_side("SubAgg1" if parts == 2 else "SubAgg2", t0, self._side_event(self.comm_stream))
             self._agg_done = torch.cuda.Event()
             self._agg_done.record(self.comm_stream)
-            self._log_side("SubAgg1" if parts == 2 else "SubAgg2", t0, self._side_event(self.comm_stream))
 
     def _gemm(self, mode, a, b, c, c2=None, stream=None, num_sms=None, scatter=False, gate=False, res=None):
         timing = self.gemm_timing
