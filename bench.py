@@ -106,6 +106,36 @@ class PopularityDrift:
         return np.log(np.stack([self.step() for _ in range(n)]))
 
 
+class NvLinkCounter:
+    """NVLink data bytes this GPU sent / received (NVML field counters
+    NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX/RX, KiB, all links), read around a timed region."""
+
+    def __init__(self, torch_device) -> None:
+        self.ok = False
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            uuid = "GPU-" + str(__import__("torch").cuda.get_device_properties(torch_device).uuid)
+            self.h = pynvml.nvmlDeviceGetHandleByUUID(uuid.encode())
+            self.nv = pynvml
+            self.read()
+            self.ok = True
+        except Exception as exc:
+            self.error = repr(exc)[:160]
+
+    def read(self):
+        nv = self.nv
+        vals = nv.nvmlDeviceGetFieldValues(self.h, [nv.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX,
+                                                    nv.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX])
+        out = []
+        for v in vals:
+            if v.nvmlReturn != 0:
+                raise RuntimeError(f"nvml field {v.fieldId} rc {v.nvmlReturn}")
+            out.append(int(v.value.ullVal) * 1024)
+        return out
+
+
 class ClockSampler:
     """In-process NVML sampler (nvidia-ml-py): SM clock + throttle reasons every
     ~20 ms on a daemon thread.  NVML is initialised before the timed region so
@@ -551,6 +581,8 @@ def main() -> None:
     torch.cuda.synchronize()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
+    nvl = NvLinkCounter(dev) if world > 1 else None
+    nvl0 = nvl.read() if nvl is not None and nvl.ok else None
     w0 = time.perf_counter()
     layer.barrier()  # device-side peer barrier: the ranks' timed regions start together
     t0.record()
@@ -564,6 +596,18 @@ def main() -> None:
     if world > 1:
         dist.barrier()
     ms_total = t0.elapsed_time(t1)
+    nvlink = None
+    if nvl0 is not None:  # NVLink bytes of the timed region from the hardware counters
+        tx1, rx1 = nvl.read()
+        v_ = torch.tensor([tx1 - nvl0[0], rx1 - nvl0[1]], dtype=torch.float64, device=dev)
+        allv = [torch.zeros_like(v_) for _ in range(world)]
+        dist.all_gather(allv, v_)
+        sec = ms_total / 1e3
+        nvlink = {"tx_GBps_per_rank": [float(a[0]) / sec / 1e9 for a in allv],
+                  "rx_GBps_per_rank": [float(a[1]) / sec / 1e9 for a in allv],
+                  "tx_bytes_per_step_per_rank": [float(a[0]) / args.steps for a in allv],
+                  "peak_GBps_per_direction": 770.0, "peak_source": "B200_PROFILING.md measured peer copy",
+                  "source": "NVML NVLINK_THROUGHPUT_DATA_TX/RX counters around the timed region (all links)"}
     ms_tensor = torch.tensor([ms_total], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(ms_tensor, op=dist.ReduceOp.MAX)
@@ -950,7 +994,7 @@ def main() -> None:
             "timed_region": "CUDA-graph replay of fwd+bwd" if use_graph else "eager stream-ordered fwd+bwd",
             "roofline": roofline, "cpu_baseline": cpu_info, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk_summary, "planner": planner_info, "imbalance": imbalance,
-            "cost_model_calibration": calibration, "exposure": exposure, "alt_placement": alt,
+            "cost_model_calibration": calibration, "exposure": exposure, "alt_placement": alt, "nvlink": nvlink,
             "emulated_ranks_on_one_gpu": emulated or None,
             "rows_per_rank": {"rows": phys_rows, "max_over_mean": max(phys_rows) / (sum(phys_rows) / len(phys_rows))},
         }

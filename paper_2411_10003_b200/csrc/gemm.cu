@@ -1070,9 +1070,257 @@ static int sm_count() {
   return n;
 }
 
+// ---- K1: the gate as a split-K cluster kernel -------------------------------------
+// One 128-token tile per cluster of KS CTAs; CTA r accumulates logits over d-slice r on
+// tcgen05 (M = 128, N = BN) and CTAs 1..KS-1 store their fp32 partials into CTA 0's smem
+// over DSMEM; CTA 0 adds them in rank order (deterministic) and runs the softmax / top-k /
+// chunk-rank epilogue.  Splitting d gives every SM ~2 CTAs (loads of one overlap the
+// prologue / epilogue of the other) and keeps the whole token matrix in flight at once --
+// the tile-per-CTA GEMM path left 20 SMs idle and serialised load -> epilogue per SM.
+constexpr int kRouteThreads = 192;  // warp 0 TMA, warp 1 MMA + TMEM, warps 2..5 epilogue
+
+template <int BN, int KS, int STAGES>
+__global__ void __launch_bounds__(kRouteThreads)
+    route_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                 const GemmParams p) {
+  constexpr uint32_t A_BYTES = BM * BK * 2, B_BYTES = BN * BK * 2, STAGE_BYTES = A_BYTES + B_BYTES;
+  constexpr uint32_t TMEM_COLS = BN < 32 ? 32 : BN;
+  constexpr uint32_t IDESC = make_idesc<BN, false, false, BM>();
+  extern __shared__ __align__(1024) uint8_t dsmem[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsmem) + 1023) & ~uintptr_t(1023));
+  float* part = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES);  // [KS-1][128][BN] (CTA 0)
+  __shared__ __align__(8) uint64_t full_bar[STAGES], empty_bar[STAGES], tfull_bar;
+  __shared__ uint32_t tmem_base_sh;
+  __shared__ int32_t route_cnt[4][BN];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int crank = (int)cluster_ctarank();
+  const int tile = blockIdx.x / KS;
+  const int row0 = tile * BM;
+  const int kb_per = p.K_fixed / BK / KS, kb0 = crank * kb_per;
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&full_bar[i], 1);
+      mbar_init(&empty_bar[i], 1);
+    }
+    mbar_init(&tfull_bar, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc<TMEM_COLS>(&tmem_base_sh);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = tmem_base_sh;
+  if (warp == 0) {
+    if (lane == 0) {  // ===== TMA producer
+      for (int kb = 0, stage = 0, phase = 0; kb < kb_per; ++kb) {
+        mbar_wait(&empty_bar[stage], phase ^ 1);
+        uint8_t* sa = smem + stage * STAGE_BYTES;
+        mbar_arrive_expect_tx(&full_bar[stage], STAGE_BYTES);
+        tma_load_2d(sa, &tmA, &full_bar[stage], (kb0 + kb) * BK, row0);
+        tma_load_2d(sa + A_BYTES, &tmB, &full_bar[stage], (kb0 + kb) * BK, 0);
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp == 1) {  // ===== MMA issuer
+    for (int kb = 0, stage = 0, phase = 0; kb < kb_per; ++kb) {
+      mbar_wait(&full_bar[stage], phase);
+      tc_fence_after();
+      if (lane == 0) {
+        const uint32_t sa = smem_u32(smem + stage * STAGE_BYTES), sb = sa + A_BYTES;
+#pragma unroll
+        for (int kk = 0; kk < BK / 16; ++kk)
+          tc_mma_bf16(tmem_base, make_sdesc(sa + kk * 32, 16, 1024), make_sdesc(sb + kk * 32, 16, 1024), IDESC,
+                      (kb | kk) != 0);
+        tc_commit(&empty_bar[stage]);
+        if (kb == kb_per - 1) tc_commit(&tfull_bar);
+      }
+      __syncwarp();
+      if (++stage == STAGES) { stage = 0; phase ^= 1; }
+    }
+  }
+  // ===== epilogue warps 2..5 (TMEM lane quarter q = warp % 4); everyone joins the cluster barrier
+  const int q = warp & 3;
+  const int r = q * 32 + lane;
+  float v[BN];
+  if (warp >= 2) {
+    mbar_wait(&tfull_bar, 0);
+    tc_fence_after();
+    const uint32_t t_row = tmem_base + ((uint32_t)(q * 32) << 16);
+#pragma unroll
+    for (int c = 0; c < BN; c += 16) {
+      uint32_t raw[16];
+      tmem_ld_32x32b_x16(t_row + c, raw);
+      tmem_ld_wait();
+#pragma unroll
+      for (int j = 0; j < 16; ++j) v[c + j] = __uint_as_float(raw[j]);
+    }
+    if (crank > 0) {  // partial logits of this d-slice -> CTA 0's smem (DSMEM)
+      const uint32_t dst = mapa_shared(smem_u32(part + ((size_t)(crank - 1) * BM + r) * BN), 0);
+#pragma unroll
+      for (int c = 0; c < BN; c += 4)
+        asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(dst + 4 * c), "f"(v[c]),
+                     "f"(v[c + 1]), "f"(v[c + 2]), "f"(v[c + 3])
+                     : "memory");
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();  // release / acquire: the partials are visible in CTA 0
+  if (warp >= 2 && crank == 0) {
+#pragma unroll 1
+    for (int s = 0; s < KS - 1; ++s) {  // rank order: deterministic sum
+      const float* pr = part + ((size_t)s * BM + r) * BN;
+#pragma unroll
+      for (int c = 0; c < BN; c += 4) {
+        const float4 x4 = *reinterpret_cast<const float4*>(pr + c);
+        v[c] += x4.x; v[c + 1] += x4.y; v[c + 2] += x4.z; v[c + 3] += x4.w;
+      }
+    }
+    const int E = p.e_real;
+    const int token = row0 + r;
+    const int chunk = row0 / BM;
+#pragma unroll
+    for (int e = 0; e < BN; ++e) v[e] = e < E ? v[e] + (p.bias ? p.bias[e] : 0.f) : -INFINITY;
+    float mx = v[0];
+#pragma unroll
+    for (int e = 1; e < BN; ++e) mx = fmaxf(mx, v[e]);
+    float ssum = 0.f, ex[BN];
+#pragma unroll
+    for (int e = 0; e < BN; ++e) {
+      ex[e] = e < E ? expf(v[e] - mx) : 0.f;
+      ssum += ex[e];
+    }
+    const float inv = 1.f / ssum;
+    float* prow = p.probs + (size_t)token * E;
+#pragma unroll
+    for (int e = 0; e < BN; e += 4)
+      if (e < E)
+        *reinterpret_cast<float4*>(prow + e) = make_float4(ex[e] * inv, ex[e + 1] * inv, ex[e + 2] * inv, ex[e + 3] * inv);
+    // top-k on logits, ties -> lowest expert index
+    uint64_t taken_lo = 0, taken_hi = 0;
+    int sel[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      sel[j] = -1;
+      if (j < p.topk) {
+        int bi = -1;
+        float best = 0.f;
+#pragma unroll
+        for (int e = 0; e < BN; ++e) {
+          const bool tk = e < 64 ? ((taken_lo >> e) & 1) : ((taken_hi >> (e - 64)) & 1);
+          if (e < E && !tk && (bi < 0 || v[e] > best)) {
+            best = v[e];
+            bi = e;
+          }
+        }
+        sel[j] = bi;
+        if (bi < 64) taken_lo |= 1ull << bi;
+        else taken_hi |= 1ull << (bi - 64);
+      }
+    }
+    // chunk ranks: pairs of expert e ordered by token inside this 128-token tile
+    int myrank[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) myrank[j] = 0;
+    const uint32_t lt_mask = (1u << lane) - 1u;
+    for (int e = 0; e < E; ++e) {
+      bool has = false;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) has |= (sel[j] == e);
+      const uint32_t b = __ballot_sync(0xffffffffu, has);
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (sel[j] == e) myrank[j] = __popc(b & lt_mask);
+      if (lane == 0) route_cnt[q][e] = __popc(b);
+    }
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (j < p.topk) {
+        const int e = sel[j];
+        int base = 0;
+        for (int qq = 0; qq < q; ++qq) base += route_cnt[qq][e];
+        p.idx[(size_t)token * p.topk + j] = e;
+        p.w[(size_t)token * p.topk + j] = ex[e] * inv;
+        p.rank[(size_t)token * p.topk + j] = base + myrank[j];
+      }
+    }
+    for (int e = r; e < E; e += 128)
+      p.chunk_counts[(size_t)chunk * E + e] = route_cnt[0][e] + route_cnt[1][e] + route_cnt[2][e] + route_cnt[3][e];
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_free<TMEM_COLS>(tmem_base);
+}
+
+template <int BN, int KS, int STAGES>
+static int launch_route(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, int tiles,
+                        cudaStream_t st) {
+  auto kern = route_kernel<BN, KS, STAGES>;
+  const int smem = STAGES * (BM * BK * 2 + BN * BK * 2) + (KS - 1) * BM * BN * 4 + 1024;
+  static int configured[64] = {0};
+  int dev = 0;
+  PP_CUDA_TRY(cudaGetDevice(&dev));
+  if (dev < 64 && !configured[dev]) {
+    PP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    configured[dev] = 1;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(tiles * KS);
+  cfg.blockDim = dim3(kRouteThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = KS;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  PP_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, ta, tb, p));
+  PP_LAUNCH_CHECK();
+  return PP_OK;
+}
+
 int route_gemm(const void* x, const void* wg, const float* bias, int T, int d, int E, int k,
                int32_t* idx, float* w, float* probs, int32_t* rank, int32_t* chunk_counts,
                cudaStream_t st) {
+  if (env_int("PPMOE_ROUTE_SPLITK", 1)) {
+    // d-split so that ~2 CTAs per SM exist (KS = 4 below 148 tiles, else 2), every slice >= one BK
+    const int tiles = T / BM;
+    int KS = env_int("PPMOE_ROUTE_KS", tiles < 148 ? 4 : 2);
+    const int BNr = E <= 16 ? 16 : E <= 32 ? 32 : E <= 64 ? 64 : 128;
+    if (BNr == 128 && KS > 2) KS = 2;  // smem: 4 stages + (KS-1) fp32 128 x 128 partials
+    if (KS != 1 && KS != 2 && KS != 4) KS = 2;
+    while (KS > 1 && (d / BK) % KS) KS >>= 1;
+    CUtensorMap ta, tb;
+    if (int rc = make_tmap(&ta, x, d, T, BK, BM)) return rc;
+    if (int rc = make_tmap(&tb, wg, d, E, BK, BNr)) return rc;
+    GemmParams p{};
+    p.e_real = E;
+    p.K_fixed = d;
+    p.bias = bias;
+    p.idx = idx;
+    p.w = w;
+    p.probs = probs;
+    p.rank = rank;
+    p.chunk_counts = chunk_counts;
+    p.topk = k;
+#define PP_ROUTE_KS(BN_)                                                 \
+  switch (KS) {                                                         \
+    case 4: return launch_route<BN_, 4, 4>(ta, tb, p, tiles, st);       \
+    case 2: return launch_route<BN_, 2, 4>(ta, tb, p, tiles, st);       \
+    default: return launch_route<BN_, 1, 6>(ta, tb, p, tiles, st);      \
+  }
+    switch (BNr) {
+      case 16: PP_ROUTE_KS(16)
+      case 32: PP_ROUTE_KS(32)
+      case 64: PP_ROUTE_KS(64)
+      default: PP_ROUTE_KS(128)
+    }
+#undef PP_ROUTE_KS
+  }
   const int BNr = E <= 16 ? 16 : E <= 32 ? 32 : E <= 64 ? 64 : 128;
   CUtensorMap ta, tb;
   if (int rc = make_tmap(&ta, x, d, T, BK, BM)) return rc;

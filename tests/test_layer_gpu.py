@@ -50,6 +50,15 @@ def test_route_exact(T, d, E, k):
     torch.testing.assert_close(probs.cpu(), rprobs, rtol=1e-5, atol=1e-7)
 
 
+@pytest.mark.parametrize("ks", ["1", "2", "4"])
+def test_route_split_k_variants(ks, monkeypatch):
+    """K1's d-split over a cluster of KS CTAs (DSMEM partials summed in rank order) gives the
+    same exact routing, ranks and chunk counts for every KS."""
+    monkeypatch.setenv("PPMOE_ROUTE_KS", ks)
+    test_route_exact(2048, 1024, 16, 2)
+    test_route_exact(1024, 512, 64, 1)
+
+
 def run_layer(T, d, f, E, k, bias=None, seed=0, **kw):
     layer = pp.MoELayer(d, f, E, k, tokens=T, seed=seed, **kw)
     x, wg = M.exact_inputs(T, d, E, seed=seed + 11)
