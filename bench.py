@@ -125,14 +125,18 @@ class NvLinkCounter:
             self.error = repr(exc)[:160]
 
     def read(self):
+        """(tx, rx) bytes summed over the links that report (field scope = link id)."""
         nv = self.nv
-        vals = nv.nvmlDeviceGetFieldValues(self.h, [nv.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX,
-                                                    nv.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX])
-        out = []
-        for v in vals:
-            if v.nvmlReturn != 0:
-                raise RuntimeError(f"nvml field {v.fieldId} rc {v.nvmlReturn}")
-            out.append(int(v.value.ullVal) * 1024)
+        ids = [(f, l) for f in (nv.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX, nv.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX)
+               for l in range(18)]
+        vals = nv.nvmlDeviceGetFieldValues(self.h, ids)
+        out, good = [0, 0], 0
+        for (f, _), v in zip(ids, vals):
+            if v.nvmlReturn == 0:
+                out[0 if f == nv.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX else 1] += int(v.value.ullVal) * 1024
+                good += 1
+        if not good:
+            raise RuntimeError(f"no NVLink throughput field readable (rc {vals[0].nvmlReturn})")
         return out
 
 
@@ -583,6 +587,7 @@ def main() -> None:
     t1 = torch.cuda.Event(enable_timing=True)
     nvl = NvLinkCounter(dev) if world > 1 else None
     nvl0 = nvl.read() if nvl is not None and nvl.ok else None
+    nvl_err = getattr(nvl, "error", None) if nvl is not None else None
     w0 = time.perf_counter()
     layer.barrier()  # device-side peer barrier: the ranks' timed regions start together
     t0.record()
@@ -596,7 +601,7 @@ def main() -> None:
     if world > 1:
         dist.barrier()
     ms_total = t0.elapsed_time(t1)
-    nvlink = None
+    nvlink = {"error": nvl_err} if nvl_err else None
     if nvl0 is not None:  # NVLink bytes of the timed region from the hardware counters
         tx1, rx1 = nvl.read()
         v_ = torch.tensor([tx1 - nvl0[0], rx1 - nvl0[1]], dtype=torch.float64, device=dev)

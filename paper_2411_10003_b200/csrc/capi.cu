@@ -1,5 +1,6 @@
 // C-ABI error plumbing shared by every entry point of libppmoe.
 #include <stdarg.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 
@@ -17,6 +18,14 @@ int fail(int code, const char* fmt, ...) {
   va_end(ap);
   t_last_error = buf;
   return code;
+}
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* v = getenv("PPMOE_PDL");
+    return v == nullptr || atoi(v) != 0;
+  }();
+  return on;
 }
 
 }  // namespace pp

@@ -7,6 +7,7 @@
 #include <stdint.h>
 #include <stdio.h>
 #include <string>
+#include <utility>
 
 #include "../../include/ppmoe.h"
 
@@ -32,6 +33,35 @@ int fail(int code, const char* fmt, ...);
 #define PP_LAUNCH_CHECK() PP_CUDA_TRY(cudaGetLastError())
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// ---- programmatic dependent launch (PDL) -------------------------------------
+// Every kernel of the library starts with pdl_grid_sync(): it waits until the kernels it
+// depends on in stream order have completed and their memory is visible, and then lets its
+// own dependents launch.  Launched with programmatic stream serialization (pdl_launch), a
+// kernel's launch processing and CTA rasterisation overlap the tail of its predecessor
+// instead of following its completion; without the attribute both instructions are no-ops.
+// PPMOE_PDL=0 turns the attribute off.
+__device__ __forceinline__ void pdl_grid_sync() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t pdl_launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 // ---- small device helpers --------------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {

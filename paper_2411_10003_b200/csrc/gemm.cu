@@ -447,6 +447,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const __grid_constant__ CUtensorMap tmB,
                         const __grid_constant__ CUtensorMap tmC,
                         const __grid_constant__ CUtensorMap tmC2, const GemmParams p) {
+  pdl_grid_sync();
   // CG = 2: CTA pair (cta_group::2).  Each CTA stages its 128 rows of A and its
   // half (BN/2 rows) of B; the leader issues 256 x BN MMAs over both CTAs' smem.
   static_assert(CG == 1 || CG == 2, "CG");
@@ -1029,20 +1030,22 @@ static int launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams
     configured[dev] = 1;
   }
   if constexpr (CG == 1) {
-    kern<<<grid, kThreads, smem, st>>>(ta, tb, tc ? *tc : dummy, tc2 ? *tc2 : dummy, p);
+    PP_CUDA_TRY(pdl_launch(kern, dim3(grid), dim3(kThreads), smem, st, ta, tb, tc ? *tc : dummy, tc2 ? *tc2 : dummy, p));
   } else {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((grid / 2) * 2);
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = 2;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL (common.cuh)
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
     PP_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, ta, tb, tc ? *tc : dummy, tc2 ? *tc2 : dummy, p));
   }
   PP_LAUNCH_CHECK();
@@ -1083,6 +1086,7 @@ template <int BN, int KS, int STAGES>
 __global__ void __launch_bounds__(kRouteThreads)
     route_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  const GemmParams p) {
+  pdl_grid_sync();
   constexpr uint32_t A_BYTES = BM * BK * 2, B_BYTES = BN * BK * 2, STAGE_BYTES = A_BYTES + B_BYTES;
   constexpr uint32_t TMEM_COLS = BN < 32 ? 32 : BN;
   constexpr uint32_t IDESC = make_idesc<BN, false, false, BM>();
@@ -1271,13 +1275,15 @@ static int launch_route(const CUtensorMap& ta, const CUtensorMap& tb, const Gemm
   cfg.blockDim = dim3(kRouteThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = KS;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL (common.cuh)
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
   PP_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, ta, tb, p));
   PP_LAUNCH_CHECK();
   return PP_OK;
@@ -1368,6 +1374,7 @@ int gate_dx_gemm(const void* dl, const void* wg, int T, int d, int E, int EP, vo
 // (c, e), every split's value loaded before the adds
 __global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, int d, int EP, int E,
                                      float* __restrict__ out) {
+  pdl_grid_sync();
   const int n = d * E;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const int c = i / E, e = i - (i / E) * E;
@@ -1407,7 +1414,7 @@ int gate_dw_gemm(const void* dl, const void* x, int T, int d, int E, int EP, int
                     : launch<128, true, true, EPI_F32, 5>(ta, tb, q, sm_count(), st, &tc);
   if (rc) return rc;
   const int n = E * d;
-  splitk_reduce_kernel<<<(n + 255) / 256, 256, 0, st>>>(ws, S, d, EP, E, dwg);
+  PP_CUDA_TRY(pdl_launch(splitk_reduce_kernel, dim3((n + 255) / 256), dim3(256), 0, st, ws, S, d, EP, E, dwg));
   PP_LAUNCH_CHECK();
   return PP_OK;
 }

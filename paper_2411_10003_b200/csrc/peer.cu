@@ -29,6 +29,7 @@ __device__ __forceinline__ uint64_t global_ns() {
 // r's own barrier counter.  epoch == 0: take the epoch from that device counter (so a
 // captured CUDA graph can replay barriers), otherwise use the host-provided value.
 __global__ void peer_barrier_kernel(void* const* signal_ptrs, int D, int me, uint64_t epoch) {
+  pdl_grid_sync();
   __shared__ uint64_t ep;
   uint64_t* own = reinterpret_cast<uint64_t*>(signal_ptrs[me]);
   if (threadIdx.x == 0) ep = epoch ? epoch : own[D] + 1;
@@ -128,6 +129,7 @@ __global__ void __launch_bounds__(512) replica_trans_kernel(void* const* w1_ptrs
                                                             int num_slots, size_t vecs, int parts, void* const* flag_ptrs,
                                                             int flag_row, const uint64_t* epoch,
                                                             unsigned int* done_ctr) {
+  pdl_grid_sync();
   __shared__ uint8_t flag[kMaxFlags];
   __shared__ int cand[kMaxItems], items[kMaxItems];
   const int D = E / m;
@@ -174,6 +176,7 @@ __global__ void __launch_bounds__(512) replica_agg_push_kernel(void* const* g1_p
                                                                void* const* stage_ptrs, const uint8_t* mask,
                                                                int E, int m, int me, int num_slots, size_t vecs,
                                                                int parts) {
+  pdl_grid_sync();
   __shared__ uint8_t flag[kMaxFlags];
   __shared__ int cand[kMaxItems], items[kMaxItems];
   const int D = E / m;
@@ -199,6 +202,7 @@ __global__ void __launch_bounds__(512) replica_agg_push_kernel(void* const* g1_p
 __global__ void __launch_bounds__(512, 1) replica_agg_reduce_kernel(float* g1, float* g2, const float* stage,
                                                                     const uint8_t* mask, int E, int m, int me,
                                                                     size_t vecs, int parts) {
+  pdl_grid_sync();
   __shared__ uint8_t flag[kMaxFlags];
   __shared__ int cand[kMaxItems], items[kMaxItems];
   __shared__ uint32_t srcmask[kMaxItems];
@@ -294,8 +298,8 @@ extern "C" int pp_peer_barrier(void* const* signal_ptrs, int32_t D, int32_t my_r
                                void* stream) {
   PP_CHECK_ARG(signal_ptrs && D >= 1 && D <= 1024 && my_rank >= 0 && my_rank < D,
                "pp_peer_barrier: bad arguments");
-  peer_barrier_kernel<<<1, ((D + 31) / 32) * 32, 0, as_stream(stream)>>>(signal_ptrs, D, my_rank,
-                                                                         epoch);
+  PP_CUDA_TRY(pdl_launch(peer_barrier_kernel, dim3(1), dim3(((D + 31) / 32) * 32), 0, as_stream(stream), signal_ptrs, D, my_rank,
+                                                                         epoch));
   PP_LAUNCH_CHECK();
   return PP_OK;
 }
@@ -314,9 +318,9 @@ extern "C" int pp_replica_trans(void* const* w1_ptrs, void* const* w2_ptrs, cons
   PP_CHECK_ARG(((size_t)d_model * d_ff) % 8 == 0, "pp_replica_trans: bad sizes");
   const int grid = max_ctas > 0 ? max_ctas : 16;
   PP_CHECK_ARG(num_slots > m, "pp_replica_trans: num_slots=%d leaves no replica slot (m=%d)", num_slots, m);
-  replica_trans_kernel<<<grid, 512, 0, as_stream(stream)>>>(w1_ptrs, w2_ptrs, mask, E, m, my_rank, num_slots,
+  PP_CUDA_TRY(pdl_launch(replica_trans_kernel, dim3(grid), dim3(512), 0, as_stream(stream), w1_ptrs, w2_ptrs, mask, E, m, my_rank, num_slots,
                                                             (size_t)d_model * d_ff / 8, parts, flag_ptrs,
-                                                            flag_row, epoch, done_ctr);
+                                                            flag_row, epoch, done_ctr));
   PP_LAUNCH_CHECK();
   return PP_OK;
 }
@@ -333,8 +337,8 @@ extern "C" int pp_replica_agg(void* const* g1_ptrs, void* const* g2_ptrs, void* 
   PP_CHECK_ARG(((size_t)d_model * d_ff) % 4 == 0, "pp_replica_agg: bad sizes");
   const int grid = max_ctas > 0 ? max_ctas : 16;
   PP_CHECK_ARG(num_slots > m, "pp_replica_agg: num_slots=%d leaves no replica slot (m=%d)", num_slots, m);
-  replica_agg_push_kernel<<<grid, 512, 0, as_stream(stream)>>>(g1_ptrs, g2_ptrs, stage_ptrs, mask, E, m,
-                                                               my_rank, num_slots, (size_t)d_model * d_ff / 4, parts);
+  PP_CUDA_TRY(pdl_launch(replica_agg_push_kernel, dim3(grid), dim3(512), 0, as_stream(stream), g1_ptrs, g2_ptrs, stage_ptrs, mask, E, m,
+                                                               my_rank, num_slots, (size_t)d_model * d_ff / 4, parts));
   PP_LAUNCH_CHECK();
   return PP_OK;
 }
@@ -349,8 +353,8 @@ extern "C" int pp_replica_agg_reduce(float* g1, float* g2, const float* stage, c
                "pp_replica_agg_reduce: bad E / m / rank (D <= 33)");
   PP_CHECK_ARG(((size_t)d_model * d_ff) % 4 == 0, "pp_replica_agg_reduce: bad sizes");
   const int grid = max_ctas > 0 ? max_ctas : 16;
-  replica_agg_reduce_kernel<<<grid, 512, 0, as_stream(stream)>>>(g1, g2, stage, mask, E, m, my_rank,
-                                                                  (size_t)d_model * d_ff / 4, parts);
+  PP_CUDA_TRY(pdl_launch(replica_agg_reduce_kernel, dim3(grid), dim3(512), 0, as_stream(stream), g1, g2, stage, mask, E, m, my_rank,
+                                                                  (size_t)d_model * d_ff / 4, parts));
   PP_LAUNCH_CHECK();
   return PP_OK;
 }
@@ -361,6 +365,7 @@ namespace pp {
 // staging entry i = [g1 part (f*d) | g2 part (d*f)] fp32
 __global__ void agg_accumulate_kernel(float* g1, float* g2, const float* staging,
                                       const int32_t* ranges, int m, size_t fd) {
+  pdl_grid_sync();
   const size_t vec = fd / 4;
   const size_t total = (size_t)m * 2 * vec;
   for (size_t x = (size_t)blockIdx.x * blockDim.x + threadIdx.x; x < total;
@@ -397,8 +402,8 @@ extern "C" int pp_agg_accumulate(float* g1_home, float* g2_home, const float* st
                                  const int32_t* ranges, int32_t m, int32_t d_model, int32_t d_ff,
                                  void* stream) {
   PP_CHECK_ARG(g1_home && g2_home && staging && ranges && m >= 1, "pp_agg_accumulate: bad arguments");
-  agg_accumulate_kernel<<<4 * 148, 256, 0, as_stream(stream)>>>(g1_home, g2_home, staging, ranges, m,
-                                                                (size_t)d_model * d_ff);
+  PP_CUDA_TRY(pdl_launch(agg_accumulate_kernel, dim3(4 * 148), dim3(256), 0, as_stream(stream), g1_home, g2_home, staging, ranges, m,
+                                                                (size_t)d_model * d_ff));
   PP_LAUNCH_CHECK();
   return PP_OK;
 }

@@ -27,6 +27,7 @@ int route_gemm(const void* x, const void* wg, const float* bias, int T, int d, i
 // (peer-mapped) -- the all-gather of the histogram without a collective library
 __global__ void slot_histogram_kernel(const int32_t* chunk_counts, int chunks_per_slot, int E,
                                       int m, int64_t* const* out_ptrs, int D, int row0) {
+  pdl_grid_sync();
   const int cell = blockIdx.x * blockDim.x + threadIdx.x;
   if (cell >= m * E) return;
   const int v = cell / E, e = cell % E;
@@ -62,6 +63,7 @@ __global__ void __launch_bounds__(kLayoutThreads)
                            int32_t* num_groups, int32_t* total_rows, int32_t* seg_start,
                            int32_t* rep_slot, int counts_from_chunks, int32_t* replica_stats,
                            int32_t* status) {
+  pdl_grid_sync();
   __shared__ int overflow;
   extern __shared__ __align__(16) uint8_t lsm[];
   const int Ev = D * m, C = T / PP_CHUNK, tid = threadIdx.x, nt = blockDim.x;
@@ -217,6 +219,7 @@ __global__ void __launch_bounds__(256)
                     void* const* recv_ptrs, int32_t* pair_dest, int32_t* pair_row,
                     const pp_group* groups, const int32_t* num_groups, __nv_bfloat16* own,
                     void* const* origin_ptrs, int me) {
+  pdl_grid_sync();
   const int lane = threadIdx.x & 31;
   const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -259,6 +262,7 @@ __global__ void __launch_bounds__(256)
     combine_kernel(void* const* out_ptrs, const int32_t* __restrict__ pair_dest,
                    const int32_t* __restrict__ pair_row, const float* __restrict__ w, int T, int d,
                    int k, __nv_bfloat16* y, const __nv_bfloat16* __restrict__ comb) {
+  pdl_grid_sync();
   const int lane = threadIdx.x & 31;
   const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -321,6 +325,7 @@ __global__ void __launch_bounds__(256)
                        __nv_bfloat16* own, const __nv_bfloat16* __restrict__ comb,
                        const int32_t* __restrict__ idx, const float* __restrict__ probs, int E,
                        __nv_bfloat16* dl) {
+  pdl_grid_sync();
   const int lane = threadIdx.x & 31;
   const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -450,8 +455,8 @@ extern "C" int pp_slot_histogram(const int32_t* chunk_counts, int32_t T, int32_t
                PP_CHUNK);
   const int cps = (T / m) / PP_CHUNK;
   const int cells = m * E;
-  slot_histogram_kernel<<<(cells + 255) / 256, 256, 0, as_stream(stream)>>>(chunk_counts, cps, E, m,
-                                                                            out_ptrs, D, row0);
+  PP_CUDA_TRY(pdl_launch(slot_histogram_kernel, dim3((cells + 255) / 256), dim3(256), 0, as_stream(stream), chunk_counts, cps, E, m,
+                                                                            out_ptrs, D, row0));
   PP_LAUNCH_CHECK();
   return PP_OK;
 }
@@ -485,9 +490,9 @@ extern "C" int pp_dispatch_layout(int64_t* counts, const uint8_t* mask,
                                      220 * 1024));
     if (dev < 64) configured[dev] = 220 * 1024;
   }
-  dispatch_layout_kernel<<<1, kLayoutThreads, smem, as_stream(stream)>>>(
+  PP_CUDA_TRY(pdl_launch(dispatch_layout_kernel, dim3(1), dim3(kLayoutThreads), smem, as_stream(stream), 
       counts, mask, chunk_counts, D, m, E, T, my_rank, max_groups, rows_capacity, num_slots, chunk_base,
-      slot_dest, groups, num_groups, total_rows, seg_start, rep_slot, counts_from_chunks, replica_stats, status);
+      slot_dest, groups, num_groups, total_rows, seg_start, rep_slot, counts_from_chunks, replica_stats, status));
   PP_LAUNCH_CHECK();
   return PP_OK;
 }
@@ -503,7 +508,7 @@ extern "C" int pp_dispatch(const void* x, const int32_t* idx, const int32_t* ran
                "pp_dispatch: null pointer");
   PP_CHECK_ARG(my_rank >= 0 && (int64_t)(my_rank + 1) * T * k < (1ll << 31), "pp_dispatch: bad my_rank");
   cudaStream_t st = as_stream(stream);
-  PP_VPL_SWITCH(d, (dispatch_kernel<VPL><<<grid_for_tokens(T), 256, 0, st>>>(
+  PP_VPL_SWITCH(d, PP_CUDA_TRY(pdl_launch(dispatch_kernel<VPL>, dim3(grid_for_tokens(T)), dim3(256), 0, st, 
                        reinterpret_cast<const __nv_bfloat16*>(x), idx, rank, chunk_base,
                        slot_dest, T, d, k, m, E, recv_ptrs, pair_dest, pair_row, groups, num_groups,
                        reinterpret_cast<__nv_bfloat16*>(own_recv), origin_ptrs, my_rank)));
@@ -515,7 +520,7 @@ extern "C" int pp_combine(void* const* out_ptrs, const int32_t* pair_dest, const
                           const float* w, int32_t T, int32_t d, int32_t k, void* y, const void* comb,
                           void* stream) {
   PP_CHECK_ARG((out_ptrs || comb) && pair_dest && pair_row && w && y, "pp_combine: null pointer");
-  PP_VPL_SWITCH(d, (combine_kernel<VPL><<<grid_for_tokens(T), 256, 0, as_stream(stream)>>>(
+  PP_VPL_SWITCH(d, PP_CUDA_TRY(pdl_launch(combine_kernel<VPL>, dim3(grid_for_tokens(T)), dim3(256), 0, as_stream(stream), 
                        out_ptrs, pair_dest, pair_row, w, T, d, k,
                        reinterpret_cast<__nv_bfloat16*>(y), reinterpret_cast<const __nv_bfloat16*>(comb))));
   PP_LAUNCH_CHECK();
@@ -539,11 +544,11 @@ extern "C" int pp_combine_bwd(const void* dy, void* const* out_ptrs, void* const
   auto* own = reinterpret_cast<__nv_bfloat16*>(own_dgrad);
   auto* cb = reinterpret_cast<const __nv_bfloat16*>(comb);
   if (EP == 64) {
-    PP_VPL_SWITCH(d, (combine_bwd_kernel<VPL, 64><<<grid_for_tokens(T), 256, 0, st>>>(
+    PP_VPL_SWITCH(d, PP_CUDA_TRY(pdl_launch(combine_bwd_kernel<VPL, 64>, dim3(grid_for_tokens(T)), dim3(256), 0, st, 
                          ddy, out_ptrs, dgrad_ptrs, pair_dest, pair_row, w, T, d, k, dw, groups, num_groups,
                          own, cb, idx, probs, E, dlp)));
   } else {
-    PP_VPL_SWITCH(d, (combine_bwd_kernel<VPL, 128><<<grid_for_tokens(T), 256, 0, st>>>(
+    PP_VPL_SWITCH(d, PP_CUDA_TRY(pdl_launch(combine_bwd_kernel<VPL, 128>, dim3(grid_for_tokens(T)), dim3(256), 0, st, 
                          ddy, out_ptrs, dgrad_ptrs, pair_dest, pair_row, w, T, d, k, dw, groups, num_groups,
                          own, cb, idx, probs, E, dlp)));
   }
@@ -561,6 +566,7 @@ __global__ void __launch_bounds__(256)
     dispatch_bwd_kernel(void* const* dxp_ptrs, const __nv_bfloat16* __restrict__ comb,
                         const int32_t* __restrict__ pair_dest, const int32_t* __restrict__ pair_row,
                         int T, int d, int k, __nv_bfloat16* dx) {
+  pdl_grid_sync();
   const int lane = threadIdx.x & 31;
   const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -633,7 +639,7 @@ extern "C" int pp_dispatch_bwd(void* const* dxp_ptrs, const void* comb, const in
   PP_CHECK_ARG((dxp_ptrs || comb) && pair_dest && pair_row && dx, "pp_dispatch_bwd: null pointer");
   PP_CHECK_ARG(k >= 1 && k <= 8, "pp_dispatch_bwd: k=%d", k);
   cudaStream_t st = as_stream(stream);
-  PP_VPL_SWITCH(d, (dispatch_bwd_kernel<VPL><<<grid_for_tokens(T), 256, 0, st>>>(
+  PP_VPL_SWITCH(d, PP_CUDA_TRY(pdl_launch(dispatch_bwd_kernel<VPL>, dim3(grid_for_tokens(T)), dim3(256), 0, st, 
                        dxp_ptrs, reinterpret_cast<const __nv_bfloat16*>(comb), pair_dest, pair_row, T, d, k,
                        reinterpret_cast<__nv_bfloat16*>(dx))));
   PP_LAUNCH_CHECK();
@@ -663,6 +669,7 @@ constexpr int kDotCtas = 592;  // 4 per SM
 
 __global__ void __launch_bounds__(512) dot_bf16_partial_kernel(const uint4* a, const uint4* b, int64_t nvec,
                                                                float* partial) {
+  pdl_grid_sync();
   float s = 0.f;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nvec; i += (int64_t)gridDim.x * blockDim.x) {
     const uint4 x = ld_nc_v4(a + i), y = ld_nc_v4(b + i);
@@ -687,6 +694,7 @@ __global__ void __launch_bounds__(512) dot_bf16_partial_kernel(const uint4* a, c
 }
 
 __global__ void dot_bf16_final_kernel(const float* partial, int n, float* out) {
+  pdl_grid_sync();
   __shared__ float ws[32];
   float s = 0.f;
   for (int i = threadIdx.x; i < n; i += blockDim.x) s += partial[i];
@@ -707,9 +715,9 @@ extern "C" int pp_dot_bf16(const void* a, const void* b, int64_t n, float* parti
   PP_CHECK_ARG(n >= 0 && n % 8 == 0, "pp_dot_bf16: n=%lld must be a multiple of 8", (long long)n);
   PP_CHECK_ARG(((uintptr_t)a | (uintptr_t)b) % 16 == 0, "pp_dot_bf16: operands must be 16-byte aligned");
   cudaStream_t st = as_stream(stream);
-  dot_bf16_partial_kernel<<<kDotCtas, 512, 0, st>>>(reinterpret_cast<const uint4*>(a),
-                                                    reinterpret_cast<const uint4*>(b), n / 8, partial);
-  dot_bf16_final_kernel<<<1, 1024, 0, st>>>(partial, kDotCtas, out);
+  PP_CUDA_TRY(pdl_launch(dot_bf16_partial_kernel, dim3(kDotCtas), dim3(512), 0, st, reinterpret_cast<const uint4*>(a),
+                                                    reinterpret_cast<const uint4*>(b), n / 8, partial));
+  PP_CUDA_TRY(pdl_launch(dot_bf16_final_kernel, dim3(1), dim3(1024), 0, st, partial, kDotCtas, out));
   PP_LAUNCH_CHECK();
   return PP_OK;
 }

@@ -153,6 +153,7 @@ __device__ __forceinline__ int64_t add_replicas(uint8_t* holder, int32_t* rep, i
 }
 
 __global__ void __launch_bounds__(kMaxPlanThreads) plan_greedy_kernel(PlanArgs a) {
+  pdl_grid_sync();
   const int L = blockIdx.x;
   const int E = a.E;
   const int d = threadIdx.x;
@@ -309,6 +310,7 @@ struct PhysArgs {
 };
 
 __global__ void __launch_bounds__(kMaxPlanThreads) plan_physical_kernel(PhysArgs a) {
+  pdl_grid_sync();
   const int L = blockIdx.x;
   const int D = a.D, E = a.E, m = E / D, rpd = a.rows / D;
   const int t = threadIdx.x;
@@ -521,6 +523,7 @@ __global__ void __launch_bounds__(kMaxPlanThreads) plan_physical_kernel(PhysArgs
 
 __global__ void derive_loads_kernel(const int64_t* counts, const uint8_t* mask, int D, int E,
                                     int64_t* H, int64_t* R) {
+  pdl_grid_sync();
   for (int x = threadIdx.x; x < D; x += blockDim.x) {
     int64_t loc = 0, rem = 0;
     for (int e = 0; e < E; ++e)
@@ -539,6 +542,7 @@ __global__ void derive_loads_kernel(const int64_t* counts, const uint8_t* mask, 
 // device (empty excluded sets); all other experts stay home.
 __global__ void top_m_mask_kernel(const int64_t* counts, int D, int E, int m_top, uint8_t* mask,
                                   int32_t* selected) {
+  pdl_grid_sync();
   extern __shared__ int64_t tot[];
   for (int e = threadIdx.x; e < E; e += blockDim.x) {
     int64_t s = 0;
@@ -563,7 +567,7 @@ extern "C" int pp_top_m_mask(const int64_t* counts, int32_t D, int32_t E, int32_
                              uint8_t* mask, int32_t* selected, void* stream) {
   PP_CHECK_ARG(counts && mask && D >= E && E >= 1 && E <= 4096, "pp_top_m_mask: bad arguments");
   PP_CHECK_ARG(m_top >= 1 && m_top <= E, "top-m policy needs 1 <= m <= E, got %d", m_top);
-  top_m_mask_kernel<<<1, 256, sizeof(int64_t) * E, as_stream(stream)>>>(counts, D, E, m_top, mask, selected);
+  PP_CUDA_TRY(pdl_launch(top_m_mask_kernel, dim3(1), dim3(256), sizeof(int64_t) * E, as_stream(stream), counts, D, E, m_top, mask, selected));
   PP_LAUNCH_CHECK();
   return PP_OK;
 }
@@ -588,7 +592,7 @@ extern "C" int pp_plan_greedy(const int64_t* counts, int32_t num_layers, int32_t
   PP_CHECK_ARG(cfg->max_replicas >= 0 && cfg->slots_per_rank >= 0, "pp_plan_greedy: bad replica bound");
   PlanArgs a{counts, E, *cm, *cfg, selected, num_selected, num_explored, mask, H, R, best_cost};
   const int threads = ((E + 31) / 32) * 32;
-  plan_greedy_kernel<<<num_layers, threads, sizeof(int64_t) * E, as_stream(stream)>>>(a);
+  PP_CUDA_TRY(pdl_launch(plan_greedy_kernel, dim3(num_layers), dim3(threads), sizeof(int64_t) * E, as_stream(stream), a));
   PP_LAUNCH_CHECK();
   return PP_OK;
 }
@@ -619,7 +623,7 @@ extern "C" int pp_plan_physical(const int64_t* counts, int32_t num_layers, int32
              mask, H, R, best_cost};
   const int threads = ((E + 31) / 32) * 32;
   const size_t smem = sizeof(int64_t) * ((size_t)D * E + E) + (size_t)D * E + E;
-  plan_physical_kernel<<<num_layers, threads, smem, as_stream(stream)>>>(a);
+  PP_CUDA_TRY(pdl_launch(plan_physical_kernel, dim3(num_layers), dim3(threads), smem, as_stream(stream), a));
   PP_LAUNCH_CHECK();
   return PP_OK;
 }
@@ -629,7 +633,7 @@ extern "C" int pp_derive_loads(const int64_t* counts, const uint8_t* mask, int32
   PP_CHECK_ARG(counts && mask && H && R, "pp_derive_loads: null pointer");
   PP_CHECK_ARG(D >= 1 && E >= 1, "pp_derive_loads: empty dims");
   if (E > D) return fail(PP_EDIM, "pp_derive_loads: identity homes need E <= D (E=%d, D=%d)", E, D);
-  derive_loads_kernel<<<1, 256, 0, as_stream(stream)>>>(counts, mask, D, E, H, R);
+  PP_CUDA_TRY(pdl_launch(derive_loads_kernel, dim3(1), dim3(256), 0, as_stream(stream), counts, mask, D, E, H, R));
   PP_LAUNCH_CHECK();
   return PP_OK;
 }

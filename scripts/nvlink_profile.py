@@ -13,7 +13,7 @@ import paper_2411_10003_b200 as pp
 
 rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
 torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)) % torch.cuda.device_count())
-dist.init_process_group("gloo")
+dist.init_process_group("gloo", timeout=__import__("datetime").timedelta(minutes=10))
 E, k, d, f, T = 16, 2, 1024, 4096, 16384
 layer = pp.MoELayer(d, f, E, k, tokens=T, group=dist.group.WORLD, planning="device",
                     planner=pp.PlannerConfig(n=1, alpha=0.5), seed=0)
