@@ -914,9 +914,30 @@ def main() -> None:
         torch.cuda.synchronize()
         dev_masks = out.mask.cpu().numpy().astype(bool)
         us_launch = p0.elapsed_time(p1) / 20 * 1e3
+        # the physically-faithful search + slot refinement (8(f) row 4) on the same matrices, as a
+        # D-device plan (D = this run's world, or 8 -- the cfg4/cfg5 target -- on one GPU)
+        Dp = world if world > 1 else (8 if E % 8 == 0 and E >= 16 else 0)
+        phys_us = None
+        if Dp:
+            from paper_2411_10003_b200.layer import default_specs as _ds
+
+            cl_d, mo_d = _ds(E, k, d, f, T * world)
+            cm_d = _device.cost_model(cl_d, mo_d)
+            cm_d.num_devices = Dp
+            pc_d = _device.planner_cfg(pp.PlannerConfig(n=0, alpha=args.alpha))
+            out_d = _device.PlanBuffers(L_rec, E, dev)
+            for _ in range(3):
+                _device.launch_plan(counts_dev, out_d, cm_d, pc_d, physical_devices=Dp, refine_slots=True)
+            p0.record()
+            for _ in range(20):
+                _device.launch_plan(counts_dev, out_d, cm_d, pc_d, physical_devices=Dp, refine_slots=True)
+            p1.record()
+            torch.cuda.synchronize()
+            phys_us = {"D": Dp, "us_per_launch": p0.elapsed_time(p1) / 20 * 1e3, "layers_per_launch": L_rec}
         planner_info = {"device_us_per_launch": us_launch, "layers_per_launch": L_rec,
                         "device_us_per_layer_equiv": us_launch / L_rec, "E_virtual": E,
                         "matrices": "this run's recorded LoadMatrices (one per instrumented iteration)",
+                        "physical_refine": phys_us,
                         "config": {"n": pcfg_.n, "alpha": pcfg_.alpha, "overlap_aware": pcfg_.overlap_aware}}
         H0 = recs[-1].sum(axis=0)
         imbalance = {"virtual_slot_H_sigma_vanilla": pm.balance_degree(H0),

@@ -40,7 +40,7 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 // own dependents launch.  Launched with programmatic stream serialization (pdl_launch), a
 // kernel's launch processing and CTA rasterisation overlap the tail of its predecessor
 // instead of following its completion; without the attribute both instructions are no-ops.
-// PPMOE_PDL=0 turns the attribute off.
+// Opt-in (PPMOE_PDL=1): see pdl_enabled() in capi.cu for why it is off by default.
 __device__ __forceinline__ void pdl_grid_sync() {
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");

@@ -1027,6 +1027,16 @@ class MoELayer(torch.nn.Module):
                      expert=int(r[4]), src_rank=int(r[5])) for r in t]
 
     def close(self) -> None:
+        """Release the peer-mapped buffers.  Collective at D > 1: every rank drains its streams
+        and meets at a barrier first, so no peer still loads from / stores into this rank's
+        memory (dispatch_bwd peer loads, Agg pushes, copy-engine pulls); the parameter and
+        main_grad views of the freed arenas are dropped."""
+        torch.cuda.synchronize()
+        if self.world > 1:
+            dist.barrier(group=self.group)
+        for prm in (self.w1, self.w2):
+            prm.main_grad = None
+            prm.data = torch.empty(0, dtype=prm.dtype, device=prm.device)
         for b in (self.w1_arena, self.w2_arena, self.g1_arena, self.g2_arena, self.xp, self.yp,
                   self.counts_buf, self.origin, self.comb, self.trans_flags,
                   self.barrier, getattr(self, "comm_barrier", None)):
