@@ -338,7 +338,7 @@ def run_stack(args, cfg_name: str, cfg: dict, world: int, rank: int, dev, group)
     g = torch.Generator(device="cpu").manual_seed(1000 + rank)
     x = torch.randn((T, d), generator=g).to(dev, torch.bfloat16)
     dy = (torch.randn((T, d), generator=g) * 0.1).to(dev, torch.bfloat16)
-    use_graph = not args.eager
+    use_graph = not args.eager and not any(m.shared_device for m in stack.moe)
 
     def step_eager():
         xin = x.detach().requires_grad_(True)
@@ -560,7 +560,7 @@ def main() -> None:
 
     # ---- step function: CUDA-graph replay of fwd+bwd at N == 1 (host cost ~ one
     # graph launch per step), eager stream-ordered calls at N > 1
-    use_graph = not args.eager
+    use_graph = not args.eager and not emulated  # ranks sharing a GPU: host barriers, no graph
     NB = int(os.environ.get("PP_BENCH_NBUF", "2"))  # input buffers / graphs: e2e stages H2D NB-1 steps ahead
     xs = [x.detach().clone() for _ in range(NB)]
     if use_graph:

@@ -173,9 +173,15 @@ class PeerBuffer:
 
 
 class _Barrier:
-    def __init__(self, group, device) -> None:
+    """Device barrier over peer memory (pp_peer_barrier: signal words, spin with a 20 s trap).
+    host=True (ranks sharing one GPU): a host barrier instead -- drain the device, then
+    dist.barrier -- so no kernel ever spins on another process's progress (on a shared GPU
+    that would depend on the driver preempting the spinning kernel)."""
+
+    def __init__(self, group, device, host: bool = False) -> None:
         self.world = dist.get_world_size(group) if group is not None else 1
         self.rank = dist.get_rank(group) if group is not None else 0
+        self.group, self.host = group, host
         if self.world > 1:
             self.sig = PeerBuffer((self.world + 1,), torch.int64, group, device)
             torch.cuda.synchronize()
@@ -187,6 +193,10 @@ class _Barrier:
 
     def __call__(self, stream=None) -> None:
         if self.world == 1:
+            return
+        if self.host:
+            torch.cuda.synchronize()
+            dist.barrier(group=self.group)
             return
         # epoch 0: the kernel advances a device-side counter, so captured graphs replay correctly
         _lib.call("pp_peer_barrier", self.sig.ptrs.data_ptr(), self.world, self.rank, 0,
@@ -257,6 +267,13 @@ class MoELayer(torch.nn.Module):
         if self.world == 1:
             self.group = None
         E, D = num_experts, self.world
+        # ranks sharing one GPU (the 1-GPU parity runs): host-synchronised barriers, Trans
+        # awaited before FWD1 instead of per-tile gates -- nothing spins on another process
+        self.shared_device = False
+        if D > 1:
+            ids = [None] * D
+            dist.all_gather_object(ids, str(torch.cuda.get_device_properties(self.device).uuid), group=self.group)
+            self.shared_device = len(set(ids)) < D
         if E % D:
             raise ValidationError(f"num_experts={E} must be a multiple of the EP world size {D}")
         self.d, self.f, self.E, self.k, self.T = d_model, d_ff, E, top_k, tokens
@@ -388,7 +405,7 @@ class MoELayer(torch.nn.Module):
         # SM engine: True = Trans issued after barrier 1, overlapping FWD1/FWD2 on the home
         # experts with the replica tiles gated on completion flags; False = issued at the
         # start of the forward and awaited before barrier 1
-        self.trans_gate = True
+        self.trans_gate = not self.shared_device
         # SM-engine Agg runs beside the backward GEMMs on agg_ctas SMs (one CTA per SM);
         # those GEMMs launch their persistent grids on the remaining SMs so neither waits
         # for the other (pushes reach NVLink rate from ~16 CTAs)
@@ -445,12 +462,12 @@ class MoELayer(torch.nn.Module):
             # layout output: [replicas of my home experts elsewhere, replicas I hold] -> the
             # GEMMs size their SM reservation for Trans / Agg from it, on device
             self.replica_stats = torch.zeros(2, dtype=torch.int32, device=dev)
-            self.comm_barrier = _Barrier(self.group, dev)
+            self.comm_barrier = _Barrier(self.group, dev, host=self.shared_device)
         elif D > 1:
             # copy engine: the replicas pull the home weights; a barrier on the comm stream
             # orders the pulls after every home's optimizer step (stream order of this rank's
             # forward start + arrival of every peer at the same point)
-            self.comm_barrier = _Barrier(self.group, dev)
+            self.comm_barrier = _Barrier(self.group, dev, host=self.shared_device)
         self._plan_pending = None
         self._mask_host = torch.zeros((E, E), dtype=torch.uint8).pin_memory() if D > 1 else None
         self.mask_cur_host = None
@@ -461,7 +478,7 @@ class MoELayer(torch.nn.Module):
         self._trans_done = None
         self._trans_iter = -1     # iteration whose Trans has been issued
         self.replica_experts = []  # replica experts held by this rank under the current plan
-        self.barrier = _Barrier(self.group, dev)
+        self.barrier = _Barrier(self.group, dev, host=self.shared_device)
         self.history = []  # host copies of LoadMatrix per iteration (optional, record_history)
         self.record_history = False
         self.events = {}
@@ -860,7 +877,10 @@ class MoELayer(torch.nn.Module):
         # SM engine: the home ranks push after barrier 1, overlapping FWD1 on the home experts,
         # and each receiver's FWD1 gates only its replica tiles on the pushers' completion flags
         sm_gate = self.replica_engine == "sm" and self.world > 1 and self.trans_gate
-        trans_done = None if sm_gate else self.issue_trans()  # no-op if a scheduler issued it earlier
+        # top-m: this iteration's mask exists only after the histogram, so its Trans is issued
+        # after barrier 1 even when it is not gated
+        late = bool(self.top_m) and self.world > 1
+        trans_done = None if (sm_gate or late) else self.issue_trans()  # no-op if a scheduler issued it
         self._route_and_layout(x)
         self._mark("route_layout")
         self._launch_planner()  # [A2A | Plan(j+1)]: the search overlaps this block's dispatch
@@ -876,8 +896,12 @@ class MoELayer(torch.nn.Module):
         self._mark("trans_wait")
         self.barrier()  # every rank's rows have landed
         self._mark("barrier1")
-        if sm_gate:
+        if sm_gate or late:
             trans_done = self.issue_trans()
+            if late and not sm_gate and trans_done is not None:
+                # ungated (ranks sharing a GPU): this rank's pushes done, then every rank's
+                torch.cuda.current_stream().wait_event(trans_done)
+                self.barrier()
         total = self.gemm_sms or _device.num_sms(self.device)
         gated = sm_gate and trans_done is not None
         plan_sms = 2 if self._plan_inflight() else 0  # the planner's CTA stays out of the static walk
@@ -985,6 +1009,8 @@ class MoELayer(torch.nn.Module):
         rank captures and replays in lockstep)."""
         if self.world != 1 and self.planning != "device":
             raise ValidationError("make_graphed_step at D > 1 needs planning='device'")
+        if self.shared_device:
+            raise ValidationError("make_graphed_step needs one GPU per rank (ranks sharing a GPU use host barriers)")
         return GraphedStep(self, x, dy, with_loss, gemm_events, timeline_events)
 
     # ---- introspection (LoadMatrix / placement of the last call) -------------

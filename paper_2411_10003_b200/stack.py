@@ -281,6 +281,8 @@ class StackGraph:
         for m in stack.moe:
             if m.world > 1 and m.planning != "device":
                 raise ValueError("MoEStack.make_graphed_step at D > 1 needs the layers' planning='device'")
+            if m.shared_device:
+                raise ValueError("MoEStack.make_graphed_step needs one GPU per rank")
         self.stack, self.x, self.dy = stack, x.detach().requires_grad_(True), dy
 
         def once():

@@ -35,8 +35,10 @@ def main():
     emulated = ngpu < world
     torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)) % ngpu)
     dev = torch.device("cuda", torch.cuda.current_device())
-    if emulated:
-        dist.init_process_group("gloo")
+    if emulated:  # fail fast instead of waiting out gloo's 30-minute default on a broken peer
+        import datetime
+
+        dist.init_process_group("gloo", timeout=datetime.timedelta(seconds=240))
     else:
         dist.init_process_group("cpu:gloo,cuda:nccl", device_id=dev)
     if rank == 0:
@@ -149,7 +151,7 @@ def main():
         okt = torch.tensor([1 if ok else 0])
         dist.broadcast(okt, 0)
         ok = bool(okt.item())
-    if layer.planning == "device":
+    if layer.planning == "device" and not layer.shared_device:
         # graph replay of the whole EP step (barriers, plan, Trans/Agg inside) == eager, bit-exact
         x, _ = M.exact_inputs(T, d, E, seed=4242 + rank)
         xd = x.to(dev)

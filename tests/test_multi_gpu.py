@@ -9,9 +9,10 @@ physically-faithful planner (plans vs the oracle's greedy_search_physical).
 With >= 2 GPUs each rank gets its own device (NCCL/NVLink).  With ONE GPU the
 ranks are emulated: D processes share cuda:0, exchange CUDA IPC handles over gloo
 and talk through the same peer-memory kernels (dispatch/combine peer stores and
-loads, barriers, Trans/Agg pushes) -- every device code path of the EP step runs,
-only the NVLink hop is replaced by local HBM.  The spin barriers progress because
-the driver time-slices the rank processes' contexts."""
+loads, Trans/Agg pushes, the layout / planner / GEMMs) -- only the NVLink hop is
+replaced by local HBM.  The layer detects the shared device and synchronises on the
+host instead of spinning on the device (barriers, Trans gates), so no kernel ever
+waits on another process's progress; the CUDA-graph replay check needs one GPU per rank."""
 import os
 import subprocess
 import sys
@@ -29,7 +30,7 @@ def _ngpus():
     return torch.cuda.device_count() if torch.cuda.is_available() else 0
 
 
-def _run(n, env_extra, timeout=900):
+def _run(n, env_extra, timeout=600):
     env = dict(os.environ, **env_extra)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(n),
            "--master-addr", "127.0.0.1", "--master-port", str(29500 + (os.getpid() % 500)),
@@ -79,4 +80,4 @@ def test_ep_layer_parity_d4(planning, engine, placement):
 @pytest.mark.skipif(_ngpus() < 1, reason="needs a GPU")
 def test_ep_layer_parity_d8_shape():
     """The N = 8 EP shape: 8 ranks, E = 16 (m = 2), emulated on the available GPUs."""
-    _run(8, dict(_env("device", "sm", "", "virtual"), PP_T="1024", PP_E="16"), timeout=1200)
+    _run(8, dict(_env("device", "sm", "", "virtual"), PP_T="1024", PP_E="16"), timeout=900)
