@@ -595,12 +595,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (gate_pending && tl.wslot >= p.gate_slot0) {  // first replica tile: Trans must have landed
           const uint64_t e = *p.gate_epoch;
           const uint64_t t0 = globaltimer_ns();
-          for (int r = 0; r < p.gate_D; ++r) {
+          bool timed_out = false;
+          for (int r = 0; r < p.gate_D && !timed_out; ++r) {
             if (r == p.gate_me) continue;
             while (ld_acquire_sys_u64(p.gate_flags + r) < e) {
               if (globaltimer_ns() - t0 > 20ull * 1000 * 1000 * 1000) {
+                // a pusher never signalled (crashed peer): record the fault next to the epoch
+                // (the host raises on it) and finish instead of hanging or killing the context
                 printf("ppmoe: replica gate timeout (rank %d waiting on %d)\n", p.gate_me, r);
-                __trap();
+                const_cast<uint64_t*>(p.gate_epoch)[1] = 1;
+                timed_out = true;
+                break;
               }
             }
           }

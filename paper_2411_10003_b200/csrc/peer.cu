@@ -25,9 +25,12 @@ __device__ __forceinline__ uint64_t global_ns() {
   return t;
 }
 
-// signal area of rank r: uint64_t[D + 1]; slot s < D is written by rank s, slot D holds
-// r's own barrier counter.  epoch == 0: take the epoch from that device counter (so a
-// captured CUDA graph can replay barriers), otherwise use the host-provided value.
+// signal area of rank r: uint64_t[D + 2]; slot s < D is written by rank s, slot D holds
+// r's own barrier counter, slot D + 1 is r's fault word.  epoch == 0: take the epoch from
+// that device counter (so a captured CUDA graph can replay barriers), otherwise use the
+// host-provided value.  A peer that never arrives (crashed rank) does not hang the GPU and
+// does not kill the context: after 20 s the wait gives up, records the fault word (the
+// host raises on it) and the kernel returns.
 __global__ void peer_barrier_kernel(void* const* signal_ptrs, int D, int me, uint64_t epoch) {
   pdl_grid_sync();
   __shared__ uint64_t ep;
@@ -48,7 +51,8 @@ __global__ void peer_barrier_kernel(void* const* signal_ptrs, int D, int me, uin
       if (global_ns() - t0 > 20ull * 1000 * 1000 * 1000) {
         printf("ppmoe: peer barrier timeout (rank %d waiting on %d, epoch %llu)\n", me, r,
                (unsigned long long)e);
-        __trap();
+        own[D + 1] = 1;  // fault word: the host raises
+        break;
       }
     }
   }

@@ -183,7 +183,7 @@ class _Barrier:
         self.rank = dist.get_rank(group) if group is not None else 0
         self.group, self.host = group, host
         if self.world > 1:
-            self.sig = PeerBuffer((self.world + 1,), torch.int64, group, device)
+            self.sig = PeerBuffer((self.world + 2,), torch.int64, group, device)  # signals, epoch, fault
             torch.cuda.synchronize()
             dist.barrier(group=group)
 
@@ -344,7 +344,7 @@ class MoELayer(torch.nn.Module):
         # layout status (sticky bits: 1 rows > capacity, 2 replica slots, 4 groups), read
         # back asynchronously after every eager forward
         self.status = torch.zeros((1,), **i32)
-        self._status_host = torch.zeros((1,), dtype=torch.int32).pin_memory()
+        self._status_host = torch.zeros((4,), dtype=torch.int64).pin_memory()  # status, fault words
         self._status_ev = None
         self.pair_dest = torch.empty((T, k), **i32)
         self.pair_row = torch.empty((T, k), **i32)
@@ -458,7 +458,7 @@ class MoELayer(torch.nn.Module):
             # Trans completion flags (slot r written by rank r) + the pushers' CTA counter
             self.trans_flags = PeerBuffer((2, D), torch.int64, self.group, dev)  # rows: W1, W2
             self._trans_ctr = torch.zeros(1, dtype=torch.int32, device=dev)
-            self._trans_epoch = torch.zeros(1, dtype=torch.int64, device=dev)
+            self._trans_epoch = torch.zeros(2, dtype=torch.int64, device=dev)  # [epoch, gate fault word]
             # layout output: [replicas of my home experts elsewhere, replicas I hold] -> the
             # GEMMs size their SM reservation for Trans / Agg from it, on device
             self.replica_stats = torch.zeros(2, dtype=torch.int32, device=dev)
@@ -558,7 +558,9 @@ class MoELayer(torch.nn.Module):
         if self.record_history:
             self.history.append(self.counts.clone())
         if not torch.cuda.is_current_stream_capturing():
-            self._status_host.copy_(self.status, non_blocking=True)
+            self._status_host[0:1].copy_(self.status, non_blocking=True)
+            for i, f in enumerate(self._fault_words()[:3]):
+                self._status_host[1 + i: 2 + i].copy_(f, non_blocking=True)
             self._status_ev = torch.cuda.Event()
             self._status_ev.record()
 
@@ -566,16 +568,32 @@ class MoELayer(torch.nn.Module):
         """Raise CapacityError if an earlier step's layout was dropped (non-blocking)."""
         if self._status_ev is None or torch.cuda.is_current_stream_capturing():
             return
-        if self._status_ev.query() and int(self._status_host[0]):
-            self._raise_status(int(self._status_host[0]))
+        if self._status_ev.query() and int(self._status_host.max()):
+            self._raise_status(int(self._status_host[0]), self._status_host[1:].tolist())
+
+    def _fault_words(self) -> list:
+        """Device fault words of the cross-rank waits (peer barriers, replica gate): nonzero
+        when a wait gave up after 20 s because a peer never arrived."""
+        out = []
+        for b in (self.barrier, getattr(self, "comm_barrier", None)):
+            if b is not None and b.world > 1:
+                out.append(b.sig.local[b.world + 1: b.world + 2])
+        if getattr(self, "_trans_epoch", None) is not None:
+            out.append(self._trans_epoch[1:2])
+        return out
 
     def check_status(self) -> None:
-        """Synchronous check of the layout status (call e.g. after graph replays)."""
+        """Synchronous check of the layout status and the cross-rank fault words (call e.g.
+        after graph replays)."""
         st = int(self.status.item())
-        if st:
-            self._raise_status(st)
+        faults = [int(f.item()) for f in self._fault_words()]
+        if st or any(faults):
+            self._raise_status(st, faults)
 
-    def _raise_status(self, st: int) -> None:
+    def _raise_status(self, st: int, faults=()) -> None:
+        if any(int(f) for f in faults):
+            raise RuntimeError("MoE layer: a cross-rank wait timed out after 20 s (a peer rank never "
+                               "arrived); the step's results are invalid")
         why = []
         if st & 1:
             why.append(f"a rank needed more than rows_capacity={self.rows_cap} receive rows")
@@ -718,7 +736,7 @@ class MoELayer(torch.nn.Module):
         if self.world == 1 or self.mask_cur is None:
             return None
         if self.replica_engine == "sm":
-            self._trans_epoch.add_(1)  # stream-ordered before this rank's FWD1 / FWD2 gates
+            self._trans_epoch[0:1].add_(1)  # stream-ordered before this rank's FWD1 / FWD2 gates
         ev = torch.cuda.Event()
         ev.record()
         with torch.cuda.stream(self.comm_stream):
