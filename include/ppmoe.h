@@ -284,7 +284,9 @@ int pp_dot_bf16(const void* a, const void* b, int64_t n, float* partial, float* 
  *   home groups (wslot < first_replica_slot) are scheduled first; before the
  *   first replica tile's loads the TMA producer waits until gate_flags[r] >=
  *   *gate_epoch for every peer r != my_rank (the completion flags of
- *   pp_replica_trans; gate_flags = this rank's [D] uint64 row).  20 s -> trap.
+ *   pp_replica_trans; gate_flags = this rank's [D] uint64 row).  After 20 s without a
+ *   flag the gate gives up and stores 1 into gate_epoch[1] (fault word; gate_epoch must
+ *   point at two uint64 words).
  * Device-adaptive SM reservation (res_stats != NULL, pp_dispatch_layout's
  *   replica_stats): the persistent walk leaves clamp(res_per_unit * (stats[0] +
  *   (res_both ? stats[1] : 0)), res_lo, res_hi) of the num_sms SMs to concurrent
@@ -362,10 +364,11 @@ int pp_ipc_import(const uint8_t* handle64, void** dev_ptr);
 int pp_ipc_close(void* dev_ptr);
 
 /* Cross-rank barrier over peer-mapped signal words.  signal_ptrs: device
- * array [D] of each rank's signal area (uint64_t[D + 1] each: D peer slots + this
- * rank's own counter).  epoch > 0: host-provided, must grow by one per call;
- * epoch == 0: taken from the device counter (CUDA-graph replayable).  Spins
- * with a 20 s timeout (traps instead of hanging). */
+ * array [D] of each rank's signal area (uint64_t[D + 2] each: D peer slots, this
+ * rank's own counter, this rank's fault word).  epoch > 0: host-provided, must grow by
+ * one per call; epoch == 0: taken from the device counter (CUDA-graph replayable).
+ * Spins with a 20 s timeout: a peer that never arrives sets the fault word to 1 and the
+ * kernel returns (no hang, no context kill; the caller checks the word). */
 int pp_peer_barrier(void* const* signal_ptrs, int32_t D, int32_t my_rank, uint64_t epoch,
                     void* stream);
 
