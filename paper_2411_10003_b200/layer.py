@@ -46,7 +46,7 @@ import torch
 import torch.distributed as dist
 
 from . import _device, _lib, memory
-from .core import ClusterSpec, LoadMatrix, ModelSpec, ValidationError
+from .core import ClusterSpec, LoadMatrix, ModelSpec, ValidationError, replica_sets, replica_transfers
 from .planner import PlannerConfig
 
 
@@ -679,27 +679,23 @@ class MoELayer(torch.nn.Module):
         self._derive_replicas(mh)
 
     def _derive_replicas(self, mh: np.ndarray) -> None:
-        D, m, E, me = self.world, self.m, self.E, self.rank
+        D, m, me = self.world, self.m, self.rank
         fd = self.d * self.f
-        reps = [[e for e in range(E) if e // m != r and mh[r * m:(r + 1) * m, e].any()] for r in range(D)]
-        if any(len(r) > self.max_replicas for r in reps):
+        if any(len(r) > self.max_replicas for r in replica_sets(mh, D, m)):
             raise ValidationError("plan needs more replica slots than max_replicas")
-        self.replica_experts = reps[me]
+        xf = replica_transfers(mh, D, m, me)
+        self.replica_experts = xf["replicas"]
         w1, w2 = self.w1_arena.ptr_list, self.w2_arena.ptr_list
         self._trans_list = []
-        for i, e in enumerate(reps[me]):
-            home, j = e // m, e % m
-            self._trans_list.append((w1[me] + (m + i) * fd * 2, w1[home] + j * fd * 2, fd * 2))
-            self._trans_list.append((w2[me] + (m + i) * fd * 2, w2[home] + j * fd * 2, fd * 2))
+        for e, home, j, slot in xf["trans_in"]:  # pulls of the home weights into my replica slots
+            self._trans_list.append((w1[me] + slot * fd * 2, w1[home] + j * fd * 2, fd * 2))
+            self._trans_list.append((w2[me] + slot * fd * 2, w2[home] + j * fd * 2, fd * 2))
         # Agg sources: for each home slot j, replicas of expert me*m+j on other ranks (rank order)
         g1, g2 = self.g1_arena.ptr_list, self.g2_arena.ptr_list
         srcs, ranges = [], [0]
         for j in range(m):
-            e = me * m + j
-            for r in range(D):
-                if r != me and e in reps[r]:
-                    slot = m + reps[r].index(e)
-                    srcs.append((g1[r] + slot * fd * 4, g2[r] + slot * fd * 4))
+            for r, slot in xf["agg_in"][j]:
+                srcs.append((g1[r] + slot * fd * 4, g2[r] + slot * fd * 4))
             ranges.append(len(srcs))
         self._agg_list = []
         if srcs:
@@ -1057,7 +1053,7 @@ class MoELayer(torch.nn.Module):
         in = received by the replica holder (Trans); Agg the reverse direction."""
         mh = self.current_mask() if mask is None else np.asarray(mask, dtype=bool)
         D, m, E = self.world, self.m, self.E
-        reps = [[e for e in range(E) if e // m != r and mh[r * m:(r + 1) * m, e].any()] for r in range(D)]
+        reps = replica_sets(mh, D, m)
         w = 2 * self.d * self.f * 2  # W1 + W2 bf16
         t_out = [sum(w for r in range(D) for e in reps[r] if e // m == h) for h in range(D)]
         t_in = [len(reps[r]) * w for r in range(D)]

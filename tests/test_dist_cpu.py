@@ -109,3 +109,67 @@ def test_plan_schedule_matches_reference_reuse_rule():
             anchor = (j // F) * F
             expect = None if anchor == 0 else anchor - 1
             assert current == expect == plan_source_iteration(j, F), (F, j)
+
+
+def _product_worker(rank, world, port, E, q):
+    """Product host logic of the N > 1 step at world size 2: each rank derives, independently,
+    its replica set, the Trans it pulls / pushes and the Agg it sums (core.replica_transfers,
+    the functions MoELayer uses for the copy-engine path and replica_traffic)."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import sys
+        from pathlib import Path
+
+        sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+        from oracle import planner_ref as P
+        from paper_2411_10003_b200 import core, memory
+
+        m = E // world
+        rng = np.random.default_rng(11)  # the same LoadMatrix on every rank (all-gathered in the layer)
+        counts = np.stack([rng.multinomial(512, rng.dirichlet(np.ones(E) * 0.3)) for _ in range(E)]).astype(np.int64)
+        cm = P.cost_model_dict(E, 2, 2048, 1e3, 1e3, 1e11, 1e6)  # cheap Trans: the plan replicates
+        mask = P.greedy_search(counts, 1, 0.5, False, cm)["mask"]
+        xf = core.replica_transfers(mask, world, m, rank)
+        cap = memory.rows_capacity(4096, 2, E, world, capacity_factor=2.0)
+        gathered = [None] * world
+        dist.all_gather_object(gathered, dict(xf=xf, cap=cap, reps=core.replica_sets(mask, world, m)))
+        if rank == 0:
+            q.put((gathered, mask))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("E", [8, 16])
+def test_two_rank_replica_transfers_product(E):
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_product_worker, args=(r, world, port, E, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res, mask = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    m = E // world
+    assert res[0]["reps"] == res[1]["reps"] and res[0]["cap"] == res[1]["cap"]
+    assert any(res[r]["xf"]["replicas"] for r in range(world))  # the plan did replicate
+    for r in range(world):
+        xf = res[r]["xf"]
+        # replica slots are dense, m .. m + #replicas - 1, ascending expert id
+        assert [s for *_, s in xf["trans_in"]] == list(range(m, m + len(xf["replicas"])))
+        assert [e for e, *_ in xf["trans_in"]] == sorted(xf["replicas"])
+        for e, home, j, slot in xf["trans_in"]:
+            # the home pushes exactly this (expert, home slot) into this rank's slot ...
+            assert (e, j, r, slot) in res[home]["xf"]["trans_out"]
+            # ... and sums this rank's grads of that slot back into home slot j (Agg)
+            assert (r, slot) in res[home]["xf"]["agg_in"][j]
+        for j, srcs in xf["agg_in"].items():
+            assert [s[0] for s in srcs] == sorted(s[0] for s in srcs)  # rank order: deterministic sum
+            assert all(r * m + j in res[s[0]]["xf"]["replicas"] for s in srcs)
+    # the mask itself: a rank holds e iff one of its slots keeps e's pairs (core.py:267-274)
+    for r in range(world):
+        held = mask[r * m:(r + 1) * m].any(axis=0)
+        assert res[0]["reps"][r] == [e for e in range(E) if e // m != r and held[e]]

@@ -263,3 +263,54 @@ def test_bench_cli_parses():
                        timeout=120)
     assert r.returncode == 0, r.stderr[-2000:]
     assert "--gpus" in r.stdout and "--impl" in r.stdout
+
+
+def test_bench_popularity_drift_is_the_reference_generator():
+    """bench.PopularityDrift (the cfg4 gate-bias drift) reproduces the reference trace
+    generator's per-iteration popularity (workload.py:113-136) bit for bit: the reference
+    draws each iteration's LoadMatrix from a generator keyed to the popularity vector's bytes
+    (_matrix_rng), so equal counts <=> identical p."""
+    from conftest import import_reference
+
+    moebal = import_reference()
+    from moebal import workload as W
+
+    import bench
+
+    E, D, inputs, k = 16, 4, 4096, 2
+    ref = W.generate_trace(W.GeneratorConfig(num_devices=D, num_experts=E, inputs_per_iteration=inputs,
+                                             top_k=k, skew=1.2, drift=0.05, seed=3), iterations=6, layers=1)
+    drift = bench.PopularityDrift(E, skew=1.2, drift=0.05, seed=3)
+    per_device = inputs // D * k
+    for rec in ref:
+        p = drift.step()
+        draw = W._matrix_rng(3, 0, p)
+        counts = np.stack([draw.multinomial(per_device, p) for _ in range(D)])
+        assert np.array_equal(counts, np.asarray(rec.load.counts)), rec.iteration
+
+
+def test_exposure_summary_on_a_handmade_timeline():
+    """exposure_summary applies the reference's exposure metric (scheduler.py:134-169): the
+    part of a Trans / Agg op not covered by compute-lane ops."""
+    from paper_2411_10003_b200.scheduler import IterationTimeline, Lane, OpKind, ScheduledOp
+    from paper_2411_10003_b200.stack import exposure_summary
+
+    ops = (ScheduledOp(OpKind.FEC, 0, 0, Lane.COMPUTE, 0.0, 1.0),
+           ScheduledOp(OpKind.SUB_TRANS1, 0, 0, Lane.NETWORK, 0.5, 1.0),   # 0.5 hidden, 0.5 exposed
+           ScheduledOp(OpKind.BEC, 0, 0, Lane.COMPUTE, 2.0, 2.0),
+           ScheduledOp(OpKind.SUB_AGG2, 0, 0, Lane.NETWORK, 3.5, 1.0))      # 0.5 hidden, 0.5 exposed
+    ex = exposure_summary(IterationTimeline(0, ops), blocks=1)
+    assert abs(ex["exposed_trans_ms"] - 500.0) < 1e-9 and abs(ex["exposed_agg_ms"] - 500.0) < 1e-9
+    assert abs(ex["makespan_ms"] - 4500.0) < 1e-9
+    assert abs(ex["exposed_replica_comm_frac"] - 1.0 / 4.5) < 1e-12
+
+
+def test_planner_cfg_struct_matches_header():
+    """pp_planner_cfg: the ctypes layout (size and offsets) the header declares."""
+    import ctypes
+
+    from paper_2411_10003_b200 import _lib
+
+    c = _lib.PlannerCfg
+    assert ctypes.sizeof(c) == 40
+    assert c.reuse_interval.offset == 16 and c.max_replicas.offset == 20 and c.iter_counter.offset == 32
