@@ -1298,9 +1298,10 @@ int route_gemm(const void* x, const void* wg, const float* bias, int T, int d, i
                int32_t* idx, float* w, float* probs, int32_t* rank, int32_t* chunk_counts,
                cudaStream_t st) {
   if (env_int("PPMOE_ROUTE_SPLITK", 1)) {
-    // d-split so that ~2 CTAs per SM exist (KS = 4 below 148 tiles, else 2), every slice >= one BK
+    // d split over a cluster of KS = 2 CTAs (cfg2: KS = 1 / 2 / 4 measured 14.4-16.8 / 14.2-15.6 /
+    // 21-22 us -- 4 needs a second wave), every slice >= one BK
     const int tiles = T / BM;
-    int KS = env_int("PPMOE_ROUTE_KS", tiles < 148 ? 4 : 2);
+    int KS = env_int("PPMOE_ROUTE_KS", 2);
     const int BNr = E <= 16 ? 16 : E <= 32 ? 32 : E <= 64 ? 64 : 128;
     if (BNr == 128 && KS > 2) KS = 2;  // smem: 4 stages + (KS-1) fp32 128 x 128 partials
     if (KS != 1 && KS != 2 && KS != 4) KS = 2;
