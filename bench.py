@@ -670,6 +670,40 @@ def main() -> None:
         exposure["exposed_replica_comm_frac_max_over_ranks"] = float(fr.item())
         exposure["source"] = "rank 0 median of 24 instrumented graph replays (external events as graph nodes)"
 
+        # ---- the A2A kernels' NVLink rate (nccl-tests all-to-all convention: algbw = this rank's
+        # send buffer T*k*d*2 / time, busbw = algbw * (D-1)/D) from the same graph-timed phases,
+        # beside NCCL's all_to_all_single on the same buffer (the collective-library ceiling)
+        try:
+            peer_pairs = int((layer.pair_dest != rank).sum().item())
+            buf = T * k * d * 2
+            dsp = sorted(ph["dispatch"] - ph["route_layout"] for _, _, ph in graph_calib)
+            cmb = sorted(ph["combine"] - ph["barrier2"] for _, _, ph in graph_calib)
+            t_d, t_c = dsp[len(dsp) // 2] / 1e3, cmb[len(cmb) // 2] / 1e3
+            a2a = {"send_buffer_bytes": buf, "peer_bytes": peer_pairs * d * 2,
+                   "dispatch_ms": t_d * 1e3, "combine_ms": t_c * 1e3,
+                   "dispatch_busbw_GBps": buf / t_d * (world - 1) / world / 1e9,
+                   "combine_busbw_GBps": buf / t_c * (world - 1) / world / 1e9,
+                   "dispatch_peer_GBps": peer_pairs * d * 2 / t_d / 1e9}
+            if not emulated:
+                src = torch.empty(buf // 2, dtype=torch.bfloat16, device=dev)
+                dst = torch.empty_like(src)
+                for _ in range(3):
+                    dist.all_to_all_single(dst, src)
+                n0, n1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                torch.cuda.synchronize()
+                n0.record()
+                for _ in range(10):
+                    dist.all_to_all_single(dst, src)
+                n1.record()
+                torch.cuda.synchronize()
+                t_n = n0.elapsed_time(n1) / 10 / 1e3
+                a2a.update({"nccl_all_to_all_ms": t_n * 1e3,
+                            "nccl_busbw_GBps": buf / t_n * (world - 1) / world / 1e9})
+                del src, dst
+            exposure["a2a"] = a2a
+        except Exception as exc:  # evidence only: never fail the bench
+            exposure["a2a"] = {"error": repr(exc)[:160]}
+
     # ---- instrumented eager pass of the same K steps: per-GEMM CUDA events on the
     # launching stream (graph replays cannot carry timing events) + phase timeline
     _lib.reset_launch_count()

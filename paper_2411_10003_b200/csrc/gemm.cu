@@ -11,7 +11,6 @@
 //   DGRAD1    dPre [rows,f]  K        W1 [slot][f][d]  MN         dXp bf16
 //   WGRAD2    dYp  [rows,d]  MN       act [rows,f]     MN         dW2[slot][d][f] fp32 (K = rows)
 //   WGRAD1    dPre [rows,f]  MN       Xp  [rows,d]     MN         dW1[slot][f][d] fp32 (K = rows)
-//   ROUTE     X    [T,d]     K        Wg [E][d]        K          softmax/top-k/chunk ranks (N = E)
 //
 // Groups (experts held by this rank) are ragged and read from device memory,
 // so no host sync is needed between routing and the GEMMs.  Every group's
@@ -40,7 +39,7 @@ constexpr int kMaxGroups = 256;
 constexpr int kTraceSteps = 1024;
 
 
-enum Epi { EPI_BF16 = 0, EPI_GELU = 1, EPI_DGELU = 2, EPI_F32 = 3, EPI_ROUTE = 4, EPI_BF16_ADD = 5, EPI_F32_ATOMIC = 6 };
+enum Epi { EPI_BF16 = 0, EPI_GELU = 1, EPI_DGELU = 2, EPI_F32 = 3 };
 
 // per-epilogue-warp staging for the TMA-store epilogue: a ring of out_bufs 32x32
 // blocks (bf16: 2 KB, SWIZZLE_64B; fp32: one 4 KB block, SWIZZLE_128B), so a warp
@@ -54,7 +53,7 @@ constexpr int out_bufs() {
 }
 template <int EPI>
 constexpr int out_base() {
-  return (EPI == EPI_DGELU || EPI == EPI_BF16_ADD) ? 2048 : 0;
+  return EPI == EPI_DGELU ? 2048 : 0;
 }
 // LSU = true: the epilogue's bf16 blocks go out through the LSUs (stage_and_store_lsu), so a
 // warp needs one 2 KB transpose block instead of a ring of TMA-store blocks -- the smem saved
@@ -85,7 +84,6 @@ struct GemmParams {
   int e_real;       // route: real expert count (<= BN; padded experts read as zero rows)
   int single_rows;  // > 0: implicit groups over rows [0, single_rows), slot 0
   int split_rows;   // with single_rows: split-K chunk size (one implicit group per chunk)
-  int m_real;       // EPI_F32_ATOMIC: rows of the output that exist (< M_fixed)
   unsigned long long* dbg;  // optional per-CTA wait-cycle counters (PPMOE_GEMM_DEBUG)
   // PPMOE_GEMM_DEBUG=2: per-k-step globaltimer trace of CTAs 0..3 (first kTraceSteps steps):
   // [cta][step][0..1] producer before/after the empty wait, [2..3] MMA before/after the full wait
@@ -227,8 +225,7 @@ __device__ __forceinline__ bool decode_tile(int t, const SchedSmem& s, const Gem
 
 template <int EPI>
 constexpr bool tma_out() {
-  return EPI == EPI_BF16 || EPI == EPI_GELU || EPI == EPI_DGELU || EPI == EPI_F32 ||
-         EPI == EPI_BF16_ADD;
+  return EPI == EPI_BF16 || EPI == EPI_GELU || EPI == EPI_DGELU || EPI == EPI_F32;
 }
 
 // Stage a 32x32 bf16 block (row = lane, 16-byte chunk j) with the SWIZZLE_64B
@@ -317,7 +314,7 @@ __device__ __forceinline__ void epilogue_chunk(const uint32_t (&raw)[32], const 
   };
   if constexpr (EPI == EPI_F32) {
     stage_and_store_f32(stage, raw, tmC, tl.n0 + c, tl.wslot * p.M_fixed + tl.m0 + (r & ~31), lane);
-  } else if constexpr (tma_out<EPI>()) {
+  } else {  // bf16 outputs: TMA-store (or LSU) epilogue
     const int col = tl.n0 + c;
     const int row = tl.row_off + tl.m0 + (r & ~31);
     // one 32x32 bf16 output block of this warp: TMA store from the ring, or LSU stores
@@ -373,7 +370,7 @@ __device__ __forceinline__ void epilogue_chunk(const uint32_t (&raw)[32], const 
       }
       put(v, tmC, p.c);
       put(g4, tmC2, p.c2);
-    } else {  // EPI_DGELU: acc * GeLU'(pre);  EPI_BF16_ADD: acc + old   (operand TMA-loaded)
+    } else {  // EPI_DGELU: acc * GeLU'(pre)   (operand TMA-loaded)
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         float x[8], f[8];
@@ -388,55 +385,10 @@ __device__ __forceinline__ void epilogue_chunk(const uint32_t (&raw)[32], const 
         }
         bf16x8_to_f32(pre_v[j], x);
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
-          f[u] = EPI == EPI_DGELU ? __uint_as_float(raw[8 * j + u]) * dgelu_f(x[u])
-                                  : __uint_as_float(raw[8 * j + u]) + x[u];
+        for (int u = 0; u < 8; ++u) f[u] = __uint_as_float(raw[8 * j + u]) * dgelu_f(x[u]);
         v[j] = f32x8_to_bf16(f);
       }
       put(v, tmC, p.c);
-    }
-  } else if constexpr (EPI == EPI_F32_ATOMIC) {  // split-K partial: out[m][n] += acc
-    if (tl.m0 + r < p.m_real) {
-      float* out = reinterpret_cast<float*>(p.c) + (size_t)(tl.m0 + r) * p.N + tl.n0 + c;
-#pragma unroll
-      for (int j = 0; j < 32; ++j) atomicAdd(out + j, __uint_as_float(raw[j]));
-    }
-  } else {
-    const size_t off = ((size_t)tl.row_off + tl.m0 + r) * p.N + tl.n0 + c;
-    if constexpr (EPI == EPI_BF16) {
-      __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.c) + off;
-#pragma unroll
-      for (int j = 0; j < 32; j += 8) {
-        float f[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) f[u] = __uint_as_float(raw[j + u]);
-        st_v4(out + j, f32x8_to_bf16(f));
-      }
-    } else if constexpr (EPI == EPI_GELU) {
-      __nv_bfloat16* pre = reinterpret_cast<__nv_bfloat16*>(p.c) + off;
-      __nv_bfloat16* act = reinterpret_cast<__nv_bfloat16*>(p.c2) + off;
-#pragma unroll
-      for (int j = 0; j < 32; j += 8) {
-        float f[8], g[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) f[u] = __uint_as_float(raw[j + u]);
-        const uint4 pv = f32x8_to_bf16(f);
-        bf16x8_to_f32(pv, f);  // GeLU of the bf16-rounded pre-activation, as the backward sees it
-#pragma unroll
-        for (int u = 0; u < 8; ++u) g[u] = gelu_f(f[u]);
-        st_v4(pre + j, pv);
-        st_v4(act + j, f32x8_to_bf16(g));
-      }
-    } else if constexpr (EPI == EPI_DGELU) {
-      __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.c) + off;
-#pragma unroll
-      for (int j = 0; j < 32; j += 8) {
-        float x[8], f[8];
-        bf16x8_to_f32(pre_v[j / 8], x);
-#pragma unroll
-        for (int u = 0; u < 8; ++u) f[u] = __uint_as_float(raw[j + u]) * dgelu_f(x[u]);
-        st_v4(out + j, f32x8_to_bf16(f));
-      }
     }
   }
 }
@@ -468,7 +420,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr uint32_t IDESC = make_idesc<BN_MMA, A_MN, B_MN, BM * CG>();  // pair: M = 256
   // epilogue warps: two per TMEM lane quarter (each takes half of the columns),
   // except the route epilogue which needs a whole logits row per thread
-  constexpr int EPI_WARPS = (EPI == EPI_ROUTE) ? 4 : (BN >= 128 ? 8 : 4);
+  constexpr int EPI_WARPS = BN >= 128 ? 8 : 4;
   constexpr int EPI_COLS = BN * 4 / EPI_WARPS;
 
   extern __shared__ __align__(1024) uint8_t dsmem[];
@@ -481,7 +433,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ __align__(8) uint64_t pre_bar[8];  // DGELU: per-epilogue-warp pre-activation loads
   __shared__ uint32_t tmem_base_sh;
   __shared__ SchedSmem sched;
-  __shared__ int32_t route_cnt[4][(EPI == EPI_ROUTE) ? BN : 1];
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -750,7 +701,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int it = 0, t = tile_of(0); t < total_tiles; t = tile_of(++it)) {
       if (!decode_tile<BN, CG>(t, sched, p, tl, cta_rank)) break;
       uint4 pre_r[4];  // LSU path: next operand block in registers (coalesced layout)
-      if constexpr (EPI == EPI_DGELU || EPI == EPI_BF16_ADD) {  // first operand block, in flight during the MMAs
+      if constexpr (EPI == EPI_DGELU) {  // first operand block, in flight during the MMAs
         if (p.lsu_epi) {
           if (tl.active)
             blk_load_lsu(pre_r, reinterpret_cast<const __nv_bfloat16*>(p.c), p.N, tl.n0 + col0,
@@ -775,97 +726,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       };
 
-      if constexpr (EPI == EPI_ROUTE) {
-        // one thread = one token; logits row in registers
-        const int E = p.e_real;
-        float v[BN];
-#pragma unroll
-        for (int c = 0; c < BN; c += 16) {
-          uint32_t raw[16];
-          tmem_ld_32x32b_x16(t_row + c, raw);
-          tmem_ld_wait();
-#pragma unroll
-          for (int j = 0; j < 16; ++j) v[c + j] = __uint_as_float(raw[j]);
-        }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty_bar[acc]);
-        const int token = tl.row_off + tl.m0 + r;
-        const int chunk = (tl.row_off + tl.m0) / BM;
-#pragma unroll
-        for (int e = 0; e < BN; ++e)
-          v[e] = e < E ? v[e] + (p.bias ? p.bias[e] : 0.f) : -INFINITY;
-        float mx = v[0];
-#pragma unroll
-        for (int e = 1; e < BN; ++e) mx = fmaxf(mx, v[e]);
-        float ssum = 0.f;
-        float ex[BN];
-#pragma unroll
-        for (int e = 0; e < BN; ++e) {
-          ex[e] = e < E ? expf(v[e] - mx) : 0.f;
-          ssum += ex[e];
-        }
-        const float inv = 1.f / ssum;
-        float* prow = p.probs + (size_t)token * E;
-#pragma unroll
-        for (int e = 0; e < BN; e += 4)
-          if (e < E)
-            *reinterpret_cast<float4*>(prow + e) =
-                make_float4(ex[e] * inv, ex[e + 1] * inv, ex[e + 2] * inv, ex[e + 3] * inv);
-        // top-k on logits, ties -> lowest expert index
-        uint64_t taken_lo = 0, taken_hi = 0;
-        int sel[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          sel[j] = -1;
-          if (j < p.topk) {
-            int bi = -1;
-            float best = 0.f;
-#pragma unroll
-            for (int e = 0; e < BN; ++e) {
-              const bool tk = e < 64 ? ((taken_lo >> e) & 1) : ((taken_hi >> (e - 64)) & 1);
-              if (e < E && !tk && (bi < 0 || v[e] > best)) {
-                best = v[e];
-                bi = e;
-              }
-            }
-            sel[j] = bi;
-            if (bi < 64) taken_lo |= 1ull << bi;
-            else taken_hi |= 1ull << (bi - 64);
-          }
-        }
-        // chunk ranks: pairs of expert e ordered by token inside this 128-token tile
-        int myrank[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) myrank[j] = 0;
-        const uint32_t lt_mask = (1u << lane) - 1u;
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        for (int e = 0; e < E; ++e) {
-          bool has = false;
-#pragma unroll
-          for (int j = 0; j < 8; ++j) has |= (sel[j] == e);
-          const uint32_t b = __ballot_sync(0xffffffffu, has);
-#pragma unroll
-          for (int j = 0; j < 8; ++j)
-            if (sel[j] == e) myrank[j] = __popc(b & lt_mask);
-          if (lane == 0) route_cnt[q][e] = __popc(b);
-        }
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          if (j < p.topk) {
-            const int e = sel[j];
-            int base = 0;
-            for (int qq = 0; qq < q; ++qq) base += route_cnt[qq][e];
-            p.idx[(size_t)token * p.topk + j] = e;
-            p.w[(size_t)token * p.topk + j] = ex[e] * inv;
-            p.rank[(size_t)token * p.topk + j] = base + myrank[j];
-          }
-        }
-        for (int e = r; e < E; e += 128)
-          p.chunk_counts[(size_t)chunk * E + e] =
-              route_cnt[0][e] + route_cnt[1][e] + route_cnt[2][e] + route_cnt[3][e];
-      } else {
+      {
         // software-pipelined: the TMEM read of chunk i+1 is in flight while chunk i is processed
         constexpr int NCH = EPI_COLS / 32;
         uint32_t rawA[32], rawB[32];
@@ -876,7 +737,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           uint32_t(&nxt)[32] = (i & 1) ? rawA : rawB;
           const int c = col0 + 32 * i;
           uint4 pre_v[4];
-          if constexpr (EPI == EPI_DGELU || EPI == EPI_BF16_ADD) {  // operand block (LSU or TMA, SWIZZLE_64B)
+          if constexpr (EPI == EPI_DGELU) {  // operand block (LSU or TMA, SWIZZLE_64B)
             if (tl.active && p.lsu_epi) {
               blk_rows_lsu(stage, pre_r, pre_v, lane);
               if (i + 1 < NCH)  // next block's loads overlap this chunk's math and stores
@@ -1297,49 +1158,18 @@ static int launch_route(const CUtensorMap& ta, const CUtensorMap& tb, const Gemm
 int route_gemm(const void* x, const void* wg, const float* bias, int T, int d, int E, int k,
                int32_t* idx, float* w, float* probs, int32_t* rank, int32_t* chunk_counts,
                cudaStream_t st) {
-  if (env_int("PPMOE_ROUTE_SPLITK", 1)) {
-    // d split over a cluster of KS = 2 CTAs (cfg2: KS = 1 / 2 / 4 measured 14.4-16.8 / 14.2-15.6 /
-    // 21-22 us -- 4 needs a second wave), every slice >= one BK
-    const int tiles = T / BM;
-    int KS = env_int("PPMOE_ROUTE_KS", 2);
-    const int BNr = E <= 16 ? 16 : E <= 32 ? 32 : E <= 64 ? 64 : 128;
-    if (BNr == 128 && KS > 2) KS = 2;  // smem: 4 stages + (KS-1) fp32 128 x 128 partials
-    if (KS != 1 && KS != 2 && KS != 4) KS = 2;
-    while (KS > 1 && (d / BK) % KS) KS >>= 1;
-    CUtensorMap ta, tb;
-    if (int rc = make_tmap(&ta, x, d, T, BK, BM)) return rc;
-    if (int rc = make_tmap(&tb, wg, d, E, BK, BNr)) return rc;
-    GemmParams p{};
-    p.e_real = E;
-    p.K_fixed = d;
-    p.bias = bias;
-    p.idx = idx;
-    p.w = w;
-    p.probs = probs;
-    p.rank = rank;
-    p.chunk_counts = chunk_counts;
-    p.topk = k;
-#define PP_ROUTE_KS(BN_)                                                 \
-  switch (KS) {                                                         \
-    case 4: return launch_route<BN_, 4, 4>(ta, tb, p, tiles, st);       \
-    case 2: return launch_route<BN_, 2, 4>(ta, tb, p, tiles, st);       \
-    default: return launch_route<BN_, 1, 6>(ta, tb, p, tiles, st);      \
-  }
-    switch (BNr) {
-      case 16: PP_ROUTE_KS(16)
-      case 32: PP_ROUTE_KS(32)
-      case 64: PP_ROUTE_KS(64)
-      default: PP_ROUTE_KS(128)
-    }
-#undef PP_ROUTE_KS
-  }
+  // d split over a cluster of KS = 2 CTAs (cfg2: KS = 1 / 2 / 4 measured 14.4-16.8 / 14.2-15.6 /
+  // 21-22 us -- 4 needs a second wave), every slice >= one BK
+  const int tiles = T / BM;
+  int KS = env_int("PPMOE_ROUTE_KS", 2);
   const int BNr = E <= 16 ? 16 : E <= 32 ? 32 : E <= 64 ? 64 : 128;
+  if (BNr == 128 && KS > 2) KS = 2;  // smem: 4 stages + (KS-1) fp32 128 x 128 partials
+  if (KS != 1 && KS != 2 && KS != 4) KS = 2;
+  while (KS > 1 && (d / BK) % KS) KS >>= 1;
   CUtensorMap ta, tb;
   if (int rc = make_tmap(&ta, x, d, T, BK, BM)) return rc;
   if (int rc = make_tmap(&tb, wg, d, E, BK, BNr)) return rc;
   GemmParams p{};
-  p.max_groups = 1;
-  p.single_rows = T;
   p.e_real = E;
   p.K_fixed = d;
   p.bias = bias;
@@ -1349,15 +1179,19 @@ int route_gemm(const void* x, const void* wg, const float* bias, int T, int d, i
   p.rank = rank;
   p.chunk_counts = chunk_counts;
   p.topk = k;
-  p.N = BNr;
-  const int grid = sm_count();
-  switch (BNr) {
-    case 16: return launch<16, false, false, EPI_ROUTE, 8>(ta, tb, p, grid, st);
-    case 32: return launch<32, false, false, EPI_ROUTE, 8>(ta, tb, p, grid, st);
-    case 64: return launch<64, false, false, EPI_ROUTE, 8>(ta, tb, p, grid, st);
-    case 128: return launch<128, false, false, EPI_ROUTE, 6>(ta, tb, p, grid, st);
-    default: return fail(PP_EINVAL, "route: E=%d unsupported by the tcgen05 gate", E);
+#define PP_ROUTE_KS(BN_)                                         \
+  switch (KS) {                                                 \
+    case 4: return launch_route<BN_, 4, 4>(ta, tb, p, tiles, st); \
+    case 2: return launch_route<BN_, 2, 4>(ta, tb, p, tiles, st); \
+    default: return launch_route<BN_, 1, 6>(ta, tb, p, tiles, st); \
   }
+  switch (BNr) {
+    case 16: PP_ROUTE_KS(16)
+    case 32: PP_ROUTE_KS(32)
+    case 64: PP_ROUTE_KS(64)
+    default: PP_ROUTE_KS(128)
+  }
+#undef PP_ROUTE_KS
 }
 
 // dx[T][d] = dl[T][EP] . wg[E][d]: the gate's input gradient (K = EP; wg rows >= E read
