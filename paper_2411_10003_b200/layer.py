@@ -344,7 +344,8 @@ class MoELayer(torch.nn.Module):
         # layout status (sticky bits: 1 rows > capacity, 2 replica slots, 4 groups), read
         # back asynchronously after every eager forward
         self.status = torch.zeros((1,), **i32)
-        self._status_host = torch.zeros((4,), dtype=torch.int64).pin_memory()  # status, fault words
+        self._status_host = torch.zeros((1,), dtype=torch.int32).pin_memory()
+        self._fault_host = torch.zeros((3,), dtype=torch.int64).pin_memory()  # cross-rank fault words
         self._status_ev = None
         self.pair_dest = torch.empty((T, k), **i32)
         self.pair_row = torch.empty((T, k), **i32)
@@ -558,9 +559,9 @@ class MoELayer(torch.nn.Module):
         if self.record_history:
             self.history.append(self.counts.clone())
         if not torch.cuda.is_current_stream_capturing():
-            self._status_host[0:1].copy_(self.status, non_blocking=True)
+            self._status_host.copy_(self.status, non_blocking=True)
             for i, f in enumerate(self._fault_words()[:3]):
-                self._status_host[1 + i: 2 + i].copy_(f, non_blocking=True)
+                self._fault_host[i: i + 1].copy_(f, non_blocking=True)
             self._status_ev = torch.cuda.Event()
             self._status_ev.record()
 
@@ -568,8 +569,8 @@ class MoELayer(torch.nn.Module):
         """Raise CapacityError if an earlier step's layout was dropped (non-blocking)."""
         if self._status_ev is None or torch.cuda.is_current_stream_capturing():
             return
-        if self._status_ev.query() and int(self._status_host.max()):
-            self._raise_status(int(self._status_host[0]), self._status_host[1:].tolist())
+        if self._status_ev.query() and (int(self._status_host[0]) or int(self._fault_host.max())):
+            self._raise_status(int(self._status_host[0]), self._fault_host.tolist())
 
     def _fault_words(self) -> list:
         """Device fault words of the cross-rank waits (peer barriers, replica gate): nonzero
