@@ -749,26 +749,31 @@ def main() -> None:
 
         from paper_2411_10003_b200 import calibrate
 
-        # graph-timed phases of the instrumented replays (no host launch gaps); 3 independent fits
-        # of 8 replays each (fit on 4, held-out error on 4) give the spread of the model error
-        samples = []
+        # graph-timed phases of the instrumented replays (no host launch gaps), each phase the
+        # max over ranks (the slowest rank sets the step, like max(H) in the model); 3 independent
+        # fits of 8 replays each (fit on 4, held-out error on 4) give the spread of the model error.
+        # Loads: per-GPU H / R under the slot routing rule the layout applies (pair (slot v, expert
+        # e) is computed on v's GPU if mask[v][e], else on e's home GPU) -- the GPU's GEMM time
+        # follows its rows; the virtual-slot H/R fit (the planner's units) is reported beside it
         m_ = E // world
         src = graph_calib if exposure is not None else [
             (c_, m2_, ph) for (c_, m2_), ph in zip(calib_samples, calibrate.per_step_phases(layer.phase_log))]
-        for counts_t, mask_t, ph in src:
+        mine = [calibrate.measured_costs(ph) for _, _, ph in src]
+        allc = [None] * world
+        dist.all_gather_object(allc, mine)
+        costs = [{k_: max(allc[r][i][k_] for r in range(world)) for k_ in mine[i]} for i in range(len(mine))]
+        samples, samples_v = [], []
+        for (counts_t, mask_t, _), c_ in zip(src, costs):
             counts_np = counts_t.cpu().numpy()
             mask_np = mask_t.cpu().numpy() if mask_t is not None else np.eye(E, dtype=np.uint8)
-            if layer.placement == "physical":
-                # per-device loads under the slot routing rule the layout applies: pair (slot v,
-                # expert e) is computed on v's device if mask[v][e], else on e's home device
-                dev_of_slot = np.arange(E) // m_
-                comp = np.where(mask_np.astype(bool), dev_of_slot[:, None], (np.arange(E) // m_)[None, :])
-                H = np.bincount(comp.ravel(), weights=counts_np.ravel(), minlength=world)
-                remote = comp != dev_of_slot[:, None]
-                R = np.bincount(comp[remote], weights=counts_np[remote], minlength=world)
-            else:
-                H, R = dv.derive_loads(counts_np, mask_np.astype("uint8"))  # pp_derive_loads kernel
-            samples.append((H, R, calibrate.measured_costs(ph)))
+            dev_of_slot = np.arange(E) // m_
+            comp = np.where(mask_np.astype(bool), dev_of_slot[:, None], (np.arange(E) // m_)[None, :])
+            H = np.bincount(comp.ravel(), weights=counts_np.ravel(), minlength=world)
+            remote = comp != dev_of_slot[:, None]
+            R = np.bincount(comp[remote], weights=counts_np[remote], minlength=world)
+            samples.append((H, R, c_))
+            Hv, Rv = dv.derive_loads(counts_np, mask_np.astype("uint8"))  # pp_derive_loads kernel
+            samples_v.append((Hv, Rv, c_))
         fits = [calibrate.fit(samples[8 * j:8 * j + 8], input_bytes=2 * d) for j in range(len(samples) // 8)] \
             if len(samples) >= 16 else [calibrate.fit(samples, input_bytes=2 * d)]
         calibration = dict(fits[0])
@@ -776,10 +781,17 @@ def main() -> None:
         calibration["fits"] = [{"compute_throughput": f_["compute_throughput"], "avg_bandwidth": f_["avg_bandwidth"],
                                 "mean_abs_rel_error": f_["mean_abs_rel_error"]} for f_ in fits]
         calibration["mean_abs_rel_error_spread"] = [min(errs_), max(errs_)]
-        calibration["phase_source"] = "graph replays" if exposure is not None else "eager steps"
-        calibration["note"] = ("fit of the reference model's B and t to this run's measured phases ("
-                               + ("per-device H/R" if layer.placement == "physical" else "virtual-slot H/R")
-                               + ", rank 0); plan objective uses these units")
+        calibration["phase_source"] = ("graph replays" if exposure is not None else "eager steps") + \
+            ", each phase the max over ranks"
+        fv = [calibrate.fit(samples_v[8 * j:8 * j + 8], input_bytes=2 * d) for j in range(len(samples_v) // 8)] \
+            if len(samples_v) >= 16 else [calibrate.fit(samples_v, input_bytes=2 * d)]
+        calibration["virtual_slot_fit"] = {
+            "compute_throughput": fv[0]["compute_throughput"], "avg_bandwidth": fv[0]["avg_bandwidth"],
+            "mean_abs_rel_error_spread": [min(f_["mean_abs_rel_error"] for f_ in fv),
+                                          max(f_["mean_abs_rel_error"] for f_ in fv)]}
+        calibration["note"] = ("fit of the reference model's B and t (Eq. 1-3 terms) to this run's measured phases "
+                               "with per-GPU H/R (t in pairs/s per GPU); virtual_slot_fit: the same with the "
+                               "virtual-slot H/R the planner searches over")
     layer.phase_log = None
 
     replica_traffic = None
