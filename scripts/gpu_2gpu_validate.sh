@@ -8,6 +8,6 @@ timeout 600 $R --master-port 29621 bench.py --gpus 2 --steps 20 --warmup 5 > gpu
 timeout 600 $R --master-port 29622 bench.py --gpus 2 --config cfg3 --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/r2_g13_n2_cfg3.log 2>&1; echo cfg3 $?
 timeout 900 $R --master-port 29623 bench.py --gpus 2 --config cfg5 --steps 5 --warmup 3 > gpurun_out/r2_g13_n2_cfg5.log 2>&1; echo cfg5 $?
 timeout 600 python -m torch.distributed.run --no-python --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29624 \
-   scripts/r2/ncu_rank0.sh gpurun_out/r2_ncu_nvlink_n2.csv --gpus 2 --steps 2 --warmup 3 --eager --profile-only > gpurun_out/r2_g13_ncu.log 2>&1; echo ncu $?
+   scripts/ncu_rank0.sh gpurun_out/r2_ncu_nvlink_n2.csv --gpus 2 --steps 2 --warmup 3 --eager --profile-only > gpurun_out/r2_g13_ncu.log 2>&1; echo ncu $?
 tail -2 gpurun_out/r2_g13_mgpu_tests.log
 for f in n2 n2_cfg3 n2_cfg5; do echo "== $f"; tail -c 400 gpurun_out/r2_g13_$f.log; echo; done

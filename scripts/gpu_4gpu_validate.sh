@@ -11,6 +11,6 @@ timeout 600 $R --nproc-per-node 4 --master-port 29653 bench.py --gpus 4 --config
 timeout 600 $R --nproc-per-node 4 --master-port 29654 bench.py --gpus 4 --config cfg4 --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/r2_g17_n4_cfg4.log 2>&1; echo cfg4 $?
 timeout 900 $R --nproc-per-node 4 --master-port 29655 bench.py --gpus 4 --config cfg5 --steps 5 --warmup 3 > gpurun_out/r2_g17_n4_cfg5.log 2>&1; echo cfg5 $?
 timeout 400 python -m torch.distributed.run --no-python --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29656 \
-   scripts/r2/ncu_rank0.sh gpurun_out/r2_ncu_nvlink_n2.csv scripts/nvlink_profile.py > gpurun_out/r2_g17_ncu.log 2>&1; echo ncu $?
+   scripts/ncu_rank0.sh gpurun_out/r2_ncu_nvlink_n2.csv scripts/nvlink_profile.py > gpurun_out/r2_g17_ncu.log 2>&1; echo ncu $?
 tail -2 gpurun_out/r2_g17_tests.log
 grep -c "" gpurun_out/r2_ncu_nvlink_n2.csv

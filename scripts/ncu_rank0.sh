@@ -1,7 +1,7 @@
 #!/bin/bash
 # torchrun --no-python wrapper: rank 0 runs under ncu (NVLink + DRAM bytes of the A2A / Trans / Agg
 # kernels), the other ranks run plainly.  Usage:
-#   python -m torch.distributed.run --no-python --nproc-per-node N ... scripts/r2/ncu_rank0.sh OUT.csv SCRIPT.py args...
+#   python -m torch.distributed.run --no-python --nproc-per-node N ... scripts/ncu_rank0.sh OUT.csv SCRIPT.py args...
 out=$1; shift
 if [ "$RANK" = "0" ]; then
   exec ncu --metrics gpu__time_duration.sum,nvltx__bytes.sum,nvlrx__bytes.sum,dram__bytes_read.sum,dram__bytes_write.sum \

@@ -1,5 +1,5 @@
 """ncu NVLink capture of the EP layer's A2A / Trans / Agg kernels at N ranks (run under torchrun
-with scripts/r2/ncu_rank0.sh-style wrapping of rank 0).  gloo plumbing (no NCCL under ncu), eager
+with scripts/ncu_rank0.sh-style wrapping of rank 0).  gloo plumbing (no NCCL under ncu), eager
 steps with device planning + SM-engine Trans/Agg at the cfg2 shape."""
 import os
 import sys
