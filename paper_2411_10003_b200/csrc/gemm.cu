@@ -418,8 +418,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   static_assert(NACC * BN <= 512, "TMEM holds 512 fp32 columns");
   static_assert(NSUB == 1 || CG == 2, "BN = 512 tiles are CTA-pair only");
   constexpr uint32_t IDESC = make_idesc<BN_MMA, A_MN, B_MN, BM * CG>();  // pair: M = 256
-  // epilogue warps: two per TMEM lane quarter (each takes half of the columns),
-  // except the route epilogue which needs a whole logits row per thread
+  // epilogue warps: two per TMEM lane quarter (each takes half of the columns) for BN >= 128
   constexpr int EPI_WARPS = BN >= 128 ? 8 : 4;
   constexpr int EPI_COLS = BN * 4 / EPI_WARPS;
 
