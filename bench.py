@@ -249,6 +249,54 @@ def cpu_baseline(cfg: dict, budget_s: float = 15.0) -> dict:
                       f"torch-CPU fp32 oracle (oracle/moe_ref.cpu_layer_step), {el:.1f}s"}
 
 
+def planner_at_scale(dev, alpha: float, with_cpu: bool, L: int = 12, E: int = 64, D: int = 8, T: int = 32768,
+                     k: int = 2, d: int = 2048, f: int = 4096) -> dict:
+    """K2 for all L blocks of one cfg4/cfg5 iteration in ONE launch (E = 64 virtual slots), vs the
+    CPU oracle (reference greedy_search restated, 1 core) on the same matrices; plans compared."""
+    import numpy as np
+    import torch
+
+    import paper_2411_10003_b200 as pp
+    from paper_2411_10003_b200 import _device
+    from paper_2411_10003_b200.layer import default_specs
+
+    rng = np.random.default_rng(7)
+    mats = []
+    for l_ in range(L):
+        pop = PopularityDrift(E, skew=1.2, drift=0.05, seed=100 + l_)
+        for _ in range(3):  # a few iterations into the drift
+            p_ = pop.step()
+        mats.append(np.stack([rng.multinomial(T * k // (E // D), p_) for _ in range(E)]).astype(np.int64))
+    recs = np.stack(mats)
+    cl, mo = default_specs(E, k, d, f, T * D)
+    cfg = pp.PlannerConfig(n=1, alpha=alpha, overlap_aware=True)
+    counts_dev = torch.from_numpy(recs).to(dev)
+    out = _device.PlanBuffers(L, E, dev)
+    cm, pc = _device.cost_model(cl, mo, E), _device.planner_cfg(cfg)
+    for _ in range(3):
+        _device.launch_plan(counts_dev, out, cm, pc)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(20):
+        _device.launch_plan(counts_dev, out, cm, pc)
+    e1.record()
+    torch.cuda.synchronize()
+    us = e0.elapsed_time(e1) / 20 * 1e3
+    res = {"blocks": L, "E_virtual": E, "device_us_per_iteration": us, "device_us_per_block_equiv": us / L,
+           "steps_explored_max": int(out.num_explored.max().item())}
+    if with_cpu:
+        from oracle import planner_ref as P
+
+        cmd = P.cost_model_dict(E, k, mo.input_bytes, mo.expert_param_bytes, mo.expert_grad_bytes,
+                                cl.avg_bandwidth, cl.compute_throughput, mo.fnec_time, mo.bnec_time)
+        t0 = time.perf_counter()
+        plans = [P.greedy_search(m_, cfg.n, cfg.alpha, cfg.overlap_aware, cmd) for m_ in recs]
+        res["cpu_oracle_ms_per_iteration"] = (time.perf_counter() - t0) * 1e3
+        dm = out.mask.cpu().numpy().astype(bool)
+        res["device_vs_oracle_plans_equal"] = f"{sum(int(np.array_equal(a['mask'], b)) for a, b in zip(plans, dm))}/{L}"
+    return res
+
+
 def cpu_planner_leg(recs, dev_masks, cluster, model, cfg, E: int, k: int, calib_samples, placement: str,
                     world: int) -> dict:
     """CPU baseline of the planner: the oracle restatement of reference greedy_search (pinned to
@@ -980,10 +1028,14 @@ def main() -> None:
             p1.record()
             torch.cuda.synchronize()
             phys_us = {"D": Dp, "us_per_launch": p0.elapsed_time(p1) / 20 * 1e3, "layers_per_launch": L_rec}
+        # the planner at the cfg4 / cfg5 scale, whatever this run's config: one iteration of a
+        # 12-block stack with E = 64 virtual slots (8 GPUs x 8 experts, 32K tokens/GPU, top-2), each
+        # block's LoadMatrix drawn from the reference generator's drifting Zipf(1.2) popularity
+        scale = planner_at_scale(dev, args.alpha, not args.no_cpu_baseline)
         planner_info = {"device_us_per_launch": us_launch, "layers_per_launch": L_rec,
                         "device_us_per_layer_equiv": us_launch / L_rec, "E_virtual": E,
                         "matrices": "this run's recorded LoadMatrices (one per instrumented iteration)",
-                        "physical_refine": phys_us,
+                        "physical_refine": phys_us, "at_cfg4_scale": scale,
                         "config": {"n": pcfg_.n, "alpha": pcfg_.alpha, "overlap_aware": pcfg_.overlap_aware}}
         H0 = recs[-1].sum(axis=0)
         imbalance = {"virtual_slot_H_sigma_vanilla": pm.balance_degree(H0),
