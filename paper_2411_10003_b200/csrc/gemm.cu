@@ -55,12 +55,9 @@ template <int EPI>
 constexpr int out_base() {
   return EPI == EPI_DGELU ? 2048 : 0;
 }
-// LSU = true: the epilogue's bf16 blocks go out through the LSUs (stage_and_store_lsu), so a
-// warp needs one 2 KB transpose block instead of a ring of TMA-store blocks -- the smem saved
-// buys operand stages (256 x 512 tiles: 4 instead of 3)
-template <int EPI, bool LSU = false>
+template <int EPI>
 constexpr int stage_bytes_per_warp() {
-  return EPI == EPI_F32 ? 4096 : out_base<EPI>() + (LSU ? 1 : out_bufs<EPI>()) * 2048;
+  return EPI == EPI_F32 ? 4096 : out_base<EPI>() + out_bufs<EPI>() * 2048;
 }
 
 struct GemmParams {
@@ -101,14 +98,10 @@ struct GemmParams {
   const uint64_t* gate_flags;
   const uint64_t* gate_epoch;
   int gate_me, gate_D, gate_slot0;
-  // bf16 epilogue I/O through the LSUs (st.global / ld.global via an smem transpose)
-  // instead of TMA stores / loads: the SM's TMA unit moves ~42 B/clk of loads + stores
-  // together, and the operand loads alone need more than that at the MMA rate
-  int lsu_epi;
-  int fast_gelu;   // FWD1: GeLU in packed bf16x2 arithmetic (on the bf16 pre-activation)
-  // DGRAD2: GeLU' in packed bf16x2 -- off by default: 1 - tanh^2 cancels in bf16 where the
-  // tanh saturates (dW1 error 1.1 % vs 0.3 % at 4x-scaled weights in the EP parity runs)
-  int fast_dgelu;
+  // FWD1: GeLU in packed bf16x2 arithmetic (on the bf16 pre-activation).  DGRAD2's GeLU' stays
+  // fp32: in bf16, 1 - tanh^2 cancels where the tanh saturates (measured dW1 error 1.1 % vs 0.3 %
+  // at 4x-scaled weights in the EP parity runs)
+  int fast_gelu;
   // device-adaptive SM reservation: the persistent walk leaves
   // clamp(res_per_unit * (res_stats[0] + (res_both ? res_stats[1] : 0)), res_lo, res_hi) SMs
   // to concurrent side kernels (Trans / Agg), sized by this iteration's replica volume
@@ -176,25 +169,6 @@ __device__ __forceinline__ uint32_t gelu_bf16x2(uint32_t xv) {
   return *reinterpret_cast<const uint32_t*>(&g);
 }
 
-// GeLU'(x) of two bf16 values in packed bf16x2 arithmetic (DGRAD2's epilogue)
-__device__ __forceinline__ uint32_t dgelu_bf16x2(uint32_t xv) {
-  const __nv_bfloat162 x = *reinterpret_cast<const __nv_bfloat162*>(&xv);
-  const __nv_bfloat162 c0 = __float2bfloat162_rn(0.7978845608028654f);
-  const __nv_bfloat162 c1 = __float2bfloat162_rn(0.7978845608028654f * 0.044715f);
-  const __nv_bfloat162 c3 = __float2bfloat162_rn(3.f * 0.7978845608028654f * 0.044715f);
-  const __nv_bfloat162 half = __float2bfloat162_rn(0.5f);
-  const __nv_bfloat162 one = __float2bfloat162_rn(1.f);
-  const __nv_bfloat162 x2 = __hmul2(x, x);
-  const __nv_bfloat162 u = __hmul2(x, __hfma2(x2, c1, c0));
-  uint32_t ur = *reinterpret_cast<const uint32_t*>(&u), tr;
-  asm("tanh.approx.bf16x2 %0, %1;" : "=r"(tr) : "r"(ur));
-  const __nv_bfloat162 t = *reinterpret_cast<const __nv_bfloat162*>(&tr);
-  const __nv_bfloat162 omt2 = __hfma2(__hneg2(t), t, one);   // 1 - t^2
-  const __nv_bfloat162 slope = __hfma2(x2, c3, c0);          // k0 (1 + 3 k1 x^2)
-  const __nv_bfloat162 g = __hfma2(__hmul2(__hmul2(x, half), omt2), slope, __hfma2(half, t, half));
-  return *reinterpret_cast<const uint32_t*>(&g);
-}
-
 __device__ __forceinline__ float dgelu_f(float x) {
   const float k0 = 0.7978845608028654f, k1 = 0.044715f;
   float u = k0 * (x + k1 * x * x * x);
@@ -247,42 +221,6 @@ __device__ __forceinline__ void stage_and_store(uint8_t* stage, const uint4 (&v)
   }
 }
 
-// LSU variant: the same conflict-free staging, then 4 coalesced 16-byte stores per lane
-// (each instruction writes 8 rows x 64 B) -- the SM's TMA unit stays with the operand loads
-__device__ __forceinline__ void stage_and_store_lsu(uint8_t* stage, const uint4 (&v)[4], __nv_bfloat16* out,
-                                                    int ld, int col, int row, int lane) {
-  __syncwarp();  // the previous block's reads of the staging buffer are done
-#pragma unroll
-  for (int j = 0; j < 4; ++j)
-    *reinterpret_cast<uint4*>(stage + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4)) = v[j];
-  __syncwarp();
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const int rr = q * 8 + (lane >> 2), c = lane & 3;
-    const uint4 w = *reinterpret_cast<const uint4*>(stage + rr * 64 + ((c ^ ((rr >> 1) & 3)) << 4));
-    st_v4(out + (size_t)(row + rr) * ld + col + c * 8, w);
-  }
-}
-
-// coalesced load of a 32x32 bf16 block (lane: rows q*8 + lane/4, 16-byte chunk lane%4) ...
-__device__ __forceinline__ void blk_load_lsu(uint4 (&r)[4], const __nv_bfloat16* src, int ld, int col, int row,
-                                             int lane) {
-#pragma unroll
-  for (int q = 0; q < 4; ++q) r[q] = ld_nc_v4(src + (size_t)(row + q * 8 + (lane >> 2)) * ld + col + (lane & 3) * 8);
-}
-// ... and its transpose through smem into "row = lane" order
-__device__ __forceinline__ void blk_rows_lsu(uint8_t* stage, const uint4 (&r)[4], uint4 (&out)[4], int lane) {
-  __syncwarp();
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const int rr = q * 8 + (lane >> 2), c = lane & 3;
-    *reinterpret_cast<uint4*>(stage + rr * 64 + ((c ^ ((rr >> 1) & 3)) << 4)) = r[q];
-  }
-  __syncwarp();
-#pragma unroll
-  for (int j = 0; j < 4; ++j) out[j] = *reinterpret_cast<const uint4*>(stage + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4));
-}
-
 // fp32 variant: 32 rows x 128 B, SWIZZLE_128B (16-byte chunk j of row l at j ^ (l & 7))
 __device__ __forceinline__ void stage_and_store_f32(uint8_t* stage, const uint32_t (&raw)[32],
                                                     const void* tmap, int col, int row, int lane) {
@@ -317,12 +255,9 @@ __device__ __forceinline__ void epilogue_chunk(const uint32_t (&raw)[32], const 
   } else {  // bf16 outputs: TMA-store (or LSU) epilogue
     const int col = tl.n0 + c;
     const int row = tl.row_off + tl.m0 + (r & ~31);
-    // one 32x32 bf16 output block of this warp: TMA store from the ring, or LSU stores
-    auto put = [&](const uint4 (&blk)[4], const CUtensorMap* tm, void* base) {
-      if (p.lsu_epi)
-        stage_and_store_lsu(stage + out_base<EPI>(), blk, reinterpret_cast<__nv_bfloat16*>(base), p.N, col, row, lane);
-      else
-        stage_and_store<NB - 1>(next_buf(), blk, tm, col, row, lane);
+    // one 32x32 bf16 output block of this warp: TMA store from the ring
+    auto put = [&](const uint4 (&blk)[4], const CUtensorMap* tm) {
+      stage_and_store<NB - 1>(next_buf(), blk, tm, col, row, lane);
     };
     uint4 v[4];
     if constexpr (EPI == EPI_BF16) {
@@ -349,7 +284,7 @@ __device__ __forceinline__ void epilogue_chunk(const uint32_t (&raw)[32], const 
         }
         bulk_commit();
       } else {
-        put(v, tmC, p.c);
+        put(v, tmC);
       }
     } else if constexpr (EPI == EPI_GELU) {
       uint4 g4[4];
@@ -368,32 +303,23 @@ __device__ __forceinline__ void epilogue_chunk(const uint32_t (&raw)[32], const 
         for (int u = 0; u < 8; ++u) g[u] = gelu_f(f[u]);
         g4[j] = f32x8_to_bf16(g);
       }
-      put(v, tmC, p.c);
-      put(g4, tmC2, p.c2);
+      put(v, tmC);
+      put(g4, tmC2);
     } else {  // EPI_DGELU: acc * GeLU'(pre)   (operand TMA-loaded)
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         float x[8], f[8];
-        if (EPI == EPI_DGELU && p.fast_dgelu) {  // GeLU' in packed bf16x2, product in fp32
-          const uint4 gp = make_uint4(dgelu_bf16x2(pre_v[j].x), dgelu_bf16x2(pre_v[j].y), dgelu_bf16x2(pre_v[j].z),
-                                      dgelu_bf16x2(pre_v[j].w));
-          bf16x8_to_f32(gp, x);
-#pragma unroll
-          for (int u = 0; u < 8; ++u) f[u] = __uint_as_float(raw[8 * j + u]) * x[u];
-          v[j] = f32x8_to_bf16(f);
-          continue;
-        }
         bf16x8_to_f32(pre_v[j], x);
 #pragma unroll
         for (int u = 0; u < 8; ++u) f[u] = __uint_as_float(raw[8 * j + u]) * dgelu_f(x[u]);
         v[j] = f32x8_to_bf16(f);
       }
-      put(v, tmC, p.c);
+      put(v, tmC);
     }
   }
 }
 
-template <int BN, bool A_MN, bool B_MN, int EPI, int STAGES, int CG, bool LSU = false>
+template <int BN, bool A_MN, bool B_MN, int EPI, int STAGES, int CG>
 __global__ void __launch_bounds__(kThreads, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
                         const __grid_constant__ CUtensorMap tmB,
@@ -690,7 +616,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ================= epilogue =================
     const int q = warp & 3;                  // TMEM lane quarter (hardware: warp % 4)
     const int col0 = ((warp - 4) >> 2) * EPI_COLS;  // column slice of this warp
-    uint8_t* stage = smem + STAGES * STAGE_BYTES + (warp - 4) * stage_bytes_per_warp<EPI, LSU>();
+    uint8_t* stage = smem + STAGES * STAGE_BYTES + (warp - 4) * stage_bytes_per_warp<EPI>();
     uint32_t pre_phase = 0;  // DGELU: parity of this warp's pre-activation TMA barrier
     int sbuf = 0;            // ring slot of the next staged output block
     const int r = q * 32 + lane;
@@ -699,13 +625,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     Tile tl;
     for (int it = 0, t = tile_of(0); t < total_tiles; t = tile_of(++it)) {
       if (!decode_tile<BN, CG>(t, sched, p, tl, cta_rank)) break;
-      uint4 pre_r[4];  // LSU path: next operand block in registers (coalesced layout)
       if constexpr (EPI == EPI_DGELU) {  // first operand block, in flight during the MMAs
-        if (p.lsu_epi) {
-          if (tl.active)
-            blk_load_lsu(pre_r, reinterpret_cast<const __nv_bfloat16*>(p.c), p.N, tl.n0 + col0,
-                         tl.row_off + tl.m0 + q * 32, lane);
-        } else if (lane == 0 && tl.active) {
+        if (lane == 0 && tl.active) {
           mbar_arrive_expect_tx(&pre_bar[warp - 4], 2048);
           tma_load_2d(stage, &tmC, &pre_bar[warp - 4], tl.n0 + col0, tl.row_off + tl.m0 + q * 32);
         }
@@ -726,23 +647,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       };
 
       {
-        // software-pipelined: the TMEM read of chunk i+1 is in flight while chunk i is processed
+        // software-pipelined: the TMEM read of chunk i+1 is in flight while chunk i is processed --
+        // except DGRAD2's epilogue, whose operand block already holds 16 more registers per thread:
+        // there the second buffer spilled (a TMEM read is ~12 cycles to its first use)
+        constexpr bool PIPE = EPI != EPI_DGELU;
         constexpr int NCH = EPI_COLS / 32;
         uint32_t rawA[32], rawB[32];
-        if (!zero) tmem_ld_32x32b_x32(t_row + col0, rawA);
+        if (!zero && PIPE) tmem_ld_32x32b_x32(t_row + col0, rawA);
 #pragma unroll
         for (int i = 0; i < NCH; ++i) {
-          uint32_t(&cur)[32] = (i & 1) ? rawB : rawA;
-          uint32_t(&nxt)[32] = (i & 1) ? rawA : rawB;
+          uint32_t(&cur)[32] = (PIPE && (i & 1)) ? rawB : rawA;
+          uint32_t(&nxt)[32] = (PIPE && (i & 1)) ? rawA : rawB;
           const int c = col0 + 32 * i;
           uint4 pre_v[4];
-          if constexpr (EPI == EPI_DGELU) {  // operand block (LSU or TMA, SWIZZLE_64B)
-            if (tl.active && p.lsu_epi) {
-              blk_rows_lsu(stage, pre_r, pre_v, lane);
-              if (i + 1 < NCH)  // next block's loads overlap this chunk's math and stores
-                blk_load_lsu(pre_r, reinterpret_cast<const __nv_bfloat16*>(p.c), p.N, tl.n0 + c + 32,
-                             tl.row_off + tl.m0 + q * 32, lane);
-            } else if (tl.active) {
+          if constexpr (EPI == EPI_DGELU) {  // operand block (TMA, SWIZZLE_64B)
+            if (tl.active) {
             mbar_wait(&pre_bar[warp - 4], pre_phase);
             pre_phase ^= 1;
 #pragma unroll
@@ -756,8 +675,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
           if (!zero) {
+            if (!PIPE) tmem_ld_32x32b_x32(t_row + c, cur);
             tmem_ld_wait();
-            if (i + 1 < NCH) tmem_ld_32x32b_x32(t_row + c + 32, nxt);
+            if (PIPE && i + 1 < NCH) tmem_ld_32x32b_x32(t_row + c + 32, nxt);
           } else {
 #pragma unroll
             for (int j = 0; j < 32; ++j) cur[j] = 0u;
@@ -879,12 +799,11 @@ static int make_out_tmap_f32(CUtensorMap* m, const void* ptr, uint64_t inner, ui
                    CU_TENSOR_MAP_DATA_TYPE_FLOAT32);
 }
 
-template <int BN, bool A_MN, bool B_MN, int EPI, int STAGES, int CG = 1, bool LSU = false>
+template <int BN, bool A_MN, bool B_MN, int EPI, int STAGES, int CG = 1>
 static int launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, int grid,
                   cudaStream_t st, const CUtensorMap* tc = nullptr, const CUtensorMap* tc2 = nullptr) {
-  auto kern = grouped_gemm_kernel<BN, A_MN, B_MN, EPI, STAGES, CG, LSU>;
-  const int staging = tma_out<EPI>() ? 8 * stage_bytes_per_warp<EPI, LSU>() : 0;
-  if (LSU && !p.lsu_epi) return fail(PP_EINVAL, "gemm: LSU-staged variant launched without lsu_epi");
+  auto kern = grouped_gemm_kernel<BN, A_MN, B_MN, EPI, STAGES, CG>;
+  const int staging = tma_out<EPI>() ? 8 * stage_bytes_per_warp<EPI>() : 0;
   const int smem = STAGES * (BM * BK * 2 + (BN / CG) * BK * 2) + staging + 1024;
   static CUtensorMap dummy{};
   static int configured[64] = {0};  // per device: the smem attribute is set once
@@ -917,12 +836,6 @@ static int launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams
   return PP_OK;
 }
 
-// PPMOE_GEMM_LSU_EPI=1: bf16 epilogue I/O through the LSUs instead of TMA (A/B switch; measured
-// slower: the SM's L2 port, not the TMA unit, carries loads and stores either way)
-static int lsu_epilogue() {
-  static const int on = getenv("PPMOE_GEMM_LSU_EPI") && atoi(getenv("PPMOE_GEMM_LSU_EPI")) != 0;
-  return on;
-}
 static int env_int(const char* name, int dflt) {
   const char* v = getenv(name);
   return v ? atoi(v) : dflt;
@@ -1367,10 +1280,8 @@ static int grouped_gemm_impl(int32_t mode, const void* a, const void* b, void* c
   p.max_groups = max_groups;
   p.c = c;
   p.c2 = c2;
-  p.lsu_epi = lsu_epilogue();
   // GeLU in packed bf16x2 arithmetic (FWD1 -4 % at cfg2; PPMOE_GEMM_FAST_GELU=0: fp32)
   p.fast_gelu = env_int("PPMOE_GEMM_FAST_GELU", 1);
-  p.fast_dgelu = env_int("PPMOE_GEMM_FAST_DGELU", 0);
   if (sc) {
     p.origin = sc->origin;
     p.scatter_ptrs = sc->ptrs;
@@ -1408,10 +1319,7 @@ static int grouped_gemm_impl(int32_t mode, const void* a, const void* b, void* c
       if ((rc = make_tmap(&ta, a, dm, R, BK, BM)) || (rc = make_tmap(&tb, b, dm, (uint64_t)S * df, BK, bkb))) return rc;
       p.N = df; p.K_fixed = dm;
       if ((rc = make_out_tmap(&tc, c, df, R)) || (rc = make_out_tmap(&tc2, c2, df, R))) return rc;
-      if (wide_df && env_int("PPMOE_GEMM_FWD1_WIDE", 0)) {
-        if (p.lsu_epi) return launch<512, false, false, EPI_GELU, 4, 2, true>(ta, tb, p, grid, st, &tc, &tc2);
-        return PP_LAUNCH_W(EPI_GELU, false, false, 3, &tc, &tc2);
-      }
+      if (wide_df && env_int("PPMOE_GEMM_FWD1_WIDE", 0)) return PP_LAUNCH_W(EPI_GELU, false, false, 3, &tc, &tc2);
       return PP_LAUNCH(EPI_GELU, false, false, 3, 5, &tc, &tc2);
     case PP_GEMM_FWD2:
       if ((rc = make_tmap(&ta, a, df, R, BK, BM)) ||
