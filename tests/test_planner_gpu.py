@@ -106,19 +106,31 @@ def test_reference_api_errors():
 
 
 def test_plan_for_iteration_reuse():
-    cl = pp.ClusterSpec(3, 1e9, 1000.0)
-    mo = pp.ModelSpec(3, 1, 1, 1e6, 1e5, 1e5)
-    fig8 = pp.LoadMatrix([[3, 0, 0], [2, 1, 0], [0, 1, 2]])
-    flat = pp.LoadMatrix([[1, 1, 1]] * 3)
-    hist = [fig8, flat, fig8, flat]
-    cfg = pp.PlannerConfig(n=1, alpha=0.5, reuse_interval=2)
-    assert pp.plan_for_iteration(hist, 0, cfg, cl, mo).selected == ()
-    assert pp.plan_for_iteration(hist, 1, cfg, cl, mo).selected == ()
-    assert pp.plan_for_iteration(hist, 2, cfg, cl, mo) == pp.greedy_search(flat, cfg, cl, mo)
-    assert pp.plan_for_iteration(hist, 3, cfg, cl, mo) == pp.greedy_search(flat, cfg, cl, mo)
-    assert pp.plan_for_iteration(hist, 4, cfg, cl, mo) == pp.greedy_search(flat, cfg, cl, mo)
+    """plan_for_iteration (device search) against the pinned oracle's reuse rule and search
+    (planner.py:132-156) on a drifting history whose plans differ between anchors."""
+    E = 8
+    rng = np.random.default_rng(31)
+    hist = [pp.LoadMatrix(np.stack([rng.multinomial(256, rng.dirichlet(np.ones(E) * (0.15 + 0.1 * (j % 3))))
+                                    for _ in range(E)]).astype(np.int64)) for j in range(9)]
+    cm = P.cost_model_dict(E, 1, 1e6, 1e5, 1e5, 1e9, 1000.0)
+    cl = pp.ClusterSpec(E, 1e9, 1000.0)
+    mo = pp.ModelSpec(E, 1, 1, 1e6, 1e5, 1e5)
+    for F in (1, 2, 3):
+        cfg = pp.PlannerConfig(n=1, alpha=0.5, reuse_interval=F)
+        seen = set()
+        for j in range(len(hist) + 1):
+            got = pp.plan_for_iteration(hist, j, cfg, cl, mo)
+            exp = P.plan_for_iteration([h.counts for h in hist], j, F,
+                                       lambda c: P.greedy_search(c, 1, 0.5, False, cm))
+            if exp is None:
+                assert got.selected == (), (F, j)
+            else:
+                assert list(got.selected) == list(exp["selected"]), (F, j)
+                assert got.replica_mask().tolist() == exp["mask"].tolist()
+                seen.add(tuple(exp["selected"]))
+        assert len(seen) > 1  # the history really changes the plan
     with pytest.raises(pp.ValidationError):
-        pp.plan_for_iteration(hist, 6, cfg, cl, mo)
+        pp.plan_for_iteration(hist, 20, pp.PlannerConfig(n=1, alpha=0.5, reuse_interval=2), cl, mo)
 
 
 # ---- physically-faithful E > D planner (pp_plan_physical, SURVEY 8(f) row 4) ----------
