@@ -13,7 +13,8 @@
  * Reference interfaces each entry point replaces (reference = arxiv 2411.10003
  * "moebal" package, /root/reference/pkg/src/moebal):
  *   pp_plan_greedy    <- planner.greedy_search        planner.py:80-129
- *                        (+ derive_loads core.py:255-275, cost _build perf_model.py:86-107)
+ *                        (+ derive_loads core.py:255-275, cost _build perf_model.py:86-107;
+ *                        with pp_planner_cfg.iter_counter: plan_for_iteration planner.py:132-156)
  *   pp_plan_physical  <- greedy_search generalised to E = m*D (opt-in; equals
  *                        pp_plan_greedy at m = 1; planner.py:88-90 lifts E == D)
  *   pp_derive_loads   <- core.derive_loads             core.py:255-275
@@ -27,6 +28,13 @@
  *   pp_replica_trans / pp_replica_agg / pp_replica_agg_reduce
  *                     <- Trans/Agg modelled by t_trans/t_agg perf_model.py:61-73,
  *                        split by partition_trans/agg scheduler.py:91-108
+ *   pp_gate_dx / pp_gate_dw
+ *                     <- the gate's backward (part of the BEC the reference prices as
+ *                        2x FEC, perf_model.py:49-51); no reference code
+ *   pp_top_m_mask     <- simulator._top_m_placement     simulator.py:318-324
+ *   pp_peer_barrier / pp_ipc_* / pp_device_*
+ *                     <- plumbing of the EP step (no reference counterpart: the
+ *                        reference models the exchange)
  */
 #ifndef PPMOE_H
 #define PPMOE_H
