@@ -851,6 +851,261 @@ static int sm_count() {
   return n;
 }
 
+// ---- staggered 256 x 512 tiles for the short-K, heavy-epilogue modes (FWD1, DGRAD2) ---------
+// Opt-in (PPMOE_GEMM_STAGGER=1) while it is being measured.  A 256 x 512 CTA-pair tile shares
+// each A block between its two N halves (25 % fewer operand bytes per flop than 256 x 256, the
+// bound for these modes: the SM's L2 port), but with both halves accumulating together the
+// single TMEM buffer exposes the whole epilogue.  Here the halves run L k-steps apart: half 0
+// takes A(kb) with B0(kb), half 1 takes the same A(kb) -- still in an NA-deep ring -- with B1(kb)
+// L steps later.  Each half has its own 256 TMEM columns and full/empty barriers, so the
+// epilogue drains half 0 while half 1's last L k-steps (and, across tiles, the next tile's
+// half 0 once drained) keep the tensor pipe busy.  No replica gate / fused scatter: those
+// launches use the double-buffered 256 x 256 kernel.
+template <bool B_MN, int EPI, int L, int NA, int NB>
+__global__ void __launch_bounds__(kThreads, 1)
+    grouped_gemm_stagger_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                                const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmC2,
+                                const GemmParams p) {
+  pdl_grid_sync();
+  constexpr int CG = 2, BN = 512, HALF = 256, BNC_H = HALF / CG;  // B rows (or cols) per CTA per half
+  constexpr uint32_t A_BYTES = BM * BK * 2, B_BYTES = BNC_H * BK * 2;
+  constexpr uint32_t IDESC = make_idesc<HALF, false, B_MN, BM * CG>();
+  constexpr int EPI_WARPS = 8, EPI_COLS = HALF * 4 / EPI_WARPS;  // per half: 128 columns per warp
+  static_assert(NA >= L + 2, "A must outlive the L-step lag plus one step of prefetch");
+  extern __shared__ __align__(1024) uint8_t dsmem[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsmem) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;                          // [NA][A_BYTES]
+  uint8_t* sB = sA + NA * A_BYTES;             // [2][NB][B_BYTES]
+  uint8_t* sEpi = sB + 2 * NB * B_BYTES;       // [8][stage_bytes_per_warp]
+  __shared__ __align__(8) uint64_t fullA[NA], emptyA[NA], fullB[2][NB], emptyB[2][NB];
+  __shared__ __align__(8) uint64_t tfull[2], tempty[2];
+  __shared__ __align__(8) uint64_t pre_bar[8];
+  __shared__ uint32_t tmem_base_sh;
+  __shared__ SchedSmem sched;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {  // tile table: groups in order (no gate / ragged-K in this kernel)
+    int G = *p.num_groups;
+    if (G > p.max_groups) G = p.max_groups;
+    if (G > kMaxGroups) G = kMaxGroups;
+    sched.G = G;
+    int acc = 0;
+    const int nt = p.N / BN;
+    for (int g = 0; g < G; ++g) {
+      const pp_group gr = p.groups[g];
+      sched.row_off[g] = gr.row_off;
+      sched.rows_pad[g] = gr.rows_pad;
+      sched.wslot[g] = gr.wslot;
+      sched.prefix[g] = acc;
+      acc += ((gr.rows_pad + BM * CG - 1) / (BM * CG)) * nt;
+    }
+    sched.prefix[G] = acc;
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    tma_prefetch_desc(&tmC);
+    if constexpr (EPI == EPI_GELU) tma_prefetch_desc(&tmC2);
+  }
+  const int cta_rank = (int)cluster_ctarank();
+  if (warp == 1 && lane == 0) {
+    for (int i = 0; i < NA; ++i) {
+      mbar_init(&fullA[i], 1);
+      mbar_init(&emptyA[i], 1);
+    }
+    for (int h = 0; h < 2; ++h)
+      for (int i = 0; i < NB; ++i) {
+        mbar_init(&fullB[h][i], 1);
+        mbar_init(&emptyB[h][i], 1);
+      }
+    for (int h = 0; h < 2; ++h) {
+      mbar_init(&tfull[h], 1);
+      mbar_init(&tempty[h], EPI_WARPS * CG);
+    }
+    for (int i = 0; i < 8; ++i) mbar_init(&pre_bar[i], 1);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc_2sm<512>(&tmem_base_sh);
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem_base = tmem_base_sh;
+  const int total_tiles = sched.prefix[sched.G];
+  const int G_walk = (int)gridDim.x / CG;
+  const int K = p.K_fixed / BK;
+  auto tile_of = [&](int it) -> int {
+    const int b = (int)blockIdx.x / CG;
+    return it * G_walk + b;
+  };
+  // unit sequence of one tile: slot s in [0, K + L): half 0 at k-step s (s < K), half 1 at s - L (s >= L)
+
+  if (warp == 0) {
+    if (lane == 0) {  // ===== TMA producer: loads in unit order
+      uint32_t seqA = 0, seqB[2] = {0, 0};
+      Tile tl;
+      for (int it = 0, t = tile_of(0); t < total_tiles; t = tile_of(++it)) {
+        if (!decode_tile<BN, CG>(t, sched, p, tl, cta_rank)) break;
+        auto bcol = [&](int h) { return tl.n0 + h * HALF + cta_rank * BNC_H; };
+        for (int sl = 0; sl < K + L; ++sl) {
+          for (int h = 0; h < 2; ++h) {
+            const int kb = h == 0 ? sl : sl - L;
+            if (kb < 0 || kb >= K) continue;
+            const int k0 = kb * BK;
+            if (h == 0) {  // A(kb) with B0(kb)
+              const uint32_t a = seqA % NA, pa = (seqA / NA) & 1;
+              mbar_wait(&emptyA[a], pa ^ 1);
+              if (cta_rank == 0) mbar_arrive_expect_tx(&fullA[a], A_BYTES * CG);
+              tma_load_2d_2sm(sA + a * A_BYTES, &tmA, mapa_shared(smem_u32(&fullA[a]), 0), k0, tl.row_off + tl.m0);
+              ++seqA;
+            }
+            const uint32_t b = seqB[h] % NB, pb = (seqB[h] / NB) & 1;
+            mbar_wait(&emptyB[h][b], pb ^ 1);
+            if (cta_rank == 0) mbar_arrive_expect_tx(&fullB[h][b], B_BYTES * CG);
+            uint8_t* dst = sB + (h * NB + b) * B_BYTES;
+            const uint32_t bar = mapa_shared(smem_u32(&fullB[h][b]), 0);
+            if constexpr (!B_MN) {
+              tma_load_2d_2sm(dst, &tmB, bar, k0, tl.wslot * p.N + bcol(h));
+            } else {
+#pragma unroll
+              for (int i = 0; i < BNC_H / 64; ++i)
+                tma_load_2d_2sm(dst + i * 8192, &tmB, bar, bcol(h) + 64 * i, tl.wslot * p.K_fixed + k0);
+            }
+            ++seqB[h];
+          }
+        }
+      }
+    }
+  } else if (warp == 1 && cta_rank == 0) {  // ===== MMA issuer (leader CTA)
+    uint32_t seqA = 0, seqB[2] = {0, 0}, accph[2] = {0, 0};
+    Tile tl;
+    for (int it = 0, t = tile_of(0); t < total_tiles; t = tile_of(++it)) {
+      if (!decode_tile<BN, CG>(t, sched, p, tl, cta_rank)) break;
+      const uint32_t seqA0 = seqA;  // A sequence number of this tile's k-step 0
+      for (int sl = 0; sl < K + L; ++sl) {
+        for (int h = 0; h < 2; ++h) {
+          const int kb = h == 0 ? sl : sl - L;
+          if (kb < 0 || kb >= K) continue;
+          if (kb == 0) {  // this half's accumulator must have been drained by the epilogue
+            mbar_wait(&tempty[h], accph[h] ^ 1);
+            tc_fence_after();
+          }
+          const uint32_t sa_seq = seqA0 + kb, a = sa_seq % NA;
+          if (h == 0) {
+            mbar_wait(&fullA[a], (sa_seq / NA) & 1);
+            ++seqA;
+          }
+          const uint32_t b = seqB[h] % NB;
+          mbar_wait(&fullB[h][b], (seqB[h] / NB) & 1);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint32_t saddr = smem_u32(sA + a * A_BYTES), sbaddr = smem_u32(sB + (h * NB + b) * B_BYTES);
+#pragma unroll
+            for (int kk = 0; kk < BK / 16; ++kk) {
+              const uint64_t ad = make_sdesc(saddr + kk * 32, 16, 1024);
+              const uint64_t bd = B_MN ? make_sdesc(sbaddr + kk * 2048, 8192, 1024) : make_sdesc(sbaddr + kk * 32, 16, 1024);
+              tc_mma_bf16_2sm(tmem_base + h * HALF, ad, bd, IDESC, (kb | kk) != 0);
+            }
+            tc_commit_2sm(&emptyB[h][b], 0x3);
+            if (h == 1) tc_commit_2sm(&emptyA[a], 0x3);  // both halves have consumed A(kb)
+            if (kb == K - 1) tc_commit_2sm(&tfull[h], 0x3);
+          }
+          __syncwarp();
+          ++seqB[h];
+          if (kb == K - 1) accph[h] ^= 1;
+        }
+      }
+    }
+  } else if (warp >= 4 && warp < 4 + EPI_WARPS) {  // ===== epilogue: half 0, then half 1, per tile
+    const int q = warp & 3;
+    const int col0 = ((warp - 4) >> 2) * EPI_COLS;
+    uint8_t* stage = sEpi + (warp - 4) * stage_bytes_per_warp<EPI>();
+    uint32_t pre_phase = 0, accph[2] = {0, 0};
+    int sbuf = 0;
+    const int r = q * 32 + lane;
+    Tile tl;
+    for (int it = 0, t = tile_of(0); t < total_tiles; t = tile_of(++it)) {
+      if (!decode_tile<BN, CG>(t, sched, p, tl, cta_rank)) break;
+      for (int h = 0; h < 2; ++h) {
+        const int cbase = h * HALF + col0;  // tile-relative column of this warp's first chunk
+        if constexpr (EPI == EPI_DGELU) {
+          if (lane == 0 && tl.active) {
+            mbar_arrive_expect_tx(&pre_bar[warp - 4], 2048);
+            tma_load_2d(stage, &tmC, &pre_bar[warp - 4], tl.n0 + cbase, tl.row_off + tl.m0 + q * 32);
+          }
+        }
+        mbar_wait(&tfull[h], accph[h]);
+        accph[h] ^= 1;
+        tc_fence_after();
+        const uint32_t t_row = tmem_base + ((uint32_t)(q * 32) << 16) + h * HALF;
+        const uint32_t tempty_c = mapa_shared(smem_u32(&tempty[h]), 0);
+        constexpr int NCH = EPI_COLS / 32;
+#pragma unroll 1
+        for (int i = 0; i < NCH; ++i) {
+          const int c = cbase + 32 * i;
+          uint4 pre_v[4];
+          if constexpr (EPI == EPI_DGELU) {
+            if (tl.active) {
+              mbar_wait(&pre_bar[warp - 4], pre_phase);
+              pre_phase ^= 1;
+#pragma unroll
+              for (int u = 0; u < 4; ++u)
+                pre_v[u] = *reinterpret_cast<const uint4*>(stage + lane * 64 + ((u ^ ((lane >> 1) & 3)) << 4));
+              __syncwarp();
+              if (lane == 0 && i + 1 < NCH) {
+                mbar_arrive_expect_tx(&pre_bar[warp - 4], 2048);
+                tma_load_2d(stage, &tmC, &pre_bar[warp - 4], tl.n0 + c + 32, tl.row_off + tl.m0 + q * 32);
+              }
+            }
+          }
+          uint32_t raw[32];
+          tmem_ld_32x32b_x32(t_row + col0 + 32 * i, raw);
+          tmem_ld_wait();
+          if (i + 1 == NCH) {  // every TMEM read of this half has completed: the MMA may reuse it
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(tempty_c);
+          }
+          if (tl.active) epilogue_chunk<EPI>(raw, p, tl, r, c, pre_v, stage, sbuf, &tmC, &tmC2, lane);
+        }
+      }
+    }
+  }
+  if (warp >= 4) bulk_wait0();
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 2) tmem_free_2sm<512>(tmem_base);
+}
+
+template <bool B_MN, int EPI>
+static int launch_stagger(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, int grid,
+                          cudaStream_t st, const CUtensorMap* tc, const CUtensorMap* tc2) {
+  constexpr int L = 3, NA = 5, NB = 2;
+  auto kern = grouped_gemm_stagger_kernel<B_MN, EPI, L, NA, NB>;
+  const int smem = NA * (BM * BK * 2) + 2 * NB * (128 * BK * 2) + 8 * stage_bytes_per_warp<EPI>() + 1024;
+  static int configured[64] = {0};
+  int dev = 0;
+  PP_CUDA_TRY(cudaGetDevice(&dev));
+  if (dev < 64 && !configured[dev]) {
+    PP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    configured[dev] = 1;
+  }
+  static CUtensorMap dummy{};
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((grid / 2) * 2);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  PP_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, ta, tb, tc ? *tc : dummy, tc2 ? *tc2 : dummy, p));
+  PP_LAUNCH_CHECK();
+  return PP_OK;
+}
+
 // ---- K1: the gate as a split-K cluster kernel -------------------------------------
 // One 128-token tile per cluster of KS CTAs; CTA r accumulates logits over d-slice r on
 // tcgen05 (M = 128, N = BN) and CTAs 1..KS-1 store their fp32 partials into CTA 0's smem
@@ -1320,6 +1575,8 @@ static int grouped_gemm_impl(int32_t mode, const void* a, const void* b, void* c
       p.N = df; p.K_fixed = dm;
       if ((rc = make_out_tmap(&tc, c, df, R)) || (rc = make_out_tmap(&tc2, c2, df, R))) return rc;
       if (wide_df && env_int("PPMOE_GEMM_FWD1_WIDE", 0)) return PP_LAUNCH_W(EPI_GELU, false, false, 3, &tc, &tc2);
+      if (wide_df && !gate && !sc && env_int("PPMOE_GEMM_STAGGER", 0))
+        return launch_stagger<false, EPI_GELU>(ta, tb, p, grid, st, &tc, &tc2);
       return PP_LAUNCH(EPI_GELU, false, false, 3, 5, &tc, &tc2);
     case PP_GEMM_FWD2:
       if ((rc = make_tmap(&ta, a, df, R, BK, BM)) ||
@@ -1336,6 +1593,8 @@ static int grouped_gemm_impl(int32_t mode, const void* a, const void* b, void* c
       PP_CHECK_ARG(c2 == c, "DGRAD2 runs in place: dPre must alias pre");
       if ((rc = make_out_tmap(&tc, c, df, R))) return rc;
       if (wide_df && env_int("PPMOE_GEMM_DGRAD2_WIDE", 0)) return PP_LAUNCH_W(EPI_DGELU, false, true, 3, &tc);
+      if (wide_df && !gate && env_int("PPMOE_GEMM_STAGGER", 0))
+        return launch_stagger<true, EPI_DGELU>(ta, tb, p, grid, st, &tc, nullptr);
       return PP_LAUNCH(EPI_DGELU, false, true, 3, 5, &tc);
     case PP_GEMM_DGRAD1:
       if ((rc = make_tmap(&ta, a, df, R, BK, BM)) || (rc = make_tmap(&tb, b, dm, (uint64_t)S * df, 64, BK))) return rc;

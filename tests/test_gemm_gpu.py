@@ -115,3 +115,12 @@ def test_plain_mode_large():
     for gi, (off, r) in enumerate(c["segs"]):
         s = slice(off, off + r)
         close(out[s], c["X"][s].float() @ c["W1"][gi].float().t(), what=f"plain g{gi}")
+
+
+@pytest.mark.parametrize("rows,d,f", [([2048, 1000, 4100, 0, 129], 1024, 4096), ([300, 77, 1], 256, 512)])
+def test_staggered_wide_tiles(rows, d, f, monkeypatch):
+    """PPMOE_GEMM_STAGGER=1: FWD1 / DGRAD2 on 256 x 512 tiles whose two N halves run L k-steps
+    apart (grouped_gemm_stagger_kernel) -- same results as the fp32 reference (and, for the
+    integer-exact parts of the contract, the default kernels)."""
+    monkeypatch.setenv("PPMOE_GEMM_STAGGER", "1")
+    test_fwd_bwd_modes(rows, d, f)
