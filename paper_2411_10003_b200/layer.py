@@ -784,8 +784,7 @@ class MoELayer(torch.nn.Module):
             if acc >= first_bytes:
                 rest.append((dst, src, nb))
                 continue
-            take = min(nb, first_bytes - acc)
-            take -= take % 16
+            take = nb if nb <= first_bytes - acc else (first_bytes - acc) - (first_bytes - acc) % 16
             if take > 0:
                 first.append((dst, src, take))
             if take < nb:

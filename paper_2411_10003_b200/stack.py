@@ -30,7 +30,7 @@ import torch.distributed as dist
 
 from .layer import MoELayer, Workspace, layer_plan
 from .perf_model import LayerCost
-from .scheduler import IterationTimeline, Lane, OpKind, ScheduledOp, partition_trans
+from .scheduler import IterationTimeline, Lane, OpKind, ScheduledOp, trans_byte_split
 
 
 def reserve_sms_gemm_grid(reserved: int = 4) -> int:
@@ -181,9 +181,9 @@ class MoEStack(torch.nn.Module):
         m.begin_iteration()
         if self.fnec_time is not None and fec_time is not None and m.trans_bytes() > 0:
             # bytes of Trans(i) the FNEC window of block i-1 can hide go first (SubTrans2)
-            tt = m.trans_bytes() / max(getattr(m, "trans_bw", 600e9), 1.0)
-            sub1, sub2 = partition_trans(tt, fec_time, self.fnec_time)
-            m.trans_split_bytes = int(m.trans_bytes() * (sub2 / tt)) if tt > 0 else 0
+            nbytes = m.trans_bytes()
+            _, m.trans_split_bytes = trans_byte_split(nbytes, nbytes / max(getattr(m, "trans_bw", 600e9), 1.0),
+                                                      fec_time, self.fnec_time)
         else:
             m.trans_split_bytes = None
         m.issue_trans()

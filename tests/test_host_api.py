@@ -314,3 +314,27 @@ def test_planner_cfg_struct_matches_header():
     c = _lib.PlannerCfg
     assert ctypes.sizeof(c) == 40
     assert c.reuse_interval.offset == 16 and c.max_replicas.offset == 20 and c.iter_counter.offset == 32
+
+
+def test_trans_copy_split():
+    """a9 on the copy engine: the SubTrans2 byte count cuts the Trans copy list so the
+    first part moves exactly that many bytes (16-byte granularity) and both parts together
+    cover every source byte once, in order."""
+    from paper_2411_10003_b200.layer import MoELayer
+    items = [(10_000, 90_000, 4096), (20_000, 80_000, 1000), (30_000, 70_000, 8192)]
+    total = sum(n for _, _, n in items)
+    for first_bytes in (0, 16, 4000, 4096, 4100, 5096, 9000, total, total + 64):
+        first, rest = MoELayer._split_copies(items, first_bytes)
+        moved = sum(n for _, _, n in first)
+        assert moved <= first_bytes and first_bytes - moved < 16 * len(items) + 16 or moved == total
+        cover = {}
+        for dst, src, n in first + rest:
+            assert dst - src == [d - s for d, s, m in items if s <= src < s + m][0]
+            for off in range(src, src + n, 8):
+                cover[off] = cover.get(off, 0) + 1
+        assert sum(cover.values()) * 8 == total and set(cover.values()) == {1}
+    bw = 1e9  # 13.3 us of Trans against a 5 us FNEC window
+    _, b2 = sc.trans_byte_split(total, total / bw, 1e-3, 5e-6)
+    assert b2 == round(5e-6 * bw)
+    _, b2 = sc.trans_byte_split(total, total / 600e9, 1e-3, 5e-6)  # all of it fits the window
+    assert b2 == total
