@@ -122,13 +122,16 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
 }
 
 // Wait for the phase with the given parity.  A pipeline bug must never hang the
-// GPU: after ~10 s of waiting the kernel traps (the launch fails with an error).
+// GPU: after ~30 s of waiting the kernel traps (the launch fails with an error).  The
+// bound is above the 20 s cross-rank waits (replica gate, peer barrier), which end with a
+// fault word instead: a late peer must surface as that fault, not as this trap in a warp
+// waiting on the gated producer.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t addr = smem_u32(bar);
   if (mbar_try_wait(addr, parity)) return;
   const uint64_t t0 = globaltimer_ns();
   while (!mbar_try_wait(addr, parity)) {
-    if (globaltimer_ns() - t0 > 10ull * 1000 * 1000 * 1000) {
+    if (globaltimer_ns() - t0 > 30ull * 1000 * 1000 * 1000) {
       printf("ppmoe: mbarrier wait timeout (block %d thread %d parity %u)\n", blockIdx.x,
              threadIdx.x, parity);
       __trap();
