@@ -1013,25 +1013,31 @@ def main() -> None:
         Dp = world if world > 1 else (8 if E % 8 == 0 and E >= 16 else 0)
         phys_us = None
         if Dp:
-            from paper_2411_10003_b200.layer import default_specs as _ds
+            try:
+                from paper_2411_10003_b200.layer import default_specs as _ds
 
-            cl_d, mo_d = _ds(E, k, d, f, T * world)
-            cm_d = _device.cost_model(cl_d, mo_d)
-            cm_d.num_devices = Dp
-            pc_d = _device.planner_cfg(pp.PlannerConfig(n=0, alpha=args.alpha))
-            out_d = _device.PlanBuffers(L_rec, E, dev)
-            for _ in range(3):
-                _device.launch_plan(counts_dev, out_d, cm_d, pc_d, physical_devices=Dp, refine_slots=True)
-            p0.record()
-            for _ in range(20):
-                _device.launch_plan(counts_dev, out_d, cm_d, pc_d, physical_devices=Dp, refine_slots=True)
-            p1.record()
-            torch.cuda.synchronize()
-            phys_us = {"D": Dp, "us_per_launch": p0.elapsed_time(p1) / 20 * 1e3, "layers_per_launch": L_rec}
+                cl_d, mo_d = _ds(E, k, d, f, T * world)
+                cm_d = _device.cost_model(cl_d, mo_d)
+                cm_d.num_devices = Dp
+                pc_d = _device.planner_cfg(pp.PlannerConfig(n=0, alpha=args.alpha))
+                out_d = _device.PlanBuffers(L_rec, E, dev)
+                for _ in range(3):
+                    _device.launch_plan(counts_dev, out_d, cm_d, pc_d, physical_devices=Dp, refine_slots=True)
+                p0.record()
+                for _ in range(20):
+                    _device.launch_plan(counts_dev, out_d, cm_d, pc_d, physical_devices=Dp, refine_slots=True)
+                p1.record()
+                torch.cuda.synchronize()
+                phys_us = {"D": Dp, "us_per_launch": p0.elapsed_time(p1) / 20 * 1e3, "layers_per_launch": L_rec}
+            except Exception as exc:  # evidence beside the headline
+                phys_us = {"error": f"{type(exc).__name__}: {exc}"[:300]}
         # the planner at the cfg4 / cfg5 scale, whatever this run's config: one iteration of a
         # 12-block stack with E = 64 virtual slots (8 GPUs x 8 experts, 32K tokens/GPU, top-2), each
         # block's LoadMatrix drawn from the reference generator's drifting Zipf(1.2) popularity
-        scale = planner_at_scale(dev, args.alpha, not args.no_cpu_baseline)
+        try:
+            scale = planner_at_scale(dev, args.alpha, not args.no_cpu_baseline)
+        except Exception as exc:  # evidence beside the headline: never lose the bench line to it
+            scale = {"error": f"{type(exc).__name__}: {exc}"[:300]}
         planner_info = {"device_us_per_launch": us_launch, "layers_per_launch": L_rec,
                         "device_us_per_layer_equiv": us_launch / L_rec, "E_virtual": E,
                         "matrices": "this run's recorded LoadMatrices (one per instrumented iteration)",
