@@ -319,6 +319,62 @@ __device__ __forceinline__ void epilogue_chunk(const uint32_t (&raw)[32], const 
   }
 }
 
+// Tile table of the persistent walk (thread 0): the group list (or the implicit groups of a
+// single-matrix / split-K launch) and the tile prefix.  Gated launches put the home groups first
+// (their replica tiles wait on Trans); ragged-K (wgrad) groups are sorted by K descending.
+template <int BN, int CG>
+__device__ __forceinline__ void build_schedule(const GemmParams& p, SchedSmem& sched) {
+  if (p.single_rows > 0) {
+    const int chunk = p.split_rows > 0 ? p.split_rows : p.single_rows;
+    const int G = p.single_rows / chunk;
+    const int nt = p.N / BN;
+    sched.G = G;
+    for (int g = 0; g <= G; ++g) {
+      if (g < G) {
+        sched.row_off[g] = g * chunk;
+        sched.rows_pad[g] = chunk;
+        sched.wslot[g] = g;  // split-K: partial g goes to its own output slice (EPI_F32)
+      }
+      sched.prefix[g] = g * (p.ragged_k ? (p.M_fixed / (BM * CG)) * nt : ((chunk + BM * CG - 1) / (BM * CG)) * nt);
+    }
+  } else {
+    int G = *p.num_groups;
+    if (G > p.max_groups) G = p.max_groups;
+    if (G > kMaxGroups) G = kMaxGroups;
+    sched.G = G;
+    int acc = 0;
+    const int nt = p.N / BN;
+    int next_home = 0;
+    if (p.gate_flags && !p.ragged_k)  // home groups first: the gated replica tiles go last
+      for (int g = 0; g < G; ++g) next_home += p.groups[g].wslot < p.gate_slot0;
+    int next_rep = next_home;
+    next_home = 0;
+    for (int g = 0; g < G; ++g) {
+      const pp_group gr = p.groups[g];
+      // ragged-K (wgrad): keep groups sorted by K descending so the static
+      // round-robin tile walk hands out the long tiles first (LPT balance)
+      int pos = g;
+      if (p.gate_flags && !p.ragged_k) pos = gr.wslot < p.gate_slot0 ? next_home++ : next_rep++;
+      if (p.ragged_k) {
+        while (pos > 0 && sched.rows_pad[pos - 1] < gr.rows_pad) {
+          sched.row_off[pos] = sched.row_off[pos - 1];
+          sched.rows_pad[pos] = sched.rows_pad[pos - 1];
+          sched.wslot[pos] = sched.wslot[pos - 1];
+          --pos;
+        }
+      }
+      sched.row_off[pos] = gr.row_off;
+      sched.rows_pad[pos] = gr.rows_pad;
+      sched.wslot[pos] = gr.wslot;
+    }
+    for (int g = 0; g < G; ++g) {
+      sched.prefix[g] = acc;
+      acc += p.ragged_k ? (p.M_fixed / (BM * CG)) * nt : ((sched.rows_pad[g] + BM * CG - 1) / (BM * CG)) * nt;
+    }
+    sched.prefix[G] = acc;
+  }
+}
+
 template <int BN, bool A_MN, bool B_MN, int EPI, int STAGES, int CG>
 __global__ void __launch_bounds__(kThreads, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
@@ -363,55 +419,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int lane = threadIdx.x & 31;
 
   // ---- schedule: copy the group table, build the tile prefix -------------
-  if (threadIdx.x == 0 && p.single_rows > 0) {
-    const int chunk = p.split_rows > 0 ? p.split_rows : p.single_rows;
-    const int G = p.single_rows / chunk;
-    const int nt = p.N / BN;
-    sched.G = G;
-    for (int g = 0; g <= G; ++g) {
-      if (g < G) {
-        sched.row_off[g] = g * chunk;
-        sched.rows_pad[g] = chunk;
-        sched.wslot[g] = g;  // split-K: partial g goes to its own output slice (EPI_F32)
-      }
-      sched.prefix[g] = g * (p.ragged_k ? (p.M_fixed / (BM * CG)) * nt : ((chunk + BM * CG - 1) / (BM * CG)) * nt);
-    }
-  } else if (threadIdx.x == 0) {
-    int G = *p.num_groups;
-    if (G > p.max_groups) G = p.max_groups;
-    if (G > kMaxGroups) G = kMaxGroups;
-    sched.G = G;
-    int acc = 0;
-    const int nt = p.N / BN;
-    int next_home = 0;
-    if (p.gate_flags && !p.ragged_k)  // home groups first: the gated replica tiles go last
-      for (int g = 0; g < G; ++g) next_home += p.groups[g].wslot < p.gate_slot0;
-    int next_rep = next_home;
-    next_home = 0;
-    for (int g = 0; g < G; ++g) {
-      const pp_group gr = p.groups[g];
-      // ragged-K (wgrad): keep groups sorted by K descending so the static
-      // round-robin tile walk hands out the long tiles first (LPT balance)
-      int pos = g;
-      if (p.gate_flags && !p.ragged_k) pos = gr.wslot < p.gate_slot0 ? next_home++ : next_rep++;
-      if (p.ragged_k) {
-        while (pos > 0 && sched.rows_pad[pos - 1] < gr.rows_pad) {
-          sched.row_off[pos] = sched.row_off[pos - 1];
-          sched.rows_pad[pos] = sched.rows_pad[pos - 1];
-          sched.wslot[pos] = sched.wslot[pos - 1];
-          --pos;
-        }
-      }
-      sched.row_off[pos] = gr.row_off;
-      sched.rows_pad[pos] = gr.rows_pad;
-      sched.wslot[pos] = gr.wslot;
-    }
-    for (int g = 0; g < G; ++g) {
-      sched.prefix[g] = acc;
-      acc += p.ragged_k ? (p.M_fixed / (BM * CG)) * nt : ((sched.rows_pad[g] + BM * CG - 1) / (BM * CG)) * nt;
-    }
-    sched.prefix[G] = acc;
-  }
+  if (threadIdx.x == 0) build_schedule<BN, CG>(p, sched);
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
@@ -851,17 +859,18 @@ static int sm_count() {
   return n;
 }
 
-// ---- staggered 256 x 512 tiles for the short-K, heavy-epilogue modes (FWD1, DGRAD2) ---------
-// Opt-in (PPMOE_GEMM_STAGGER=1) while it is being measured.  A 256 x 512 CTA-pair tile shares
-// each A block between its two N halves (25 % fewer operand bytes per flop than 256 x 256, the
-// bound for these modes: the SM's L2 port), but with both halves accumulating together the
-// single TMEM buffer exposes the whole epilogue.  Here the halves run L k-steps apart: half 0
-// takes A(kb) with B0(kb), half 1 takes the same A(kb) -- still in an NA-deep ring -- with B1(kb)
-// L steps later.  Each half has its own 256 TMEM columns and full/empty barriers, so the
-// epilogue drains half 0 while half 1's last L k-steps (and, across tiles, the next tile's
-// half 0 once drained) keep the tensor pipe busy.  No replica gate / fused scatter: those
-// launches use the double-buffered 256 x 256 kernel.
-template <bool B_MN, int EPI, int L, int NA, int NB>
+// ---- staggered 256 x 512 tiles ---------------------------------------------------------------
+// Opt-in while it is being measured: PPMOE_GEMM_STAGGER=1 (FWD1, DGRAD2: short K, heavy
+// epilogues), PPMOE_GEMM_STAGGER_WGRAD=1 (WGRAD1/2: ragged K, fp32 epilogue).  A 256 x 512
+// CTA-pair tile shares each A block between its two N halves (25 % fewer operand bytes per flop
+// than 256 x 256, the bound for these modes: the SM's L2 port), but with both halves
+// accumulating together the single TMEM buffer exposes the whole epilogue.  Here the halves
+// run L k-steps apart: half 0 takes A(kb) with B0(kb), half 1 takes the same A(kb) -- still in
+// an NA-deep ring -- with B1(kb) L steps later.  Each half has its own 256 TMEM columns and
+// full/empty barriers, so the epilogue drains half 0 while half 1's last L k-steps (and, across
+// tiles, the next tile's half 0 once drained) keep the tensor pipe busy.  No replica gate / SM
+// reservation / fused scatter: those launches use the double-buffered 256 x 256 kernel.
+template <bool A_MN, bool B_MN, int EPI, int L, int NA, int NB>
 __global__ void __launch_bounds__(kThreads, 1)
     grouped_gemm_stagger_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                                 const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmC2,
@@ -869,7 +878,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   pdl_grid_sync();
   constexpr int CG = 2, BN = 512, HALF = 256, BNC_H = HALF / CG;  // B rows (or cols) per CTA per half
   constexpr uint32_t A_BYTES = BM * BK * 2, B_BYTES = BNC_H * BK * 2;
-  constexpr uint32_t IDESC = make_idesc<HALF, false, B_MN, BM * CG>();
+  constexpr uint32_t IDESC = make_idesc<HALF, A_MN, B_MN, BM * CG>();
   constexpr int EPI_WARPS = 8, EPI_COLS = HALF * 4 / EPI_WARPS;  // per half: 128 columns per warp
   static_assert(NA >= L + 2, "A must outlive the L-step lag plus one step of prefetch");
   extern __shared__ __align__(1024) uint8_t dsmem[];
@@ -883,23 +892,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ uint32_t tmem_base_sh;
   __shared__ SchedSmem sched;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) {  // tile table: groups in order (no gate / ragged-K in this kernel)
-    int G = *p.num_groups;
-    if (G > p.max_groups) G = p.max_groups;
-    if (G > kMaxGroups) G = kMaxGroups;
-    sched.G = G;
-    int acc = 0;
-    const int nt = p.N / BN;
-    for (int g = 0; g < G; ++g) {
-      const pp_group gr = p.groups[g];
-      sched.row_off[g] = gr.row_off;
-      sched.rows_pad[g] = gr.rows_pad;
-      sched.wslot[g] = gr.wslot;
-      sched.prefix[g] = acc;
-      acc += ((gr.rows_pad + BM * CG - 1) / (BM * CG)) * nt;
-    }
-    sched.prefix[G] = acc;
-  }
+  if (threadIdx.x == 0) build_schedule<BN, CG>(p, sched);
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
@@ -931,12 +924,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem_base = tmem_base_sh;
   const int total_tiles = sched.prefix[sched.G];
   const int G_walk = (int)gridDim.x / CG;
-  const int K = p.K_fixed / BK;
+  const bool snake = p.ragged_k != 0;  // wgrad: LPT-sorted groups dealt in snake order
   auto tile_of = [&](int it) -> int {
     const int b = (int)blockIdx.x / CG;
-    return it * G_walk + b;
+    return it * G_walk + ((snake && (it & 1)) ? (G_walk - 1 - b) : b);
   };
-  // unit sequence of one tile: slot s in [0, K + L): half 0 at k-step s (s < K), half 1 at s - L (s >= L)
+  // unit sequence of one tile (K = its k-steps): slot s in [0, K + L): half 0 at k-step s (s < K),
+  // half 1 at s - L (s >= L)
 
   if (warp == 0) {
     if (lane == 0) {  // ===== TMA producer: loads in unit order
@@ -944,8 +938,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       Tile tl;
       for (int it = 0, t = tile_of(0); t < total_tiles; t = tile_of(++it)) {
         if (!decode_tile<BN, CG>(t, sched, p, tl, cta_rank)) break;
+        const int K = tl.num_kb;
         auto bcol = [&](int h) { return tl.n0 + h * HALF + cta_rank * BNC_H; };
-        for (int sl = 0; sl < K + L; ++sl) {
+        for (int sl = 0; K > 0 && sl < K + L; ++sl) {
           for (int h = 0; h < 2; ++h) {
             const int kb = h == 0 ? sl : sl - L;
             if (kb < 0 || kb >= K) continue;
@@ -954,7 +949,14 @@ __global__ void __launch_bounds__(kThreads, 1)
               const uint32_t a = seqA % NA, pa = (seqA / NA) & 1;
               mbar_wait(&emptyA[a], pa ^ 1);
               if (cta_rank == 0) mbar_arrive_expect_tx(&fullA[a], A_BYTES * CG);
-              tma_load_2d_2sm(sA + a * A_BYTES, &tmA, mapa_shared(smem_u32(&fullA[a]), 0), k0, tl.row_off + tl.m0);
+              const uint32_t bar = mapa_shared(smem_u32(&fullA[a]), 0);
+              if constexpr (!A_MN) {
+                tma_load_2d_2sm(sA + a * A_BYTES, &tmA, bar, k0, tl.row_off + tl.m0);
+              } else {  // wgrad: A = the group's token rows, MN-major
+#pragma unroll
+                for (int i = 0; i < BM / 64; ++i)
+                  tma_load_2d_2sm(sA + a * A_BYTES + i * 8192, &tmA, bar, tl.m0 + 64 * i, tl.row_off + k0);
+              }
               ++seqA;
             }
             const uint32_t b = seqB[h] % NB, pb = (seqB[h] / NB) & 1;
@@ -965,9 +967,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             if constexpr (!B_MN) {
               tma_load_2d_2sm(dst, &tmB, bar, k0, tl.wslot * p.N + bcol(h));
             } else {
+              const int brow = p.ragged_k ? tl.row_off + k0 : tl.wslot * p.K_fixed + k0;
 #pragma unroll
-              for (int i = 0; i < BNC_H / 64; ++i)
-                tma_load_2d_2sm(dst + i * 8192, &tmB, bar, bcol(h) + 64 * i, tl.wslot * p.K_fixed + k0);
+              for (int i = 0; i < BNC_H / 64; ++i) tma_load_2d_2sm(dst + i * 8192, &tmB, bar, bcol(h) + 64 * i, brow);
             }
             ++seqB[h];
           }
@@ -979,6 +981,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     Tile tl;
     for (int it = 0, t = tile_of(0); t < total_tiles; t = tile_of(++it)) {
       if (!decode_tile<BN, CG>(t, sched, p, tl, cta_rank)) break;
+      const int K = tl.num_kb;
+      if (K == 0) {  // empty wgrad group: no MMAs, the epilogues write zeros
+        for (int h = 0; h < 2; ++h) {
+          mbar_wait(&tempty[h], accph[h] ^ 1);
+          if (lane == 0) {
+            mbar_arrive(&tfull[h]);
+            mbar_arrive_cluster(mapa_shared(smem_u32(&tfull[h]), 1));
+          }
+          __syncwarp();
+          accph[h] ^= 1;
+        }
+        continue;
+      }
       const uint32_t seqA0 = seqA;  // A sequence number of this tile's k-step 0
       for (int sl = 0; sl < K + L; ++sl) {
         for (int h = 0; h < 2; ++h) {
@@ -1000,7 +1015,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t saddr = smem_u32(sA + a * A_BYTES), sbaddr = smem_u32(sB + (h * NB + b) * B_BYTES);
 #pragma unroll
             for (int kk = 0; kk < BK / 16; ++kk) {
-              const uint64_t ad = make_sdesc(saddr + kk * 32, 16, 1024);
+              const uint64_t ad = A_MN ? make_sdesc(saddr + kk * 2048, 8192, 1024) : make_sdesc(saddr + kk * 32, 16, 1024);
               const uint64_t bd = B_MN ? make_sdesc(sbaddr + kk * 2048, 8192, 1024) : make_sdesc(sbaddr + kk * 32, 16, 1024);
               tc_mma_bf16_2sm(tmem_base + h * HALF, ad, bd, IDESC, (kb | kk) != 0);
             }
@@ -1024,6 +1039,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     Tile tl;
     for (int it = 0, t = tile_of(0); t < total_tiles; t = tile_of(++it)) {
       if (!decode_tile<BN, CG>(t, sched, p, tl, cta_rank)) break;
+      const bool zero = tl.num_kb == 0;
       for (int h = 0; h < 2; ++h) {
         const int cbase = h * HALF + col0;  // tile-relative column of this warp's first chunk
         if constexpr (EPI == EPI_DGELU) {
@@ -1057,8 +1073,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
           uint32_t raw[32];
-          tmem_ld_32x32b_x32(t_row + col0 + 32 * i, raw);
-          tmem_ld_wait();
+          if (!zero) {
+            tmem_ld_32x32b_x32(t_row + col0 + 32 * i, raw);
+            tmem_ld_wait();
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) raw[j] = 0u;
+          }
           if (i + 1 == NCH) {  // every TMEM read of this half has completed: the MMA may reuse it
             tc_fence_before();
             __syncwarp();
@@ -1075,11 +1096,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 2) tmem_free_2sm<512>(tmem_base);
 }
 
-template <bool B_MN, int EPI>
+template <bool A_MN, bool B_MN, int EPI>
 static int launch_stagger(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, int grid,
                           cudaStream_t st, const CUtensorMap* tc, const CUtensorMap* tc2) {
   constexpr int L = 3, NA = 5, NB = 2;
-  auto kern = grouped_gemm_stagger_kernel<B_MN, EPI, L, NA, NB>;
+  auto kern = grouped_gemm_stagger_kernel<A_MN, B_MN, EPI, L, NA, NB>;
   const int smem = NA * (BM * BK * 2) + 2 * NB * (128 * BK * 2) + 8 * stage_bytes_per_warp<EPI>() + 1024;
   static int configured[64] = {0};
   int dev = 0;
@@ -1235,23 +1256,29 @@ __global__ void __launch_bounds__(kRouteThreads)
       if (e < E)
         *reinterpret_cast<float4*>(prow + e) = make_float4(ex[e] * inv, ex[e + 1] * inv, ex[e + 2] * inv, ex[e + 3] * inv);
     // top-k on logits, ties -> lowest expert index
+    // (the weight of a pick is captured with it: indexing ex[] by a runtime expert id would put
+    // the array in local memory)
     uint64_t taken_lo = 0, taken_hi = 0;
     int sel[8];
+    float wsel[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       sel[j] = -1;
+      wsel[j] = 0.f;
       if (j < p.topk) {
         int bi = -1;
-        float best = 0.f;
+        float best = 0.f, bex = 0.f;
 #pragma unroll
         for (int e = 0; e < BN; ++e) {
           const bool tk = e < 64 ? ((taken_lo >> e) & 1) : ((taken_hi >> (e - 64)) & 1);
           if (e < E && !tk && (bi < 0 || v[e] > best)) {
             best = v[e];
+            bex = ex[e];
             bi = e;
           }
         }
         sel[j] = bi;
+        wsel[j] = bex * inv;
         if (bi < 64) taken_lo |= 1ull << bi;
         else taken_hi |= 1ull << (bi - 64);
       }
@@ -1279,7 +1306,7 @@ __global__ void __launch_bounds__(kRouteThreads)
         int base = 0;
         for (int qq = 0; qq < q; ++qq) base += route_cnt[qq][e];
         p.idx[(size_t)token * p.topk + j] = e;
-        p.w[(size_t)token * p.topk + j] = ex[e] * inv;
+        p.w[(size_t)token * p.topk + j] = wsel[j];
         p.rank[(size_t)token * p.topk + j] = base + myrank[j];
       }
     }
@@ -1576,7 +1603,7 @@ static int grouped_gemm_impl(int32_t mode, const void* a, const void* b, void* c
       if ((rc = make_out_tmap(&tc, c, df, R)) || (rc = make_out_tmap(&tc2, c2, df, R))) return rc;
       if (wide_df && env_int("PPMOE_GEMM_FWD1_WIDE", 0)) return PP_LAUNCH_W(EPI_GELU, false, false, 3, &tc, &tc2);
       if (wide_df && !gate && !sc && env_int("PPMOE_GEMM_STAGGER", 0))
-        return launch_stagger<false, EPI_GELU>(ta, tb, p, grid, st, &tc, &tc2);
+        return launch_stagger<false, false, EPI_GELU>(ta, tb, p, grid, st, &tc, &tc2);
       return PP_LAUNCH(EPI_GELU, false, false, 3, 5, &tc, &tc2);
     case PP_GEMM_FWD2:
       if ((rc = make_tmap(&ta, a, df, R, BK, BM)) ||
@@ -1594,7 +1621,7 @@ static int grouped_gemm_impl(int32_t mode, const void* a, const void* b, void* c
       if ((rc = make_out_tmap(&tc, c, df, R))) return rc;
       if (wide_df && env_int("PPMOE_GEMM_DGRAD2_WIDE", 0)) return PP_LAUNCH_W(EPI_DGELU, false, true, 3, &tc);
       if (wide_df && !gate && env_int("PPMOE_GEMM_STAGGER", 0))
-        return launch_stagger<true, EPI_DGELU>(ta, tb, p, grid, st, &tc, nullptr);
+        return launch_stagger<false, true, EPI_DGELU>(ta, tb, p, grid, st, &tc, nullptr);
       return PP_LAUNCH(EPI_DGELU, false, true, 3, 5, &tc);
     case PP_GEMM_DGRAD1:
       if ((rc = make_tmap(&ta, a, df, R, BK, BM)) || (rc = make_tmap(&tb, b, dm, (uint64_t)S * df, 64, BK))) return rc;
@@ -1606,12 +1633,16 @@ static int grouped_gemm_impl(int32_t mode, const void* a, const void* b, void* c
       if ((rc = make_tmap(&ta, a, dm, R, 64, BK)) || (rc = make_tmap(&tb, b, df, R, 64, BK))) return rc;
       p.M_fixed = dm; p.N = df; p.ragged_k = 1;
       if ((rc = make_out_tmap_f32(&tc, c, df, (uint64_t)S * dm))) return rc;
+      if (wide_df && !gate && env_int("PPMOE_GEMM_STAGGER_WGRAD", 0))
+        return launch_stagger<true, true, EPI_F32>(ta, tb, p, grid, st, &tc, nullptr);
       if (wide_df) return PP_LAUNCH_W(EPI_F32, true, true, 3, &tc);
       return PP_LAUNCH(EPI_F32, true, true, 3, 5, &tc);
     case PP_GEMM_WGRAD1:
       if ((rc = make_tmap(&ta, a, df, R, 64, BK)) || (rc = make_tmap(&tb, b, dm, R, 64, BK))) return rc;
       p.M_fixed = df; p.N = dm; p.ragged_k = 1;
       if ((rc = make_out_tmap_f32(&tc, c, dm, (uint64_t)S * df))) return rc;
+      if (wide_dm && !gate && env_int("PPMOE_GEMM_STAGGER_WGRAD", 0))
+        return launch_stagger<true, true, EPI_F32>(ta, tb, p, grid, st, &tc, nullptr);
       if (wide_dm) return PP_LAUNCH_W(EPI_F32, true, true, 3, &tc);
       return PP_LAUNCH(EPI_F32, true, true, 3, 5, &tc);
     case PP_GEMM_PLAIN:
