@@ -338,3 +338,23 @@ def test_trans_copy_split():
     assert b2 == round(5e-6 * bw)
     _, b2 = sc.trans_byte_split(total, total / 600e9, 1e-3, 5e-6)  # all of it fits the window
     assert b2 == total
+
+
+def test_calibration_fits_total_expert_compute():
+    """t is fitted to FEC + BEC (= 3 maxH / t in the model): with a measured BEC/FEC ratio of 2.4
+    instead of the model's 2, the layer prediction stays exact and the ratio is reported."""
+    from paper_2411_10003_b200 import calibrate
+
+    t_true, B_true, ib = 5e7, 4e11, 2048.0
+    rng = np.random.default_rng(1)
+    samples = []
+    for _ in range(8):
+        H = rng.integers(20000, 40000, size=4)
+        R = rng.integers(5000, 15000, size=4)
+        fec = H.max() / t_true
+        a2a = R.max() * ib / B_true
+        samples.append((H, R, {"a2a_total": 4 * a2a, "fec": fec, "bec": 2.4 * fec, "layer": 4 * a2a + 3.4 * fec}))
+    fit = calibrate.fit(samples, input_bytes=ib)
+    assert abs(fit["compute_throughput"] / (t_true * 3 / 3.4) - 1) < 1e-9
+    assert fit["mean_abs_rel_error"] < 1e-9
+    assert abs(fit["bec_over_fec_measured"] - 2.4) < 1e-9
