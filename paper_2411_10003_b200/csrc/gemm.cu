@@ -1096,10 +1096,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 2) tmem_free_2sm<512>(tmem_base);
 }
 
-template <bool A_MN, bool B_MN, int EPI>
-static int launch_stagger(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, int grid,
-                          cudaStream_t st, const CUtensorMap* tc, const CUtensorMap* tc2) {
-  constexpr int L = 3, NA = 5, NB = 2;
+template <bool A_MN, bool B_MN, int EPI, int L, int NA, int NB>
+static int launch_stagger_v(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, int grid,
+                            cudaStream_t st, const CUtensorMap* tc, const CUtensorMap* tc2) {
   auto kern = grouped_gemm_stagger_kernel<A_MN, B_MN, EPI, L, NA, NB>;
   const int smem = NA * (BM * BK * 2) + 2 * NB * (128 * BK * 2) + 8 * stage_bytes_per_warp<EPI>() + 1024;
   static int configured[64] = {0};
@@ -1125,6 +1124,17 @@ static int launch_stagger(const CUtensorMap& ta, const CUtensorMap& tb, const Ge
   PP_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, ta, tb, tc ? *tc : dummy, tc2 ? *tc2 : dummy, p));
   PP_LAUNCH_CHECK();
   return PP_OK;
+}
+
+// variant = the knob's value: 1 -> (L, NA, NB) = (3, 5, 2), 2 -> (2, 4, 3), 3 -> (4, 6, 2); the
+// lag L sets how much of a half's epilogue the other half's MMAs cover, NA >= L + 2 the A ring,
+// NB the per-half B ring (smem: NA * 16 KB + 2 * NB * 16 KB + the epilogue staging)
+template <bool A_MN, bool B_MN, int EPI>
+static int launch_stagger(int variant, const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p,
+                          int grid, cudaStream_t st, const CUtensorMap* tc, const CUtensorMap* tc2) {
+  if (variant == 2) return launch_stagger_v<A_MN, B_MN, EPI, 2, 4, 3>(ta, tb, p, grid, st, tc, tc2);
+  if (variant == 3) return launch_stagger_v<A_MN, B_MN, EPI, 4, 6, 2>(ta, tb, p, grid, st, tc, tc2);
+  return launch_stagger_v<A_MN, B_MN, EPI, 3, 5, 2>(ta, tb, p, grid, st, tc, tc2);
 }
 
 // ---- K1: the gate as a split-K cluster kernel -------------------------------------
@@ -1603,7 +1613,7 @@ static int grouped_gemm_impl(int32_t mode, const void* a, const void* b, void* c
       if ((rc = make_out_tmap(&tc, c, df, R)) || (rc = make_out_tmap(&tc2, c2, df, R))) return rc;
       if (wide_df && env_int("PPMOE_GEMM_FWD1_WIDE", 0)) return PP_LAUNCH_W(EPI_GELU, false, false, 3, &tc, &tc2);
       if (wide_df && !gate && !sc && env_int("PPMOE_GEMM_STAGGER", 0))
-        return launch_stagger<false, false, EPI_GELU>(ta, tb, p, grid, st, &tc, &tc2);
+        return launch_stagger<false, false, EPI_GELU>(env_int("PPMOE_GEMM_STAGGER", 0), ta, tb, p, grid, st, &tc, &tc2);
       return PP_LAUNCH(EPI_GELU, false, false, 3, 5, &tc, &tc2);
     case PP_GEMM_FWD2:
       if ((rc = make_tmap(&ta, a, df, R, BK, BM)) ||
@@ -1621,7 +1631,7 @@ static int grouped_gemm_impl(int32_t mode, const void* a, const void* b, void* c
       if ((rc = make_out_tmap(&tc, c, df, R))) return rc;
       if (wide_df && env_int("PPMOE_GEMM_DGRAD2_WIDE", 0)) return PP_LAUNCH_W(EPI_DGELU, false, true, 3, &tc);
       if (wide_df && !gate && env_int("PPMOE_GEMM_STAGGER", 0))
-        return launch_stagger<false, true, EPI_DGELU>(ta, tb, p, grid, st, &tc, nullptr);
+        return launch_stagger<false, true, EPI_DGELU>(env_int("PPMOE_GEMM_STAGGER", 0), ta, tb, p, grid, st, &tc, nullptr);
       return PP_LAUNCH(EPI_DGELU, false, true, 3, 5, &tc);
     case PP_GEMM_DGRAD1:
       if ((rc = make_tmap(&ta, a, df, R, BK, BM)) || (rc = make_tmap(&tb, b, dm, (uint64_t)S * df, 64, BK))) return rc;
@@ -1634,7 +1644,7 @@ static int grouped_gemm_impl(int32_t mode, const void* a, const void* b, void* c
       p.M_fixed = dm; p.N = df; p.ragged_k = 1;
       if ((rc = make_out_tmap_f32(&tc, c, df, (uint64_t)S * dm))) return rc;
       if (wide_df && !gate && env_int("PPMOE_GEMM_STAGGER_WGRAD", 0))
-        return launch_stagger<true, true, EPI_F32>(ta, tb, p, grid, st, &tc, nullptr);
+        return launch_stagger<true, true, EPI_F32>(env_int("PPMOE_GEMM_STAGGER_WGRAD", 0), ta, tb, p, grid, st, &tc, nullptr);
       if (wide_df) return PP_LAUNCH_W(EPI_F32, true, true, 3, &tc);
       return PP_LAUNCH(EPI_F32, true, true, 3, 5, &tc);
     case PP_GEMM_WGRAD1:
@@ -1642,7 +1652,7 @@ static int grouped_gemm_impl(int32_t mode, const void* a, const void* b, void* c
       p.M_fixed = df; p.N = dm; p.ragged_k = 1;
       if ((rc = make_out_tmap_f32(&tc, c, dm, (uint64_t)S * df))) return rc;
       if (wide_dm && !gate && env_int("PPMOE_GEMM_STAGGER_WGRAD", 0))
-        return launch_stagger<true, true, EPI_F32>(ta, tb, p, grid, st, &tc, nullptr);
+        return launch_stagger<true, true, EPI_F32>(env_int("PPMOE_GEMM_STAGGER_WGRAD", 0), ta, tb, p, grid, st, &tc, nullptr);
       if (wide_dm) return PP_LAUNCH_W(EPI_F32, true, true, 3, &tc);
       return PP_LAUNCH(EPI_F32, true, true, 3, 5, &tc);
     case PP_GEMM_PLAIN:

@@ -7,12 +7,12 @@ timeout 2400 python -m pytest tests -q -m gpu --timeout 900 > gpurun_out/v1_test
 timeout 300 python bench.py > gpurun_out/v1_bench.log 2>&1; echo bench $?
 timeout 300 python bench.py --impl reference --steps 5 --warmup 3 > gpurun_out/v1_ref.log 2>&1; echo ref $?
 timeout 300 python scripts/gemm_bench.py > gpurun_out/v1_gemm.log 2>&1; echo gemm $?
-PPMOE_GEMM_STAGGER=1 PPMOE_GEMM_STAGGER_WGRAD=1 timeout 300 python scripts/gemm_bench.py FWD1 DGRAD2 WGRAD2 WGRAD1 > gpurun_out/v1_gemm_stagger.log 2>&1; echo gemm_stagger $?
+for v in 1 2 3; do PPMOE_GEMM_STAGGER=$v PPMOE_GEMM_STAGGER_WGRAD=$v timeout 300 python scripts/gemm_bench.py FWD1 DGRAD2 WGRAD2 WGRAD1 > gpurun_out/v1_gemm_stagger$v.log 2>&1; echo gemm_stagger$v $?; done
 PPMOE_GEMM_STAGGER=1 PPMOE_GEMM_STAGGER_WGRAD=1 timeout 300 python bench.py --no-cpu-baseline > gpurun_out/v1_bench_stagger.log 2>&1; echo bench_stagger $?
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/v1_launches.csv \
    python bench.py --steps 2 --warmup 3 --profile-only > /dev/null 2>&1; echo ncu $?
 tail -3 gpurun_out/v1_tests.log; tail -1 gpurun_out/v1_smoke.log; head -c 300 gpurun_out/v1_bench.log; echo
-cat gpurun_out/v1_gemm.log gpurun_out/v1_gemm_stagger.log
+for f in gpurun_out/v1_gemm.log gpurun_out/v1_gemm_stagger*.log; do echo == $f; cat $f; done
 python - <<'PY'
 import json
 for f in ("gpurun_out/v1_bench.log", "gpurun_out/v1_bench_stagger.log"):

@@ -119,17 +119,21 @@ def test_plain_mode_large():
         close(out[s], c["X"][s].float() @ c["W1"][gi].float().t(), what=f"plain g{gi}")
 
 
-@pytest.mark.parametrize("rows,d,f", [([2048, 1000, 4100, 0, 129], 1024, 4096), ([300, 77, 1], 256, 512)])
-def test_staggered_wide_tiles(rows, d, f):
-    """PPMOE_GEMM_STAGGER=1 / PPMOE_GEMM_STAGGER_WGRAD=1: FWD1 / DGRAD2 and WGRAD1 / WGRAD2 on
-    256 x 512 tiles whose two N halves run L k-steps apart (grouped_gemm_stagger_kernel; the
-    wgrad groups include an empty one), checked against the fp32 reference like every mode.
+@pytest.mark.parametrize("rows,d,f,variant", [([2048, 1000, 4100, 0, 129], 1024, 4096, 1),
+                                              ([2048, 1000, 4100, 0, 129], 1024, 4096, 2),
+                                              ([2048, 1000, 4100, 0, 129], 1024, 4096, 3),
+                                              ([300, 77, 1], 256, 512, 1)])
+def test_staggered_wide_tiles(rows, d, f, variant):
+    """PPMOE_GEMM_STAGGER=v / PPMOE_GEMM_STAGGER_WGRAD=v (v = 1, 2, 3: lag / ring variants): FWD1 /
+    DGRAD2 and WGRAD1 / WGRAD2 on 256 x 512 tiles whose two N halves run L k-steps apart
+    (grouped_gemm_stagger_kernel; the wgrad groups include an empty one), checked against the
+    fp32 reference like every mode.
     Opt-in kernel: it runs in a child process so a pipeline fault cannot poison this one's
     CUDA context (and with it the rest of the suite)."""
     import subprocess
     import sys
     code = ("import sys; sys.path.insert(0, %r); import test_gemm_gpu as t; "
             "t.test_fwd_bwd_modes(%r, %d, %d); print('STAGGER_OK')" % (str(Path(__file__).parent), rows, d, f))
-    env = dict(os.environ, PPMOE_GEMM_STAGGER="1", PPMOE_GEMM_STAGGER_WGRAD="1")
+    env = dict(os.environ, PPMOE_GEMM_STAGGER=str(variant), PPMOE_GEMM_STAGGER_WGRAD=str(variant))
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and "STAGGER_OK" in r.stdout, (r.stdout + r.stderr)[-3000:]

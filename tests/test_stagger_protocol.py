@@ -126,9 +126,10 @@ def run(tiles_K, L=3, NA=5, NB=2, seed=0):
 
 def test_protocol_random_interleavings():
     rng = random.Random(1234)
-    for seed in range(400):
-        tiles = [rng.choice([0, 1, 2, 3, 4, 5, 16]) for _ in range(rng.randint(1, 5))]
-        run(tiles, seed=seed)
+    for L, NA, NB in ((3, 5, 2), (2, 4, 3), (4, 6, 2)):  # the kernel's three variants
+        for seed in range(200):
+            tiles = [rng.choice([0, 1, 2, 3, 4, 5, 16]) for _ in range(rng.randint(1, 5))]
+            run(tiles, L=L, NA=NA, NB=NB, seed=seed)
 
 
 def test_model_detects_an_undersized_a_ring():
