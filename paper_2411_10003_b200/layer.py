@@ -412,6 +412,10 @@ class MoELayer(torch.nn.Module):
         # for the other (pushes reach NVLink rate from ~16 CTAs)
         self.agg_ctas = 16
         self.agg_ctas_w2 = 16  # the W2 half has DGRAD2 + WGRAD1 to hide under: may use fewer SMs
+        # the W1 half's home-side reduce of the last layer to run backward (a single layer, or
+        # block 0 of a stack) tails the iteration with no GEMM after DGRAD1 to disturb: it takes
+        # a full grid (its CTAs fill the SMs DGRAD1 frees) instead of agg_ctas SMs
+        self.agg_tail_reduce_ctas = 2 * _device.num_sms(dev)
         # SMs the GEMMs leave to Trans / Agg per replica this rank sends or receives (device-side,
         # clamped to [2, trans_ctas / agg_ctas])
         self.res_per_replica = 4
@@ -822,9 +826,10 @@ class MoELayer(torch.nn.Module):
                           self.agg_stage.ptrs.data_ptr(), self.mask_cur.data_ptr(), self.E, self.m, self.rank,
                           self.slots, self.d, self.f, parts, nctas, cs)
                 self.comm_barrier(self.comm_stream)  # every replica's grads have landed here
+                tail = parts == 1 and self.block_index == 0
                 _lib.call("pp_replica_agg_reduce", self.g1_arena.local.data_ptr(), self.g2_arena.local.data_ptr(),
                           self.agg_stage.local.data_ptr(), self.mask_cur.data_ptr(), self.E, self.m, self.rank,
-                          self.d, self.f, parts, nctas, cs)
+                          self.d, self.f, parts, self.agg_tail_reduce_ctas if tail else nctas, cs)
             self._log_side("SubAgg1" if parts == 2 else "SubAgg2", t0, self._side_event(self.comm_stream))
             self._agg_done = torch.cuda.Event()
             self._agg_done.record(self.comm_stream)
