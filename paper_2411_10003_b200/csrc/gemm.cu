@@ -1414,25 +1414,37 @@ int gate_dx_gemm(const void* dl, const void* wg, int T, int d, int E, int EP, vo
   return launch<256, false, true, EPI_BF16, 4>(ta, tb, p, sm_count(), st, &tc);
 }
 
-// dwg[e][c] = sum_s ws[s][c][e] (fixed order over the splits: bit-deterministic); thread per
-// (c, e), every split's value loaded before the adds
-__global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, int d, int EP, int E,
-                                     float* __restrict__ out) {
+// dwg[e][c] = sum_s ws[s][c][e] in a fixed order (bit-deterministic): a CTA takes 64 outputs;
+// quarter q of its threads sums splits [q*S/4, (q+1)*S/4) in order (every load issued before
+// the adds), then thread q = 0 adds the four quarter sums in q order.  Four times the threads of
+// one-thread-per-output, a quarter of the dependent load rounds.
+constexpr int kReduceOuts = 64;
+__global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restrict__ ws, int splits, int d, int EP,
+                                                            int E, float* __restrict__ out) {
   pdl_grid_sync();
+  __shared__ float part[4][kReduceOuts];
   const int n = d * E;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+  const int o = threadIdx.x % kReduceOuts, q = threadIdx.x / kReduceOuts;
+  const int i = blockIdx.x * kReduceOuts + o;
+  const int per = (splits + 3) / 4, s_begin = q * per, s_end = min(splits, s_begin + per);
+  float acc = 0.f;
+  if (i < n) {
     const int c = i / E, e = i - (i / E) * E;
     const float* src = ws + (size_t)c * EP + e;
     const size_t stride = (size_t)d * EP;
-    float acc = 0.f;
-    for (int s0 = 0; s0 < splits; s0 += 8) {
+    for (int s0 = s_begin; s0 < s_end; s0 += 8) {
       float v[8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) v[u] = s0 + u < splits ? __ldcs(src + (size_t)(s0 + u) * stride) : 0.f;
+      for (int u = 0; u < 8; ++u) v[u] = s0 + u < s_end ? __ldcs(src + (size_t)(s0 + u) * stride) : 0.f;
 #pragma unroll
       for (int u = 0; u < 8; ++u) acc += v[u];
     }
-    out[(size_t)e * d + c] = acc;
+  }
+  part[q][o] = acc;
+  __syncthreads();
+  if (q == 0 && i < n) {
+    const int c = i / E, e = i - (i / E) * E;
+    out[(size_t)e * d + c] = ((part[0][o] + part[1][o]) + part[2][o]) + part[3][o];
   }
 }
 
@@ -1458,7 +1470,8 @@ int gate_dw_gemm(const void* dl, const void* x, int T, int d, int E, int EP, int
                     : launch<128, true, true, EPI_F32, 5>(ta, tb, q, sm_count(), st, &tc);
   if (rc) return rc;
   const int n = E * d;
-  PP_CUDA_TRY(pdl_launch(splitk_reduce_kernel, dim3((n + 255) / 256), dim3(256), 0, st, ws, S, d, EP, E, dwg));
+  PP_CUDA_TRY(pdl_launch(splitk_reduce_kernel, dim3((n + kReduceOuts - 1) / kReduceOuts), dim3(256), 0, st, ws, S, d,
+                         EP, E, dwg));
   PP_LAUNCH_CHECK();
   return PP_OK;
 }
