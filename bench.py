@@ -689,6 +689,31 @@ def main() -> None:
         pm = {names.get(m, str(m)): statistics.median(v) for m, v in per.items()}
         gemm_graph = {"ms_per_step": sum(pm.values()), "per_mode_ms": pm}
 
+    # ---- the step's phases inside graph replays (the layer's phase marks captured as
+    # external-event graph nodes): the small kernels' in-step durations, no host launch gaps
+    # (N > 1: derived from the exposure section's instrumented replays below)
+    phases_graph = None
+    if use_graph and world == 1:
+        try:
+            from paper_2411_10003_b200 import calibrate as _cal
+
+            tp = layer.make_graphed_step(xs[0].clone(), dy.clone(), with_loss=True, timeline_events=True)
+            acc_ph = {}
+            for _ in range(8):
+                for i in range(3):
+                    run_step(i)
+                tp()
+                run_step(0)
+                torch.cuda.synchronize()
+                prev = 0.0
+                for name, t_ in sorted(_cal.per_step_phases(tp.phase_log)[0].items(), key=lambda kv: kv[1]):
+                    acc_ph.setdefault(name, []).append(t_ - prev)
+                    prev = t_
+            del tp
+            phases_graph = {k_: statistics.median(v_) for k_, v_ in acc_ph.items()}
+        except Exception as exc:  # evidence beside the headline
+            phases_graph = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+
     # ---- exposed replica communication of the graphed EP step: the reference's metric
     # (IterationTimeline.exposed_*, scheduler.py:134-169) on CUDA events captured as graph
     # nodes, replayed between timed-graph replays; median replay, max over ranks
@@ -711,6 +736,13 @@ def main() -> None:
             samples_exp.append(exposure_summary(tlg.timeline()))
             graph_calib.append((counts_r, mask_before, _cal.per_step_phases(tlg.phase_log)[0]))
         del tlg
+        acc_ph = {}
+        for _, _, ph in graph_calib:
+            prev = 0.0
+            for name, t_ in sorted(ph.items(), key=lambda kv: kv[1]):
+                acc_ph.setdefault(name, []).append(t_ - prev)
+                prev = t_
+        phases_graph = {k_: statistics.median(v_) for k_, v_ in acc_ph.items()}
         samples_exp.sort(key=lambda e_: e_["exposed_replica_comm_frac"])
         exposure = samples_exp[len(samples_exp) // 2]
         fr = torch.tensor([exposure["exposed_replica_comm_frac"]], dtype=torch.float64, device=dev)
@@ -1120,6 +1152,7 @@ def main() -> None:
                                    "planning": layer.planning,
                                    "replica_engine": layer.replica_engine}},
             "host_enqueue_ms_per_step": host_ms, "phase_ms_rank0": phases,
+            "phase_ms_graph_rank0": phases_graph,
             "side_stream_ms_rank0": side_ms, "replica_traffic": replica_traffic,
             "timed_region": "CUDA-graph replay of fwd+bwd" if use_graph else "eager stream-ordered fwd+bwd",
             "roofline": roofline, "cpu_baseline": cpu_info, "e2e": e2e, "gpu_launches": launches,
