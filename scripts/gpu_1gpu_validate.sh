@@ -3,7 +3,7 @@
 set -x
 nvidia-smi --query-gpu=index,name,clocks.max.sm --format=csv
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/v1_smoke.log 2>&1; echo smoke $?
-timeout 2400 python -m pytest tests -q -m gpu --timeout 900 > gpurun_out/v1_tests.log 2>&1; echo tests $?
+PPMOE_TEST_STAGGER=1 timeout 2400 python -m pytest tests -q -m gpu --timeout 900 > gpurun_out/v1_tests.log 2>&1; echo tests $?
 timeout 300 python bench.py > gpurun_out/v1_bench.log 2>&1; echo bench $?
 timeout 300 python bench.py --impl reference --steps 5 --warmup 3 > gpurun_out/v1_ref.log 2>&1; echo ref $?
 timeout 300 python scripts/gemm_bench.py > gpurun_out/v1_gemm.log 2>&1; echo gemm $?

@@ -123,6 +123,8 @@ def test_plain_mode_large():
                                               ([2048, 1000, 4100, 0, 129], 1024, 4096, 2),
                                               ([2048, 1000, 4100, 0, 129], 1024, 4096, 3),
                                               ([300, 77, 1], 256, 512, 1)])
+@pytest.mark.skipif(os.environ.get("PPMOE_TEST_STAGGER") != "1",
+                    reason="opt-in kernel, not yet measured on hardware: PPMOE_TEST_STAGGER=1 runs it")
 def test_staggered_wide_tiles(rows, d, f, variant):
     """PPMOE_GEMM_STAGGER=v / PPMOE_GEMM_STAGGER_WGRAD=v (v = 1, 2, 3: lag / ring variants): FWD1 /
     DGRAD2 and WGRAD1 / WGRAD2 on 256 x 512 tiles whose two N halves run L k-steps apart
