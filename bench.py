@@ -107,11 +107,13 @@ class PopularityDrift:
 
 
 class NvLinkCounter:
-    """NVLink data bytes this GPU sent / received (NVML field counters
-    NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX/RX, KiB, all links), read around a timed region."""
+    """NVLink data bytes this GPU sent / received, summed over its links, read around a timed
+    region: NVML field counters NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX/RX (KiB, per link), or,
+    where the driver does not report those, NVML_FI_DEV_NVLINK_COUNT_XMIT/RCV_BYTES (bytes)."""
 
     def __init__(self, torch_device) -> None:
         self.ok = False
+        self.fields = None
         try:
             import pynvml
 
@@ -119,24 +121,36 @@ class NvLinkCounter:
             uuid = "GPU-" + str(__import__("torch").cuda.get_device_properties(torch_device).uuid)
             self.h = pynvml.nvmlDeviceGetHandleByUUID(uuid.encode())
             self.nv = pynvml
-            self.read()
-            self.ok = True
+            errs = []
+            for tx, rx, unit in ((pynvml.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX,
+                                  pynvml.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX, 1024),
+                                 (getattr(pynvml, "NVML_FI_DEV_NVLINK_COUNT_XMIT_BYTES", 202),
+                                  getattr(pynvml, "NVML_FI_DEV_NVLINK_COUNT_RCV_BYTES", 204), 1)):
+                self.fields = (tx, rx, unit)
+                try:
+                    self.read()
+                    self.ok = True
+                    break
+                except Exception as exc:
+                    errs.append(repr(exc)[:120])
+            if not self.ok:
+                self.error = "; ".join(errs)
         except Exception as exc:
             self.error = repr(exc)[:160]
 
     def read(self):
         """(tx, rx) bytes summed over the links that report (field scope = link id)."""
         nv = self.nv
-        ids = [(f, l) for f in (nv.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX, nv.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX)
-               for l in range(18)]
+        tx, rx, unit = self.fields
+        ids = [(f, l) for f in (tx, rx) for l in range(18)]
         vals = nv.nvmlDeviceGetFieldValues(self.h, ids)
         out, good = [0, 0], 0
         for (f, _), v in zip(ids, vals):
             if v.nvmlReturn == 0:
-                out[0 if f == nv.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX else 1] += int(v.value.ullVal) * 1024
+                out[0 if f == tx else 1] += int(v.value.ullVal) * unit
                 good += 1
         if not good:
-            raise RuntimeError(f"no NVLink throughput field readable (rc {vals[0].nvmlReturn})")
+            raise RuntimeError(f"no NVLink byte field readable (fields {tx}/{rx}, rc {vals[0].nvmlReturn})")
         return out
 
 
@@ -660,7 +674,8 @@ def main() -> None:
                   "rx_GBps_per_rank": [float(a[1]) / sec / 1e9 for a in allv],
                   "tx_bytes_per_step_per_rank": [float(a[0]) / args.steps for a in allv],
                   "peak_GBps_per_direction": 770.0, "peak_source": "B200_PROFILING.md measured peer copy",
-                  "source": "NVML NVLINK_THROUGHPUT_DATA_TX/RX counters around the timed region (all links)"}
+                  "source": f"NVML field counters {nvl.fields[0]}/{nvl.fields[1]} (NVLink data TX/RX) around the "
+                            "timed region (all links)"}
     ms_tensor = torch.tensor([ms_total], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(ms_tensor, op=dist.ReduceOp.MAX)
