@@ -108,12 +108,12 @@ class PopularityDrift:
 
 class NvLinkCounter:
     """NVLink data bytes this GPU sent / received, summed over its links, read around a timed
-    region: NVML field counters NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX/RX (KiB, per link), or,
-    where the driver does not report those, NVML_FI_DEV_NVLINK_COUNT_XMIT/RCV_BYTES (bytes)."""
+    region.  Two NVML field sets are read side by side -- NVLINK_THROUGHPUT_DATA_TX/RX (KiB, per
+    link) and NVLINK_COUNT_XMIT/RCV_BYTES (bytes, per link) -- and the first whose counters moved
+    is reported (drivers differ in which they maintain)."""
 
     def __init__(self, torch_device) -> None:
         self.ok = False
-        self.fields = None
         try:
             import pynvml
 
@@ -121,37 +121,44 @@ class NvLinkCounter:
             uuid = "GPU-" + str(__import__("torch").cuda.get_device_properties(torch_device).uuid)
             self.h = pynvml.nvmlDeviceGetHandleByUUID(uuid.encode())
             self.nv = pynvml
-            errs = []
-            for tx, rx, unit in ((pynvml.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX,
-                                  pynvml.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX, 1024),
-                                 (getattr(pynvml, "NVML_FI_DEV_NVLINK_COUNT_XMIT_BYTES", 202),
-                                  getattr(pynvml, "NVML_FI_DEV_NVLINK_COUNT_RCV_BYTES", 204), 1)):
-                self.fields = (tx, rx, unit)
-                try:
-                    self.read()
-                    self.ok = True
-                    break
-                except Exception as exc:
-                    errs.append(repr(exc)[:120])
-            if not self.ok:
-                self.error = "; ".join(errs)
+            self.sets = [("THROUGHPUT_DATA", pynvml.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX,
+                          pynvml.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX, 1024),
+                         ("COUNT_BYTES", getattr(pynvml, "NVML_FI_DEV_NVLINK_COUNT_XMIT_BYTES", 202),
+                          getattr(pynvml, "NVML_FI_DEV_NVLINK_COUNT_RCV_BYTES", 204), 1)]
+            self.read()
+            self.ok = True
         except Exception as exc:
             self.error = repr(exc)[:160]
 
-    def read(self):
-        """(tx, rx) bytes summed over the links that report (field scope = link id)."""
+    def read(self) -> dict:
+        """{field set: (tx, rx) bytes summed over the links that report (scope = link id)}."""
         nv = self.nv
-        tx, rx, unit = self.fields
-        ids = [(f, l) for f in (tx, rx) for l in range(18)]
-        vals = nv.nvmlDeviceGetFieldValues(self.h, ids)
-        out, good = [0, 0], 0
-        for (f, _), v in zip(ids, vals):
-            if v.nvmlReturn == 0:
-                out[0 if f == tx else 1] += int(v.value.ullVal) * unit
-                good += 1
-        if not good:
-            raise RuntimeError(f"no NVLink byte field readable (fields {tx}/{rx}, rc {vals[0].nvmlReturn})")
+        out = {}
+        for name, tx, rx, unit in self.sets:
+            ids = [(f, l) for f in (tx, rx) for l in range(18)]
+            try:
+                vals = nv.nvmlDeviceGetFieldValues(self.h, ids)
+            except Exception:
+                continue
+            acc, good = [0, 0], 0
+            for (f, _), v in zip(ids, vals):
+                if v.nvmlReturn == 0:
+                    acc[0 if f == tx else 1] += int(v.value.ullVal) * unit
+                    good += 1
+            if good:
+                out[name] = tuple(acc)
+        if not out:
+            raise RuntimeError("no NVLink byte field readable")
         return out
+
+    @staticmethod
+    def delta(a: dict, b: dict):
+        """(field set, tx bytes, rx bytes) of the first set whose counters moved between reads."""
+        for name in a:
+            if name in b and (b[name][0] - a[name][0] or b[name][1] - a[name][1]):
+                return name, b[name][0] - a[name][0], b[name][1] - a[name][1]
+        name = next(iter(a))
+        return name, 0, 0
 
 
 class ClockSampler:
@@ -665,8 +672,8 @@ def main() -> None:
     ms_total = t0.elapsed_time(t1)
     nvlink = {"error": nvl_err} if nvl_err else None
     if nvl0 is not None:  # NVLink bytes of the timed region from the hardware counters
-        tx1, rx1 = nvl.read()
-        v_ = torch.tensor([tx1 - nvl0[0], rx1 - nvl0[1]], dtype=torch.float64, device=dev)
+        fset, dtx, drx = NvLinkCounter.delta(nvl0, nvl.read())
+        v_ = torch.tensor([dtx, drx], dtype=torch.float64, device=dev)
         allv = [torch.zeros_like(v_) for _ in range(world)]
         dist.all_gather(allv, v_)
         sec = ms_total / 1e3
@@ -674,8 +681,8 @@ def main() -> None:
                   "rx_GBps_per_rank": [float(a[1]) / sec / 1e9 for a in allv],
                   "tx_bytes_per_step_per_rank": [float(a[0]) / args.steps for a in allv],
                   "peak_GBps_per_direction": 770.0, "peak_source": "B200_PROFILING.md measured peer copy",
-                  "source": f"NVML field counters {nvl.fields[0]}/{nvl.fields[1]} (NVLink data TX/RX) around the "
-                            "timed region (all links)"}
+                  "source": f"NVML NVLINK_{fset} TX/RX field counters around the timed region (all links; "
+                            "rank 0's field set)"}
     ms_tensor = torch.tensor([ms_total], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(ms_tensor, op=dist.ReduceOp.MAX)
