@@ -358,3 +358,20 @@ def test_calibration_fits_total_expert_compute():
     assert abs(fit["compute_throughput"] / (t_true * 3 / 3.4) - 1) < 1e-9
     assert fit["mean_abs_rel_error"] < 1e-9
     assert abs(fit["bec_over_fec_measured"] - 2.4) < 1e-9
+
+
+def test_bench_nvlink_counter_delta():
+    """The NVLink counter reports the first NVML field set whose counters moved over the timed
+    region (drivers maintain one or the other), and zero when none did."""
+    import sys
+    from pathlib import Path
+
+    sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+    import bench
+
+    a = {"THROUGHPUT_DATA": (10, 10), "COUNT_BYTES": (5, 5)}
+    assert bench.NvLinkCounter.delta(a, {"THROUGHPUT_DATA": (10, 10), "COUNT_BYTES": (105, 55)}) == \
+        ("COUNT_BYTES", 100, 50)
+    assert bench.NvLinkCounter.delta(a, {"THROUGHPUT_DATA": (2058, 10), "COUNT_BYTES": (105, 55)}) == \
+        ("THROUGHPUT_DATA", 2048, 0)
+    assert bench.NvLinkCounter.delta(a, a) == ("THROUGHPUT_DATA", 0, 0)
