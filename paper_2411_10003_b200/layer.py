@@ -413,8 +413,11 @@ class MoELayer(torch.nn.Module):
         self.agg_ctas = 16
         self.agg_ctas_w2 = 16  # the W2 half has DGRAD2 + WGRAD1 to hide under: may use fewer SMs
         # the W1 half's home-side reduce of the last layer to run backward (a single layer, or
-        # block 0 of a stack) tails the iteration with no GEMM after DGRAD1 to disturb: it takes
-        # a full grid (its CTAs fill the SMs DGRAD1 frees) instead of agg_ctas SMs
+        # block 0 of a stack: block_index, set by MoEStack) tails the iteration with no GEMM after
+        # DGRAD1 to disturb: it takes a full grid (its CTAs fill the SMs DGRAD1 frees) instead of
+        # agg_ctas SMs.  Models that chain their own MoELayers should give the later-running
+        # layers block_index > 0 (or set agg_tail_reduce_ctas = agg_ctas) so a persistent GEMM
+        # that follows never finds its SMs taken.
         self.agg_tail_reduce_ctas = 2 * _device.num_sms(dev)
         # SMs the GEMMs leave to Trans / Agg per replica this rank sends or receives (device-side,
         # clamped to [2, trans_ctas / agg_ctas])
